@@ -1,0 +1,519 @@
+"""Pins of the CPU oracle (oracle/) against what the paper and the mathematics fix.
+
+Every expected value here comes from something other than the oracle: dense matrices
+assembled from the finite-difference stencil (numpy/scipy eigvalsh, expm, solve), closed
+forms of the paper's theorems, mpmath high-precision evaluation of definitions, or the
+worked examples printed in SPEC.md (tests/golden/spec_examples.json, cited there).
+None of these tests runs on a GPU.
+"""
+from __future__ import annotations
+
+import json
+import os
+
+import mpmath
+import numpy as np
+import pytest
+import scipy.linalg as sla
+
+import synth
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+# ------------------------------------------------------------------------------------------
+# dense test-side model, assembled from the FD stencil ("Delta_h denotes discrete
+# Laplacian corresponding to homogeneous Dirichlet boundary conditions")
+# ------------------------------------------------------------------------------------------
+def lap1(n):
+    h = 1.0 / (n + 1)
+    return (np.diag(-2.0 * np.ones(n)) + np.diag(np.ones(n - 1), 1) + np.diag(np.ones(n - 1), -1)) / h**2
+
+
+def lapnd(n, dim):
+    """Kronecker-sum Laplacian on [z][y][x] (x fastest) ordering."""
+    L1, I = lap1(n), np.eye(n)
+    if dim == 1:
+        return L1
+    if dim == 2:
+        return np.kron(I, L1) + np.kron(L1, I)
+    return np.kron(np.kron(I, I), L1) + np.kron(np.kron(I, L1), I) + np.kron(np.kron(L1, I), I)
+
+
+def Lh(s):
+    return s.a * lapnd(s.n, s.dim) - s.c * np.eye(s.N)
+
+
+def dense_ops(s):
+    """A = exp(dt L_h); dt*phi1(dt L), dt*phi2(dt L) via L^{-1} (L is invertible)."""
+    L = Lh(s)
+    A = sla.expm(s.dt * L)
+    I = np.eye(s.N)
+    Phi1 = np.linalg.solve(L, A - I)  # dt * phi1(dt L) = L^{-1}(e^{dt L} - I)
+    Phi2 = np.linalg.solve(L, np.linalg.solve(L, A - I - s.dt * L)) / s.dt  # dt*phi2(dtL)
+    return A, Phi1, Phi2
+
+
+def Nfun(s, u):
+    return sum(qp * u**p for p, qp in enumerate(s.q))
+
+
+def dense_residual(s, u0, U):
+    A, P1, P2 = dense_ops(s)
+    u0 = u0.reshape(-1)
+    U = U.reshape(s.nt, -1)
+    R = np.empty_like(U)
+    for n in range(1, s.nt + 1):
+        prev = u0 if n == 1 else U[n - 2]
+        prev2 = u0 if n <= 2 else U[n - 3]
+        r = A @ prev - U[n - 1]
+        if s.q:
+            if s.scheme == 0:
+                r += P1 @ Nfun(s, prev)
+            else:
+                r += (P1 + P2) @ Nfun(s, prev) - P2 @ Nfun(s, prev2)
+        R[n - 1] = r
+    return R
+
+
+def dense_sequential(s, u0):
+    A, P1, P2 = dense_ops(s)
+    prev = u0.reshape(-1).copy()
+    prev2 = prev.copy()
+    out = []
+    for _ in range(s.nt):
+        cur = A @ prev
+        if s.q:
+            if s.scheme == 0:
+                cur += P1 @ Nfun(s, prev)
+            else:
+                cur += (P1 + P2) @ Nfun(s, prev) - P2 @ Nfun(s, prev2)
+        out.append(cur)
+        prev2, prev = prev, cur
+    return np.array(out)
+
+
+def alpha_circulant(nt, alpha):
+    """C_0^alpha: ones on the subdiagonal, alpha at (1, N_t)."""
+    C = np.diag(np.ones(nt - 1), -1)
+    C[0, nt - 1] = alpha
+    return C
+
+
+def dense_Qalpha(s, alpha):
+    A, _, _ = dense_ops(s)
+    return np.eye(s.N * s.nt) - np.kron(alpha_circulant(s.nt, alpha), A)
+
+
+def spec(orc, dim, n, a=1.0, c=1.0, T=1.0, nt=8, alpha=1e-2, scheme=0, q=()):
+    return orc.Spec(dim, n, a, c, T, nt, alpha, scheme, tuple(q))
+
+
+def rel(a, b):
+    return np.abs(np.asarray(a) - np.asarray(b)).max() / max(np.abs(np.asarray(b)).max(), 1e-300)
+
+
+# ------------------------------------------------------------------------------------------
+# P1 spectra
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("n", [1, 2, 3, 5, 8, 16, 31])
+def test_axis_eigs_vs_dense_stencil(orc, n):
+    got = np.sort(orc.axis_eigs(n))
+    want = np.sort(np.linalg.eigvalsh(lap1(n)))
+    assert rel(got, want) < 1e-13
+
+
+def test_axis_eigs_spec_example(orc):
+    g = GOLD["dirichlet_eigs_n3"]
+    got = np.sort(orc.axis_eigs(g["n"]))[::-1]
+    assert np.allclose(got, g["values"], atol=1e-6)
+
+
+def test_dense_stencil_column_spec_example():
+    g = GOLD["column_of_L"]  # pins the test-side stencil itself
+    assert np.allclose(lap1(g["n"])[:, 0], g["values"])
+
+
+@pytest.mark.parametrize("dim,n,a,c", [(2, 4, 0.5, 1.0), (3, 3, 1.0, 1.0), (2, 5, 0.1, 0.5)])
+def test_mode_eigs_kronecker_sum(orc, dim, n, a, c):
+    s = spec(orc, dim, n, a=a, c=c)
+    mu, _, _, _ = orc.mode_tables(s)
+    assert rel(np.sort(mu.reshape(-1)), np.sort(np.linalg.eigvalsh(Lh(s)))) < 1e-13
+
+
+# ------------------------------------------------------------------------------------------
+# P2 the DST basis V
+# ------------------------------------------------------------------------------------------
+def dst_matrix(orc, s):
+    return np.array([orc.dst(s, e.reshape((s.n,) * s.dim)).reshape(-1) for e in np.eye(s.N)]).T
+
+
+@pytest.mark.parametrize("dim,n", [(1, 7), (1, 12), (2, 4), (3, 3)])
+def test_dst_orthonormal_and_diagonalizes_stencil(orc, dim, n):
+    s = spec(orc, dim, n)
+    V = dst_matrix(orc, s)
+    assert np.abs(V @ V - np.eye(s.N)).max() < 1e-14  # V = V^T = V^{-1}
+    assert np.abs(V - V.T).max() < 1e-15
+    L = lapnd(n, dim)
+    D = V @ L @ V
+    mu, _, _, _ = orc.mode_tables(orc.Spec(dim, n, 1.0, 0.0, 1.0, 1, 0.5))
+    off = D - np.diag(np.diag(D))
+    assert np.abs(off).max() < 1e-10 * np.abs(L).max()
+    assert rel(np.diag(D), mu.reshape(-1)) < 1e-12  # mode J <-> eigenvalue mu_J, same index
+
+
+def test_dst_of_sampled_sine_mode(orc):
+    n, k = 15, 6
+    s = spec(orc, 1, n)
+    v = synth.sine_table(n, k)[k - 1]
+    out = orc.dst(s, v)
+    want = np.zeros(n)
+    want[k - 1] = np.sqrt((n + 1) / 2.0)
+    assert np.abs(out - want).max() < 1e-14
+
+
+def test_dst_sample_matches_full(orc):
+    s = spec(orc, 2, 9)
+    v = np.random.default_rng(0).standard_normal((9, 9))
+    full = orc.dst(s, v).reshape(-1)
+    idx = np.array([0, 5, 17, 80, 44])
+    assert np.abs(orc.dst_sample(s, v, idx) - full[idx]).max() < 1e-15
+
+
+# ------------------------------------------------------------------------------------------
+# P3 the propagator A = exp(dt L_h) and the phi functions
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("dim,n,a,c,dt", [(1, 8, 1.0, 1.0, 0.1), (2, 5, 0.5, 1.0, 0.05), (3, 3, 1.0, 1.0, 0.02)])
+def test_apply_A_vs_dense_expm(orc, dim, n, a, c, dt):
+    s = spec(orc, dim, n, a=a, c=c, T=dt, nt=1)
+    v = np.random.default_rng(1).standard_normal((n,) * dim)
+    want = sla.expm(dt * Lh(s)) @ v.reshape(-1)
+    assert rel(orc.apply_A(s, v).reshape(-1), want) < 1e-12
+
+
+def test_scalar_exponential_spec_example(orc):
+    g = GOLD["scalar_exponential"]
+    # n = 1 grid, a = 0: L_h = -c = d (a scalar), so E = exp(dt d)
+    s = spec(orc, 1, 1, a=0.0, c=-g["d"], T=g["dt"], nt=1)
+    _, E, _, _ = orc.mode_tables(s)
+    assert abs(E[0] - g["value"]) < 5e-10
+
+
+def test_phi_functions_vs_mpmath(orc):
+    mpmath.mp.dps = 40
+    zs = np.array([-1e-8, -0.0097, -0.3, -0.4999, -0.5001, -0.7, -2.0, -13.0, -300.0, -13107.0])
+    for z in zs:
+        s = spec(orc, 1, 1, a=0.0, c=-float(z), T=1.0, nt=1)  # dt = 1, mu = z
+        _, E, f1, f2 = orc.mode_tables(s)
+        zm = mpmath.mpf(float(z))
+        e = mpmath.exp(zm)
+        w1 = (e - 1) / zm
+        w2 = (e - 1 - zm) / zm**2
+        assert abs(f1[0] - float(w1)) <= 2e-16 * abs(float(w1))
+        assert abs(f2[0] - float(w2)) <= 2e-16 * abs(float(w2))
+        assert abs(E[0] - float(e)) <= 2e-16 * float(e) + 1e-300
+
+
+# ------------------------------------------------------------------------------------------
+# P4 / P9 / P11 sequential stepping
+# ------------------------------------------------------------------------------------------
+def test_sequential_c1_equals_dense_exponential(orc):
+    cfg = synth.CONFIGS["c1"]
+    s = orc.spec(cfg)
+    u0 = synth.initial_condition(cfg)
+    U = orc.sequential(s, u0)
+    L = Lh(s)
+    lam, W = np.linalg.eigh(L)  # symmetric stencil: LAPACK eigendecomposition
+    for n in (1, 7, 32):  # exponential Euler is exact for the linear problem: u_n = e^{n dt L} u_0
+        assert np.abs(U[n - 1] - sla.expm(n * s.dt * L) @ u0).max() < 1e-13 * np.abs(u0).max()
+        assert rel(U[n - 1], W @ (np.exp(n * s.dt * lam) * (W.T @ u0))) < 1e-12
+
+
+@pytest.mark.parametrize("scheme", [0, 1])
+@pytest.mark.parametrize("dim,n", [(1, 9), (2, 4)])
+def test_sequential_nonlinear_vs_dense(orc, scheme, dim, n):
+    s = spec(orc, dim, n, a=0.3, c=0.5, T=0.5, nt=6, scheme=scheme, q=synth.CUBIC)
+    u0 = np.random.default_rng(2).uniform(-1, 1, (n,) * dim)
+    assert rel(orc.sequential(s, u0).reshape(s.nt, -1), dense_sequential(s, u0)) < 1e-12
+
+
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_etd_with_linear_nonlinearity_closed_form(orc, scheme):
+    """N(u) = -M u keeps a sine mode in its mode: ETD1 u_n = g^n u_0 with
+    g = E - M dt phi1; ETD2 is the 2-term recurrence (P9).  mu from the dense stencil."""
+    n, k, M = 11, 3, 2.0
+    s = spec(orc, 1, n, a=0.7, c=0.2, T=1.0, nt=10, scheme=scheme, q=(0.0, -M))
+    u0 = synth.sine_table(n, k)[k - 1]
+    mu = np.sort(np.linalg.eigvalsh(Lh(s)))[::-1][k - 1]  # k-th smoothest mode
+    z = s.dt * mu
+    E = np.exp(z)
+    p1 = s.dt * np.expm1(z) / z
+    p2 = s.dt * (np.expm1(z) - z) / z**2
+    amp = [1.0, 1.0]  # u_{-1} := u_0 for the N history (reading R6)
+    for _ in range(s.nt):
+        if scheme == 0:
+            nxt = (E - M * p1) * amp[-1]
+        else:
+            nxt = E * amp[-1] - M * (p1 + p2) * amp[-1] + M * p2 * amp[-2]
+        amp.append(nxt)
+    U = orc.sequential(s, u0)
+    for m in range(1, s.nt + 1):
+        assert np.abs(U[m - 1] - amp[m + 1] * u0).max() < 1e-13
+
+
+@pytest.mark.parametrize("scheme,order", [(0, 1), (1, 2)])
+def test_etd_convergence_order(orc, scheme, order):
+    """Scalar u' = (mu - M) u split as L = mu (linear), N = -M u: ETD1 is first order and
+    ETD2 (Cox-Matthews) second order in dt (global error at T)."""
+    M, T = 3.0, 1.0
+    errs = []
+    for nt in (16, 32, 64):
+        s = spec(orc, 1, 1, a=0.0, c=0.5, T=T, nt=nt, scheme=scheme, q=(0.0, -M))
+        U = orc.sequential(s, np.array([1.0]))
+        errs.append(abs(U[-1, 0] - np.exp((-0.5 - M) * T)))
+    r1, r2 = errs[0] / errs[1], errs[1] / errs[2]
+    assert abs(np.log2(r1) - order) < 0.15 and abs(np.log2(r2) - order) < 0.1
+
+
+# ------------------------------------------------------------------------------------------
+# P5 the all-at-once residual
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("scheme,q", [(0, ()), (0, synth.CUBIC), (1, synth.CUBIC)])
+@pytest.mark.parametrize("dim,n", [(1, 7), (2, 4)])
+def test_residual_vs_dense(orc, scheme, q, dim, n):
+    s = spec(orc, dim, n, a=0.5, c=1.0, T=0.4, nt=5, scheme=scheme, q=q)
+    rng = np.random.default_rng(3)
+    u0 = rng.uniform(-1, 1, (n,) * dim)
+    U = rng.standard_normal((s.nt,) + (n,) * dim)
+    R, rn2 = orc.residual(s, u0, U)
+    want = dense_residual(s, u0, U)
+    assert rel(R.reshape(s.nt, -1), want) < 1e-12
+    assert abs(rn2 - (want**2).sum()) < 1e-12 * (want**2).sum()
+
+
+def test_residual_linear_is_f_minus_QU(orc):
+    """Linear: r = f - Q U with f = (A u_0, 0, ..., 0), Q = I - C_0 (x) A."""
+    s = spec(orc, 1, 6, nt=5)
+    rng = np.random.default_rng(4)
+    u0, U = rng.standard_normal(6), rng.standard_normal((5, 6))
+    A, _, _ = dense_ops(s)
+    f = np.zeros(30)
+    f[:6] = A @ u0
+    Q = np.eye(30) - np.kron(alpha_circulant(5, 0.0), A)
+    R, _ = orc.residual(s, u0, U)
+    assert rel(R.reshape(-1), f - Q @ U.reshape(-1)) < 1e-13
+    assert rel(orc.apply_Q(s, U).reshape(-1), Q @ U.reshape(-1)) < 1e-13
+    Qa = dense_Qalpha(s, s.alpha)
+    assert rel(orc.apply_Qalpha(s, U).reshape(-1), Qa @ U.reshape(-1)) < 1e-13
+
+
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_residual_vanishes_at_sequential_solution(orc, scheme):
+    s = spec(orc, 2, 6, a=0.5, c=0.5, T=0.5, nt=8, scheme=scheme, q=synth.CUBIC)
+    u0 = np.random.default_rng(5).uniform(-1, 1, (6, 6))
+    U = orc.sequential(s, u0)
+    R, _ = orc.residual(s, u0, U)
+    assert np.abs(R).max() < 1e-14 * max(1.0, np.abs(U).max()) * 10
+
+
+# ------------------------------------------------------------------------------------------
+# P6 the alpha-circulant preconditioner (Steps (a)-(c))
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("alpha", [0.3, 1e-2, 1e-4])
+@pytest.mark.parametrize("dim,n,nt", [(1, 5, 8), (1, 6, 7), (2, 3, 6), (1, 4, 16)])
+def test_precond_vs_dense_solve(orc, alpha, dim, n, nt):
+    s = spec(orc, dim, n, a=0.8, c=0.3, T=0.5, nt=nt, alpha=alpha)
+    R = np.random.default_rng(6).standard_normal((nt,) + (n,) * dim)
+    S, leak = orc.precond(s, R)
+    want = np.linalg.solve(dense_Qalpha(s, alpha), R.reshape(-1))
+    kappa = alpha ** (-(nt - 1) / nt)  # cond(Gamma_alpha)
+    assert rel(S.reshape(-1), want) < 1e-15 * kappa * 50
+    assert leak < 1e-8  # SPEC.md:356 leakage diagnostic
+
+
+def _recurrence_mp(alpha, z, r):
+    """Per-mode closed form of Q_alpha^{-1}, 40 digits:
+    w_m = sum_{l<=m} z^{m-l} r_l, s_Nt = w_Nt/(1 - alpha z^Nt), s_m = w_m + alpha z^m s_Nt."""
+    mpmath.mp.dps = 40
+    z, alpha = mpmath.mpf(z), mpmath.mpf(alpha)
+    nt = len(r)
+    w, acc = [], mpmath.mpf(0)
+    for m in range(nt):
+        acc = z * acc + mpmath.mpf(float(r[m]))
+        w.append(acc)
+    sN = w[-1] / (1 - alpha * z**nt)
+    return np.array([float(w[m] + alpha * z ** (m + 1) * sN) for m in range(nt)])
+
+
+@pytest.mark.parametrize("alpha,nt", [(1e-2, 32), (1e-3, 64), (1e-4, 64), (1e-3, 256)])
+def test_mode_precond_vs_recurrence(orc, alpha, nt):
+    s = spec(orc, 2, 15, a=0.5, c=1.0, T=1.0, nt=nt, alpha=alpha)
+    _, E, _, _ = orc.mode_tables(s)
+    rng = np.random.default_rng(7)
+    for J in (0, 7, 100, 224):
+        r = rng.standard_normal(nt)
+        got = orc.mode_precond(s, J, r)
+        want = _recurrence_mp(alpha, E.reshape(-1)[J], r)
+        assert rel(got, want) < 1e-17 * alpha ** (-(nt - 1) / nt) * 10
+
+
+def test_precond_physical_equals_per_mode(orc):
+    """Steps (a)-(c) in physical space = per-mode version in the DST basis (A4)."""
+    s = spec(orc, 2, 5, a=0.5, c=1.0, T=1.0, nt=8, alpha=1e-3)
+    R = np.random.default_rng(8).standard_normal((8, 5, 5))
+    S, _ = orc.precond(s, R)
+    Rh = np.array([orc.dst(s, r) for r in R]).reshape(8, -1)
+    Sh = np.array([orc.dst(s, x) for x in S]).reshape(8, -1)
+    for J in range(25):
+        assert rel(orc.mode_precond(s, J, Rh[:, J]), Sh[:, J]) < 1e-12
+
+
+def test_precond_alpha_to_zero_is_forward_substitution(orc):
+    """alpha -> 0: Q_alpha^{-1} -> Q^{-1} = sequential forward substitution, O(alpha) gap."""
+    s0 = spec(orc, 1, 6, a=1.0, c=1.0, T=1.0, nt=8, alpha=1e-9)
+    R = np.random.default_rng(9).standard_normal((8, 6))
+    S, _ = orc.precond(s0, R)
+    A, _, _ = dense_ops(s0)
+    x = np.zeros(6)
+    want = []
+    for m in range(8):  # (Q s)_m = s_m - A s_{m-1} = r_m
+        x = R[m] + A @ x
+        want.append(x)
+    assert rel(S, np.array(want)) < 1e-7
+
+
+def test_precond_inverts_Qalpha(orc):
+    s = spec(orc, 2, 4, a=1.0, c=1.0, T=1.0, nt=16, alpha=1e-3)
+    V = np.random.default_rng(10).standard_normal((16, 4, 4))
+    S, _ = orc.precond(s, orc.apply_Qalpha(s, V))
+    assert rel(S, V) < 1e-11
+
+
+# ------------------------------------------------------------------------------------------
+# P7 fixed-point history: exact per-mode contraction (Thm 2.1 / Thm 3.1, Appendix A3)
+# ------------------------------------------------------------------------------------------
+def test_contraction_spec_example(orc):
+    g = GOLD["contraction_factor"]
+    # one grid point, a = 0, c = 1, T = 1: mu T = -1 (the lambda_max T of the example)
+    s = spec(orc, 1, 1, a=0.0, c=1.0, T=1.0, nt=8, alpha=g["alpha"])
+    _, st, its, hist = orc.fixed_point(s, np.array([1.0]), tol=1e-14, maxit=20)
+    ratios = hist[1:] / hist[:-1]
+    assert np.abs(ratios - g["value"]).max() < g["abs_tol"]
+
+
+@pytest.mark.parametrize("cfgname", ["c1"])
+def test_fixed_point_history_closed_form(orc, cfgname):
+    """r^k_J = (-psi_J)^k r^0_J with psi_J = alpha e^{mu_J T}/(1 - alpha e^{mu_J T}), so
+    ||r^k||^2 = sum_J psi_J^{2k} |r^0_J|^2 (r^0 = f = (A u_0, 0, ...)).  Dense eigh only."""
+    cfg = synth.CONFIGS[cfgname]
+    s = orc.spec(cfg)
+    u0 = synth.initial_condition(cfg)
+    lam, W = np.linalg.eigh(Lh(s))
+    c0 = W.T @ (sla.expm(s.dt * Lh(s)) @ u0.reshape(-1))
+    eT = np.exp(lam * cfg.T)
+    psi = cfg.alpha * eT / (1 - cfg.alpha * eT)
+    _, st, its, hist = orc.fixed_point(s, u0, tol=cfg.tol)
+    assert st == 0 and its == 2  # SURVEY 8c.6 prediction for c1
+    r0 = np.sqrt((c0**2).sum())
+    for k in range(len(hist)):
+        want = np.sqrt(((psi**k * c0) ** 2).sum()) / r0
+        assert abs(hist[k] - want) < 1e-9 * want + 1e-15
+
+
+def test_fixed_point_obeys_theorem21_bound(orc):
+    s = spec(orc, 2, 7, a=0.05, c=0.0, T=0.5, nt=16, alpha=0.05)
+    u0 = np.random.default_rng(11).uniform(-1, 1, (7, 7))
+    lmax = np.linalg.eigvalsh(Lh(s)).max()
+    psi_max = s.alpha * np.exp(lmax * s.T) / (1 - s.alpha * np.exp(lmax * s.T))
+    _, st, its, hist = orc.fixed_point(s, u0, tol=1e-13)
+    assert st == 0
+    assert np.all(hist[1:] / hist[:-1] <= psi_max * (1 + 1e-6) + 1e-12)
+
+
+def test_fixed_point_converges_to_sequential(orc):
+    cfg = synth.CONFIGS["c2"].scaled(15, 16)
+    s = orc.spec(cfg)
+    u0 = synth.initial_condition(cfg)
+    U, st, its, hist = orc.fixed_point(s, u0, tol=1e-12)
+    assert st == 0
+    assert rel(U, orc.sequential(s, u0)) < 1e-11
+
+
+# ------------------------------------------------------------------------------------------
+# P8 GMRES (Thm 3.3, Lemma 3.4, Thm 3.14)
+# ------------------------------------------------------------------------------------------
+def test_gmres_terminates_in_nx_plus_one(orc):
+    s = spec(orc, 1, 4, a=1.0, c=0.0, T=0.6, nt=6, alpha=0.3)
+    u0 = np.random.default_rng(12).standard_normal(4)
+    U, st, its, hist = orc.gmres(s, u0, tol=1e-13, restart=50, maxit=50)
+    assert st == 0 and its <= s.N + 1  # Thm 3.3
+    assert rel(U, dense_sequential(s, u0).reshape(U.shape)) < 1e-11
+
+
+def test_preconditioned_spectrum_in_disk(orc):
+    """Lemma 3.4: eigenvalues of Q_alpha^{-1} Q within alpha/(1-alpha) of 1.
+    The matrix is assembled column by column from the oracle's own Q and Q_alpha^{-1}."""
+    s = spec(orc, 1, 4, a=1.0, c=0.5, T=0.6, nt=6, alpha=0.2)
+    n = s.N * s.nt
+    cols = []
+    for e in np.eye(n):
+        S, _ = orc.precond(s, orc.apply_Q(s, e.reshape(s.nt, s.n)))
+        cols.append(S.reshape(-1))
+    ev = np.linalg.eigvals(np.array(cols).T)
+    assert np.abs(ev - 1).max() <= s.alpha / (1 - s.alpha) + 1e-10
+
+
+def test_gmres_elman_bound(orc):
+    """Thm 3.14: ||r^k|| <= (4 alpha (1-alpha))^{k/2} ||r^0|| for
+    alpha < 2/(3+sqrt(Nt)) (constant as in the lemmas' proofs, reading R12)."""
+    nt = 8
+    alpha = 0.15
+    assert alpha < 2 / (3 + np.sqrt(nt))
+    s = spec(orc, 1, 8, a=0.05, c=0.0, T=0.5, nt=nt, alpha=alpha)
+    u0 = np.random.default_rng(13).standard_normal(8)
+    _, st, its, hist = orc.gmres(s, u0, tol=1e-13, restart=50, maxit=50)
+    for k, h in enumerate(hist):
+        assert h <= (4 * alpha * (1 - alpha)) ** (k / 2) * (1 + 1e-9)
+
+
+def test_gmres_c1_matches_sequential(orc):
+    cfg = synth.CONFIGS["c1"]
+    s = orc.spec(cfg)
+    u0 = synth.initial_condition(cfg)
+    U, st, its, hist = orc.gmres(s, u0, tol=cfg.tol, restart=20)
+    assert st == 0 and its <= 3
+    assert rel(U, orc.sequential(s, u0)) < 1e-12
+
+
+def test_gmres_rejects_nonlinear(orc):
+    s = spec(orc, 1, 4, q=synth.CUBIC)
+    _, st, _, _ = orc.gmres(s, np.ones(4))
+    assert st == 2
+
+
+# ------------------------------------------------------------------------------------------
+# P10 / P11 Picard sweeps for ETD1 / ETD2
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_picard_converges_to_sequential(orc, scheme):
+    base = synth.CONFIGS["c3" if scheme == 0 else "c5"]
+    cfg = base.scaled(15, 16)
+    s = orc.spec(cfg)
+    u0 = synth.initial_condition(cfg)
+    U, st, its, hist = orc.fixed_point(s, u0, tol=1e-12)
+    assert st == 0
+    assert rel(U, orc.sequential(s, u0)) < 1e-11
+
+
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_picard_small_alpha_recovers_sequential_stepping(orc, scheme):
+    """alpha -> 0 (north_star): the preconditioner becomes forward substitution, so after k
+    Picard sweeps the first k slices equal sequential stepping (O(alpha) gap)."""
+    s = spec(orc, 1, 9, a=0.5, c=0.5, T=0.5, nt=6, alpha=1e-10, scheme=scheme, q=synth.CUBIC)
+    u0 = np.random.default_rng(14).uniform(-1, 1, 9)
+    seq = orc.sequential(s, u0)
+    for k in (1, 2, 3):
+        U, _, _, _ = orc.fixed_point(s, u0, tol=0.0, maxit=k - 1)  # exactly k sweeps
+        err = np.abs(U - seq).max(axis=1)
+        assert err[:k].max() < 1e-7
+        assert err[k] > 1e3 * err[:k].max()  # slice k+1 not yet exact
