@@ -1,0 +1,145 @@
+/*
+ * expd.h -- C-ABI of the B200-native Exp-ParaDiag hot path (libexpd.so).
+ *
+ * Method: Garai & Chamakuri, "Exp-ParaDiag: Time-Parallel Exponential Integrators for
+ * Parabolic PDEs", arXiv 2603.04350.  Citations are PAPER.md line numbers (the paper's
+ * LaTeX source) with the equation / step; "R<k>" are the readings listed in DESIGN.md.
+ *
+ * Problem: u_t = (a Delta - c) u + N(u) on (0,1)^dim,
+ * homogeneous Dirichlet, n interior points per axis (h = 1/(n+1)), second-order finite
+ * differences, N_t steps of size dt, alpha-circulant parameter alpha.
+ *
+ * Conventions for every entry point:
+ *   - every call returns expd_status; nothing else crosses the ABI (no exceptions);
+ *   - on any error the output buffers are left untouched when the error is detected
+ *     before launch (INVALID_ARG / UNSUPPORTED); later CUDA errors may leave them
+ *     partially written;
+ *   - expd_plan_last_error() returns a human-readable message for the last failure;
+ *   - device pointers must live on the plan's device; all work is enqueued on the
+ *     plan's CUDA stream; "blocking" calls synchronise that stream;
+ *   - layouts: a physical slice is n^dim doubles, x fastest ([z][y][x]); a space-time
+ *     vector is nt_local consecutive slices, slice m-1 holding u_m (PAPER.md:98,
+ *     U = (u_1, ..., u_Nt)); u0 is one slice;
+ *   - with nranks > 1 every function is collective over the plan's communicator and
+ *     must be called by all ranks in the same order with identical problems.
+ *
+ * Ownership: the caller owns u0, U, R, S and the workspace (e.g. torch tensors passed
+ * as data_ptr()).  The plan owns only its small tables (KBs .. tens of MB of per-mode
+ * multipliers live in the caller's workspace) and never allocates in a solve loop.
+ */
+#ifndef EXPD_H
+#define EXPD_H
+#include <stddef.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  EXPD_OK = 0,
+  EXPD_ERR_INVALID_ARG = 1,   /* bad sizes, null pointers, alpha <= 0, ...        */
+  EXPD_ERR_UNSUPPORTED = 2,   /* valid math, not built (e.g. nt not a power of 2) */
+  EXPD_ERR_CUDA = 3,
+  EXPD_ERR_NCCL = 4,
+  EXPD_ERR_OOM = 5,           /* workspace too small                              */
+  EXPD_ERR_BREAKDOWN = 6,     /* |1 - lambda_k E_J| < 1e-14, NaN/Inf residual     */
+  EXPD_ERR_NOT_CONVERGED = 7  /* maxit reached; the report is still filled        */
+} expd_status;
+
+typedef enum {
+  EXPD_EXP_EULER = 0, /* linear (npoly = 0) or ETD1: u_n = E u_{n-1} + dt phi1 N(u_{n-1}) (R5) */
+  EXPD_ETD2 = 1       /* u_n = E u_{n-1} + dt[(phi1+phi2) N_{n-1} - phi2 N_{n-2}] (R6)        */
+} expd_scheme;
+
+typedef struct {
+  int dim;            /* 1, 2 or 3 (Remark 2.2)                       */
+  int n;              /* interior points per axis; requires n+1 = 2^m, 4 <= n+1 <= 4096 */
+  double a, c;        /* L_h = a Delta_h - c I, a > 0, c >= 0      */
+  double dt;          /* Delta t > 0                                                      */
+  int nt;             /* N_t: a power of two, 4 <= nt <= 256                              */
+  double alpha;       /* 0 < alpha <= 1 (Gamma_alpha singular at 0 -> INVALID_ARG, R10) */
+  expd_scheme scheme;
+  int npoly;          /* N(u) = sum_{p < npoly} q[p] u^p; 0 = linear; 0 <= npoly <= 8     */
+  double q[8];
+} expd_problem;
+
+typedef struct {
+  int rank, nranks;   /* this build: nranks == 1 (multi-GPU sharding: DESIGN.md)  */
+  void* nccl_comm;    /* ncclComm_t or NULL when nranks == 1                       */
+} expd_dist;
+
+typedef struct expd_plan expd_plan;
+
+typedef struct {
+  int iterations;     /* fixed point: preconditioner updates applied before rho_k < tol
+                         (R8); GMRES: Arnoldi matvecs                                   */
+  int sweeps;         /* HBM passes of the fused sweep (fixed point: iterations + 1)    */
+  int converged;      /* 1 if the tolerance was met                                     */
+  int hist_len;       /* entries written to hist                                        */
+  double rel_residual;/* last relative residual                                         */
+  double seconds;     /* wall time of the iteration loop (excludes setup / final IDST)  */
+  double* hist;       /* caller buffer of maxit + 2 doubles, or NULL                    */
+} expd_report;
+
+/* Validate the problem and build the plan's tables (per-axis eigenvalues lambda_j,
+   twiddles omega^q, Gamma_alpha powers, lambda_k) in long double rounded to double.
+   cuda_stream: a cudaStream_t (NULL = legacy default stream).  *out receives the plan. */
+expd_status expd_plan_create(const expd_problem* prob, const expd_dist* dist, int device, void* cuda_stream,
+                             expd_plan** out);
+/* Workspace the caller must provide: the spectral state, nonlinear history, per-mode
+   multiplier tables, transform scratch and krylov_vectors GMRES basis vectors
+   (0 = fixed point / primitives only).  */
+expd_status expd_plan_workspace_bytes(const expd_plan* plan, int krylov_vectors, size_t* bytes);
+/* Hand the plan a device buffer of at least the queried size (256-byte aligned).  The
+   number of GMRES basis vectors the buffer holds is derived from its size. */
+expd_status expd_plan_set_workspace(expd_plan* plan, void* d_ptr, size_t bytes);
+void expd_plan_destroy(expd_plan* plan);
+const char* expd_plan_last_error(const expd_plan* plan);
+
+/* All-at-once residual R = F(U) - Q U, slice by slice
+   R_n = A u_{n-1} + Phi[N] - u_n,  A = exp(dt L_h) (R5, R6).
+   u0: [n^dim], U, R: [nt][n^dim] physical, device.  rnorm2_host (nullable): receives
+   ||R||_2^2 (the call then synchronises).  Async otherwise.  R must not alias U. */
+expd_status expd_residual(expd_plan* plan, const double* u0, const double* U, double* R, double* rnorm2_host);
+
+/* S = Q_alpha^{-1} R by Steps (a)-(c): alpha-scaled time DFT,
+   per-frequency spatial solve (I - lambda_k A)^{-1} as DST / divide by (1 - lambda_k E_J)
+   / IDST, inverse DFT and unscaling.  R, S: [nt][n^dim] physical, device; S may alias R.
+   Async. */
+expd_status expd_precond_apply(expd_plan* plan, const double* R, double* S);
+
+/* Preconditioned Richardson / Picard (3.2) from the initial guess in
+   U (zeros per PAPER.md:895): sweep k computes r^k = F(U^k) - Q U^k, rho_k =
+   ||r^k|| / ||r^0||, U^{k+1} = U^k + Q_alpha^{-1} r^k; stops after the first sweep with
+   rho_k < tol (R8), returning U^{k+1} in U.  Blocking.  report (nullable). */
+expd_status expd_fixed_point_solve(expd_plan* plan, const double* u0, double* U, double tol, int maxit,
+                                   expd_report* report);
+
+/* Left-preconditioned restarted GMRES(restart) on Q_alpha^{-1} Q u = Q_alpha^{-1} f
+   (PAPER.md:284-289), classical Gram-Schmidt applied twice (R11), Givens rotations;
+   stops when ||Q_alpha^{-1}(f - Q x)|| / ||Q_alpha^{-1}(f - Q x_0)|| < tol.
+   Linear problems only (npoly == 0, else UNSUPPORTED).  The effective restart is
+   min(restart, krylov vectors in the workspace - 1).  U: initial guess in, solution out.
+   Blocking. */
+expd_status expd_gmres_solve(expd_plan* plan, const double* u0, double* U, double tol, int restart, int maxit,
+                             expd_report* report);
+
+/* ---- lower-level entry points used by the solver loop and the benchmark -------------- */
+/* Spectral-state sweep, the hot path of one Exp-ParaDiag iteration on data already in
+   the workspace (after expd_load_state): [nonlinear: N-hat of every slice (stage 3)] ->
+   fused residual + ||r||^2 + preconditioner + update (stages 1, 2).  Async; the residual
+   norm squared of this sweep is left on the device (read by expd_sweep_norm2). */
+expd_status expd_load_state(expd_plan* plan, const double* u0, const double* U);
+expd_status expd_sweep(expd_plan* plan);
+expd_status expd_sweep_norm2(expd_plan* plan, double* rnorm2_host); /* synchronises */
+expd_status expd_store_state(expd_plan* plan, double* U);           /* U = V U-hat, async */
+/* out = V in for nslices physical slices (the orthonormal DST-I along every axis,
+   PAPER.md:141; V = V^T = V^{-1}).  in, out: [nslices][n^dim] device; out may alias in.
+   Uses the workspace's transform scratch.  Async. */
+expd_status expd_dst(expd_plan* plan, const double* in, double* out, long nslices);
+/* Number of kernels one expd_sweep launches (for the benchmark's launch count). */
+int expd_sweep_kernel_launches(const expd_plan* plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,8 @@
+"""B200-native Exp-ParaDiag hot path (arXiv 2603.04350).
+
+libexpd.so (csrc/, C-ABI include/expd.h) holds every kernel; expd.py is the ctypes
+binding.  See DESIGN.md.
+"""
+from .expd import EXPORTS, ExpdError, Plan, Problem, load_library  # noqa: F401
+
+__all__ = ["Plan", "Problem", "ExpdError", "load_library", "EXPORTS"]

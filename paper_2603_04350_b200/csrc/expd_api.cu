@@ -1,0 +1,585 @@
+// expd_api.cu -- host side of libexpd.so: plan (tables), workspace carving, the C-ABI
+// entry points of include/expd.h, and the solver drivers (Richardson / Picard (3.2) and
+// left-preconditioned restarted GMRES with CGS2).  Every arithmetic step on the space-time
+// data runs in the kernels of k_time.cu / k_dst.cu / k_vec.cu; the host does only the
+// O(restart^2) Givens / least-squares scalars of GMRES and the convergence tests.
+#include <cuda_runtime.h>
+
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/expd.h"
+#include "expd_internal.h"
+
+using namespace expd;
+
+struct expd_plan {
+  expd_problem prob{};
+  expd_dist dist{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  Geom g{};
+  int sms = 148;
+  int nl = 0;  // 0 linear, 1 ETD1, 2 ETD2
+  double a1 = 0.0;
+  // small device tables owned by the plan
+  double* d_lam = nullptr;   // [n]
+  double2* d_twt = nullptr;  // [nt]  e^{+2 pi i q/nt}
+  double* d_g = nullptr;     // [nt]  alpha^{t/nt}
+  double* d_ginv = nullptr;  // [nt]
+  double2* d_twM = nullptr;  // [M]   e^{-2 pi i q/M}
+  double* d_sinp = nullptr;  // [M]   sin(pi i/M)
+  double* h_pin = nullptr;   // pinned host scalars [256]
+  // workspace (caller-owned)
+  char* ws = nullptr;
+  size_t ws_bytes = 0;
+  double *Uh = nullptr, *Nh = nullptr, *T1 = nullptr, *u0h = nullptr, *E = nullptr, *C1 = nullptr, *C2 = nullptr;
+  double *scratch = nullptr, *partial = nullptr, *dscal = nullptr;
+  double* krylov = nullptr;
+  int krylov_cap = 0;
+  int time_grid = 0, vgrid = 0;
+  bool tables_ready = false;
+  // CUDA graph of one sweep (captured on a private stream, launched on `stream`)
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t sweep_exec = nullptr;
+  std::string err;
+};
+
+static const size_t kAlign = 256;
+static size_t align_up(size_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+static expd_status fail(expd_plan* p, expd_status s, const std::string& m) {
+  if (p) p->err = m;
+  return s;
+}
+#define CUDA_TRY(p, x)                                                                       \
+  do {                                                                                       \
+    cudaError_t e_ = (x);                                                                    \
+    if (e_ != cudaSuccess)                                                                   \
+      return fail(p, EXPD_ERR_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));        \
+  } while (0)
+
+static bool is_pow2(long v) { return v > 0 && (v & (v - 1)) == 0; }
+
+// ---------------------------------------------------------------------------------------
+// tables (long double, rounded to double): PAPER.md:113-114 (omega, Gamma_alpha, lambda_k),
+// reading R1 (lambda_j), DST-I twiddles.
+// ---------------------------------------------------------------------------------------
+static const long double PI_L = 3.141592653589793238462643383279502884197L;
+
+static expd_status build_tables(expd_plan* p) {
+  const expd_problem& P = p->prob;
+  const int n = P.n, M = n + 1, nt = P.nt;
+  std::vector<double> lam(n), g(nt), gi(nt), sinp(M);
+  std::vector<double2> twt(nt), twM(M);
+  const long double h = 1.0L / (long double)M;
+  for (int j = 1; j <= n; ++j) {
+    long double s = sinl(PI_L * (long double)j / (2.0L * (long double)M));
+    lam[j - 1] = (double)(-4.0L / (h * h) * s * s);
+  }
+  for (int q = 0; q < nt; ++q) {
+    long double ang = 2.0L * PI_L * (long double)q / (long double)nt;
+    twt[q] = make_double2((double)cosl(ang), (double)sinl(ang));
+    long double gq = powl((long double)P.alpha, (long double)q / (long double)nt);
+    g[q] = (double)gq;
+    gi[q] = (double)(1.0L / gq);
+  }
+  for (int q = 0; q < M; ++q) {
+    long double ang = 2.0L * PI_L * (long double)q / (long double)M;
+    twM[q] = make_double2((double)cosl(ang), (double)(-sinl(ang)));
+    sinp[q] = (double)sinl(PI_L * (long double)q / (long double)M);
+  }
+  p->a1 = (double)powl((long double)P.alpha, 1.0L / (long double)nt);
+  CUDA_TRY(p, cudaSetDevice(p->device));
+  CUDA_TRY(p, cudaMalloc(&p->d_lam, sizeof(double) * n));
+  CUDA_TRY(p, cudaMalloc(&p->d_twt, sizeof(double2) * nt));
+  CUDA_TRY(p, cudaMalloc(&p->d_g, sizeof(double) * nt));
+  CUDA_TRY(p, cudaMalloc(&p->d_ginv, sizeof(double) * nt));
+  CUDA_TRY(p, cudaMalloc(&p->d_twM, sizeof(double2) * M));
+  CUDA_TRY(p, cudaMalloc(&p->d_sinp, sizeof(double) * M));
+  CUDA_TRY(p, cudaMallocHost(&p->h_pin, sizeof(double) * 256));
+  CUDA_TRY(p, cudaMemcpy(p->d_lam, lam.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
+  CUDA_TRY(p, cudaMemcpy(p->d_twt, twt.data(), sizeof(double2) * nt, cudaMemcpyHostToDevice));
+  CUDA_TRY(p, cudaMemcpy(p->d_g, g.data(), sizeof(double) * nt, cudaMemcpyHostToDevice));
+  CUDA_TRY(p, cudaMemcpy(p->d_ginv, gi.data(), sizeof(double) * nt, cudaMemcpyHostToDevice));
+  CUDA_TRY(p, cudaMemcpy(p->d_twM, twM.data(), sizeof(double2) * M, cudaMemcpyHostToDevice));
+  CUDA_TRY(p, cudaMemcpy(p->d_sinp, sinp.data(), sizeof(double) * M, cudaMemcpyHostToDevice));
+  return EXPD_OK;
+}
+
+extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dist* dist, int device,
+                                        void* cuda_stream, expd_plan** out) {
+  if (!prob || !out) return EXPD_ERR_INVALID_ARG;
+  *out = nullptr;
+  const expd_problem& P = *prob;
+  if (P.dim < 1 || P.dim > 3 || P.n < 3 || !is_pow2((long)P.n + 1) || P.n + 1 > 4096 || !(P.a > 0.0) ||
+      !(P.c >= 0.0) || !(P.dt > 0.0) || P.nt < 4 || !is_pow2(P.nt) || !(P.alpha > 0.0) || !(P.alpha <= 1.0) ||
+      P.npoly < 0 || P.npoly > 8 || (P.scheme != EXPD_EXP_EULER && P.scheme != EXPD_ETD2) ||
+      !std::isfinite(P.a) || !std::isfinite(P.c) || !std::isfinite(P.dt))
+    return EXPD_ERR_INVALID_ARG;
+  if (P.nt > 256) return EXPD_ERR_UNSUPPORTED;
+  int nranks = dist ? dist->nranks : 1;
+  if (nranks < 1 || (dist && (dist->rank < 0 || dist->rank >= nranks))) return EXPD_ERR_INVALID_ARG;
+  if (nranks != 1) return EXPD_ERR_UNSUPPORTED;
+  // breakdown guard: min_{k,J} |1 - lambda_k E_J| >= 1 - alpha^{1/nt} max_J E_J (R10)
+  {
+    long double h = 1.0L / (long double)(P.n + 1);
+    long double s = sinl(PI_L / (2.0L * (long double)(P.n + 1)));
+    long double mu_max = (long double)P.a * (long double)P.dim * (-4.0L / (h * h) * s * s) - (long double)P.c;
+    long double Emax = expl((long double)P.dt * mu_max);
+    long double a1 = powl((long double)P.alpha, 1.0L / (long double)P.nt);
+    if (1.0L - a1 * Emax < 1e-14L) return EXPD_ERR_BREAKDOWN;
+  }
+  expd_plan* p = new expd_plan();
+  p->prob = P;
+  if (dist) p->dist = *dist;
+  else p->dist.nranks = 1;
+  p->device = device;
+  p->stream = (cudaStream_t)cuda_stream;
+  p->g.dim = P.dim;
+  p->g.n = P.n;
+  p->g.M = P.n + 1;
+  long N = 1, npad = P.n + 1;
+  for (int i = 0; i < P.dim; ++i) N *= P.n;
+  for (int i = 1; i < P.dim; ++i) npad *= P.n;
+  p->g.N = N;
+  p->g.npad = npad;
+  p->nl = P.npoly > 0 ? (P.scheme == EXPD_ETD2 ? 2 : 1) : 0;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete p;
+    return EXPD_ERR_CUDA;
+  }
+  cudaDeviceGetAttribute(&p->sms, cudaDevAttrMultiProcessorCount, device);
+  expd_status st = build_tables(p);
+  if (st != EXPD_OK) {
+    expd_plan_destroy(p);
+    return st;
+  }
+  p->time_grid = time_fused_grid(P.nt, npad / 2, p->sms);
+  p->vgrid = vec_grid(p->sms);
+  *out = p;
+  return EXPD_OK;
+}
+
+// workspace layout (every block 256-byte aligned)
+struct Layout {
+  size_t Uh, Nh, T1, u0h, E, C1, C2, scratch, partial, dscal, krylov, total, vec;
+};
+static Layout layout(const expd_plan* p, int kv) {
+  Layout L{};
+  const size_t vec = align_up(sizeof(double) * (size_t)p->prob.nt * (size_t)p->g.npad);
+  const size_t sl = align_up(sizeof(double) * (size_t)p->g.npad);
+  size_t off = 0;
+  L.vec = vec;
+  L.Uh = off; off += vec;
+  L.Nh = off; off += (p->nl ? vec : 0);
+  L.T1 = off; off += vec;
+  L.u0h = off; off += sl;
+  L.E = off; off += sl;
+  L.C1 = off; off += sl;
+  L.C2 = off; off += sl;
+  L.scratch = off; off += align_up(sizeof(double) * dst_scratch_doubles(p->g, nonlin_chunk_slices(p->g)));
+  L.partial = off; off += align_up(sizeof(double) * 32 * (size_t)(p->sms * 8 + 64));
+  L.dscal = off; off += align_up(sizeof(double) * 256);
+  L.krylov = off; off += (size_t)kv * vec;
+  L.total = off;
+  return L;
+}
+
+extern "C" expd_status expd_plan_workspace_bytes(const expd_plan* p, int krylov_vectors, size_t* bytes) {
+  if (!p || !bytes || krylov_vectors < 0 || krylov_vectors > 32) return EXPD_ERR_INVALID_ARG;
+  *bytes = layout(p, krylov_vectors).total;
+  return EXPD_OK;
+}
+
+extern "C" expd_status expd_plan_set_workspace(expd_plan* p, void* d_ptr, size_t bytes) {
+  if (!p || !d_ptr) return EXPD_ERR_INVALID_ARG;
+  if (((uintptr_t)d_ptr) % kAlign) return fail(p, EXPD_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
+  Layout L0 = layout(p, 0);
+  if (bytes < L0.total) return fail(p, EXPD_ERR_OOM, "workspace smaller than expd_plan_workspace_bytes(plan, 0)");
+  int kv = (int)((bytes - L0.total) / L0.vec);
+  if (kv > 32) kv = 32;
+  Layout L = layout(p, kv);
+  p->ws = (char*)d_ptr;
+  p->ws_bytes = bytes;
+  auto at = [&](size_t off) { return (double*)(p->ws + off); };
+  p->Uh = at(L.Uh);
+  p->Nh = p->nl ? at(L.Nh) : nullptr;
+  p->T1 = at(L.T1);
+  p->u0h = at(L.u0h);
+  p->E = at(L.E);
+  p->C1 = at(L.C1);
+  p->C2 = at(L.C2);
+  p->scratch = at(L.scratch);
+  p->partial = at(L.partial);
+  p->dscal = at(L.dscal);
+  p->krylov = kv ? at(L.krylov) : nullptr;
+  p->krylov_cap = kv;
+  if (p->sweep_exec) {
+    cudaGraphExecDestroy(p->sweep_exec);
+    p->sweep_exec = nullptr;
+  }
+  CUDA_TRY(p, cudaSetDevice(p->device));
+  CUDA_TRY(p, mode_tables(p->g, p->d_lam, p->prob.a, p->prob.c, p->prob.dt, p->prob.scheme, p->E, p->C1, p->C2,
+                          p->stream));
+  p->tables_ready = true;
+  return EXPD_OK;
+}
+
+extern "C" void expd_plan_destroy(expd_plan* p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  if (p->sweep_exec) cudaGraphExecDestroy(p->sweep_exec);
+  if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
+  cudaFree(p->d_lam);
+  cudaFree(p->d_twt);
+  cudaFree(p->d_g);
+  cudaFree(p->d_ginv);
+  cudaFree(p->d_twM);
+  cudaFree(p->d_sinp);
+  if (p->h_pin) cudaFreeHost(p->h_pin);
+  delete p;
+}
+
+extern "C" const char* expd_plan_last_error(const expd_plan* p) { return p ? p->err.c_str() : "null plan"; }
+
+// ---------------------------------------------------------------------------------------
+// internal helpers
+// ---------------------------------------------------------------------------------------
+static DstTables dst_tables(const expd_plan* p) { return DstTables{p->d_twM, p->d_sinp}; }
+
+static TimeArgs time_args(const expd_plan* p, const double* X, double* Y, bool with_partial) {
+  TimeArgs a{};
+  a.nt = p->prob.nt;
+  a.npad = p->g.npad;
+  a.npairs = p->g.npad / 2;
+  a.X = X;
+  a.Y = Y;
+  a.u0h = p->u0h;
+  a.Nh = p->Nh;
+  a.E = p->E;
+  a.C1 = p->C1;
+  a.C2 = p->C2;
+  a.g = p->d_g;
+  a.ginv = p->d_ginv;
+  a.tw = p->d_twt;
+  a.a1 = p->a1;
+  a.half_inv_nt = 0.5 / (double)p->prob.nt;
+  a.partial = with_partial ? p->partial : nullptr;
+  return a;
+}
+
+static expd_status ready(expd_plan* p) {
+  if (!p) return EXPD_ERR_INVALID_ARG;
+  if (!p->ws || !p->tables_ready) return fail(p, EXPD_ERR_INVALID_ARG, "workspace not set");
+  if (cudaSetDevice(p->device) != cudaSuccess) return fail(p, EXPD_ERR_CUDA, "cudaSetDevice");
+  return EXPD_OK;
+}
+
+// spectral u0 and (nonlinear) N-hat_0 = V N(u_0)
+static expd_status load_u0(expd_plan* p, const double* u0) {
+  CUDA_TRY(p, dst_slices(p->g, dst_tables(p), u0, false, p->u0h, true, 1, p->scratch, p->stream));
+  if (p->nl)
+    CUDA_TRY(p, nonlin_phys_slices(p->g, dst_tables(p), u0, p->Nh, 1, p->prob.npoly, p->prob.q, p->scratch,
+                                   p->stream));
+  return EXPD_OK;
+}
+
+// One sweep on the spectral state: stage 3 (nonlinear history of u_1..u_{nt-1}), then the
+// fused residual / norm / preconditioner / update (stages 1, 2), then the norm reduction.
+static cudaError_t enqueue_sweep(expd_plan* p, cudaStream_t st) {
+  cudaError_t e;
+  if (p->nl) {
+    e = nonlin_slices(p->g, dst_tables(p), p->Uh, p->Nh + p->g.npad, p->prob.nt - 1, p->prob.npoly, p->prob.q,
+                      p->scratch, st);
+    if (e != cudaSuccess) return e;
+  }
+  TimeArgs a = time_args(p, p->Uh, p->Uh, true);
+  e = launch_time_fused(a, RM_RESID, OUT_UPDATE, p->nl, p->time_grid, st);
+  if (e != cudaSuccess) return e;
+  return reduce_partials(p->partial, p->time_grid, p->dscal, st);
+}
+
+static expd_status sweep(expd_plan* p, bool use_graph) {
+  if (!use_graph) {
+    CUDA_TRY(p, enqueue_sweep(p, p->stream));
+    return EXPD_OK;
+  }
+  if (!p->sweep_exec) {
+    cudaGraph_t graph;
+    if (!p->cap_stream) CUDA_TRY(p, cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
+    CUDA_TRY(p, cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal));
+    cudaError_t e = enqueue_sweep(p, p->cap_stream);
+    cudaError_t e2 = cudaStreamEndCapture(p->cap_stream, &graph);
+    if (e != cudaSuccess) return fail(p, EXPD_ERR_CUDA, std::string("sweep capture: ") + cudaGetErrorString(e));
+    if (e2 != cudaSuccess) return fail(p, EXPD_ERR_CUDA, std::string("end capture: ") + cudaGetErrorString(e2));
+    e = cudaGraphInstantiate(&p->sweep_exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (e != cudaSuccess) return fail(p, EXPD_ERR_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+  }
+  CUDA_TRY(p, cudaGraphLaunch(p->sweep_exec, p->stream));
+  return EXPD_OK;
+}
+
+static bool graphs_enabled() {
+  const char* s = getenv("EXPD_NO_GRAPH");
+  return !(s && s[0] == '1');
+}
+
+static expd_status read_scalars(expd_plan* p, int count, double* out) {
+  CUDA_TRY(p, cudaMemcpyAsync(p->h_pin, p->dscal, sizeof(double) * count, cudaMemcpyDeviceToHost, p->stream));
+  CUDA_TRY(p, cudaStreamSynchronize(p->stream));
+  for (int i = 0; i < count; ++i) out[i] = p->h_pin[i];
+  return EXPD_OK;
+}
+
+// ---------------------------------------------------------------------------------------
+// C-ABI: primitives
+// ---------------------------------------------------------------------------------------
+extern "C" expd_status expd_residual(expd_plan* p, const double* u0, const double* U, double* R,
+                                     double* rnorm2_host) {
+  expd_status s = ready(p);
+  if (s) return s;
+  if (!u0 || !U || !R || U == R) return fail(p, EXPD_ERR_INVALID_ARG, "expd_residual: bad pointers");
+  const long nt = p->prob.nt;
+  s = load_u0(p, u0);
+  if (s) return s;
+  CUDA_TRY(p, dst_slices(p->g, dst_tables(p), U, false, p->Uh, true, nt, p->scratch, p->stream));
+  if (p->nl && nt > 1)  // N-hat_m = V N(u_m), m = 1..nt-1, straight from the physical slices
+    CUDA_TRY(p, nonlin_phys_slices(p->g, dst_tables(p), U, p->Nh + p->g.npad, nt - 1, p->prob.npoly, p->prob.q,
+                                   p->scratch, p->stream));
+  TimeArgs a = time_args(p, p->Uh, p->T1, true);
+  CUDA_TRY(p, launch_resid_only(a, p->nl, p->time_grid, p->stream));
+  CUDA_TRY(p, reduce_partials(p->partial, p->time_grid, p->dscal, p->stream));
+  CUDA_TRY(p, dst_slices(p->g, dst_tables(p), p->T1, true, R, false, nt, p->scratch, p->stream));
+  if (rnorm2_host) return read_scalars(p, 1, rnorm2_host);
+  return EXPD_OK;
+}
+
+extern "C" expd_status expd_precond_apply(expd_plan* p, const double* R, double* S) {
+  expd_status s = ready(p);
+  if (s) return s;
+  if (!R || !S) return fail(p, EXPD_ERR_INVALID_ARG, "expd_precond_apply: bad pointers");
+  const long nt = p->prob.nt;
+  CUDA_TRY(p, dst_slices(p->g, dst_tables(p), R, false, p->T1, true, nt, p->scratch, p->stream));
+  TimeArgs a = time_args(p, p->T1, p->T1, false);
+  CUDA_TRY(p, launch_time_fused(a, RM_INPUT, OUT_S, 0, p->time_grid, p->stream));
+  CUDA_TRY(p, dst_slices(p->g, dst_tables(p), p->T1, true, S, false, nt, p->scratch, p->stream));
+  return EXPD_OK;
+}
+
+extern "C" expd_status expd_load_state(expd_plan* p, const double* u0, const double* U) {
+  expd_status s = ready(p);
+  if (s) return s;
+  if (!u0) return fail(p, EXPD_ERR_INVALID_ARG, "expd_load_state: u0 is null");
+  s = load_u0(p, u0);
+  if (s) return s;
+  if (U) CUDA_TRY(p, dst_slices(p->g, dst_tables(p), U, false, p->Uh, true, p->prob.nt, p->scratch, p->stream));
+  else CUDA_TRY(p, cudaMemsetAsync(p->Uh, 0, sizeof(double) * p->prob.nt * p->g.npad, p->stream));
+  return EXPD_OK;
+}
+
+extern "C" expd_status expd_sweep(expd_plan* p) {
+  expd_status s = ready(p);
+  if (s) return s;
+  return sweep(p, graphs_enabled());
+}
+
+extern "C" expd_status expd_sweep_norm2(expd_plan* p, double* rnorm2_host) {
+  expd_status s = ready(p);
+  if (s) return s;
+  if (!rnorm2_host) return EXPD_ERR_INVALID_ARG;
+  return read_scalars(p, 1, rnorm2_host);
+}
+
+extern "C" expd_status expd_store_state(expd_plan* p, double* U) {
+  expd_status s = ready(p);
+  if (s) return s;
+  if (!U) return EXPD_ERR_INVALID_ARG;
+  CUDA_TRY(p, dst_slices(p->g, dst_tables(p), p->Uh, true, U, false, p->prob.nt, p->scratch, p->stream));
+  return EXPD_OK;
+}
+
+extern "C" expd_status expd_dst(expd_plan* p, const double* in, double* out, long nslices) {
+  expd_status s = ready(p);
+  if (s) return s;
+  if (!in || !out || nslices < 0) return fail(p, EXPD_ERR_INVALID_ARG, "expd_dst: bad args");
+  const long chunk = p->prob.nt;  // T1 holds nt spectral slices
+  for (long s0 = 0; s0 < nslices; s0 += chunk) {
+    long ns = nslices - s0 < chunk ? nslices - s0 : chunk;
+    CUDA_TRY(p, dst_slices(p->g, dst_tables(p), in + s0 * p->g.N, false, p->T1, true, ns, p->scratch, p->stream));
+    // drop the pad column: spectral rows of n+1 doubles -> rows of n doubles
+    CUDA_TRY(p, cudaMemcpy2DAsync(out + s0 * p->g.N, sizeof(double) * p->g.n, p->T1, sizeof(double) * p->g.M,
+                                  sizeof(double) * p->g.n, (size_t)ns * (p->g.N / p->g.n),
+                                  cudaMemcpyDeviceToDevice, p->stream));
+  }
+  return EXPD_OK;
+}
+
+extern "C" int expd_sweep_kernel_launches(const expd_plan* p) {
+  if (!p) return 0;
+  int k = 2;  // fused time pass + norm reduction
+  if (p->nl) k += nonlin_kernel_launches(p->g, p->prob.nt - 1);
+  return k;
+}
+
+// ---------------------------------------------------------------------------------------
+// solvers
+// ---------------------------------------------------------------------------------------
+static void fill_report(expd_report* r, int its, int sweeps, int conv, const std::vector<double>& hist,
+                        double secs) {
+  if (!r) return;
+  r->iterations = its;
+  r->sweeps = sweeps;
+  r->converged = conv;
+  r->rel_residual = hist.empty() ? 0.0 : hist.back();
+  r->seconds = secs;
+  r->hist_len = (int)hist.size();
+  if (r->hist)
+    for (size_t i = 0; i < hist.size(); ++i) r->hist[i] = hist[i];
+}
+
+extern "C" expd_status expd_fixed_point_solve(expd_plan* p, const double* u0, double* U, double tol, int maxit,
+                                              expd_report* report) {
+  expd_status s = ready(p);
+  if (s) return s;
+  if (!u0 || !U || maxit < 0 || !(tol >= 0.0)) return fail(p, EXPD_ERR_INVALID_ARG, "fixed_point: bad args");
+  s = expd_load_state(p, u0, U);
+  if (s) return s;
+  CUDA_TRY(p, cudaStreamSynchronize(p->stream));
+  const bool graphs = graphs_enabled();
+  std::vector<double> hist;
+  double r0 = 0.0;
+  int k = 0, conv = 0;
+  auto t0 = std::chrono::steady_clock::now();
+  for (k = 0; k <= maxit; ++k) {
+    s = sweep(p, graphs && k > 0);  // first sweep eager (kernel attributes), then the graph
+    if (s) return s;
+    double rn2;
+    s = read_scalars(p, 1, &rn2);
+    if (s) return s;
+    if (!std::isfinite(rn2)) {
+      fill_report(report, k, k + 1, 0, hist, 0.0);
+      return fail(p, EXPD_ERR_BREAKDOWN, "non-finite residual norm");
+    }
+    double rn = std::sqrt(rn2);
+    if (k == 0) r0 = rn;
+    double rho = r0 > 0.0 ? rn / r0 : 0.0;
+    hist.push_back(rho);
+    if (rho < tol) {
+      conv = 1;
+      break;
+    }
+  }
+  double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  int its = conv ? k : maxit;
+  fill_report(report, its, conv ? k + 1 : maxit + 1, conv, hist, secs);
+  s = expd_store_state(p, U);
+  if (s) return s;
+  CUDA_TRY(p, cudaStreamSynchronize(p->stream));
+  return conv ? EXPD_OK : EXPD_ERR_NOT_CONVERGED;
+}
+
+extern "C" expd_status expd_gmres_solve(expd_plan* p, const double* u0, double* U, double tol, int restart,
+                                        int maxit, expd_report* report) {
+  expd_status s = ready(p);
+  if (s) return s;
+  if (!u0 || !U || maxit < 0 || restart < 1 || !(tol >= 0.0)) return fail(p, EXPD_ERR_INVALID_ARG, "gmres: bad args");
+  if (p->nl) return fail(p, EXPD_ERR_UNSUPPORTED, "GMRES is for linear problems (npoly == 0)");
+  if (p->krylov_cap < 1) return fail(p, EXPD_ERR_OOM, "workspace holds no Krylov vectors");
+  const int m = restart < p->krylov_cap ? restart : p->krylov_cap;
+  const long len = (long)p->prob.nt * p->g.npad;
+  const size_t vstride = align_up(sizeof(double) * (size_t)len) / sizeof(double);
+  auto Vk = [&](int i) { return p->krylov + (size_t)i * vstride; };
+  s = expd_load_state(p, u0, U);
+  if (s) return s;
+  CUDA_TRY(p, cudaStreamSynchronize(p->stream));
+  std::vector<double> hist{1.0};
+  std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), gv(m + 1), y(m), hcol(m + 1), h2(m + 1);
+  std::vector<const double*> Vp(m + 1);
+  double beta0 = -1.0;
+  int its = 0, conv = 0;
+  double* dcoef = p->dscal + 128;  // device coefficient scratch (128 doubles)
+  auto t0 = std::chrono::steady_clock::now();
+  while (its < maxit) {
+    // z = Q_alpha^{-1}(f - Q x)  [K1: residual -> precondition], beta = ||z||
+    TimeArgs a = time_args(p, p->Uh, p->T1, false);
+    CUDA_TRY(p, launch_time_fused(a, RM_RESID, OUT_S, 0, p->time_grid, p->stream));
+    const double* t1c = p->T1;
+    CUDA_TRY(p, multi_dot(&t1c, 1, p->T1, len, p->partial, p->vgrid, p->dscal, p->stream));
+    double b2;
+    s = read_scalars(p, 1, &b2);
+    if (s) return s;
+    double beta = std::sqrt(b2);
+    if (beta0 < 0.0) beta0 = beta;
+    if (beta0 == 0.0 || beta / beta0 < tol) {
+      conv = 1;
+      break;
+    }
+    CUDA_TRY(p, scale_copy(p->T1, 1.0 / beta, Vk(0), len, p->stream));
+    std::fill(gv.begin(), gv.end(), 0.0);
+    gv[0] = beta;
+    int j = 0, done = 0;
+    for (j = 0; j < m && its < maxit; ++j) {
+      for (int i = 0; i <= j; ++i) Vp[i] = Vk(i);
+      TimeArgs q = time_args(p, Vk(j), p->T1, false);
+      CUDA_TRY(p, launch_time_fused(q, RM_QOP, OUT_S, 0, p->time_grid, p->stream));  // w = P Q v_j
+      // CGS2: h = V^T w ; w -= V h ; h2 = V^T w ; w -= V h2 ; ||w||^2
+      CUDA_TRY(p, multi_dot(Vp.data(), j + 1, p->T1, len, p->partial, p->vgrid, dcoef, p->stream));
+      CUDA_TRY(p, multi_axpy_dot(Vp.data(), j + 1, dcoef, p->T1, len, p->partial, p->vgrid, dcoef + 40, 1,
+                                 p->stream));
+      CUDA_TRY(p, multi_axpy_dot(Vp.data(), j + 1, dcoef + 40, p->T1, len, p->partial, p->vgrid, dcoef + 80, 2,
+                                 p->stream));
+      CUDA_TRY(p, cudaMemcpyAsync(p->h_pin, dcoef, sizeof(double) * 81, cudaMemcpyDeviceToHost, p->stream));
+      CUDA_TRY(p, cudaStreamSynchronize(p->stream));
+      for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = p->h_pin[i] + p->h_pin[40 + i];
+      double hn = std::sqrt(p->h_pin[80]);
+      double hsub = hn;
+      for (int i = 0; i < j; ++i) {
+        double a0 = H[(size_t)i * m + j], b0 = H[(size_t)(i + 1) * m + j];
+        H[(size_t)i * m + j] = cs[i] * a0 + sn[i] * b0;
+        H[(size_t)(i + 1) * m + j] = -sn[i] * a0 + cs[i] * b0;
+      }
+      double a0 = H[(size_t)j * m + j];
+      double den = std::sqrt(a0 * a0 + hsub * hsub);
+      cs[j] = den > 0.0 ? a0 / den : 1.0;
+      sn[j] = den > 0.0 ? hsub / den : 0.0;
+      H[(size_t)j * m + j] = den;
+      gv[j + 1] = -sn[j] * gv[j];
+      gv[j] = cs[j] * gv[j];
+      ++its;
+      double rel = std::fabs(gv[j + 1]) / beta0;
+      hist.push_back(rel);
+      if (rel < tol || hn == 0.0) {
+        done = 1;
+        ++j;
+        break;
+      }
+      if (j + 1 < m) CUDA_TRY(p, scale_copy(p->T1, 1.0 / hn, Vk(j + 1), len, p->stream));
+    }
+    for (int i = j - 1; i >= 0; --i) {
+      double sacc = gv[i];
+      for (int l = i + 1; l < j; ++l) sacc -= H[(size_t)i * m + l] * y[l];
+      y[i] = sacc / H[(size_t)i * m + i];
+    }
+    for (int i = 0; i < j; ++i) Vp[i] = Vk(i);
+    CUDA_TRY(p, cudaMemcpyAsync(dcoef, y.data(), sizeof(double) * j, cudaMemcpyHostToDevice, p->stream));
+    CUDA_TRY(p, lincomb_add(Vp.data(), j, dcoef, p->Uh, len, p->stream));
+    CUDA_TRY(p, cudaStreamSynchronize(p->stream));
+    if (done) {
+      conv = 1;
+      break;
+    }
+  }
+  double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  fill_report(report, its, its, conv, hist, secs);
+  s = expd_store_state(p, U);
+  if (s) return s;
+  CUDA_TRY(p, cudaStreamSynchronize(p->stream));
+  return conv ? EXPD_OK : EXPD_ERR_NOT_CONVERGED;
+}

@@ -1,0 +1,82 @@
+// expd_internal.h -- internal types shared by the host driver and the kernels of libexpd.so.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstddef>
+#include <cstdint>
+
+namespace expd {
+
+// Spectral layout: every x-line of a spectral slice is padded
+// from n to n+1 doubles (n+1 = 2^m), so a spectral slice holds n^{dim-1} (n+1) doubles,
+// every line and every pair of modes (2p, 2p+1) is 16-byte aligned, and the pad entry
+// (jx = n) is an inert dummy mode that stays exactly 0 (its tables are 0).
+struct Geom {
+  int dim, n;
+  long N;     // n^dim physical points per slice
+  long npad;  // spectral slice length n^{dim-1} (n+1)
+  int M;      // n + 1
+};
+
+// Per-launch parameters of the time-local fused kernel (K1).
+struct TimeArgs {
+  int nt;
+  long npad;
+  long npairs;        // npad / 2
+  const double* X;    // input space-time vector [nt][npad]
+  double* Y;          // output [nt][npad] (may alias X)
+  const double* u0h;  // spectral u_0 [npad]
+  const double* Nh;   // nonlinear history [nt][npad], Nh[m] = V N(u_m), m = 0..nt-1
+  const double* E;    // [npad] E_J = exp(dt mu_J), 0 on pads
+  const double* C1;   // [npad] ETD1: dt phi1 ; ETD2: dt (phi1 + phi2)
+  const double* C2;   // [npad] ETD2: dt phi2
+  const double* g;    // [nt] alpha^{t/nt}
+  const double* ginv; // [nt] alpha^{-t/nt}
+  const double2* tw;  // [nt] exp(+2 pi i q / nt)
+  double a1;          // alpha^{1/nt}
+  double half_inv_nt; // 1 / (2 nt)
+  double* partial;    // [gridDim.x] per-CTA sum of r^2 (nullable)
+};
+
+enum ResidMode { RM_INPUT = 0, RM_RESID = 1, RM_QOP = 2 };
+enum OutMode { OUT_S = 0, OUT_UPDATE = 1 };
+
+// kernel launchers (k_time.cu)
+cudaError_t launch_time_fused(const TimeArgs& a, int rmode, int outmode, int nl, int grid, cudaStream_t st);
+int time_fused_grid(int nt, long npairs, int sms);
+cudaError_t launch_resid_only(const TimeArgs& a, int nl, int grid, cudaStream_t st);
+
+// DST-I / nonlinear (k_dst.cu)
+struct DstTables {
+  const double2* tw;   // [M] exp(-2 pi i q / M)
+  const double* sinp;  // [M] sin(pi i / M)
+};
+// Orthonormal DST-I of every slice along every axis: physical (row stride n) <-> spectral
+// (row stride n+1).  src/dst may alias only when both are spectral.
+cudaError_t dst_slices(const Geom& g, const DstTables& t, const double* src, bool src_spectral, double* dst,
+                       bool dst_spectral, long nslices, double* scratch, cudaStream_t st);
+// N-hat = V N(V u-hat) for nslices spectral slices (stage 3 of the sweep, K4).
+cudaError_t nonlin_slices(const Geom& g, const DstTables& t, const double* uhat, double* nhat, long nslices,
+                          int npoly, const double* q, double* scratch, cudaStream_t st);
+// N-hat = V N(u) for physical slices u (row stride n).
+cudaError_t nonlin_phys_slices(const Geom& g, const DstTables& t, const double* u, double* nhat, long nslices,
+                               int npoly, const double* q, double* scratch, cudaStream_t st);
+size_t dst_scratch_doubles(const Geom& g, long max_slices);
+int nonlin_chunk_slices(const Geom& g);
+int nonlin_kernel_launches(const Geom& g, long nslices);
+
+// vector kernels (k_vec.cu)
+cudaError_t mode_tables(const Geom& g, const double* lam_axis, double a, double c, double dt, int scheme,
+                        double* E, double* C1, double* C2, cudaStream_t st);
+cudaError_t reduce_partials(const double* partial, int n, double* out, cudaStream_t st);
+// GMRES / CGS2 helpers over vectors of length len (all 16-byte aligned, len even)
+cudaError_t multi_dot(const double* const* V, int nv, const double* w, long len, double* partial, int grid,
+                      double* out, cudaStream_t st);
+cudaError_t multi_axpy_dot(const double* const* V, int nv, const double* coef_dev, double* w, long len,
+                           double* partial, int grid, double* out, int want_dot, cudaStream_t st);
+cudaError_t scale_copy(const double* x, double s, double* y, long len, cudaStream_t st);
+cudaError_t lincomb_add(const double* const* V, int nv, const double* coef_dev, double* x, long len,
+                        cudaStream_t st);
+int vec_grid(int sms);
+
+}  // namespace expd

@@ -1,0 +1,262 @@
+// k_vec.cu -- per-mode multiplier tables, deterministic reductions, and the GMRES
+// (classical Gram-Schmidt twice, R11) vector kernels K6/K7 (stage 4 of the hot path,
+// BASELINE.json:5 "dot products and norms for the preconditioned-GMRES variant").
+// Reductions are warp-shuffle + fixed-order block sums into per-CTA partials, then a
+// fixed-order single-CTA sum: the result does not depend on scheduling.
+#include "expd_internal.h"
+
+namespace expd {
+
+// ---------------------------------------------------------------------------------------
+// E_J = exp(dt mu_J), mu_J = a sum_axes lambda_{j} - c (R1);
+// ETD1: C1 = dt phi1(z); ETD2: C1 = dt (phi1 + phi2)(z), C2 = dt phi2(z), z = dt mu_J (R5,
+// R6); Taylor series for |z| < 1/2 (R7).  Pad modes (jx = n) get 0.
+// ---------------------------------------------------------------------------------------
+__device__ void phi12(double z, double* p1, double* p2) {
+  if (fabs(z) < 0.5) {
+    // Horner on sum_k z^k/(k+1)! and sum_k z^k/(k+2)!, 22 terms (|z|^22/23! < 1e-29)
+    double a = 0.0, b = 0.0;
+    for (int k = 21; k >= 0; --k) {
+      double f1 = 1.0, f2 = 1.0;
+      // 1/(k+1)! and 1/(k+2)! computed exactly enough in double by a short product
+      for (int i = 2; i <= k + 1; ++i) f1 /= (double)i;
+      f2 = f1 / (double)(k + 2);
+      a = fma(a, z, f1);
+      b = fma(b, z, f2);
+    }
+    *p1 = a;
+    *p2 = b;
+  } else {
+    double em1 = expm1(z);
+    *p1 = em1 / z;
+    *p2 = (em1 - z) / (z * z);
+  }
+}
+
+__global__ void k_mode_tables(int dim, int n, int M, long npad, const double* lam, double a, double c, double dt,
+                              int scheme, double* E, double* C1, double* C2) {
+  for (long J = blockIdx.x * (long)blockDim.x + threadIdx.x; J < npad; J += (long)gridDim.x * blockDim.x) {
+    const int jx = (int)(J % M);
+    double e = 0.0, c1 = 0.0, c2 = 0.0;
+    if (jx < n) {
+      long r = J / M;
+      double s = lam[jx];
+      for (int ax = 1; ax < dim; ++ax) {
+        s += lam[r % n];
+        r /= n;
+      }
+      const double mu = a * s - c;
+      const double z = dt * mu;
+      e = exp(z);
+      double p1, p2;
+      phi12(z, &p1, &p2);
+      if (scheme == 0) {
+        c1 = dt * p1;
+      } else {
+        c1 = dt * (p1 + p2);
+        c2 = dt * p2;
+      }
+    }
+    E[J] = e;
+    if (C1) C1[J] = c1;
+    if (C2) C2[J] = c2;
+  }
+}
+
+cudaError_t mode_tables(const Geom& g, const double* lam_axis, double a, double c, double dt, int scheme,
+                        double* E, double* C1, double* C2, cudaStream_t st) {
+  k_mode_tables<<<1024, 256, 0, st>>>(g.dim, g.n, g.M, g.npad, lam_axis, a, c, dt, scheme, E, C1, C2);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// block reduction helper (256 threads)
+// ---------------------------------------------------------------------------------------
+template <int NV>
+__device__ __forceinline__ void block_sum_store(double (&v)[NV], double* out, int stride) {
+  __shared__ double red[NV][8];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    double x = v[i];
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    if ((threadIdx.x & 31) == 0) red[i][threadIdx.x >> 5] = x;
+  }
+  __syncthreads();
+  if (threadIdx.x < NV) {
+    double x = 0.0;
+    for (int w = 0; w < 8; ++w) x += red[threadIdx.x][w];
+    out[threadIdx.x * stride + blockIdx.x] = x;
+  }
+}
+
+__global__ void k_reduce_rows(const double* partial, int n, int rows, double* out) {
+  // one warp per row, fixed lane order, then fixed shuffle tree
+  const int row = blockIdx.x;
+  if (row >= rows) return;
+  double x = 0.0;
+  for (int i = threadIdx.x; i < n; i += 32) x += partial[(long)row * n + i];
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  if (threadIdx.x == 0) out[row] = x;
+}
+
+cudaError_t reduce_partials(const double* partial, int n, double* out, cudaStream_t st) {
+  k_reduce_rows<<<1, 32, 0, st>>>(partial, n, 1, out);
+  return cudaGetLastError();
+}
+
+int vec_grid(int sms) { return sms * 4; }
+
+struct VecPtrs {
+  const double* v[32];
+};
+
+// h_i = <V_i, w>, i < nv   (K6 pass 1)
+template <int NV>
+__global__ void __launch_bounds__(256) k_multi_dot(VecPtrs V, const double* __restrict__ w, long len2,
+                                                   double* partial) {
+  double acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+  const double2* w2 = reinterpret_cast<const double2*>(w);
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < len2; e += (long)gridDim.x * blockDim.x) {
+    double2 x = __ldcs(w2 + e);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      double2 v = __ldcs(reinterpret_cast<const double2*>(V.v[i]) + e);
+      acc[i] = fma(v.x, x.x, fma(v.y, x.y, acc[i]));
+    }
+  }
+  block_sum_store<NV>(acc, partial, gridDim.x);
+}
+
+// w <- w - sum_i coef_i V_i ; then (WANT == 1) h2_i = <V_i, w> or (WANT == 2) ||w||^2
+template <int NV, int WANT>
+__global__ void __launch_bounds__(256) k_axpy_dot(VecPtrs V, const double* __restrict__ coef, double* w, long len2,
+                                                  double* partial) {
+  constexpr int NO = WANT == 1 ? NV : 1;
+  double acc[NO];
+#pragma unroll
+  for (int i = 0; i < NO; ++i) acc[i] = 0.0;
+  double cf[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) cf[i] = coef[i];
+  double2* w2 = reinterpret_cast<double2*>(w);
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < len2; e += (long)gridDim.x * blockDim.x) {
+    double2 x = w2[e];
+    double2 vv[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      vv[i] = __ldcs(reinterpret_cast<const double2*>(V.v[i]) + e);
+      x.x = fma(-cf[i], vv[i].x, x.x);
+      x.y = fma(-cf[i], vv[i].y, x.y);
+    }
+    w2[e] = x;
+    if constexpr (WANT == 1) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) acc[i] = fma(vv[i].x, x.x, fma(vv[i].y, x.y, acc[i]));
+    } else if constexpr (WANT == 2) {
+      acc[0] = fma(x.x, x.x, fma(x.y, x.y, acc[0]));
+    }
+  }
+  if constexpr (WANT > 0) block_sum_store<NO>(acc, partial, gridDim.x);
+}
+
+// x <- x + sum_i coef_i V_i   (K7)
+template <int NV>
+__global__ void __launch_bounds__(256) k_lincomb(VecPtrs V, const double* __restrict__ coef, double* x, long len2) {
+  double cf[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) cf[i] = coef[i];
+  double2* x2 = reinterpret_cast<double2*>(x);
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < len2; e += (long)gridDim.x * blockDim.x) {
+    double2 a = x2[e];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      double2 v = __ldcs(reinterpret_cast<const double2*>(V.v[i]) + e);
+      a.x = fma(cf[i], v.x, a.x);
+      a.y = fma(cf[i], v.y, a.y);
+    }
+    x2[e] = a;
+  }
+}
+
+__global__ void k_scale_copy(const double* __restrict__ x, double s, double* y, long len2) {
+  const double2* x2 = reinterpret_cast<const double2*>(x);
+  double2* y2 = reinterpret_cast<double2*>(y);
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < len2; e += (long)gridDim.x * blockDim.x) {
+    double2 a = __ldcs(x2 + e);
+    y2[e] = make_double2(s * a.x, s * a.y);
+  }
+}
+
+#define NV_SWITCH(nv, EXPR)                                                           \
+  switch (nv) {                                                                       \
+    case 1: { constexpr int NVc = 1; EXPR; } break;                                   \
+    case 2: { constexpr int NVc = 2; EXPR; } break;                                   \
+    case 3: { constexpr int NVc = 3; EXPR; } break;                                   \
+    case 4: { constexpr int NVc = 4; EXPR; } break;                                   \
+    case 5: { constexpr int NVc = 5; EXPR; } break;                                   \
+    case 6: { constexpr int NVc = 6; EXPR; } break;                                   \
+    case 7: { constexpr int NVc = 7; EXPR; } break;                                   \
+    case 8: { constexpr int NVc = 8; EXPR; } break;                                   \
+    default: return cudaErrorInvalidValue;                                            \
+  }
+
+static VecPtrs pack(const double* const* V, int nv) {
+  VecPtrs p{};
+  for (int i = 0; i < nv && i < 32; ++i) p.v[i] = V[i];
+  return p;
+}
+
+// For nv > 8 the vectors are processed in groups of up to 8 (one extra pass over w per
+// group); restart <= 8 keeps every CGS2 sweep a single pass.
+cudaError_t multi_dot(const double* const* V, int nv, const double* w, long len, double* partial, int grid,
+                      double* out, cudaStream_t st) {
+  const long len2 = len / 2;
+  for (int g0 = 0; g0 < nv; g0 += 8) {
+    int ng = nv - g0 < 8 ? nv - g0 : 8;
+    VecPtrs p = pack(V + g0, ng);
+    NV_SWITCH(ng, (k_multi_dot<NVc><<<grid, 256, 0, st>>>(p, w, len2, partial)));
+    k_reduce_rows<<<ng, 32, 0, st>>>(partial, grid, ng, out + g0);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t multi_axpy_dot(const double* const* V, int nv, const double* coef_dev, double* w, long len,
+                           double* partial, int grid, double* out, int want_dot, cudaStream_t st) {
+  const long len2 = len / 2;
+  for (int g0 = 0; g0 < nv; g0 += 8) {
+    int ng = nv - g0 < 8 ? nv - g0 : 8;
+    VecPtrs p = pack(V + g0, ng);
+    const bool last = g0 + ng >= nv;
+    if (last && want_dot == 2) {
+      NV_SWITCH(ng, (k_axpy_dot<NVc, 2><<<grid, 256, 0, st>>>(p, coef_dev + g0, w, len2, partial)));
+      k_reduce_rows<<<1, 32, 0, st>>>(partial, grid, 1, out);
+    } else if (last && want_dot == 1 && nv <= 8) {
+      NV_SWITCH(ng, (k_axpy_dot<NVc, 1><<<grid, 256, 0, st>>>(p, coef_dev + g0, w, len2, partial)));
+      k_reduce_rows<<<ng, 32, 0, st>>>(partial, grid, ng, out);
+    } else {
+      NV_SWITCH(ng, (k_axpy_dot<NVc, 0><<<grid, 256, 0, st>>>(p, coef_dev + g0, w, len2, partial)));
+    }
+  }
+  if (want_dot == 1 && nv > 8) return multi_dot(V, nv, w, len, partial, grid, out, st);
+  return cudaGetLastError();
+}
+
+cudaError_t lincomb_add(const double* const* V, int nv, const double* coef_dev, double* x, long len,
+                        cudaStream_t st) {
+  const long len2 = len / 2;
+  for (int g0 = 0; g0 < nv; g0 += 8) {
+    int ng = nv - g0 < 8 ? nv - g0 : 8;
+    VecPtrs p = pack(V + g0, ng);
+    NV_SWITCH(ng, (k_lincomb<NVc><<<vec_grid(148), 256, 0, st>>>(p, coef_dev + g0, x, len2)));
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t scale_copy(const double* x, double s, double* y, long len, cudaStream_t st) {
+  k_scale_copy<<<1184, 256, 0, st>>>(x, s, y, len / 2);
+  return cudaGetLastError();
+}
+
+}  // namespace expd

@@ -1,0 +1,286 @@
+"""Thin ctypes binding of libexpd.so (C-ABI: include/expd.h).
+
+Argument marshalling only: every step of the Exp-ParaDiag path runs in the library's
+CUDA kernels.  torch supplies device memory (the caller-owned workspace and vectors) and
+the CUDA stream.  There is no CPU fallback: if the extension is missing or no CUDA
+device is visible, constructing a Plan raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libexpd.so")
+
+EXPD_OK = 0
+STATUS = {
+    0: "EXPD_OK",
+    1: "EXPD_ERR_INVALID_ARG",
+    2: "EXPD_ERR_UNSUPPORTED",
+    3: "EXPD_ERR_CUDA",
+    4: "EXPD_ERR_NCCL",
+    5: "EXPD_ERR_OOM",
+    6: "EXPD_ERR_BREAKDOWN",
+    7: "EXPD_ERR_NOT_CONVERGED",
+}
+
+# every symbol include/expd.h declares (checked by tests/test_abi.py)
+EXPORTS = [
+    "expd_plan_create",
+    "expd_plan_workspace_bytes",
+    "expd_plan_set_workspace",
+    "expd_plan_destroy",
+    "expd_plan_last_error",
+    "expd_residual",
+    "expd_precond_apply",
+    "expd_fixed_point_solve",
+    "expd_gmres_solve",
+    "expd_load_state",
+    "expd_sweep",
+    "expd_sweep_norm2",
+    "expd_store_state",
+    "expd_sweep_kernel_launches",
+    "expd_dst",
+]
+
+
+class ExpdError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class _Problem(C.Structure):
+    _fields_ = [
+        ("dim", C.c_int),
+        ("n", C.c_int),
+        ("a", C.c_double),
+        ("c", C.c_double),
+        ("dt", C.c_double),
+        ("nt", C.c_int),
+        ("alpha", C.c_double),
+        ("scheme", C.c_int),
+        ("npoly", C.c_int),
+        ("q", C.c_double * 8),
+    ]
+
+
+class _Dist(C.Structure):
+    _fields_ = [("rank", C.c_int), ("nranks", C.c_int), ("nccl_comm", C.c_void_p)]
+
+
+class _Report(C.Structure):
+    _fields_ = [
+        ("iterations", C.c_int),
+        ("sweeps", C.c_int),
+        ("converged", C.c_int),
+        ("hist_len", C.c_int),
+        ("rel_residual", C.c_double),
+        ("seconds", C.c_double),
+        ("hist", C.POINTER(C.c_double)),
+    ]
+
+
+_lib = None
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libexpd.so (raises if it was not built: run paper_2603_04350_b200.build)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(path):
+        raise RuntimeError(f"{path} missing: build it with `python -m paper_2603_04350_b200.build`")
+    lib = C.CDLL(path)
+    vp, dp, sz = C.c_void_p, C.POINTER(C.c_double), C.c_size_t
+    sig = {
+        "expd_plan_create": (C.c_int, [C.POINTER(_Problem), C.POINTER(_Dist), C.c_int, vp, C.POINTER(vp)]),
+        "expd_plan_workspace_bytes": (C.c_int, [vp, C.c_int, C.POINTER(sz)]),
+        "expd_plan_set_workspace": (C.c_int, [vp, vp, sz]),
+        "expd_plan_destroy": (None, [vp]),
+        "expd_plan_last_error": (C.c_char_p, [vp]),
+        "expd_residual": (C.c_int, [vp, vp, vp, vp, dp]),
+        "expd_precond_apply": (C.c_int, [vp, vp, vp]),
+        "expd_fixed_point_solve": (C.c_int, [vp, vp, vp, C.c_double, C.c_int, C.POINTER(_Report)]),
+        "expd_gmres_solve": (C.c_int, [vp, vp, vp, C.c_double, C.c_int, C.c_int, C.POINTER(_Report)]),
+        "expd_load_state": (C.c_int, [vp, vp, vp]),
+        "expd_sweep": (C.c_int, [vp]),
+        "expd_sweep_norm2": (C.c_int, [vp, dp]),
+        "expd_store_state": (C.c_int, [vp, vp]),
+        "expd_sweep_kernel_launches": (C.c_int, [vp]),
+        "expd_dst": (C.c_int, [vp, vp, vp, C.c_long]),
+    }
+    for name, (res, args) in sig.items():
+        f = getattr(lib, name)
+        f.restype, f.argtypes = res, args
+    _lib = lib
+    return lib
+
+
+@dataclass
+class Problem:
+    """u_t = (a Delta - c) u + N(u) on (0,1)^dim, Dirichlet, n points/axis, nt steps of dt
+    (PAPER.md:53-61, :87-98); N(u) = sum_p q[p] u^p; scheme 0 = exp. Euler / ETD1, 1 = ETD2."""
+
+    dim: int
+    n: int
+    a: float
+    c: float
+    dt: float
+    nt: int
+    alpha: float
+    scheme: int = 0
+    q: tuple = field(default_factory=tuple)
+
+    @classmethod
+    def from_config(cls, cfg) -> "Problem":
+        return cls(cfg.dim, cfg.n, cfg.a, cfg.c, cfg.T / cfg.nt, cfg.nt, cfg.alpha, cfg.scheme, tuple(cfg.q))
+
+    @property
+    def N(self) -> int:
+        return self.n ** self.dim
+
+    @property
+    def shape(self) -> tuple:
+        return (self.n,) * self.dim
+
+    def _c(self) -> _Problem:
+        p = _Problem()
+        p.dim, p.n, p.a, p.c, p.dt, p.nt, p.alpha = self.dim, self.n, self.a, self.c, self.dt, self.nt, self.alpha
+        p.scheme, p.npoly = self.scheme, len(self.q)
+        for i, v in enumerate(self.q):
+            p.q[i] = float(v)
+        return p
+
+
+def _ptr(t: torch.Tensor | None):
+    if t is None:
+        return None
+    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
+        raise ValueError("expected a contiguous float64 CUDA tensor")
+    return C.c_void_p(t.data_ptr())
+
+
+class Plan:
+    """An expd_plan plus its torch-allocated workspace on one device."""
+
+    def __init__(self, problem: Problem, device: int | None = None, krylov_vectors: int = 0, stream=None):
+        if not torch.cuda.is_available():
+            raise RuntimeError("expd requires a CUDA device (no CPU fallback)")
+        self.lib = load_library()
+        self.problem = problem
+        self.device = torch.cuda.current_device() if device is None else device
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        self._p = problem._c()
+        dist = _Dist(0, 1, None)
+        handle = C.c_void_p()
+        st = self.lib.expd_plan_create(C.byref(self._p), C.byref(dist), self.device,
+                                       C.c_void_p(self.stream.cuda_stream), C.byref(handle))
+        if st != EXPD_OK:
+            raise ExpdError(st, "expd_plan_create")
+        self.handle = handle
+        nbytes = C.c_size_t()
+        self._check(self.lib.expd_plan_workspace_bytes(self.handle, krylov_vectors, C.byref(nbytes)))
+        self.workspace = torch.empty(nbytes.value + 256, dtype=torch.uint8, device=f"cuda:{self.device}")
+        base = self.workspace.data_ptr()
+        aligned = (base + 255) // 256 * 256
+        self._check(self.lib.expd_plan_set_workspace(self.handle, C.c_void_p(aligned), nbytes.value))
+
+    def _check(self, st: int):
+        if st != EXPD_OK:
+            msg = self.lib.expd_plan_last_error(self.handle).decode() if getattr(self, "handle", None) else ""
+            raise ExpdError(st, msg)
+
+    def close(self):
+        if getattr(self, "handle", None):
+            self.lib.expd_plan_destroy(self.handle)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def _vec(self):
+        return torch.empty((self.problem.nt,) + self.problem.shape, dtype=torch.float64,
+                           device=f"cuda:{self.device}")
+
+    # ---- primitives ------------------------------------------------------------------
+    def residual(self, u0: torch.Tensor, U: torch.Tensor, R: torch.Tensor | None = None, norm: bool = False):
+        R = self._vec() if R is None else R
+        rn = C.c_double()
+        self._check(self.lib.expd_residual(self.handle, _ptr(u0), _ptr(U), _ptr(R),
+                                           C.pointer(rn) if norm else None))
+        return (R, rn.value) if norm else R
+
+    def precond_apply(self, R: torch.Tensor, S: torch.Tensor | None = None):
+        S = self._vec() if S is None else S
+        self._check(self.lib.expd_precond_apply(self.handle, _ptr(R), _ptr(S)))
+        return S
+
+    # ---- solvers ---------------------------------------------------------------------
+    def _report(self, maxit):
+        hist = (C.c_double * (maxit + 2))()
+        r = _Report()
+        r.hist = C.cast(hist, C.POINTER(C.c_double))
+        return r, hist
+
+    @staticmethod
+    def _rdict(r, hist, status):
+        return {
+            "status": STATUS.get(status, status),
+            "iterations": r.iterations,
+            "sweeps": r.sweeps,
+            "converged": bool(r.converged),
+            "rel_residual": r.rel_residual,
+            "seconds": r.seconds,
+            "hist": [hist[i] for i in range(r.hist_len)],
+        }
+
+    def fixed_point_solve(self, u0, U=None, tol=1e-12, maxit=100):
+        U = torch.zeros((self.problem.nt,) + self.problem.shape, dtype=torch.float64,
+                        device=f"cuda:{self.device}") if U is None else U
+        r, hist = self._report(maxit)
+        st = self.lib.expd_fixed_point_solve(self.handle, _ptr(u0), _ptr(U), tol, maxit, C.byref(r))
+        if st not in (EXPD_OK, 7):
+            self._check(st)
+        return U, self._rdict(r, hist, st)
+
+    def gmres_solve(self, u0, U=None, tol=1e-12, restart=20, maxit=100):
+        U = torch.zeros((self.problem.nt,) + self.problem.shape, dtype=torch.float64,
+                        device=f"cuda:{self.device}") if U is None else U
+        r, hist = self._report(maxit)
+        st = self.lib.expd_gmres_solve(self.handle, _ptr(u0), _ptr(U), tol, restart, maxit, C.byref(r))
+        if st not in (EXPD_OK, 7):
+            self._check(st)
+        return U, self._rdict(r, hist, st)
+
+    # ---- spectral-state sweep (benchmark / fine-grained driving) ----------------------
+    def load_state(self, u0, U=None):
+        self._check(self.lib.expd_load_state(self.handle, _ptr(u0), _ptr(U)))
+
+    def sweep(self):
+        self._check(self.lib.expd_sweep(self.handle))
+
+    def sweep_norm2(self) -> float:
+        v = C.c_double()
+        self._check(self.lib.expd_sweep_norm2(self.handle, C.byref(v)))
+        return v.value
+
+    def store_state(self, U):
+        self._check(self.lib.expd_store_state(self.handle, _ptr(U)))
+
+    def dst(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """V x for a stack of physical slices [..., n, ..., n]."""
+        out = torch.empty_like(x) if out is None else out
+        ns = x.numel() // self.problem.N
+        self._check(self.lib.expd_dst(self.handle, _ptr(x), _ptr(out), ns))
+        return out
+
+    def sweep_kernel_launches(self) -> int:
+        return int(self.lib.expd_sweep_kernel_launches(self.handle))

@@ -1,0 +1,175 @@
+"""GPU parity: the CUDA path (through the C-ABI, libexpd.so) against the CPU oracle.
+
+Tolerances (BASELINE.json:5 north_star):
+  * a single preconditioner apply or residual: relative max error <= 1e-11
+    (max |gpu - oracle| / max |oracle|, reading R9);
+  * solves: identical iteration counts, final solution relative max error <= 1e-9.
+Every input is seeded (synth/); every expected value is computed by oracle/ on the same
+bytes in the same process.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2603_04350_b200 import ExpdError, Plan, Problem  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def T(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(DEV)
+
+
+def H(t):
+    return t.detach().cpu().numpy()
+
+
+def relmax(got, want):
+    return float(np.abs(got - want).max() / max(np.abs(want).max(), 1e-300))
+
+
+def cfg_small(name, n, nt):
+    return synth.CONFIGS[name].scaled(n, nt)
+
+
+# ------------------------------------------------------------------------------------------
+# the DST (K2/K3)
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("dim,n", [(1, 3), (1, 7), (1, 63), (1, 4095), (2, 7), (2, 15), (2, 63), (2, 255),
+                                   (3, 7), (3, 15)])
+def test_dst_matches_oracle(orc, dim, n):
+    cfg = synth.Config("t", dim, n, 1.0, 1.0, 1.0, 4, 1e-2)
+    plan = Plan(Problem.from_config(cfg))
+    x = np.random.default_rng(dim * 1000 + n).standard_normal((3,) + cfg.shape)
+    got = H(plan.dst(T(x)))
+    s = orc.spec(cfg)
+    for i in range(3):
+        assert relmax(got[i], orc.dst(s, x[i])) < 1e-13
+
+
+@pytest.mark.parametrize("dim,n", [(2, 2047), (3, 255)])
+def test_dst_full_size_sampled(orc, dim, n):
+    cfg = synth.Config("t", dim, n, 1.0, 1.0, 1.0, 4, 1e-2)
+    plan = Plan(Problem.from_config(cfg))
+    x = np.random.default_rng(5).standard_normal(cfg.shape)
+    got = H(plan.dst(T(x))).reshape(-1)
+    idx = np.random.default_rng(6).integers(0, cfg.N, 12)
+    want = orc.dst_sample(orc.spec(cfg), x, idx)
+    assert relmax(got[idx], want) < 1e-12 * np.sqrt(cfg.N) / np.abs(want).max() + 1e-12
+
+
+# ------------------------------------------------------------------------------------------
+# preconditioner apply (Steps (a)-(c)) and residual
+# ------------------------------------------------------------------------------------------
+PRECOND_CASES = [
+    ("c1", None, None),
+    ("c2", 31, 64),
+    ("c3", 31, 128),
+    ("c4", 7, 64),
+    ("c5", 31, 256),
+    ("c2", 7, 4),
+    ("c2", 7, 8),
+    ("c2", 15, 16),
+    ("c2", 3, 32),
+]
+
+
+@pytest.mark.parametrize("name,n,nt", PRECOND_CASES)
+def test_precond_apply_parity(orc, name, n, nt):
+    cfg = synth.CONFIGS[name] if n is None else cfg_small(name, n, nt)
+    plan = Plan(Problem.from_config(cfg))
+    R = synth.random_spacetime(cfg)
+    S = H(plan.precond_apply(T(R)))
+    want, leak = orc.precond(orc.spec(cfg), R)
+    assert leak < 1e-8
+    assert relmax(S, want) < 1e-11
+
+
+@pytest.mark.parametrize("name,n,nt", [("c1", None, None), ("c2", 31, 64), ("c3", 31, 128), ("c4", 7, 64),
+                                       ("c5", 31, 256), ("c5", 7, 4)])
+def test_residual_parity(orc, name, n, nt):
+    cfg = synth.CONFIGS[name] if n is None else cfg_small(name, n, nt)
+    plan = Plan(Problem.from_config(cfg))
+    u0 = synth.initial_condition(cfg)
+    U = synth.random_spacetime(cfg, scale=0.5)
+    R, rn2 = plan.residual(T(u0), T(U), norm=True)
+    want, wn2 = orc.residual(orc.spec(cfg), u0, U)
+    assert relmax(H(R), want) < 1e-11
+    assert abs(rn2 - wn2) < 1e-11 * wn2
+
+
+def test_precond_zero_and_alias(orc):
+    cfg = cfg_small("c2", 15, 32)
+    plan = Plan(Problem.from_config(cfg))
+    Z = torch.zeros((cfg.nt,) + cfg.shape, dtype=torch.float64, device=DEV)
+    assert float(plan.precond_apply(Z).abs().max()) == 0.0
+    R = synth.random_spacetime(cfg)
+    Rt = T(R)
+    plan.precond_apply(Rt, Rt)  # S may alias R
+    want, _ = orc.precond(orc.spec(cfg), R)
+    assert relmax(H(Rt), want) < 1e-11
+
+
+# ------------------------------------------------------------------------------------------
+# solvers
+# ------------------------------------------------------------------------------------------
+SOLVE_CASES = [("c1", None, None), ("c2", 63, 64), ("c3", 63, 128), ("c5", 63, 256), ("c4", 15, 64)]
+
+
+@pytest.mark.parametrize("name,n,nt", SOLVE_CASES)
+def test_fixed_point_parity(orc, name, n, nt):
+    cfg = synth.CONFIGS[name] if n is None else cfg_small(name, n, nt)
+    plan = Plan(Problem.from_config(cfg))
+    u0 = synth.initial_condition(cfg)
+    U, rep = plan.fixed_point_solve(T(u0), tol=cfg.tol, maxit=50)
+    Uo, st, its, hist = orc.fixed_point(orc.spec(cfg), u0, tol=cfg.tol, maxit=50)
+    assert st == 0 and rep["converged"]
+    assert rep["iterations"] == its
+    assert relmax(H(U), Uo) < 1e-9
+    h = np.array(rep["hist"])
+    big = hist > 1e-9  # above the roundoff floor the histories agree closely
+    assert np.allclose(h[big], hist[big], rtol=1e-6)
+
+
+@pytest.mark.parametrize("name,n,nt", [("c1", None, None), ("c2", 63, 64), ("c4", 15, 64)])
+def test_gmres_parity(orc, name, n, nt):
+    cfg = synth.CONFIGS[name] if n is None else cfg_small(name, n, nt)
+    plan = Plan(Problem.from_config(cfg), krylov_vectors=21)
+    u0 = synth.initial_condition(cfg)
+    U, rep = plan.gmres_solve(T(u0), tol=cfg.tol, restart=20, maxit=50)
+    Uo, st, its, hist = orc.gmres(orc.spec(cfg), u0, tol=cfg.tol, restart=20, maxit=50)
+    assert st == 0 and rep["converged"]
+    assert rep["iterations"] == its
+    assert relmax(H(U), Uo) < 1e-9
+
+
+def test_gmres_small_restart_matches_oracle(orc):
+    cfg = synth.Config("g", 1, 15, 0.05, 0.0, 0.5, 16, 0.2)
+    plan = Plan(Problem.from_config(cfg), krylov_vectors=3)
+    u0 = np.random.default_rng(3).standard_normal(15)
+    U, rep = plan.gmres_solve(T(u0), tol=1e-12, restart=3, maxit=60)
+    Uo, st, its, hist = orc.gmres(orc.spec(cfg), u0, tol=1e-12, restart=3, maxit=60)
+    assert rep["iterations"] == its
+    assert relmax(H(U), Uo) < 1e-9
+
+
+# ------------------------------------------------------------------------------------------
+# argument validation (synchronous, before any launch)
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("kw,status", [({"alpha": 0.0}, 1), ({"nt": 12}, 1), ({"n": 10}, 1), ({"nt": 512}, 2),
+                                       ({"a": -1.0}, 1), ({"dim": 4}, 1)])
+def test_invalid_problems(kw, status):
+    base = dict(dim=2, n=15, a=1.0, c=1.0, dt=0.1, nt=16, alpha=1e-2)
+    base.update(kw)
+    with pytest.raises(ExpdError) as ei:
+        Plan(Problem(**base))
+    assert ei.value.status == status
