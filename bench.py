@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""Benchmark of the Exp-ParaDiag hot path (BASELINE.json metric: space-time
+DOF-iterations/s per sweep; achieved HBM GB/s vs B200 peak).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5] [--impl reference]
+
+A step is one Exp-ParaDiag sweep of the whole hot path on the resident c5 workload
+(BASELINE.json:11; the largest config, it fits one GPU): stage 3 (N-hat = V N(V u-hat) for
+every slice), then the fused residual + ||r||^2 + alpha-circulant preconditioner + update
+(stages 1, 2), the norm reduction and the device->host read of the residual norm that the
+convergence test needs.  K steps are timed with CUDA events on the plan's stream between
+barrier + synchronize, max over ranks.  Inputs (8.6 GB per space-time array) exceed the
+126 MB L2, so no flush is needed.
+
+--impl reference times the CPU oracle (oracle/, naive long-double sums) on host cores, on
+a bounded sample of the same workload.
+
+N > 1 (torchrun): this round's library has no multi-rank path yet; every
+rank solves its own independent c5 problem (weak scaling over independent problems, no
+collective on the data path).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+BYTES_PER_DOF = {  # algorithmic fp64 bytes per space-time dof
+    "k1_linear": 16,      # read U-hat, write U-hat
+    "k1_nonlinear": 24,   # read U-hat, read N-hat, write U-hat
+    "stage3": 16,         # read U-hat slice, write N-hat slice
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c5")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            parts = [x.strip() for x in l.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() in ("active", "1", "yes"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------
+# CPU oracle baseline (oracle/ as it stands; rank 0, N = 1 only)
+# ------------------------------------------------------------------------------------------
+def oracle_sample_step(cfg, u_slice):
+    """One bounded sample of the oracle's sweep: A u on one full-size slice (2 naive DSTs,
+    O(n) sums per output, long double).  The oracle's sweep is 10 such DST applications per
+    time slice (residual: A and the two Phi products = 6; Step (b): DST and IDST of the real
+    and imaginary parts = 4) plus O(Nt) DFT sums per point (< 3 % of its work at c5), so one
+    sample is 1/(5 Nt) of a sweep: N_st / (5 Nt) equivalent DOF-iterations."""
+    import oracle
+
+    oracle.apply_A(oracle.spec(cfg), u_slice)
+    return cfg.nst / (5.0 * cfg.nt)
+
+
+def cpu_baseline(cfg, nsamples=1):
+    import numpy as np
+
+    import oracle
+
+    oracle.build()
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    u = np.random.default_rng(0).standard_normal(cfg.shape)
+    t0 = time.perf_counter()
+    dofs = 0.0
+    for _ in range(nsamples):
+        dofs += oracle_sample_step(cfg, u)
+    dt = time.perf_counter() - t0
+    return {"value": dofs / dt, "unit": "DOF-iter/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
+            "kind": "oracle",
+            "sample": f"{nsamples} x oracle A u on one {cfg.name} slice ({cfg.n}^{cfg.dim}, 2 naive long-double "
+                      f"DSTs) = 1/(5 Nt) of an oracle sweep each; {dt:.1f} s"}
+
+
+def run_reference(args):
+    import synth
+
+    ws, rank, local = dist_env()
+    cfg = synth.CONFIGS[args.config]
+    if rank != 0:
+        return 0
+    import numpy as np
+
+    import oracle
+
+    oracle.build()
+    cores = os.cpu_count() or 1
+    os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    u = np.random.default_rng(0).standard_normal(cfg.shape)
+    for _ in range(args.warmup):
+        oracle_sample_step(cfg, u)
+    t0 = time.perf_counter()
+    dofs = 0.0
+    for _ in range(args.steps):
+        dofs += oracle_sample_step(cfg, u)
+    dt = time.perf_counter() - t0
+    value = dofs / dt
+    line = {
+        "impl": "reference", "metric": "space-time DOF-iterations/s per Exp-ParaDiag sweep", "value": value,
+        "unit": "DOF-iter/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * dt / max(args.steps, 1), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f80 (long double accumulation)", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.dim}D n={cfg.n} Nt={cfg.nt} ETD2 Picard sweep (BASELINE.json:11)"},
+        "cpu_baseline": {"value": value, "unit": "DOF-iter/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
+                         "kind": "oracle",
+                         "sample": f"each step: oracle A u on one {cfg.name} slice = N_st/(5 Nt) DOF-iterations"},
+        "e2e": {"value": value, "unit": "DOF-iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------
+# the GPU path
+# ------------------------------------------------------------------------------------------
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2603_04350_b200 import Plan, Problem
+    from paper_2603_04350_b200 import build as pbuild
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if rank == 0:
+        pbuild.build()
+    if ws > 1:
+        dist.barrier()
+
+    cfg = synth.CONFIGS[args.config]
+    if ws > 1:  # independent problem per rank (weak scaling)
+        cfg = synth.Config(**{**cfg.__dict__, "seed": cfg.seed + 1000 * rank})
+    prob = Problem.from_config(cfg)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    plan = Plan(prob, device=local, stream=stream)
+    u0 = torch.from_numpy(synth.initial_condition(cfg)).to(dev)
+    plan.load_state(u0, None)
+    plan.set_profiling(True)
+    nl = len(cfg.q) > 0
+
+    def step():
+        plan.sweep()
+        return plan.sweep_norm2()  # convergence-test scalar (device -> host, syncs)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    ev0.record(stream)
+    ms_nl, ms_k1, norms = [], [], []
+    for _ in range(args.steps):
+        norms.append(step())
+        a, b = plan.sweep_stage_ms()
+        ms_nl.append(a)
+        ms_k1.append(b)
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    ck = clocks.stop()
+    ms = ev0.elapsed_time(ev1)
+    if ws > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = cfg.nst * args.steps * ws / (ms * 1e-3)
+
+    pk = peaks()
+    hbm_peak = pk["hbm_gbs"] if pk else 6650.0
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if pk else "fallback (B200_PROFILING.md)"
+    k1_bytes = (BYTES_PER_DOF["k1_nonlinear"] if nl else BYTES_PER_DOF["k1_linear"]) * cfg.nst
+    s3_bytes = BYTES_PER_DOF["stage3"] * cfg.N * (cfg.nt - 1) if nl else 0
+    k1_ms = statistics.mean(ms_k1)
+    s3_ms = statistics.mean(ms_nl) if nl else 0.0
+    k1_gbs = k1_bytes / (k1_ms * 1e-3) / 1e9
+    traffic = None
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        traffic = prof.get(f"{cfg.name}:k1", None)
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "kernel": "k_time_fused (K1: residual+norm+preconditioner+update)",
+                "achieved": k1_gbs, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
+                "frac": k1_gbs / hbm_peak, "traffic": traffic,
+                "algorithmic_bytes_per_launch": k1_bytes, "launch_ms": k1_ms}
+    kernels = {"k1_ms": k1_ms, "k1_gbs": k1_gbs, "stage3_ms": s3_ms,
+               "stage3_gbs": (s3_bytes / (s3_ms * 1e-3) / 1e9) if s3_ms > 0 else None,
+               "sweep_ms": ms_step,
+               "sweep_algorithmic_gbs": (k1_bytes + s3_bytes) / (ms_step * 1e-3) / 1e9,
+               "sweep_frac_of_peak": (k1_bytes + s3_bytes) / (ms_step * 1e-3) / 1e9 / hbm_peak}
+
+    # e2e: full solve through the C-ABI with host buffers (H2D u0, solve, final IDST, D2H U)
+    e2e = None
+    if not args.no_e2e:
+        u0_h = torch.from_numpy(synth.initial_condition(cfg)).pin_memory()
+        U_h = torch.empty((cfg.nt,) + cfg.shape, dtype=torch.float64).pin_memory()
+        u0_d = torch.empty_like(u0_h, device=dev)
+        U_d = torch.empty((cfg.nt,) + cfg.shape, dtype=torch.float64, device=dev)
+        plan.set_profiling(False)
+        tot_ms, tot_sweeps = 0.0, 0
+        for i in range(args.e2e_steps + 1):
+            torch.cuda.synchronize(dev)
+            a0 = torch.cuda.Event(enable_timing=True)
+            a1 = torch.cuda.Event(enable_timing=True)
+            a0.record(stream)
+            u0_d.copy_(u0_h, non_blocking=True)
+            U_d.zero_()
+            _, rep = plan.fixed_point_solve(u0_d, U_d, tol=cfg.tol, maxit=100)
+            U_h.copy_(U_d, non_blocking=True)
+            a1.record(stream)
+            torch.cuda.synchronize(dev)
+            if i > 0:  # first solve is warm-up
+                tot_ms += a0.elapsed_time(a1)
+                tot_sweeps += rep["sweeps"]
+        e2e = {"value": cfg.nst * tot_sweeps * ws / (tot_ms * 1e-3), "unit": "DOF-iter/s",
+               "h2d_bytes_per_step": u0_h.numel() * 8, "d2h_bytes_per_step": U_h.numel() * 8,
+               "what": f"full fixed-point solve per step ({rep['sweeps']} sweeps, {rep['iterations']} iterations, "
+                       f"rel residual {rep['rel_residual']:.2e}) incl. setup DSTs, final IDST and host copies"}
+
+    cpu = None
+    if rank == 0 and ws == 1 and not args.no_cpu:
+        try:
+            cpu = cpu_baseline(cfg)
+        except Exception as e:  # pragma: no cover
+            cpu = {"error": str(e)}
+
+    launches = plan.sweep_kernel_launches() * args.steps
+    line = {
+        "metric": "space-time DOF-iterations/s per Exp-ParaDiag sweep", "value": value, "unit": "DOF-iter/s",
+        "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.dim}D n={cfg.n} Nt={cfg.nt} "
+                               f"{'ETD2' if cfg.scheme == 1 else 'exp. Euler'} "
+                               f"{'Picard' if nl else 'fixed-point'} sweep (BASELINE.json:11)",
+                   "n_st": cfg.nst, "alpha": cfg.alpha,
+                   "l2": "inputs 8.6 GB per space-time array >> 126 MB L2 (no flush needed)",
+                   "parallelism": "single GPU" if ws == 1 else f"{ws} independent problems (weak scaling)"},
+        "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+        "gpu_launches": launches, "clocks": ck,
+        "residual_norm_last": float(np.sqrt(norms[-1])) if norms else None,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

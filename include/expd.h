@@ -136,6 +136,12 @@ expd_status expd_store_state(expd_plan* plan, double* U);           /* U = V U-h
    PAPER.md:141; V = V^T = V^{-1}).  in, out: [nslices][n^dim] device; out may alias in.
    Uses the workspace's transform scratch.  Async. */
 expd_status expd_dst(expd_plan* plan, const double* in, double* out, long nslices);
+/* Stage timing of expd_sweep with CUDA events recorded on the plan's stream (inside the
+   sweep's CUDA graph): enable != 0 turns it on.  expd_sweep_stage_ms waits for the last
+   sweep and returns the device time of stage 3 (N-hat of all slices; 0 when linear) and of
+   the fused time-local kernel K1, in milliseconds. */
+expd_status expd_set_profiling(expd_plan* plan, int enable);
+expd_status expd_sweep_stage_ms(expd_plan* plan, double* ms_nonlin, double* ms_time);
 /* Number of kernels one expd_sweep launches (for the benchmark's launch count). */
 int expd_sweep_kernel_launches(const expd_plan* plan);
 

@@ -47,6 +47,10 @@ struct expd_plan {
   // CUDA graph of one sweep (captured on a private stream, launched on `stream`)
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t sweep_exec = nullptr;
+  bool capturing = false;
+  // optional stage timing: ev[0] before stage 3, ev[1] before K1, ev[2] after K1
+  bool prof = false;
+  cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   std::string err;
 };
 
@@ -236,6 +240,8 @@ extern "C" void expd_plan_destroy(expd_plan* p) {
   cudaSetDevice(p->device);
   if (p->sweep_exec) cudaGraphExecDestroy(p->sweep_exec);
   if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
+  for (int i = 0; i < 3; ++i)
+    if (p->ev[i]) cudaEventDestroy(p->ev[i]);
   cudaFree(p->d_lam);
   cudaFree(p->d_twt);
   cudaFree(p->d_g);
@@ -292,16 +298,24 @@ static expd_status load_u0(expd_plan* p, const double* u0) {
 
 // One sweep on the spectral state: stage 3 (nonlinear history of u_1..u_{nt-1}), then the
 // fused residual / norm / preconditioner / update (stages 1, 2), then the norm reduction.
+static cudaError_t record(expd_plan* p, int i, cudaStream_t st) {
+  if (!p->prof) return cudaSuccess;
+  return p->capturing ? cudaEventRecordWithFlags(p->ev[i], st, cudaEventRecordExternal) : cudaEventRecord(p->ev[i], st);
+}
+
 static cudaError_t enqueue_sweep(expd_plan* p, cudaStream_t st) {
-  cudaError_t e;
+  cudaError_t e = record(p, 0, st);
+  if (e != cudaSuccess) return e;
   if (p->nl) {
     e = nonlin_slices(p->g, dst_tables(p), p->Uh, p->Nh + p->g.npad, p->prob.nt - 1, p->prob.npoly, p->prob.q,
                       p->scratch, st);
     if (e != cudaSuccess) return e;
   }
+  if ((e = record(p, 1, st)) != cudaSuccess) return e;
   TimeArgs a = time_args(p, p->Uh, p->Uh, true);
   e = launch_time_fused(a, RM_RESID, OUT_UPDATE, p->nl, p->time_grid, st);
   if (e != cudaSuccess) return e;
+  if ((e = record(p, 2, st)) != cudaSuccess) return e;
   return reduce_partials(p->partial, p->time_grid, p->dscal, st);
 }
 
@@ -314,7 +328,9 @@ static expd_status sweep(expd_plan* p, bool use_graph) {
     cudaGraph_t graph;
     if (!p->cap_stream) CUDA_TRY(p, cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
     CUDA_TRY(p, cudaStreamBeginCapture(p->cap_stream, cudaStreamCaptureModeThreadLocal));
+    p->capturing = true;
     cudaError_t e = enqueue_sweep(p, p->cap_stream);
+    p->capturing = false;
     cudaError_t e2 = cudaStreamEndCapture(p->cap_stream, &graph);
     if (e != cudaSuccess) return fail(p, EXPD_ERR_CUDA, std::string("sweep capture: ") + cudaGetErrorString(e));
     if (e2 != cudaSuccess) return fail(p, EXPD_ERR_CUDA, std::string("end capture: ") + cudaGetErrorString(e2));
@@ -418,6 +434,30 @@ extern "C" expd_status expd_dst(expd_plan* p, const double* in, double* out, lon
                                   sizeof(double) * p->g.n, (size_t)ns * (p->g.N / p->g.n),
                                   cudaMemcpyDeviceToDevice, p->stream));
   }
+  return EXPD_OK;
+}
+
+extern "C" expd_status expd_set_profiling(expd_plan* p, int enable) {
+  expd_status s = ready(p);
+  if (s) return s;
+  for (int i = 0; i < 3; ++i)
+    if (!p->ev[i]) CUDA_TRY(p, cudaEventCreate(&p->ev[i]));
+  if (p->prof != (enable != 0) && p->sweep_exec) {
+    cudaGraphExecDestroy(p->sweep_exec);  // recapture with / without the event nodes
+    p->sweep_exec = nullptr;
+  }
+  p->prof = enable != 0;
+  return EXPD_OK;
+}
+
+extern "C" expd_status expd_sweep_stage_ms(expd_plan* p, double* ms_nonlin, double* ms_time) {
+  if (!p || !p->prof) return fail(p, EXPD_ERR_INVALID_ARG, "profiling not enabled");
+  float a = 0.f, b = 0.f;
+  CUDA_TRY(p, cudaEventSynchronize(p->ev[2]));
+  CUDA_TRY(p, cudaEventElapsedTime(&a, p->ev[0], p->ev[1]));
+  CUDA_TRY(p, cudaEventElapsedTime(&b, p->ev[1], p->ev[2]));
+  if (ms_nonlin) *ms_nonlin = a;
+  if (ms_time) *ms_time = b;
   return EXPD_OK;
 }
 

@@ -45,6 +45,8 @@ EXPORTS = [
     "expd_store_state",
     "expd_sweep_kernel_launches",
     "expd_dst",
+    "expd_set_profiling",
+    "expd_sweep_stage_ms",
 ]
 
 
@@ -113,6 +115,8 @@ def load_library(path: str = LIB_PATH):
         "expd_store_state": (C.c_int, [vp, vp]),
         "expd_sweep_kernel_launches": (C.c_int, [vp]),
         "expd_dst": (C.c_int, [vp, vp, vp, C.c_long]),
+        "expd_set_profiling": (C.c_int, [vp, C.c_int]),
+        "expd_sweep_stage_ms": (C.c_int, [vp, dp, dp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -281,6 +285,15 @@ class Plan:
         ns = x.numel() // self.problem.N
         self._check(self.lib.expd_dst(self.handle, _ptr(x), _ptr(out), ns))
         return out
+
+    def set_profiling(self, enable: bool = True):
+        self._check(self.lib.expd_set_profiling(self.handle, int(enable)))
+
+    def sweep_stage_ms(self):
+        """(stage-3 ms, K1 ms) of the last sweep (device time, CUDA events)."""
+        a, b = C.c_double(), C.c_double()
+        self._check(self.lib.expd_sweep_stage_ms(self.handle, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def sweep_kernel_launches(self) -> int:
         return int(self.lib.expd_sweep_kernel_launches(self.handle))
