@@ -26,14 +26,27 @@ namespace expd {
 
 template <int NT>
 struct TimeCfg;
-// P x Q = NT; S mode pairs per CTA; MINB resident CTAs per SM (register budget)
-template <> struct TimeCfg<4>   { static constexpr int P = 4,  Q = 1,  S = 128, MINB = 3; };
-template <> struct TimeCfg<8>   { static constexpr int P = 8,  Q = 1,  S = 128, MINB = 3; };
-template <> struct TimeCfg<16>  { static constexpr int P = 16, Q = 1,  S = 128, MINB = 3; };
-template <> struct TimeCfg<32>  { static constexpr int P = 8,  Q = 4,  S = 32,  MINB = 3; };
-template <> struct TimeCfg<64>  { static constexpr int P = 8,  Q = 8,  S = 16,  MINB = 3; };
-template <> struct TimeCfg<128> { static constexpr int P = 16, Q = 8,  S = 16,  MINB = 3; };
-template <> struct TimeCfg<256> { static constexpr int P = 16, Q = 16, S = 8,   MINB = 2; };
+// Radix plan of the length-NT time FFT (Stockham stages R_0 .. R_{L-1}); the last stage
+// has a small radix so that a thread can own a frequency set together with its Hermitian
+// partner set; TPS = NT / R_0 threads per mode pair; S = 256 / TPS pairs per CTA.
+template <int NT> struct TimeCfg;
+template <> struct TimeCfg<4>   { static constexpr int L = 1, R0 = 4, R1 = 1, R2 = 1; };
+template <> struct TimeCfg<8>   { static constexpr int L = 1, R0 = 8, R1 = 1, R2 = 1; };
+template <> struct TimeCfg<16>  { static constexpr int L = 2, R0 = 4, R1 = 4, R2 = 1; };
+template <> struct TimeCfg<32>  { static constexpr int L = 2, R0 = 8, R1 = 4, R2 = 1; };
+template <> struct TimeCfg<64>  { static constexpr int L = 3, R0 = 8, R1 = 2, R2 = 4; };
+template <> struct TimeCfg<128> { static constexpr int L = 3, R0 = 8, R1 = 4, R2 = 4; };
+template <> struct TimeCfg<256> { static constexpr int L = 3, R0 = 8, R1 = 8, R2 = 4; };
+template <int NT>
+struct TimeGeo {
+  using C = TimeCfg<NT>;
+  static constexpr int L = C::L, R0 = C::R0;
+  static constexpr int RL = L == 1 ? C::R0 : (L == 2 ? C::R1 : C::R2);  // last forward radix
+  static constexpr int TPS = NT / R0;                                    // threads per pair
+  static constexpr int THREADS = 256;
+  static constexpr int S = THREADS / TPS;                                // pairs per CTA
+  static constexpr int NSL = NT / RL;                                    // Ns of the last stage
+};
 
 __device__ __forceinline__ double2 ld2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
 __device__ __forceinline__ double2 ld2cs(const double* p) {  // streaming: read once
@@ -84,19 +97,67 @@ __device__ __forceinline__ void divide_pair(double2& Zk, double2& Zkp, double2 t
   Zkp = wkp;
 }
 
+// One Stockham stage between shared buffers: job (s, j), inputs x[j + r NT/R], twiddle
+// w^{r (j mod NS) NT/(NS R)} (w = e^{DIR 2 pi i/NT}), DFT-R, outputs y[(j/NS) NS R + j mod NS + r NS].
+template <int NT, int S, int THREADS, int R, int NS, int DIR>
+__device__ __forceinline__ void tstage(const double2* __restrict__ in, double2* __restrict__ out,
+                                       const double2* __restrict__ stw) {
+  constexpr int JOBS = S * (NT / R);
+#pragma unroll
+  for (int J = threadIdx.x; J < JOBS; J += THREADS) {
+    const int s = J % S, j = J / S, k = j % NS;
+    double2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = in[(j + r * (NT / R)) * S + s];
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      const double2 w = stw[(r * k * (NT / (NS * R))) % NT];
+      v[r] = DIR > 0 ? cmul(v[r], w) : cmulc(v[r], w);
+    }
+    DFT<R, DIR>::run(v);
+    const int base = (j / NS) * NS * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) out[(base + r * NS) * S + s] = v[r];
+  }
+}
+
+// Last forward stage (radix RL, NS = NT/RL) of two partner jobs ja, jb (their frequency sets
+// k = j + NS r are Hermitian partners), the pair divide, and the first inverse stage
+// (radix RL, NS = 1: no twiddles) on the same sets.
+template <int NT, int RL>
+__device__ __forceinline__ void pair_divide(double2 (&va)[RL], double2 (&vb)[RL], bool pj0, const double2* stw,
+                                            int ja, int jb, double ba, double bb, double hin) {
+  constexpr int NS = NT / RL;
+  if (!pj0) {
+#pragma unroll
+    for (int r = 0; r < RL; ++r) divide_pair(va[r], vb[RL - 1 - r], stw[ja + NS * r], ba, bb, hin, false);
+  } else {
+    // ja = 0: frequencies NS r, partner NS (RL - r) mod RL; self at r = 0 and RL/2
+    divide_pair(va[0], va[0], stw[0], ba, bb, hin, true);
+#pragma unroll
+    for (int r = 1; r < (RL + 1) / 2; ++r) divide_pair(va[r], va[RL - r], stw[NS * r], ba, bb, hin, false);
+    if constexpr (RL % 2 == 0) divide_pair(va[RL / 2], va[RL / 2], stw[NS * (RL / 2)], ba, bb, hin, true);
+    if (jb != ja) {
+      // jb = NS/2: frequencies NS/2 + NS r, partner index RL-1-r
+#pragma unroll
+      for (int r = 0; r < RL / 2; ++r) divide_pair(vb[r], vb[RL - 1 - r], stw[jb + NS * r], ba, bb, hin, false);
+      if constexpr (RL % 2 == 1) divide_pair(vb[RL / 2], vb[RL / 2], stw[jb + NS * (RL / 2)], ba, bb, hin, true);
+    }
+  }
+}
+
 template <int NT, int RM, int OUTM, int NL>
-__global__ void __launch_bounds__(TimeCfg<NT>::S * TimeCfg<NT>::Q, TimeCfg<NT>::MINB)
-    k_time_fused(const TimeArgs a) {
-  constexpr int P = TimeCfg<NT>::P, Q = TimeCfg<NT>::Q, S = TimeCfg<NT>::S;
-  constexpr int THREADS = S * Q;
-  constexpr int NSTASH = (OUTM == OUT_UPDATE) ? NT * S : 0;
-  static_assert(P * Q == NT, "cfg");
+__global__ void __launch_bounds__(256, 2) k_time_fused(const TimeArgs a) {
+  using G = TimeGeo<NT>;
+  using C = TimeCfg<NT>;
+  constexpr int L = G::L, R0 = G::R0, RL = G::RL, TPS = G::TPS, S = G::S, THREADS = G::THREADS;
+  constexpr int NSL = G::NSL;
   extern __shared__ double2 smem[];
-  double2* buf = smem;                    // [NT][S]   (index (k1*Q + m2)*S + s)
-  double2* stash = smem + NT * S;         // [NT][S]   u_t of the tile (update mode)
-  double2* stw = smem + NT * S + NSTASH;  // [NT]      twiddles
-  double* sg = reinterpret_cast<double*>(stw + NT);  // [NT] gamma
-  double* sgi = sg + NT;                  // [NT] gamma^{-1}
+  double2* buf0 = smem;                      // [NT][S]
+  double2* buf1 = smem + (L > 1 ? NT * S : 0);
+  double2* stw = smem + (L > 1 ? 2 * NT * S : 0);  // [NT] e^{+2 pi i q/NT}
+  double* sg = reinterpret_cast<double*>(stw + NT);  // [NT] alpha^{t/NT}
+  double* sgi = sg + NT;                              // [NT] alpha^{-t/NT}
 
   const int tid = threadIdx.x;
   for (int i = tid; i < NT; i += THREADS) {
@@ -108,28 +169,30 @@ __global__ void __launch_bounds__(TimeCfg<NT>::S * TimeCfg<NT>::Q, TimeCfg<NT>::
 
   const long npad = a.npad;
   const long ntiles = (a.npairs + S - 1) / S;
+  const double hin = a.half_inv_nt;
   double nrm = 0.0;
-  const int s = tid % S;
-  const int m2 = tid / S;
+  const int s = tid % S;   // pair within the tile (fastest: conflict-free shared accesses)
+  const int j = tid / S;   // stage-0 job: times j + r TPS
 
   for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const long pair = tile * S + s;
     const bool valid = pair < a.npairs;
     const long base = 2 * pair;
 
-    // ---------------- phase A: residual, Gamma, DFT-P over m1, twiddle -----------------
-    double2 y[P];
+    // ---- phase A: stage 1 residual (+ ||r||^2), Gamma_alpha, forward stage 0 ----------
+    double2 y[R0];
+    double2 xv[(OUTM == OUT_UPDATE) ? R0 : 1];
     double2 Ej = make_double2(0.0, 0.0), c1 = Ej, c2 = Ej;
     if (valid && RM != RM_INPUT) Ej = ld2(a.E + base);
     if (valid && NL >= 1) c1 = ld2(a.C1 + base);
     if (valid && NL == 2) c2 = ld2(a.C2 + base);
 #pragma unroll
-    for (int m1 = 0; m1 < P; ++m1) {
-      const int t = Q * m1 + m2;
-      double2 cur = make_double2(0.0, 0.0), r;
+    for (int r = 0; r < R0; ++r) {
+      const int t = j + r * TPS;
+      double2 cur = make_double2(0.0, 0.0), rr;
       if (valid) cur = (OUTM == OUT_UPDATE) ? ld2(a.X + (long)t * npad + base) : ld2cs(a.X + (long)t * npad + base);
       if constexpr (RM == RM_INPUT) {
-        r = cur;
+        rr = cur;
       } else {
         double2 prev = make_double2(0.0, 0.0);
         if (valid) {
@@ -137,99 +200,102 @@ __global__ void __launch_bounds__(TimeCfg<NT>::S * TimeCfg<NT>::Q, TimeCfg<NT>::
           else if (RM == RM_RESID) prev = ld2(a.u0h + base);
         }
         if constexpr (RM == RM_RESID) {
-          r = make_double2(fma(Ej.x, prev.x, -cur.x), fma(Ej.y, prev.y, -cur.y));
+          rr = make_double2(fma(Ej.x, prev.x, -cur.x), fma(Ej.y, prev.y, -cur.y));
           if constexpr (NL >= 1) {
-            double2 nm1 = valid ? ld2(a.Nh + (long)t * npad + base) : make_double2(0.0, 0.0);
-            r.x = fma(c1.x, nm1.x, r.x);
-            r.y = fma(c1.y, nm1.y, r.y);
+            double2 nm1 = valid ? ld2cs(a.Nh + (long)t * npad + base) : make_double2(0.0, 0.0);
+            rr.x = fma(c1.x, nm1.x, rr.x);
+            rr.y = fma(c1.y, nm1.y, rr.y);
             if constexpr (NL == 2) {
               double2 nm2 = valid ? ld2(a.Nh + (long)(t > 0 ? t - 1 : 0) * npad + base) : make_double2(0.0, 0.0);
-              r.x = fma(-c2.x, nm2.x, r.x);
-              r.y = fma(-c2.y, nm2.y, r.y);
+              rr.x = fma(-c2.x, nm2.x, rr.x);
+              rr.y = fma(-c2.y, nm2.y, rr.y);
             }
           }
         } else {  // RM_QOP: (Q v)_t = v_t - E v_{t-1}, v_{-1} = 0
-          r = make_double2(fma(-Ej.x, prev.x, cur.x), fma(-Ej.y, prev.y, cur.y));
+          rr = make_double2(fma(-Ej.x, prev.x, cur.x), fma(-Ej.y, prev.y, cur.y));
         }
       }
-      nrm = fma(r.x, r.x, fma(r.y, r.y, nrm));
-      if constexpr (OUTM == OUT_UPDATE) stash[t * S + s] = cur;
-      y[m1] = cscale(r, sg[t]);
+      nrm = fma(rr.x, rr.x, fma(rr.y, rr.y, nrm));
+      if constexpr (OUTM == OUT_UPDATE) xv[r] = cur;
+      y[r] = cscale(rr, sg[t]);
     }
-    DFT<P, +1>::run(y);
-#pragma unroll
-    for (int k1 = 1; k1 < P; ++k1) y[k1] = cmul(y[k1], stw[(k1 * m2) % NT]);
-#pragma unroll
-    for (int k1 = 0; k1 < P; ++k1) buf[(k1 * Q + m2) * S + s] = y[k1];
-    __syncthreads();
+    DFT<R0, +1>::run(y);
 
-    // ---------------- phase B: DFT-Q, Hermitian pair divide, inverse DFT-Q --------------
-    for (int job = tid; job < S * (P / 2); job += THREADS) {
-      const int js = job % S, kp = job / S;
-      const long jpair = tile * S + js;
-      const int k1a = kp == 0 ? 0 : kp;
-      const int k1b = kp == 0 ? P / 2 : P - kp;
-      double2 Za[Q], Zb[Q];
+    if constexpr (L == 1) {
+      // single stage: job 0 owns every frequency; divide its Hermitian pairs in place
+      const double2 Ep = valid ? ld2(a.E + base) : make_double2(0.0, 0.0);
+      const double ba = a.a1 * Ep.x, bb = a.a1 * Ep.y;
+      double2 dummy[R0];
+      pair_divide<NT, R0>(y, dummy, true, stw, 0, 0, ba, bb, hin);
+      DFT<R0, -1>::run(y);
+    } else {
 #pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        Za[q] = buf[(k1a * Q + q) * S + js];
-        Zb[q] = buf[(k1b * Q + q) * S + js];
+      for (int r = 0; r < R0; ++r) buf0[(j * R0 + r) * S + s] = y[r];
+      __syncthreads();
+      const double2* pin = buf0;
+      double2* pout = buf1;
+      if constexpr (L == 3) {  // forward middle stage
+        tstage<NT, S, THREADS, C::R1, R0, +1>(buf0, buf1, stw);
+        __syncthreads();
+        pin = buf1;
+        pout = buf0;
       }
-      DFT<Q, +1>::run(Za);
-      DFT<Q, +1>::run(Zb);
-      double2 Ep = jpair < a.npairs ? ld2(a.E + 2 * jpair) : make_double2(0.0, 0.0);
-      const double ba = a.a1 * Ep.x, bb = a.a1 * Ep.y, hin = a.half_inv_nt;
-      if (kp != 0) {
+      // ---- pair stage: last forward stage, divide, first inverse stage ---------------
+      for (int PJ = tid; PJ < S * (NSL / 2); PJ += THREADS) {
+        const int ps = PJ % S, pj = PJ / S;
+        const int ja = pj, jb = pj == 0 ? NSL / 2 : NSL - pj;
+        const long jpair = tile * S + ps;
+        double2 va[RL], vb[RL];
 #pragma unroll
-        for (int k2 = 0; k2 < Q; ++k2)
-          divide_pair(Za[k2], Zb[Q - 1 - k2], stw[k1a + P * k2], ba, bb, hin, false);
-      } else {
-        // k1 = 0: frequencies P k2, partner P (Q - k2) mod Q; self at k2 = 0 and Q/2
-        divide_pair(Za[0], Za[0], stw[0], ba, bb, hin, true);
+        for (int r = 0; r < RL; ++r) {
+          va[r] = pin[(ja + r * NSL) * S + ps];
+          vb[r] = pin[(jb + r * NSL) * S + ps];
+        }
 #pragma unroll
-        for (int k2 = 1; k2 < (Q + 1) / 2; ++k2) divide_pair(Za[k2], Za[Q - k2], stw[P * k2], ba, bb, hin, false);
-        if constexpr (Q % 2 == 0 && Q >= 2) divide_pair(Za[Q / 2], Za[Q / 2], stw[P * (Q / 2)], ba, bb, hin, true);
-        // k1 = P/2: frequencies P/2 + P k2, partner index Q-1-k2
+        for (int r = 1; r < RL; ++r) {
+          va[r] = cmul(va[r], stw[(r * ja) % NT]);
+          vb[r] = cmul(vb[r], stw[(r * jb) % NT]);
+        }
+        DFT<RL, +1>::run(va);
+        DFT<RL, +1>::run(vb);
+        const double2 Ep = jpair < a.npairs ? ld2(a.E + 2 * jpair) : make_double2(0.0, 0.0);
+        pair_divide<NT, RL>(va, vb, pj == 0, stw, ja, jb, a.a1 * Ep.x, a.a1 * Ep.y, hin);
+        DFT<RL, -1>::run(va);
+        DFT<RL, -1>::run(vb);
 #pragma unroll
-        for (int k2 = 0; k2 < Q / 2; ++k2)
-          divide_pair(Zb[k2], Zb[Q - 1 - k2], stw[P / 2 + P * k2], ba, bb, hin, false);
-        if constexpr (Q % 2 == 1) divide_pair(Zb[Q / 2], Zb[Q / 2], stw[P / 2 + P * (Q / 2)], ba, bb, hin, true);
+        for (int r = 0; r < RL; ++r) {
+          pout[(ja * RL + r) * S + ps] = va[r];
+          pout[(jb * RL + r) * S + ps] = vb[r];
+        }
       }
-      DFT<Q, -1>::run(Za);
-      DFT<Q, -1>::run(Zb);
-#pragma unroll
-      for (int q = 1; q < Q; ++q) {
-        Za[q] = cmulc(Za[q], stw[(k1a * q) % NT]);
-        Zb[q] = cmulc(Zb[q], stw[(k1b * q) % NT]);
+      __syncthreads();
+      if constexpr (L == 3) {  // inverse middle stage (radix R1, NS = RL)
+        tstage<NT, S, THREADS, C::R1, RL, -1>(buf0, buf1, stw);
+        __syncthreads();
       }
-      // each job rewrites exactly the rows it read: no barrier needed inside phase B
+      const double2* cin = (L == 3) ? buf1 : buf1;
+      // ---- phase C input: inverse last stage (radix R0, NS = TPS) ----------------------
 #pragma unroll
-      for (int q = 0; q < Q; ++q) {
-        buf[(k1a * Q + q) * S + js] = Za[q];
-        buf[(k1b * Q + q) * S + js] = Zb[q];
-      }
+      for (int r = 0; r < R0; ++r) y[r] = cin[(j + r * TPS) * S + s];
+#pragma unroll
+      for (int r = 1; r < R0; ++r) y[r] = cmulc(y[r], stw[(r * j) % NT]);
+      DFT<R0, -1>::run(y);
     }
-    __syncthreads();
-
-    // ---------------- phase C: inverse DFT-P over k1, Gamma^{-1}, update ----------------
-#pragma unroll
-    for (int k1 = 0; k1 < P; ++k1) y[k1] = buf[(k1 * Q + m2) * S + s];
-    DFT<P, -1>::run(y);
+    // ---- phase C: Gamma_alpha^{-1}, update, store (times j + r TPS) -------------------
     if (valid) {
 #pragma unroll
-      for (int m1 = 0; m1 < P; ++m1) {
-        const int t = Q * m1 + m2;
-        double2 sv = cscale(y[m1], sgi[t]);
-        if constexpr (OUTM == OUT_UPDATE) sv = cadd(stash[t * S + s], sv);
+      for (int r = 0; r < R0; ++r) {
+        const int t = j + r * TPS;
+        double2 sv = cscale(y[r], sgi[t]);
+        if constexpr (OUTM == OUT_UPDATE) sv = cadd(xv[r], sv);
         st2(a.Y + (long)t * npad + base, sv);
       }
     }
-    __syncthreads();
   }
 
   if (a.partial) {
     // fixed-order block reduction (deterministic for a fixed grid)
-    __shared__ double red[32];
+    __shared__ double red[THREADS / 32];
     for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
     if ((tid & 31) == 0) red[tid >> 5] = nrm;
     __syncthreads();
@@ -243,8 +309,8 @@ __global__ void __launch_bounds__(TimeCfg<NT>::S * TimeCfg<NT>::Q, TimeCfg<NT>::
 
 template <int NT, int OUTM>
 static size_t time_smem_bytes() {
-  const size_t tile = (size_t)NT * TimeCfg<NT>::S;
-  return sizeof(double2) * (tile * (OUTM == OUT_UPDATE ? 2 : 1) + NT) + sizeof(double) * 2 * NT;
+  const size_t tile = TimeGeo<NT>::L > 1 ? (size_t)NT * TimeGeo<NT>::S : 0;
+  return sizeof(double2) * (2 * tile + NT) + sizeof(double) * 2 * NT;
 }
 
 template <int NT, int RM, int OUTM, int NL>
@@ -257,7 +323,7 @@ static cudaError_t launch_t(const TimeArgs& a, int grid, cudaStream_t st) {
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  k<<<grid, TimeCfg<NT>::S * TimeCfg<NT>::Q, sm, st>>>(a);
+  k<<<grid, TimeGeo<NT>::THREADS, sm, st>>>(a);
   return cudaGetLastError();
 }
 
@@ -294,15 +360,18 @@ cudaError_t launch_time_fused(const TimeArgs& a, int rmode, int outmode, int nl,
 // Persistent grid: a fixed multiple of the SM count (deterministic partial order), capped
 // by the number of tiles.
 int time_fused_grid(int nt, long npairs, int sms) {
-  int S = 8;
+  int S = 32;
   switch (nt) {
-    case 4: case 8: case 16: S = 128; break;
-    case 32: S = 32; break;
-    case 64: case 128: S = 16; break;
-    default: S = 8;
+    case 4: S = TimeGeo<4>::S; break;
+    case 8: S = TimeGeo<8>::S; break;
+    case 16: S = TimeGeo<16>::S; break;
+    case 32: S = TimeGeo<32>::S; break;
+    case 64: S = TimeGeo<64>::S; break;
+    case 128: S = TimeGeo<128>::S; break;
+    default: S = TimeGeo<256>::S;
   }
   long ntiles = (npairs + S - 1) / S;
-  long g = (long)sms * 3;
+  long g = (long)sms * 2;
   return (int)(ntiles < g ? (ntiles > 0 ? ntiles : 1) : g);
 }
 
