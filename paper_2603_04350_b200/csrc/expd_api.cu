@@ -48,6 +48,7 @@ struct expd_plan {
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t sweep_exec = nullptr;
   bool capturing = false;
+  bool eager_done = false;  // one eager sweep (kernel attributes) before the first capture
   // optional stage timing: ev[0] before stage 3, ev[1] before K1, ev[2] after K1
   bool prof = false;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
@@ -320,7 +321,8 @@ static cudaError_t enqueue_sweep(expd_plan* p, cudaStream_t st) {
 }
 
 static expd_status sweep(expd_plan* p, bool use_graph) {
-  if (!use_graph) {
+  if (!use_graph || !p->eager_done) {
+    p->eager_done = true;
     CUDA_TRY(p, enqueue_sweep(p, p->stream));
     return EXPD_OK;
   }
@@ -498,7 +500,7 @@ extern "C" expd_status expd_fixed_point_solve(expd_plan* p, const double* u0, do
   int k = 0, conv = 0;
   auto t0 = std::chrono::steady_clock::now();
   for (k = 0; k <= maxit; ++k) {
-    s = sweep(p, graphs && k > 0);  // first sweep eager (kernel attributes), then the graph
+    s = sweep(p, graphs);  // the first sweep of a plan runs eagerly, then the captured graph
     if (s) return s;
     double rn2;
     s = read_scalars(p, 1, &rn2);

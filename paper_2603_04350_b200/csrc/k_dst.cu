@@ -6,15 +6,17 @@
 //   y_0 = 0, y_i = sin(pi i/M)(x_i + x_{M-i}) + (x_i - x_{M-i})/2          (i = 1..M-1)
 //   Y_k = sum_i y_i e^{-2 pi i ik/M}                                         (complex FFT)
 //   F_{2k} = -Im Y_k,  F_1 = Re Y_0 / 2,  F_{2k+1} = F_{2k-1} + Re Y_k       (prefix sum)
-// and V x = sqrt(2/M) F.  Two real lines travel as one complex sequence (their Y's are
-// separated with the k <-> M-k Hermitian pairing), so one complex FFT of length M
-// transforms two lines.  For strided axes the two lines are two adjacent columns, i.e.
-// one 16-byte double2 per grid row in the padded spectral layout.
+// and V x = sqrt(2/M) F.  Two real lines travel as one complex sequence (rows 2q, 2q+1
+// or columns 2c, 2c+1 -- for columns that is one aligned double2 per grid row), and
+// their Y's are separated with the k <-> M-k Hermitian pairing.
 //
-// One CTA owns PP line pairs in shared memory ([M][PP] complex, pair index fastest:
-// conflict-free 16-byte accesses) and runs: load -> preprocess -> in-place Stockham
-// radix-16 FFT -> Hermitian unpack -> chunked prefix sum -> scale -> store.  The fused
-// nonlinear column kernel does transform -> N(u) pointwise -> transform in one visit.
+// Per line pair, T = M/R0 threads run a register-resident Stockham FFT (radix R0 = 16 or
+// 8 first, a middle radix, a small last radix): stage 0 is fed straight from global memory
+// (preprocessing fused into the load), shared memory carries only the stage transposes,
+// and the last stage is run on Hermitian partner jobs (j, NS - j) so the unpack happens
+// in registers.  The prefix sum is a per-thread chunk scan + warp-shuffle scan +
+// cross-warp offsets.  Shared layout [position][group] with a 1/16 padding swizzle keeps
+// every 16-byte access conflict-free.  G line pairs share a CTA.
 #include "expd_internal.h"
 #include "fft_dev.cuh"
 
@@ -31,328 +33,363 @@ __device__ __forceinline__ double poly_eval(const Poly& P, double u) {
   return acc;
 }
 
-template <int M>
-struct DstCfg {
-  static constexpr int PPmax = 4096 / M;
-  static constexpr int PP = PPmax < M / 2 ? PPmax : (M / 2 > 0 ? M / 2 : 1);  // line pairs / CTA
-  static constexpr int THREADS = (PP * M / 16) < 32 ? 32 : PP * M / 16;
-  static constexpr int C = (M / 16 < 1) ? 1 : (M / 16 > 32 ? 32 : M / 16);  // scan chunks / pair
-  static constexpr int L = (M / 2) / C;
+// radix plan: NST stages R0 (first), RMID (middle, if NST == 3), RL (last)
+template <int M> struct DPlan;
+template <> struct DPlan<4>    { static constexpr int NST = 1, R0 = 4,  RMID = 1,  RL = 4; };
+template <> struct DPlan<8>    { static constexpr int NST = 1, R0 = 8,  RMID = 1,  RL = 8; };
+template <> struct DPlan<16>   { static constexpr int NST = 1, R0 = 16, RMID = 1,  RL = 16; };
+template <> struct DPlan<32>   { static constexpr int NST = 2, R0 = 8,  RMID = 1,  RL = 4; };
+template <> struct DPlan<64>   { static constexpr int NST = 3, R0 = 8,  RMID = 2,  RL = 4; };
+template <> struct DPlan<128>  { static constexpr int NST = 2, R0 = 16, RMID = 1,  RL = 8; };
+template <> struct DPlan<256>  { static constexpr int NST = 3, R0 = 16, RMID = 2,  RL = 8; };
+template <> struct DPlan<512>  { static constexpr int NST = 3, R0 = 16, RMID = 4,  RL = 8; };
+template <> struct DPlan<1024> { static constexpr int NST = 3, R0 = 16, RMID = 8,  RL = 8; };
+template <> struct DPlan<2048> { static constexpr int NST = 3, R0 = 16, RMID = 16, RL = 8; };
+template <> struct DPlan<4096> { static constexpr int NST = 3, R0 = 16, RMID = 16, RL = 16; };
+
+template <int M, int G>
+struct DGeo {
+  using P = DPlan<M>;
+  static constexpr int NST = P::NST, R0 = P::R0, RMID = P::RMID, RL = P::RL;
+  static constexpr int T = M / R0;                 // threads per line pair
+  static constexpr int THREADS = G * T;
+  static constexpr int NSM = R0;                   // Ns of the middle stage
+  static constexpr int NSL = M / RL;               // Ns of the last stage
+  static constexpr int L = (M / 2) / T;            // prefix-sum chunk per thread (= R0/2)
+  static constexpr int SW = M + M / 16;            // swizzled positions per group
+  static constexpr int JW = G >= 32 ? 1 : 32 / G;  // threads of one group inside a warp
+  static constexpr int NWB = (T + JW - 1) / JW;    // warp blocks per group
 };
 
-// One in-place Stockham pass of radix R with NS = product of earlier radices.
-template <int M, int PP, int THREADS, int R, int NS>
-__device__ __forceinline__ void stockham_pass(double2* A, const double2* __restrict__ tw) {
-  constexpr int JOBS = PP * M / R;
-  constexpr int JT = (JOBS + THREADS - 1) / THREADS;
+__device__ __forceinline__ int swz(int p) { return p + (p >> 4); }
+
+template <int G>
+__device__ __forceinline__ double2& at(double2* buf, int p, int g) {
+  return buf[swz(p) * G + g];
+}
+
+// y_i from z_i and its mirror z_{M-i} (sin(pi i/M) = sin(pi (M-i)/M))
+__device__ __forceinline__ double2 preprocess(double2 z, double2 zm, double s) {
+  double2 sum = cadd(z, zm), dif = csub(z, zm);
+  return make_double2(fma(s, sum.x, 0.5 * dif.x), fma(s, sum.y, 0.5 * dif.y));
+}
+
+// e_k (even output F_{2k}) and w_k (prefix-sum increment) of both lines from Z_k, Z_{M-k}
+__device__ __forceinline__ void unpack(double2 Zk, double2 Zm, bool k0, double2& e, double2& w) {
+  e = make_double2(-0.5 * (Zk.y - Zm.y), 0.5 * (Zk.x - Zm.x));
+  w = make_double2(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y + Zm.y));
+  if (k0) w = make_double2(0.5 * w.x, 0.5 * w.y);
+}
+
+// In-place middle Stockham stage (radix R, NS) on all groups.
+template <int M, int G, int R, int NS>
+__device__ __forceinline__ void mid_stage(double2* buf, const double2* __restrict__ tw) {
+  using D = DGeo<M, G>;
+  constexpr int JOBS = G * (M / R);
+  constexpr int JT = (JOBS + D::THREADS - 1) / D::THREADS;
   double2 v[JT][R];
 #pragma unroll
   for (int jt = 0; jt < JT; ++jt) {
-    const int J = threadIdx.x + jt * THREADS;
+    const int J = threadIdx.x + jt * D::THREADS;
     if (J < JOBS) {
-      const int p = J % PP, j = J / PP, k = j % NS;
+      const int g = J % G, jm = J / G, k = jm % NS;
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[jt][r] = A[(j + r * (M / R)) * PP + p];
-      if constexpr (NS > 1) {
+      for (int r = 0; r < R; ++r) v[jt][r] = at<G>(buf, jm + r * (M / R), g);
 #pragma unroll
-        for (int r = 1; r < R; ++r) v[jt][r] = cmul(v[jt][r], __ldg(tw + ((r * k * (M / (NS * R))) % M)));
-      }
+      for (int r = 1; r < R; ++r) v[jt][r] = cmul(v[jt][r], __ldg(tw + (r * k * (M / (NS * R))) % M));
       DFT<R, -1>::run(v[jt]);
     }
   }
   __syncthreads();
 #pragma unroll
   for (int jt = 0; jt < JT; ++jt) {
-    const int J = threadIdx.x + jt * THREADS;
+    const int J = threadIdx.x + jt * D::THREADS;
     if (J < JOBS) {
-      const int p = J % PP, j = J / PP, k = j % NS;
-      const int base = (j / NS) * NS * R + k;
+      const int g = J % G, jm = J / G, k = jm % NS;
+      const int base = (jm / NS) * NS * R + k;
 #pragma unroll
-      for (int r = 0; r < R; ++r) A[(base + r * NS) * PP + p] = v[jt][r];
+      for (int r = 0; r < R; ++r) at<G>(buf, base + r * NS, g) = v[jt][r];
     }
   }
   __syncthreads();
 }
 
-template <int M, int PP, int THREADS>
-__device__ __forceinline__ void fft_smem(double2* A, const double2* tw) {
-  if constexpr (M == 4) {
-    stockham_pass<M, PP, THREADS, 4, 1>(A, tw);
-  } else if constexpr (M == 8) {
-    stockham_pass<M, PP, THREADS, 8, 1>(A, tw);
-  } else if constexpr (M == 16) {
-    stockham_pass<M, PP, THREADS, 16, 1>(A, tw);
-  } else if constexpr (M == 32) {
-    stockham_pass<M, PP, THREADS, 16, 1>(A, tw);
-    stockham_pass<M, PP, THREADS, 2, 16>(A, tw);
-  } else if constexpr (M == 64) {
-    stockham_pass<M, PP, THREADS, 16, 1>(A, tw);
-    stockham_pass<M, PP, THREADS, 4, 16>(A, tw);
-  } else if constexpr (M == 128) {
-    stockham_pass<M, PP, THREADS, 16, 1>(A, tw);
-    stockham_pass<M, PP, THREADS, 8, 16>(A, tw);
-  } else if constexpr (M == 256) {
-    stockham_pass<M, PP, THREADS, 16, 1>(A, tw);
-    stockham_pass<M, PP, THREADS, 16, 16>(A, tw);
-  } else if constexpr (M == 512) {
-    stockham_pass<M, PP, THREADS, 16, 1>(A, tw);
-    stockham_pass<M, PP, THREADS, 16, 16>(A, tw);
-    stockham_pass<M, PP, THREADS, 2, 256>(A, tw);
-  } else if constexpr (M == 1024) {
-    stockham_pass<M, PP, THREADS, 16, 1>(A, tw);
-    stockham_pass<M, PP, THREADS, 16, 16>(A, tw);
-    stockham_pass<M, PP, THREADS, 4, 256>(A, tw);
-  } else if constexpr (M == 2048) {
-    stockham_pass<M, PP, THREADS, 16, 1>(A, tw);
-    stockham_pass<M, PP, THREADS, 16, 16>(A, tw);
-    stockham_pass<M, PP, THREADS, 8, 256>(A, tw);
+// The DST of G line pairs whose stage-0 inputs are already preprocessed in v[R0] (thread
+// (g, j) holds y_i, i = j + T r).  Leaves F_{p+1} (unscaled) for the thread's positions
+// p = 2 c L - 1 + q, q = 0..2L-1 (c = j) in out[].  Starts with a barrier (buf may be in
+// use by the caller) and ends with buf holding this thread's positions' values.
+template <int M, int G>
+__device__ __forceinline__ void dst_core(double2 (&v)[DGeo<M, G>::R0], double2* buf, double2* wt,
+                                         const double2* __restrict__ tw, double2 (&out)[2 * DGeo<M, G>::L]) {
+  using D = DGeo<M, G>;
+  constexpr int R0 = D::R0, RL = D::RL, NSL = D::NSL, T = D::T, L = D::L;
+  const int g = threadIdx.x % G, j = threadIdx.x / G;
+  DFT<R0, -1>::run(v);
+  __syncthreads();
+  if constexpr (D::NST == 1) {
+    // one thread owns the whole sequence: unpack in registers
+#pragma unroll
+    for (int k = 0; k < M / 2; ++k) {
+      double2 e, w;
+      unpack(v[k], v[(M - k) % M], k == 0, e, w);
+      if (k >= 1) at<G>(buf, 2 * k - 1, g) = e;
+      at<G>(buf, 2 * k, g) = w;
+    }
   } else {
-    static_assert(M == 4096, "unsupported M");
-    stockham_pass<M, PP, THREADS, 16, 1>(A, tw);
-    stockham_pass<M, PP, THREADS, 16, 16>(A, tw);
-    stockham_pass<M, PP, THREADS, 16, 256>(A, tw);
-  }
-}
-
-// In: A[i][p] = z_i for i = 1..M-1 (A[0] ignored).  Out: A[pos][p] = F_{pos+1} (unscaled)
-// for pos = 0..M-2.  tot: [C][PP] scratch.  Begins and ends with all threads synced.
-template <int M>
-__device__ __forceinline__ void dst_core(double2* A, double2* tot, const double2* tw, const double* sinp) {
-  using Cf = DstCfg<M>;
-  constexpr int PP = Cf::PP, THREADS = Cf::THREADS, C = Cf::C, L = Cf::L;
-  const int tid = threadIdx.x;
-  // preprocess: pairs (i, M-i), i = 1..M/2
-  for (int J = tid; J < PP * (M / 2); J += THREADS) {
-    const int p = J % PP, i = J / PP + 1;
-    const double s = __ldg(sinp + i);
-    double2 a = A[i * PP + p];
-    if (i == M / 2) {
-      A[i * PP + p] = make_double2(2.0 * s * a.x, 2.0 * s * a.y);
-    } else {
-      double2 b = A[(M - i) * PP + p];
-      double2 sum = cadd(a, b), dif = csub(a, b);
-      A[i * PP + p] = make_double2(fma(s, sum.x, 0.5 * dif.x), fma(s, sum.y, 0.5 * dif.y));
-      A[(M - i) * PP + p] = make_double2(fma(s, sum.x, -0.5 * dif.x), fma(s, sum.y, -0.5 * dif.y));
-    }
-  }
-  for (int p = tid; p < PP; p += THREADS) A[p] = make_double2(0.0, 0.0);
-  __syncthreads();
-  fft_smem<M, PP, THREADS>(A, tw);
-  // Hermitian unpack of the two lines: even outputs and the prefix-sum increments w_k
-  constexpr int KJ = (PP * (M / 2) + THREADS - 1) / THREADS;
-  double2 ev[KJ], wv[KJ];
 #pragma unroll
-  for (int jt = 0; jt < KJ; ++jt) {
-    const int J = tid + jt * THREADS;
-    if (J < PP * (M / 2)) {
-      const int p = J % PP, k = J / PP;
-      double2 Zk = A[k * PP + p], Zm = A[((M - k) % M) * PP + p];
-      ev[jt] = make_double2(-0.5 * (Zk.y - Zm.y), 0.5 * (Zk.x - Zm.x));
-      wv[jt] = make_double2(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y + Zm.y));
-      if (k == 0) wv[jt] = make_double2(0.5 * wv[jt].x, 0.5 * wv[jt].y);
-    }
-  }
-  __syncthreads();
+    for (int r = 0; r < R0; ++r) at<G>(buf, j * R0 + r, g) = v[r];
+    __syncthreads();
+    if constexpr (D::NST == 3) mid_stage<M, G, D::RMID, D::NSM>(buf, tw);
+    // last stage on Hermitian partner jobs, then the unpack
+    constexpr int PJOBS = G * (NSL / 2);
+    constexpr int PJT = (PJOBS + D::THREADS - 1) / D::THREADS;
+    double2 va[PJT][RL], vb[PJT][RL];
 #pragma unroll
-  for (int jt = 0; jt < KJ; ++jt) {
-    const int J = tid + jt * THREADS;
-    if (J < PP * (M / 2)) {
-      const int p = J % PP, k = J / PP;
-      if (k >= 1) A[(2 * k - 1) * PP + p] = ev[jt];
-      A[(2 * k) * PP + p] = wv[jt];
-    }
-  }
-  __syncthreads();
-  // chunked inclusive scan of A[2k], k = 0..M/2-1, per pair
-  const int p = tid % PP, c = tid / PP;
-  double2 acc = make_double2(0.0, 0.0);
-  if (c < C) {
-#pragma unroll 4
-    for (int l = 0; l < L; ++l) {
-      const int k = c * L + l;
-      acc = cadd(acc, A[(2 * k) * PP + p]);
-      A[(2 * k) * PP + p] = acc;
-    }
-    tot[c * PP + p] = acc;
-  }
-  __syncthreads();
-  if (c < C && c > 0) {
-    double2 off = make_double2(0.0, 0.0);
-    for (int cc = 0; cc < c; ++cc) off = cadd(off, tot[cc * PP + p]);
-#pragma unroll 4
-    for (int l = 0; l < L; ++l) {
-      const int k = c * L + l;
-      A[(2 * k) * PP + p] = cadd(A[(2 * k) * PP + p], off);
-    }
-  }
-  __syncthreads();
-}
-
-// ---------------------------------------------------------------------------------------
-// x-axis (contiguous) transform of row pairs.  rows_per_slice = n^{dim-1}.
-// in: row r of slice s at in + s*in_slice + r*in_rs; out likewise.  NLOAD: apply N(u)
-// to the loaded values (physical input); NLMID: transform, N, transform (dim == 1).
-// ---------------------------------------------------------------------------------------
-template <int M, bool NLOAD, bool NLMID>
-__global__ void __launch_bounds__(DstCfg<M>::THREADS) k_dst_rows(const double* __restrict__ in, long in_slice,
-                                                                 int in_rs, double* __restrict__ out,
-                                                                 long out_slice, int out_rs, int rows_per_slice,
-                                                                 const double2* tw, const double* sinp, Poly poly) {
-  using Cf = DstCfg<M>;
-  constexpr int PP = Cf::PP, THREADS = Cf::THREADS;
-  constexpr int n = M - 1;
-  extern __shared__ double2 sm[];
-  double2* A = sm;
-  double2* tot = sm + M * PP;
-  const long slice = blockIdx.y;
-  const int pair0 = blockIdx.x * PP;
-  const double* inS = in + slice * in_slice;
-  double* outS = out + slice * out_slice;
-  // load: 2*PP rows, n values each, lanes along the row (coalesced)
-  for (int J = threadIdx.x; J < 2 * PP * n; J += THREADS) {
-    const int rr = J / n, i = J % n;  // local row, position
-    const int p = rr >> 1, half = rr & 1;
-    const int row = 2 * (pair0 + p) + half;
-    double v = 0.0;
-    if (row < rows_per_slice) v = __ldg(inS + (long)row * in_rs + i);
-    if constexpr (NLOAD) v = poly_eval(poly, v);
-    double* slot = reinterpret_cast<double*>(&A[(i + 1) * PP + p]) + half;
-    *slot = v;
-  }
-  __syncthreads();
-  dst_core<M>(A, tot, tw, sinp);
-  const double scale = sqrt(2.0 / (double)M);
-  if constexpr (NLMID) {
-    // A[pos] = F_{pos+1}: physical values u = scale * F; N(u) moves to slot pos+1
-    constexpr int JT = (PP * n + THREADS - 1) / THREADS;
-    double2 tmp[JT];
+    for (int pt = 0; pt < PJT; ++pt) {
+      const int PJ = threadIdx.x + pt * D::THREADS;
+      if (PJ < PJOBS) {
+        const int gg = PJ % G, pj = PJ / G;
+        const int ja = pj, jb = pj == 0 ? NSL / 2 : NSL - pj;
 #pragma unroll
-    for (int jt = 0; jt < JT; ++jt) {
-      const int J = threadIdx.x + jt * THREADS;
-      if (J < PP * n) {
-        double2 u = A[(J / PP) * PP + (J % PP)];
-        tmp[jt] = make_double2(poly_eval(poly, scale * u.x), poly_eval(poly, scale * u.y));
+        for (int r = 0; r < RL; ++r) {
+          va[pt][r] = at<G>(buf, ja + r * NSL, gg);
+          vb[pt][r] = at<G>(buf, jb + r * NSL, gg);
+        }
+#pragma unroll
+        for (int r = 1; r < RL; ++r) {
+          va[pt][r] = cmul(va[pt][r], __ldg(tw + (r * ja) % M));
+          vb[pt][r] = cmul(vb[pt][r], __ldg(tw + (r * jb) % M));
+        }
+        DFT<RL, -1>::run(va[pt]);
+        DFT<RL, -1>::run(vb[pt]);
       }
     }
     __syncthreads();
 #pragma unroll
-    for (int jt = 0; jt < JT; ++jt) {
-      const int J = threadIdx.x + jt * THREADS;
-      if (J < PP * n) A[(J / PP + 1) * PP + (J % PP)] = tmp[jt];
+    for (int pt = 0; pt < PJT; ++pt) {
+      const int PJ = threadIdx.x + pt * D::THREADS;
+      if (PJ < PJOBS) {
+        const int gg = PJ % G, pj = PJ / G;
+        const int ja = pj, jb = pj == 0 ? NSL / 2 : NSL - pj;
+#pragma unroll
+        for (int r = 0; r < RL / 2; ++r) {
+          double2 e, w;
+          const int ka = ja + NSL * r, kb = jb + NSL * r;
+          unpack(va[pt][r], pj == 0 ? va[pt][(RL - r) % RL] : vb[pt][RL - 1 - r], ka == 0, e, w);
+          if (ka >= 1) at<G>(buf, 2 * ka - 1, gg) = e;
+          at<G>(buf, 2 * ka, gg) = w;
+          unpack(vb[pt][r], pj == 0 ? vb[pt][RL - 1 - r] : va[pt][RL - 1 - r], false, e, w);
+          at<G>(buf, 2 * kb - 1, gg) = e;
+          at<G>(buf, 2 * kb, gg) = w;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  // prefix sum of w_k over k: chunk k in [c L, c L + L), c = j
+  double2 tot = make_double2(0.0, 0.0);
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    const int k = j * L + l;
+    if (k >= 1) out[2 * l] = at<G>(buf, 2 * k - 1, g);
+    tot = cadd(tot, at<G>(buf, 2 * k, g));
+    out[2 * l + 1] = tot;
+  }
+  // inclusive scan of chunk totals across the group's threads (lanes g + G*j')
+  double2 inc = tot;
+  const int lane = threadIdx.x & 31;
+  if constexpr (D::JW > 1) {
+#pragma unroll
+    for (int d = 1; d < D::JW; d <<= 1) {
+      double ox = __shfl_up_sync(0xffffffffu, inc.x, d * G);
+      double oy = __shfl_up_sync(0xffffffffu, inc.y, d * G);
+      if (lane >= d * G) inc = cadd(inc, make_double2(ox, oy));
+    }
+  }
+  const int jw = j / D::JW;
+  if constexpr (D::NWB > 1) {
+    if (j % D::JW == D::JW - 1 || j == T - 1) wt[jw * G + g] = inc;
+    __syncthreads();
+  }
+  double2 off = csub(inc, tot);  // exclusive within the warp block
+  if constexpr (D::NWB > 1) {
+    for (int b = 0; b < jw; ++b) off = cadd(off, wt[b * G + g]);
+  }
+#pragma unroll
+  for (int l = 0; l < L; ++l) out[2 * l + 1] = cadd(out[2 * l + 1], off);
+  if (j == 0) out[0] = make_double2(0.0, 0.0);  // position -1 does not exist
+}
+
+// asynchronous global -> shared copies (LDGSTS): every load of a work item is in flight
+// at once, without holding registers, before the item's math starts
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+// ---------------------------------------------------------------------------------------
+// x-axis transform of row pairs.  Row r of slice s at in + s*in_slice + r*in_rs (length
+// n = M-1); output rows likewise (out_rs == M: padded spectral row, pad written as 0).
+// MODE 0: V; 1: V N(in) (N applied on load, physical input); 2: V N(V in) (dim 1).
+// ---------------------------------------------------------------------------------------
+template <int M, int G, int MODE>
+__global__ void __launch_bounds__(DGeo<M, G>::THREADS) k_rows(const double* __restrict__ in, long in_slice,
+                                                               int in_rs, double* __restrict__ out, long out_slice,
+                                                               int out_rs, int rows_per_slice,
+                                                               const double2* __restrict__ tw,
+                                                               const double* __restrict__ sinp, Poly poly) {
+  using D = DGeo<M, G>;
+  constexpr int R0 = D::R0, T = D::T, L = D::L, THREADS = D::THREADS;
+  constexpr int n = M - 1;
+  extern __shared__ double2 dsm[];
+  double2* buf = dsm;                // [SW][G]   (aliases the raw rows below)
+  double2* wt = dsm + D::SW * G;     // [NWB][G]
+  double* raw = reinterpret_cast<double*>(dsm);  // [2G][M] raw rows
+  const int g = threadIdx.x % G, j = threadIdx.x / G;
+  const long slice = blockIdx.y;
+  const int row0 = 2 * blockIdx.x * G;  // first row of the CTA
+  const double* inS = in + slice * in_slice;
+  // 1. all loads of the item in flight at once
+  for (int idx = threadIdx.x; idx < 2 * G * n; idx += THREADS) {
+    const int rr = idx / n, pos = idx % n;
+    if (row0 + rr < rows_per_slice) cp_async8(raw + rr * M + pos, inS + (long)(row0 + rr) * in_rs + pos);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const bool has_a = row0 + 2 * g < rows_per_slice, has_b = row0 + 2 * g + 1 < rows_per_slice;
+  auto ld = [&](int i) -> double2 {  // z_i, i in [1, M-1]
+    double a = has_a ? raw[(2 * g) * M + i - 1] : 0.0, b = has_b ? raw[(2 * g + 1) * M + i - 1] : 0.0;
+    if constexpr (MODE == 1) {
+      a = has_a ? poly_eval(poly, a) : 0.0;
+      b = has_b ? poly_eval(poly, b) : 0.0;
+    }
+    return make_double2(a, b);
+  };
+  double2 v[R0];
+#pragma unroll
+  for (int r = 0; r < R0; ++r) {
+    const int i = j + T * r;
+    v[r] = i == 0 ? make_double2(0.0, 0.0) : preprocess(ld(i), ld(M - i), __ldg(sinp + i));
+  }
+  double2 o[2 * L];
+  dst_core<M, G>(v, buf, wt, tw, o);
+  const double scale = sqrt(2.0 / (double)M);
+  if constexpr (MODE == 2) {
+    // physical values u = scale F; N(u) becomes the input of the second transform
+#pragma unroll
+    for (int q = 0; q < 2 * L; ++q) {
+      const int p = 2 * j * L - 1 + q;
+      if (p >= 0) at<G>(buf, p, g) = make_double2(poly_eval(poly, scale * o[q].x), poly_eval(poly, scale * o[q].y));
     }
     __syncthreads();
-    dst_core<M>(A, tot, tw, sinp);
+#pragma unroll
+    for (int r = 0; r < R0; ++r) {
+      const int i = j + T * r;
+      v[r] = i == 0 ? make_double2(0.0, 0.0)
+                    : preprocess(at<G>(buf, i - 1, g), at<G>(buf, M - i - 1, g), __ldg(sinp + i));
+    }
+    dst_core<M, G>(v, buf, wt, tw, o);
   }
-  // store rows (out_rs == M: padded spectral row, write 0 at the pad position)
-  for (int J = threadIdx.x; J < 2 * PP * out_rs; J += THREADS) {
-    const int rr = J / out_rs, i = J % out_rs;
-    const int p = rr >> 1, half = rr & 1;
-    const int row = 2 * (pair0 + p) + half;
+  // 2. outputs through shared memory, then coalesced row stores
+#pragma unroll
+  for (int q = 0; q < 2 * L; ++q) {
+    const int p = 2 * j * L - 1 + q;
+    if (p >= 0) at<G>(buf, p, g) = make_double2(scale * o[q].x, scale * o[q].y);
+  }
+  __syncthreads();
+  double* outS = out + slice * out_slice;
+  for (int idx = threadIdx.x; idx < 2 * G * out_rs; idx += THREADS) {
+    const int rr = idx / out_rs, pos = idx % out_rs;
+    const int row = row0 + rr;
     if (row < rows_per_slice) {
-      double v = 0.0;
-      if (i < n) v = scale * reinterpret_cast<const double*>(&A[i * PP + p])[half];
-      outS[(long)row * out_rs + i] = v;
+      double val = 0.0;  // pad position of a spectral row stays 0
+      if (pos < n) {
+        const double2 vv = at<G>(buf, pos, rr >> 1);
+        val = (rr & 1) ? vv.y : vv.x;
+      }
+      outS[(long)row * out_rs + pos] = val;
     }
   }
 }
 
 // ---------------------------------------------------------------------------------------
-// strided-axis transform of column pairs in the padded spectral layout.
-// line pair lp = (o, cp): base = o*outer_stride + 2*cp, element i at base + i*stride.
-// NLMID: transform, N(u) pointwise, transform (the fused stage-3 visit).
+// strided-axis transform of column pairs in the padded spectral layout: line pair
+// (o, cp): base = o*outer_stride + 2*cp, element i-1 at base + (i-1)*stride.
+// NL: transform, N(u) pointwise, transform (the fused stage-3 visit).
 // ---------------------------------------------------------------------------------------
-template <int M, bool NLMID>
-__global__ void __launch_bounds__(DstCfg<M>::THREADS) k_dst_cols(const double* in, long in_slice, double* out,
-                                                                 long out_slice, long stride, long outer_stride,
-                                                                 const double2* tw, const double* sinp,
-                                                                 Poly poly) {
-  using Cf = DstCfg<M>;
-  constexpr int PP = Cf::PP, THREADS = Cf::THREADS;
+template <int M, int G, bool NL>
+__global__ void __launch_bounds__(DGeo<M, G>::THREADS) k_cols(const double* in, long in_slice, double* out,
+                                                               long out_slice, long stride, long outer_stride,
+                                                               const double2* __restrict__ tw,
+                                                               const double* __restrict__ sinp, Poly poly) {
+  using D = DGeo<M, G>;
+  constexpr int R0 = D::R0, T = D::T, L = D::L, THREADS = D::THREADS;
   constexpr int n = M - 1;
-  constexpr int GROUPS = (M / 2) / PP;  // column-pair groups per outer index
-  extern __shared__ double2 sm[];
-  double2* A = sm;
-  double2* tot = sm + M * PP;
+  constexpr int GROUPS = (M / 2) / G;  // column-pair groups per outer index
+  extern __shared__ double2 dsm[];
+  double2* buf = dsm;                // [SW][G] (aliases raw [n][G])
+  double2* wt = dsm + D::SW * G;     // [NWB][G]
   const long slice = blockIdx.y;
   const long o = blockIdx.x / GROUPS;
-  const int cp0 = (blockIdx.x % GROUPS) * PP;
-  const double* inB = in + slice * in_slice + o * outer_stride + 2 * cp0;
-  double* outB = out + slice * out_slice + o * outer_stride + 2 * cp0;
-  for (int J = threadIdx.x; J < PP * n; J += THREADS) {
-    const int p = J % PP, i = J / PP;
-    A[(i + 1) * PP + p] = __ldg(reinterpret_cast<const double2*>(inB + (long)i * stride) + p);
+  const int cp0 = (blockIdx.x % GROUPS) * G;
+  const double2* ib = reinterpret_cast<const double2*>(in + slice * in_slice + o * outer_stride + 2 * cp0);
+  double2* ob = reinterpret_cast<double2*>(out + slice * out_slice + o * outer_stride + 2 * cp0);
+  const long st2 = stride / 2;  // in double2 units (stride is even: padded rows)
+  for (int idx = threadIdx.x; idx < n * G; idx += THREADS) {
+    const int pos = idx / G, gg = idx % G;
+    cp_async16(dsm + idx, ib + (long)pos * st2 + gg);
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const int g = threadIdx.x % G, j = threadIdx.x / G;
+  double2 v[R0];
+#pragma unroll
+  for (int r = 0; r < R0; ++r) {
+    const int i = j + T * r;
+    v[r] = i == 0 ? make_double2(0.0, 0.0) : preprocess(dsm[(i - 1) * G + g], dsm[(M - i - 1) * G + g], __ldg(sinp + i));
+  }
+  double2 oo[2 * L];
+  dst_core<M, G>(v, buf, wt, tw, oo);
+  const double scale = sqrt(2.0 / (double)M);
+  if constexpr (NL) {
+#pragma unroll
+    for (int q = 0; q < 2 * L; ++q) {
+      const int p = 2 * j * L - 1 + q;
+      if (p >= 0) at<G>(buf, p, g) = make_double2(poly_eval(poly, scale * oo[q].x), poly_eval(poly, scale * oo[q].y));
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R0; ++r) {
+      const int i = j + T * r;
+      v[r] = i == 0 ? make_double2(0.0, 0.0)
+                    : preprocess(at<G>(buf, i - 1, g), at<G>(buf, M - i - 1, g), __ldg(sinp + i));
+    }
+    dst_core<M, G>(v, buf, wt, tw, oo);
+  }
+#pragma unroll
+  for (int q = 0; q < 2 * L; ++q) {
+    const int p = 2 * j * L - 1 + q;
+    if (p >= 0) at<G>(buf, p, g) = make_double2(scale * oo[q].x, scale * oo[q].y);
   }
   __syncthreads();
-  dst_core<M>(A, tot, tw, sinp);
-  const double scale = sqrt(2.0 / (double)M);
-  if constexpr (NLMID) {
-    constexpr int JT = (PP * n + THREADS - 1) / THREADS;
-    double2 tmp[JT];
-#pragma unroll
-    for (int jt = 0; jt < JT; ++jt) {
-      const int J = threadIdx.x + jt * THREADS;
-      if (J < PP * n) {
-        double2 u = A[(J / PP) * PP + (J % PP)];
-        tmp[jt] = make_double2(poly_eval(poly, scale * u.x), poly_eval(poly, scale * u.y));
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int jt = 0; jt < JT; ++jt) {
-      const int J = threadIdx.x + jt * THREADS;
-      if (J < PP * n) A[(J / PP + 1) * PP + (J % PP)] = tmp[jt];
-    }
-    __syncthreads();
-    dst_core<M>(A, tot, tw, sinp);
-  }
-  for (int J = threadIdx.x; J < PP * n; J += THREADS) {
-    const int p = J % PP, i = J / PP;
-    double2 v = A[i * PP + p];
-    reinterpret_cast<double2*>(outB + (long)i * stride)[p] = make_double2(scale * v.x, scale * v.y);
+  for (int idx = threadIdx.x; idx < n * G; idx += THREADS) {
+    const int pos = idx / G, gg = idx % G;
+    ob[(long)pos * st2 + gg] = at<G>(buf, pos, gg);
   }
 }
 
 // ---------------------------------------------------------------------------------------
 // host-side dispatch
 // ---------------------------------------------------------------------------------------
-template <int M>
-static size_t dst_smem() {
-  return sizeof(double2) * (size_t)(M * DstCfg<M>::PP + DstCfg<M>::C * DstCfg<M>::PP);
-}
-
-template <int M, bool A_, bool B_>
-static cudaError_t rows_launch(const double* in, long in_slice, int in_rs, double* out, long out_slice, int out_rs,
-                               int rows, long nslices, const DstTables& t, const Poly& P, cudaStream_t st) {
-  auto k = k_dst_rows<M, A_, B_>;
-  static bool attr = false;
-  size_t sm = dst_smem<M>();
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  int pairs = (rows + 1) / 2;
-  dim3 grid((pairs + DstCfg<M>::PP - 1) / DstCfg<M>::PP, (unsigned)nslices);
-  k<<<grid, DstCfg<M>::THREADS, sm, st>>>(in, in_slice, in_rs, out, out_slice, out_rs, rows, t.tw, t.sinp, P);
-  return cudaGetLastError();
-}
-
-template <int M, bool NL>
-static cudaError_t cols_launch(const double* in, long in_slice, double* out, long out_slice, long stride,
-                               long outer_stride, long nouter, long nslices, const DstTables& t, const Poly& P,
-                               cudaStream_t st) {
-  auto k = k_dst_cols<M, NL>;
-  static bool attr = false;
-  size_t sm = dst_smem<M>();
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  dim3 grid((unsigned)(nouter * ((M / 2) / DstCfg<M>::PP)), (unsigned)nslices);
-  k<<<grid, DstCfg<M>::THREADS, sm, st>>>(in, in_slice, out, out_slice, stride, outer_stride, t.tw, t.sinp, P);
-  return cudaGetLastError();
-}
+template <int M> struct RowG { static constexpr int T = M / DPlan<M>::R0; static constexpr int G = T >= 128 ? 1 : 128 / T; };
+template <int M> struct ColG { static constexpr int T = M / DPlan<M>::R0; static constexpr int G0 = T >= 64 ? 2 : 128 / T; static constexpr int G = G0 > M / 2 ? M / 2 : G0; };
 
 struct RowsOp {
   const double* in; long in_slice; int in_rs; double* out; long out_slice; int out_rs; int rows; long nslices;
@@ -363,50 +400,87 @@ struct ColsOp {
   bool nl;
 };
 
+template <int M, int G>
+static size_t dst_smem() {
+  return sizeof(double2) * (size_t)(DGeo<M, G>::SW * G + DGeo<M, G>::NWB * G + 1);
+}
+template <typename K>
+static cudaError_t smem_attr(K k, size_t bytes, bool& done) {
+  if (!done) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    if (e != cudaSuccess) return e;
+    done = true;
+  }
+  return cudaSuccess;
+}
+
+template <int M, int MODE>
+static cudaError_t rows_launch(const RowsOp& o, const DstTables& t, const Poly& P, cudaStream_t st) {
+  constexpr int G = RowG<M>::G;
+  int pairs = (o.rows + 1) / 2;
+  dim3 grid((pairs + G - 1) / G, (unsigned)o.nslices);
+  const size_t sm = dst_smem<M, G>();
+  static bool done = false;  // per instantiation
+  cudaError_t e = smem_attr(k_rows<M, G, MODE>, sm, done);
+  if (e != cudaSuccess) return e;
+  k_rows<M, G, MODE><<<grid, DGeo<M, G>::THREADS, sm, st>>>(o.in, o.in_slice, o.in_rs, o.out, o.out_slice, o.out_rs,
+                                                            o.rows, t.tw, t.sinp, P);
+  return cudaGetLastError();
+}
 template <int M>
 static cudaError_t run_rows(const RowsOp& o, const DstTables& t, const Poly& P, cudaStream_t st) {
-  if (o.nlload) return rows_launch<M, true, false>(o.in, o.in_slice, o.in_rs, o.out, o.out_slice, o.out_rs, o.rows, o.nslices, t, P, st);
-  if (o.nlmid) return rows_launch<M, false, true>(o.in, o.in_slice, o.in_rs, o.out, o.out_slice, o.out_rs, o.rows, o.nslices, t, P, st);
-  return rows_launch<M, false, false>(o.in, o.in_slice, o.in_rs, o.out, o.out_slice, o.out_rs, o.rows, o.nslices, t, P, st);
+  if (o.nlload) return rows_launch<M, 1>(o, t, P, st);
+  if (o.nlmid) return rows_launch<M, 2>(o, t, P, st);
+  return rows_launch<M, 0>(o, t, P, st);
 }
 template <int M>
 static cudaError_t run_cols(const ColsOp& o, const DstTables& t, const Poly& P, cudaStream_t st) {
-  if (o.nl) return cols_launch<M, true>(o.in, o.in_slice, o.out, o.out_slice, o.stride, o.outer_stride, o.nouter, o.nslices, t, P, st);
-  return cols_launch<M, false>(o.in, o.in_slice, o.out, o.out_slice, o.stride, o.outer_stride, o.nouter, o.nslices, t, P, st);
+  constexpr int G = ColG<M>::G;
+  dim3 grid((unsigned)(o.nouter * ((M / 2) / G)), (unsigned)o.nslices);
+  const size_t sm = dst_smem<M, G>();
+  cudaError_t e;
+  static bool done_nl = false, done_pl = false;  // per instantiation
+  if (o.nl) {
+    if ((e = smem_attr(k_cols<M, G, true>, sm, done_nl)) != cudaSuccess) return e;
+    k_cols<M, G, true><<<grid, DGeo<M, G>::THREADS, sm, st>>>(o.in, o.in_slice, o.out, o.out_slice, o.stride,
+                                                               o.outer_stride, t.tw, t.sinp, P);
+  } else {
+    if ((e = smem_attr(k_cols<M, G, false>, sm, done_pl)) != cudaSuccess) return e;
+    k_cols<M, G, false><<<grid, DGeo<M, G>::THREADS, sm, st>>>(o.in, o.in_slice, o.out, o.out_slice, o.stride,
+                                                                o.outer_stride, t.tw, t.sinp, P);
+  }
+  return cudaGetLastError();
 }
-
-template <int M> struct RowsCall { static cudaError_t go(const RowsOp& o, const DstTables& t, const Poly& P, cudaStream_t st) { return run_rows<M>(o, t, P, st); } };
-template <int M> struct ColsCall { static cudaError_t go(const ColsOp& o, const DstTables& t, const Poly& P, cudaStream_t st) { return run_cols<M>(o, t, P, st); } };
 
 static cudaError_t rows(int M, const RowsOp& o, const DstTables& t, const Poly& P, cudaStream_t st) {
   switch (M) {
-    case 4: return RowsCall<4>::go(o, t, P, st);
-    case 8: return RowsCall<8>::go(o, t, P, st);
-    case 16: return RowsCall<16>::go(o, t, P, st);
-    case 32: return RowsCall<32>::go(o, t, P, st);
-    case 64: return RowsCall<64>::go(o, t, P, st);
-    case 128: return RowsCall<128>::go(o, t, P, st);
-    case 256: return RowsCall<256>::go(o, t, P, st);
-    case 512: return RowsCall<512>::go(o, t, P, st);
-    case 1024: return RowsCall<1024>::go(o, t, P, st);
-    case 2048: return RowsCall<2048>::go(o, t, P, st);
-    case 4096: return RowsCall<4096>::go(o, t, P, st);
+    case 4: return run_rows<4>(o, t, P, st);
+    case 8: return run_rows<8>(o, t, P, st);
+    case 16: return run_rows<16>(o, t, P, st);
+    case 32: return run_rows<32>(o, t, P, st);
+    case 64: return run_rows<64>(o, t, P, st);
+    case 128: return run_rows<128>(o, t, P, st);
+    case 256: return run_rows<256>(o, t, P, st);
+    case 512: return run_rows<512>(o, t, P, st);
+    case 1024: return run_rows<1024>(o, t, P, st);
+    case 2048: return run_rows<2048>(o, t, P, st);
+    case 4096: return run_rows<4096>(o, t, P, st);
     default: return cudaErrorInvalidValue;
   }
 }
 static cudaError_t cols(int M, const ColsOp& o, const DstTables& t, const Poly& P, cudaStream_t st) {
   switch (M) {
-    case 4: return ColsCall<4>::go(o, t, P, st);
-    case 8: return ColsCall<8>::go(o, t, P, st);
-    case 16: return ColsCall<16>::go(o, t, P, st);
-    case 32: return ColsCall<32>::go(o, t, P, st);
-    case 64: return ColsCall<64>::go(o, t, P, st);
-    case 128: return ColsCall<128>::go(o, t, P, st);
-    case 256: return ColsCall<256>::go(o, t, P, st);
-    case 512: return ColsCall<512>::go(o, t, P, st);
-    case 1024: return ColsCall<1024>::go(o, t, P, st);
-    case 2048: return ColsCall<2048>::go(o, t, P, st);
-    case 4096: return ColsCall<4096>::go(o, t, P, st);
+    case 4: return run_cols<4>(o, t, P, st);
+    case 8: return run_cols<8>(o, t, P, st);
+    case 16: return run_cols<16>(o, t, P, st);
+    case 32: return run_cols<32>(o, t, P, st);
+    case 64: return run_cols<64>(o, t, P, st);
+    case 128: return run_cols<128>(o, t, P, st);
+    case 256: return run_cols<256>(o, t, P, st);
+    case 512: return run_cols<512>(o, t, P, st);
+    case 1024: return run_cols<1024>(o, t, P, st);
+    case 2048: return run_cols<2048>(o, t, P, st);
+    case 4096: return run_cols<4096>(o, t, P, st);
     default: return cudaErrorInvalidValue;
   }
 }
