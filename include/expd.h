@@ -142,6 +142,12 @@ expd_status expd_dst(expd_plan* plan, const double* in, double* out, long nslice
    the fused time-local kernel K1, in milliseconds. */
 expd_status expd_set_profiling(expd_plan* plan, int enable);
 expd_status expd_sweep_stage_ms(expd_plan* plan, double* ms_nonlin, double* ms_time);
+/* Diagnostics for tuning: average device time (ms, CUDA events) of `reps` back-to-back
+   launches of one kernel family on the workspace's spectral state: which = 0 x-axis DST
+   pass, 1 strided-axis DST pass, 2 fused strided IDST -> N -> DST pass (each over nslices
+   slices, 1 <= nslices <= nt), 3 the fused time-local kernel K1 (whole state).  The
+   workspace contents are overwritten with transformed data. */
+expd_status expd_debug_kernel_ms(expd_plan* plan, int which, long nslices, int reps, double* ms);
 /* Number of kernels one expd_sweep launches (for the benchmark's launch count). */
 int expd_sweep_kernel_launches(const expd_plan* plan);
 

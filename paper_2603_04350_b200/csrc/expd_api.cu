@@ -463,6 +463,33 @@ extern "C" expd_status expd_sweep_stage_ms(expd_plan* p, double* ms_nonlin, doub
   return EXPD_OK;
 }
 
+extern "C" expd_status expd_debug_kernel_ms(expd_plan* p, int which, long nslices, int reps, double* ms) {
+  expd_status s = ready(p);
+  if (s) return s;
+  if (!ms || reps < 1 || nslices < 1 || nslices > p->prob.nt) return fail(p, EXPD_ERR_INVALID_ARG, "debug: bad args");
+  float m = 0.f;
+  if (which <= 2) {
+    CUDA_TRY(p, dst_debug_time(p->g, dst_tables(p), which, p->Uh, p->T1, nslices, p->prob.npoly, p->prob.q, reps, &m,
+                               p->stream));
+  } else {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    TimeArgs a = time_args(p, p->Uh, p->Uh, true);
+    CUDA_TRY(p, launch_time_fused(a, RM_RESID, OUT_UPDATE, p->nl, p->time_grid, p->stream));
+    cudaEventRecord(e0, p->stream);
+    for (int i = 0; i < reps; ++i) CUDA_TRY(p, launch_time_fused(a, RM_RESID, OUT_UPDATE, p->nl, p->time_grid, p->stream));
+    cudaEventRecord(e1, p->stream);
+    cudaEventSynchronize(e1);
+    cudaEventElapsedTime(&m, e0, e1);
+    m /= reps;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  }
+  *ms = m;
+  return EXPD_OK;
+}
+
 extern "C" int expd_sweep_kernel_launches(const expd_plan* p) {
   if (!p) return 0;
   int k = 2;  // fused time pass + norm reduction

@@ -62,6 +62,8 @@ cudaError_t nonlin_slices(const Geom& g, const DstTables& t, const double* uhat,
 cudaError_t nonlin_phys_slices(const Geom& g, const DstTables& t, const double* u, double* nhat, long nslices,
                                int npoly, const double* q, double* scratch, cudaStream_t st);
 size_t dst_scratch_doubles(const Geom& g, long max_slices);
+cudaError_t dst_debug_time(const Geom& g, const DstTables& t, int which, double* a, double* b, long nslices,
+                           int npoly, const double* q, int reps, float* ms, cudaStream_t st);
 int nonlin_chunk_slices(const Geom& g);
 int nonlin_kernel_launches(const Geom& g, long nslices);
 

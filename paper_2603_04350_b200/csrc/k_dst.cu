@@ -17,6 +17,8 @@
 // in registers.  The prefix sum is a per-thread chunk scan + warp-shuffle scan +
 // cross-warp offsets.  Shared layout [position][group] with a 1/16 padding swizzle keeps
 // every 16-byte access conflict-free.  G line pairs share a CTA.
+#include <cstdlib>
+
 #include "expd_internal.h"
 #include "fft_dev.cuh"
 
@@ -33,39 +35,41 @@ __device__ __forceinline__ double poly_eval(const Poly& P, double u) {
   return acc;
 }
 
-// radix plan: NST stages R0 (first), RMID (middle, if NST == 3), RL (last)
+// radix plan: R0 (first stage, fed from the load), up to two middle radices RM1, RM2
+// (1 = absent) and the last radix RL (run on Hermitian partner jobs).
 template <int M> struct DPlan;
-template <> struct DPlan<4>    { static constexpr int NST = 1, R0 = 4,  RMID = 1,  RL = 4; };
-template <> struct DPlan<8>    { static constexpr int NST = 1, R0 = 8,  RMID = 1,  RL = 8; };
-template <> struct DPlan<16>   { static constexpr int NST = 1, R0 = 16, RMID = 1,  RL = 16; };
-template <> struct DPlan<32>   { static constexpr int NST = 2, R0 = 8,  RMID = 1,  RL = 4; };
-template <> struct DPlan<64>   { static constexpr int NST = 3, R0 = 8,  RMID = 2,  RL = 4; };
-template <> struct DPlan<128>  { static constexpr int NST = 2, R0 = 16, RMID = 1,  RL = 8; };
-template <> struct DPlan<256>  { static constexpr int NST = 3, R0 = 16, RMID = 2,  RL = 8; };
-template <> struct DPlan<512>  { static constexpr int NST = 3, R0 = 16, RMID = 4,  RL = 8; };
-template <> struct DPlan<1024> { static constexpr int NST = 3, R0 = 16, RMID = 8,  RL = 8; };
-template <> struct DPlan<2048> { static constexpr int NST = 3, R0 = 16, RMID = 16, RL = 8; };
-template <> struct DPlan<4096> { static constexpr int NST = 3, R0 = 16, RMID = 16, RL = 16; };
+template <> struct DPlan<4>    { static constexpr int NST = 1, R0 = 4,  RM1 = 1,  RM2 = 1, RL = 4; };
+template <> struct DPlan<8>    { static constexpr int NST = 1, R0 = 8,  RM1 = 1,  RM2 = 1, RL = 8; };
+template <> struct DPlan<16>   { static constexpr int NST = 1, R0 = 16, RM1 = 1,  RM2 = 1, RL = 16; };
+template <> struct DPlan<32>   { static constexpr int NST = 2, R0 = 8,  RM1 = 1,  RM2 = 1, RL = 4; };
+template <> struct DPlan<64>   { static constexpr int NST = 3, R0 = 8,  RM1 = 2,  RM2 = 1, RL = 4; };
+template <> struct DPlan<128>  { static constexpr int NST = 2, R0 = 16, RM1 = 1,  RM2 = 1, RL = 8; };
+template <> struct DPlan<256>  { static constexpr int NST = 3, R0 = 16, RM1 = 2,  RM2 = 1, RL = 8; };
+template <> struct DPlan<512>  { static constexpr int NST = 3, R0 = 16, RM1 = 4,  RM2 = 1, RL = 8; };
+template <> struct DPlan<1024> { static constexpr int NST = 3, R0 = 16, RM1 = 8,  RM2 = 1, RL = 8; };
+template <> struct DPlan<2048> { static constexpr int NST = 3, R0 = 16, RM1 = 16, RM2 = 1, RL = 8; };
+template <> struct DPlan<4096> { static constexpr int NST = 3, R0 = 16, RM1 = 16, RM2 = 1, RL = 16; };
 
 template <int M, int G>
 struct DGeo {
   using P = DPlan<M>;
-  static constexpr int NST = P::NST, R0 = P::R0, RMID = P::RMID, RL = P::RL;
+  static constexpr int NST = P::NST, R0 = P::R0, RM1 = P::RM1, RM2 = P::RM2, RL = P::RL;
   static constexpr int T = M / R0;                 // threads per line pair
   static constexpr int THREADS = G * T;
-  static constexpr int NSM = R0;                   // Ns of the middle stage
   static constexpr int NSL = M / RL;               // Ns of the last stage
   static constexpr int L = (M / 2) / T;            // prefix-sum chunk per thread (= R0/2)
-  static constexpr int SW = M + M / 16;            // swizzled positions per group
+  static constexpr int PADP = R0 < 8 ? 8 : R0;     // swizzle period: one pad slot per PADP
+  static constexpr int SW = M + M / PADP + 1;      // swizzled positions per group
   static constexpr int JW = G >= 32 ? 1 : 32 / G;  // threads of one group inside a warp
   static constexpr int NWB = (T + JW - 1) / JW;    // warp blocks per group
 };
 
-__device__ __forceinline__ int swz(int p) { return p + (p >> 4); }
+template <int PADP>
+__device__ __forceinline__ int swz(int p) { return p + p / PADP; }
 
-template <int G>
+template <int G, int PADP>
 __device__ __forceinline__ double2& at(double2* buf, int p, int g) {
-  return buf[swz(p) * G + g];
+  return buf[swz<PADP>(p) * G + g];
 }
 
 // y_i from z_i and its mirror z_{M-i} (sin(pi i/M) = sin(pi (M-i)/M))
@@ -81,22 +85,51 @@ __device__ __forceinline__ void unpack(double2 Zk, double2 Zm, bool k0, double2&
   if (k0) w = make_double2(0.5 * w.x, 0.5 * w.y);
 }
 
+// Shared-memory positions a + r*STRIDE of group g.  When STRIDE is a multiple of the
+// swizzle period the swizzle is linear in r, so every access is base + immediate offset.
+template <int G, int PADP, int STRIDE>
+struct Walk {
+  double2* p0;
+  int a;
+  __device__ __forceinline__ Walk(double2* buf, int a_, int g) : a(a_) {
+    p0 = buf + ((STRIDE % PADP == 0) ? swz<PADP>(a_) * G + g : g);
+  }
+  __device__ __forceinline__ double2& operator[](int r) const {
+    if constexpr (STRIDE % PADP == 0) return p0[r * (STRIDE + STRIDE / PADP) * G];
+    else return p0[swz<PADP>(a + r * STRIDE) * G];
+  }
+};
+
+// t[r] = w^{r b}, r = 0..R-1, from the single table entry w^b by products (binary
+// splitting: at most 2 log2 R roundings deep), instead of R-1 table loads.
+template <int R>
+__device__ __forceinline__ void tw_powers(const double2* __restrict__ tw, int b, double2 (&t)[R]) {
+  t[0] = make_double2(1.0, 0.0);
+  if constexpr (R > 1) t[1] = __ldg(tw + b);
+#pragma unroll
+  for (int r = 2; r < R; ++r) t[r] = (r % 2 == 0) ? cmul(t[r / 2], t[r / 2]) : cmul(t[r - 1], t[1]);
+}
+
 // In-place middle Stockham stage (radix R, NS) on all groups.
 template <int M, int G, int R, int NS>
 __device__ __forceinline__ void mid_stage(double2* buf, const double2* __restrict__ tw) {
   using D = DGeo<M, G>;
   constexpr int JOBS = G * (M / R);
   constexpr int JT = (JOBS + D::THREADS - 1) / D::THREADS;
+  constexpr int TWS = M / (NS * R);  // twiddle index step per k
   double2 v[JT][R];
 #pragma unroll
   for (int jt = 0; jt < JT; ++jt) {
     const int J = threadIdx.x + jt * D::THREADS;
     if (J < JOBS) {
       const int g = J % G, jm = J / G, k = jm % NS;
+      Walk<G, D::PADP, M / R> in(buf, jm, g);
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[jt][r] = at<G>(buf, jm + r * (M / R), g);
+      for (int r = 0; r < R; ++r) v[jt][r] = in[r];
+      double2 t[R];
+      tw_powers<R>(tw, k * TWS, t);
 #pragma unroll
-      for (int r = 1; r < R; ++r) v[jt][r] = cmul(v[jt][r], __ldg(tw + (r * k * (M / (NS * R))) % M));
+      for (int r = 1; r < R; ++r) v[jt][r] = cmul(v[jt][r], t[r]);
       DFT<R, -1>::run(v[jt]);
     }
   }
@@ -106,9 +139,9 @@ __device__ __forceinline__ void mid_stage(double2* buf, const double2* __restric
     const int J = threadIdx.x + jt * D::THREADS;
     if (J < JOBS) {
       const int g = J % G, jm = J / G, k = jm % NS;
-      const int base = (jm / NS) * NS * R + k;
+      Walk<G, D::PADP, NS> out(buf, (jm / NS) * NS * R + k, g);
 #pragma unroll
-      for (int r = 0; r < R; ++r) at<G>(buf, base + r * NS, g) = v[jt][r];
+      for (int r = 0; r < R; ++r) out[r] = v[jt][r];
     }
   }
   __syncthreads();
@@ -122,7 +155,7 @@ template <int M, int G>
 __device__ __forceinline__ void dst_core(double2 (&v)[DGeo<M, G>::R0], double2* buf, double2* wt,
                                          const double2* __restrict__ tw, double2 (&out)[2 * DGeo<M, G>::L]) {
   using D = DGeo<M, G>;
-  constexpr int R0 = D::R0, RL = D::RL, NSL = D::NSL, T = D::T, L = D::L;
+  constexpr int R0 = D::R0, RL = D::RL, NSL = D::NSL, T = D::T, L = D::L, PADP = D::PADP;
   const int g = threadIdx.x % G, j = threadIdx.x / G;
   DFT<R0, -1>::run(v);
   __syncthreads();
@@ -132,14 +165,19 @@ __device__ __forceinline__ void dst_core(double2 (&v)[DGeo<M, G>::R0], double2* 
     for (int k = 0; k < M / 2; ++k) {
       double2 e, w;
       unpack(v[k], v[(M - k) % M], k == 0, e, w);
-      if (k >= 1) at<G>(buf, 2 * k - 1, g) = e;
-      at<G>(buf, 2 * k, g) = w;
+      if (k >= 1) at<G, PADP>(buf, 2 * k - 1, g) = e;
+      at<G, PADP>(buf, 2 * k, g) = w;
     }
   } else {
+    {
+      // R0 (<= 16) consecutive positions from a multiple of R0: the swizzle is linear there
+      double2* o0 = buf + swz<PADP>(j * R0) * G + g;
 #pragma unroll
-    for (int r = 0; r < R0; ++r) at<G>(buf, j * R0 + r, g) = v[r];
+      for (int r = 0; r < R0; ++r) o0[r * G] = v[r];
+    }
     __syncthreads();
-    if constexpr (D::NST == 3) mid_stage<M, G, D::RMID, D::NSM>(buf, tw);
+    if constexpr (D::RM1 > 1) mid_stage<M, G, D::RM1, R0>(buf, tw);
+    if constexpr (D::RM2 > 1) mid_stage<M, G, D::RM2, R0 * D::RM1>(buf, tw);
     // last stage on Hermitian partner jobs, then the unpack
     constexpr int PJOBS = G * (NSL / 2);
     constexpr int PJT = (PJOBS + D::THREADS - 1) / D::THREADS;
@@ -150,15 +188,20 @@ __device__ __forceinline__ void dst_core(double2 (&v)[DGeo<M, G>::R0], double2* 
       if (PJ < PJOBS) {
         const int gg = PJ % G, pj = PJ / G;
         const int ja = pj, jb = pj == 0 ? NSL / 2 : NSL - pj;
+        Walk<G, PADP, NSL> ia(buf, ja, gg), ib(buf, jb, gg);
 #pragma unroll
         for (int r = 0; r < RL; ++r) {
-          va[pt][r] = at<G>(buf, ja + r * NSL, gg);
-          vb[pt][r] = at<G>(buf, jb + r * NSL, gg);
+          va[pt][r] = ia[r];
+          vb[pt][r] = ib[r];
         }
+        {
+          double2 t[RL];
+          tw_powers<RL>(tw, ja, t);
 #pragma unroll
-        for (int r = 1; r < RL; ++r) {
-          va[pt][r] = cmul(va[pt][r], __ldg(tw + (r * ja) % M));
-          vb[pt][r] = cmul(vb[pt][r], __ldg(tw + (r * jb) % M));
+          for (int r = 1; r < RL; ++r) va[pt][r] = cmul(va[pt][r], t[r]);
+          tw_powers<RL>(tw, jb, t);
+#pragma unroll
+          for (int r = 1; r < RL; ++r) vb[pt][r] = cmul(vb[pt][r], t[r]);
         }
         DFT<RL, -1>::run(va[pt]);
         DFT<RL, -1>::run(vb[pt]);
@@ -171,29 +214,39 @@ __device__ __forceinline__ void dst_core(double2 (&v)[DGeo<M, G>::R0], double2* 
       if (PJ < PJOBS) {
         const int gg = PJ % G, pj = PJ / G;
         const int ja = pj, jb = pj == 0 ? NSL / 2 : NSL - pj;
+        // positions 2k-1 (e_k) and 2k (w_k) for k = ja + NSL r and k = jb + NSL r
+        Walk<G, PADP, 2 * NSL> ea(buf, 2 * ja - 1 < 0 ? 0 : 2 * ja - 1, gg), wa(buf, 2 * ja, gg);
+        Walk<G, PADP, 2 * NSL> eb(buf, 2 * jb - 1, gg), wb(buf, 2 * jb, gg);
 #pragma unroll
         for (int r = 0; r < RL / 2; ++r) {
           double2 e, w;
-          const int ka = ja + NSL * r, kb = jb + NSL * r;
+          const int ka = ja + NSL * r;
           unpack(va[pt][r], pj == 0 ? va[pt][(RL - r) % RL] : vb[pt][RL - 1 - r], ka == 0, e, w);
-          if (ka >= 1) at<G>(buf, 2 * ka - 1, gg) = e;
-          at<G>(buf, 2 * ka, gg) = w;
+          if (ka >= 1) {
+            if (ja >= 1) ea[r] = e;
+            else at<G, PADP>(buf, 2 * ka - 1, gg) = e;
+          }
+          wa[r] = w;
           unpack(vb[pt][r], pj == 0 ? vb[pt][RL - 1 - r] : va[pt][RL - 1 - r], false, e, w);
-          at<G>(buf, 2 * kb - 1, gg) = e;
-          at<G>(buf, 2 * kb, gg) = w;
+          eb[r] = e;
+          wb[r] = w;
         }
       }
     }
   }
   __syncthreads();
-  // prefix sum of w_k over k: chunk k in [c L, c L + L), c = j
+  // prefix sum of w_k over k: chunk k in [c L, c L + L), c = j  (positions 2cL-1 .. 2cL+2L-2)
   double2 tot = make_double2(0.0, 0.0);
+  {
+    // positions 2jL .. 2jL+2L-1 (2L <= 16, 2jL a multiple of 2L): linear swizzle
+    const double2* P = buf + swz<PADP>(2 * j * L) * G + g;
 #pragma unroll
-  for (int l = 0; l < L; ++l) {
-    const int k = j * L + l;
-    if (k >= 1) out[2 * l] = at<G>(buf, 2 * k - 1, g);
-    tot = cadd(tot, at<G>(buf, 2 * k, g));
-    out[2 * l + 1] = tot;
+    for (int l = 0; l < L; ++l) {
+      if (l >= 1) out[2 * l] = P[(2 * l - 1) * G];
+      tot = cadd(tot, P[(2 * l) * G]);
+      out[2 * l + 1] = tot;
+    }
+    out[0] = at<G, PADP>(buf, j > 0 ? 2 * j * L - 1 : 0, g);  // overwritten for j == 0 below
   }
   // inclusive scan of chunk totals across the group's threads (lanes g + G*j')
   double2 inc = tot;
@@ -217,171 +270,160 @@ __device__ __forceinline__ void dst_core(double2 (&v)[DGeo<M, G>::R0], double2* 
   }
 #pragma unroll
   for (int l = 0; l < L; ++l) out[2 * l + 1] = cadd(out[2 * l + 1], off);
-  if (j == 0) out[0] = make_double2(0.0, 0.0);  // position -1 does not exist
-}
-
-// asynchronous global -> shared copies (LDGSTS): every load of a work item is in flight
-// at once, without holding registers, before the item's math starts
-__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
-  unsigned s = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem));
-}
-__device__ __forceinline__ void cp_async_wait_all() {
-  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+  out[0] = j == 0 ? make_double2(0.0, 0.0) : out[0];  // position -1 does not exist
 }
 
 // ---------------------------------------------------------------------------------------
 // x-axis transform of row pairs.  Row r of slice s at in + s*in_slice + r*in_rs (length
 // n = M-1); output rows likewise (out_rs == M: padded spectral row, pad written as 0).
 // MODE 0: V; 1: V N(in) (N applied on load, physical input); 2: V N(V in) (dim 1).
+// Each thread loads only its own stage-0 elements (coalesced), parks them in shared
+// memory for its mirror partner, and stores its outputs straight from registers.
 // ---------------------------------------------------------------------------------------
 template <int M, int G, int MODE>
-__global__ void __launch_bounds__(DGeo<M, G>::THREADS) k_rows(const double* __restrict__ in, long in_slice,
-                                                               int in_rs, double* __restrict__ out, long out_slice,
-                                                               int out_rs, int rows_per_slice,
-                                                               const double2* __restrict__ tw,
-                                                               const double* __restrict__ sinp, Poly poly) {
+__global__ void __launch_bounds__(DGeo<M, G>::THREADS, (DGeo<M, G>::THREADS <= 512 ? 512 / DGeo<M, G>::THREADS : 1))
+    k_rows(const double* __restrict__ in, long in_slice, int in_rs, double* __restrict__ out, long out_slice,
+           int out_rs, int rows_per_slice, const double2* __restrict__ tw, const double* __restrict__ sinp,
+           Poly poly) {
   using D = DGeo<M, G>;
-  constexpr int R0 = D::R0, T = D::T, L = D::L, THREADS = D::THREADS;
-  constexpr int n = M - 1;
+  constexpr int R0 = D::R0, T = D::T, L = D::L, PADP = D::PADP;
   extern __shared__ double2 dsm[];
-  double2* buf = dsm;                // [SW][G]   (aliases the raw rows below)
-  double2* wt = dsm + D::SW * G;     // [NWB][G]
-  double* raw = reinterpret_cast<double*>(dsm);  // [2G][M] raw rows
+  double2* buf = dsm;             // [SW][G] swizzled work buffer; also raw [M][G]
+  double2* wt = dsm + D::SW * G;  // [NWB][G]
   const int g = threadIdx.x % G, j = threadIdx.x / G;
   const long slice = blockIdx.y;
-  const int row0 = 2 * blockIdx.x * G;  // first row of the CTA
-  const double* inS = in + slice * in_slice;
-  // 1. all loads of the item in flight at once
-  for (int idx = threadIdx.x; idx < 2 * G * n; idx += THREADS) {
-    const int rr = idx / n, pos = idx % n;
-    if (row0 + rr < rows_per_slice) cp_async8(raw + rr * M + pos, inS + (long)(row0 + rr) * in_rs + pos);
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  const bool has_a = row0 + 2 * g < rows_per_slice, has_b = row0 + 2 * g + 1 < rows_per_slice;
-  auto ld = [&](int i) -> double2 {  // z_i, i in [1, M-1]
-    double a = has_a ? raw[(2 * g) * M + i - 1] : 0.0, b = has_b ? raw[(2 * g + 1) * M + i - 1] : 0.0;
-    if constexpr (MODE == 1) {
-      a = has_a ? poly_eval(poly, a) : 0.0;
-      b = has_b ? poly_eval(poly, b) : 0.0;
-    }
-    return make_double2(a, b);
-  };
-  double2 v[R0];
-#pragma unroll
-  for (int r = 0; r < R0; ++r) {
-    const int i = j + T * r;
-    v[r] = i == 0 ? make_double2(0.0, 0.0) : preprocess(ld(i), ld(M - i), __ldg(sinp + i));
-  }
-  double2 o[2 * L];
-  dst_core<M, G>(v, buf, wt, tw, o);
+  const int ra = 2 * (blockIdx.x * G + g), rb = ra + 1;
+  const bool has_a = ra < rows_per_slice, has_b = rb < rows_per_slice;
+  const double* ia = in + slice * in_slice + (long)ra * in_rs;
+  const double* ib = in + slice * in_slice + (long)rb * in_rs;
   const double scale = sqrt(2.0 / (double)M);
-  if constexpr (MODE == 2) {
-    // physical values u = scale F; N(u) becomes the input of the second transform
+  double2 o[2 * L];
 #pragma unroll
-    for (int q = 0; q < 2 * L; ++q) {
-      const int p = 2 * j * L - 1 + q;
-      if (p >= 0) at<G>(buf, p, g) = make_double2(poly_eval(poly, scale * o[q].x), poly_eval(poly, scale * o[q].y));
-    }
-    __syncthreads();
+  for (int pass = 0; pass < (MODE == 2 ? 2 : 1); ++pass) {
+    double2 v[R0];
+    if (pass == 0) {
+      double2 z[R0];
 #pragma unroll
-    for (int r = 0; r < R0; ++r) {
-      const int i = j + T * r;
-      v[r] = i == 0 ? make_double2(0.0, 0.0)
-                    : preprocess(at<G>(buf, i - 1, g), at<G>(buf, M - i - 1, g), __ldg(sinp + i));
+      for (int r = 0; r < R0; ++r) {
+        const int i = j + T * r;
+        double a = 0.0, b = 0.0;
+        if (i >= 1) {
+          if (has_a) a = __ldg(ia + i - 1);
+          if (has_b) b = __ldg(ib + i - 1);
+          if constexpr (MODE == 1) {
+            a = has_a ? poly_eval(poly, a) : 0.0;
+            b = has_b ? poly_eval(poly, b) : 0.0;
+          }
+        }
+        z[r] = make_double2(a, b);
+      }
+#pragma unroll
+      for (int r = 0; r < R0; ++r) dsm[(j + T * r) * G + g] = z[r];  // raw [M][G]
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < R0; ++r) {
+        const int i = j + T * r;
+        v[r] = i == 0 ? make_double2(0.0, 0.0) : preprocess(z[r], dsm[(M - i) * G + g], __ldg(sinp + i));
+      }
+    } else {
+      // N(u) of the first transform sits in buf at position i-1 (grid index i)
+#pragma unroll
+      for (int r = 0; r < R0; ++r) {
+        const int i = j + T * r;
+        v[r] = i == 0 ? make_double2(0.0, 0.0)
+                      : preprocess(at<G, PADP>(buf, i - 1, g), at<G, PADP>(buf, M - i - 1, g), __ldg(sinp + i));
+      }
     }
     dst_core<M, G>(v, buf, wt, tw, o);
+    if (MODE == 2 && pass == 0) {
+#pragma unroll
+      for (int q = 0; q < 2 * L; ++q) {
+        const int p = 2 * j * L - 1 + q;
+        if (p >= 0) at<G, PADP>(buf, p, g) = make_double2(poly_eval(poly, scale * o[q].x), poly_eval(poly, scale * o[q].y));
+      }
+      __syncthreads();
+    }
   }
-  // 2. outputs through shared memory, then coalesced row stores
+  double* oa = out + slice * out_slice + (long)ra * out_rs;
+  double* ob = out + slice * out_slice + (long)rb * out_rs;
 #pragma unroll
   for (int q = 0; q < 2 * L; ++q) {
     const int p = 2 * j * L - 1 + q;
-    if (p >= 0) at<G>(buf, p, g) = make_double2(scale * o[q].x, scale * o[q].y);
-  }
-  __syncthreads();
-  double* outS = out + slice * out_slice;
-  for (int idx = threadIdx.x; idx < 2 * G * out_rs; idx += THREADS) {
-    const int rr = idx / out_rs, pos = idx % out_rs;
-    const int row = row0 + rr;
-    if (row < rows_per_slice) {
-      double val = 0.0;  // pad position of a spectral row stays 0
-      if (pos < n) {
-        const double2 vv = at<G>(buf, pos, rr >> 1);
-        val = (rr & 1) ? vv.y : vv.x;
-      }
-      outS[(long)row * out_rs + pos] = val;
+    if (p >= 0) {
+      if (has_a) oa[p] = scale * o[q].x;
+      if (has_b) ob[p] = scale * o[q].y;
     }
+  }
+  if (out_rs == M && j == T - 1) {  // pad position of a spectral row stays 0
+    if (has_a) oa[M - 1] = 0.0;
+    if (has_b) ob[M - 1] = 0.0;
   }
 }
 
 // ---------------------------------------------------------------------------------------
 // strided-axis transform of column pairs in the padded spectral layout: line pair
-// (o, cp): base = o*outer_stride + 2*cp, element i-1 at base + (i-1)*stride.
+// (o, cp): base = o*outer_stride + 2*cp, element i-1 at base + (i-1)*stride (one double2).
 // NL: transform, N(u) pointwise, transform (the fused stage-3 visit).
 // ---------------------------------------------------------------------------------------
 template <int M, int G, bool NL>
-__global__ void __launch_bounds__(DGeo<M, G>::THREADS) k_cols(const double* in, long in_slice, double* out,
-                                                               long out_slice, long stride, long outer_stride,
-                                                               const double2* __restrict__ tw,
-                                                               const double* __restrict__ sinp, Poly poly) {
+__global__ void __launch_bounds__(DGeo<M, G>::THREADS, (DGeo<M, G>::THREADS <= 512 ? 512 / DGeo<M, G>::THREADS : 1))
+    k_cols(const double* in, long in_slice, double* out, long out_slice, long stride, long outer_stride,
+           const double2* __restrict__ tw, const double* __restrict__ sinp, Poly poly) {
   using D = DGeo<M, G>;
-  constexpr int R0 = D::R0, T = D::T, L = D::L, THREADS = D::THREADS;
-  constexpr int n = M - 1;
+  constexpr int R0 = D::R0, T = D::T, L = D::L, PADP = D::PADP;
   constexpr int GROUPS = (M / 2) / G;  // column-pair groups per outer index
   extern __shared__ double2 dsm[];
-  double2* buf = dsm;                // [SW][G] (aliases raw [n][G])
-  double2* wt = dsm + D::SW * G;     // [NWB][G]
+  double2* buf = dsm;             // [SW][G] (also raw [M][G])
+  double2* wt = dsm + D::SW * G;  // [NWB][G]
+  const int g = threadIdx.x % G, j = threadIdx.x / G;
   const long slice = blockIdx.y;
   const long o = blockIdx.x / GROUPS;
-  const int cp0 = (blockIdx.x % GROUPS) * G;
-  const double2* ib = reinterpret_cast<const double2*>(in + slice * in_slice + o * outer_stride + 2 * cp0);
-  double2* ob = reinterpret_cast<double2*>(out + slice * out_slice + o * outer_stride + 2 * cp0);
+  const int cp = (blockIdx.x % GROUPS) * G + g;
   const long st2 = stride / 2;  // in double2 units (stride is even: padded rows)
-  for (int idx = threadIdx.x; idx < n * G; idx += THREADS) {
-    const int pos = idx / G, gg = idx % G;
-    cp_async16(dsm + idx, ib + (long)pos * st2 + gg);
-  }
-  cp_async_wait_all();
-  __syncthreads();
-  const int g = threadIdx.x % G, j = threadIdx.x / G;
-  double2 v[R0];
-#pragma unroll
-  for (int r = 0; r < R0; ++r) {
-    const int i = j + T * r;
-    v[r] = i == 0 ? make_double2(0.0, 0.0) : preprocess(dsm[(i - 1) * G + g], dsm[(M - i - 1) * G + g], __ldg(sinp + i));
-  }
-  double2 oo[2 * L];
-  dst_core<M, G>(v, buf, wt, tw, oo);
+  const double2* ib = reinterpret_cast<const double2*>(in + slice * in_slice + o * outer_stride) + cp;
+  double2* ob = reinterpret_cast<double2*>(out + slice * out_slice + o * outer_stride) + cp;
   const double scale = sqrt(2.0 / (double)M);
-  if constexpr (NL) {
+  double2 oo[2 * L];
 #pragma unroll
-    for (int q = 0; q < 2 * L; ++q) {
-      const int p = 2 * j * L - 1 + q;
-      if (p >= 0) at<G>(buf, p, g) = make_double2(poly_eval(poly, scale * oo[q].x), poly_eval(poly, scale * oo[q].y));
-    }
-    __syncthreads();
+  for (int pass = 0; pass < (NL ? 2 : 1); ++pass) {
+    double2 v[R0];
+    if (pass == 0) {
+      double2 z[R0];
 #pragma unroll
-    for (int r = 0; r < R0; ++r) {
-      const int i = j + T * r;
-      v[r] = i == 0 ? make_double2(0.0, 0.0)
-                    : preprocess(at<G>(buf, i - 1, g), at<G>(buf, M - i - 1, g), __ldg(sinp + i));
+      for (int r = 0; r < R0; ++r) {
+        const int i = j + T * r;
+        z[r] = i >= 1 ? ib[(long)(i - 1) * st2] : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int r = 0; r < R0; ++r) dsm[(j + T * r) * G + g] = z[r];  // raw [M][G]
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < R0; ++r) {
+        const int i = j + T * r;
+        v[r] = i == 0 ? make_double2(0.0, 0.0) : preprocess(z[r], dsm[(M - i) * G + g], __ldg(sinp + i));
+      }
+    } else {
+#pragma unroll
+      for (int r = 0; r < R0; ++r) {
+        const int i = j + T * r;
+        v[r] = i == 0 ? make_double2(0.0, 0.0)
+                      : preprocess(at<G, PADP>(buf, i - 1, g), at<G, PADP>(buf, M - i - 1, g), __ldg(sinp + i));
+      }
     }
     dst_core<M, G>(v, buf, wt, tw, oo);
+    if (NL && pass == 0) {
+#pragma unroll
+      for (int q = 0; q < 2 * L; ++q) {
+        const int p = 2 * j * L - 1 + q;
+        if (p >= 0) at<G, PADP>(buf, p, g) = make_double2(poly_eval(poly, scale * oo[q].x), poly_eval(poly, scale * oo[q].y));
+      }
+      __syncthreads();
+    }
   }
 #pragma unroll
   for (int q = 0; q < 2 * L; ++q) {
     const int p = 2 * j * L - 1 + q;
-    if (p >= 0) at<G>(buf, p, g) = make_double2(scale * oo[q].x, scale * oo[q].y);
-  }
-  __syncthreads();
-  for (int idx = threadIdx.x; idx < n * G; idx += THREADS) {
-    const int pos = idx / G, gg = idx % G;
-    ob[(long)pos * st2 + gg] = at<G>(buf, pos, gg);
+    if (p >= 0) ob[(long)p * st2] = make_double2(scale * oo[q].x, scale * oo[q].y);
   }
 }
 
@@ -389,7 +431,7 @@ __global__ void __launch_bounds__(DGeo<M, G>::THREADS) k_cols(const double* in, 
 // host-side dispatch
 // ---------------------------------------------------------------------------------------
 template <int M> struct RowG { static constexpr int T = M / DPlan<M>::R0; static constexpr int G = T >= 128 ? 1 : 128 / T; };
-template <int M> struct ColG { static constexpr int T = M / DPlan<M>::R0; static constexpr int G0 = T >= 64 ? 2 : 128 / T; static constexpr int G = G0 > M / 2 ? M / 2 : G0; };
+template <int M> struct ColG { static constexpr int T = M / DPlan<M>::R0; static constexpr int G0 = T >= 128 ? 2 : 256 / T; static constexpr int G = G0 > M / 2 ? M / 2 : G0; };
 
 struct RowsOp {
   const double* in; long in_slice; int in_rs; double* out; long out_slice; int out_rs; int rows; long nslices;
@@ -433,9 +475,8 @@ static cudaError_t run_rows(const RowsOp& o, const DstTables& t, const Poly& P, 
   if (o.nlmid) return rows_launch<M, 2>(o, t, P, st);
   return rows_launch<M, 0>(o, t, P, st);
 }
-template <int M>
-static cudaError_t run_cols(const ColsOp& o, const DstTables& t, const Poly& P, cudaStream_t st) {
-  constexpr int G = ColG<M>::G;
+template <int M, int G>
+static cudaError_t run_cols_g(const ColsOp& o, const DstTables& t, const Poly& P, cudaStream_t st) {
   dim3 grid((unsigned)(o.nouter * ((M / 2) / G)), (unsigned)o.nslices);
   const size_t sm = dst_smem<M, G>();
   cudaError_t e;
@@ -450,6 +491,19 @@ static cudaError_t run_cols(const ColsOp& o, const DstTables& t, const Poly& P, 
                                                                 o.outer_stride, t.tw, t.sinp, P);
   }
   return cudaGetLastError();
+}
+
+template <int M>
+static cudaError_t run_cols(const ColsOp& o, const DstTables& t, const Poly& P, cudaStream_t st) {
+  if constexpr (M == 2048) {
+    static int g1 = -1;  // tuning switch: EXPD_COLG=1 selects one column pair per CTA
+    if (g1 < 0) {
+      const char* e = getenv("EXPD_COLG");
+      g1 = (e && e[0] == '1') ? 1 : 0;
+    }
+    if (g1) return run_cols_g<M, 1>(o, t, P, st);
+  }
+  return run_cols_g<M, ColG<M>::G>(o, t, P, st);
 }
 
 static cudaError_t rows(int M, const RowsOp& o, const DstTables& t, const Poly& P, cudaStream_t st) {
@@ -602,6 +656,34 @@ cudaError_t nonlin_phys_slices(const Geom& g, const DstTables& t, const double* 
   CK(rows(g.M, r, t, P, st));
   for (int ax = 1; ax < g.dim; ++ax) CK(cols(g.M, col_op(g, ax, nhat, nhat, nslices, false), t, P, st));
   return cudaSuccess;
+}
+
+// Diagnostics: time one kernel family on spectral slices of the workspace (which: 0 row
+// pass, 1 strided pass, 2 fused strided N pass), reps launches, returns ms per launch.
+cudaError_t dst_debug_time(const Geom& g, const DstTables& t, int which, double* a, double* b, long nslices,
+                           int npoly, const double* q, int reps, float* ms, cudaStream_t st) {
+  Poly P = make_poly(npoly, q);
+  const int rows_ps = (int)(g.N / g.n);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  auto one = [&]() -> cudaError_t {
+    if (which == 0) {
+      RowsOp r{a, g.npad, g.M, b, g.npad, g.M, rows_ps, nslices, false, false};
+      return rows(g.M, r, t, P, st);
+    }
+    return cols(g.M, col_op(g, g.dim - 1, a, b, nslices, which == 2), t, P, st);
+  };
+  CK(one());
+  cudaEventRecord(e0, st);
+  for (int i = 0; i < reps; ++i) CK(one());
+  cudaEventRecord(e1, st);
+  cudaEventSynchronize(e1);
+  cudaEventElapsedTime(ms, e0, e1);
+  *ms /= reps;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return cudaGetLastError();
 }
 
 size_t dst_scratch_doubles(const Geom& g, long max_slices) { return (size_t)g.npad * (size_t)max_slices; }

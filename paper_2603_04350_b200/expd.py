@@ -47,6 +47,7 @@ EXPORTS = [
     "expd_dst",
     "expd_set_profiling",
     "expd_sweep_stage_ms",
+    "expd_debug_kernel_ms",
 ]
 
 
@@ -117,6 +118,7 @@ def load_library(path: str = LIB_PATH):
         "expd_dst": (C.c_int, [vp, vp, vp, C.c_long]),
         "expd_set_profiling": (C.c_int, [vp, C.c_int]),
         "expd_sweep_stage_ms": (C.c_int, [vp, dp, dp]),
+        "expd_debug_kernel_ms": (C.c_int, [vp, C.c_int, C.c_long, C.c_int, dp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -294,6 +296,11 @@ class Plan:
         a, b = C.c_double(), C.c_double()
         self._check(self.lib.expd_sweep_stage_ms(self.handle, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    def debug_kernel_ms(self, which: int, nslices: int = 1, reps: int = 10) -> float:
+        v = C.c_double()
+        self._check(self.lib.expd_debug_kernel_ms(self.handle, which, nslices, reps, C.byref(v)))
+        return v.value
 
     def sweep_kernel_launches(self) -> int:
         return int(self.lib.expd_sweep_kernel_launches(self.handle))
