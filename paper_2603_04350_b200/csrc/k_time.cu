@@ -19,6 +19,8 @@
 // in registers, then runs the inverse DFT-Q; phase C inverts the DFT-P and applies the
 // update.  Shared memory carries the two transposes; the divisor's 1/Nt (both unitary
 // 1/sqrt(Nt) factors) is folded into the reciprocal.
+#include <cstdlib>
+
 #include "expd_internal.h"
 #include "fft_dev.cuh"
 
@@ -29,6 +31,9 @@ struct TimeCfg;
 // Radix plan of the length-NT time FFT (Stockham stages R_0 .. R_{L-1}); the last stage
 // has a small radix so that a thread can own a frequency set together with its Hermitian
 // partner set; TPS = NT / R_0 threads per mode pair; S = 256 / TPS pairs per CTA.
+#ifndef EXPD_K1_THREADS
+#define EXPD_K1_THREADS 256
+#endif
 template <int NT> struct TimeCfg;
 template <> struct TimeCfg<4>   { static constexpr int L = 1, R0 = 4, R1 = 1, R2 = 1; };
 template <> struct TimeCfg<8>   { static constexpr int L = 1, R0 = 8, R1 = 1, R2 = 1; };
@@ -43,7 +48,7 @@ struct TimeGeo {
   static constexpr int L = C::L, R0 = C::R0;
   static constexpr int RL = L == 1 ? C::R0 : (L == 2 ? C::R1 : C::R2);  // last forward radix
   static constexpr int TPS = NT / R0;                                    // threads per pair
-  static constexpr int THREADS = 256;
+  static constexpr int THREADS = EXPD_K1_THREADS;
   static constexpr int S = THREADS / TPS;                                // pairs per CTA
   static constexpr int NSL = NT / RL;                                    // Ns of the last stage
 };
@@ -111,7 +116,7 @@ __device__ __forceinline__ void tstage(const double2* __restrict__ in, double2* 
     for (int r = 0; r < R; ++r) v[r] = in[(j + r * (NT / R)) * S + s];
 #pragma unroll
     for (int r = 1; r < R; ++r) {
-      const double2 w = stw[(r * k * (NT / (NS * R))) % NT];
+      const double2 w = stw[(r * k * (NT / (NS * R))) & (NT - 1)];
       v[r] = DIR > 0 ? cmul(v[r], w) : cmulc(v[r], w);
     }
     DFT<R, DIR>::run(v);
@@ -146,8 +151,14 @@ __device__ __forceinline__ void pair_divide(double2 (&va)[RL], double2 (&vb)[RL]
   }
 }
 
+#ifndef EXPD_K1_MINB
+#define EXPD_K1_MINB 2
+#endif
+#ifndef EXPD_K1_REREAD
+#define EXPD_K1_REREAD 0
+#endif
 template <int NT, int RM, int OUTM, int NL>
-__global__ void __launch_bounds__(256, 2) k_time_fused(const TimeArgs a) {
+__global__ void __launch_bounds__(EXPD_K1_THREADS, EXPD_K1_MINB) k_time_fused(const TimeArgs a) {
   using G = TimeGeo<NT>;
   using C = TimeCfg<NT>;
   constexpr int L = G::L, R0 = G::R0, RL = G::RL, TPS = G::TPS, S = G::S, THREADS = G::THREADS;
@@ -181,7 +192,7 @@ __global__ void __launch_bounds__(256, 2) k_time_fused(const TimeArgs a) {
 
     // ---- phase A: stage 1 residual (+ ||r||^2), Gamma_alpha, forward stage 0 ----------
     double2 y[R0];
-    double2 xv[(OUTM == OUT_UPDATE) ? R0 : 1];
+    double2 xv[(OUTM == OUT_UPDATE && !EXPD_K1_REREAD) ? R0 : 1];
     double2 Ej = make_double2(0.0, 0.0), c1 = Ej, c2 = Ej;
     if (valid && RM != RM_INPUT) Ej = ld2(a.E + base);
     if (valid && NL >= 1) c1 = ld2(a.C1 + base);
@@ -216,7 +227,7 @@ __global__ void __launch_bounds__(256, 2) k_time_fused(const TimeArgs a) {
         }
       }
       nrm = fma(rr.x, rr.x, fma(rr.y, rr.y, nrm));
-      if constexpr (OUTM == OUT_UPDATE) xv[r] = cur;
+      if constexpr (OUTM == OUT_UPDATE && !EXPD_K1_REREAD) xv[r] = cur;
       y[r] = cscale(rr, sg[t]);
     }
     DFT<R0, +1>::run(y);
@@ -253,8 +264,8 @@ __global__ void __launch_bounds__(256, 2) k_time_fused(const TimeArgs a) {
         }
 #pragma unroll
         for (int r = 1; r < RL; ++r) {
-          va[r] = cmul(va[r], stw[(r * ja) % NT]);
-          vb[r] = cmul(vb[r], stw[(r * jb) % NT]);
+          va[r] = cmul(va[r], stw[(r * ja) & (NT - 1)]);
+          vb[r] = cmul(vb[r], stw[(r * jb) & (NT - 1)]);
         }
         DFT<RL, +1>::run(va);
         DFT<RL, +1>::run(vb);
@@ -278,7 +289,7 @@ __global__ void __launch_bounds__(256, 2) k_time_fused(const TimeArgs a) {
 #pragma unroll
       for (int r = 0; r < R0; ++r) y[r] = cin[(j + r * TPS) * S + s];
 #pragma unroll
-      for (int r = 1; r < R0; ++r) y[r] = cmulc(y[r], stw[(r * j) % NT]);
+      for (int r = 1; r < R0; ++r) y[r] = cmulc(y[r], stw[(r * j) & (NT - 1)]);
       DFT<R0, -1>::run(y);
     }
     // ---- phase C: Gamma_alpha^{-1}, update, store (times j + r TPS) -------------------
@@ -287,7 +298,10 @@ __global__ void __launch_bounds__(256, 2) k_time_fused(const TimeArgs a) {
       for (int r = 0; r < R0; ++r) {
         const int t = j + r * TPS;
         double2 sv = cscale(y[r], sgi[t]);
-        if constexpr (OUTM == OUT_UPDATE) sv = cadd(xv[r], sv);
+        if constexpr (OUTM == OUT_UPDATE) {
+          if constexpr (EXPD_K1_REREAD) sv = cadd(ld2(a.X + (long)t * npad + base), sv);  // L2 hit
+          else sv = cadd(xv[r], sv);
+        }
         st2(a.Y + (long)t * npad + base, sv);
       }
     }
@@ -307,14 +321,248 @@ __global__ void __launch_bounds__(256, 2) k_time_fused(const TimeArgs a) {
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// K1, software-pipelined: one persistent CTA per SM; while tile i is transformed, the
+// U-hat / N-hat time columns (and the per-mode tables) of tile i+1 stream into the other
+// half of a double-buffered shared-memory stage with cp.async, so phase A never waits on
+// HBM latency.  Phase C takes u_t for the update from the staged tile, not registers.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem, bool valid) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = valid ? 16 : 0;  // zero-fill past the last mode pair
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <int NT, int RM, int NL>
+struct PipeLayout {
+  using G = TimeGeo<NT>;
+  static constexpr int S = G::S;
+  static constexpr int TILE = NT * S;                   // double2 per staged array
+  static constexpr int NARR = (RM == RM_INPUT ? 1 : 1) + (NL ? 1 : 0);  // X (+ N-hat)
+  static constexpr int AUX = 4 * S;                     // E, C1, C2, u0-hat per pair
+  static constexpr int STAGE = NARR * TILE + AUX;       // double2 per pipeline stage
+  static constexpr size_t BYTES = sizeof(double2) * (2 * STAGE + 2 * TILE + NT) + sizeof(double) * 2 * NT;
+};
+
+template <int NT, int RM, int NL>
+__device__ __forceinline__ void pipe_issue(const TimeArgs& a, long tile, double2* stage) {
+  using PL = PipeLayout<NT, RM, NL>;
+  constexpr int S = PL::S, TILE = PL::TILE, THREADS = TimeGeo<NT>::THREADS;
+  const long npad = a.npad;
+  for (int c = threadIdx.x; c < TILE; c += THREADS) {
+    const int t = c / S, s = c % S;
+    const long pair = tile * S + s;
+    const bool ok = pair < a.npairs;
+    const long off = (long)t * npad + 2 * (ok ? pair : 0);
+    cpa16(stage + c, a.X + off, ok);
+    if constexpr (NL) cpa16(stage + TILE + c, a.Nh + off, ok);
+  }
+  if (threadIdx.x < S) {
+    const int s = threadIdx.x;
+    const long pair = tile * S + s;
+    const bool ok = pair < a.npairs;
+    const long off = 2 * (ok ? pair : 0);
+    double2* aux = stage + PL::NARR * TILE;
+    cpa16(aux + s, a.E + off, ok);
+    if constexpr (NL >= 1) cpa16(aux + S + s, a.C1 + off, ok);
+    if constexpr (NL == 2) cpa16(aux + 2 * S + s, a.C2 + off, ok);
+    if constexpr (RM == RM_RESID) cpa16(aux + 3 * S + s, a.u0h + off, ok);
+  }
+  cpa_commit();
+}
+
+template <int NT, int RM, int OUTM, int NL>
+__global__ void __launch_bounds__(EXPD_K1_THREADS, 256 / EXPD_K1_THREADS) k_time_pipe(const TimeArgs a) {
+  using G = TimeGeo<NT>;
+  using C = TimeCfg<NT>;
+  using PL = PipeLayout<NT, RM, NL>;
+  constexpr int L = G::L, R0 = G::R0, RL = G::RL, TPS = G::TPS, S = G::S, THREADS = G::THREADS;
+  constexpr int NSL = G::NSL, TILE = PL::TILE;
+  static_assert(L > 1, "pipelined kernel needs a multi-stage FFT");
+  extern __shared__ double2 smem[];
+  double2* buf0 = smem + 2 * PL::STAGE;  // [NT][S]
+  double2* buf1 = buf0 + TILE;
+  double2* stw = buf1 + TILE;            // [NT] e^{+2 pi i q/NT}
+  double* sg = reinterpret_cast<double*>(stw + NT);
+  double* sgi = sg + NT;
+
+  const int tid = threadIdx.x;
+  for (int i = tid; i < NT; i += THREADS) {
+    stw[i] = a.tw[i];
+    sg[i] = a.g[i];
+    sgi[i] = a.ginv[i];
+  }
+  const long npad = a.npad;
+  const long ntiles = (a.npairs + S - 1) / S;
+  const double hin = a.half_inv_nt;
+  double nrm = 0.0;
+  const int s = tid % S;
+  const int j = tid / S;
+
+  long tile = blockIdx.x;
+  int cur = 0;
+  if (tile < ntiles) pipe_issue<NT, RM, NL>(a, tile, smem);
+  for (; tile < ntiles; tile += gridDim.x, cur ^= 1) {
+    const long next = tile + gridDim.x;
+    if (next < ntiles) {
+      pipe_issue<NT, RM, NL>(a, next, smem + (cur ^ 1) * PL::STAGE);
+      cpa_wait<1>();
+    } else {
+      cpa_wait<0>();
+    }
+    __syncthreads();
+    const double2* X = smem + cur * PL::STAGE;
+    const double2* NH = X + TILE;
+    const double2* aux = X + PL::NARR * TILE;
+    const long pair = tile * S + s;
+    const bool valid = pair < a.npairs;
+    const long base = 2 * pair;
+
+    // ---- phase A: residual (+ ||r||^2), Gamma_alpha, forward stage 0 (times j + r TPS) ---
+    double2 y[R0];
+    const double2 Ej = aux[s];
+    const double2 c1 = NL >= 1 ? aux[S + s] : make_double2(0.0, 0.0);
+    const double2 c2 = NL == 2 ? aux[2 * S + s] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int r = 0; r < R0; ++r) {
+      const int t = j + r * TPS;
+      const double2 xc = X[t * S + s];
+      double2 rr;
+      if constexpr (RM == RM_INPUT) {
+        rr = xc;
+      } else {
+        const double2 prev = t > 0 ? X[(t - 1) * S + s] : (RM == RM_RESID ? aux[3 * S + s] : make_double2(0.0, 0.0));
+        if constexpr (RM == RM_RESID) {
+          rr = make_double2(fma(Ej.x, prev.x, -xc.x), fma(Ej.y, prev.y, -xc.y));
+          if constexpr (NL >= 1) {
+            const double2 nm1 = NH[t * S + s];
+            rr.x = fma(c1.x, nm1.x, rr.x);
+            rr.y = fma(c1.y, nm1.y, rr.y);
+            if constexpr (NL == 2) {
+              const double2 nm2 = NH[(t > 0 ? t - 1 : 0) * S + s];
+              rr.x = fma(-c2.x, nm2.x, rr.x);
+              rr.y = fma(-c2.y, nm2.y, rr.y);
+            }
+          }
+        } else {  // RM_QOP
+          rr = make_double2(fma(-Ej.x, prev.x, xc.x), fma(-Ej.y, prev.y, xc.y));
+        }
+      }
+      nrm = fma(rr.x, rr.x, fma(rr.y, rr.y, nrm));
+      y[r] = cscale(rr, sg[t]);
+    }
+    DFT<R0, +1>::run(y);
+#pragma unroll
+    for (int r = 0; r < R0; ++r) buf0[(j * R0 + r) * S + s] = y[r];
+    __syncthreads();
+    const double2* pin = buf0;
+    double2* pout = buf1;
+    if constexpr (L == 3) {
+      tstage<NT, S, THREADS, C::R1, R0, +1>(buf0, buf1, stw);
+      __syncthreads();
+      pin = buf1;
+      pout = buf0;
+    }
+    for (int PJ = tid; PJ < S * (NSL / 2); PJ += THREADS) {
+      const int ps = PJ % S, pj = PJ / S;
+      const int ja = pj, jb = pj == 0 ? NSL / 2 : NSL - pj;
+      double2 va[RL], vb[RL];
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        va[r] = pin[(ja + r * NSL) * S + ps];
+        vb[r] = pin[(jb + r * NSL) * S + ps];
+      }
+#pragma unroll
+      for (int r = 1; r < RL; ++r) {
+        va[r] = cmul(va[r], stw[(r * ja) & (NT - 1)]);
+        vb[r] = cmul(vb[r], stw[(r * jb) & (NT - 1)]);
+      }
+      DFT<RL, +1>::run(va);
+      DFT<RL, +1>::run(vb);
+      const double2 Ep = aux[ps];
+#ifdef EXPD_K1_NODIV_EXPERIMENT
+      pair_divide<NT, RL>(va, vb, false, stw, ja, jb, a.a1 * Ep.x, a.a1 * Ep.y, hin);
+#else
+      pair_divide<NT, RL>(va, vb, pj == 0, stw, ja, jb, a.a1 * Ep.x, a.a1 * Ep.y, hin);
+#endif
+      DFT<RL, -1>::run(va);
+      DFT<RL, -1>::run(vb);
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        pout[(ja * RL + r) * S + ps] = va[r];
+        pout[(jb * RL + r) * S + ps] = vb[r];
+      }
+    }
+    __syncthreads();
+    if constexpr (L == 3) {
+      tstage<NT, S, THREADS, C::R1, RL, -1>(buf0, buf1, stw);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < R0; ++r) y[r] = buf1[(j + r * TPS) * S + s];
+#pragma unroll
+    for (int r = 1; r < R0; ++r) y[r] = cmulc(y[r], stw[(r * j) & (NT - 1)]);
+    DFT<R0, -1>::run(y);
+    // ---- phase C: Gamma_alpha^{-1}, update (u_t from the staged tile), store ------------
+    if (valid) {
+#pragma unroll
+      for (int r = 0; r < R0; ++r) {
+        const int t = j + r * TPS;
+        double2 sv = cscale(y[r], sgi[t]);
+        if constexpr (OUTM == OUT_UPDATE) sv = cadd(X[t * S + s], sv);
+        st2(a.Y + (long)t * npad + base, sv);
+      }
+    }
+    __syncthreads();  // stage `cur` is refilled by the next iteration's prefetch
+  }
+
+  if (a.partial) {
+    __shared__ double red[THREADS / 32];
+    for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+    if ((tid & 31) == 0) red[tid >> 5] = nrm;
+    __syncthreads();
+    if (tid < 32) {
+      double v = tid < THREADS / 32 ? red[tid] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (tid == 0) a.partial[blockIdx.x] = v;
+    }
+  }
+}
+
 template <int NT, int OUTM>
 static size_t time_smem_bytes() {
   const size_t tile = TimeGeo<NT>::L > 1 ? (size_t)NT * TimeGeo<NT>::S : 0;
   return sizeof(double2) * (2 * tile + NT) + sizeof(double) * 2 * NT;
 }
 
+static bool use_pipe() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EXPD_K1_PIPE");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <int NT, int RM, int OUTM, int NL>
 static cudaError_t launch_t(const TimeArgs& a, int grid, cudaStream_t st) {
+  if constexpr (TimeGeo<NT>::L > 1) {
+    if (use_pipe()) {
+      auto kp = k_time_pipe<NT, RM, OUTM, NL>;
+      const size_t smp = PipeLayout<NT, RM, NL>::BYTES;
+      static bool attr_p = false;
+      if (!attr_p) {
+        cudaError_t e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);
+        if (e != cudaSuccess) return e;
+        attr_p = true;
+      }
+      kp<<<grid, TimeGeo<NT>::THREADS, smp, st>>>(a);
+      return cudaGetLastError();
+    }
+  }
   auto k = k_time_fused<NT, RM, OUTM, NL>;
   size_t sm = time_smem_bytes<NT, OUTM>();
   static bool attr_done = false;  // per-instantiation, host-side
@@ -371,7 +619,7 @@ int time_fused_grid(int nt, long npairs, int sms) {
     default: S = TimeGeo<256>::S;
   }
   long ntiles = (npairs + S - 1) / S;
-  long g = (long)sms * 2;
+  long g = (long)sms * ((nt >= 16 && use_pipe()) ? 256 / EXPD_K1_THREADS : EXPD_K1_MINB);
   return (int)(ntiles < g ? (ntiles > 0 ? ntiles : 1) : g);
 }
 

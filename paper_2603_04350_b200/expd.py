@@ -14,7 +14,7 @@ from dataclasses import dataclass, field
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libexpd.so")
+LIB_PATH = os.environ.get("EXPD_LIB", os.path.join(_HERE, "libexpd.so"))  # override: tuning A/B only
 
 EXPD_OK = 0
 STATUS = {
