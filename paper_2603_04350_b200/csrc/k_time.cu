@@ -336,20 +336,26 @@ __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_gro
 template <int N>
 __device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
-template <int NT, int RM, int NL>
+// DB: double-buffered stage, one CTA per SM.  !DB: one stage per CTA, two CTAs per SM
+// (the other CTA's math hides this one's cp.async latency); buf0 then aliases the N-hat
+// part of the stage (N-hat is dead once phase A has run).
+template <int NT, int RM, int NL, bool DB>
 struct PipeLayout {
   using G = TimeGeo<NT>;
   static constexpr int S = G::S;
   static constexpr int TILE = NT * S;                   // double2 per staged array
-  static constexpr int NARR = (RM == RM_INPUT ? 1 : 1) + (NL ? 1 : 0);  // X (+ N-hat)
+  static constexpr int NARR = 1 + (NL ? 1 : 0);         // X (+ N-hat)
   static constexpr int AUX = 4 * S;                     // E, C1, C2, u0-hat per pair
   static constexpr int STAGE = NARR * TILE + AUX;       // double2 per pipeline stage
-  static constexpr size_t BYTES = sizeof(double2) * (2 * STAGE + 2 * TILE + NT) + sizeof(double) * 2 * NT;
+  static constexpr bool ALIAS = !DB && NL;              // buf0 inside the stage's N-hat block
+  static constexpr int NSTAGE = DB ? 2 : 1;
+  static constexpr int FFTBUF = ALIAS ? TILE : 2 * TILE;
+  static constexpr size_t BYTES = sizeof(double2) * (NSTAGE * STAGE + FFTBUF + NT) + sizeof(double) * 2 * NT;
 };
 
-template <int NT, int RM, int NL>
+template <int NT, int RM, int NL, bool DB>
 __device__ __forceinline__ void pipe_issue(const TimeArgs& a, long tile, double2* stage) {
-  using PL = PipeLayout<NT, RM, NL>;
+  using PL = PipeLayout<NT, RM, NL, DB>;
   constexpr int S = PL::S, TILE = PL::TILE, THREADS = TimeGeo<NT>::THREADS;
   const long npad = a.npad;
   for (int c = threadIdx.x; c < TILE; c += THREADS) {
@@ -374,18 +380,18 @@ __device__ __forceinline__ void pipe_issue(const TimeArgs& a, long tile, double2
   cpa_commit();
 }
 
-template <int NT, int RM, int OUTM, int NL>
-__global__ void __launch_bounds__(EXPD_K1_THREADS, 256 / EXPD_K1_THREADS) k_time_pipe(const TimeArgs a) {
+template <int NT, int RM, int OUTM, int NL, bool DB>
+__global__ void __launch_bounds__(EXPD_K1_THREADS, DB ? 1 : 2) k_time_pipe(const TimeArgs a) {
   using G = TimeGeo<NT>;
   using C = TimeCfg<NT>;
-  using PL = PipeLayout<NT, RM, NL>;
+  using PL = PipeLayout<NT, RM, NL, DB>;
   constexpr int L = G::L, R0 = G::R0, RL = G::RL, TPS = G::TPS, S = G::S, THREADS = G::THREADS;
   constexpr int NSL = G::NSL, TILE = PL::TILE;
   static_assert(L > 1, "pipelined kernel needs a multi-stage FFT");
   extern __shared__ double2 smem[];
-  double2* buf0 = smem + 2 * PL::STAGE;  // [NT][S]
-  double2* buf1 = buf0 + TILE;
-  double2* stw = buf1 + TILE;            // [NT] e^{+2 pi i q/NT}
+  double2* buf0 = PL::ALIAS ? smem + TILE : smem + PL::NSTAGE * PL::STAGE;  // [NT][S]
+  double2* buf1 = PL::ALIAS ? smem + PL::STAGE : buf0 + TILE;
+  double2* stw = smem + PL::NSTAGE * PL::STAGE + PL::FFTBUF;  // [NT] e^{+2 pi i q/NT}
   double* sg = reinterpret_cast<double*>(stw + NT);
   double* sgi = sg + NT;
 
@@ -404,13 +410,18 @@ __global__ void __launch_bounds__(EXPD_K1_THREADS, 256 / EXPD_K1_THREADS) k_time
 
   long tile = blockIdx.x;
   int cur = 0;
-  if (tile < ntiles) pipe_issue<NT, RM, NL>(a, tile, smem);
-  for (; tile < ntiles; tile += gridDim.x, cur ^= 1) {
-    const long next = tile + gridDim.x;
-    if (next < ntiles) {
-      pipe_issue<NT, RM, NL>(a, next, smem + (cur ^ 1) * PL::STAGE);
-      cpa_wait<1>();
+  if (DB && tile < ntiles) pipe_issue<NT, RM, NL, DB>(a, tile, smem);
+  for (; tile < ntiles; tile += gridDim.x, cur ^= (DB ? 1 : 0)) {
+    if constexpr (DB) {
+      const long next = tile + gridDim.x;
+      if (next < ntiles) {
+        pipe_issue<NT, RM, NL, DB>(a, next, smem + (cur ^ 1) * PL::STAGE);
+        cpa_wait<1>();
+      } else {
+        cpa_wait<0>();
+      }
     } else {
+      pipe_issue<NT, RM, NL, DB>(a, tile, smem);
       cpa_wait<0>();
     }
     __syncthreads();
@@ -455,6 +466,7 @@ __global__ void __launch_bounds__(EXPD_K1_THREADS, 256 / EXPD_K1_THREADS) k_time
       y[r] = cscale(rr, sg[t]);
     }
     DFT<R0, +1>::run(y);
+    if constexpr (PL::ALIAS) __syncthreads();  // every thread is done reading N-hat
 #pragma unroll
     for (int r = 0; r < R0; ++r) buf0[(j * R0 + r) * S + s] = y[r];
     __syncthreads();
@@ -538,30 +550,37 @@ static size_t time_smem_bytes() {
   return sizeof(double2) * (2 * tile + NT) + sizeof(double) * 2 * NT;
 }
 
-static bool use_pipe() {
+// EXPD_K1_PIPE: 0 = register-load kernel, 1 = double-buffered pipe (1 CTA/SM),
+// 2 (default) = single-stage pipe with two CTAs per SM
+static int pipe_mode() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("EXPD_K1_PIPE");
-    v = (e && e[0] == '0') ? 0 : 1;
+    v = (e && (e[0] == '0' || e[0] == '1')) ? e[0] - '0' : 2;
   }
-  return v == 1;
+  return v;
+}
+static bool use_pipe() { return pipe_mode() > 0; }
+
+template <int NT, int RM, int OUTM, int NL, bool DB>
+static cudaError_t launch_pipe(const TimeArgs& a, int grid, cudaStream_t st) {
+  auto kp = k_time_pipe<NT, RM, OUTM, NL, DB>;
+  const size_t smp = PipeLayout<NT, RM, NL, DB>::BYTES;
+  static bool attr_p = false;
+  if (!attr_p) {
+    cudaError_t e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);
+    if (e != cudaSuccess) return e;
+    attr_p = true;
+  }
+  kp<<<grid, TimeGeo<NT>::THREADS, smp, st>>>(a);
+  return cudaGetLastError();
 }
 
 template <int NT, int RM, int OUTM, int NL>
 static cudaError_t launch_t(const TimeArgs& a, int grid, cudaStream_t st) {
   if constexpr (TimeGeo<NT>::L > 1) {
-    if (use_pipe()) {
-      auto kp = k_time_pipe<NT, RM, OUTM, NL>;
-      const size_t smp = PipeLayout<NT, RM, NL>::BYTES;
-      static bool attr_p = false;
-      if (!attr_p) {
-        cudaError_t e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);
-        if (e != cudaSuccess) return e;
-        attr_p = true;
-      }
-      kp<<<grid, TimeGeo<NT>::THREADS, smp, st>>>(a);
-      return cudaGetLastError();
-    }
+    if (pipe_mode() == 1) return launch_pipe<NT, RM, OUTM, NL, true>(a, grid, st);
+    if (pipe_mode() == 2) return launch_pipe<NT, RM, OUTM, NL, false>(a, grid, st);
   }
   auto k = k_time_fused<NT, RM, OUTM, NL>;
   size_t sm = time_smem_bytes<NT, OUTM>();
@@ -619,7 +638,7 @@ int time_fused_grid(int nt, long npairs, int sms) {
     default: S = TimeGeo<256>::S;
   }
   long ntiles = (npairs + S - 1) / S;
-  long g = (long)sms * ((nt >= 16 && use_pipe()) ? 256 / EXPD_K1_THREADS : EXPD_K1_MINB);
+  long g = (long)sms * ((nt >= 16 && use_pipe()) ? (pipe_mode() == 1 ? 1 : 2) : EXPD_K1_MINB);
   return (int)(ntiles < g ? (ntiles > 0 ? ntiles : 1) : g);
 }
 
