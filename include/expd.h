@@ -136,6 +136,11 @@ expd_status expd_store_state(expd_plan* plan, double* U);           /* U = V U-h
    PAPER.md:141; V = V^T = V^{-1}).  in, out: [nslices][n^dim] device; out may alias in.
    Uses the workspace's transform scratch.  Async. */
 expd_status expd_dst(expd_plan* plan, const double* in, double* out, long nslices);
+/* nhat = V N(V uhat) for nslices slices of DST coefficients (stage 3 of a Picard sweep,
+   BASELINE.json:5; N(u) = sum_p q[p] u^p from the plan's problem).  uhat, nhat:
+   [nslices][n^dim] device, mode j_i - 1 along each axis, x fastest; nhat may alias uhat.
+   Uses the workspace's spectral temporary and transform scratch.  Async. */
+expd_status expd_nonlin_hat(expd_plan* plan, const double* uhat, double* nhat, long nslices);
 /* Stage timing of expd_sweep with CUDA events recorded on the plan's stream (inside the
    sweep's CUDA graph): enable != 0 turns it on.  expd_sweep_stage_ms waits for the last
    sweep and returns the device time of stage 3 (N-hat of all slices; 0 when linear) and of
@@ -145,7 +150,8 @@ expd_status expd_sweep_stage_ms(expd_plan* plan, double* ms_nonlin, double* ms_t
 /* Diagnostics for tuning: average device time (ms, CUDA events) of `reps` back-to-back
    launches of one kernel family on the workspace's spectral state: which = 0 x-axis DST
    pass, 1 strided-axis DST pass, 2 fused strided IDST -> N -> DST pass (each over nslices
-   slices, 1 <= nslices <= nt), 3 the fused time-local kernel K1 (whole state).  The
+   slices, 1 <= nslices <= nt), 3 the fused time-local kernel K1 (whole state), 4 / 5 / 6
+   the TMA line kernels (x-axis, strided axis, fused strided [V, N, V]).  The
    workspace contents are overwritten with transformed data. */
 expd_status expd_debug_kernel_ms(expd_plan* plan, int which, long nslices, int reps, double* ms);
 /* Number of kernels one expd_sweep launches (for the benchmark's launch count). */

@@ -439,6 +439,27 @@ extern "C" expd_status expd_dst(expd_plan* p, const double* in, double* out, lon
   return EXPD_OK;
 }
 
+extern "C" expd_status expd_nonlin_hat(expd_plan* p, const double* uhat, double* nhat, long nslices) {
+  expd_status s = ready(p);
+  if (s) return s;
+  if (!uhat || !nhat || nslices < 0) return fail(p, EXPD_ERR_INVALID_ARG, "expd_nonlin_hat: bad args");
+  const long chunk = p->prob.nt / 2;  // T1 holds nt padded slices: input half, output half
+  const size_t row = sizeof(double) * p->g.n, prow = sizeof(double) * p->g.M;
+  const size_t rows = (size_t)(p->g.N / p->g.n);
+  double* tin = p->T1;
+  double* tout = p->T1 + chunk * p->g.npad;
+  for (long s0 = 0; s0 < nslices; s0 += chunk) {
+    const long ns = nslices - s0 < chunk ? nslices - s0 : chunk;
+    CUDA_TRY(p, cudaMemsetAsync(tin, 0, sizeof(double) * ns * p->g.npad, p->stream));
+    CUDA_TRY(p, cudaMemcpy2DAsync(tin, prow, uhat + s0 * p->g.N, row, row, (size_t)ns * rows, cudaMemcpyDeviceToDevice,
+                                  p->stream));
+    CUDA_TRY(p, nonlin_slices(p->g, dst_tables(p), tin, tout, ns, p->prob.npoly, p->prob.q, p->scratch, p->stream));
+    CUDA_TRY(p, cudaMemcpy2DAsync(nhat + s0 * p->g.N, row, tout, prow, row, (size_t)ns * rows, cudaMemcpyDeviceToDevice,
+                                  p->stream));
+  }
+  return EXPD_OK;
+}
+
 extern "C" expd_status expd_set_profiling(expd_plan* p, int enable) {
   expd_status s = ready(p);
   if (s) return s;
@@ -468,7 +489,9 @@ extern "C" expd_status expd_debug_kernel_ms(expd_plan* p, int which, long nslice
   if (s) return s;
   if (!ms || reps < 1 || nslices < 1 || nslices > p->prob.nt) return fail(p, EXPD_ERR_INVALID_ARG, "debug: bad args");
   float m = 0.f;
-  if (which <= 2) {
+  if (which >= 4 && (which > 6 || !line_supported(p->g) || p->g.dim < 2))
+    return fail(p, EXPD_ERR_UNSUPPORTED, "debug: no line kernel for this geometry");
+  if (which != 3) {
     CUDA_TRY(p, dst_debug_time(p->g, dst_tables(p), which, p->Uh, p->T1, nslices, p->prob.npoly, p->prob.q, reps, &m,
                                p->stream));
   } else {

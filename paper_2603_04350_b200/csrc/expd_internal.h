@@ -18,6 +18,19 @@ struct Geom {
   int M;      // n + 1
 };
 
+// Pointwise nonlinearity N(u) = sum_{p < npoly} q[p] u^p (stage 3; BASELINE.json:9, :11).
+struct Poly {
+  int npoly;
+  double q[8];
+};
+#ifdef __CUDACC__
+__device__ __forceinline__ double poly_eval(const Poly& P, double u) {
+  double acc = 0.0;
+  for (int k = P.npoly - 1; k >= 0; --k) acc = fma(acc, u, P.q[k]);
+  return acc;
+}
+#endif
+
 // Per-launch parameters of the time-local fused kernel (K1).
 struct TimeArgs {
   int nt;
@@ -65,6 +78,11 @@ size_t dst_scratch_doubles(const Geom& g, long max_slices);
 cudaError_t dst_debug_time(const Geom& g, const DstTables& t, int which, double* a, double* b, long nslices,
                            int npoly, const double* q, int reps, float* ms, cudaStream_t st);
 int nonlin_chunk_slices(const Geom& g);
+// TMA line kernels (k_line.cu): one axis pass (0 = x rows, 1 = y, 2 = z) over padded
+// spectral slices, nl fusing [V, N, V] on a strided axis.  in / out may alias.
+bool line_supported(const Geom& g);
+cudaError_t line_pass(const Geom& g, const DstTables& t, const Poly& P, int ax, bool nl, const double* in,
+                      double* out, long nslices, cudaStream_t st);
 int nonlin_kernel_launches(const Geom& g, long nslices);
 
 // vector kernels (k_vec.cu)

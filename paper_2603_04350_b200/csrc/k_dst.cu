@@ -24,16 +24,6 @@
 
 namespace expd {
 
-struct Poly {
-  int npoly;
-  double q[8];
-};
-
-__device__ __forceinline__ double poly_eval(const Poly& P, double u) {
-  double acc = 0.0;
-  for (int k = P.npoly - 1; k >= 0; --k) acc = fma(acc, u, P.q[k]);
-  return acc;
-}
 
 // radix plan: R0 (first stage, fed from the load), up to two middle radices RM1, RM2
 // (1 = absent) and the last radix RL (run on Hermitian partner jobs).
@@ -569,6 +559,14 @@ static ColsOp col_op(const Geom& g, int axis, const double* in, double* out, lon
   return o;
 }
 
+static bool use_line(const Geom& g);
+// one strided-axis pass of padded spectral slices (TMA line kernel when available)
+static cudaError_t colpass(const Geom& g, const DstTables& t, const Poly& P, int ax, const double* in, double* out,
+                           long nslices, cudaStream_t st) {
+  if (use_line(g)) return line_pass(g, t, P, ax, false, in, out, nslices, st);
+  return cols(g.M, col_op(g, ax, in, out, nslices, false), t, P, st);
+}
+
 cudaError_t dst_slices(const Geom& g, const DstTables& t, const double* src, bool src_spectral, double* dst,
                        bool dst_spectral, long nslices, double* scratch, cudaStream_t st) {
   if (nslices <= 0) return cudaSuccess;
@@ -579,7 +577,7 @@ cudaError_t dst_slices(const Geom& g, const DstTables& t, const double* src, boo
     // physical -> spectral: x first (into dst), then strided axes in place
     RowsOp r{src, phys_slice, g.n, dst, g.npad, g.M, rows_ps, nslices, false, false};
     CK(rows(g.M, r, t, P, st));
-    for (int ax = 1; ax < g.dim; ++ax) CK(cols(g.M, col_op(g, ax, dst, dst, nslices, false), t, P, st));
+    for (int ax = 1; ax < g.dim; ++ax) CK(colpass(g, t, P, ax, dst, dst, nslices, st));
     return cudaSuccess;
   }
   if (src_spectral && !dst_spectral) {
@@ -590,7 +588,7 @@ cudaError_t dst_slices(const Geom& g, const DstTables& t, const double* src, boo
       const long ns = nslices - s0 < chunk ? nslices - s0 : chunk;
       const double* cur = src + s0 * g.npad;
       for (int ax = 1; ax < g.dim; ++ax) {
-        CK(cols(g.M, col_op(g, ax, cur, scratch, ns, false), t, P, st));
+        CK(colpass(g, t, P, ax, cur, scratch, ns, st));
         cur = scratch;
       }
       RowsOp r{cur, g.npad, g.M, dst + s0 * phys_slice, phys_slice, g.n, rows_ps, ns, false, false};
@@ -600,17 +598,25 @@ cudaError_t dst_slices(const Geom& g, const DstTables& t, const double* src, boo
   }
   if (src_spectral && dst_spectral) {
     RowsOp r{src, g.npad, g.M, dst, g.npad, g.M, rows_ps, nslices, false, false};
-    CK(rows(g.M, r, t, P, st));
-    for (int ax = 1; ax < g.dim; ++ax) CK(cols(g.M, col_op(g, ax, dst, dst, nslices, false), t, P, st));
+    if (use_line(g)) CK(line_pass(g, t, P, 0, false, src, dst, nslices, st));
+    else CK(rows(g.M, r, t, P, st));
+    for (int ax = 1; ax < g.dim; ++ax) CK(colpass(g, t, P, ax, dst, dst, nslices, st));
     return cudaSuccess;
   }
   return cudaErrorInvalidValue;
 }
 
 int nonlin_chunk_slices(const Geom& g) {
-  // keep one chunk's intermediate (npad doubles per slice) around 32 MB so it stays in L2
+  // keep one chunk's intermediate (npad doubles per slice) within ~EXPD_CHUNK_MB (default
+  // 64) MB so it stays in the 126 MB L2 between the axis passes
+  static long mb = -1;
+  if (mb < 0) {
+    const char* e = getenv("EXPD_CHUNK_MB");
+    mb = e ? atol(e) : 64;
+    if (mb < 1) mb = 64;
+  }
   long per = g.npad * 8;
-  long c = (32l << 20) / (per > 0 ? per : 1);
+  long c = (mb << 20) / (per > 0 ? per : 1);
   return (int)(c < 1 ? 1 : (c > 64 ? 64 : c));
 }
 
@@ -621,15 +627,34 @@ int nonlin_kernel_launches(const Geom& g, long nslices) {
   return (int)(nch * per);
 }
 
+static bool use_line(const Geom& g) {
+  static int v = -1;  // tuning switch: EXPD_LINE=0 keeps the k_rows / k_cols kernels
+  if (v < 0) {
+    const char* e = getenv("EXPD_LINE");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v && g.dim >= 2 && line_supported(g);
+}
+
 cudaError_t nonlin_slices(const Geom& g, const DstTables& t, const double* uhat, double* nhat, long nslices,
                           int npoly, const double* q, double* scratch, cudaStream_t st) {
   Poly P = make_poly(npoly, q);
   const int rows_ps = (int)(g.N / g.n);
   const long chunk = nonlin_chunk_slices(g);
+  const bool tl = use_line(g);
   for (long s0 = 0; s0 < nslices; s0 += chunk) {
     long ns = nslices - s0 < chunk ? nslices - s0 : chunk;
     const double* in = uhat + s0 * g.npad;
     double* out = nhat + s0 * g.npad;
+    if (tl) {
+      // x (inverse) -> scratch ; [dim 3: y] ; last axis fused [V, N, V] ; [dim 3: y] ; x -> out
+      CK(line_pass(g, t, P, 0, false, in, scratch, ns, st));
+      if (g.dim == 3) CK(line_pass(g, t, P, 1, false, scratch, scratch, ns, st));
+      CK(line_pass(g, t, P, g.dim - 1, true, scratch, scratch, ns, st));
+      if (g.dim == 3) CK(line_pass(g, t, P, 1, false, scratch, scratch, ns, st));
+      CK(line_pass(g, t, P, 0, false, scratch, out, ns, st));
+      continue;
+    }
     if (g.dim == 1) {
       RowsOp r{in, g.npad, g.M, out, g.npad, g.M, rows_ps, ns, false, true};
       CK(rows(g.M, r, t, P, st));
@@ -654,7 +679,8 @@ cudaError_t nonlin_phys_slices(const Geom& g, const DstTables& t, const double* 
   const int rows_ps = (int)(g.N / g.n);
   RowsOp r{u, g.N, g.n, nhat, g.npad, g.M, rows_ps, nslices, true, false};
   CK(rows(g.M, r, t, P, st));
-  for (int ax = 1; ax < g.dim; ++ax) CK(cols(g.M, col_op(g, ax, nhat, nhat, nslices, false), t, P, st));
+  Poly P0 = make_poly(0, nullptr);
+  for (int ax = 1; ax < g.dim; ++ax) CK(colpass(g, t, P0, ax, nhat, nhat, nslices, st));
   return cudaSuccess;
 }
 
@@ -668,6 +694,7 @@ cudaError_t dst_debug_time(const Geom& g, const DstTables& t, int which, double*
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   auto one = [&]() -> cudaError_t {
+    if (which >= 4) return line_pass(g, t, P, which == 4 ? 0 : g.dim - 1, which == 6, a, b, nslices, st);
     if (which == 0) {
       RowsOp r{a, g.npad, g.M, b, g.npad, g.M, rows_ps, nslices, false, false};
       return rows(g.M, r, t, P, st);

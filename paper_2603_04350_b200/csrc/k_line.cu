@@ -1,0 +1,538 @@
+// k_line.cu -- K2/K3/K4 v2: the orthonormal DST-I V (L_h = V_h D_h V_h^{-1},
+// V_h orthogonal; reading R1) along one axis of padded spectral slices, and the fused
+// strided-axis pass [V, N(.), V] of stage 3 (N-hat = V N(V u-hat), BASELINE.json:5), for
+// line lengths M = n+1 in {256, ..., 4096}.
+//
+// Same arithmetic as k_dst.cu (sinft pre-processing, complex FFT of two real lines packed
+// as one complex sequence, Hermitian unpack, prefix sum for the odd outputs), re-organised
+// around the Blackwell async-copy engine:
+//   * persistent CTAs, one line pair per work item, two shared-memory buffers: the TMA
+//     brings item i+1 while item i is transformed (no exposed HBM / L2 latency);
+//   * x-axis (ROW) items: the two rows are loaded / stored as TMA tensor boxes
+//     {16 doubles, M/16} with the 128-byte swizzle, so the mirror reads of the
+//     pre-processing and the per-thread chunk writes of the result are bank-conflict free;
+//   * strided-axis (COL) items: one column pair (16 B per grid row) moved as TMA boxes
+//     of {2 doubles, 256 rows} into / out of a linear layout (the result is compacted
+//     from the padded work layout before the store);
+//   * the last stage of the prefix sum leaves every thread 2L consecutive outputs
+//     (F_{2k+1}, F_{2k+2}) pairs, written in the layout the TMA store reads.
+// All loads and stores of the data go through the TMA: no thread issues a global access
+// for the data, so the LSU carries only the twiddle / sine table reads.
+//
+// DST-I: with M = n+1 and F_j = sum_i x_i sin(pi i j / M),
+//   y_0 = 0, y_i = sin(pi i/M)(x_i + x_{M-i}) + (x_i - x_{M-i})/2,   Y = FFT_M(y),
+//   F_{2k} = -Im Y_k (k >= 1),  F_{2k+1} = sum_{k' <= k} Re Y_{k'} (Re Y_0 halved),
+// V x = sqrt(2/M) F.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <mutex>
+
+#include "expd_internal.h"
+#include "fft_dev.cuh"
+#include "tma_dev.cuh"
+
+namespace expd {
+
+// Radix plan: first radix R0 (fed by the pre-processing), middle radices RM1 (RM2 = 1
+// here), last radix RL (run on Hermitian partner jobs).  T = M / R0 threads per line pair.
+template <int M> struct LPlan;
+template <> struct LPlan<256>  { static constexpr int R0 = 8,  RM1 = 4,  RL = 8; };
+template <> struct LPlan<512>  { static constexpr int R0 = 16, RM1 = 4,  RL = 8; };
+template <> struct LPlan<1024> { static constexpr int R0 = 16, RM1 = 8,  RL = 8; };
+template <> struct LPlan<2048> { static constexpr int R0 = 16, RM1 = 16, RL = 8; };
+template <> struct LPlan<4096> { static constexpr int R0 = 16, RM1 = 16, RL = 16; };
+
+template <int M>
+struct LGeo {
+  static constexpr int R0 = LPlan<M>::R0, RM1 = LPlan<M>::RM1, RL = LPlan<M>::RL;
+  static_assert(R0 * RM1 * RL == M, "radix plan");
+  static constexpr int T = M / R0;            // threads per line pair (= CTA size)
+  static constexpr int NSL = M / RL;          // Ns of the last stage
+  static constexpr int L = (M / 2) / T;       // k-values per thread in the prefix sum (= R0/2)
+  static constexpr int PADP = R0;             // one pad slot per PADP positions
+  static constexpr int SW = M + M / PADP;     // padded positions per line pair
+  static constexpr int NW = T / 32;           // warps per CTA
+  static constexpr size_t BUFB = ((size_t)SW * 16 + 1023) / 1024 * 1024;  // bytes per buffer (1 KB aligned)
+  static_assert(M % 256 == 0, "COL boxes of 256 rows");
+  static constexpr size_t SMEM = 1024 + 2 * BUFB + 16 * (NW > 0 ? NW : 1) + 16;
+  // resident CTAs per SM: shared memory (228 KB, 1 KB reserved per CTA) and >= 160 registers
+  static constexpr int MINB_SMEM = (int)((228 * 1024) / (SMEM + 1024));
+  static constexpr int MINB_REG = 65536 / (T * 160);
+  static constexpr int MINB = MINB_SMEM < MINB_REG ? (MINB_SMEM > 0 ? MINB_SMEM : 1) : MINB_REG;
+};
+
+enum LineAxis { AX_ROW = 0, AX_COL_Y = 1, AX_COL_Z = 2 };
+constexpr int CBR = 256;  // grid rows per TMA box of a strided-axis (COL) item
+
+struct LineArgs {
+  long nitems;
+  int per_slice;   // items per slice
+  int inner;       // ROW: row pairs per slice; COL: column pairs per outer index
+  int rows;        // ROW: rows per slice (for the incomplete last pair)
+  const double2* tw;   // [M] exp(-2 pi i q / M)
+  const double* sinp;  // [M] sin(pi i / M)
+  Poly poly;
+};
+
+template <int PADP>
+__device__ __forceinline__ int lswz(int p) { return p + p / PADP; }
+
+// byte offset of double x of a row stored as TMA boxes {16, M/16} with the 128-byte swizzle
+__device__ __forceinline__ uint32_t row_sw(int x) {
+  const int o = x >> 4, c = x & 15;
+  return (uint32_t)(o * 128 + ((((c >> 1) ^ (o & 7))) << 4) + ((c & 1) << 3));
+}
+
+__device__ __forceinline__ double2 lpre(double2 z, double2 zm, double s) {
+  double2 sum = cadd(z, zm), dif = csub(z, zm);
+  return make_double2(fma(s, sum.x, 0.5 * dif.x), fma(s, sum.y, 0.5 * dif.y));
+}
+__device__ __forceinline__ void lunpack(double2 Zk, double2 Zm, bool k0, double2& e, double2& w) {
+  e = make_double2(-0.5 * (Zk.y - Zm.y), 0.5 * (Zk.x - Zm.x));
+  w = make_double2(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y + Zm.y));
+  if (k0) w = make_double2(0.5 * w.x, 0.5 * w.y);
+}
+template <int R>
+__device__ __forceinline__ void ltw(const double2* __restrict__ tw, int b, double2 (&t)[R]) {
+  t[0] = make_double2(1.0, 0.0);
+  if constexpr (R > 1) t[1] = __ldg(tw + b);
+#pragma unroll
+  for (int r = 2; r < R; ++r) t[r] = (r % 2 == 0) ? cmul(t[r / 2], t[r / 2]) : cmul(t[r - 1], t[1]);
+}
+
+// In-place middle Stockham stage (radix R, NS) of the line pair in buf (padded layout).
+template <int M, int R, int NS>
+__device__ __forceinline__ void lmid(double2* buf, const double2* __restrict__ tw) {
+  using D = LGeo<M>;
+  constexpr int JOBS = M / R;
+  constexpr int JT = (JOBS + D::T - 1) / D::T;
+  constexpr int TWS = M / (NS * R);
+  double2 v[JT][R];
+#pragma unroll
+  for (int jt = 0; jt < JT; ++jt) {
+    const int jm = threadIdx.x + jt * D::T;
+    if (JOBS % D::T == 0 || jm < JOBS) {
+      const int k = jm % NS;
+#pragma unroll
+      for (int r = 0; r < R; ++r) v[jt][r] = buf[lswz<D::PADP>(jm + r * (M / R))];
+      double2 t[R];
+      ltw<R>(tw, k * TWS, t);
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[jt][r] = cmul(v[jt][r], t[r]);
+      DFT<R, -1>::run(v[jt]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int jt = 0; jt < JT; ++jt) {
+    const int jm = threadIdx.x + jt * D::T;
+    if (JOBS % D::T == 0 || jm < JOBS) {
+      const int k = jm % NS, base = (jm / NS) * NS * R + k;
+#pragma unroll
+      for (int r = 0; r < R; ++r) buf[lswz<D::PADP>(base + r * NS)] = v[jt][r];
+    }
+  }
+  __syncthreads();
+}
+
+// DST core of one line pair: stage-0 inputs y_i (i = j + T r) in v; leaves the unscaled
+// F at natural positions [2jL, 2jL + 2L) in out (F_m sits at position m-1; position M-1
+// is the spectral pad and returns 0).  Starts with a barrier (buf may still be read by
+// the caller's stage-0 loads) and ends with buf free for the caller.
+template <int M>
+__device__ __forceinline__ void lcore(double2 (&v)[LGeo<M>::R0], double2* buf, double2* wt,
+                                      const double2* __restrict__ tw, double2 (&out)[2 * LGeo<M>::L]) {
+  using D = LGeo<M>;
+  constexpr int R0 = D::R0, RL = D::RL, NSL = D::NSL, T = D::T, L = D::L, PADP = D::PADP;
+  const int j = threadIdx.x;
+  DFT<R0, -1>::run(v);
+  __syncthreads();
+  {
+    double2* o0 = buf + lswz<PADP>(j * R0);  // R0 = PADP consecutive positions: contiguous
+#pragma unroll
+    for (int r = 0; r < R0; ++r) o0[r] = v[r];
+  }
+  __syncthreads();
+  lmid<M, D::RM1, R0>(buf, tw);
+  // last stage on Hermitian partner jobs (ja, jb): frequency sets k = ja + NSL r and
+  // jb + NSL r pair up as k <-> M - k; then the unpack into e_k (position 2k-1), w_k (2k)
+  constexpr int PJOBS = NSL / 2;
+  constexpr int PJT = (PJOBS + T - 1) / T;
+  double2 va[PJT][RL], vb[PJT][RL];
+#pragma unroll
+  for (int pt = 0; pt < PJT; ++pt) {
+    const int pj = j + pt * T;
+    if (PJOBS % T == 0 || pj < PJOBS) {
+      const int ja = pj, jb = pj == 0 ? NSL / 2 : NSL - pj;
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        va[pt][r] = buf[lswz<PADP>(ja + r * NSL)];
+        vb[pt][r] = buf[lswz<PADP>(jb + r * NSL)];
+      }
+      double2 t[RL];
+      ltw<RL>(tw, ja, t);
+#pragma unroll
+      for (int r = 1; r < RL; ++r) va[pt][r] = cmul(va[pt][r], t[r]);
+      ltw<RL>(tw, jb, t);
+#pragma unroll
+      for (int r = 1; r < RL; ++r) vb[pt][r] = cmul(vb[pt][r], t[r]);
+      DFT<RL, -1>::run(va[pt]);
+      DFT<RL, -1>::run(vb[pt]);
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int pt = 0; pt < PJT; ++pt) {
+    const int pj = j + pt * T;
+    if (PJOBS % T == 0 || pj < PJOBS) {
+      const int ja = pj, jb = pj == 0 ? NSL / 2 : NSL - pj;
+#pragma unroll
+      for (int r = 0; r < RL / 2; ++r) {
+        double2 e, w;
+        const int ka = ja + NSL * r;
+        lunpack(va[pt][r], pj == 0 ? va[pt][(RL - r) % RL] : vb[pt][RL - 1 - r], ka == 0, e, w);
+        if (ka >= 1) buf[lswz<PADP>(2 * ka - 1)] = e;
+        buf[lswz<PADP>(2 * ka)] = w;
+        const int kb = jb + NSL * r;
+        lunpack(vb[pt][r], pj == 0 ? vb[pt][RL - 1 - r] : va[pt][RL - 1 - r], false, e, w);
+        buf[lswz<PADP>(2 * kb - 1)] = e;
+        buf[lswz<PADP>(2 * kb)] = w;
+      }
+    }
+  }
+  __syncthreads();
+  // prefix sum: thread j owns k in [jL, jL + L) -> positions [2jL, 2jL + 2L):
+  // out[2l] = F_{2k+1} = sum_{k' <= k} w_k', out[2l+1] = F_{2k+2} = e_{k+1}
+  double2 tot = make_double2(0.0, 0.0);
+  {
+    const double2* P = buf + lswz<PADP>(2 * j * L);  // 2L <= PADP consecutive positions
+#pragma unroll
+    for (int l = 0; l < L; ++l) {
+      tot = cadd(tot, P[2 * l]);
+      out[2 * l] = tot;
+      out[2 * l + 1] = (j == T - 1 && l == L - 1) ? make_double2(0.0, 0.0) : P[2 * l + 1];
+    }
+  }
+  double2 inc = tot;
+  const int lane = j & 31;
+#pragma unroll
+  for (int d = 1; d < 32 && d < T; d <<= 1) {
+    double ox = __shfl_up_sync(0xffffffffu, inc.x, d);
+    double oy = __shfl_up_sync(0xffffffffu, inc.y, d);
+    if (lane >= d) inc = cadd(inc, make_double2(ox, oy));
+  }
+  double2 off = csub(inc, tot);
+  if constexpr (D::NW > 1) {
+    if (lane == 31) wt[j >> 5] = inc;
+    __syncthreads();
+    for (int b = 0; b < (j >> 5); ++b) off = cadd(off, wt[b]);
+  }
+#pragma unroll
+  for (int l = 0; l < L; ++l) out[2 * l] = cadd(out[2 * l], off);
+}
+
+// ---------------------------------------------------------------------------------------
+// the persistent line kernel
+// ---------------------------------------------------------------------------------------
+template <int AX>
+__device__ __forceinline__ void line_coords(const LineArgs& a, long item, int& c0, int& c1, int& c2, int& c3) {
+  const long s = item / a.per_slice;
+  const int w = (int)(item % a.per_slice);
+  if constexpr (AX == AX_ROW) {
+    c0 = 0; c1 = 0; c2 = 2 * w; c3 = (int)s;  // rows 2w, 2w+1 of slice s
+  } else {
+    const int o = w / a.inner, cp = w % a.inner;
+    c0 = 2 * cp;
+    if constexpr (AX == AX_COL_Y) { c1 = 0; c2 = o; }
+    else { c1 = o; c2 = 0; }
+    c3 = (int)s;
+  }
+}
+
+template <int M, int AX>
+__device__ __forceinline__ void line_issue_load(const CUtensorMap* map, const LineArgs& a, long item, char* buf,
+                                                uint64_t* bar) {
+  using D = LGeo<M>;
+  int c0, c1, c2, c3;
+  line_coords<AX>(a, item, c0, c1, c2, c3);
+  mbar_arrive_expect_tx(bar, (uint32_t)(M * 16));
+  if constexpr (AX == AX_ROW) {
+    tma_load_4d(buf, map, bar, 0, 0, c2, c3);
+    tma_load_4d(buf + M * 8, map, bar, 0, 0, c2 + 1, c3);
+  } else {
+    // linear raw layout: grid row p at byte 16 p (boxes of CBR rows, 4 KB aligned)
+#pragma unroll
+    for (int b = 0; b < M / CBR; ++b) {
+      char* dst = buf + (size_t)b * CBR * 16;
+      if constexpr (AX == AX_COL_Y) tma_load_4d(dst, map, bar, c0, b * CBR, c2, c3);
+      else tma_load_4d(dst, map, bar, c0, c1, b * CBR, c3);
+    }
+  }
+}
+
+template <int M, int AX>
+__device__ __forceinline__ void line_issue_store(const CUtensorMap* map, const LineArgs& a, long item,
+                                                 const char* buf) {
+  using D = LGeo<M>;
+  int c0, c1, c2, c3;
+  line_coords<AX>(a, item, c0, c1, c2, c3);
+  if constexpr (AX == AX_ROW) {
+    tma_store_4d(map, buf, 0, 0, c2, c3);
+    if (c2 + 1 < a.rows) tma_store_4d(map, buf + M * 8, 0, 0, c2 + 1, c3);
+  } else {
+#pragma unroll
+    for (int b = 0; b < M / CBR; ++b) {
+      const char* src = buf + (size_t)b * CBR * 16;
+      if constexpr (AX == AX_COL_Y) tma_store_4d(map, src, c0, b * CBR, c2, c3);
+      else tma_store_4d(map, src, c0, c1, b * CBR, c3);
+    }
+  }
+  bulk_commit();
+}
+
+template <int M, int AX, bool NL>
+__global__ void __launch_bounds__(LGeo<M>::T, LGeo<M>::MINB) k_line(const __grid_constant__ CUtensorMap in_map,
+                                                     const __grid_constant__ CUtensorMap out_map,
+                                                     const __grid_constant__ LineArgs a) {
+  using D = LGeo<M>;
+  constexpr int R0 = D::R0, T = D::T, L = D::L, PADP = D::PADP;
+  extern __shared__ unsigned char lsm_raw[];
+  char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(lsm_raw) + 1023) & ~uintptr_t(1023));
+  double2* wt = reinterpret_cast<double2*>(base + 2 * D::BUFB);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wt + (D::NW > 0 ? D::NW : 1));
+  const int j = threadIdx.x;
+  __builtin_assume(j < T);
+  const double scale = sqrt(2.0 / (double)M);
+
+  if (j == 0) {
+    prefetch_tmap(&in_map);
+    prefetch_tmap(&out_map);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  long item = blockIdx.x;
+  if (j == 0 && item < a.nitems) line_issue_load<M, AX>(&in_map, a, item, base, &bar[0]);
+
+  for (int it = 0; item < a.nitems; ++it, item += gridDim.x) {
+    const int cur = it & 1;
+    char* cb = base + cur * D::BUFB;
+    double2* buf = reinterpret_cast<double2*>(cb);
+    const long next = item + gridDim.x;
+    if (j == 0 && next < a.nitems) {
+      bulk_wait_read0();  // the previous item's stores have left the other buffer
+      line_issue_load<M, AX>(&in_map, a, next, base + (cur ^ 1) * D::BUFB, &bar[cur ^ 1]);
+    }
+    // the twiddle / sine tables are re-read every item: an opaque copy of the pointers keeps
+    // the compiler from hoisting ~30 loop-invariant twiddles into registers for the whole loop
+    const double2* tw = a.tw;
+    const double* sinp = a.sinp;
+    asm volatile("" : "+l"(tw), "+l"(sinp));
+    mbar_wait(&bar[cur], (uint32_t)((it >> 1) & 1));
+
+    double2 out[2 * L];
+#pragma unroll 1
+    for (int pass = 0; pass < (NL ? 2 : 1); ++pass) {
+      double2 v[R0];
+#pragma unroll
+      for (int r = 0; r < R0; ++r) {
+        const int i = j + T * r;
+        if (i == 0) {
+          v[r] = make_double2(0.0, 0.0);
+        } else if (AX == AX_ROW && pass == 0) {
+          const uint32_t o1 = row_sw(i - 1), o2 = row_sw(M - i - 1);
+          const double2 z = make_double2(*reinterpret_cast<const double*>(cb + o1),
+                                         *reinterpret_cast<const double*>(cb + M * 8 + o1));
+          const double2 zm = make_double2(*reinterpret_cast<const double*>(cb + o2),
+                                          *reinterpret_cast<const double*>(cb + M * 8 + o2));
+          v[r] = lpre(z, zm, __ldg(sinp + i));
+        } else if (pass == 0) {  // COL raw: linear, grid row p at buf[p]
+          v[r] = lpre(buf[i - 1], buf[M - i - 1], __ldg(sinp + i));
+        } else {
+          v[r] = lpre(buf[lswz<PADP>(i - 1)], buf[lswz<PADP>(M - i - 1)], __ldg(sinp + i));
+        }
+      }
+      lcore<M>(v, buf, wt, tw, out);
+      if (NL && pass == 0) {
+        __syncthreads();  // everyone has read (e, w) of pass 0
+#pragma unroll
+        for (int q = 0; q < 2 * L; ++q)
+          buf[lswz<PADP>(2 * j * L + q)] =
+              make_double2(poly_eval(a.poly, scale * out[q].x), poly_eval(a.poly, scale * out[q].y));
+        __syncthreads();
+      }
+    }
+    __syncthreads();  // (e, w) reads done before the result overwrites the buffer
+    if constexpr (AX == AX_ROW) {
+      // rows a / b in the 128B-swizzled box layout: positions [2jL, 2jL+2L) as 16-byte pairs
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        const int x = 2 * j * L + 2 * l;
+        const uint32_t off = row_sw(x);
+        *reinterpret_cast<double2*>(cb + off) = make_double2(scale * out[2 * l].x, scale * out[2 * l + 1].x);
+        *reinterpret_cast<double2*>(cb + M * 8 + off) = make_double2(scale * out[2 * l].y, scale * out[2 * l + 1].y);
+      }
+    } else {
+      // chunk -> padded layout (conflict free), then compact in place to the linear layout
+      // the TMA store reads (position p at buf[p]); every thread moves positions j + T r
+#pragma unroll
+      for (int q = 0; q < 2 * L; ++q) buf[lswz<PADP>(2 * j * L + q)] = make_double2(scale * out[q].x, scale * out[q].y);
+      __syncthreads();
+      double2 c[R0];
+#pragma unroll
+      for (int r = 0; r < R0; ++r) c[r] = buf[lswz<PADP>(j + T * r)];
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < R0; ++r) buf[j + T * r] = c[r];
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (j == 0) line_issue_store<M, AX>(&out_map, a, item, cb);
+  }
+  if (j == 0) bulk_wait0();
+}
+
+// ---------------------------------------------------------------------------------------
+// host side: tensor maps and launches
+// ---------------------------------------------------------------------------------------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(p);
+  });
+  return fn;
+}
+
+bool line_supported(const Geom& g) {
+  return g.M >= 256 && g.M <= 4096 && encode_fn() != nullptr;
+}
+
+// 4-D fp64 tensor map: dims d[0..3] (d[0] contiguous), byte strides s[1..3], box b[0..3]
+static cudaError_t make_map(CUtensorMap* m, const double* ptr, const cuuint64_t d[4], const cuuint64_t s[3],
+                            const cuuint32_t b[4], bool sw128) {
+  EncodeTiledFn f = encode_fn();
+  if (!f) return cudaErrorNotSupported;
+  const cuuint32_t es[4] = {1, 1, 1, 1};
+  CUresult r = f(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, const_cast<double*>(ptr), d, s, b, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, sw128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS && getenv("EXPD_DEBUG"))
+    fprintf(stderr, "expd: cuTensorMapEncodeTiled failed (%d): dims %llu %llu %llu %llu box %u %u %u %u\n", (int)r,
+            (unsigned long long)d[0], (unsigned long long)d[1], (unsigned long long)d[2], (unsigned long long)d[3],
+            b[0], b[1], b[2], b[3]);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+// Tensor map of nslices padded spectral slices for one axis pass.
+static cudaError_t axis_map(CUtensorMap* m, const Geom& g, int ax, const double* ptr, long nslices) {
+  const cuuint64_t M = (cuuint64_t)g.M, n = (cuuint64_t)g.n;
+  const cuuint64_t rows = (cuuint64_t)(g.npad / g.M);  // spectral rows per slice
+  const cuuint64_t sl = (cuuint64_t)g.npad * 8;
+  if (ax == AX_ROW) {
+    const cuuint64_t d[4] = {16, M / 16, rows, (cuuint64_t)nslices};
+    const cuuint64_t s[3] = {128, M * 8, sl};
+    const cuuint32_t b[4] = {16, (cuuint32_t)(M / 16), 1, 1};
+    return make_map(m, ptr, d, s, b, true);
+  }
+  const cuuint64_t nz = g.dim == 3 ? n : 1;
+  const cuuint64_t d[4] = {M, n, nz, (cuuint64_t)nslices};
+  const cuuint64_t s[3] = {M * 8, n * M * 8, sl};
+  if (ax == AX_COL_Y) {
+    const cuuint32_t b[4] = {2, (cuuint32_t)CBR, 1, 1};
+    return make_map(m, ptr, d, s, b, false);
+  }
+  const cuuint32_t b[4] = {2, 1, (cuuint32_t)CBR, 1};
+  return make_map(m, ptr, d, s, b, false);
+}
+
+static int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+template <int M, int AX, bool NL>
+static cudaError_t launch_line(const Geom& g, const DstTables& t, const Poly& P, const double* in, double* out,
+                               long nslices, cudaStream_t st) {
+  using D = LGeo<M>;
+  auto k = k_line<M, AX, NL>;
+  static int per_sm = 0;  // per instantiation
+  if (!per_sm) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)D::SMEM);
+    if (e != cudaSuccess) return e;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, D::T, D::SMEM);
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) per_sm = 1;
+  }
+  CUtensorMap mi, mo;
+  cudaError_t e = axis_map(&mi, g, AX, in, nslices);
+  if (e != cudaSuccess) return e;
+  if ((e = axis_map(&mo, g, AX, out, nslices)) != cudaSuccess) return e;
+  LineArgs a{};
+  const int rows = (int)(g.npad / g.M);
+  if (AX == AX_ROW) {
+    a.inner = (rows + 1) / 2;
+    a.per_slice = a.inner;
+  } else {
+    a.inner = g.M / 2;
+    a.per_slice = a.inner * (g.dim == 3 ? g.n : 1);
+  }
+  a.rows = rows;
+  a.nitems = (long)a.per_slice * nslices;
+  a.tw = t.tw;
+  a.sinp = t.sinp;
+  a.poly = P;
+  long grid = (long)sm_count() * per_sm;
+  if (grid > a.nitems) grid = a.nitems;
+  if (grid < 1) return cudaSuccess;
+  k<<<(unsigned)grid, D::T, D::SMEM, st>>>(mi, mo, a);
+  return cudaGetLastError();
+}
+
+template <int M>
+static cudaError_t line_pass_m(const Geom& g, const DstTables& t, const Poly& P, int ax, bool nl, const double* in,
+                               double* out, long nslices, cudaStream_t st) {
+  if (ax == AX_ROW) return launch_line<M, AX_ROW, false>(g, t, P, in, out, nslices, st);
+  if (ax == AX_COL_Y)
+    return nl ? launch_line<M, AX_COL_Y, true>(g, t, P, in, out, nslices, st)
+              : launch_line<M, AX_COL_Y, false>(g, t, P, in, out, nslices, st);
+  return nl ? launch_line<M, AX_COL_Z, true>(g, t, P, in, out, nslices, st)
+            : launch_line<M, AX_COL_Z, false>(g, t, P, in, out, nslices, st);
+}
+
+// One axis pass (ax: 0 = x rows, 1 = y, 2 = z) of nslices padded spectral slices; nl
+// (strided axes only) fuses [V, N, V].  in and out may alias (each item reads and writes
+// only its own lines).
+cudaError_t line_pass(const Geom& g, const DstTables& t, const Poly& P, int ax, bool nl, const double* in,
+                      double* out, long nslices, cudaStream_t st) {
+  if (nslices <= 0) return cudaSuccess;
+  if (ax == AX_ROW && nl) return cudaErrorInvalidValue;
+  switch (g.M) {
+    case 256: return line_pass_m<256>(g, t, P, ax, nl, in, out, nslices, st);
+    case 512: return line_pass_m<512>(g, t, P, ax, nl, in, out, nslices, st);
+    case 1024: return line_pass_m<1024>(g, t, P, ax, nl, in, out, nslices, st);
+    case 2048: return line_pass_m<2048>(g, t, P, ax, nl, in, out, nslices, st);
+    case 4096: return line_pass_m<4096>(g, t, P, ax, nl, in, out, nslices, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace expd

@@ -45,6 +45,7 @@ EXPORTS = [
     "expd_store_state",
     "expd_sweep_kernel_launches",
     "expd_dst",
+    "expd_nonlin_hat",
     "expd_set_profiling",
     "expd_sweep_stage_ms",
     "expd_debug_kernel_ms",
@@ -116,6 +117,7 @@ def load_library(path: str = LIB_PATH):
         "expd_store_state": (C.c_int, [vp, vp]),
         "expd_sweep_kernel_launches": (C.c_int, [vp]),
         "expd_dst": (C.c_int, [vp, vp, vp, C.c_long]),
+        "expd_nonlin_hat": (C.c_int, [vp, vp, vp, C.c_long]),
         "expd_set_profiling": (C.c_int, [vp, C.c_int]),
         "expd_sweep_stage_ms": (C.c_int, [vp, dp, dp]),
         "expd_debug_kernel_ms": (C.c_int, [vp, C.c_int, C.c_long, C.c_int, dp]),
@@ -286,6 +288,13 @@ class Plan:
         out = torch.empty_like(x) if out is None else out
         ns = x.numel() // self.problem.N
         self._check(self.lib.expd_dst(self.handle, _ptr(x), _ptr(out), ns))
+        return out
+
+    def nonlin_hat(self, uhat: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+        """V N(V uhat) for a stack of DST-coefficient slices [..., n, ..., n] (stage 3)."""
+        out = torch.empty_like(uhat) if out is None else out
+        ns = uhat.numel() // self.problem.N
+        self._check(self.lib.expd_nonlin_hat(self.handle, _ptr(uhat), _ptr(out), ns))
         return out
 
     def set_profiling(self, enable: bool = True):

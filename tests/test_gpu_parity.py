@@ -68,6 +68,34 @@ def test_dst_full_size_sampled(orc, dim, n):
 
 
 # ------------------------------------------------------------------------------------------
+# stage 3: N-hat = V N(V u-hat) (K4; the TMA line kernels for n+1 >= 256)
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("dim,n,ns", [(2, 31, 3), (2, 255, 3), (2, 511, 2), (3, 255, 1), (2, 1023, 1)])
+def test_nonlin_hat_parity(orc, dim, n, ns):
+    cfg = synth.Config("t", dim, n, 1.0, 1.0, 1.0, 8, 1e-2, q=(0.0, 0.0, 0.0, -1.0), scheme=1)
+    plan = Plan(Problem.from_config(cfg))
+    s = orc.spec(cfg)
+    uh = np.random.default_rng(dim * 7 + n).standard_normal((ns,) + cfg.shape) / np.sqrt(cfg.N)
+    got = H(plan.nonlin_hat(T(uh)))
+    for i in range(ns):
+        want = orc.dst(s, orc.nonlin(s, orc.dst(s, uh[i])))
+        assert relmax(got[i], want) < 1e-12
+
+
+def test_nonlin_hat_full_size_sampled(orc):
+    # c5's slice (2047^2): the full-size launch configuration of the sweep's stage 3
+    cfg = synth.CONFIGS["c5"].scaled(2047, 4)
+    plan = Plan(Problem.from_config(cfg))
+    s = orc.spec(cfg)
+    uh = np.random.default_rng(55).standard_normal((2,) + cfg.shape) / np.sqrt(cfg.N)
+    got = H(plan.nonlin_hat(T(uh))).reshape(2, -1)
+    idx = np.random.default_rng(56).integers(0, cfg.N, 24)
+    for i in range(2):
+        want = orc.dst_sample(s, orc.nonlin(s, orc.dst(s, uh[i])), idx)
+        assert np.abs(got[i][idx] - want).max() < 1e-12 * np.abs(got[i]).max()
+
+
+# ------------------------------------------------------------------------------------------
 # preconditioner apply (Steps (a)-(c)) and residual
 # ------------------------------------------------------------------------------------------
 PRECOND_CASES = [
@@ -122,7 +150,8 @@ def test_precond_zero_and_alias(orc):
 # ------------------------------------------------------------------------------------------
 # solvers
 # ------------------------------------------------------------------------------------------
-SOLVE_CASES = [("c1", None, None), ("c2", 63, 64), ("c3", 63, 128), ("c5", 63, 256), ("c4", 15, 64)]
+SOLVE_CASES = [("c1", None, None), ("c2", 63, 64), ("c3", 63, 128), ("c5", 63, 256), ("c4", 15, 64),
+               ("c3", 255, 16), ("c5", 255, 16)]
 
 
 @pytest.mark.parametrize("name,n,nt", SOLVE_CASES)
