@@ -25,8 +25,19 @@ struct Poly {
 };
 #ifdef __CUDACC__
 __device__ __forceinline__ double poly_eval(const Poly& P, double u) {
-  double acc = 0.0;
-  for (int k = P.npoly - 1; k >= 0; --k) acc = fma(acc, u, P.q[k]);
+  // straight-line Horner (unused coefficients are 0): no loop, no dynamic indexing
+  double acc = P.q[3];
+  acc = fma(acc, u, P.q[2]);
+  acc = fma(acc, u, P.q[1]);
+  acc = fma(acc, u, P.q[0]);
+  if (P.npoly > 4) {
+    double hi = P.q[7];
+    hi = fma(hi, u, P.q[6]);
+    hi = fma(hi, u, P.q[5]);
+    hi = fma(hi, u, P.q[4]);
+    const double u2 = u * u;
+    acc = fma(hi, u2 * u2, acc);
+  }
   return acc;
 }
 #endif

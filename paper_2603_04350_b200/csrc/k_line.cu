@@ -45,23 +45,25 @@ template <> struct LPlan<1024> { static constexpr int R0 = 16, RM1 = 8,  RL = 8;
 template <> struct LPlan<2048> { static constexpr int R0 = 16, RM1 = 16, RL = 8; };
 template <> struct LPlan<4096> { static constexpr int R0 = 16, RM1 = 16, RL = 16; };
 
-template <int M>
+template <int M, int G, int NBUF>
 struct LGeo {
   static constexpr int R0 = LPlan<M>::R0, RM1 = LPlan<M>::RM1, RL = LPlan<M>::RL;
   static_assert(R0 * RM1 * RL == M, "radix plan");
-  static constexpr int T = M / R0;            // threads per line pair (= CTA size)
+  static_assert(M % 256 == 0, "COL boxes of 256 rows");
+  static constexpr int T = M / R0;            // threads per line pair
+  static constexpr int THREADS = G * T;       // G line pairs per item (g = tid % G)
   static constexpr int NSL = M / RL;          // Ns of the last stage
   static constexpr int L = (M / 2) / T;       // k-values per thread in the prefix sum (= R0/2)
   static constexpr int PADP = R0;             // one pad slot per PADP positions
   static constexpr int SW = M + M / PADP;     // padded positions per line pair
-  static constexpr int NW = T / 32;           // warps per CTA
-  static constexpr size_t BUFB = ((size_t)SW * 16 + 1023) / 1024 * 1024;  // bytes per buffer (1 KB aligned)
-  static_assert(M % 256 == 0, "COL boxes of 256 rows");
-  static constexpr size_t SMEM = 1024 + 2 * BUFB + 16 * (NW > 0 ? NW : 1) + 16;
+  static constexpr int JW = 32 / G;           // threads of one line pair inside a warp
+  static constexpr int NWB = T / JW;          // warp blocks per line pair
+  static constexpr size_t BUFB = ((size_t)G * SW * 16 + 1023) / 1024 * 1024;  // bytes per buffer
+  static constexpr size_t SMEM = 1024 + NBUF * BUFB + 16 * (size_t)(NWB * G) + 16;
   // resident CTAs per SM: shared memory (228 KB, 1 KB reserved per CTA) and >= 160 registers
   static constexpr int MINB_SMEM = (int)((228 * 1024) / (SMEM + 1024));
-  static constexpr int MINB_REG = 65536 / (T * 160);
-  static constexpr int MINB = MINB_SMEM < MINB_REG ? (MINB_SMEM > 0 ? MINB_SMEM : 1) : MINB_REG;
+  static constexpr int MINB_REG = 65536 / (THREADS * 160);
+  static constexpr int MINB = MINB_SMEM < MINB_REG ? (MINB_SMEM > 0 ? MINB_SMEM : 1) : (MINB_REG > 0 ? MINB_REG : 1);
 };
 
 enum LineAxis { AX_ROW = 0, AX_COL_Y = 1, AX_COL_Z = 2 };
@@ -70,7 +72,7 @@ constexpr int CBR = 256;  // grid rows per TMA box of a strided-axis (COL) item
 struct LineArgs {
   long nitems;
   int per_slice;   // items per slice
-  int inner;       // ROW: row pairs per slice; COL: column pairs per outer index
+  int inner;       // ROW: row pairs per slice; COL: column-pair groups per outer index
   int rows;        // ROW: rows per slice (for the incomplete last pair)
   const double2* tw;   // [M] exp(-2 pi i q / M)
   const double* sinp;  // [M] sin(pi i / M)
@@ -103,21 +105,27 @@ __device__ __forceinline__ void ltw(const double2* __restrict__ tw, int b, doubl
   for (int r = 2; r < R; ++r) t[r] = (r % 2 == 0) ? cmul(t[r / 2], t[r / 2]) : cmul(t[r - 1], t[1]);
 }
 
-// In-place middle Stockham stage (radix R, NS) of the line pair in buf (padded layout).
-template <int M, int R, int NS>
+// position p of line pair g in the padded work layout [SW][G]
+template <int M, int G>
+__device__ __forceinline__ double2& lat(double2* buf, int p, int g) {
+  return buf[lswz<LGeo<M, G, 1>::PADP>(p) * G + g];
+}
+
+// In-place middle Stockham stage (radix R, NS) of the G line pairs in buf.
+template <int M, int G, int R, int NS>
 __device__ __forceinline__ void lmid(double2* buf, const double2* __restrict__ tw) {
-  using D = LGeo<M>;
-  constexpr int JOBS = M / R;
-  constexpr int JT = (JOBS + D::T - 1) / D::T;
+  using D = LGeo<M, G, 1>;
+  constexpr int JOBS = G * (M / R);
+  constexpr int JT = (JOBS + D::THREADS - 1) / D::THREADS;
   constexpr int TWS = M / (NS * R);
   double2 v[JT][R];
 #pragma unroll
   for (int jt = 0; jt < JT; ++jt) {
-    const int jm = threadIdx.x + jt * D::T;
-    if (JOBS % D::T == 0 || jm < JOBS) {
-      const int k = jm % NS;
+    const int J = threadIdx.x + jt * D::THREADS;
+    if (JOBS % D::THREADS == 0 || J < JOBS) {
+      const int g = J % G, jm = J / G, k = jm % NS;
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[jt][r] = buf[lswz<D::PADP>(jm + r * (M / R))];
+      for (int r = 0; r < R; ++r) v[jt][r] = lat<M, G>(buf, jm + r * (M / R), g);
       double2 t[R];
       ltw<R>(tw, k * TWS, t);
 #pragma unroll
@@ -128,49 +136,50 @@ __device__ __forceinline__ void lmid(double2* buf, const double2* __restrict__ t
   __syncthreads();
 #pragma unroll
   for (int jt = 0; jt < JT; ++jt) {
-    const int jm = threadIdx.x + jt * D::T;
-    if (JOBS % D::T == 0 || jm < JOBS) {
-      const int k = jm % NS, base = (jm / NS) * NS * R + k;
+    const int J = threadIdx.x + jt * D::THREADS;
+    if (JOBS % D::THREADS == 0 || J < JOBS) {
+      const int g = J % G, jm = J / G, k = jm % NS, base = (jm / NS) * NS * R + k;
 #pragma unroll
-      for (int r = 0; r < R; ++r) buf[lswz<D::PADP>(base + r * NS)] = v[jt][r];
+      for (int r = 0; r < R; ++r) lat<M, G>(buf, base + r * NS, g) = v[jt][r];
     }
   }
   __syncthreads();
 }
 
-// DST core of one line pair: stage-0 inputs y_i (i = j + T r) in v; leaves the unscaled
-// F at natural positions [2jL, 2jL + 2L) in out (F_m sits at position m-1; position M-1
-// is the spectral pad and returns 0).  Starts with a barrier (buf may still be read by
-// the caller's stage-0 loads) and ends with buf free for the caller.
-template <int M>
-__device__ __forceinline__ void lcore(double2 (&v)[LGeo<M>::R0], double2* buf, double2* wt,
-                                      const double2* __restrict__ tw, double2 (&out)[2 * LGeo<M>::L]) {
-  using D = LGeo<M>;
+// DST core of G line pairs: thread (g, j) holds the stage-0 inputs y_i (i = j + T r) of
+// line pair g in v; leaves the unscaled F at natural positions [2jL, 2jL + 2L) in out
+// (F_m sits at position m-1; position M-1 is the spectral pad and returns 0).  Starts with
+// a barrier (buf may still be read by the caller's stage-0 loads).
+template <int M, int G>
+__device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* buf, double2* wt,
+                                      const double2* __restrict__ tw, double2 (&out)[2 * LGeo<M, G, 1>::L]) {
+  using D = LGeo<M, G, 1>;
   constexpr int R0 = D::R0, RL = D::RL, NSL = D::NSL, T = D::T, L = D::L, PADP = D::PADP;
-  const int j = threadIdx.x;
+  const int g = threadIdx.x % G, j = threadIdx.x / G;
   DFT<R0, -1>::run(v);
   __syncthreads();
   {
-    double2* o0 = buf + lswz<PADP>(j * R0);  // R0 = PADP consecutive positions: contiguous
+    double2* o0 = buf + lswz<PADP>(j * R0) * G + g;  // R0 = PADP consecutive positions: linear
 #pragma unroll
-    for (int r = 0; r < R0; ++r) o0[r] = v[r];
+    for (int r = 0; r < R0; ++r) o0[r * G] = v[r];
   }
   __syncthreads();
-  lmid<M, D::RM1, R0>(buf, tw);
+  lmid<M, G, D::RM1, R0>(buf, tw);
   // last stage on Hermitian partner jobs (ja, jb): frequency sets k = ja + NSL r and
   // jb + NSL r pair up as k <-> M - k; then the unpack into e_k (position 2k-1), w_k (2k)
-  constexpr int PJOBS = NSL / 2;
-  constexpr int PJT = (PJOBS + T - 1) / T;
+  constexpr int PJOBS = G * (NSL / 2);
+  constexpr int PJT = (PJOBS + D::THREADS - 1) / D::THREADS;
   double2 va[PJT][RL], vb[PJT][RL];
 #pragma unroll
   for (int pt = 0; pt < PJT; ++pt) {
-    const int pj = j + pt * T;
-    if (PJOBS % T == 0 || pj < PJOBS) {
+    const int PJ = threadIdx.x + pt * D::THREADS;
+    if (PJOBS % D::THREADS == 0 || PJ < PJOBS) {
+      const int gg = PJ % G, pj = PJ / G;
       const int ja = pj, jb = pj == 0 ? NSL / 2 : NSL - pj;
 #pragma unroll
       for (int r = 0; r < RL; ++r) {
-        va[pt][r] = buf[lswz<PADP>(ja + r * NSL)];
-        vb[pt][r] = buf[lswz<PADP>(jb + r * NSL)];
+        va[pt][r] = lat<M, G>(buf, ja + r * NSL, gg);
+        vb[pt][r] = lat<M, G>(buf, jb + r * NSL, gg);
       }
       double2 t[RL];
       ltw<RL>(tw, ja, t);
@@ -186,49 +195,51 @@ __device__ __forceinline__ void lcore(double2 (&v)[LGeo<M>::R0], double2* buf, d
   __syncthreads();
 #pragma unroll
   for (int pt = 0; pt < PJT; ++pt) {
-    const int pj = j + pt * T;
-    if (PJOBS % T == 0 || pj < PJOBS) {
+    const int PJ = threadIdx.x + pt * D::THREADS;
+    if (PJOBS % D::THREADS == 0 || PJ < PJOBS) {
+      const int gg = PJ % G, pj = PJ / G;
       const int ja = pj, jb = pj == 0 ? NSL / 2 : NSL - pj;
 #pragma unroll
       for (int r = 0; r < RL / 2; ++r) {
         double2 e, w;
         const int ka = ja + NSL * r;
         lunpack(va[pt][r], pj == 0 ? va[pt][(RL - r) % RL] : vb[pt][RL - 1 - r], ka == 0, e, w);
-        if (ka >= 1) buf[lswz<PADP>(2 * ka - 1)] = e;
-        buf[lswz<PADP>(2 * ka)] = w;
+        if (ka >= 1) lat<M, G>(buf, 2 * ka - 1, gg) = e;
+        lat<M, G>(buf, 2 * ka, gg) = w;
         const int kb = jb + NSL * r;
         lunpack(vb[pt][r], pj == 0 ? vb[pt][RL - 1 - r] : va[pt][RL - 1 - r], false, e, w);
-        buf[lswz<PADP>(2 * kb - 1)] = e;
-        buf[lswz<PADP>(2 * kb)] = w;
+        lat<M, G>(buf, 2 * kb - 1, gg) = e;
+        lat<M, G>(buf, 2 * kb, gg) = w;
       }
     }
   }
   __syncthreads();
-  // prefix sum: thread j owns k in [jL, jL + L) -> positions [2jL, 2jL + 2L):
+  // prefix sum: thread (g, j) owns k in [jL, jL + L) -> positions [2jL, 2jL + 2L):
   // out[2l] = F_{2k+1} = sum_{k' <= k} w_k', out[2l+1] = F_{2k+2} = e_{k+1}
   double2 tot = make_double2(0.0, 0.0);
   {
-    const double2* P = buf + lswz<PADP>(2 * j * L);  // 2L <= PADP consecutive positions
+    const double2* P = buf + lswz<PADP>(2 * j * L) * G + g;  // 2L <= PADP consecutive positions
 #pragma unroll
     for (int l = 0; l < L; ++l) {
-      tot = cadd(tot, P[2 * l]);
+      tot = cadd(tot, P[(2 * l) * G]);
       out[2 * l] = tot;
-      out[2 * l + 1] = (j == T - 1 && l == L - 1) ? make_double2(0.0, 0.0) : P[2 * l + 1];
+      out[2 * l + 1] = (j == T - 1 && l == L - 1) ? make_double2(0.0, 0.0) : P[(2 * l + 1) * G];
     }
   }
   double2 inc = tot;
-  const int lane = j & 31;
+  const int lane = threadIdx.x & 31;
 #pragma unroll
-  for (int d = 1; d < 32 && d < T; d <<= 1) {
-    double ox = __shfl_up_sync(0xffffffffu, inc.x, d);
-    double oy = __shfl_up_sync(0xffffffffu, inc.y, d);
-    if (lane >= d) inc = cadd(inc, make_double2(ox, oy));
+  for (int d = 1; d < D::JW && d < T; d <<= 1) {
+    double ox = __shfl_up_sync(0xffffffffu, inc.x, d * G);
+    double oy = __shfl_up_sync(0xffffffffu, inc.y, d * G);
+    if (lane >= d * G) inc = cadd(inc, make_double2(ox, oy));
   }
   double2 off = csub(inc, tot);
-  if constexpr (D::NW > 1) {
-    if (lane == 31) wt[j >> 5] = inc;
+  if constexpr (D::NWB > 1) {
+    const int jw = j / D::JW;
+    if (j % D::JW == D::JW - 1) wt[jw * G + g] = inc;
     __syncthreads();
-    for (int b = 0; b < (j >> 5); ++b) off = cadd(off, wt[b]);
+    for (int b = 0; b < jw; ++b) off = cadd(off, wt[b * G + g]);
   }
 #pragma unroll
   for (int l = 0; l < L; ++l) out[2 * l] = cadd(out[2 * l], off);
@@ -237,55 +248,53 @@ __device__ __forceinline__ void lcore(double2 (&v)[LGeo<M>::R0], double2* buf, d
 // ---------------------------------------------------------------------------------------
 // the persistent line kernel
 // ---------------------------------------------------------------------------------------
-template <int AX>
+template <int AX, int G>
 __device__ __forceinline__ void line_coords(const LineArgs& a, long item, int& c0, int& c1, int& c2, int& c3) {
   const long s = item / a.per_slice;
   const int w = (int)(item % a.per_slice);
   if constexpr (AX == AX_ROW) {
     c0 = 0; c1 = 0; c2 = 2 * w; c3 = (int)s;  // rows 2w, 2w+1 of slice s
   } else {
-    const int o = w / a.inner, cp = w % a.inner;
-    c0 = 2 * cp;
+    const int o = w / a.inner, cg = w % a.inner;
+    c0 = 2 * G * cg;
     if constexpr (AX == AX_COL_Y) { c1 = 0; c2 = o; }
     else { c1 = o; c2 = 0; }
     c3 = (int)s;
   }
 }
 
-template <int M, int AX>
+template <int M, int AX, int G>
 __device__ __forceinline__ void line_issue_load(const CUtensorMap* map, const LineArgs& a, long item, char* buf,
                                                 uint64_t* bar) {
-  using D = LGeo<M>;
   int c0, c1, c2, c3;
-  line_coords<AX>(a, item, c0, c1, c2, c3);
-  mbar_arrive_expect_tx(bar, (uint32_t)(M * 16));
+  line_coords<AX, G>(a, item, c0, c1, c2, c3);
+  mbar_arrive_expect_tx(bar, (uint32_t)(G * M * 16));
   if constexpr (AX == AX_ROW) {
     tma_load_4d(buf, map, bar, 0, 0, c2, c3);
     tma_load_4d(buf + M * 8, map, bar, 0, 0, c2 + 1, c3);
   } else {
-    // linear raw layout: grid row p at byte 16 p (boxes of CBR rows, 4 KB aligned)
+    // linear raw layout [row][G]: grid row p of pair g at double2 p*G + g (boxes of CBR rows)
 #pragma unroll
     for (int b = 0; b < M / CBR; ++b) {
-      char* dst = buf + (size_t)b * CBR * 16;
+      char* dst = buf + (size_t)b * CBR * 16 * G;
       if constexpr (AX == AX_COL_Y) tma_load_4d(dst, map, bar, c0, b * CBR, c2, c3);
       else tma_load_4d(dst, map, bar, c0, c1, b * CBR, c3);
     }
   }
 }
 
-template <int M, int AX>
+template <int M, int AX, int G>
 __device__ __forceinline__ void line_issue_store(const CUtensorMap* map, const LineArgs& a, long item,
                                                  const char* buf) {
-  using D = LGeo<M>;
   int c0, c1, c2, c3;
-  line_coords<AX>(a, item, c0, c1, c2, c3);
+  line_coords<AX, G>(a, item, c0, c1, c2, c3);
   if constexpr (AX == AX_ROW) {
     tma_store_4d(map, buf, 0, 0, c2, c3);
     if (c2 + 1 < a.rows) tma_store_4d(map, buf + M * 8, 0, 0, c2 + 1, c3);
   } else {
 #pragma unroll
     for (int b = 0; b < M / CBR; ++b) {
-      const char* src = buf + (size_t)b * CBR * 16;
+      const char* src = buf + (size_t)b * CBR * 16 * G;
       if constexpr (AX == AX_COL_Y) tma_store_4d(map, src, c0, b * CBR, c2, c3);
       else tma_store_4d(map, src, c0, c1, b * CBR, c3);
     }
@@ -293,21 +302,25 @@ __device__ __forceinline__ void line_issue_store(const CUtensorMap* map, const L
   bulk_commit();
 }
 
-template <int M, int AX, bool NL>
-__global__ void __launch_bounds__(LGeo<M>::T, LGeo<M>::MINB) k_line(const __grid_constant__ CUtensorMap in_map,
-                                                     const __grid_constant__ CUtensorMap out_map,
-                                                     const __grid_constant__ LineArgs a) {
-  using D = LGeo<M>;
+// G line pairs per item, NBUF shared-memory buffers (2: the next item's TMA load overlaps
+// this item's transform; 1: overlap comes from the other CTAs on the SM).
+template <int M, int AX, bool NL, int G, int NBUF>
+__global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::MINB)
+    k_line(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
+           const __grid_constant__ LineArgs a) {
+  using D = LGeo<M, G, NBUF>;
+  static_assert(AX != AX_ROW || G == 1, "row items are one row pair");
   constexpr int R0 = D::R0, T = D::T, L = D::L, PADP = D::PADP;
   extern __shared__ unsigned char lsm_raw[];
   char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(lsm_raw) + 1023) & ~uintptr_t(1023));
-  double2* wt = reinterpret_cast<double2*>(base + 2 * D::BUFB);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(wt + (D::NW > 0 ? D::NW : 1));
-  const int j = threadIdx.x;
-  __builtin_assume(j < T);
+  double2* wt = reinterpret_cast<double2*>(base + NBUF * D::BUFB);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wt + D::NWB * G);
+  const int tid = threadIdx.x;
+  __builtin_assume(tid < D::THREADS);
+  const int g = tid % G, j = tid / G;
   const double scale = sqrt(2.0 / (double)M);
 
-  if (j == 0) {
+  if (tid == 0) {
     prefetch_tmap(&in_map);
     prefetch_tmap(&out_map);
     mbar_init(&bar[0], 1);
@@ -316,52 +329,58 @@ __global__ void __launch_bounds__(LGeo<M>::T, LGeo<M>::MINB) k_line(const __grid
   }
   __syncthreads();
   long item = blockIdx.x;
-  if (j == 0 && item < a.nitems) line_issue_load<M, AX>(&in_map, a, item, base, &bar[0]);
+  if (tid == 0 && item < a.nitems) line_issue_load<M, AX, G>(&in_map, a, item, base, &bar[0]);
 
   for (int it = 0; item < a.nitems; ++it, item += gridDim.x) {
-    const int cur = it & 1;
+    const int cur = NBUF == 2 ? (it & 1) : 0;
     char* cb = base + cur * D::BUFB;
     double2* buf = reinterpret_cast<double2*>(cb);
     const long next = item + gridDim.x;
-    if (j == 0 && next < a.nitems) {
+    if (NBUF == 2 && tid == 0 && next < a.nitems) {
       bulk_wait_read0();  // the previous item's stores have left the other buffer
-      line_issue_load<M, AX>(&in_map, a, next, base + (cur ^ 1) * D::BUFB, &bar[cur ^ 1]);
+      line_issue_load<M, AX, G>(&in_map, a, next, base + (cur ^ 1) * D::BUFB, &bar[cur ^ 1]);
     }
     // the twiddle / sine tables are re-read every item: an opaque copy of the pointers keeps
     // the compiler from hoisting ~30 loop-invariant twiddles into registers for the whole loop
     const double2* tw = a.tw;
     const double* sinp = a.sinp;
     asm volatile("" : "+l"(tw), "+l"(sinp));
-    mbar_wait(&bar[cur], (uint32_t)((it >> 1) & 1));
+    mbar_wait(&bar[cur], (uint32_t)((NBUF == 2 ? (it >> 1) : it) & 1));
 
     double2 out[2 * L];
+    // NL: two passes [V, N, V] through ONE copy of the transform code (the trip count is
+    // opaque to the compiler, which would otherwise unroll it into ~8000 instructions and
+    // thrash the instruction cache)
+    int npass = NL ? 2 : 1;
+    asm volatile("" : "+r"(npass));
 #pragma unroll 1
-    for (int pass = 0; pass < (NL ? 2 : 1); ++pass) {
+    for (int pass = 0; pass < npass; ++pass) {
       double2 v[R0];
 #pragma unroll
       for (int r = 0; r < R0; ++r) {
         const int i = j + T * r;
         if (i == 0) {
           v[r] = make_double2(0.0, 0.0);
-        } else if (AX == AX_ROW && pass == 0) {
+        } else if (AX == AX_ROW) {
           const uint32_t o1 = row_sw(i - 1), o2 = row_sw(M - i - 1);
           const double2 z = make_double2(*reinterpret_cast<const double*>(cb + o1),
                                          *reinterpret_cast<const double*>(cb + M * 8 + o1));
           const double2 zm = make_double2(*reinterpret_cast<const double*>(cb + o2),
                                           *reinterpret_cast<const double*>(cb + M * 8 + o2));
           v[r] = lpre(z, zm, __ldg(sinp + i));
-        } else if (pass == 0) {  // COL raw: linear, grid row p at buf[p]
-          v[r] = lpre(buf[i - 1], buf[M - i - 1], __ldg(sinp + i));
         } else {
-          v[r] = lpre(buf[lswz<PADP>(i - 1)], buf[lswz<PADP>(M - i - 1)], __ldg(sinp + i));
+          // pass 0: raw [row][G] linear; pass 1: the padded layout written by the N step
+          const int p1 = i - 1, p2 = M - i - 1;
+          const int q1 = pass ? lswz<PADP>(p1) : p1, q2 = pass ? lswz<PADP>(p2) : p2;
+          v[r] = lpre(buf[q1 * G + g], buf[q2 * G + g], __ldg(sinp + i));
         }
       }
-      lcore<M>(v, buf, wt, tw, out);
-      if (NL && pass == 0) {
+      lcore<M, G>(v, buf, wt, tw, out);
+      if (NL && pass + 1 < npass) {
         __syncthreads();  // everyone has read (e, w) of pass 0
 #pragma unroll
         for (int q = 0; q < 2 * L; ++q)
-          buf[lswz<PADP>(2 * j * L + q)] =
+          lat<M, G>(buf, 2 * j * L + q, g) =
               make_double2(poly_eval(a.poly, scale * out[q].x), poly_eval(a.poly, scale * out[q].y));
         __syncthreads();
       }
@@ -377,23 +396,29 @@ __global__ void __launch_bounds__(LGeo<M>::T, LGeo<M>::MINB) k_line(const __grid
         *reinterpret_cast<double2*>(cb + M * 8 + off) = make_double2(scale * out[2 * l].y, scale * out[2 * l + 1].y);
       }
     } else {
-      // chunk -> padded layout (conflict free), then compact in place to the linear layout
-      // the TMA store reads (position p at buf[p]); every thread moves positions j + T r
+      // chunk -> padded layout (conflict free), then compact in place to the linear [row][G]
+      // layout the TMA store reads; thread (g, j) moves positions j + T r of pair g
 #pragma unroll
-      for (int q = 0; q < 2 * L; ++q) buf[lswz<PADP>(2 * j * L + q)] = make_double2(scale * out[q].x, scale * out[q].y);
+      for (int q = 0; q < 2 * L; ++q) lat<M, G>(buf, 2 * j * L + q, g) = make_double2(scale * out[q].x, scale * out[q].y);
       __syncthreads();
       double2 c[R0];
 #pragma unroll
-      for (int r = 0; r < R0; ++r) c[r] = buf[lswz<PADP>(j + T * r)];
+      for (int r = 0; r < R0; ++r) c[r] = lat<M, G>(buf, j + T * r, g);
       __syncthreads();
 #pragma unroll
-      for (int r = 0; r < R0; ++r) buf[j + T * r] = c[r];
+      for (int r = 0; r < R0; ++r) buf[(j + T * r) * G + g] = c[r];
     }
     fence_proxy_async_smem();
     __syncthreads();
-    if (j == 0) line_issue_store<M, AX>(&out_map, a, item, cb);
+    if (tid == 0) {
+      line_issue_store<M, AX, G>(&out_map, a, item, cb);
+      if (NBUF == 1 && next < a.nitems) {
+        bulk_wait_read0();  // the store has read the buffer: refill it
+        line_issue_load<M, AX, G>(&in_map, a, next, base, &bar[0]);
+      }
+    }
   }
-  if (j == 0) bulk_wait0();
+  if (tid == 0) bulk_wait0();
 }
 
 // ---------------------------------------------------------------------------------------
@@ -436,8 +461,8 @@ static cudaError_t make_map(CUtensorMap* m, const double* ptr, const cuuint64_t 
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-// Tensor map of nslices padded spectral slices for one axis pass.
-static cudaError_t axis_map(CUtensorMap* m, const Geom& g, int ax, const double* ptr, long nslices) {
+// Tensor map of nslices padded spectral slices for one axis pass (COL: G column pairs).
+static cudaError_t axis_map(CUtensorMap* m, const Geom& g, int ax, const double* ptr, long nslices, int G) {
   const cuuint64_t M = (cuuint64_t)g.M, n = (cuuint64_t)g.n;
   const cuuint64_t rows = (cuuint64_t)(g.npad / g.M);  // spectral rows per slice
   const cuuint64_t sl = (cuuint64_t)g.npad * 8;
@@ -451,10 +476,10 @@ static cudaError_t axis_map(CUtensorMap* m, const Geom& g, int ax, const double*
   const cuuint64_t d[4] = {M, n, nz, (cuuint64_t)nslices};
   const cuuint64_t s[3] = {M * 8, n * M * 8, sl};
   if (ax == AX_COL_Y) {
-    const cuuint32_t b[4] = {2, (cuuint32_t)CBR, 1, 1};
+    const cuuint32_t b[4] = {(cuuint32_t)(2 * G), (cuuint32_t)CBR, 1, 1};
     return make_map(m, ptr, d, s, b, false);
   }
-  const cuuint32_t b[4] = {2, 1, (cuuint32_t)CBR, 1};
+  const cuuint32_t b[4] = {(cuuint32_t)(2 * G), 1, (cuuint32_t)CBR, 1};
   return make_map(m, ptr, d, s, b, false);
 }
 
@@ -469,30 +494,30 @@ static int sm_count() {
   return n;
 }
 
-template <int M, int AX, bool NL>
+template <int M, int AX, bool NL, int G, int NBUF>
 static cudaError_t launch_line(const Geom& g, const DstTables& t, const Poly& P, const double* in, double* out,
                                long nslices, cudaStream_t st) {
-  using D = LGeo<M>;
-  auto k = k_line<M, AX, NL>;
+  using D = LGeo<M, G, NBUF>;
+  auto k = k_line<M, AX, NL, G, NBUF>;
   static int per_sm = 0;  // per instantiation
   if (!per_sm) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)D::SMEM);
     if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, D::T, D::SMEM);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, D::THREADS, D::SMEM);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) per_sm = 1;
   }
   CUtensorMap mi, mo;
-  cudaError_t e = axis_map(&mi, g, AX, in, nslices);
+  cudaError_t e = axis_map(&mi, g, AX, in, nslices, G);
   if (e != cudaSuccess) return e;
-  if ((e = axis_map(&mo, g, AX, out, nslices)) != cudaSuccess) return e;
+  if ((e = axis_map(&mo, g, AX, out, nslices, G)) != cudaSuccess) return e;
   LineArgs a{};
   const int rows = (int)(g.npad / g.M);
   if (AX == AX_ROW) {
     a.inner = (rows + 1) / 2;
     a.per_slice = a.inner;
   } else {
-    a.inner = g.M / 2;
+    a.inner = g.M / (2 * G);
     a.per_slice = a.inner * (g.dim == 3 ? g.n : 1);
   }
   a.rows = rows;
@@ -503,19 +528,53 @@ static cudaError_t launch_line(const Geom& g, const DstTables& t, const Poly& P,
   long grid = (long)sm_count() * per_sm;
   if (grid > a.nitems) grid = a.nitems;
   if (grid < 1) return cudaSuccess;
-  k<<<(unsigned)grid, D::T, D::SMEM, st>>>(mi, mo, a);
+  k<<<(unsigned)grid, D::THREADS, D::SMEM, st>>>(mi, mo, a);
   return cudaGetLastError();
+}
+
+// strided-axis variant (G column pairs per item, NBUF buffers); EXPD_COLV=<G><NBUF>
+// (e.g. 12, 22, 21, 41) overrides the default for tuning
+static int colv() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EXPD_COLV");
+    v = e ? atoi(e) : 0;
+  }
+  return v;
+}
+
+template <int M, int AX, bool NL>
+static cudaError_t launch_col(const Geom& g, const DstTables& t, const Poly& P, const double* in, double* out,
+                              long nslices, cudaStream_t st) {
+  if constexpr (M == 2048) {
+    // measured on c5 (profiles/r01): plain strided pass fastest with 2 column pairs per item
+    // (32-byte TMA rows), the fused [V, N, V] pass with 1 pair and 1 buffer (more CTAs / SM)
+    switch (colv()) {
+      case 11: return launch_line<M, AX, NL, 1, 1>(g, t, P, in, out, nslices, st);
+      case 12: return launch_line<M, AX, NL, 1, 2>(g, t, P, in, out, nslices, st);
+      case 21: return launch_line<M, AX, NL, 2, 1>(g, t, P, in, out, nslices, st);
+      case 22: return launch_line<M, AX, NL, 2, 2>(g, t, P, in, out, nslices, st);
+      case 41: return launch_line<M, AX, NL, 4, 1>(g, t, P, in, out, nslices, st);
+      default:
+        if constexpr (NL) return launch_line<M, AX, NL, 1, 1>(g, t, P, in, out, nslices, st);
+        else return launch_line<M, AX, NL, 2, 2>(g, t, P, in, out, nslices, st);
+    }
+  } else if constexpr (M == 4096) {
+    return launch_line<M, AX, NL, 1, 2>(g, t, P, in, out, nslices, st);
+  } else {
+    return launch_line<M, AX, NL, 2, 2>(g, t, P, in, out, nslices, st);
+  }
 }
 
 template <int M>
 static cudaError_t line_pass_m(const Geom& g, const DstTables& t, const Poly& P, int ax, bool nl, const double* in,
                                double* out, long nslices, cudaStream_t st) {
-  if (ax == AX_ROW) return launch_line<M, AX_ROW, false>(g, t, P, in, out, nslices, st);
+  if (ax == AX_ROW) return launch_line<M, AX_ROW, false, 1, 2>(g, t, P, in, out, nslices, st);
   if (ax == AX_COL_Y)
-    return nl ? launch_line<M, AX_COL_Y, true>(g, t, P, in, out, nslices, st)
-              : launch_line<M, AX_COL_Y, false>(g, t, P, in, out, nslices, st);
-  return nl ? launch_line<M, AX_COL_Z, true>(g, t, P, in, out, nslices, st)
-            : launch_line<M, AX_COL_Z, false>(g, t, P, in, out, nslices, st);
+    return nl ? launch_col<M, AX_COL_Y, true>(g, t, P, in, out, nslices, st)
+              : launch_col<M, AX_COL_Y, false>(g, t, P, in, out, nslices, st);
+  return nl ? launch_col<M, AX_COL_Z, true>(g, t, P, in, out, nslices, st)
+            : launch_col<M, AX_COL_Z, false>(g, t, P, in, out, nslices, st);
 }
 
 // One axis pass (ax: 0 = x rows, 1 = y, 2 = z) of nslices padded spectral slices; nl
