@@ -15,9 +15,9 @@ barrier + synchronize, max over ranks.  Inputs (8.6 GB per space-time array) exc
 --impl reference times the CPU oracle (oracle/, naive long-double sums) on host cores, on
 a bounded sample of the same workload.
 
-N > 1 (torchrun): this round's library has no multi-rank path yet; every
-rank solves its own independent c5 problem (weak scaling over independent problems, no
-collective on the data path).
+N > 1 (torchrun): one c5 problem distributed over the ranks (SURVEY §8e, strong scaling):
+mode slabs for the fused time-local kernel, time slabs for stage 3, two NCCL all-to-alls
+and one allreduce per sweep.
 """
 from __future__ import annotations
 
@@ -50,6 +50,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--dist1", action="store_true",
+                    help="N = 1: run the distributed schedule (1-rank NCCL communicator) instead")
     return ap.parse_args()
 
 
@@ -180,7 +182,7 @@ def run_reference(args):
     line = {
         "impl": "reference", "metric": "space-time DOF-iterations/s per Exp-ParaDiag sweep", "value": value,
         "unit": "DOF-iter/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * dt / max(args.steps, 1), "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": 1e3 * dt / max(args.steps, 1), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f80 (long double accumulation)", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.dim}D n={cfg.n} Nt={cfg.nt} ETD2 Picard sweep (BASELINE.json:11)"},
         "cpu_baseline": {"value": value, "unit": "DOF-iter/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
@@ -201,7 +203,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     import synth
-    from paper_2603_04350_b200 import Plan, Problem
+    from paper_2603_04350_b200 import Comm, Plan, Problem
     from paper_2603_04350_b200 import build as pbuild
 
     ws, rank, local = dist_env()
@@ -215,12 +217,12 @@ def run_ours(args):
         dist.barrier()
 
     cfg = synth.CONFIGS[args.config]
-    if ws > 1:  # independent problem per rank (weak scaling)
-        cfg = synth.Config(**{**cfg.__dict__, "seed": cfg.seed + 1000 * rank})
     prob = Problem.from_config(cfg)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
-    plan = Plan(prob, device=local, stream=stream)
+    comm = Comm(rank, ws, local) if (ws > 1 or args.dist1) else None
+    plan = Plan(prob, device=local, stream=stream, comm=comm)
+    lay = plan.layout
     u0 = torch.from_numpy(synth.initial_condition(cfg)).to(dev)
     plan.load_state(u0, None)
     plan.set_profiling(True)
@@ -257,13 +259,17 @@ def run_ours(args):
         dist.barrier()
         ms = float(t.item())
     ms_step = ms / args.steps
-    value = cfg.nst * args.steps * ws / (ms * 1e-3)
+    value = cfg.nst * args.steps / (ms * 1e-3)  # one problem over all ranks (strong scaling)
 
     pk = peaks()
     hbm_peak = pk["hbm_gbs"] if pk else 6650.0
     peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if pk else "fallback (B200_PROFILING.md)"
-    k1_bytes = (BYTES_PER_DOF["k1_nonlinear"] if nl else BYTES_PER_DOF["k1_linear"]) * cfg.nst
-    s3_bytes = BYTES_PER_DOF["stage3"] * cfg.N * (cfg.nt - 1) if nl else 0
+    # this rank's share: K1 on its mode slab (nt x mode_len padded entries, of which the
+    # n^dim real modes are counted), stage 3 on its time slab
+    share = lay["mode_len"] / lay["npad"]
+    k1_bytes = (BYTES_PER_DOF["k1_nonlinear"] if nl else BYTES_PER_DOF["k1_linear"]) * cfg.nst * share
+    s3_slices = (cfg.nt - 1) if ws == 1 else lay["nt_local"]
+    s3_bytes = BYTES_PER_DOF["stage3"] * cfg.N * s3_slices if nl else 0
     k1_ms = statistics.mean(ms_k1)
     s3_ms = statistics.mean(ms_nl) if nl else 0.0
     k1_gbs = k1_bytes / (k1_ms * 1e-3) / 1e9
@@ -287,9 +293,9 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         u0_h = torch.from_numpy(synth.initial_condition(cfg)).pin_memory()
-        U_h = torch.empty((cfg.nt,) + cfg.shape, dtype=torch.float64).pin_memory()
+        U_h = torch.empty((lay["nt_local"],) + cfg.shape, dtype=torch.float64).pin_memory()
         u0_d = torch.empty_like(u0_h, device=dev)
-        U_d = torch.empty((cfg.nt,) + cfg.shape, dtype=torch.float64, device=dev)
+        U_d = torch.empty((lay["nt_local"],) + cfg.shape, dtype=torch.float64, device=dev)
         plan.set_profiling(False)
         tot_ms, tot_sweeps = 0.0, 0
         for i in range(args.e2e_steps + 1):
@@ -306,8 +312,12 @@ def run_ours(args):
             if i > 0:  # first solve is warm-up
                 tot_ms += a0.elapsed_time(a1)
                 tot_sweeps += rep["sweeps"]
-        e2e = {"value": cfg.nst * tot_sweeps * ws / (tot_ms * 1e-3), "unit": "DOF-iter/s",
-               "h2d_bytes_per_step": u0_h.numel() * 8, "d2h_bytes_per_step": U_h.numel() * 8,
+        if ws > 1:
+            t = torch.tensor([tot_ms], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            tot_ms = float(t.item())
+        e2e = {"value": cfg.nst * tot_sweeps / (tot_ms * 1e-3), "unit": "DOF-iter/s",
+               "h2d_bytes_per_step": u0_h.numel() * 8 * ws, "d2h_bytes_per_step": cfg.nst * 8,
                "what": f"full fixed-point solve per step ({rep['sweeps']} sweeps, {rep['iterations']} iterations, "
                        f"rel residual {rep['rel_residual']:.2e}) incl. setup DSTs, final IDST and host copies"}
 
@@ -322,19 +332,23 @@ def run_ours(args):
     line = {
         "metric": "space-time DOF-iterations/s per Exp-ParaDiag sweep", "value": value, "unit": "DOF-iter/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "config": {"workload": f"{cfg.name}: {cfg.dim}D n={cfg.n} Nt={cfg.nt} "
                                f"{'ETD2' if cfg.scheme == 1 else 'exp. Euler'} "
                                f"{'Picard' if nl else 'fixed-point'} sweep (BASELINE.json:11)",
                    "n_st": cfg.nst, "alpha": cfg.alpha,
                    "l2": "inputs 8.6 GB per space-time array >> 126 MB L2 (no flush needed)",
-                   "parallelism": "single GPU" if ws == 1 else f"{ws} independent problems (weak scaling)"},
+                   "parallelism": "single GPU" if ws == 1 else
+                   f"{ws} GPUs: mode slabs (K1) / time slabs (stage 3), NCCL all-to-all + allreduce"},
         "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches, "clocks": ck,
         "residual_norm_last": float(np.sqrt(norms[-1])) if norms else None,
     }
     if rank == 0:
         print(json.dumps(line), flush=True)
+    plan.close()
+    if comm is not None:
+        comm.close()
     if ws > 1:
         dist.destroy_process_group()
     return 0

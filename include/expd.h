@@ -63,9 +63,22 @@ typedef struct {
 } expd_problem;
 
 typedef struct {
-  int rank, nranks;   /* this build: nranks == 1 (multi-GPU sharding: DESIGN.md)  */
-  void* nccl_comm;    /* ncclComm_t or NULL when nranks == 1                       */
+  int rank, nranks;   /* 1 <= nranks <= 64, nt % nranks == 0                  */
+  void* nccl_comm;    /* ncclComm_t (expd_nccl_comm_init) or NULL when nranks == 1; with
+                         nranks == 1 and a communicator the distributed schedule runs on one
+                         GPU (all-to-alls become local copies) -- used by the GPU tests     */
 } expd_dist;
+
+/* Partition of a space-time vector over the ranks:
+   time slab = slices [t0, t0 + nt_local) (physical API vectors U, R, S and stage 3);
+   mode slab = padded spectral entries [mode_off, mode_off + mode_len) of every slice
+   (the time-local fused kernel K1).  npad = entries of a padded spectral slice
+   (n^{dim-1} (n+1)). */
+typedef struct {
+  int rank, nranks;
+  long npad, mode_off, mode_len;
+  int t0, nt_local;
+} expd_layout;
 
 typedef struct expd_plan expd_plan;
 
@@ -122,6 +135,25 @@ expd_status expd_fixed_point_solve(expd_plan* plan, const double* u0, double* U,
    Blocking. */
 expd_status expd_gmres_solve(expd_plan* plan, const double* u0, double* U, double tol, int restart, int maxit,
                              expd_report* report);
+
+/* ---- multi-GPU ---------------------------------------------------------------------- */
+/* The rank's slabs; INVALID_ARG when nt % nranks != 0 or there are fewer x-lines than ranks.
+   Pure host computation (no device needed). */
+expd_status expd_layout_query(const expd_problem* prob, int rank, int nranks, expd_layout* out);
+/* The all-to-all schedule between the layouts, as the messages this rank posts, in order:
+   direction 0 = mode slab [nt][mode_len] -> time slab [nt_local][npad]; 1 = time slab ->
+   mode slab [nt + shift][mode_len] (global slice t lands in slice t + shift).  Each message
+   is 4 longs {peer, src_off, dst_off, count} (doubles; src_off of recvs and dst_off of
+   sends are 0).  Writes sends / recvs when cap >= the count; returns the number of messages
+   per list (sends and recvs have equal length), or -1 on invalid arguments.  Host only. */
+long expd_a2a_schedule(const expd_problem* prob, int rank, int nranks, int direction, int shift, long* sends,
+                       long* recvs, long cap);
+/* NCCL communicator for a plan (NCCL is loaded at run time: the process's libnccl.so.2).
+   Rank 0 creates the 128-byte id, the caller broadcasts it (e.g. torch.distributed), every
+   rank calls expd_nccl_comm_init (collective).  The caller owns the communicator. */
+expd_status expd_nccl_unique_id(unsigned char id[128]);
+expd_status expd_nccl_comm_init(const unsigned char id[128], int nranks, int rank, int device, void** comm);
+void expd_nccl_comm_destroy(void* comm);
 
 /* ---- lower-level entry points used by the solver loop and the benchmark -------------- */
 /* Spectral-state sweep, the hot path of one Exp-ParaDiag iteration on data already in

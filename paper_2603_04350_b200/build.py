@@ -33,6 +33,24 @@ NVCC_FLAGS = [
 ]
 
 
+def _nccl_include():
+    """nccl.h of the NCCL the process loads (torch's wheel), else the system one (types
+    only: libexpd.so loads libnccl.so.2 at run time)."""
+    try:
+        import nvidia.nccl  # noqa: F401
+
+        for base in nvidia.nccl.__path__:
+            inc = os.path.join(base, "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return ["-I", inc]
+    except Exception:
+        pass
+    return []
+
+
+NVCC_FLAGS += _nccl_include()
+
+
 def _sources():
     return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
 
@@ -77,7 +95,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
                 if verbose:
                     print("compiled", os.path.relpath(s, ROOT))
     if force or jobs or _stale(LIB, objs):
-        cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB, *objs, "-lcudart"]
+        cmd = [NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", LIB, *objs, "-lcudart", "-ldl"]
         subprocess.check_call(cmd)
     return LIB
 

@@ -1,0 +1,277 @@
+// dist.cu -- multi-GPU plumbing of the sweep:
+// the mode-slab / time-slab partition, the all-to-all message schedules between the two
+// layouts, and their execution with NCCL point-to-point calls (NCCL is loaded at run time,
+// so the single-GPU library has no NCCL dependency).
+//
+// Partition (P ranks, nt % P == 0):
+//   * time slab of rank r: slices [r nt/P, (r+1) nt/P) of a space-time vector, full
+//     spatial slices -- where the space-local stage 3 (N-hat = V N(V u-hat)) runs;
+//   * mode slab of rank r: a contiguous range [off_r, off_r + len_r) of the padded spectral
+//     entries of every slice (whole padded x-lines for dim >= 2, mode pairs for dim 1), all
+//     nt slices -- where the time-local K1 (residual, alpha-circulant preconditioner,
+//     update) runs.  In the DST basis every spatial mode is an independent length-nt
+//     problem ("naturally parallelizable"), so K1 needs no
+//     communication; norms and GMRES inner products are partial sums + one allreduce.
+// A schedule is plain data (a list of messages), so the same list is executed by NCCL
+// here and by torch.distributed (gloo) in the CPU tests (tests/test_dist_cpu.py).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "../../include/expd.h"
+#include "expd_internal.h"
+
+namespace expd {
+
+bool dist_layout(const Geom& g, int nt, int rank, int nranks, DistLayout* L) {
+  if (nranks < 1 || nranks > EXPD_MAX_RANKS || rank < 0 || rank >= nranks || nt % nranks != 0) return false;
+  L->rank = rank;
+  L->nranks = nranks;
+  L->nt = nt;
+  L->npad = g.npad;
+  L->unit = g.dim >= 2 ? g.M : 2;  // whole padded x-lines (dim >= 2) or mode pairs (dim 1)
+  const long units = g.npad / L->unit;
+  if (units < nranks) return false;
+  const long base = units / nranks, rem = units % nranks;
+  long off = 0;
+  for (int q = 0; q < nranks; ++q) {
+    const long u = base + (q < rem ? 1 : 0);
+    L->mode_off[q] = off * L->unit;
+    L->mode_len[q] = u * L->unit;
+    off += u;
+    L->t0[q] = q * (nt / nranks);
+    L->ntl[q] = nt / nranks;
+  }
+  return true;
+}
+
+// Messages of one all-to-all between the layouts, in the order both sides post them.
+//   MODE_TO_TIME: src = mode slab [nt][len_r], dst = time slab [ntl_r][npad];
+//   TIME_TO_MODE: src = time slab [ntl_r][npad], dst = mode slab [nt + shift][len_r],
+//                 global slice t lands in dst slice t + shift.
+// Self messages (peer == rank) are local copies.
+void a2a_schedule(const DistLayout& L, int dir, int shift, std::vector<A2AMsg>& sends, std::vector<A2AMsg>& recvs) {
+  sends.clear();
+  recvs.clear();
+  const int r = L.rank, P = L.nranks;
+  for (int q = 0; q < P; ++q) {
+    if (dir == A2A_MODE_TO_TIME) {
+      for (int i = 0; i < L.ntl[q]; ++i) {  // r -> q: the slices of q's time slab
+        const long t = L.t0[q] + i;
+        sends.push_back({q, t * L.mode_len[r], 0, L.mode_len[r]});
+      }
+      for (int i = 0; i < L.ntl[r]; ++i) {  // q -> r: q's modes of r's slices
+        recvs.push_back({q, 0, (long)i * L.npad + L.mode_off[q], L.mode_len[q]});
+      }
+    } else {
+      for (int i = 0; i < L.ntl[r]; ++i) {  // r -> q: q's modes of r's slices
+        sends.push_back({q, (long)i * L.npad + L.mode_off[q], 0, L.mode_len[q]});
+      }
+      for (int i = 0; i < L.ntl[q]; ++i) {  // q -> r: r's modes of q's slices
+        const long t = L.t0[q] + i;
+        recvs.push_back({q, 0, (t + shift) * L.mode_len[r], L.mode_len[r]});
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// NCCL, loaded at run time
+// ---------------------------------------------------------------------------------------
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*);
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int);
+  ncclResult_t (*CommDestroy)(ncclComm_t);
+  ncclResult_t (*GroupStart)();
+  ncclResult_t (*GroupEnd)();
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t);
+  ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t, cudaStream_t);
+  const char* (*GetErrorString)(ncclResult_t);
+  bool ok;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api{};
+  static std::once_flag once;
+  std::call_once(once, [] {
+    // prefer the NCCL the process already loaded (torch's), else the default search
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return;
+    bool ok = true;
+    auto sym = [&](const char* n) {
+      void* p = dlsym(h, n);
+      if (!p) ok = false;
+      return p;
+    };
+    api.GetUniqueId = (decltype(api.GetUniqueId))sym("ncclGetUniqueId");
+    api.CommInitRank = (decltype(api.CommInitRank))sym("ncclCommInitRank");
+    api.CommDestroy = (decltype(api.CommDestroy))sym("ncclCommDestroy");
+    api.GroupStart = (decltype(api.GroupStart))sym("ncclGroupStart");
+    api.GroupEnd = (decltype(api.GroupEnd))sym("ncclGroupEnd");
+    api.Send = (decltype(api.Send))sym("ncclSend");
+    api.Recv = (decltype(api.Recv))sym("ncclRecv");
+    api.AllReduce = (decltype(api.AllReduce))sym("ncclAllReduce");
+    api.GetErrorString = (decltype(api.GetErrorString))sym("ncclGetErrorString");
+    api.ok = ok;
+  });
+  return api;
+}
+
+static std::string nccl_err(ncclResult_t r) {
+  NcclApi& a = nccl();
+  return a.ok ? std::string(a.GetErrorString(r)) : std::string("NCCL not loaded");
+}
+
+// Execute one schedule: NCCL send / recv for peers, cudaMemcpy2DAsync for the self part.
+int a2a_execute(void* comm, const DistLayout& L, const std::vector<A2AMsg>& sends, const std::vector<A2AMsg>& recvs,
+                const double* src, double* dst, cudaStream_t st, std::string& err) {
+  NcclApi& a = nccl();
+  // self part: pair the k-th self send with the k-th self recv
+  std::vector<const A2AMsg*> ss, rr;
+  for (const auto& m : sends)
+    if (m.peer == L.rank) ss.push_back(&m);
+  for (const auto& m : recvs)
+    if (m.peer == L.rank) rr.push_back(&m);
+  if (ss.size() != rr.size()) {
+    err = "a2a: self schedule mismatch";
+    return EXPD_ERR_INVALID_ARG;
+  }
+  for (size_t k = 0; k < ss.size(); ++k) {
+    cudaError_t e = cudaMemcpyAsync(dst + rr[k]->dst_off, src + ss[k]->src_off, sizeof(double) * ss[k]->count,
+                                    cudaMemcpyDeviceToDevice, st);
+    if (e != cudaSuccess) {
+      err = std::string("a2a self copy: ") + cudaGetErrorString(e);
+      return EXPD_ERR_CUDA;
+    }
+  }
+  if (L.nranks == 1) return EXPD_OK;
+  if (!a.ok || !comm) {
+    err = "a2a: NCCL unavailable";
+    return EXPD_ERR_NCCL;
+  }
+  ncclComm_t c = (ncclComm_t)comm;
+  ncclResult_t r = a.GroupStart();
+  for (const auto& m : sends)
+    if (r == ncclSuccess && m.peer != L.rank) r = a.Send(src + m.src_off, (size_t)m.count, ncclFloat64, m.peer, c, st);
+  for (const auto& m : recvs)
+    if (r == ncclSuccess && m.peer != L.rank) r = a.Recv(dst + m.dst_off, (size_t)m.count, ncclFloat64, m.peer, c, st);
+  ncclResult_t r2 = a.GroupEnd();
+  if (r != ncclSuccess || r2 != ncclSuccess) {
+    err = "a2a: " + nccl_err(r != ncclSuccess ? r : r2);
+    return EXPD_ERR_NCCL;
+  }
+  return EXPD_OK;
+}
+
+int allreduce_sum(void* comm, int nranks, double* buf, long count, cudaStream_t st, std::string& err) {
+  if (nranks == 1 && !comm) return EXPD_OK;
+  NcclApi& a = nccl();
+  if (!a.ok || !comm) {
+    err = "allreduce: NCCL unavailable";
+    return EXPD_ERR_NCCL;
+  }
+  ncclResult_t r = a.AllReduce(buf, buf, (size_t)count, ncclFloat64, ncclSum, (ncclComm_t)comm, st);
+  if (r != ncclSuccess) {
+    err = "allreduce: " + nccl_err(r);
+    return EXPD_ERR_NCCL;
+  }
+  return EXPD_OK;
+}
+
+}  // namespace expd
+
+using namespace expd;
+
+// ---------------------------------------------------------------------------------------
+// C-ABI (include/expd.h "Multi-GPU")
+// ---------------------------------------------------------------------------------------
+static bool geom_of(const expd_problem* p, Geom* g) {
+  if (!p || p->dim < 1 || p->dim > 3 || p->n < 3) return false;
+  g->dim = p->dim;
+  g->n = p->n;
+  g->M = p->n + 1;
+  long N = 1, npad = p->n + 1;
+  for (int i = 0; i < p->dim; ++i) N *= p->n;
+  for (int i = 1; i < p->dim; ++i) npad *= p->n;
+  g->N = N;
+  g->npad = npad;
+  return true;
+}
+
+extern "C" expd_status expd_layout_query(const expd_problem* prob, int rank, int nranks, expd_layout* out) {
+  Geom g{};
+  if (!out || !geom_of(prob, &g)) return EXPD_ERR_INVALID_ARG;
+  DistLayout L{};
+  if (!dist_layout(g, prob->nt, rank, nranks, &L)) return EXPD_ERR_INVALID_ARG;
+  out->rank = rank;
+  out->nranks = nranks;
+  out->npad = L.npad;
+  out->mode_off = L.mode_off[rank];
+  out->mode_len = L.mode_len[rank];
+  out->t0 = L.t0[rank];
+  out->nt_local = L.ntl[rank];
+  return EXPD_OK;
+}
+
+extern "C" long expd_a2a_schedule(const expd_problem* prob, int rank, int nranks, int direction, int shift,
+                                  long* sends, long* recvs, long cap) {
+  Geom g{};
+  if (!geom_of(prob, &g)) return -1;
+  DistLayout L{};
+  if (!dist_layout(g, prob->nt, rank, nranks, &L)) return -1;
+  if (direction != A2A_MODE_TO_TIME && direction != A2A_TIME_TO_MODE) return -1;
+  std::vector<A2AMsg> s, r;
+  a2a_schedule(L, direction, shift, s, r);
+  const long n = (long)s.size();
+  if ((long)r.size() != n) return -1;
+  if (sends && recvs && cap >= n) {
+    for (long i = 0; i < n; ++i) {
+      sends[4 * i + 0] = s[i].peer;
+      sends[4 * i + 1] = s[i].src_off;
+      sends[4 * i + 2] = s[i].dst_off;
+      sends[4 * i + 3] = s[i].count;
+      recvs[4 * i + 0] = r[i].peer;
+      recvs[4 * i + 1] = r[i].src_off;
+      recvs[4 * i + 2] = r[i].dst_off;
+      recvs[4 * i + 3] = r[i].count;
+    }
+  }
+  return n;
+}
+
+extern "C" expd_status expd_nccl_unique_id(unsigned char id[128]) {
+  NcclApi& a = nccl();
+  if (!id) return EXPD_ERR_INVALID_ARG;
+  if (!a.ok) return EXPD_ERR_NCCL;
+  ncclUniqueId u;
+  if (a.GetUniqueId(&u) != ncclSuccess) return EXPD_ERR_NCCL;
+  static_assert(sizeof(u.internal) == 128, "ncclUniqueId size");
+  memcpy(id, u.internal, 128);
+  return EXPD_OK;
+}
+
+extern "C" expd_status expd_nccl_comm_init(const unsigned char id[128], int nranks, int rank, int device,
+                                           void** comm) {
+  NcclApi& a = nccl();
+  if (!id || !comm || nranks < 1 || rank < 0 || rank >= nranks) return EXPD_ERR_INVALID_ARG;
+  if (!a.ok) return EXPD_ERR_NCCL;
+  if (cudaSetDevice(device) != cudaSuccess) return EXPD_ERR_CUDA;
+  ncclUniqueId u;
+  memcpy(u.internal, id, 128);
+  ncclComm_t c = nullptr;
+  if (a.CommInitRank(&c, nranks, u, rank) != ncclSuccess) return EXPD_ERR_NCCL;
+  *comm = (void*)c;
+  return EXPD_OK;
+}
+
+extern "C" void expd_nccl_comm_destroy(void* comm) {
+  NcclApi& a = nccl();
+  if (comm && a.ok) a.CommDestroy((ncclComm_t)comm);
+}

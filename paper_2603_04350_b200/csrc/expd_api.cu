@@ -20,7 +20,7 @@ using namespace expd;
 
 struct expd_plan {
   expd_problem prob{};
-  expd_dist dist{};
+  expd_dist dinfo{};
   int device = 0;
   cudaStream_t stream = nullptr;
   Geom g{};
@@ -38,6 +38,13 @@ struct expd_plan {
   // workspace (caller-owned)
   char* ws = nullptr;
   size_t ws_bytes = 0;
+  // distribution: dist = the mode-slab / time-slab schedule with all-to-alls
+  bool dist = false;
+  DistLayout L{};
+  long mlen = 0, moff = 0;  // this rank's mode slab (= the whole slice when !dist)
+  int ntl = 0, t0 = 0;      // this rank's time slab (= all slices when !dist)
+  std::vector<A2AMsg> m2t_s, m2t_r, t2m_s, t2m_r, t2m1_s, t2m1_r;  // all-to-all schedules
+  double *UT = nullptr, *NT = nullptr;  // time-slab spectral staging [ntl][npad] (dist only)
   double *Uh = nullptr, *Nh = nullptr, *T1 = nullptr, *u0h = nullptr, *E = nullptr, *C1 = nullptr, *C2 = nullptr;
   double *scratch = nullptr, *partial = nullptr, *dscal = nullptr;
   double* krylov = nullptr;
@@ -129,8 +136,9 @@ extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dis
     return EXPD_ERR_INVALID_ARG;
   if (P.nt > 256) return EXPD_ERR_UNSUPPORTED;
   int nranks = dist ? dist->nranks : 1;
-  if (nranks < 1 || (dist && (dist->rank < 0 || dist->rank >= nranks))) return EXPD_ERR_INVALID_ARG;
-  if (nranks != 1) return EXPD_ERR_UNSUPPORTED;
+  if (nranks < 1 || nranks > EXPD_MAX_RANKS || (dist && (dist->rank < 0 || dist->rank >= nranks)))
+    return EXPD_ERR_INVALID_ARG;
+  if (nranks > 1 && (!dist->nccl_comm || P.nt % nranks != 0)) return EXPD_ERR_INVALID_ARG;
   // breakdown guard: min_{k,J} |1 - lambda_k E_J| >= 1 - alpha^{1/nt} max_J E_J (R10)
   {
     long double h = 1.0L / (long double)(P.n + 1);
@@ -142,8 +150,8 @@ extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dis
   }
   expd_plan* p = new expd_plan();
   p->prob = P;
-  if (dist) p->dist = *dist;
-  else p->dist.nranks = 1;
+  if (dist) p->dinfo = *dist;
+  else p->dinfo.nranks = 1;
   p->device = device;
   p->stream = (cudaStream_t)cuda_stream;
   p->g.dim = P.dim;
@@ -165,7 +173,21 @@ extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dis
     expd_plan_destroy(p);
     return st;
   }
-  p->time_grid = time_fused_grid(P.nt, npad / 2, p->sms);
+  p->dist = nranks > 1 || (dist && dist->nccl_comm);
+  if (!dist_layout(p->g, P.nt, p->dist ? dist->rank : 0, p->dist ? nranks : 1, &p->L)) {
+    expd_plan_destroy(p);
+    return EXPD_ERR_INVALID_ARG;
+  }
+  p->mlen = p->L.mode_len[p->L.rank];
+  p->moff = p->L.mode_off[p->L.rank];
+  p->ntl = p->L.ntl[p->L.rank];
+  p->t0 = p->L.t0[p->L.rank];
+  if (p->dist) {
+    a2a_schedule(p->L, A2A_MODE_TO_TIME, 0, p->m2t_s, p->m2t_r);
+    a2a_schedule(p->L, A2A_TIME_TO_MODE, 0, p->t2m_s, p->t2m_r);
+    a2a_schedule(p->L, A2A_TIME_TO_MODE, 1, p->t2m1_s, p->t2m1_r);
+  }
+  p->time_grid = time_fused_grid(P.nt, p->mlen / 2, p->sms);
   p->vgrid = vec_grid(p->sms);
   *out = p;
   return EXPD_OK;
@@ -173,17 +195,23 @@ extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dis
 
 // workspace layout (every block 256-byte aligned)
 struct Layout {
-  size_t Uh, Nh, T1, u0h, E, C1, C2, scratch, partial, dscal, krylov, total, vec;
+  size_t Uh, Nh, T1, UT, NT, u0h, E, C1, C2, scratch, partial, dscal, krylov, total, vec;
 };
 static Layout layout(const expd_plan* p, int kv) {
   Layout L{};
-  const size_t vec = align_up(sizeof(double) * (size_t)p->prob.nt * (size_t)p->g.npad);
+  // space-time vectors in the mode slab: [nt][mlen]; N-hat gets one extra slice when
+  // distributed (stage 3 of the last time slab lands there, unused)
+  const size_t vec = align_up(sizeof(double) * (size_t)p->prob.nt * (size_t)p->mlen);
+  const size_t nhv = align_up(sizeof(double) * (size_t)(p->prob.nt + (p->dist ? 1 : 0)) * (size_t)p->mlen);
+  const size_t tsl = p->dist ? align_up(sizeof(double) * (size_t)p->ntl * (size_t)p->g.npad) : 0;
   const size_t sl = align_up(sizeof(double) * (size_t)p->g.npad);
   size_t off = 0;
   L.vec = vec;
   L.Uh = off; off += vec;
-  L.Nh = off; off += (p->nl ? vec : 0);
+  L.Nh = off; off += (p->nl ? nhv : 0);
   L.T1 = off; off += vec;
+  L.UT = off; off += tsl;
+  L.NT = off; off += (p->nl ? tsl : 0);
   L.u0h = off; off += sl;
   L.E = off; off += sl;
   L.C1 = off; off += sl;
@@ -216,6 +244,8 @@ extern "C" expd_status expd_plan_set_workspace(expd_plan* p, void* d_ptr, size_t
   p->Uh = at(L.Uh);
   p->Nh = p->nl ? at(L.Nh) : nullptr;
   p->T1 = at(L.T1);
+  p->UT = p->dist ? at(L.UT) : nullptr;
+  p->NT = (p->dist && p->nl) ? at(L.NT) : nullptr;
   p->u0h = at(L.u0h);
   p->E = at(L.E);
   p->C1 = at(L.C1);
@@ -263,15 +293,15 @@ static DstTables dst_tables(const expd_plan* p) { return DstTables{p->d_twM, p->
 static TimeArgs time_args(const expd_plan* p, const double* X, double* Y, bool with_partial) {
   TimeArgs a{};
   a.nt = p->prob.nt;
-  a.npad = p->g.npad;
-  a.npairs = p->g.npad / 2;
+  a.npad = p->mlen;  // mode slab: slice stride and mode count (= npad on one GPU)
+  a.npairs = p->mlen / 2;
   a.X = X;
   a.Y = Y;
-  a.u0h = p->u0h;
+  a.u0h = p->u0h + p->moff;
   a.Nh = p->Nh;
-  a.E = p->E;
-  a.C1 = p->C1;
-  a.C2 = p->C2;
+  a.E = p->E + p->moff;
+  a.C1 = p->C1 + p->moff;
+  a.C2 = p->C2 + p->moff;
   a.g = p->d_g;
   a.ginv = p->d_ginv;
   a.tw = p->d_twt;
@@ -289,11 +319,53 @@ static expd_status ready(expd_plan* p) {
 }
 
 // spectral u0 and (nonlinear) N-hat_0 = V N(u_0)
+// ---- distribution helpers (no-ops / local copies on one GPU) ---------------------------
+enum { A2A_M2T = 0, A2A_T2M = 1, A2A_T2M_SHIFT = 2 };
+static expd_status a2a(expd_plan* p, int which, const double* src, double* dst) {
+  const std::vector<A2AMsg>* s = &p->m2t_s;
+  const std::vector<A2AMsg>* r = &p->m2t_r;
+  if (which == A2A_T2M) { s = &p->t2m_s; r = &p->t2m_r; }
+  if (which == A2A_T2M_SHIFT) { s = &p->t2m1_s; r = &p->t2m1_r; }
+  int st = a2a_execute(p->dinfo.nccl_comm, p->L, *s, *r, src, dst, p->stream, p->err);
+  return (expd_status)st;
+}
+static expd_status allreduce(expd_plan* p, double* buf, long count) {
+  if (!p->dist) return EXPD_OK;
+  return (expd_status)allreduce_sum(p->dinfo.nccl_comm, p->L.nranks, buf, count, p->stream, p->err);
+}
+
+// spectral u0 (full slice, every rank) and (nonlinear) N-hat_0 = V N(u_0) (this rank's
+// mode slab of it in Nh slice 0)
 static expd_status load_u0(expd_plan* p, const double* u0) {
   CUDA_TRY(p, dst_slices(p->g, dst_tables(p), u0, false, p->u0h, true, 1, p->scratch, p->stream));
-  if (p->nl)
-    CUDA_TRY(p, nonlin_phys_slices(p->g, dst_tables(p), u0, p->Nh, 1, p->prob.npoly, p->prob.q, p->scratch,
+  if (p->nl) {
+    double* full = p->dist ? p->UT : p->Nh;
+    CUDA_TRY(p, nonlin_phys_slices(p->g, dst_tables(p), u0, full, 1, p->prob.npoly, p->prob.q, p->scratch,
                                    p->stream));
+    if (p->dist)
+      CUDA_TRY(p, cudaMemcpyAsync(p->Nh, p->UT + p->moff, sizeof(double) * p->mlen, cudaMemcpyDeviceToDevice,
+                                  p->stream));
+  }
+  return EXPD_OK;
+}
+
+// physical time-slab slices (the API layout) <-> the spectral mode slab
+static expd_status phys_to_mode(expd_plan* p, const double* U, double* mode) {
+  if (!p->dist) {
+    CUDA_TRY(p, dst_slices(p->g, dst_tables(p), U, false, mode, true, p->prob.nt, p->scratch, p->stream));
+    return EXPD_OK;
+  }
+  CUDA_TRY(p, dst_slices(p->g, dst_tables(p), U, false, p->UT, true, p->ntl, p->scratch, p->stream));
+  return a2a(p, A2A_T2M, p->UT, mode);
+}
+static expd_status mode_to_phys(expd_plan* p, const double* mode, double* U) {
+  if (!p->dist) {
+    CUDA_TRY(p, dst_slices(p->g, dst_tables(p), mode, true, U, false, p->prob.nt, p->scratch, p->stream));
+    return EXPD_OK;
+  }
+  expd_status s = a2a(p, A2A_M2T, mode, p->UT);
+  if (s) return s;
+  CUDA_TRY(p, dst_slices(p->g, dst_tables(p), p->UT, true, U, false, p->ntl, p->scratch, p->stream));
   return EXPD_OK;
 }
 
@@ -320,7 +392,29 @@ static cudaError_t enqueue_sweep(expd_plan* p, cudaStream_t st) {
   return reduce_partials(p->partial, p->time_grid, p->dscal, st);
 }
 
+// The distributed sweep: all-to-all U-hat (mode -> time slab), stage 3 on the
+// local time slices, all-to-all N-hat back (time slab -> mode slab, shifted one slice:
+// N-hat_m = V N(u_m) sits in slice m while U-hat slice t holds u_{t+1}), K1 on the mode
+// slab, allreduce of ||r||^2.
+static expd_status sweep_dist(expd_plan* p) {
+  expd_status s;
+  CUDA_TRY(p, record(p, 0, p->stream));
+  if (p->nl) {
+    if ((s = a2a(p, A2A_M2T, p->Uh, p->UT))) return s;
+    CUDA_TRY(p, nonlin_slices(p->g, dst_tables(p), p->UT, p->NT, p->ntl, p->prob.npoly, p->prob.q, p->scratch,
+                              p->stream));
+    if ((s = a2a(p, A2A_T2M_SHIFT, p->NT, p->Nh))) return s;
+  }
+  CUDA_TRY(p, record(p, 1, p->stream));
+  TimeArgs a = time_args(p, p->Uh, p->Uh, true);
+  CUDA_TRY(p, launch_time_fused(a, RM_RESID, OUT_UPDATE, p->nl, p->time_grid, p->stream));
+  CUDA_TRY(p, record(p, 2, p->stream));
+  CUDA_TRY(p, reduce_partials(p->partial, p->time_grid, p->dscal, p->stream));
+  return allreduce(p, p->dscal, 1);
+}
+
 static expd_status sweep(expd_plan* p, bool use_graph) {
+  if (p->dist) return sweep_dist(p);
   if (!use_graph || !p->eager_done) {
     p->eager_done = true;
     CUDA_TRY(p, enqueue_sweep(p, p->stream));
@@ -367,14 +461,20 @@ extern "C" expd_status expd_residual(expd_plan* p, const double* u0, const doubl
   const long nt = p->prob.nt;
   s = load_u0(p, u0);
   if (s) return s;
-  CUDA_TRY(p, dst_slices(p->g, dst_tables(p), U, false, p->Uh, true, nt, p->scratch, p->stream));
-  if (p->nl && nt > 1)  // N-hat_m = V N(u_m), m = 1..nt-1, straight from the physical slices
+  if ((s = phys_to_mode(p, U, p->Uh))) return s;
+  if (p->nl && !p->dist && nt > 1)  // N-hat_m = V N(u_m), m = 1..nt-1, from the physical slices
     CUDA_TRY(p, nonlin_phys_slices(p->g, dst_tables(p), U, p->Nh + p->g.npad, nt - 1, p->prob.npoly, p->prob.q,
                                    p->scratch, p->stream));
+  if (p->nl && p->dist) {  // local physical slices -> N-hat time slab -> mode slab (shifted)
+    CUDA_TRY(p, nonlin_phys_slices(p->g, dst_tables(p), U, p->NT, p->ntl, p->prob.npoly, p->prob.q, p->scratch,
+                                   p->stream));
+    if ((s = a2a(p, A2A_T2M_SHIFT, p->NT, p->Nh))) return s;
+  }
   TimeArgs a = time_args(p, p->Uh, p->T1, true);
   CUDA_TRY(p, launch_resid_only(a, p->nl, p->time_grid, p->stream));
   CUDA_TRY(p, reduce_partials(p->partial, p->time_grid, p->dscal, p->stream));
-  CUDA_TRY(p, dst_slices(p->g, dst_tables(p), p->T1, true, R, false, nt, p->scratch, p->stream));
+  if ((s = allreduce(p, p->dscal, 1))) return s;
+  if ((s = mode_to_phys(p, p->T1, R))) return s;
   if (rnorm2_host) return read_scalars(p, 1, rnorm2_host);
   return EXPD_OK;
 }
@@ -383,12 +483,10 @@ extern "C" expd_status expd_precond_apply(expd_plan* p, const double* R, double*
   expd_status s = ready(p);
   if (s) return s;
   if (!R || !S) return fail(p, EXPD_ERR_INVALID_ARG, "expd_precond_apply: bad pointers");
-  const long nt = p->prob.nt;
-  CUDA_TRY(p, dst_slices(p->g, dst_tables(p), R, false, p->T1, true, nt, p->scratch, p->stream));
+  if ((s = phys_to_mode(p, R, p->T1))) return s;
   TimeArgs a = time_args(p, p->T1, p->T1, false);
   CUDA_TRY(p, launch_time_fused(a, RM_INPUT, OUT_S, 0, p->time_grid, p->stream));
-  CUDA_TRY(p, dst_slices(p->g, dst_tables(p), p->T1, true, S, false, nt, p->scratch, p->stream));
-  return EXPD_OK;
+  return mode_to_phys(p, p->T1, S);
 }
 
 extern "C" expd_status expd_load_state(expd_plan* p, const double* u0, const double* U) {
@@ -397,8 +495,8 @@ extern "C" expd_status expd_load_state(expd_plan* p, const double* u0, const dou
   if (!u0) return fail(p, EXPD_ERR_INVALID_ARG, "expd_load_state: u0 is null");
   s = load_u0(p, u0);
   if (s) return s;
-  if (U) CUDA_TRY(p, dst_slices(p->g, dst_tables(p), U, false, p->Uh, true, p->prob.nt, p->scratch, p->stream));
-  else CUDA_TRY(p, cudaMemsetAsync(p->Uh, 0, sizeof(double) * p->prob.nt * p->g.npad, p->stream));
+  if (U) return phys_to_mode(p, U, p->Uh);
+  CUDA_TRY(p, cudaMemsetAsync(p->Uh, 0, sizeof(double) * p->prob.nt * p->mlen, p->stream));
   return EXPD_OK;
 }
 
@@ -419,20 +517,21 @@ extern "C" expd_status expd_store_state(expd_plan* p, double* U) {
   expd_status s = ready(p);
   if (s) return s;
   if (!U) return EXPD_ERR_INVALID_ARG;
-  CUDA_TRY(p, dst_slices(p->g, dst_tables(p), p->Uh, true, U, false, p->prob.nt, p->scratch, p->stream));
-  return EXPD_OK;
+  return mode_to_phys(p, p->Uh, U);
 }
 
 extern "C" expd_status expd_dst(expd_plan* p, const double* in, double* out, long nslices) {
   expd_status s = ready(p);
   if (s) return s;
   if (!in || !out || nslices < 0) return fail(p, EXPD_ERR_INVALID_ARG, "expd_dst: bad args");
-  const long chunk = p->prob.nt;  // T1 holds nt spectral slices
+  // spectral temporary: T1 (nt padded slices) on one GPU, the time-slab staging otherwise
+  const long chunk = p->dist ? p->ntl : p->prob.nt;
+  double* tmp = p->dist ? p->UT : p->T1;
   for (long s0 = 0; s0 < nslices; s0 += chunk) {
     long ns = nslices - s0 < chunk ? nslices - s0 : chunk;
-    CUDA_TRY(p, dst_slices(p->g, dst_tables(p), in + s0 * p->g.N, false, p->T1, true, ns, p->scratch, p->stream));
+    CUDA_TRY(p, dst_slices(p->g, dst_tables(p), in + s0 * p->g.N, false, tmp, true, ns, p->scratch, p->stream));
     // drop the pad column: spectral rows of n+1 doubles -> rows of n doubles
-    CUDA_TRY(p, cudaMemcpy2DAsync(out + s0 * p->g.N, sizeof(double) * p->g.n, p->T1, sizeof(double) * p->g.M,
+    CUDA_TRY(p, cudaMemcpy2DAsync(out + s0 * p->g.N, sizeof(double) * p->g.n, tmp, sizeof(double) * p->g.M,
                                   sizeof(double) * p->g.n, (size_t)ns * (p->g.N / p->g.n),
                                   cudaMemcpyDeviceToDevice, p->stream));
   }
@@ -443,11 +542,13 @@ extern "C" expd_status expd_nonlin_hat(expd_plan* p, const double* uhat, double*
   expd_status s = ready(p);
   if (s) return s;
   if (!uhat || !nhat || nslices < 0) return fail(p, EXPD_ERR_INVALID_ARG, "expd_nonlin_hat: bad args");
-  const long chunk = p->prob.nt / 2;  // T1 holds nt padded slices: input half, output half
+  // T1 (nt padded slices: input half, output half) on one GPU; UT / NT when distributed
+  const long chunk = p->dist ? p->ntl : p->prob.nt / 2;
   const size_t row = sizeof(double) * p->g.n, prow = sizeof(double) * p->g.M;
   const size_t rows = (size_t)(p->g.N / p->g.n);
-  double* tin = p->T1;
-  double* tout = p->T1 + chunk * p->g.npad;
+  if (p->dist && !p->nl) return fail(p, EXPD_ERR_UNSUPPORTED, "expd_nonlin_hat: linear distributed plan");
+  double* tin = p->dist ? p->UT : p->T1;
+  double* tout = p->dist ? p->NT : p->T1 + chunk * p->g.npad;
   for (long s0 = 0; s0 < nslices; s0 += chunk) {
     const long ns = nslices - s0 < chunk ? nslices - s0 : chunk;
     CUDA_TRY(p, cudaMemsetAsync(tin, 0, sizeof(double) * ns * p->g.npad, p->stream));
@@ -488,6 +589,7 @@ extern "C" expd_status expd_debug_kernel_ms(expd_plan* p, int which, long nslice
   expd_status s = ready(p);
   if (s) return s;
   if (!ms || reps < 1 || nslices < 1 || nslices > p->prob.nt) return fail(p, EXPD_ERR_INVALID_ARG, "debug: bad args");
+  if (p->dist) return fail(p, EXPD_ERR_UNSUPPORTED, "debug timing: single-GPU plans only");
   float m = 0.f;
   if (which >= 4 && (which > 6 || !line_supported(p->g) || p->g.dim < 2))
     return fail(p, EXPD_ERR_UNSUPPORTED, "debug: no line kernel for this geometry");
@@ -585,7 +687,7 @@ extern "C" expd_status expd_gmres_solve(expd_plan* p, const double* u0, double* 
   if (p->nl) return fail(p, EXPD_ERR_UNSUPPORTED, "GMRES is for linear problems (npoly == 0)");
   if (p->krylov_cap < 1) return fail(p, EXPD_ERR_OOM, "workspace holds no Krylov vectors");
   const int m = restart < p->krylov_cap ? restart : p->krylov_cap;
-  const long len = (long)p->prob.nt * p->g.npad;
+  const long len = (long)p->prob.nt * p->mlen;  // this rank's mode slab of a space-time vector
   const size_t vstride = align_up(sizeof(double) * (size_t)len) / sizeof(double);
   auto Vk = [&](int i) { return p->krylov + (size_t)i * vstride; };
   s = expd_load_state(p, u0, U);
@@ -604,6 +706,7 @@ extern "C" expd_status expd_gmres_solve(expd_plan* p, const double* u0, double* 
     CUDA_TRY(p, launch_time_fused(a, RM_RESID, OUT_S, 0, p->time_grid, p->stream));
     const double* t1c = p->T1;
     CUDA_TRY(p, multi_dot(&t1c, 1, p->T1, len, p->partial, p->vgrid, p->dscal, p->stream));
+    if ((s = allreduce(p, p->dscal, 1))) return s;
     double b2;
     s = read_scalars(p, 1, &b2);
     if (s) return s;
@@ -622,11 +725,15 @@ extern "C" expd_status expd_gmres_solve(expd_plan* p, const double* u0, double* 
       TimeArgs q = time_args(p, Vk(j), p->T1, false);
       CUDA_TRY(p, launch_time_fused(q, RM_QOP, OUT_S, 0, p->time_grid, p->stream));  // w = P Q v_j
       // CGS2: h = V^T w ; w -= V h ; h2 = V^T w ; w -= V h2 ; ||w||^2
+      // (distributed: every partial inner product is completed by an allreduce before use)
       CUDA_TRY(p, multi_dot(Vp.data(), j + 1, p->T1, len, p->partial, p->vgrid, dcoef, p->stream));
+      if ((s = allreduce(p, dcoef, j + 1))) return s;
       CUDA_TRY(p, multi_axpy_dot(Vp.data(), j + 1, dcoef, p->T1, len, p->partial, p->vgrid, dcoef + 40, 1,
                                  p->stream));
+      if ((s = allreduce(p, dcoef + 40, j + 1))) return s;
       CUDA_TRY(p, multi_axpy_dot(Vp.data(), j + 1, dcoef + 40, p->T1, len, p->partial, p->vgrid, dcoef + 80, 2,
                                  p->stream));
+      if ((s = allreduce(p, dcoef + 80, 1))) return s;
       CUDA_TRY(p, cudaMemcpyAsync(p->h_pin, dcoef, sizeof(double) * 81, cudaMemcpyDeviceToHost, p->stream));
       CUDA_TRY(p, cudaStreamSynchronize(p->stream));
       for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = p->h_pin[i] + p->h_pin[40 + i];

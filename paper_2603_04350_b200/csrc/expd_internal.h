@@ -4,6 +4,8 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <string>
+#include <vector>
 
 namespace expd {
 
@@ -109,5 +111,27 @@ cudaError_t scale_copy(const double* x, double s, double* y, long len, cudaStrea
 cudaError_t lincomb_add(const double* const* V, int nv, const double* coef_dev, double* x, long len,
                         cudaStream_t st);
 int vec_grid(int sms);
+
+// ---- multi-GPU (dist.cu) ----------------------------------------------------------------
+constexpr int EXPD_MAX_RANKS = 64;
+struct DistLayout {
+  int rank, nranks, nt;
+  long npad;                       // entries per full padded spectral slice
+  long unit;                       // partition unit of the mode slabs
+  long mode_off[EXPD_MAX_RANKS];   // mode slab of rank q: entries [off, off + len) of every slice
+  long mode_len[EXPD_MAX_RANKS];
+  int t0[EXPD_MAX_RANKS];          // time slab of rank q: slices [t0, t0 + ntl)
+  int ntl[EXPD_MAX_RANKS];
+};
+struct A2AMsg {
+  int peer;
+  long src_off, dst_off, count;  // doubles
+};
+enum A2ADir { A2A_MODE_TO_TIME = 0, A2A_TIME_TO_MODE = 1 };
+bool dist_layout(const Geom& g, int nt, int rank, int nranks, DistLayout* L);
+void a2a_schedule(const DistLayout& L, int dir, int shift, std::vector<A2AMsg>& sends, std::vector<A2AMsg>& recvs);
+int a2a_execute(void* comm, const DistLayout& L, const std::vector<A2AMsg>& sends, const std::vector<A2AMsg>& recvs,
+                const double* src, double* dst, cudaStream_t st, std::string& err);
+int allreduce_sum(void* comm, int nranks, double* buf, long count, cudaStream_t st, std::string& err);
 
 }  // namespace expd

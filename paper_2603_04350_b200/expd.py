@@ -49,6 +49,11 @@ EXPORTS = [
     "expd_set_profiling",
     "expd_sweep_stage_ms",
     "expd_debug_kernel_ms",
+    "expd_layout_query",
+    "expd_a2a_schedule",
+    "expd_nccl_unique_id",
+    "expd_nccl_comm_init",
+    "expd_nccl_comm_destroy",
 ]
 
 
@@ -75,6 +80,11 @@ class _Problem(C.Structure):
 
 class _Dist(C.Structure):
     _fields_ = [("rank", C.c_int), ("nranks", C.c_int), ("nccl_comm", C.c_void_p)]
+
+
+class _Layout(C.Structure):
+    _fields_ = [("rank", C.c_int), ("nranks", C.c_int), ("npad", C.c_long), ("mode_off", C.c_long),
+                ("mode_len", C.c_long), ("t0", C.c_int), ("nt_local", C.c_int)]
 
 
 class _Report(C.Structure):
@@ -121,6 +131,12 @@ def load_library(path: str = LIB_PATH):
         "expd_set_profiling": (C.c_int, [vp, C.c_int]),
         "expd_sweep_stage_ms": (C.c_int, [vp, dp, dp]),
         "expd_debug_kernel_ms": (C.c_int, [vp, C.c_int, C.c_long, C.c_int, dp]),
+        "expd_layout_query": (C.c_int, [C.POINTER(_Problem), C.c_int, C.c_int, C.POINTER(_Layout)]),
+        "expd_a2a_schedule": (C.c_long, [C.POINTER(_Problem), C.c_int, C.c_int, C.c_int, C.c_int,
+                                         C.POINTER(C.c_long), C.POINTER(C.c_long), C.c_long]),
+        "expd_nccl_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),
+        "expd_nccl_comm_init": (C.c_int, [C.POINTER(C.c_ubyte), C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
+        "expd_nccl_comm_destroy": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -165,6 +181,73 @@ class Problem:
         return p
 
 
+def layout(problem: Problem, rank: int, nranks: int) -> dict:
+    """This rank's time slab and mode slab (expd_layout_query; host only, no device)."""
+    lib = load_library()
+    out = _Layout()
+    st = lib.expd_layout_query(C.byref(problem._c()), rank, nranks, C.byref(out))
+    if st != EXPD_OK:
+        raise ExpdError(st, "expd_layout_query")
+    return {k: getattr(out, k) for k, _ in _Layout._fields_}
+
+
+def a2a_schedule(problem: Problem, rank: int, nranks: int, direction: int, shift: int = 0):
+    """The all-to-all messages this rank posts (expd_a2a_schedule): two int64 arrays
+    (sends, recvs) of rows {peer, src_off, dst_off, count}, in posting order."""
+    import numpy as np
+
+    lib = load_library()
+    p = problem._c()
+    n = lib.expd_a2a_schedule(C.byref(p), rank, nranks, direction, shift, None, None, 0)
+    if n < 0:
+        raise ExpdError(1, "expd_a2a_schedule")
+    s = np.zeros((n, 4), dtype=np.int64)
+    r = np.zeros((n, 4), dtype=np.int64)
+    lp = C.POINTER(C.c_long)
+    lib.expd_a2a_schedule(C.byref(p), rank, nranks, direction, shift, s.ctypes.data_as(lp), r.ctypes.data_as(lp), n)
+    return s, r
+
+
+class Comm:
+    """An NCCL communicator for distributed plans.  Rank 0's unique id is
+    broadcast over a torch.distributed process group; the library creates the communicator
+    (expd_nccl_comm_init) and this object owns it."""
+
+    def __init__(self, rank: int, nranks: int, device: int, group=None):
+        import torch.distributed as dist
+
+        self.lib = load_library()
+        self.rank, self.nranks, self.device = rank, nranks, device
+        uid = (C.c_ubyte * 128)()
+        if rank == 0:
+            st = self.lib.expd_nccl_unique_id(uid)
+            if st != EXPD_OK:
+                raise ExpdError(st, "expd_nccl_unique_id")
+        if nranks > 1:
+            backend = dist.get_backend(group)
+            t = torch.tensor(list(bytes(uid)), dtype=torch.uint8)
+            if backend == "nccl":
+                t = t.to(f"cuda:{device}")
+            dist.broadcast(t, src=0, group=group)
+            uid = (C.c_ubyte * 128)(*t.cpu().tolist())
+        h = C.c_void_p()
+        st = self.lib.expd_nccl_comm_init(uid, nranks, rank, device, C.byref(h))
+        if st != EXPD_OK:
+            raise ExpdError(st, "expd_nccl_comm_init")
+        self.ptr = h
+
+    def close(self):
+        if getattr(self, "ptr", None):
+            self.lib.expd_nccl_comm_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
 def _ptr(t: torch.Tensor | None):
     if t is None:
         return None
@@ -176,7 +259,8 @@ def _ptr(t: torch.Tensor | None):
 class Plan:
     """An expd_plan plus its torch-allocated workspace on one device."""
 
-    def __init__(self, problem: Problem, device: int | None = None, krylov_vectors: int = 0, stream=None):
+    def __init__(self, problem: Problem, device: int | None = None, krylov_vectors: int = 0, stream=None,
+                 comm: Comm | None = None):
         if not torch.cuda.is_available():
             raise RuntimeError("expd requires a CUDA device (no CPU fallback)")
         self.lib = load_library()
@@ -184,7 +268,11 @@ class Plan:
         self.device = torch.cuda.current_device() if device is None else device
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
         self._p = problem._c()
-        dist = _Dist(0, 1, None)
+        # comm: distributed schedule (time slabs in the API, mode slabs for K1); with
+        # comm.nranks == 1 it runs on one GPU with local copies for the all-to-alls
+        self.comm = comm
+        dist = _Dist(comm.rank, comm.nranks, comm.ptr) if comm is not None else _Dist(0, 1, None)
+        self.layout = layout(problem, dist.rank, dist.nranks)
         handle = C.c_void_p()
         st = self.lib.expd_plan_create(C.byref(self._p), C.byref(dist), self.device,
                                        C.c_void_p(self.stream.cuda_stream), C.byref(handle))
@@ -215,7 +303,8 @@ class Plan:
             pass
 
     def _vec(self):
-        return torch.empty((self.problem.nt,) + self.problem.shape, dtype=torch.float64,
+        """A physical space-time vector of this rank: its time slab (all nt slices on one GPU)."""
+        return torch.empty((self.layout["nt_local"],) + self.problem.shape, dtype=torch.float64,
                            device=f"cuda:{self.device}")
 
     # ---- primitives ------------------------------------------------------------------
@@ -251,8 +340,7 @@ class Plan:
         }
 
     def fixed_point_solve(self, u0, U=None, tol=1e-12, maxit=100):
-        U = torch.zeros((self.problem.nt,) + self.problem.shape, dtype=torch.float64,
-                        device=f"cuda:{self.device}") if U is None else U
+        U = self._vec().zero_() if U is None else U
         r, hist = self._report(maxit)
         st = self.lib.expd_fixed_point_solve(self.handle, _ptr(u0), _ptr(U), tol, maxit, C.byref(r))
         if st not in (EXPD_OK, 7):
@@ -260,8 +348,7 @@ class Plan:
         return U, self._rdict(r, hist, st)
 
     def gmres_solve(self, u0, U=None, tol=1e-12, restart=20, maxit=100):
-        U = torch.zeros((self.problem.nt,) + self.problem.shape, dtype=torch.float64,
-                        device=f"cuda:{self.device}") if U is None else U
+        U = self._vec().zero_() if U is None else U
         r, hist = self._report(maxit)
         st = self.lib.expd_gmres_solve(self.handle, _ptr(u0), _ptr(U), tol, restart, maxit, C.byref(r))
         if st not in (EXPD_OK, 7):

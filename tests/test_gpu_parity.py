@@ -202,3 +202,66 @@ def test_invalid_problems(kw, status):
     with pytest.raises(ExpdError) as ei:
         Plan(Problem(**base))
     assert ei.value.status == status
+
+
+# ------------------------------------------------------------------------------------------
+# the distributed schedule on one GPU: a real NCCL communicator of one rank,
+# mode-slab K1, time-slab stage 3, all-to-alls (here local copies) and allreduces
+# ------------------------------------------------------------------------------------------
+@pytest.fixture(scope="module")
+def comm1():
+    from paper_2603_04350_b200 import Comm
+
+    c = Comm(0, 1, 0)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("name,n,nt", [("c1", None, None), ("c3", 63, 128), ("c5", 63, 256), ("c2", 63, 64),
+                                       ("c5", 255, 16)])
+def test_dist1_fixed_point_parity(orc, comm1, name, n, nt):
+    cfg = synth.CONFIGS[name] if n is None else cfg_small(name, n, nt)
+    plan = Plan(Problem.from_config(cfg), comm=comm1)
+    u0 = synth.initial_condition(cfg)
+    U, rep = plan.fixed_point_solve(T(u0), tol=cfg.tol, maxit=50)
+    Uo, st, its, hist = orc.fixed_point(orc.spec(cfg), u0, tol=cfg.tol, maxit=50)
+    assert st == 0 and rep["converged"] and rep["iterations"] == its
+    assert relmax(H(U), Uo) < 1e-9
+
+
+@pytest.mark.parametrize("name,n,nt", [("c2", 63, 64), ("c4", 15, 64)])
+def test_dist1_gmres_parity(orc, comm1, name, n, nt):
+    cfg = cfg_small(name, n, nt)
+    plan = Plan(Problem.from_config(cfg), krylov_vectors=21, comm=comm1)
+    u0 = synth.initial_condition(cfg)
+    U, rep = plan.gmres_solve(T(u0), tol=cfg.tol, restart=20, maxit=50)
+    Uo, st, its, hist = orc.gmres(orc.spec(cfg), u0, tol=cfg.tol, restart=20, maxit=50)
+    assert st == 0 and rep["converged"] and rep["iterations"] == its
+    assert relmax(H(U), Uo) < 1e-9
+
+
+@pytest.mark.parametrize("name,n,nt", [("c5", 31, 256), ("c3", 255, 8)])
+def test_dist1_primitives_parity(orc, comm1, name, n, nt):
+    cfg = cfg_small(name, n, nt)
+    plan = Plan(Problem.from_config(cfg), comm=comm1)
+    s = orc.spec(cfg)
+    R = synth.random_spacetime(cfg)
+    want, _ = orc.precond(s, R)
+    assert relmax(H(plan.precond_apply(T(R))), want) < 1e-11
+    u0 = synth.initial_condition(cfg)
+    U = synth.random_spacetime(cfg, scale=0.5)
+    Rg, rn2 = plan.residual(T(u0), T(U), norm=True)
+    want, wn2 = orc.residual(s, u0, U)
+    assert relmax(H(Rg), want) < 1e-11
+    assert abs(rn2 - wn2) < 1e-11 * wn2
+
+
+def test_dist1_matches_single_gpu_schedule(comm1):
+    # same problem through both schedules: the same kernels on the same modes, so the
+    # solutions agree to rounding (only the all-to-all copies and the stage-3 chunking differ)
+    cfg = cfg_small("c5", 255, 16)
+    u0 = T(synth.initial_condition(cfg))
+    U1, r1 = Plan(Problem.from_config(cfg)).fixed_point_solve(u0, tol=cfg.tol, maxit=50)
+    U2, r2 = Plan(Problem.from_config(cfg), comm=comm1).fixed_point_solve(u0, tol=cfg.tol, maxit=50)
+    assert r1["iterations"] == r2["iterations"]
+    assert relmax(H(U2), H(U1)) < 1e-13
