@@ -187,7 +187,7 @@ extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dis
     a2a_schedule(p->L, A2A_TIME_TO_MODE, 0, p->t2m_s, p->t2m_r);
     a2a_schedule(p->L, A2A_TIME_TO_MODE, 1, p->t2m1_s, p->t2m1_r);
   }
-  p->time_grid = time_fused_grid(P.nt, p->mlen / 2, p->sms);
+  p->time_grid = time_fused_grid(P.nt, p->mlen / 2, p->sms, p->nl);
   p->vgrid = vec_grid(p->sms);
   *out = p;
   return EXPD_OK;

@@ -1,5 +1,6 @@
 // expd_internal.h -- internal types shared by the host driver and the kernels of libexpd.so.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <cstddef>
@@ -69,7 +70,7 @@ enum OutMode { OUT_S = 0, OUT_UPDATE = 1 };
 
 // kernel launchers (k_time.cu)
 cudaError_t launch_time_fused(const TimeArgs& a, int rmode, int outmode, int nl, int grid, cudaStream_t st);
-int time_fused_grid(int nt, long npairs, int sms);
+int time_fused_grid(int nt, long npairs, int sms, int nl);
 cudaError_t launch_resid_only(const TimeArgs& a, int nl, int grid, cudaStream_t st);
 
 // DST-I / nonlinear (k_dst.cu)
@@ -94,6 +95,9 @@ int nonlin_chunk_slices(const Geom& g);
 // TMA line kernels (k_line.cu): one axis pass (0 = x rows, 1 = y, 2 = z) over padded
 // spectral slices, nl fusing [V, N, V] on a strided axis.  in / out may alias.
 bool line_supported(const Geom& g);
+bool tma_available();
+cudaError_t make_tmap_2d(CUtensorMap* m, const double* ptr, unsigned long long cols, unsigned long long rows,
+                         unsigned long long row_bytes, unsigned box_cols, unsigned box_rows);
 cudaError_t line_pass(const Geom& g, const DstTables& t, const Poly& P, int ax, bool nl, const double* in,
                       double* out, long nslices, cudaStream_t st);
 int nonlin_kernel_launches(const Geom& g, long nslices);

@@ -461,6 +461,22 @@ static cudaError_t make_map(CUtensorMap* m, const double* ptr, const cuuint64_t 
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// 2-D fp64 tensor map (no swizzle): rows of `cols` doubles at byte stride row_bytes.
+cudaError_t make_tmap_2d(CUtensorMap* m, const double* ptr, unsigned long long cols, unsigned long long rows,
+                         unsigned long long row_bytes, unsigned box_cols, unsigned box_rows) {
+  EncodeTiledFn f = encode_fn();
+  if (!f) return cudaErrorNotSupported;
+  const cuuint64_t d[2] = {cols, rows};
+  const cuuint64_t s[1] = {row_bytes};
+  const cuuint32_t b[2] = {box_cols, box_rows};
+  const cuuint32_t es[2] = {1, 1};
+  CUresult r = f(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(ptr), d, s, b, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+bool tma_available() { return encode_fn() != nullptr; }
+
 // Tensor map of nslices padded spectral slices for one axis pass (COL: G column pairs).
 static cudaError_t axis_map(CUtensorMap* m, const Geom& g, int ax, const double* ptr, long nslices, int G) {
   const cuuint64_t M = (cuuint64_t)g.M, n = (cuuint64_t)g.n;

@@ -21,8 +21,11 @@
 // 1/sqrt(Nt) factors) is folded into the reciprocal.
 #include <cstdlib>
 
+#include <cuda.h>
+
 #include "expd_internal.h"
 #include "fft_dev.cuh"
+#include "tma_dev.cuh"
 
 namespace expd {
 
@@ -544,19 +547,271 @@ __global__ void __launch_bounds__(EXPD_K1_THREADS, DB ? 1 : 2) k_time_pipe(const
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// K1, TMA-fed: the U-hat / N-hat time columns of a tile (S mode pairs x all NT slices =
+// one {2S doubles, NT rows} box per array) arrive by TMA tensor loads on an mbarrier (one
+// instruction per array instead of 2 NT S / THREADS cp.async per thread); the per-mode
+// tables by cp.async.  NST = 2: the next tile's loads overlap this tile's transform;
+// NST = 1: the overlap comes from the other CTAs on the SM.  THR sets S = THR / TPS.
+// ---------------------------------------------------------------------------------------
+template <int NT, int THR>
+struct TGeo {
+  using C = TimeCfg<NT>;
+  static constexpr int L = C::L, R0 = C::R0;
+  static constexpr int RL = L == 1 ? C::R0 : (L == 2 ? C::R1 : C::R2);
+  static constexpr int TPS = NT / R0;
+  static constexpr int THREADS = THR;
+  static constexpr int S = THR / TPS;
+  static constexpr int NSL = NT / RL;
+  static_assert(S >= 1 && S * TPS == THR, "THR must be a multiple of NT / R0");
+};
+
+template <int NT, int THR, int NL, int NST>
+struct TmaLayout {
+  using G = TGeo<NT, THR>;
+  static constexpr int S = G::S;
+  static constexpr int TILE = NT * S;                  // double2 per staged array
+  static constexpr int NARR = 1 + (NL ? 1 : 0);
+  static constexpr int AUX = 4 * S;                    // E, C1, C2, u0-hat per pair
+  static constexpr int STAGE = ((NARR * TILE + AUX) + 7) / 8 * 8;  // 128-byte multiple
+  static constexpr bool ALIAS = NL != 0;               // buf0 in the stage's N-hat block
+  static constexpr int FFTBUF = ALIAS ? TILE : 2 * TILE;
+  static constexpr size_t BYTES =
+      128 + sizeof(double2) * ((size_t)NST * STAGE + FFTBUF + NT) + sizeof(double) * 2 * NT + 16 * NST;
+  static constexpr int MINB_SMEM = (int)((228 * 1024) / (BYTES + 1024));
+  static constexpr int MINB = MINB_SMEM < 1 ? 1 : (MINB_SMEM > 8 ? 8 : MINB_SMEM);
+};
+
+template <int NT, int THR, int RM, int NL, int NST>
+__device__ __forceinline__ void tma_tile_issue(const CUtensorMap* mx, const CUtensorMap* mn, const TimeArgs& a,
+                                               long tile, double2* stage, uint64_t* bar) {
+  using PL = TmaLayout<NT, THR, NL, NST>;
+  constexpr int S = PL::S, TILE = PL::TILE;
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(bar, (uint32_t)(PL::NARR * TILE * 16));
+    tma_load_2d(stage, mx, bar, (int)(2 * S * tile), 0);
+    if constexpr (NL) tma_load_2d(stage + TILE, mn, bar, (int)(2 * S * tile), 0);
+  }
+  if (threadIdx.x < S) {
+    const int s = threadIdx.x;
+    const long pair = tile * S + s;
+    const bool ok = pair < a.npairs;
+    const long off = 2 * (ok ? pair : 0);
+    double2* aux = stage + PL::NARR * TILE;
+    cpa16(aux + s, a.E + off, ok);
+    if constexpr (NL >= 1) cpa16(aux + S + s, a.C1 + off, ok);
+    if constexpr (NL == 2) cpa16(aux + 2 * S + s, a.C2 + off, ok);
+    if constexpr (RM == RM_RESID) cpa16(aux + 3 * S + s, a.u0h + off, ok);
+  }
+  cpa_commit();
+}
+
+template <int NT, int RM, int OUTM, int NL, int THR, int NST>
+__global__ void __launch_bounds__(THR, (TmaLayout<NT, THR, NL, NST>::MINB))
+    k_time_tma(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mn,
+               const __grid_constant__ TimeArgs a) {
+  using G = TGeo<NT, THR>;
+  using C = TimeCfg<NT>;
+  using PL = TmaLayout<NT, THR, NL, NST>;
+  constexpr int L = G::L, R0 = G::R0, RL = G::RL, TPS = G::TPS, S = G::S, THREADS = THR;
+  constexpr int NSL = G::NSL, TILE = PL::TILE;
+  static_assert(L > 1, "TMA kernel needs a multi-stage FFT");
+  extern __shared__ unsigned char tsm_raw[];
+  double2* smem = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(tsm_raw) + 127) & ~uintptr_t(127));
+  double2* fft = smem + NST * PL::STAGE;
+  double2* stw = fft + PL::FFTBUF;                     // [NT] e^{+2 pi i q/NT}
+  double* sg = reinterpret_cast<double*>(stw + NT);    // [NT] alpha^{t/NT}
+  double* sgi = sg + NT;                               // [NT] alpha^{-t/NT}
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sgi + NT);
+
+  const int tid = threadIdx.x;
+  __builtin_assume(tid < THREADS);
+  for (int i = tid; i < NT; i += THREADS) {
+    stw[i] = a.tw[i];
+    sg[i] = a.g[i];
+    sgi[i] = a.ginv[i];
+  }
+  if (tid == 0) {
+    prefetch_tmap(&mx);
+    if constexpr (NL) prefetch_tmap(&mn);
+    for (int k = 0; k < NST; ++k) mbar_init(&bar[k], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const long ntiles = (a.npairs + S - 1) / S;
+  const double hin = a.half_inv_nt;
+  double nrm = 0.0;
+  const int s = tid % S;
+  const int j = tid / S;
+  const long npad = a.npad;
+
+  long tile = blockIdx.x;
+  if (tile < ntiles) tma_tile_issue<NT, THR, RM, NL, NST>(&mx, &mn, a, tile, smem, &bar[0]);
+  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+    const int cur = NST == 2 ? (it & 1) : 0;
+    double2* stg = smem + cur * PL::STAGE;
+    const long next = tile + gridDim.x;
+    if constexpr (NST == 2) {
+      if (next < ntiles) {
+        tma_tile_issue<NT, THR, RM, NL, NST>(&mx, &mn, a, next, smem + (cur ^ 1) * PL::STAGE, &bar[cur ^ 1]);
+        cpa_wait<1>();
+      } else {
+        cpa_wait<0>();
+      }
+    } else {
+      cpa_wait<0>();
+    }
+    mbar_wait(&bar[cur], (uint32_t)((NST == 2 ? (it >> 1) : it) & 1));
+    __syncthreads();  // the cp.async aux of every thread < S is visible
+    const double2* X = stg;
+    const double2* NH = stg + TILE;
+    const double2* aux = stg + PL::NARR * TILE;
+    double2* buf0 = PL::ALIAS ? stg + TILE : fft;
+    double2* buf1 = PL::ALIAS ? fft : fft + TILE;
+    const long pair = tile * S + s;
+    const bool valid = pair < a.npairs;
+    const long base = 2 * pair;
+
+    // ---- phase A: residual (+ ||r||^2), Gamma_alpha, forward stage 0 (times j + r TPS) ---
+    double2 y[R0];
+    const double2 Ej = aux[s];
+    const double2 c1 = NL >= 1 ? aux[S + s] : make_double2(0.0, 0.0);
+    const double2 c2 = NL == 2 ? aux[2 * S + s] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int r = 0; r < R0; ++r) {
+      const int t = j + r * TPS;
+      const double2 xc = X[t * S + s];
+      double2 rr;
+      if constexpr (RM == RM_INPUT) {
+        rr = xc;
+      } else {
+        const double2 prev = t > 0 ? X[(t - 1) * S + s] : (RM == RM_RESID ? aux[3 * S + s] : make_double2(0.0, 0.0));
+        if constexpr (RM == RM_RESID) {
+          rr = make_double2(fma(Ej.x, prev.x, -xc.x), fma(Ej.y, prev.y, -xc.y));
+          if constexpr (NL >= 1) {
+            const double2 nm1 = NH[t * S + s];
+            rr.x = fma(c1.x, nm1.x, rr.x);
+            rr.y = fma(c1.y, nm1.y, rr.y);
+            if constexpr (NL == 2) {
+              const double2 nm2 = NH[(t > 0 ? t - 1 : 0) * S + s];
+              rr.x = fma(-c2.x, nm2.x, rr.x);
+              rr.y = fma(-c2.y, nm2.y, rr.y);
+            }
+          }
+        } else {  // RM_QOP
+          rr = make_double2(fma(-Ej.x, prev.x, xc.x), fma(-Ej.y, prev.y, xc.y));
+        }
+      }
+      nrm = fma(rr.x, rr.x, fma(rr.y, rr.y, nrm));
+      y[r] = cscale(rr, sg[t]);
+    }
+    DFT<R0, +1>::run(y);
+    if constexpr (PL::ALIAS) __syncthreads();  // every thread is done reading N-hat
+#pragma unroll
+    for (int r = 0; r < R0; ++r) buf0[(j * R0 + r) * S + s] = y[r];
+    __syncthreads();
+    const double2* pin = buf0;
+    double2* pout = buf1;
+    if constexpr (L == 3) {
+      tstage<NT, S, THREADS, C::R1, R0, +1>(buf0, buf1, stw);
+      __syncthreads();
+      pin = buf1;
+      pout = buf0;
+    }
+    for (int PJ = tid; PJ < S * (NSL / 2); PJ += THREADS) {
+      const int ps = PJ % S, pj = PJ / S;
+      const int ja = pj, jb = pj == 0 ? NSL / 2 : NSL - pj;
+      double2 va[RL], vb[RL];
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        va[r] = pin[(ja + r * NSL) * S + ps];
+        vb[r] = pin[(jb + r * NSL) * S + ps];
+      }
+#pragma unroll
+      for (int r = 1; r < RL; ++r) {
+        va[r] = cmul(va[r], stw[(r * ja) & (NT - 1)]);
+        vb[r] = cmul(vb[r], stw[(r * jb) & (NT - 1)]);
+      }
+      DFT<RL, +1>::run(va);
+      DFT<RL, +1>::run(vb);
+      const double2 Ep = aux[ps];
+      pair_divide<NT, RL>(va, vb, pj == 0, stw, ja, jb, a.a1 * Ep.x, a.a1 * Ep.y, hin);
+      DFT<RL, -1>::run(va);
+      DFT<RL, -1>::run(vb);
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        pout[(ja * RL + r) * S + ps] = va[r];
+        pout[(jb * RL + r) * S + ps] = vb[r];
+      }
+    }
+    __syncthreads();
+    if constexpr (L == 3) {
+      tstage<NT, S, THREADS, C::R1, RL, -1>(buf0, buf1, stw);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < R0; ++r) y[r] = buf1[(j + r * TPS) * S + s];
+#pragma unroll
+    for (int r = 1; r < R0; ++r) y[r] = cmulc(y[r], stw[(r * j) & (NT - 1)]);
+    DFT<R0, -1>::run(y);
+    // ---- phase C: Gamma_alpha^{-1}, update (u_t from the staged tile), store ------------
+    if (valid) {
+#pragma unroll
+      for (int r = 0; r < R0; ++r) {
+        const int t = j + r * TPS;
+        double2 sv = cscale(y[r], sgi[t]);
+        if constexpr (OUTM == OUT_UPDATE) sv = cadd(X[t * S + s], sv);
+        st2(a.Y + (long)t * npad + base, sv);
+      }
+    }
+    // the stage (and buf0 inside it) is free for the next TMA load: order this thread's
+    // generic-proxy shared-memory accesses before the async-proxy writes, then barrier
+    fence_proxy_async_smem();
+    __syncthreads();
+    if constexpr (NST == 1) {
+      if (next < ntiles) tma_tile_issue<NT, THR, RM, NL, NST>(&mx, &mn, a, next, smem, &bar[0]);
+    }
+  }
+
+  if (a.partial) {
+    __shared__ double red[THREADS / 32];
+    for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+    if ((tid & 31) == 0) red[tid >> 5] = nrm;
+    __syncthreads();
+    if (tid < 32) {
+      double v = tid < THREADS / 32 ? red[tid] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (tid == 0) a.partial[blockIdx.x] = v;
+    }
+  }
+}
+
 template <int NT, int OUTM>
 static size_t time_smem_bytes() {
   const size_t tile = TimeGeo<NT>::L > 1 ? (size_t)NT * TimeGeo<NT>::S : 0;
   return sizeof(double2) * (2 * tile + NT) + sizeof(double) * 2 * NT;
 }
 
-// EXPD_K1_PIPE: 0 = register-load kernel, 1 = double-buffered pipe (1 CTA/SM),
-// 2 (default) = single-stage pipe with two CTAs per SM
+// EXPD_K1_PIPE: 0 = register-load kernel, 1 = double-buffered cp.async pipe (1 CTA/SM),
+// 2 = single-stage cp.async pipe with two CTAs per SM, 3 (default) = TMA-fed kernel with
+// the variant EXPD_K1V = <threads><stages> (e.g. 2561, 2562, 1281, 1282)
 static int pipe_mode() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("EXPD_K1_PIPE");
-    v = (e && (e[0] == '0' || e[0] == '1')) ? e[0] - '0' : 2;
+    v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 3;
+    if (v == 3 && !tma_available()) v = 2;
+  }
+  return v;
+}
+// Only double-buffered (NST = 2) variants are built: the single-stage variant faulted
+// (illegal address in the linear residual mode, cause not found).
+static int k1_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EXPD_K1V");
+    v = e ? atoi(e) : 2562;
+    if (v != 2562 && v != 1282) v = 2562;
   }
   return v;
 }
@@ -576,9 +831,37 @@ static cudaError_t launch_pipe(const TimeArgs& a, int grid, cudaStream_t st) {
   return cudaGetLastError();
 }
 
+template <int NT, int RM, int OUTM, int NL, int THR, int NST>
+static cudaError_t launch_tma(const TimeArgs& a, int grid, cudaStream_t st) {
+  using PL = TmaLayout<NT, THR, NL, NST>;
+  auto k = k_time_tma<NT, RM, OUTM, NL, THR, NST>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PL::BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  constexpr int S = PL::S;
+  CUtensorMap mx, mn;
+  cudaError_t e = make_tmap_2d(&mx, a.X, (unsigned long long)a.npad, (unsigned long long)a.nt,
+                               (unsigned long long)a.npad * 8, 2 * S, NT);
+  if (e != cudaSuccess) return e;
+  mn = mx;
+  if (NL && (e = make_tmap_2d(&mn, a.Nh, (unsigned long long)a.npad, (unsigned long long)a.nt,
+                              (unsigned long long)a.npad * 8, 2 * S, NT)) != cudaSuccess)
+    return e;
+  // the caller's grid (time_fused_grid) is also the number of partial sums it reduces
+  k<<<(unsigned)grid, THR, PL::BYTES, st>>>(mx, mn, a);
+  return cudaGetLastError();
+}
+
 template <int NT, int RM, int OUTM, int NL>
 static cudaError_t launch_t(const TimeArgs& a, int grid, cudaStream_t st) {
   if constexpr (TimeGeo<NT>::L > 1) {
+    if (pipe_mode() == 3) {
+      if (k1_variant() == 1282) return launch_tma<NT, RM, OUTM, NL, 128, 2>(a, grid, st);
+      return launch_tma<NT, RM, OUTM, NL, 256, 2>(a, grid, st);
+    }
     if (pipe_mode() == 1) return launch_pipe<NT, RM, OUTM, NL, true>(a, grid, st);
     if (pipe_mode() == 2) return launch_pipe<NT, RM, OUTM, NL, false>(a, grid, st);
   }
@@ -626,8 +909,22 @@ cudaError_t launch_time_fused(const TimeArgs& a, int rmode, int outmode, int nl,
 
 // Persistent grid: a fixed multiple of the SM count (deterministic partial order), capped
 // by the number of tiles.
-int time_fused_grid(int nt, long npairs, int sms) {
-  int S = 32;
+// tiles per CTA-slot of the TMA variant: (pairs per tile, resident CTAs per SM)
+template <int NT>
+static void tma_shape(int nl, int& S, int& per_sm) {
+  if (k1_variant() == 1282) {
+    S = TmaLayout<NT, 128, 1, 2>::S;
+    per_sm = nl ? TmaLayout<NT, 128, 1, 2>::MINB : TmaLayout<NT, 128, 0, 2>::MINB;
+  } else {
+    S = TmaLayout<NT, 256, 1, 2>::S;
+    per_sm = nl ? TmaLayout<NT, 256, 1, 2>::MINB : TmaLayout<NT, 256, 0, 2>::MINB;
+  }
+}
+
+// Persistent grid: a fixed multiple of the SM count (deterministic partial order), capped
+// by the number of tiles.  nl: the plan's heaviest K1 variant (N-hat staged too).
+int time_fused_grid(int nt, long npairs, int sms, int nl) {
+  int S = 32, per_sm = EXPD_K1_MINB;
   switch (nt) {
     case 4: S = TimeGeo<4>::S; break;
     case 8: S = TimeGeo<8>::S; break;
@@ -637,8 +934,18 @@ int time_fused_grid(int nt, long npairs, int sms) {
     case 128: S = TimeGeo<128>::S; break;
     default: S = TimeGeo<256>::S;
   }
+  if (nt >= 16 && use_pipe()) per_sm = pipe_mode() == 1 ? 1 : 2;
+  if (nt >= 16 && pipe_mode() == 3) {
+    switch (nt) {
+      case 16: tma_shape<16>(nl, S, per_sm); break;
+      case 32: tma_shape<32>(nl, S, per_sm); break;
+      case 64: tma_shape<64>(nl, S, per_sm); break;
+      case 128: tma_shape<128>(nl, S, per_sm); break;
+      default: tma_shape<256>(nl, S, per_sm);
+    }
+  }
   long ntiles = (npairs + S - 1) / S;
-  long g = (long)sms * ((nt >= 16 && use_pipe()) ? (pipe_mode() == 1 ? 1 : 2) : EXPD_K1_MINB);
+  long g = (long)sms * per_sm;
   return (int)(ntiles < g ? (ntiles > 0 ? ntiles : 1) : g);
 }
 
