@@ -607,13 +607,16 @@ cudaError_t dst_slices(const Geom& g, const DstTables& t, const double* src, boo
 }
 
 int nonlin_chunk_slices(const Geom& g) {
-  // keep one chunk's intermediate (npad doubles per slice) within ~EXPD_CHUNK_MB (default
-  // 64) MB so it stays in the 126 MB L2 between the axis passes
+  // slices per stage-3 chunk: the chunk's intermediate (npad doubles per slice) is about
+  // EXPD_CHUNK_MB (default 512) MB.  Measured on c5 (profiles/r01): 2-slice chunks that fit
+  // the 126 MB L2 lose more to launch tails than the L2 residency saves -- the axis passes
+  // are shared-memory / fp64 bound and the extra HBM round trip of the intermediate
+  // overlaps them (64 MB: 21.7 ms stage 3, 512 MB: 18.9 ms)
   static long mb = -1;
   if (mb < 0) {
     const char* e = getenv("EXPD_CHUNK_MB");
-    mb = e ? atol(e) : 64;
-    if (mb < 1) mb = 64;
+    mb = e ? atol(e) : 512;
+    if (mb < 1) mb = 512;
   }
   long per = g.npad * 8;
   long c = (mb << 20) / (per > 0 ? per : 1);

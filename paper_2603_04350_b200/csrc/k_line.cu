@@ -56,13 +56,19 @@ struct LGeo {
   static constexpr int L = (M / 2) / T;       // k-values per thread in the prefix sum (= R0/2)
   static constexpr int PADP = R0;             // one pad slot per PADP positions
   static constexpr int SW = M + M / PADP;     // padded positions per line pair
+  static constexpr int WS = (M / 2) / L * (L + 1);  // one unpacked array W or E (padded)
+  static constexpr int SWB = SW > 2 * WS ? SW : 2 * WS;
   static constexpr int JW = 32 / G;           // threads of one line pair inside a warp
   static constexpr int NWB = T / JW;          // warp blocks per line pair
-  static constexpr size_t BUFB = ((size_t)G * SW * 16 + 1023) / 1024 * 1024;  // bytes per buffer
+  static constexpr size_t BUFB = ((size_t)G * SWB * 16 + 1023) / 1024 * 1024;  // bytes per buffer
   static constexpr size_t SMEM = 1024 + NBUF * BUFB + 16 * (size_t)(NWB * G) + 16;
-  // resident CTAs per SM: shared memory (228 KB, 1 KB reserved per CTA) and >= 160 registers
+  // resident CTAs per SM: shared memory (228 KB, 1 KB reserved per CTA) and >= EXPD_LINE_REGS
+  // registers per thread
+#ifndef EXPD_LINE_REGS
+#define EXPD_LINE_REGS 160
+#endif
   static constexpr int MINB_SMEM = (int)((228 * 1024) / (SMEM + 1024));
-  static constexpr int MINB_REG = 65536 / (THREADS * 160);
+  static constexpr int MINB_REG = 65536 / (THREADS * EXPD_LINE_REGS);
   static constexpr int MINB = MINB_SMEM < MINB_REG ? (MINB_SMEM > 0 ? MINB_SMEM : 1) : (MINB_REG > 0 ? MINB_REG : 1);
 };
 
@@ -97,12 +103,29 @@ __device__ __forceinline__ void lunpack(double2 Zk, double2 Zm, bool k0, double2
   w = make_double2(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y + Zm.y));
   if (k0) w = make_double2(0.5 * w.x, 0.5 * w.y);
 }
+// v[r] *= w^{r b}, r = 1..R-1, from the single table entry w^b.  EXPD_LINE_TWSEQ: running
+// product (two live twiddles, r roundings deep); default: binary splitting (all R powers
+// live, <= 2 log2 R roundings deep).
 template <int R>
-__device__ __forceinline__ void ltw(const double2* __restrict__ tw, int b, double2 (&t)[R]) {
-  t[0] = make_double2(1.0, 0.0);
-  if constexpr (R > 1) t[1] = __ldg(tw + b);
+__device__ __forceinline__ void ltwmul(const double2* __restrict__ tw, int b, double2* v) {
+  if constexpr (R > 1) {
+    const double2 w1 = __ldg(tw + b);
+#ifdef EXPD_LINE_TWSEQ
+    double2 cur = w1;
 #pragma unroll
-  for (int r = 2; r < R; ++r) t[r] = (r % 2 == 0) ? cmul(t[r / 2], t[r / 2]) : cmul(t[r - 1], t[1]);
+    for (int r = 1; r < R; ++r) {
+      v[r] = cmul(v[r], cur);
+      if (r + 1 < R) cur = cmul(cur, w1);
+    }
+#else
+    double2 t[R];
+    t[1] = w1;
+#pragma unroll
+    for (int r = 2; r < R; ++r) t[r] = (r % 2 == 0) ? cmul(t[r / 2], t[r / 2]) : cmul(t[r - 1], t[1]);
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[r] = cmul(v[r], t[r]);
+#endif
+  }
 }
 
 // position p of line pair g in the padded work layout [SW][G]
@@ -126,10 +149,7 @@ __device__ __forceinline__ void lmid(double2* buf, const double2* __restrict__ t
       const int g = J % G, jm = J / G, k = jm % NS;
 #pragma unroll
       for (int r = 0; r < R; ++r) v[jt][r] = lat<M, G>(buf, jm + r * (M / R), g);
-      double2 t[R];
-      ltw<R>(tw, k * TWS, t);
-#pragma unroll
-      for (int r = 1; r < R; ++r) v[jt][r] = cmul(v[jt][r], t[r]);
+      ltwmul<R>(tw, k * TWS, v[jt]);
       DFT<R, -1>::run(v[jt]);
     }
   }
@@ -181,18 +201,18 @@ __device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* 
         va[pt][r] = lat<M, G>(buf, ja + r * NSL, gg);
         vb[pt][r] = lat<M, G>(buf, jb + r * NSL, gg);
       }
-      double2 t[RL];
-      ltw<RL>(tw, ja, t);
-#pragma unroll
-      for (int r = 1; r < RL; ++r) va[pt][r] = cmul(va[pt][r], t[r]);
-      ltw<RL>(tw, jb, t);
-#pragma unroll
-      for (int r = 1; r < RL; ++r) vb[pt][r] = cmul(vb[pt][r], t[r]);
+      ltwmul<RL>(tw, ja, va[pt]);
+      ltwmul<RL>(tw, jb, vb[pt]);
       DFT<RL, -1>::run(va[pt]);
       DFT<RL, -1>::run(vb[pt]);
     }
   }
   __syncthreads();
+  // unpack into two arrays W[k] = w_k (k = 0..M/2-1) and E[k] = e_k (k = 1..M/2), each
+  // padded with one slot per L entries: consecutive threads write consecutive k and the
+  // prefix below reads L consecutive entries per thread, both without bank conflicts
+  double2* Wb = buf;
+  double2* Eb = buf + D::WS * G;
 #pragma unroll
   for (int pt = 0; pt < PJT; ++pt) {
     const int PJ = threadIdx.x + pt * D::THREADS;
@@ -204,12 +224,12 @@ __device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* 
         double2 e, w;
         const int ka = ja + NSL * r;
         lunpack(va[pt][r], pj == 0 ? va[pt][(RL - r) % RL] : vb[pt][RL - 1 - r], ka == 0, e, w);
-        if (ka >= 1) lat<M, G>(buf, 2 * ka - 1, gg) = e;
-        lat<M, G>(buf, 2 * ka, gg) = w;
+        if (ka >= 1) Eb[lswz<L>(ka) * G + gg] = e;
+        Wb[lswz<L>(ka) * G + gg] = w;
         const int kb = jb + NSL * r;
         lunpack(vb[pt][r], pj == 0 ? vb[pt][RL - 1 - r] : va[pt][RL - 1 - r], false, e, w);
-        lat<M, G>(buf, 2 * kb - 1, gg) = e;
-        lat<M, G>(buf, 2 * kb, gg) = w;
+        Eb[lswz<L>(kb) * G + gg] = e;
+        Wb[lswz<L>(kb) * G + gg] = w;
       }
     }
   }
@@ -218,12 +238,14 @@ __device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* 
   // out[2l] = F_{2k+1} = sum_{k' <= k} w_k', out[2l+1] = F_{2k+2} = e_{k+1}
   double2 tot = make_double2(0.0, 0.0);
   {
-    const double2* P = buf + lswz<PADP>(2 * j * L) * G + g;  // 2L <= PADP consecutive positions
+    const double2* Pw = Wb + (j * (L + 1)) * G + g;  // W[jL .. jL + L): contiguous
+    const double2* Pe = Eb + (j * (L + 1)) * G + g;  // E[jL + 1 .. jL + L]: skips the pad slot
 #pragma unroll
     for (int l = 0; l < L; ++l) {
-      tot = cadd(tot, P[(2 * l) * G]);
+      tot = cadd(tot, Pw[l * G]);
       out[2 * l] = tot;
-      out[2 * l + 1] = (j == T - 1 && l == L - 1) ? make_double2(0.0, 0.0) : P[(2 * l + 1) * G];
+      const int el = l + 1 < L ? l + 1 : L + 1;
+      out[2 * l + 1] = (j == T - 1 && l == L - 1) ? make_double2(0.0, 0.0) : Pe[el * G];
     }
   }
   double2 inc = tot;
@@ -585,7 +607,15 @@ static cudaError_t launch_col(const Geom& g, const DstTables& t, const Poly& P, 
 template <int M>
 static cudaError_t line_pass_m(const Geom& g, const DstTables& t, const Poly& P, int ax, bool nl, const double* in,
                                double* out, long nslices, cudaStream_t st) {
-  if (ax == AX_ROW) return launch_line<M, AX_ROW, false, 1, 2>(g, t, P, in, out, nslices, st);
+  if (ax == AX_ROW) {
+    static int rv = -1;  // EXPD_ROWV=1: one buffer per CTA (more CTAs per SM)
+    if (rv < 0) {
+      const char* e = getenv("EXPD_ROWV");
+      rv = e ? atoi(e) : 2;
+    }
+    if (rv == 1) return launch_line<M, AX_ROW, false, 1, 1>(g, t, P, in, out, nslices, st);
+    return launch_line<M, AX_ROW, false, 1, 2>(g, t, P, in, out, nslices, st);
+  }
   if (ax == AX_COL_Y)
     return nl ? launch_col<M, AX_COL_Y, true>(g, t, P, in, out, nslices, st)
               : launch_col<M, AX_COL_Y, false>(g, t, P, in, out, nslices, st);
