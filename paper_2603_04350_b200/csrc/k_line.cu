@@ -107,9 +107,8 @@ __device__ __forceinline__ void lunpack(double2 Zk, double2 Zm, bool k0, double2
 // product (two live twiddles, r roundings deep); default: binary splitting (all R powers
 // live, <= 2 log2 R roundings deep).
 template <int R>
-__device__ __forceinline__ void ltwmul(const double2* __restrict__ tw, int b, double2* v) {
+__device__ __forceinline__ void ltwmul_w(double2 w1, double2* v) {
   if constexpr (R > 1) {
-    const double2 w1 = __ldg(tw + b);
 #ifdef EXPD_LINE_TWSEQ
     double2 cur = w1;
 #pragma unroll
@@ -127,6 +126,20 @@ __device__ __forceinline__ void ltwmul(const double2* __restrict__ tw, int b, do
 #endif
   }
 }
+template <int R>
+__device__ __forceinline__ void ltwmul(const double2* __restrict__ tw, int b, double2* v) {
+  if constexpr (R > 1) ltwmul_w<R>(__ldg(tw + b), v);
+}
+
+// Per-thread table values of one item, loaded before the item's data lands (their L1 / L2
+// latency then hides behind the TMA wait): sin(pi i/M) of the stage-0 positions and the
+// base twiddles of the thread's middle-stage job and last-stage partner jobs (valid when
+// each thread owns exactly one such job, the configurations used here).
+template <int M, int G>
+struct LPre {
+  double sp[LGeo<M, G, 1>::R0];
+  double2 tmid, ta, tb;
+};
 
 // position p of line pair g in the padded work layout [SW][G]
 template <int M, int G>
@@ -136,7 +149,7 @@ __device__ __forceinline__ double2& lat(double2* buf, int p, int g) {
 
 // In-place middle Stockham stage (radix R, NS) of the G line pairs in buf.
 template <int M, int G, int R, int NS>
-__device__ __forceinline__ void lmid(double2* buf, const double2* __restrict__ tw) {
+__device__ __forceinline__ void lmid(double2* buf, const double2* __restrict__ tw, double2 tpre) {
   using D = LGeo<M, G, 1>;
   constexpr int JOBS = G * (M / R);
   constexpr int JT = (JOBS + D::THREADS - 1) / D::THREADS;
@@ -149,7 +162,8 @@ __device__ __forceinline__ void lmid(double2* buf, const double2* __restrict__ t
       const int g = J % G, jm = J / G, k = jm % NS;
 #pragma unroll
       for (int r = 0; r < R; ++r) v[jt][r] = lat<M, G>(buf, jm + r * (M / R), g);
-      ltwmul<R>(tw, k * TWS, v[jt]);
+      if (JT == 1) ltwmul_w<R>(tpre, v[jt]);
+      else ltwmul<R>(tw, k * TWS, v[jt]);
       DFT<R, -1>::run(v[jt]);
     }
   }
@@ -172,7 +186,8 @@ __device__ __forceinline__ void lmid(double2* buf, const double2* __restrict__ t
 // a barrier (buf may still be read by the caller's stage-0 loads).
 template <int M, int G>
 __device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* buf, double2* wt,
-                                      const double2* __restrict__ tw, double2 (&out)[2 * LGeo<M, G, 1>::L]) {
+                                      const double2* __restrict__ tw, double2 (&out)[2 * LGeo<M, G, 1>::L],
+                                      const LPre<M, G>& pre) {
   using D = LGeo<M, G, 1>;
   constexpr int R0 = D::R0, RL = D::RL, NSL = D::NSL, T = D::T, L = D::L, PADP = D::PADP;
   const int g = threadIdx.x % G, j = threadIdx.x / G;
@@ -184,7 +199,7 @@ __device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* 
     for (int r = 0; r < R0; ++r) o0[r * G] = v[r];
   }
   __syncthreads();
-  lmid<M, G, D::RM1, R0>(buf, tw);
+  lmid<M, G, D::RM1, R0>(buf, tw, pre.tmid);
   // last stage on Hermitian partner jobs (ja, jb): frequency sets k = ja + NSL r and
   // jb + NSL r pair up as k <-> M - k; then the unpack into e_k (position 2k-1), w_k (2k)
   constexpr int PJOBS = G * (NSL / 2);
@@ -201,8 +216,13 @@ __device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* 
         va[pt][r] = lat<M, G>(buf, ja + r * NSL, gg);
         vb[pt][r] = lat<M, G>(buf, jb + r * NSL, gg);
       }
-      ltwmul<RL>(tw, ja, va[pt]);
-      ltwmul<RL>(tw, jb, vb[pt]);
+      if (PJT == 1) {
+        ltwmul_w<RL>(pre.ta, va[pt]);
+        ltwmul_w<RL>(pre.tb, vb[pt]);
+      } else {
+        ltwmul<RL>(tw, ja, va[pt]);
+        ltwmul<RL>(tw, jb, vb[pt]);
+      }
       DFT<RL, -1>::run(va[pt]);
       DFT<RL, -1>::run(vb[pt]);
     }
@@ -367,6 +387,16 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
     const double2* tw = a.tw;
     const double* sinp = a.sinp;
     asm volatile("" : "+l"(tw), "+l"(sinp));
+    LPre<M, G> pre;
+    {
+#pragma unroll
+      for (int r = 0; r < R0; ++r) pre.sp[r] = __ldg(sinp + j + T * r);  // sinp[0] = 0
+      constexpr int NS1 = R0, TWS1 = M / (NS1 * D::RM1);
+      pre.tmid = __ldg(tw + (j % NS1) * TWS1);
+      constexpr int NSL = D::NSL;
+      pre.ta = __ldg(tw + (j < NSL / 2 ? j : 0));
+      pre.tb = __ldg(tw + (j == 0 ? NSL / 2 : (j < NSL / 2 ? NSL - j : 0)));
+    }
     mbar_wait(&bar[cur], (uint32_t)((NBUF == 2 ? (it >> 1) : it) & 1));
 
     double2 out[2 * L];
@@ -389,15 +419,15 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
                                          *reinterpret_cast<const double*>(cb + M * 8 + o1));
           const double2 zm = make_double2(*reinterpret_cast<const double*>(cb + o2),
                                           *reinterpret_cast<const double*>(cb + M * 8 + o2));
-          v[r] = lpre(z, zm, __ldg(sinp + i));
+          v[r] = lpre(z, zm, pre.sp[r]);
         } else {
           // pass 0: raw [row][G] linear; pass 1: the padded layout written by the N step
           const int p1 = i - 1, p2 = M - i - 1;
           const int q1 = pass ? lswz<PADP>(p1) : p1, q2 = pass ? lswz<PADP>(p2) : p2;
-          v[r] = lpre(buf[q1 * G + g], buf[q2 * G + g], __ldg(sinp + i));
+          v[r] = lpre(buf[q1 * G + g], buf[q2 * G + g], pre.sp[r]);
         }
       }
-      lcore<M, G>(v, buf, wt, tw, out);
+      lcore<M, G>(v, buf, wt, tw, out, pre);
       if (NL && pass + 1 < npass) {
         __syncthreads();  // everyone has read (e, w) of pass 0
 #pragma unroll
