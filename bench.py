@@ -33,6 +33,21 @@ import time
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+# fp64 FMA throughput of this pool's B200 (not in MEASURED_PEAKS.json): a DFMA loop measured
+# 34.19 TFLOP/s (profiles/r01_probe_fp64_hbm.txt, tools/probe_fp64.cu); nominal 148 SMs x 64
+# DFMA/clk x 2 x 1.965 GHz = 37.2 TFLOP/s
+FP64_PEAK_TFLOPS = 34.19
+
+
+def dst_flops_per_line_pair(M: int) -> float:
+    """Algorithmic fp64 flops of one DST-I transform of two real lines of length M-1
+    (DESIGN.md "K2/K3"): complex FFT of length M (5 M log2 M, the radix-2 count) + the
+    sinft pre-processing, Hermitian unpack, prefix sum and scaling (15 flops per point)."""
+    import math
+
+    return 5.0 * M * math.log2(M) + 15.0 * M
+
+
 BYTES_PER_DOF = {  # algorithmic fp64 bytes per space-time dof (DESIGN.md "Byte model")
     "k1_linear": 16,      # read U-hat, write U-hat
     "k1_nonlinear": 24,   # read U-hat, read N-hat, write U-hat
@@ -279,15 +294,40 @@ def run_ours(args):
         traffic = prof.get(f"{cfg.name}:k1", None)
     except Exception:
         pass
-    roofline = {"bound": "hbm", "kernel": "k_time_fused (K1: residual+norm+preconditioner+update)",
-                "achieved": k1_gbs, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
-                "frac": k1_gbs / hbm_peak, "traffic": traffic,
-                "algorithmic_bytes_per_launch": k1_bytes, "launch_ms": k1_ms}
-    kernels = {"k1_ms": k1_ms, "k1_gbs": k1_gbs, "stage3_ms": s3_ms,
+    k1_roof = {"bound": "hbm", "kernel": "k_time_tma (K1: residual + ||r||^2 + alpha-circulant preconditioner + "
+                                        "update, one HBM pass)",
+               "achieved": k1_gbs, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
+               "frac": k1_gbs / hbm_peak, "traffic": traffic,
+               "algorithmic_bytes_per_launch": k1_bytes, "launch_ms": k1_ms, "launches_per_step": 1}
+    kernels = {"k1": k1_roof, "stage3_ms": s3_ms,
                "stage3_gbs": (s3_bytes / (s3_ms * 1e-3) / 1e9) if s3_ms > 0 else None,
                "sweep_ms": ms_step,
                "sweep_algorithmic_gbs": (k1_bytes + s3_bytes) / (ms_step * 1e-3) / 1e9,
                "sweep_frac_of_peak": (k1_bytes + s3_bytes) / (ms_step * 1e-3) / 1e9 / hbm_peak}
+    roofline = k1_roof
+    if nl and ws == 1 and cfg.dim == 2:
+        # stage-3 kernel families, timed live with CUDA events on the plan's stream after the
+        # timed region (16-slice launches, as in the sweep's chunks); fp64-bound
+        ns = min(16, cfg.nt)
+        M = cfg.n + 1
+        pairs = ((cfg.n + 1) // 2) * ns
+        f_t = dst_flops_per_line_pair(M) * pairs                      # one axis transform
+        f_nl = 2 * f_t + 3.0 * 2 * M * pairs                          # [V, N, V], cubic N
+        fam = {}
+        for which, label, flops, per_step in ((4, "line_x", f_t, 2), (6, "line_y_nl", f_nl, 1)):
+            ms_l = plan.debug_kernel_ms(which, ns, 5)
+            tf = flops / (ms_l * 1e-3) / 1e12
+            fam[label] = {"bound": "alu", "kernel": f"k_line ({label}: {'x-axis DST-I' if which == 4 else 'fused y [V, N(u), V]'})",
+                          "achieved": tf, "peak": FP64_PEAK_TFLOPS,
+                          "peak_source": "measured DFMA loop (profiles/r01_probe_fp64_hbm.txt)", "unit": "TFLOP/s",
+                          "frac": tf / FP64_PEAK_TFLOPS, "traffic": None, "algorithmic_flops_per_launch": flops,
+                          "launch_ms": ms_l, "slices_per_launch": ns,
+                          "ms_per_step": ms_l * per_step * (cfg.nt - 1) / ns}
+        kernels.update(fam)
+        # the dominant kernel of the step by device time
+        cand = [(k1_ms, k1_roof)] + [(v["ms_per_step"], v) for v in fam.values()]
+        roofline = max(cand, key=lambda x: x[0])[1]
+        kernels["dominant"] = roofline["kernel"]
 
     # e2e: full solve through the C-ABI with host buffers (H2D u0, solve, final IDST, D2H U)
     e2e = None
