@@ -354,7 +354,9 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
   static_assert(AX != AX_ROW || G == 1, "row items are one row pair");
   constexpr int R0 = D::R0, T = D::T, L = D::L, PADP = D::PADP;
   extern __shared__ unsigned char lsm_raw[];
-  char* base = reinterpret_cast<char*>((reinterpret_cast<uintptr_t>(lsm_raw) + 1023) & ~uintptr_t(1023));
+  // 1 KB-aligned base as an offset from the __shared__ array (pointer arithmetic on the
+  // array keeps the shared address space: LDS/STS, not generic LD/ST)
+  char* base = reinterpret_cast<char*>(lsm_raw + ((1024u - (smem_u32(lsm_raw) & 1023u)) & 1023u));
   double2* wt = reinterpret_cast<double2*>(base + NBUF * D::BUFB);
   uint64_t* bar = reinterpret_cast<uint64_t*>(wt + D::NWB * G);
   const int tid = threadIdx.x;

@@ -617,7 +617,8 @@ __global__ void __launch_bounds__(THR, (TmaLayout<NT, THR, NL, NST>::MINB))
   constexpr int NSL = G::NSL, TILE = PL::TILE;
   static_assert(L > 1, "TMA kernel needs a multi-stage FFT");
   extern __shared__ unsigned char tsm_raw[];
-  double2* smem = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(tsm_raw) + 127) & ~uintptr_t(127));
+  // 128-byte aligned base as an offset from the __shared__ array (keeps LDS/STS)
+  double2* smem = reinterpret_cast<double2*>(tsm_raw + ((128u - (smem_u32(tsm_raw) & 127u)) & 127u));
   double2* fft = smem + NST * PL::STAGE;
   double2* stw = fft + PL::FFTBUF;                     // [NT] e^{+2 pi i q/NT}
   double* sg = reinterpret_cast<double*>(stw + NT);    // [NT] alpha^{t/NT}
