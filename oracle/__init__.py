@@ -103,6 +103,7 @@ def lib():
             "orc_fixed_point": (C.c_int, [pp, dp, dp, C.c_double, C.c_int, dp, C.POINTER(C.c_int)]),
             "orc_gmres": (C.c_int, [pp, dp, dp, C.c_double, C.c_int, C.c_int, dp, C.POINTER(C.c_int)]),
             "orc_mode_residual": (None, [pp, C.c_long, dp, C.c_double, dp, dp]),
+            "orc_dst_sample_batch": (None, [pp, dp, C.c_long, C.POINTER(C.c_long), C.c_int, dp]),
             "orc_mode_precond": (None, [pp, C.c_long, dp, dp]),
         }
         for name, (res, args) in sig.items():
@@ -149,6 +150,18 @@ def dst_sample(s: Spec, v, idx) -> np.ndarray:
     out = np.empty(len(idx))
     p = s.c_struct()
     lib().orc_dst_sample(C.byref(p), _p(v), idx.ctypes.data_as(C.POINTER(C.c_long)), len(idx), _p(out))
+    return out
+
+
+def dst_sample_batch(s: Spec, V, idx) -> np.ndarray:
+    """dst_sample of every slice of V [nslices][n..n] at the flat mode indices idx:
+    an array [nslices][len(idx)]."""
+    V = _f64(V)
+    idx = np.ascontiguousarray(idx, dtype=np.int64)
+    ns = V.shape[0]
+    out = np.empty((ns, len(idx)))
+    p = s.c_struct()
+    lib().orc_dst_sample_batch(C.byref(p), _p(V), ns, idx.ctypes.data_as(C.POINTER(C.c_long)), len(idx), _p(out))
     return out
 
 

@@ -207,6 +207,46 @@ void orc_dst_sample(const orc_problem* p, const double* in, const long* idx, int
   free(S);
 }
 
+/* The same sampled outputs for nslices consecutive slices (one sine table for all; the
+   sums per output are those of orc_dst_sample). */
+void orc_dst_sample_batch(const orc_problem* p, const double* in, long nslices, const long* idx, int ns,
+                          double* out) {
+  ld* S = sine_table(p->n);
+  long N = orc_nmodes(p);
+  long n = p->n;
+  long rest = N / n;
+  ld* red = (ld*)malloc(sizeof(ld) * (size_t)rest);
+  for (long t = 0; t < nslices; ++t) {
+    const double* v = in + t * N;
+    for (int s = 0; s < ns; ++s) {
+      int j[3] = {0, 0, 0};
+      long r = idx[s];
+      for (int ax = 0; ax < p->dim; ++ax) { j[ax] = (int)(r % n); r /= n; }
+#pragma omp parallel for schedule(static)
+      for (long l = 0; l < rest; ++l) {
+        ld acc = 0.0L;
+        const ld* Sj = S + (long)j[0] * n;
+        for (long i = 0; i < n; ++i) acc += Sj[i] * v[l * n + i];
+        red[l] = acc;
+      }
+      long len = rest;
+      for (int ax = 1; ax < p->dim; ++ax) {
+        long nl = len / n;
+        const ld* Sj = S + (long)j[ax] * n;
+        for (long l = 0; l < nl; ++l) {
+          ld acc = 0.0L;
+          for (long i = 0; i < n; ++i) acc += Sj[i] * red[l * n + i];
+          red[l] = acc;
+        }
+        len = nl;
+      }
+      out[t * ns + s] = (double)red[0];
+    }
+  }
+  free(red);
+  free(S);
+}
+
 /* ------------------------------------------------------------------------------------ */
 /* operators on one slice                                                                */
 /* ------------------------------------------------------------------------------------ */

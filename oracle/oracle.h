@@ -46,6 +46,8 @@ void orc_mode_tables(const orc_problem* p, double* mu, double* E, double* dtphi1
 /* Orthonormal DST-I along every axis: out = V in, V = V^T = V^{-1}. */
 void orc_dst(const orc_problem* p, const double* in, double* out);
 /* Selected entries of V in: out[s] = (V in)[idx[s]]. */
+void orc_dst_sample_batch(const orc_problem* p, const double* in, long nslices, const long* idx, int ns,
+                          double* out);
 void orc_dst_sample(const orc_problem* p, const double* in, const long* idx, int ns, double* out);
 /* A v = V diag(E) V v with A = exp(dt L_h). */
 void orc_apply_A(const orc_problem* p, const double* v, double* out);

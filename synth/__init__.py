@@ -136,3 +136,25 @@ def random_spacetime(cfg: Config, seed: int | None = None, scale: float = 1.0) -
 def random_slice(cfg: Config, seed: int) -> np.ndarray:
     rng = np.random.default_rng(seed)
     return rng.standard_normal(cfg.shape)
+
+
+def sparse_spacetime(cfg: Config, nmodes: int = 8, seed: int = 77):
+    """A space-time vector [nt][n..n] that is a sum of nmodes fixed sine modes with seeded
+    N(0,1) coefficients per slice (full-size parity input whose DST coefficients are
+    nonzero only on those modes).  Returns (U, ks) with ks[m] = (k_x, k_y[, k_z])."""
+    rng = np.random.default_rng(seed)
+    kmax = min(64, cfg.n)
+    ks = rng.integers(1, kmax + 1, size=(nmodes, cfg.dim))
+    coef = rng.standard_normal((cfg.nt, nmodes))
+    S = sine_table(cfg.n, kmax)
+    phi = np.empty((nmodes,) + cfg.shape)
+    for m, k in enumerate(ks):
+        f = S[k[0] - 1]
+        if cfg.dim >= 2:
+            f = np.multiply.outer(S[k[1] - 1], f)
+        if cfg.dim == 3:
+            f = np.multiply.outer(S[k[2] - 1], f)
+        phi[m] = f
+    U = (coef @ phi.reshape(nmodes, -1)).reshape((cfg.nt,) + cfg.shape)
+    return U, ks
+

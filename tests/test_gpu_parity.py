@@ -95,6 +95,36 @@ def test_nonlin_hat_full_size_sampled(orc):
         assert np.abs(got[i][idx] - want).max() < 1e-12 * np.abs(got[i]).max()
 
 
+def test_sweep_full_size_sampled(orc):
+    # one fused sweep (K1: residual + preconditioner + update) at c5's full size and launch
+    # configuration (linear variant of c5: stage 3 is checked separately above), compared at
+    # sampled modes with the oracle's per-mode residual and Steps (a)-(c); the DST
+    # coefficients of input and output are taken by the oracle's plain sums
+    cfg = synth.Config("c5lin", 2, 2047, 0.1, 0.5, 1.0, 256, 1e-3, scheme=1, seed=5)
+    s = orc.spec(cfg)
+    u0 = synth.initial_condition(synth.CONFIGS["c5"])
+    U, ks = synth.sparse_spacetime(cfg, nmodes=6)
+    plan = Plan(Problem.from_config(cfg))
+    plan.load_state(T(u0), T(U))
+    plan.sweep()
+    rn2 = plan.sweep_norm2()
+    Ud = torch.empty((cfg.nt,) + cfg.shape, dtype=torch.float64, device=DEV)
+    plan.store_state(Ud)
+    U2 = H(Ud)
+    del Ud, plan
+    n = cfg.n
+    J = [int((k[1] - 1) * n + (k[0] - 1)) for k in ks[:3]] + [5 * n + 7]  # 3 active modes + 1 inactive
+    uh0 = orc.dst_sample(s, u0, J)
+    uh = orc.dst_sample_batch(s, U, J)     # [nt][modes]
+    uh2 = orc.dst_sample_batch(s, U2, J)
+    scale = np.abs(uh).max()
+    for m, j in enumerate(J):
+        r = orc.mode_residual(s, j, uh[:, m], uh0[m])
+        want = uh[:, m] + orc.mode_precond(s, j, r)
+        assert np.abs(uh2[:, m] - want).max() < 1e-11 * scale, j
+    assert np.isfinite(rn2) and rn2 > 0
+
+
 # ------------------------------------------------------------------------------------------
 # preconditioner apply (Steps (a)-(c)) and residual
 # ------------------------------------------------------------------------------------------

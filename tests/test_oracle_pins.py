@@ -517,3 +517,14 @@ def test_picard_small_alpha_recovers_sequential_stepping(orc, scheme):
         err = np.abs(U - seq).max(axis=1)
         assert err[:k].max() < 1e-7
         assert err[k] > 1e3 * err[:k].max()  # slice k+1 not yet exact
+
+
+def test_dst_sample_batch_equals_per_slice(orc):
+    cfg = synth.Config("t", 2, 15, 1.0, 1.0, 1.0, 4, 1e-2)
+    s = orc.spec(cfg)
+    V = np.random.default_rng(3).standard_normal((3,) + cfg.shape)
+    idx = [0, 17, 224, 100]
+    got = orc.dst_sample_batch(s, V, idx)
+    for t in range(3):
+        assert np.array_equal(got[t], orc.dst_sample(s, V[t], idx))
+        assert np.allclose(got[t], orc.dst(s, V[t]).reshape(-1)[idx], atol=1e-13)
