@@ -745,6 +745,9 @@ __global__ void __launch_bounds__(THR, (TmaLayout<NT, THR, NL, NST>::MINB))
         pout[(jb * RL + r) * S + ps] = vb[r];
       }
     }
+    // last generic-proxy writes into the stage (buf0 aliases its N-hat block): order them
+    // before the next TMA write into the stage (the later accesses are reads)
+    if constexpr (PL::ALIAS) fence_proxy_async_smem();
     __syncthreads();
     if constexpr (L == 3) {
       tstage<NT, S, THREADS, C::R1, RL, -1>(buf0, buf1, stw);
@@ -765,10 +768,7 @@ __global__ void __launch_bounds__(THR, (TmaLayout<NT, THR, NL, NST>::MINB))
         st2(a.Y + (long)t * npad + base, sv);
       }
     }
-    // the stage (and buf0 inside it) is free for the next TMA load: order this thread's
-    // generic-proxy shared-memory accesses before the async-proxy writes, then barrier
-    fence_proxy_async_smem();
-    __syncthreads();
+    __syncthreads();  // every read of the stage is done: it may be refilled by TMA
     if constexpr (NST == 1) {
       if (next < ntiles) tma_tile_issue<NT, THR, RM, NL, NST>(&mx, &mn, a, next, smem, &bar[0]);
     }
