@@ -47,7 +47,10 @@ typedef enum {
 
 typedef enum {
   EXPD_EXP_EULER = 0, /* linear (npoly = 0) or ETD1: u_n = E u_{n-1} + dt phi1 N(u_{n-1}) (R5) */
-  EXPD_ETD2 = 1       /* u_n = E u_{n-1} + dt[(phi1+phi2) N_{n-1} - phi2 N_{n-2}] (R6)        */
+  EXPD_ETD2 = 1,      /* u_n = E u_{n-1} + dt[(phi1+phi2) N_{n-1} - phi2 N_{n-2}] (R6)        */
+  EXPD_IF_IMEX = 2    /* the paper's own: IF scheme (6.1) u_n = E u_{n-1} + dt N(u_n)
+                         (PAPER.md:815), solved by the IMEX-type iteration (7.2)/(7.3)
+                         (PAPER.md:1209-1220): N of the same slice, lagged one sweep    */
 } expd_scheme;
 
 typedef struct {

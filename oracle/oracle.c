@@ -290,6 +290,28 @@ static ld nonlin_ld(const orc_problem* p, ld u) {
   return acc;
 }
 
+/* N'(u) = sum_p p q_p u^{p-1} (the Newton step of the IF scheme's implicit solve). */
+static ld dnonlin_ld(const orc_problem* p, ld u) {
+  ld acc = 0.0L;
+  for (int k = p->npoly - 1; k >= 1; --k) acc = acc * u + (ld)k * (ld)p->q[k];
+  return acc;
+}
+
+/* IF scheme (6.1): the implicit part of one step, pointwise: the v with
+   v - dt N(v) = w, by Newton's method from v = w (scalar, long double; for N = -u^3 the map
+   v - dt N(v) is strictly increasing, so the root is unique). */
+static ld if_solve_ld(const orc_problem* p, ld w) {
+  ld v = w;
+  for (int it = 0; it < 100; ++it) {
+    ld f = v - (ld)p->dt * nonlin_ld(p, v) - w;
+    ld df = 1.0L - (ld)p->dt * dnonlin_ld(p, v);
+    ld dv = f / df;
+    v -= dv;
+    if (fabsl(dv) <= 1e-19L * (1.0L + fabsl(v))) break;
+  }
+  return v;
+}
+
 void orc_apply_A(const orc_problem* p, const double* v, double* out) {
   ctx_t c;
   ctx_init(&c, p);
@@ -348,7 +370,10 @@ void orc_sequential(const orc_problem* p, const double* u0, double* U) {
   for (long i = 0; i < N; ++i) nm2[i] = nonlin_ld(p, prev[i]);
   for (int n = 1; n <= p->nt; ++n) {
     apply_mult_ld(&c, c.E, prev, cur);
-    if (nonlin) {
+    if (nonlin && p->scheme == 2) {
+      /* IF (6.1): u_n = A u_{n-1} + dt N(u_n), implicit pointwise */
+      for (long i = 0; i < N; ++i) cur[i] = if_solve_ld(p, cur[i]);
+    } else if (nonlin) {
       for (long i = 0; i < N; ++i) nm1[i] = nonlin_ld(p, prev[i]);
       add_phi_terms_ld(&c, nm1, nm2, cur);
       memcpy(nm2, nm1, sizeof(ld) * (size_t)N);
@@ -371,7 +396,11 @@ static void residual_ld(const ctx_t* c, const ld* u0, const ld* U, ld* R) {
     const ld* prev = (n == 1) ? u0 : U + (size_t)(n - 2) * N;
     ld* r = R + (size_t)(n - 1) * N;
     apply_mult_ld(c, c->E, prev, r);
-    if (nonlin) {
+    if (nonlin && p->scheme == 2) {
+      /* IF / IMEX-type: + dt N(u_n) of the same slice */
+      const ld* un = U + (size_t)(n - 1) * N;
+      for (long i = 0; i < N; ++i) r[i] += (ld)p->dt * nonlin_ld(p, un[i]);
+    } else if (nonlin) {
       const ld* prev2 = (n <= 2) ? u0 : U + (size_t)(n - 3) * N; /* u_{n-2}; u_{-1} -> u_0 (R6) */
       ld* nm1 = (ld*)malloc(sizeof(ld) * (size_t)N);
       ld* nm2 = (ld*)malloc(sizeof(ld) * (size_t)N);
@@ -689,7 +718,9 @@ void orc_mode_residual(const orc_problem* p, long J, const double* uhat, double 
   for (int n = 1; n <= p->nt; ++n) {
     ld prev = (n == 1) ? (ld)uhat0 : (ld)uhat[n - 2];
     ld r = E * prev - (ld)uhat[n - 1];
-    if (nonlin) {
+    if (nonlin && p->scheme == 2) {
+      r += (ld)p->dt * (ld)nhat[n - 1];  /* nhat[n-1] = N-hat of u_n (same slice) */
+    } else if (nonlin) {
       ld nm1 = nhat[n - 1];                    /* N_{n-1}                       */
       ld nm2 = (n >= 2) ? nhat[n - 2] : nhat[0]; /* N_{n-2}, N_{-1} := N_0 (R6)   */
       if (p->scheme == 0) r += f1 * nm1;

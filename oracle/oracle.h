@@ -30,7 +30,8 @@ typedef struct {
   double dt;       /* Delta t                                       */
   int nt;          /* N_t                                                          */
   double alpha;    /* alpha-circulant parameter                  */
-  int scheme;      /* 0: exponential Euler / ETD1, 1: ETD2 (readings R5, R6)       */
+  int scheme;      /* 0: exponential Euler / ETD1, 1: ETD2 (readings R5, R6),      *
+                    * 2: IF scheme (6.1) / IMEX-type iteration (7.2) */
   int npoly;       /* N(u) = sum_{p<npoly} q[p] u^p ; 0 = linear                   */
   double q[8];
 } orc_problem;
@@ -88,7 +89,7 @@ int orc_gmres(const orc_problem* p, const double* u0, double* U, double tol, int
 /* Per-spectral-mode versions (sampled full-size parity; reading R4: in the DST basis
    Step (b) is the divide by 1 - lambda_k E_J).
    uhat: [nt] (u_1..u_Nt of mode J), uhat0 = u_0 of mode J,
-   nhat: [nt] (N_0..N_{Nt-1} of mode J, may be NULL when linear). */
+   nhat: [nt] (N_0..N_{Nt-1} of mode J, may be NULL when linear; scheme 2: N of u_1..u_Nt). */
 void orc_mode_residual(const orc_problem* p, long J, const double* uhat, double uhat0, const double* nhat,
                        double* rhat);
 void orc_mode_precond(const orc_problem* p, long J, const double* rhat, double* shat);

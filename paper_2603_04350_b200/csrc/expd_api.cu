@@ -25,7 +25,8 @@ struct expd_plan {
   cudaStream_t stream = nullptr;
   Geom g{};
   int sms = 148;
-  int nl = 0;  // 0 linear, 1 ETD1, 2 ETD2
+  int nl = 0;      // 0 linear, 1 ETD1 / IF-IMEX, 2 ETD2
+  int nshift = 0;  // IF / IMEX-type: K1 reads N-hat of the same slice (one slice later)
   double a1 = 0.0;
   // small device tables owned by the plan
   double* d_lam = nullptr;   // [n]
@@ -131,7 +132,8 @@ extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dis
   const expd_problem& P = *prob;
   if (P.dim < 1 || P.dim > 3 || P.n < 3 || !is_pow2((long)P.n + 1) || P.n + 1 > 4096 || !(P.a > 0.0) ||
       !(P.c >= 0.0) || !(P.dt > 0.0) || P.nt < 4 || !is_pow2(P.nt) || !(P.alpha > 0.0) || !(P.alpha <= 1.0) ||
-      P.npoly < 0 || P.npoly > 8 || (P.scheme != EXPD_EXP_EULER && P.scheme != EXPD_ETD2) ||
+      P.npoly < 0 || P.npoly > 8 ||
+      (P.scheme != EXPD_EXP_EULER && P.scheme != EXPD_ETD2 && P.scheme != EXPD_IF_IMEX) ||
       !std::isfinite(P.a) || !std::isfinite(P.c) || !std::isfinite(P.dt))
     return EXPD_ERR_INVALID_ARG;
   if (P.nt > 256) return EXPD_ERR_UNSUPPORTED;
@@ -162,7 +164,9 @@ extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dis
   for (int i = 1; i < P.dim; ++i) npad *= P.n;
   p->g.N = N;
   p->g.npad = npad;
+  // K1 form: 0 linear, 1 one N-hat term (ETD1; IF/IMEX with N of the same slice), 2 ETD2
   p->nl = P.npoly > 0 ? (P.scheme == EXPD_ETD2 ? 2 : 1) : 0;
+  p->nshift = (P.npoly > 0 && P.scheme == EXPD_IF_IMEX) ? 1 : 0;
   if (cudaSetDevice(device) != cudaSuccess) {
     delete p;
     return EXPD_ERR_CUDA;
@@ -202,7 +206,8 @@ static Layout layout(const expd_plan* p, int kv) {
   // space-time vectors in the mode slab: [nt][mlen]; N-hat gets one extra slice when
   // distributed (stage 3 of the last time slab lands there, unused)
   const size_t vec = align_up(sizeof(double) * (size_t)p->prob.nt * (size_t)p->mlen);
-  const size_t nhv = align_up(sizeof(double) * (size_t)(p->prob.nt + (p->dist ? 1 : 0)) * (size_t)p->mlen);
+  const size_t nhv = align_up(sizeof(double) * (size_t)(p->prob.nt + ((p->dist || p->nshift) ? 1 : 0)) *
+                              (size_t)p->mlen);
   const size_t tsl = p->dist ? align_up(sizeof(double) * (size_t)p->ntl * (size_t)p->g.npad) : 0;
   const size_t sl = align_up(sizeof(double) * (size_t)p->g.npad);
   size_t off = 0;
@@ -298,7 +303,7 @@ static TimeArgs time_args(const expd_plan* p, const double* X, double* Y, bool w
   a.X = X;
   a.Y = Y;
   a.u0h = p->u0h + p->moff;
-  a.Nh = p->Nh;
+  a.Nh = p->Nh ? p->Nh + p->nshift * p->mlen : nullptr;  // IF / IMEX: N-hat of u_{t+1} for slice t
   a.E = p->E + p->moff;
   a.C1 = p->C1 + p->moff;
   a.C2 = p->C2 + p->moff;
@@ -380,8 +385,8 @@ static cudaError_t enqueue_sweep(expd_plan* p, cudaStream_t st) {
   cudaError_t e = record(p, 0, st);
   if (e != cudaSuccess) return e;
   if (p->nl) {
-    e = nonlin_slices(p->g, dst_tables(p), p->Uh, p->Nh + p->g.npad, p->prob.nt - 1, p->prob.npoly, p->prob.q,
-                      p->scratch, st);
+    e = nonlin_slices(p->g, dst_tables(p), p->Uh, p->Nh + p->g.npad, p->prob.nt - 1 + p->nshift, p->prob.npoly,
+                      p->prob.q, p->scratch, st);
     if (e != cudaSuccess) return e;
   }
   if ((e = record(p, 1, st)) != cudaSuccess) return e;
@@ -463,8 +468,8 @@ extern "C" expd_status expd_residual(expd_plan* p, const double* u0, const doubl
   if (s) return s;
   if ((s = phys_to_mode(p, U, p->Uh))) return s;
   if (p->nl && !p->dist && nt > 1)  // N-hat_m = V N(u_m), m = 1..nt-1, from the physical slices
-    CUDA_TRY(p, nonlin_phys_slices(p->g, dst_tables(p), U, p->Nh + p->g.npad, nt - 1, p->prob.npoly, p->prob.q,
-                                   p->scratch, p->stream));
+    CUDA_TRY(p, nonlin_phys_slices(p->g, dst_tables(p), U, p->Nh + p->g.npad, nt - 1 + p->nshift, p->prob.npoly,
+                                   p->prob.q, p->scratch, p->stream));
   if (p->nl && p->dist) {  // local physical slices -> N-hat time slab -> mode slab (shifted)
     CUDA_TRY(p, nonlin_phys_slices(p->g, dst_tables(p), U, p->NT, p->ntl, p->prob.npoly, p->prob.q, p->scratch,
                                    p->stream));
@@ -618,7 +623,7 @@ extern "C" expd_status expd_debug_kernel_ms(expd_plan* p, int which, long nslice
 extern "C" int expd_sweep_kernel_launches(const expd_plan* p) {
   if (!p) return 0;
   int k = 2;  // fused time pass + norm reduction
-  if (p->nl) k += nonlin_kernel_launches(p->g, p->prob.nt - 1);
+  if (p->nl) k += nonlin_kernel_launches(p->g, p->prob.nt - 1 + p->nshift);
   return k;
 }
 

@@ -52,6 +52,8 @@ __global__ void k_mode_tables(int dim, int n, int M, long npad, const double* la
       phi12(z, &p1, &p2);
       if (scheme == 0) {
         c1 = dt * p1;
+      } else if (scheme == 2) {  // IF / IMEX-type: dt N(u_n), no phi
+        c1 = dt;
       } else {
         c1 = dt * (p1 + p2);
         c2 = dt * p2;

@@ -68,6 +68,11 @@ CONFIGS = {
     "c4": Config("c4", 3, 255, 1.0, 1.0, 1.0, 64, 1e-4, solvers=("gmres", "fixed_point"), tol=1e-10, seed=4),
     # BASELINE.json:11 -- 2D u_t = 0.1 Lap u - 0.5 u - u^3, ETD2 Picard
     "c5": Config("c5", 2, 2047, 0.1, 0.5, 1.0, 256, 1e-3, scheme=1, q=CUBIC, seed=5),
+    # NEXT-1: the paper's own nonlinear iteration -- IF scheme (6.1) solved by
+    # the IMEX-type Exp-ParaDiag iteration (7.2)/(7.3) -- on the
+    # c3 and c5 problems (not BASELINE.json configs)
+    "c3if": Config("c3if", 2, 511, 1.0, 1.0, 0.5, 128, 1e-3, scheme=2, q=CUBIC, seed=3),
+    "c5if": Config("c5if", 2, 2047, 0.1, 0.5, 1.0, 256, 1e-3, scheme=2, q=CUBIC, seed=5),
 }
 
 

@@ -221,7 +221,10 @@ def _dist_picard_worker(rank, P, port, name, n, nt, out_dir):
             rn2 = 0.0
             for e in modes:  # K1 on the mode slab: residual, ||r||^2, preconditioner, update
                 c = e - off
-                r = oracle.mode_residual(s, J[e], Uh[:, c], u0h[e], Nh[: cfg.nt, c] if nl else None)
+                nh = None
+                if nl:  # ETD: N-hat_0..N-hat_{nt-1}; IF / IMEX (scheme 2): N-hat of u_1..u_nt
+                    nh = Nh[1: cfg.nt + 1, c] if cfg.scheme == 2 else Nh[: cfg.nt, c]
+                r = oracle.mode_residual(s, J[e], Uh[:, c], u0h[e], nh)
                 rn2 += float(np.dot(r, r))
                 Uh[:, c] += oracle.mode_precond(s, J[e], r)
             t = torch.tensor([rn2], dtype=torch.float64)
@@ -240,7 +243,8 @@ def _dist_picard_worker(rank, P, port, name, n, nt, out_dir):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("P,name,n,nt", [(2, "c3", 15, 8), (2, "c5", 15, 8), (2, "c2", 15, 8), (4, "c5", 7, 8)])
+@pytest.mark.parametrize("P,name,n,nt", [(2, "c3", 15, 8), (2, "c5", 15, 8), (2, "c2", 15, 8), (4, "c5", 7, 8),
+                                         (2, "c5if", 15, 8)])
 def test_distributed_sweep_matches_oracle(tmp_path, P, name, n, nt):
     import oracle
 

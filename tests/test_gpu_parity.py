@@ -153,7 +153,7 @@ def test_precond_apply_parity(orc, name, n, nt):
 
 
 @pytest.mark.parametrize("name,n,nt", [("c1", None, None), ("c2", 31, 64), ("c3", 31, 128), ("c4", 7, 64),
-                                       ("c5", 31, 256), ("c5", 7, 4)])
+                                       ("c5", 31, 256), ("c5", 7, 4), ("c5if", 31, 256), ("c3if", 255, 8)])
 def test_residual_parity(orc, name, n, nt):
     cfg = synth.CONFIGS[name] if n is None else cfg_small(name, n, nt)
     plan = Plan(Problem.from_config(cfg))
@@ -181,7 +181,9 @@ def test_precond_zero_and_alias(orc):
 # solvers
 # ------------------------------------------------------------------------------------------
 SOLVE_CASES = [("c1", None, None), ("c2", 63, 64), ("c3", 63, 128), ("c5", 63, 256), ("c4", 15, 64),
-               ("c3", 255, 16), ("c5", 255, 16)]
+               ("c3", 255, 16), ("c5", 255, 16),
+               # NEXT-1: IF scheme (6.1) by the IMEX-type iteration (7.2)
+               ("c3if", 63, 128), ("c5if", 63, 256), ("c5if", 255, 16)]
 
 
 @pytest.mark.parametrize("name,n,nt", SOLVE_CASES)
@@ -248,7 +250,7 @@ def comm1():
 
 
 @pytest.mark.parametrize("name,n,nt", [("c1", None, None), ("c3", 63, 128), ("c5", 63, 256), ("c2", 63, 64),
-                                       ("c5", 255, 16)])
+                                       ("c5", 255, 16), ("c3if", 63, 128), ("c5if", 255, 16)])
 def test_dist1_fixed_point_parity(orc, comm1, name, n, nt):
     cfg = synth.CONFIGS[name] if n is None else cfg_small(name, n, nt)
     plan = Plan(Problem.from_config(cfg), comm=comm1)

@@ -67,13 +67,28 @@ def dense_residual(s, u0, U):
         prev = u0 if n == 1 else U[n - 2]
         prev2 = u0 if n <= 2 else U[n - 3]
         r = A @ prev - U[n - 1]
-        if s.q:
+        if s.q and s.scheme == 2:  # IF / IMEX-type: dt N(u_n) of the same slice
+            r += s.dt * Nfun(s, U[n - 1])
+        elif s.q:
             if s.scheme == 0:
                 r += P1 @ Nfun(s, prev)
             else:
                 r += (P1 + P2) @ Nfun(s, prev) - P2 @ Nfun(s, prev2)
         R[n - 1] = r
     return R
+
+
+def if_implicit_bisect(s, w):
+    """The v with v - dt N(v) = w, pointwise, by bisection (test-side, independent of the
+    oracle's Newton): for N = -u^3 (or -M u) the map is strictly increasing."""
+    lo = w - 1.0 - np.abs(w)
+    hi = w + 1.0 + np.abs(w)
+    for _ in range(200):
+        mid = 0.5 * (lo + hi)
+        f = mid - s.dt * Nfun(s, mid) - w
+        hi = np.where(f > 0, mid, hi)
+        lo = np.where(f > 0, lo, mid)
+    return 0.5 * (lo + hi)
 
 
 def dense_sequential(s, u0):
@@ -83,7 +98,9 @@ def dense_sequential(s, u0):
     out = []
     for _ in range(s.nt):
         cur = A @ prev
-        if s.q:
+        if s.q and s.scheme == 2:
+            cur = if_implicit_bisect(s, cur)
+        elif s.q:
             if s.scheme == 0:
                 cur += P1 @ Nfun(s, prev)
             else:
@@ -528,3 +545,83 @@ def test_dst_sample_batch_equals_per_slice(orc):
     for t in range(3):
         assert np.array_equal(got[t], orc.dst_sample(s, V[t], idx))
         assert np.allclose(got[t], orc.dst(s, V[t]).reshape(-1)[idx], atol=1e-13)
+
+
+# ------------------------------------------------------------------------------------------
+# NEXT-1: the IF scheme (6.1) and the IMEX-type Exp-ParaDiag iteration (7.2)/(7.3)
+# (PAPER.md:812-816, :1209-1220), scheme 2
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("dim,n", [(1, 9), (2, 4)])
+def test_if_sequential_vs_dense(orc, dim, n):
+    """u_n = A u_{n-1} + dt N(u_n): dense expm + test-side bisection vs the oracle (DSTs +
+    Newton)."""
+    s = spec(orc, dim, n, a=0.3, c=0.5, T=0.5, nt=6, scheme=2, q=synth.CUBIC)
+    u0 = np.random.default_rng(2).uniform(-1, 1, (n,) * dim)
+    assert rel(orc.sequential(s, u0).reshape(s.nt, -1), dense_sequential(s, u0)) < 1e-12
+
+
+def test_if_linear_nonlinearity_closed_form(orc):
+    """N(u) = -M u: (1 + dt M) u_n = A u_{n-1}, so a sine mode decays by E/(1 + dt M) per
+    step (mu from the dense stencil)."""
+    n, k, M = 11, 3, 2.0
+    s = spec(orc, 1, n, a=0.7, c=0.2, T=1.0, nt=10, scheme=2, q=(0.0, -M))
+    u0 = synth.sine_table(n, k)[k - 1]
+    mu = np.sort(np.linalg.eigvalsh(Lh(s)))[::-1][k - 1]
+    g = np.exp(s.dt * mu) / (1.0 + s.dt * M)
+    U = orc.sequential(s, u0)
+    for m in range(1, s.nt + 1):
+        assert np.abs(U[m - 1] - g**m * u0).max() < 1e-13
+
+
+def test_if_convergence_order(orc):
+    """Scalar u' = (mu - M) u with L = mu, N = -M u treated by the IF scheme: first order."""
+    M, T = 3.0, 1.0
+    errs = []
+    for nt in (16, 32, 64):
+        s = spec(orc, 1, 1, a=0.0, c=0.5, T=T, nt=nt, scheme=2, q=(0.0, -M))
+        U = orc.sequential(s, np.array([1.0]))
+        errs.append(abs(U[-1, 0] - np.exp((-0.5 - M) * T)))
+    r1, r2 = errs[0] / errs[1], errs[1] / errs[2]
+    assert abs(np.log2(r1) - 1) < 0.15 and abs(np.log2(r2) - 1) < 0.1
+
+
+@pytest.mark.parametrize("dim,n", [(1, 7), (2, 4)])
+def test_if_residual_vs_dense(orc, dim, n):
+    s = spec(orc, dim, n, a=0.5, c=1.0, T=0.4, nt=5, scheme=2, q=synth.CUBIC)
+    rng = np.random.default_rng(3)
+    u0 = rng.uniform(-1, 1, (n,) * dim)
+    U = rng.standard_normal((s.nt,) + (n,) * dim)
+    R, _ = orc.residual(s, u0, U)
+    assert rel(R.reshape(s.nt, -1), dense_residual(s, u0, U)) < 1e-12
+
+
+def test_imex_iteration_converges_to_if_scheme(orc):
+    """The IMEX-type iteration (7.2) (Picard on the all-at-once system (7.3)) converges to
+    the IF solution (6.1): its fixed point."""
+    cfg = synth.CONFIGS["c3"].scaled(15, 16)
+    s = spec(orc, cfg.dim, cfg.n, cfg.a, cfg.c, cfg.T, cfg.nt, cfg.alpha, 2, cfg.q)
+    u0 = synth.initial_condition(cfg)
+    U, st, its, hist = orc.fixed_point(s, u0, tol=1e-12)
+    assert st == 0 and its >= 2
+    assert rel(U, orc.sequential(s, u0)) < 1e-11
+
+
+def test_imex_iteration_linear_rate(orc):
+    """N = -M u: the iteration is linear, U^{k+1} = U^k + Q_alpha^{-1}(F(U^k) - Q U^k) with
+    F = f - dt M U; on a single sine mode its error contracts by the spectral radius of
+    I - Q_alpha^{-1}(Q + dt M) restricted to that mode (dense nt x nt matrices)."""
+    n, k, M, nt = 7, 2, 4.0, 8
+    s = spec(orc, 1, n, a=0.5, c=0.3, T=1.0, nt=nt, alpha=0.05, scheme=2, q=(0.0, -M))
+    u0 = synth.sine_table(n, k)[k - 1]
+    mu = np.sort(np.linalg.eigvalsh(Lh(s)))[::-1][k - 1]
+    E = np.exp(s.dt * mu)
+    C0 = np.diag(np.ones(nt - 1), -1)
+    Q = np.eye(nt) - E * C0
+    Qa = np.eye(nt) - E * alpha_circulant(nt, s.alpha)
+    G = np.eye(nt) - np.linalg.solve(Qa, Q + s.dt * M * np.eye(nt))
+    rho = np.abs(np.linalg.eigvals(G)).max()
+    U, st, its, hist = orc.fixed_point(s, u0, tol=1e-13, maxit=60)
+    ratios = hist[3:its] / hist[2:its - 1]
+    assert st == 0 and len(ratios) >= 2
+    assert abs(ratios[-1] / rho - 1.0) < 0.05
+
