@@ -129,6 +129,38 @@ __device__ __forceinline__ void tstage(const double2* __restrict__ in, double2* 
   }
 }
 
+// v[r] *= w1^r (DIR > 0) or conj(w1)^r (DIR < 0), r = 1..R-1, powers by products from
+// one base twiddle held in a register (binary splitting, <= 2 log2 R roundings deep): the
+// twiddles cost fp64 products instead of shared-memory table loads.
+template <int R, int DIR>
+__device__ __forceinline__ void twpow_mul(double2* v, double2 w1) {
+  if constexpr (R > 1) {
+    double2 t[R];
+    t[1] = w1;
+#pragma unroll
+    for (int r = 2; r < R; ++r) t[r] = (r % 2 == 0) ? cmul(t[r / 2], t[r / 2]) : cmul(t[r - 1], t[1]);
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[r] = DIR > 0 ? cmul(v[r], t[r]) : cmulc(v[r], t[r]);
+  }
+}
+
+// tstage with the job's base twiddle w^{k NT/(NS R)} in a register (one job per thread).
+template <int NT, int S, int THREADS, int R, int NS, int DIR>
+__device__ __forceinline__ void tstage_pw(const double2* __restrict__ in, double2* __restrict__ out, double2 w1) {
+  constexpr int JOBS = S * (NT / R);
+  static_assert(JOBS == THREADS, "one job per thread");
+  const int J = threadIdx.x;
+  const int s = J % S, j = J / S, k = j % NS;
+  double2 v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) v[r] = in[(j + r * (NT / R)) * S + s];
+  twpow_mul<R, DIR>(v, w1);
+  DFT<R, DIR>::run(v);
+  const int base = (j / NS) * NS * R + k;
+#pragma unroll
+  for (int r = 0; r < R; ++r) out[(base + r * NS) * S + s] = v[r];
+}
+
 // Last forward stage (radix RL, NS = NT/RL) of two partner jobs ja, jb (their frequency sets
 // k = j + NS r are Hermitian partners), the pair divide, and the first inverse stage
 // (radix RL, NS = 1: no twiddles) on the same sets.
@@ -645,6 +677,18 @@ __global__ void __launch_bounds__(THR, (TmaLayout<NT, THR, NL, NST>::MINB))
   const int s = tid % S;
   const int j = tid / S;
   const long npad = a.npad;
+  // loop-invariant base twiddles of this thread's jobs (each stage has one job per thread
+  // in the L = 3 plans used at NT >= 64; other plans keep the table loads)
+  constexpr bool PW = (L == 3) && (S * (NT / C::R1) == THREADS) && (S * (NSL / 2) == THREADS);
+  double2 w_fm = make_double2(1.0, 0.0), w_im = w_fm, w_pa = w_fm, w_pb = w_fm, w_c = w_fm;
+  if constexpr (PW) {
+    w_fm = stw[((j % R0) * (NT / (R0 * C::R1))) & (NT - 1)];   // forward middle stage, NS = R0
+    w_im = stw[((j % RL) * (NT / (RL * C::R1))) & (NT - 1)];   // inverse middle stage, NS = RL
+    const int pj = tid / S;
+    w_pa = stw[pj & (NT - 1)];
+    w_pb = stw[(pj == 0 ? NSL / 2 : NSL - pj) & (NT - 1)];
+    w_c = stw[j & (NT - 1)];                                     // phase C (inverse stage 0)
+  }
 
   long tile = blockIdx.x;
   if (tile < ntiles) tma_tile_issue<NT, THR, RM, NL, NST>(&mx, &mn, a, tile, smem, &bar[0]);
@@ -675,6 +719,7 @@ __global__ void __launch_bounds__(THR, (TmaLayout<NT, THR, NL, NST>::MINB))
 
     // ---- phase A: residual (+ ||r||^2), Gamma_alpha, forward stage 0 (times j + r TPS) ---
     double2 y[R0];
+    double2 xv[OUTM == OUT_UPDATE ? R0 : 1];  // u_t kept in registers for the update
     const double2 Ej = aux[s];
     const double2 c1 = NL >= 1 ? aux[S + s] : make_double2(0.0, 0.0);
     const double2 c2 = NL == 2 ? aux[2 * S + s] : make_double2(0.0, 0.0);
@@ -682,6 +727,7 @@ __global__ void __launch_bounds__(THR, (TmaLayout<NT, THR, NL, NST>::MINB))
     for (int r = 0; r < R0; ++r) {
       const int t = j + r * TPS;
       const double2 xc = X[t * S + s];
+      if constexpr (OUTM == OUT_UPDATE) xv[r] = xc;
       double2 rr;
       if constexpr (RM == RM_INPUT) {
         rr = xc;
@@ -714,7 +760,8 @@ __global__ void __launch_bounds__(THR, (TmaLayout<NT, THR, NL, NST>::MINB))
     const double2* pin = buf0;
     double2* pout = buf1;
     if constexpr (L == 3) {
-      tstage<NT, S, THREADS, C::R1, R0, +1>(buf0, buf1, stw);
+      if constexpr (PW) tstage_pw<NT, S, THREADS, C::R1, R0, +1>(buf0, buf1, w_fm);
+      else tstage<NT, S, THREADS, C::R1, R0, +1>(buf0, buf1, stw);
       __syncthreads();
       pin = buf1;
       pout = buf0;
@@ -728,10 +775,15 @@ __global__ void __launch_bounds__(THR, (TmaLayout<NT, THR, NL, NST>::MINB))
         va[r] = pin[(ja + r * NSL) * S + ps];
         vb[r] = pin[(jb + r * NSL) * S + ps];
       }
+      if constexpr (PW) {
+        twpow_mul<RL, +1>(va, w_pa);
+        twpow_mul<RL, +1>(vb, w_pb);
+      } else {
 #pragma unroll
-      for (int r = 1; r < RL; ++r) {
-        va[r] = cmul(va[r], stw[(r * ja) & (NT - 1)]);
-        vb[r] = cmul(vb[r], stw[(r * jb) & (NT - 1)]);
+        for (int r = 1; r < RL; ++r) {
+          va[r] = cmul(va[r], stw[(r * ja) & (NT - 1)]);
+          vb[r] = cmul(vb[r], stw[(r * jb) & (NT - 1)]);
+        }
       }
       DFT<RL, +1>::run(va);
       DFT<RL, +1>::run(vb);
@@ -750,13 +802,18 @@ __global__ void __launch_bounds__(THR, (TmaLayout<NT, THR, NL, NST>::MINB))
     if constexpr (PL::ALIAS) fence_proxy_async_smem();
     __syncthreads();
     if constexpr (L == 3) {
-      tstage<NT, S, THREADS, C::R1, RL, -1>(buf0, buf1, stw);
+      if constexpr (PW) tstage_pw<NT, S, THREADS, C::R1, RL, -1>(buf0, buf1, w_im);
+      else tstage<NT, S, THREADS, C::R1, RL, -1>(buf0, buf1, stw);
       __syncthreads();
     }
 #pragma unroll
     for (int r = 0; r < R0; ++r) y[r] = buf1[(j + r * TPS) * S + s];
+    if constexpr (PW) {
+      twpow_mul<R0, -1>(y, w_c);
+    } else {
 #pragma unroll
-    for (int r = 1; r < R0; ++r) y[r] = cmulc(y[r], stw[(r * j) & (NT - 1)]);
+      for (int r = 1; r < R0; ++r) y[r] = cmulc(y[r], stw[(r * j) & (NT - 1)]);
+    }
     DFT<R0, -1>::run(y);
     // ---- phase C: Gamma_alpha^{-1}, update (u_t from the staged tile), store ------------
     if (valid) {
@@ -764,7 +821,7 @@ __global__ void __launch_bounds__(THR, (TmaLayout<NT, THR, NL, NST>::MINB))
       for (int r = 0; r < R0; ++r) {
         const int t = j + r * TPS;
         double2 sv = cscale(y[r], sgi[t]);
-        if constexpr (OUTM == OUT_UPDATE) sv = cadd(X[t * S + s], sv);
+        if constexpr (OUTM == OUT_UPDATE) sv = cadd(xv[r], sv);
         st2(a.Y + (long)t * npad + base, sv);
       }
     }
