@@ -42,7 +42,7 @@ template <> struct TimeCfg<4>   { static constexpr int L = 1, R0 = 4, R1 = 1, R2
 template <> struct TimeCfg<8>   { static constexpr int L = 1, R0 = 8, R1 = 1, R2 = 1; };
 template <> struct TimeCfg<16>  { static constexpr int L = 2, R0 = 4, R1 = 4, R2 = 1; };
 template <> struct TimeCfg<32>  { static constexpr int L = 2, R0 = 8, R1 = 4, R2 = 1; };
-template <> struct TimeCfg<64>  { static constexpr int L = 3, R0 = 8, R1 = 2, R2 = 4; };
+template <> struct TimeCfg<64>  { static constexpr int L = 2, R0 = 8, R1 = 8, R2 = 1; };
 template <> struct TimeCfg<128> { static constexpr int L = 3, R0 = 8, R1 = 4, R2 = 4; };
 template <> struct TimeCfg<256> { static constexpr int L = 3, R0 = 8, R1 = 8, R2 = 4; };
 template <int NT>
