@@ -139,19 +139,24 @@ class ClockSampler:
 # ------------------------------------------------------------------------------------------
 # CPU oracle baseline (oracle/ as it stands; rank 0, N = 1 only)
 # ------------------------------------------------------------------------------------------
-def oracle_sample_step(cfg, u_slice):
-    """One bounded sample of the oracle's sweep: A u on one full-size slice (2 naive DSTs,
-    O(n) sums per output, long double).  The oracle's sweep is 10 such DST applications per
+REF_ROWS = 256  # rows per CPU-baseline sample
+
+
+def oracle_sample_step(cfg, u_rows):
+    """One bounded sample of the oracle's sweep: the x-axis DST-I (plain O(n) long-double
+    sums per output) of REF_ROWS rows of a c5 slice.  The oracle's sweep applies 10 DSTs per
     time slice (residual: A and the two Phi products = 6; Step (b): DST and IDST of the real
-    and imaginary parts = 4) plus O(Nt) DFT sums per point (< 3 % of its work at c5), so one
-    sample is 1/(5 Nt) of a sweep: N_st / (5 Nt) equivalent DOF-iterations."""
+    and imaginary parts = 4), each dim axis passes over the slice's n^{dim-1} rows, plus
+    O(Nt) DFT sums per point (< 3 % of its work at c5): one sample is
+    REF_ROWS / (10 dim n^{dim-1} Nt) of a sweep, i.e. that fraction of N_st DOF-iterations."""
     import oracle
 
-    oracle.apply_A(oracle.spec(cfg), u_slice)
-    return cfg.nst / (5.0 * cfg.nt)
+    oracle.dst_x_rows(oracle.spec(cfg), u_rows)
+    rows_per_slice = cfg.n ** (cfg.dim - 1)
+    return cfg.nst * u_rows.shape[0] / (10.0 * cfg.dim * rows_per_slice * cfg.nt)
 
 
-def cpu_baseline(cfg, nsamples=1):
+def cpu_baseline(cfg, nsamples=4):
     import numpy as np
 
     import oracle
@@ -159,7 +164,8 @@ def cpu_baseline(cfg, nsamples=1):
     oracle.build()
     cores = os.cpu_count() or 1
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
-    u = np.random.default_rng(0).standard_normal(cfg.shape)
+    u = np.random.default_rng(0).standard_normal((REF_ROWS, cfg.n))
+    oracle_sample_step(cfg, u)  # warm-up (library load, OpenMP pool)
     t0 = time.perf_counter()
     dofs = 0.0
     for _ in range(nsamples):
@@ -167,8 +173,8 @@ def cpu_baseline(cfg, nsamples=1):
     dt = time.perf_counter() - t0
     return {"value": dofs / dt, "unit": "DOF-iter/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
             "kind": "oracle",
-            "sample": f"{nsamples} x oracle A u on one {cfg.name} slice ({cfg.n}^{cfg.dim}, 2 naive long-double "
-                      f"DSTs) = 1/(5 Nt) of an oracle sweep each; {dt:.1f} s"}
+            "sample": f"{nsamples} x oracle x-axis DST-I of {REF_ROWS} rows of a {cfg.name} slice (plain long-double "
+                      f"sums) = {REF_ROWS}/(10 dim n^(dim-1) Nt) of an oracle sweep each; {dt:.1f} s"}
 
 
 def run_reference(args):
@@ -185,7 +191,7 @@ def run_reference(args):
     oracle.build()
     cores = os.cpu_count() or 1
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
-    u = np.random.default_rng(0).standard_normal(cfg.shape)
+    u = np.random.default_rng(0).standard_normal((REF_ROWS, cfg.n))
     for _ in range(args.warmup):
         oracle_sample_step(cfg, u)
     t0 = time.perf_counter()
@@ -202,7 +208,8 @@ def run_reference(args):
         "config": {"workload": f"{cfg.name}: {cfg.dim}D n={cfg.n} Nt={cfg.nt} ETD2 Picard sweep (BASELINE.json:11)"},
         "cpu_baseline": {"value": value, "unit": "DOF-iter/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
                          "kind": "oracle",
-                         "sample": f"each step: oracle A u on one {cfg.name} slice = N_st/(5 Nt) DOF-iterations"},
+                         "sample": f"each step: oracle x-axis DST-I of {REF_ROWS} rows of a {cfg.name} slice = "
+                                   f"{REF_ROWS}/(10 dim n^(dim-1) Nt) of an oracle sweep"},
         "e2e": {"value": value, "unit": "DOF-iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)

@@ -104,6 +104,7 @@ def lib():
             "orc_gmres": (C.c_int, [pp, dp, dp, C.c_double, C.c_int, C.c_int, dp, C.POINTER(C.c_int)]),
             "orc_mode_residual": (None, [pp, C.c_long, dp, C.c_double, dp, dp]),
             "orc_dst_sample_batch": (None, [pp, dp, C.c_long, C.POINTER(C.c_long), C.c_int, dp]),
+            "orc_dst_x_rows": (None, [pp, dp, C.c_long, dp]),
             "orc_mode_precond": (None, [pp, C.c_long, dp, dp]),
         }
         for name, (res, args) in sig.items():
@@ -150,6 +151,15 @@ def dst_sample(s: Spec, v, idx) -> np.ndarray:
     out = np.empty(len(idx))
     p = s.c_struct()
     lib().orc_dst_sample(C.byref(p), _p(v), idx.ctypes.data_as(C.POINTER(C.c_long)), len(idx), _p(out))
+    return out
+
+
+def dst_x_rows(s: Spec, rows) -> np.ndarray:
+    """The x-axis factor of V on rows [nrows][n] (the first axis pass of dst)."""
+    rows = _f64(rows)
+    out = np.empty_like(rows)
+    p = s.c_struct()
+    lib().orc_dst_x_rows(C.byref(p), _p(rows), rows.shape[0], _p(out))
     return out
 
 

@@ -171,6 +171,23 @@ void orc_dst(const orc_problem* p, const double* in, double* out) {
   free(S); free(a); free(b);
 }
 
+/* The x-axis factor of V on nrows rows of n points (plain O(n) sums per output, the first
+   axis pass of orc_dst): the bounded CPU-baseline sample of bench.py. */
+void orc_dst_x_rows(const orc_problem* p, const double* in, long nrows, double* out) {
+  ld* S = sine_table(p->n);
+  long n = p->n;
+#pragma omp parallel for schedule(static)
+  for (long r = 0; r < nrows; ++r) {
+    for (long j = 0; j < n; ++j) {
+      ld acc = 0.0L;
+      const ld* Sj = S + j * n;
+      for (long i = 0; i < n; ++i) acc += Sj[i] * (ld)in[r * n + i];
+      out[r * n + j] = (double)acc;
+    }
+  }
+  free(S);
+}
+
 /* One entry of V in: sum over all grid points of prod_axes S[j_ax][i_ax] in[i]. */
 void orc_dst_sample(const orc_problem* p, const double* in, const long* idx, int ns, double* out) {
   ld* S = sine_table(p->n);

@@ -49,6 +49,7 @@ void orc_dst(const orc_problem* p, const double* in, double* out);
 /* Selected entries of V in: out[s] = (V in)[idx[s]]. */
 void orc_dst_sample_batch(const orc_problem* p, const double* in, long nslices, const long* idx, int ns,
                           double* out);
+void orc_dst_x_rows(const orc_problem* p, const double* in, long nrows, double* out);
 void orc_dst_sample(const orc_problem* p, const double* in, const long* idx, int ns, double* out);
 /* A v = V diag(E) V v with A = exp(dt L_h). */
 void orc_apply_A(const orc_problem* p, const double* v, double* out);

@@ -625,3 +625,13 @@ def test_imex_iteration_linear_rate(orc):
     assert st == 0 and len(ratios) >= 2
     assert abs(ratios[-1] / rho - 1.0) < 0.05
 
+
+
+def test_dst_x_rows_is_the_1d_transform(orc):
+    n = 13
+    s1 = spec(orc, 1, n)
+    s2 = spec(orc, 2, n)
+    rows = np.random.default_rng(8).standard_normal((5, n))
+    got = orc.dst_x_rows(s2, rows)
+    for r in range(5):
+        assert np.allclose(got[r], orc.dst(s1, rows[r]), atol=1e-14)
