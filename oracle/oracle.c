@@ -383,6 +383,28 @@ void orc_sequential(const orc_problem* p, const double* u0, double* U) {
   ld* nm1 = (ld*)malloc(sizeof(ld) * (size_t)N);
   ld* nm2 = (ld*)malloc(sizeof(ld) * (size_t)N);
   for (long i = 0; i < N; ++i) prev[i] = u0[i];
+  if (p->scheme == 3) {
+    /* exponential BDF2 (4.1): u_n = 4/3 A u_{n-1} - 1/3 B u_{n-2}, B = A^2,
+       started by u_1 = A u_0 (reading R16); U holds the unknowns v = (u_2, .., u_{Nt+1})
+       of the all-at-once system (4.2), Nt = p->nt of them. */
+    ld* um2 = (ld*)malloc(sizeof(ld) * (size_t)N);
+    ld* t1 = (ld*)malloc(sizeof(ld) * (size_t)N);
+    memcpy(um2, prev, sizeof(ld) * (size_t)N);       /* u_0 */
+    apply_mult_ld(&c, c.E, um2, prev);                /* u_1 = A u_0 */
+    for (int n = 2; n <= p->nt + 1; ++n) {
+      apply_mult_ld(&c, c.E, prev, cur);              /* A u_{n-1} */
+      apply_mult_ld(&c, c.E, um2, t1);
+      apply_mult_ld(&c, c.E, t1, nm1);                /* B u_{n-2} = A (A u_{n-2}) */
+      for (long i = 0; i < N; ++i) cur[i] = (4.0L / 3.0L) * cur[i] - (1.0L / 3.0L) * nm1[i];
+      for (long i = 0; i < N; ++i) U[(size_t)(n - 2) * N + i] = (double)cur[i];
+      memcpy(um2, prev, sizeof(ld) * (size_t)N);
+      memcpy(prev, cur, sizeof(ld) * (size_t)N);
+    }
+    free(um2); free(t1);
+    free(prev); free(cur); free(nm1); free(nm2);
+    ctx_free(&c);
+    return;
+  }
   /* N(u_{-1}) := N(u_0) (R6) */
   for (long i = 0; i < N; ++i) nm2[i] = nonlin_ld(p, prev[i]);
   for (int n = 1; n <= p->nt; ++n) {
@@ -404,10 +426,39 @@ void orc_sequential(const orc_problem* p, const double* u0, double* U) {
 
 /* r_n = A u_{n-1} + Phi[N] - u_n, n = 1..Nt, U in long double (PAPER.md:181-183 gives
    f - Q u for the linear part: f = (A u_0, 0, ..., 0), (Q u)_n = u_n - A u_{n-1}). */
+/* BDF2 (scheme 3): r = f_2 - R v, v = (u_2, .., u_{Nt+1}), u_1 = A u_0:
+   r_1 = 4/3 A u_1 - 1/3 B u_0 - v_1, r_2 = 4/3 A v_1 - 1/3 B u_1 - v_2,
+   r_n = 4/3 A v_{n-1} - 1/3 B v_{n-2} - v_n. */
+static void residual_bdf2_ld(const ctx_t* c, const ld* u0, const ld* U, ld* R) {
+  const orc_problem* p = c->p;
+  long N = c->N;
+  ld* u1 = (ld*)malloc(sizeof(ld) * (size_t)N);
+  apply_mult_ld(c, c->E, u0, u1);
+#pragma omp parallel for schedule(dynamic, 1)
+  for (int n = 1; n <= p->nt; ++n) {
+    const ld* p1 = (n == 1) ? u1 : U + (size_t)(n - 2) * N;                       /* v_{n-1} */
+    const ld* p2 = (n == 1) ? u0 : (n == 2) ? u1 : U + (size_t)(n - 3) * N;       /* v_{n-2} */
+    ld* r = R + (size_t)(n - 1) * N;
+    ld* t1 = (ld*)malloc(sizeof(ld) * (size_t)N);
+    ld* t2 = (ld*)malloc(sizeof(ld) * (size_t)N);
+    apply_mult_ld(c, c->E, p1, r);
+    apply_mult_ld(c, c->E, p2, t1);
+    apply_mult_ld(c, c->E, t1, t2);
+    const ld* vn = U + (size_t)(n - 1) * N;
+    for (long i = 0; i < N; ++i) r[i] = (4.0L / 3.0L) * r[i] - (1.0L / 3.0L) * t2[i] - vn[i];
+    free(t1); free(t2);
+  }
+  free(u1);
+}
+
 static void residual_ld(const ctx_t* c, const ld* u0, const ld* U, ld* R) {
   const orc_problem* p = c->p;
   long N = c->N;
   int nonlin = p->npoly > 0;
+  if (p->scheme == 3) {
+    residual_bdf2_ld(c, u0, U, R);
+    return;
+  }
 #pragma omp parallel for schedule(dynamic, 1)
   for (int n = 1; n <= p->nt; ++n) {
     const ld* prev = (n == 1) ? u0 : U + (size_t)(n - 2) * N;
@@ -458,6 +509,37 @@ void orc_residual(const orc_problem* p, const double* u0, const double* U, doubl
 static void apply_Qcorner_ld(const ctx_t* c, ld corner, const ld* V, ld* out) {
   const orc_problem* p = c->p;
   long N = c->N;
+  if (p->scheme == 3) {
+    /* BDF2: R v = v - 4/3 (C_0 (x) A) v + 1/3 (C_1 (x) B) v; with
+       corner alpha: R_alpha, C_0^alpha(1, L) = alpha, C_1^alpha(1, L-1) = C_1^alpha(2, L) =
+       alpha */
+    const int L = p->nt;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int n = 1; n <= L; ++n) {
+      ld* o = out + (size_t)(n - 1) * N;
+      const ld* vn = V + (size_t)(n - 1) * N;
+      ld* t1 = (ld*)malloc(sizeof(ld) * (size_t)N);
+      ld* t2 = (ld*)malloc(sizeof(ld) * (size_t)N);
+      for (long i = 0; i < N; ++i) o[i] = vn[i];
+      /* C_0 part: v_{n-1} (n >= 2), alpha v_L (n = 1) */
+      const ld* a0 = (n >= 2) ? V + (size_t)(n - 2) * N : V + (size_t)(L - 1) * N;
+      ld w0 = (n >= 2) ? 1.0L : corner;
+      if (w0 != 0.0L) {
+        apply_mult_ld(c, c->E, a0, t1);
+        for (long i = 0; i < N; ++i) o[i] -= (4.0L / 3.0L) * w0 * t1[i];
+      }
+      /* C_1 part: v_{n-2} (n >= 3), alpha v_{L-1} (n = 1), alpha v_L (n = 2) */
+      const ld* a1 = (n >= 3) ? V + (size_t)(n - 3) * N : V + (size_t)(L - 3 + n) * N;
+      ld w1 = (n >= 3) ? 1.0L : corner;
+      if (w1 != 0.0L) {
+        apply_mult_ld(c, c->E, a1, t1);
+        apply_mult_ld(c, c->E, t1, t2);
+        for (long i = 0; i < N; ++i) o[i] += (1.0L / 3.0L) * w1 * t2[i];
+      }
+      free(t1); free(t2);
+    }
+    return;
+  }
 #pragma omp parallel for schedule(dynamic, 1)
   for (int n = 1; n <= p->nt; ++n) {
     ld* o = out + (size_t)(n - 1) * N;
@@ -544,8 +626,17 @@ static ld precond_ld(const ctx_t* c, const ld* R, ld* Sout) {
     dst_ld(p, c->S, yr, tr);
     dst_ld(p, c->S, yi, ti);
     ld lre = a1 * cs[k], lim = a1 * sn[k];
+    /* BDF2: lambda_{1,k} = alpha^{2/L} e^{4 pi i (k-1)/L} */
+    int q2 = (int)((2L * k) % nt);
+    ld l1re = powl((ld)p->alpha, 2.0L / (ld)nt) * cs[q2], l1im = powl((ld)p->alpha, 2.0L / (ld)nt) * sn[q2];
     for (long J = 0; J < N; ++J) {
       ld dre = 1.0L - lre * c->E[J], dim = -lim * c->E[J]; /* 1 - lambda_k E_J */
+      if (p->scheme == 3) {
+        /* 1 - 4/3 lambda_{0,k} E_J + 1/3 lambda_{1,k} E_J^2 (Step (b), (4.5)) */
+        ld e2 = c->E[J] * c->E[J];
+        dre = 1.0L - (4.0L / 3.0L) * lre * c->E[J] + (1.0L / 3.0L) * l1re * e2;
+        dim = -(4.0L / 3.0L) * lim * c->E[J] + (1.0L / 3.0L) * l1im * e2;
+      }
       ld den = dre * dre + dim * dim;
       ld xr = (tr[J] * dre + ti[J] * dim) / den;
       ld xi = (ti[J] * dre - tr[J] * dim) / den;
@@ -732,6 +823,15 @@ void orc_mode_residual(const orc_problem* p, long J, const double* uhat, double 
   ld E, f1, f2;
   mode_coefs_ld(p, J, &E, &f1, &f2);
   int nonlin = p->npoly > 0 && nhat;
+  if (p->scheme == 3) {  /* BDF2 (see residual_bdf2_ld), u_1 = E u_0 */
+    ld u1 = E * (ld)uhat0;
+    for (int n = 1; n <= p->nt; ++n) {
+      ld p1 = (n == 1) ? u1 : (ld)uhat[n - 2];
+      ld p2 = (n == 1) ? (ld)uhat0 : (n == 2) ? u1 : (ld)uhat[n - 3];
+      rhat[n - 1] = (double)((4.0L / 3.0L) * E * p1 - (1.0L / 3.0L) * E * E * p2 - (ld)uhat[n - 1]);
+    }
+    return;
+  }
   for (int n = 1; n <= p->nt; ++n) {
     ld prev = (n == 1) ? (ld)uhat0 : (ld)uhat[n - 2];
     ld r = E * prev - (ld)uhat[n - 1];
@@ -771,8 +871,14 @@ void orc_mode_precond(const orc_problem* p, long J, const double* rhat, double* 
       are += cs[q] * y;
       aim += sn[q] * y;
     }
-    /* Step (b): divide by 1 - lambda_k E_J */
+    /* Step (b): divide by 1 - lambda_k E_J (BDF2: 1 - 4/3 lambda_{0,k} E + 1/3 lambda_{1,k} E^2) */
     ld dre = 1.0L - a1 * cs[k] * E, dim = -a1 * sn[k] * E;
+    if (p->scheme == 3) {
+      int q2 = (int)((2L * k) % nt);
+      ld a2 = powl((ld)p->alpha, 2.0L / (ld)nt);
+      dre = 1.0L - (4.0L / 3.0L) * a1 * cs[k] * E + (1.0L / 3.0L) * a2 * cs[q2] * E * E;
+      dim = -(4.0L / 3.0L) * a1 * sn[k] * E + (1.0L / 3.0L) * a2 * sn[q2] * E * E;
+    }
     ld den = dre * dre + dim * dim;
     ld yr = is * are, yi = is * aim;
     Yr[k] = (yr * dre + yi * dim) / den;

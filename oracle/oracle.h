@@ -31,7 +31,9 @@ typedef struct {
   int nt;          /* N_t                                                          */
   double alpha;    /* alpha-circulant parameter                  */
   int scheme;      /* 0: exponential Euler / ETD1, 1: ETD2 (readings R5, R6),      *
-                    * 2: IF scheme (6.1) / IMEX-type iteration (7.2) */
+                    * 2: IF scheme (6.1) / IMEX-type iteration (7.2), *
+                    * 3: exponential BDF2 (4.1)-(4.5), linear only:  *
+                    *    nt unknowns u_2..u_{nt+1}, u_1 = A u_0 (reading R16)           */
   int npoly;       /* N(u) = sum_{p<npoly} q[p] u^p ; 0 = linear                   */
   double q[8];
 } orc_problem;

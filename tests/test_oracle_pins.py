@@ -635,3 +635,118 @@ def test_dst_x_rows_is_the_1d_transform(orc):
     got = orc.dst_x_rows(s2, rows)
     for r in range(5):
         assert np.allclose(got[r], orc.dst(s1, rows[r]), atol=1e-14)
+
+
+# ------------------------------------------------------------------------------------------
+# NEXT-2: exponential BDF2 (4.1)-(4.5), scheme 3, linear: unknowns
+# v = (u_2, .., u_{L+1}), L = nt, started by u_1 = A u_0 (reading R16)
+# ------------------------------------------------------------------------------------------
+def bdf2_dense(s):
+    """R, R_alpha of (4.2), (4.4) as dense Kronecker products."""
+    A = sla.expm(s.dt * Lh(s))
+    B = A @ A
+    L = s.nt
+    C0 = np.diag(np.ones(L - 1), -1)
+    C1 = np.diag(np.ones(L - 2), -2)
+    C0a, C1a = C0.copy(), C1.copy()
+    C0a[0, L - 1] = s.alpha
+    C1a[0, L - 2] = s.alpha
+    C1a[1, L - 1] = s.alpha
+    I = np.eye(L * s.N)
+    R = I - 4.0 / 3.0 * np.kron(C0, A) + 1.0 / 3.0 * np.kron(C1, B)
+    Ra = I - 4.0 / 3.0 * np.kron(C0a, A) + 1.0 / 3.0 * np.kron(C1a, B)
+    return A, B, R, Ra
+
+
+def test_bdf2_sequential_exact_for_linear(orc):
+    """With u_1 = A u_0 the linear BDF2 recursion reproduces u_n = A^n u_0."""
+    s = spec(orc, 1, 9, a=0.5, c=0.3, T=1.0, nt=8, scheme=3)
+    u0 = np.random.default_rng(5).standard_normal(9)
+    A = sla.expm(s.dt * Lh(s))
+    U = orc.sequential(s, u0)
+    for n in range(2, s.nt + 2):
+        assert rel(U[n - 2], np.linalg.matrix_power(A, n) @ u0) < 1e-12
+
+
+@pytest.mark.parametrize("dim,n", [(1, 6), (2, 3)])
+def test_bdf2_residual_and_operators_vs_dense(orc, dim, n):
+    s = spec(orc, dim, n, a=0.5, c=1.0, T=0.6, nt=6, alpha=0.05, scheme=3)
+    A, B, R, Ra = bdf2_dense(s)
+    rng = np.random.default_rng(6)
+    u0 = rng.standard_normal((n,) * dim)
+    U = rng.standard_normal((s.nt,) + (n,) * dim)
+    u0f, u1f = u0.reshape(-1), A @ u0.reshape(-1)
+    f2 = np.zeros(s.nt * s.N)
+    f2[: s.N] = 4.0 / 3.0 * A @ u1f - 1.0 / 3.0 * B @ u0f
+    f2[s.N: 2 * s.N] = -1.0 / 3.0 * B @ u1f
+    Rr, _ = orc.residual(s, u0, U)
+    assert rel(Rr.reshape(-1), f2 - R @ U.reshape(-1)) < 1e-12
+    assert rel(orc.apply_Q(s, U).reshape(-1), R @ U.reshape(-1)) < 1e-12
+    assert rel(orc.apply_Qalpha(s, U).reshape(-1), Ra @ U.reshape(-1)) < 1e-12
+    S, leak = orc.precond(s, U)
+    assert leak < 1e-8
+    assert rel(S.reshape(-1), np.linalg.solve(Ra, U.reshape(-1))) < 1e-11
+
+
+def test_bdf2_simultaneous_diagonalization():
+    """C_1^alpha = P_alpha D_1 P_alpha^{-1} with lambda_{1,n} = alpha^{2/L} e^{4 pi i (n-1)/L}
+    and the same P_alpha as C_0^alpha."""
+    L, alpha = 7, 0.3
+    C1a = np.diag(np.ones(L - 2), -2).astype(complex)
+    C1a[0, L - 2] = alpha
+    C1a[1, L - 1] = alpha
+    w = np.exp(2j * np.pi / L)
+    F = np.array([[w ** (k * m) for m in range(L)] for k in range(L)]) / np.sqrt(L)
+    Ga = np.diag([alpha ** (m / L) for m in range(L)])
+    P = np.linalg.inv(Ga) @ F.conj().T
+    D1 = np.diag([alpha ** (2 / L) * np.exp(4j * np.pi * k / L) for k in range(L)])
+    assert np.abs(P @ D1 @ np.linalg.inv(P) - C1a).max() < 1e-13
+
+
+@pytest.mark.parametrize("z,alpha,L", [(-0.3, 0.05, 8), (-2.0, 0.2, 6), (-0.01, 0.01, 10)])
+def test_bdf2_theorem_4_1_spectrum(z, alpha, L):
+    """Thm 4.1: sigma(M_z) = {0 (L-2 times), -alpha e^{Lz}/(1 - alpha
+    e^{Lz}), -alpha (e^z/3)^L / (1 - alpha (e^z/3)^L)}, rho(M_z) <= alpha/(1-alpha)."""
+    e = np.exp(z)
+    C0 = np.diag(np.ones(L - 1), -1)
+    C1 = np.diag(np.ones(L - 2), -2)
+    C0a, C1a = C0.copy(), C1.copy()
+    C0a[0, L - 1] = alpha
+    C1a[0, L - 2] = alpha
+    C1a[1, L - 1] = alpha
+    T = np.eye(L) - 4.0 / 3.0 * e * C0 + 1.0 / 3.0 * e * e * C1
+    Ta = np.eye(L) - 4.0 / 3.0 * e * C0a + 1.0 / 3.0 * e * e * C1a
+    ev = np.linalg.eigvals(np.eye(L) - np.linalg.solve(Ta, T))
+    # r_- = -alpha e^{Lz}, r_+ = -alpha (e^z/3)^L (PAPER.md:559); sigma = 1 - 1/(1 + r)
+    r_minus, r_plus = -alpha * e ** L, -alpha * (e / 3.0) ** L
+    want = sorted([0.0] * (L - 2) + [r_minus / (1 + r_minus), r_plus / (1 + r_plus)])
+    got = sorted(ev.real)
+    assert np.abs(ev.imag).max() < 1e-10
+    assert np.allclose(got, want, atol=1e-12)
+    assert np.abs(ev).max() <= alpha / (1 - alpha) + 1e-14
+
+
+def test_bdf2_fixed_point_and_gmres_reach_sequential(orc):
+    s = spec(orc, 2, 5, a=0.5, c=0.3, T=1.0, nt=8, alpha=0.05, scheme=3)
+    u0 = np.random.default_rng(9).standard_normal((5, 5))
+    seq = orc.sequential(s, u0)
+    U, st, its, hist = orc.fixed_point(s, u0, tol=1e-12)
+    assert st == 0 and rel(U, seq) < 1e-11
+    Ug, stg, itsg, _ = orc.gmres(s, u0, tol=1e-13, restart=60, maxit=60)
+    assert stg == 0 and rel(Ug, seq) < 1e-11
+    assert itsg <= 2 * 5 + 1  # Thm 4.3 bound with N_x = 5 per axis (PAPER.md:620)
+
+
+def test_bdf2_fixed_point_rate_is_theorem_4_1(orc):
+    """A single sine mode: the fixed-point residual contracts per sweep by the largest
+    |eigenvalue| of M_z, z = dt mu_J (Thm 4.1), i.e. alpha e^{Lz}/(1 - alpha e^{Lz})."""
+    n, k, L, alpha = 9, 1, 8, 0.2
+    s = spec(orc, 1, n, a=0.05, c=0.01, T=0.4, nt=L, alpha=alpha, scheme=3)
+    u0 = synth.sine_table(n, k)[k - 1]
+    mu = np.sort(np.linalg.eigvalsh(Lh(s)))[::-1][k - 1]
+    ez = np.exp(s.dt * mu)
+    rho = alpha * ez ** L / (1 - alpha * ez ** L)
+    U, st, its, hist = orc.fixed_point(s, u0, tol=1e-14, maxit=40)
+    ratios = hist[2:its] / hist[1:its - 1]
+    assert len(ratios) >= 2
+    assert abs(ratios[-1] / rho - 1.0) < 1e-3
