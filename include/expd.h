@@ -48,9 +48,13 @@ typedef enum {
 typedef enum {
   EXPD_EXP_EULER = 0, /* linear (npoly = 0) or ETD1: u_n = E u_{n-1} + dt phi1 N(u_{n-1}) (R5) */
   EXPD_ETD2 = 1,      /* u_n = E u_{n-1} + dt[(phi1+phi2) N_{n-1} - phi2 N_{n-2}] (R6)        */
-  EXPD_IF_IMEX = 2    /* the paper's own: IF scheme (6.1) u_n = E u_{n-1} + dt N(u_n)
+  EXPD_IF_IMEX = 2,   /* the paper's own: IF scheme (6.1) u_n = E u_{n-1} + dt N(u_n)
                          (PAPER.md:815), solved by the IMEX-type iteration (7.2)/(7.3)
                          (PAPER.md:1209-1220): N of the same slice, lagged one sweep    */
+  EXPD_BDF2 = 3       /* exponential BDF2 all-at-once system (4.1)-(4.5),
+                         linear problems only (npoly = 0): the nt unknowns of U are
+                         u_2 .. u_{nt+1} (u_1 = A u_0, reading R16; T = (nt+1) dt); the
+                         preconditioner divides by 1 - 4/3 lambda_k E + 1/3 lambda_k^2 E^2 */
 } expd_scheme;
 
 typedef struct {

@@ -27,6 +27,7 @@ struct expd_plan {
   int sms = 148;
   int nl = 0;      // 0 linear, 1 ETD1 / IF-IMEX, 2 ETD2
   int nshift = 0;  // IF / IMEX-type: K1 reads N-hat of the same slice (one slice later)
+  int k1 = 0;      // K1 form: nl, or 3 for the BDF2 system
   double a1 = 0.0;
   // small device tables owned by the plan
   double* d_lam = nullptr;   // [n]
@@ -133,7 +134,9 @@ extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dis
   if (P.dim < 1 || P.dim > 3 || P.n < 3 || !is_pow2((long)P.n + 1) || P.n + 1 > 4096 || !(P.a > 0.0) ||
       !(P.c >= 0.0) || !(P.dt > 0.0) || P.nt < 4 || !is_pow2(P.nt) || !(P.alpha > 0.0) || !(P.alpha <= 1.0) ||
       P.npoly < 0 || P.npoly > 8 ||
-      (P.scheme != EXPD_EXP_EULER && P.scheme != EXPD_ETD2 && P.scheme != EXPD_IF_IMEX) ||
+      (P.scheme != EXPD_EXP_EULER && P.scheme != EXPD_ETD2 && P.scheme != EXPD_IF_IMEX &&
+       P.scheme != EXPD_BDF2) ||
+      (P.scheme == EXPD_BDF2 && P.npoly > 0) ||
       !std::isfinite(P.a) || !std::isfinite(P.c) || !std::isfinite(P.dt))
     return EXPD_ERR_INVALID_ARG;
   if (P.nt > 256) return EXPD_ERR_UNSUPPORTED;
@@ -167,6 +170,7 @@ extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dis
   // K1 form: 0 linear, 1 one N-hat term (ETD1; IF/IMEX with N of the same slice), 2 ETD2
   p->nl = P.npoly > 0 ? (P.scheme == EXPD_ETD2 ? 2 : 1) : 0;
   p->nshift = (P.npoly > 0 && P.scheme == EXPD_IF_IMEX) ? 1 : 0;
+  p->k1 = P.scheme == EXPD_BDF2 ? 3 : p->nl;  // K1 form (3: the BDF2 system)
   if (cudaSetDevice(device) != cudaSuccess) {
     delete p;
     return EXPD_ERR_CUDA;
@@ -391,7 +395,7 @@ static cudaError_t enqueue_sweep(expd_plan* p, cudaStream_t st) {
   }
   if ((e = record(p, 1, st)) != cudaSuccess) return e;
   TimeArgs a = time_args(p, p->Uh, p->Uh, true);
-  e = launch_time_fused(a, RM_RESID, OUT_UPDATE, p->nl, p->time_grid, st);
+  e = launch_time_fused(a, RM_RESID, OUT_UPDATE, p->k1, p->time_grid, st);
   if (e != cudaSuccess) return e;
   if ((e = record(p, 2, st)) != cudaSuccess) return e;
   return reduce_partials(p->partial, p->time_grid, p->dscal, st);
@@ -412,7 +416,7 @@ static expd_status sweep_dist(expd_plan* p) {
   }
   CUDA_TRY(p, record(p, 1, p->stream));
   TimeArgs a = time_args(p, p->Uh, p->Uh, true);
-  CUDA_TRY(p, launch_time_fused(a, RM_RESID, OUT_UPDATE, p->nl, p->time_grid, p->stream));
+  CUDA_TRY(p, launch_time_fused(a, RM_RESID, OUT_UPDATE, p->k1, p->time_grid, p->stream));
   CUDA_TRY(p, record(p, 2, p->stream));
   CUDA_TRY(p, reduce_partials(p->partial, p->time_grid, p->dscal, p->stream));
   return allreduce(p, p->dscal, 1);
@@ -476,7 +480,7 @@ extern "C" expd_status expd_residual(expd_plan* p, const double* u0, const doubl
     if ((s = a2a(p, A2A_T2M_SHIFT, p->NT, p->Nh))) return s;
   }
   TimeArgs a = time_args(p, p->Uh, p->T1, true);
-  CUDA_TRY(p, launch_resid_only(a, p->nl, p->time_grid, p->stream));
+  CUDA_TRY(p, launch_resid_only(a, p->k1, p->time_grid, p->stream));
   CUDA_TRY(p, reduce_partials(p->partial, p->time_grid, p->dscal, p->stream));
   if ((s = allreduce(p, p->dscal, 1))) return s;
   if ((s = mode_to_phys(p, p->T1, R))) return s;
@@ -490,7 +494,7 @@ extern "C" expd_status expd_precond_apply(expd_plan* p, const double* R, double*
   if (!R || !S) return fail(p, EXPD_ERR_INVALID_ARG, "expd_precond_apply: bad pointers");
   if ((s = phys_to_mode(p, R, p->T1))) return s;
   TimeArgs a = time_args(p, p->T1, p->T1, false);
-  CUDA_TRY(p, launch_time_fused(a, RM_INPUT, OUT_S, 0, p->time_grid, p->stream));
+  CUDA_TRY(p, launch_time_fused(a, RM_INPUT, OUT_S, p->k1 == 3 ? 3 : 0, p->time_grid, p->stream));
   return mode_to_phys(p, p->T1, S);
 }
 
@@ -606,9 +610,9 @@ extern "C" expd_status expd_debug_kernel_ms(expd_plan* p, int which, long nslice
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
     TimeArgs a = time_args(p, p->Uh, p->Uh, true);
-    CUDA_TRY(p, launch_time_fused(a, RM_RESID, OUT_UPDATE, p->nl, p->time_grid, p->stream));
+    CUDA_TRY(p, launch_time_fused(a, RM_RESID, OUT_UPDATE, p->k1, p->time_grid, p->stream));
     cudaEventRecord(e0, p->stream);
-    for (int i = 0; i < reps; ++i) CUDA_TRY(p, launch_time_fused(a, RM_RESID, OUT_UPDATE, p->nl, p->time_grid, p->stream));
+    for (int i = 0; i < reps; ++i) CUDA_TRY(p, launch_time_fused(a, RM_RESID, OUT_UPDATE, p->k1, p->time_grid, p->stream));
     cudaEventRecord(e1, p->stream);
     cudaEventSynchronize(e1);
     cudaEventElapsedTime(&m, e0, e1);
@@ -708,7 +712,7 @@ extern "C" expd_status expd_gmres_solve(expd_plan* p, const double* u0, double* 
   while (its < maxit) {
     // z = Q_alpha^{-1}(f - Q x)  [K1: residual -> precondition], beta = ||z||
     TimeArgs a = time_args(p, p->Uh, p->T1, false);
-    CUDA_TRY(p, launch_time_fused(a, RM_RESID, OUT_S, 0, p->time_grid, p->stream));
+    CUDA_TRY(p, launch_time_fused(a, RM_RESID, OUT_S, p->k1, p->time_grid, p->stream));
     const double* t1c = p->T1;
     CUDA_TRY(p, multi_dot(&t1c, 1, p->T1, len, p->partial, p->vgrid, p->dscal, p->stream));
     if ((s = allreduce(p, p->dscal, 1))) return s;
@@ -728,7 +732,7 @@ extern "C" expd_status expd_gmres_solve(expd_plan* p, const double* u0, double* 
     for (j = 0; j < m && its < maxit; ++j) {
       for (int i = 0; i <= j; ++i) Vp[i] = Vk(i);
       TimeArgs q = time_args(p, Vk(j), p->T1, false);
-      CUDA_TRY(p, launch_time_fused(q, RM_QOP, OUT_S, 0, p->time_grid, p->stream));  // w = P Q v_j
+      CUDA_TRY(p, launch_time_fused(q, RM_QOP, OUT_S, p->k1, p->time_grid, p->stream));  // w = P Q v_j
       // CGS2: h = V^T w ; w -= V h ; h2 = V^T w ; w -= V h2 ; ||w||^2
       // (distributed: every partial inner product is completed by an allreduce before use)
       CUDA_TRY(p, multi_dot(Vp.data(), j + 1, p->T1, len, p->partial, p->vgrid, dcoef, p->stream));

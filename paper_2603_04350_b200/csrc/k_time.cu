@@ -82,13 +82,28 @@ __device__ __forceinline__ double2 half_divisor(double beta, double c, double s,
   return make_double2(u * r, v * r);
 }
 
+// BDF2: 1 - 4/3 lambda_{0,k} E + 1/3 lambda_{1,k} E^2 with
+// lambda_{1,k} = lambda_{0,k}^2 = (1 - x)(1 - x/3), x = beta e^{i theta}: the product of two
+// first-order reciprocals.
+__device__ __forceinline__ double2 half_divisor_bdf2(double beta, double c, double s, double half_inv_nt) {
+  return cmul(half_divisor(beta, c, s, half_inv_nt), half_divisor(beta * (1.0 / 3.0), c, s, 1.0));
+}
+
+// NL == 3 marks the BDF2 system (linear): residual f2 - R v, Q-operator R v, BDF2 divisor
+template <int NL>
+struct K1Form {
+  static constexpr bool HASN = NL == 1 || NL == 2;  // an N-hat term in the residual
+  static constexpr bool BDF = NL == 3;
+};
+
 // W_k = A Z_k + B conj(Z_kp),  W_kp = conj(A) Z_kp + conj(B) conj(Z_k)
 // with A = (da + db)/2, B = (da - db)/2 for the two modes of the pair (Hermitian unpack,
 // divide, repack in one step).  tw = e^{2 pi i k/Nt}.
+template <bool BDF = false>
 __device__ __forceinline__ void divide_pair(double2& Zk, double2& Zkp, double2 tw, double ba, double bb,
                                             double hin, bool self) {
-  double2 da = half_divisor(ba, tw.x, tw.y, hin);
-  double2 db = half_divisor(bb, tw.x, tw.y, hin);
+  double2 da = BDF ? half_divisor_bdf2(ba, tw.x, tw.y, hin) : half_divisor(ba, tw.x, tw.y, hin);
+  double2 db = BDF ? half_divisor_bdf2(bb, tw.x, tw.y, hin) : half_divisor(bb, tw.x, tw.y, hin);
   double2 A = cadd(da, db), B = csub(da, db);
   double2 zk = Zk, zkp = Zkp;
   // A*zk + B*conj(zkp)
@@ -164,26 +179,45 @@ __device__ __forceinline__ void tstage_pw(const double2* __restrict__ in, double
 // Last forward stage (radix RL, NS = NT/RL) of two partner jobs ja, jb (their frequency sets
 // k = j + NS r are Hermitian partners), the pair divide, and the first inverse stage
 // (radix RL, NS = 1: no twiddles) on the same sets.
-template <int NT, int RL>
+template <int NT, int RL, bool BDF = false>
 __device__ __forceinline__ void pair_divide(double2 (&va)[RL], double2 (&vb)[RL], bool pj0, const double2* stw,
                                             int ja, int jb, double ba, double bb, double hin) {
   constexpr int NS = NT / RL;
   if (!pj0) {
 #pragma unroll
-    for (int r = 0; r < RL; ++r) divide_pair(va[r], vb[RL - 1 - r], stw[ja + NS * r], ba, bb, hin, false);
+    for (int r = 0; r < RL; ++r) divide_pair<BDF>(va[r], vb[RL - 1 - r], stw[ja + NS * r], ba, bb, hin, false);
   } else {
     // ja = 0: frequencies NS r, partner NS (RL - r) mod RL; self at r = 0 and RL/2
-    divide_pair(va[0], va[0], stw[0], ba, bb, hin, true);
+    divide_pair<BDF>(va[0], va[0], stw[0], ba, bb, hin, true);
 #pragma unroll
-    for (int r = 1; r < (RL + 1) / 2; ++r) divide_pair(va[r], va[RL - r], stw[NS * r], ba, bb, hin, false);
-    if constexpr (RL % 2 == 0) divide_pair(va[RL / 2], va[RL / 2], stw[NS * (RL / 2)], ba, bb, hin, true);
+    for (int r = 1; r < (RL + 1) / 2; ++r) divide_pair<BDF>(va[r], va[RL - r], stw[NS * r], ba, bb, hin, false);
+    if constexpr (RL % 2 == 0) divide_pair<BDF>(va[RL / 2], va[RL / 2], stw[NS * (RL / 2)], ba, bb, hin, true);
     if (jb != ja) {
       // jb = NS/2: frequencies NS/2 + NS r, partner index RL-1-r
 #pragma unroll
-      for (int r = 0; r < RL / 2; ++r) divide_pair(vb[r], vb[RL - 1 - r], stw[jb + NS * r], ba, bb, hin, false);
-      if constexpr (RL % 2 == 1) divide_pair(vb[RL / 2], vb[RL / 2], stw[jb + NS * (RL / 2)], ba, bb, hin, true);
+      for (int r = 0; r < RL / 2; ++r)
+        divide_pair<BDF>(vb[r], vb[RL - 1 - r], stw[jb + NS * r], ba, bb, hin, false);
+      if constexpr (RL % 2 == 1)
+        divide_pair<BDF>(vb[RL / 2], vb[RL / 2], stw[jb + NS * (RL / 2)], ba, bb, hin, true);
     }
   }
+}
+
+// BDF2 time-local residual / Q-operator of one mode pair at time t:
+// RESID: r_t = 4/3 E p1 - 1/3 E^2 p2 - x_t, p1 = v_{t-1} (u_1 = E u_0 at t = 0), p2 = v_{t-2}
+// (u_1 at t = 1, u_0 at t = 0);  QOP: (R v)_t = v_t - 4/3 E v_{t-1} + 1/3 E^2 v_{t-2}.
+template <bool RESID>
+__device__ __forceinline__ double2 bdf2_form(double2 E, double2 xc, double2 xm1, double2 xm2, double2 u0, int t) {
+  const double2 u1 = make_double2(E.x * u0.x, E.y * u0.y);
+  const double2 zero = make_double2(0.0, 0.0);
+  const double2 p1 = t >= 1 ? xm1 : (RESID ? u1 : zero);
+  const double2 p2 = t >= 2 ? xm2 : (t == 1 ? (RESID ? u1 : zero) : (RESID ? u0 : zero));
+  const double c43 = 4.0 / 3.0, c13 = 1.0 / 3.0;
+  const double2 e2 = make_double2(E.x * E.x, E.y * E.y);
+  double2 r;
+  r.x = fma(c43 * E.x, p1.x, -c13 * e2.x * p2.x);
+  r.y = fma(c43 * E.y, p1.y, -c13 * e2.y * p2.y);
+  return RESID ? make_double2(r.x - xc.x, r.y - xc.y) : make_double2(xc.x - r.x, xc.y - r.y);
 }
 
 #ifndef EXPD_K1_MINB
@@ -230,7 +264,7 @@ __global__ void __launch_bounds__(EXPD_K1_THREADS, EXPD_K1_MINB) k_time_fused(co
     double2 xv[(OUTM == OUT_UPDATE && !EXPD_K1_REREAD) ? R0 : 1];
     double2 Ej = make_double2(0.0, 0.0), c1 = Ej, c2 = Ej;
     if (valid && RM != RM_INPUT) Ej = ld2(a.E + base);
-    if (valid && NL >= 1) c1 = ld2(a.C1 + base);
+    if (valid && K1Form<NL>::HASN) c1 = ld2(a.C1 + base);
     if (valid && NL == 2) c2 = ld2(a.C2 + base);
 #pragma unroll
     for (int r = 0; r < R0; ++r) {
@@ -239,6 +273,14 @@ __global__ void __launch_bounds__(EXPD_K1_THREADS, EXPD_K1_MINB) k_time_fused(co
       if (valid) cur = (OUTM == OUT_UPDATE) ? ld2(a.X + (long)t * npad + base) : ld2cs(a.X + (long)t * npad + base);
       if constexpr (RM == RM_INPUT) {
         rr = cur;
+      } else if constexpr (K1Form<NL>::BDF) {
+        double2 xm1 = make_double2(0.0, 0.0), xm2 = xm1, u0 = xm1;
+        if (valid) {
+          if (t >= 1) xm1 = ld2(a.X + (long)(t - 1) * npad + base);
+          if (t >= 2) xm2 = ld2(a.X + (long)(t - 2) * npad + base);
+          if (RM == RM_RESID) u0 = ld2(a.u0h + base);
+        }
+        rr = bdf2_form<RM == RM_RESID>(Ej, cur, xm1, xm2, u0, t);
       } else {
         double2 prev = make_double2(0.0, 0.0);
         if (valid) {
@@ -247,7 +289,7 @@ __global__ void __launch_bounds__(EXPD_K1_THREADS, EXPD_K1_MINB) k_time_fused(co
         }
         if constexpr (RM == RM_RESID) {
           rr = make_double2(fma(Ej.x, prev.x, -cur.x), fma(Ej.y, prev.y, -cur.y));
-          if constexpr (NL >= 1) {
+          if constexpr (K1Form<NL>::HASN) {
             double2 nm1 = valid ? ld2cs(a.Nh + (long)t * npad + base) : make_double2(0.0, 0.0);
             rr.x = fma(c1.x, nm1.x, rr.x);
             rr.y = fma(c1.y, nm1.y, rr.y);
@@ -272,7 +314,7 @@ __global__ void __launch_bounds__(EXPD_K1_THREADS, EXPD_K1_MINB) k_time_fused(co
       const double2 Ep = valid ? ld2(a.E + base) : make_double2(0.0, 0.0);
       const double ba = a.a1 * Ep.x, bb = a.a1 * Ep.y;
       double2 dummy[R0];
-      pair_divide<NT, R0>(y, dummy, true, stw, 0, 0, ba, bb, hin);
+      pair_divide<NT, R0, K1Form<NL>::BDF>(y, dummy, true, stw, 0, 0, ba, bb, hin);
       DFT<R0, -1>::run(y);
     } else {
 #pragma unroll
@@ -305,7 +347,7 @@ __global__ void __launch_bounds__(EXPD_K1_THREADS, EXPD_K1_MINB) k_time_fused(co
         DFT<RL, +1>::run(va);
         DFT<RL, +1>::run(vb);
         const double2 Ep = jpair < a.npairs ? ld2(a.E + 2 * jpair) : make_double2(0.0, 0.0);
-        pair_divide<NT, RL>(va, vb, pj == 0, stw, ja, jb, a.a1 * Ep.x, a.a1 * Ep.y, hin);
+        pair_divide<NT, RL, K1Form<NL>::BDF>(va, vb, pj == 0, stw, ja, jb, a.a1 * Ep.x, a.a1 * Ep.y, hin);
         DFT<RL, -1>::run(va);
         DFT<RL, -1>::run(vb);
 #pragma unroll
@@ -603,10 +645,10 @@ struct TmaLayout {
   using G = TGeo<NT, THR>;
   static constexpr int S = G::S;
   static constexpr int TILE = NT * S;                  // double2 per staged array
-  static constexpr int NARR = 1 + (NL ? 1 : 0);
+  static constexpr int NARR = 1 + (K1Form<NL>::HASN ? 1 : 0);
   static constexpr int AUX = 4 * S;                    // E, C1, C2, u0-hat per pair
   static constexpr int STAGE = ((NARR * TILE + AUX) + 7) / 8 * 8;  // 128-byte multiple
-  static constexpr bool ALIAS = NL != 0;               // buf0 in the stage's N-hat block
+  static constexpr bool ALIAS = K1Form<NL>::HASN;      // buf0 in the stage's N-hat block
   static constexpr int FFTBUF = ALIAS ? TILE : 2 * TILE;
   static constexpr size_t BYTES =
       128 + sizeof(double2) * ((size_t)NST * STAGE + FFTBUF + NT) + sizeof(double) * 2 * NT + 16 * NST;
@@ -622,7 +664,7 @@ __device__ __forceinline__ void tma_tile_issue(const CUtensorMap* mx, const CUte
   if (threadIdx.x == 0) {
     mbar_arrive_expect_tx(bar, (uint32_t)(PL::NARR * TILE * 16));
     tma_load_2d(stage, mx, bar, (int)(2 * S * tile), 0);
-    if constexpr (NL) tma_load_2d(stage + TILE, mn, bar, (int)(2 * S * tile), 0);
+    if constexpr (K1Form<NL>::HASN) tma_load_2d(stage + TILE, mn, bar, (int)(2 * S * tile), 0);
   }
   if (threadIdx.x < S) {
     const int s = threadIdx.x;
@@ -631,7 +673,7 @@ __device__ __forceinline__ void tma_tile_issue(const CUtensorMap* mx, const CUte
     const long off = 2 * (ok ? pair : 0);
     double2* aux = stage + PL::NARR * TILE;
     cpa16(aux + s, a.E + off, ok);
-    if constexpr (NL >= 1) cpa16(aux + S + s, a.C1 + off, ok);
+    if constexpr (K1Form<NL>::HASN) cpa16(aux + S + s, a.C1 + off, ok);
     if constexpr (NL == 2) cpa16(aux + 2 * S + s, a.C2 + off, ok);
     if constexpr (RM == RM_RESID) cpa16(aux + 3 * S + s, a.u0h + off, ok);
   }
@@ -666,7 +708,7 @@ __global__ void __launch_bounds__(THR, (TmaLayout<NT, THR, NL, NST>::MINB))
   }
   if (tid == 0) {
     prefetch_tmap(&mx);
-    if constexpr (NL) prefetch_tmap(&mn);
+    if constexpr (K1Form<NL>::HASN) prefetch_tmap(&mn);
     for (int k = 0; k < NST; ++k) mbar_init(&bar[k], 1);
     mbar_fence_init();
   }
@@ -721,7 +763,7 @@ __global__ void __launch_bounds__(THR, (TmaLayout<NT, THR, NL, NST>::MINB))
     double2 y[R0];
     double2 xv[OUTM == OUT_UPDATE ? R0 : 1];  // u_t kept in registers for the update
     const double2 Ej = aux[s];
-    const double2 c1 = NL >= 1 ? aux[S + s] : make_double2(0.0, 0.0);
+    const double2 c1 = K1Form<NL>::HASN ? aux[S + s] : make_double2(0.0, 0.0);
     const double2 c2 = NL == 2 ? aux[2 * S + s] : make_double2(0.0, 0.0);
 #pragma unroll
     for (int r = 0; r < R0; ++r) {
@@ -731,11 +773,17 @@ __global__ void __launch_bounds__(THR, (TmaLayout<NT, THR, NL, NST>::MINB))
       double2 rr;
       if constexpr (RM == RM_INPUT) {
         rr = xc;
+      } else if constexpr (K1Form<NL>::BDF) {
+        const double2 zero = make_double2(0.0, 0.0);
+        const double2 xm1 = t >= 1 ? X[(t - 1) * S + s] : zero;
+        const double2 xm2 = t >= 2 ? X[(t - 2) * S + s] : zero;
+        const double2 u0 = RM == RM_RESID ? aux[3 * S + s] : zero;
+        rr = bdf2_form<RM == RM_RESID>(Ej, xc, xm1, xm2, u0, t);
       } else {
         const double2 prev = t > 0 ? X[(t - 1) * S + s] : (RM == RM_RESID ? aux[3 * S + s] : make_double2(0.0, 0.0));
         if constexpr (RM == RM_RESID) {
           rr = make_double2(fma(Ej.x, prev.x, -xc.x), fma(Ej.y, prev.y, -xc.y));
-          if constexpr (NL >= 1) {
+          if constexpr (K1Form<NL>::HASN) {
             const double2 nm1 = NH[t * S + s];
             rr.x = fma(c1.x, nm1.x, rr.x);
             rr.y = fma(c1.y, nm1.y, rr.y);
@@ -788,7 +836,7 @@ __global__ void __launch_bounds__(THR, (TmaLayout<NT, THR, NL, NST>::MINB))
       DFT<RL, +1>::run(va);
       DFT<RL, +1>::run(vb);
       const double2 Ep = aux[ps];
-      pair_divide<NT, RL>(va, vb, pj == 0, stw, ja, jb, a.a1 * Ep.x, a.a1 * Ep.y, hin);
+      pair_divide<NT, RL, K1Form<NL>::BDF>(va, vb, pj == 0, stw, ja, jb, a.a1 * Ep.x, a.a1 * Ep.y, hin);
       DFT<RL, -1>::run(va);
       DFT<RL, -1>::run(vb);
 #pragma unroll
@@ -905,7 +953,7 @@ static cudaError_t launch_tma(const TimeArgs& a, int grid, cudaStream_t st) {
                                (unsigned long long)a.npad * 8, 2 * S, NT);
   if (e != cudaSuccess) return e;
   mn = mx;
-  if (NL && (e = make_tmap_2d(&mn, a.Nh, (unsigned long long)a.npad, (unsigned long long)a.nt,
+  if (K1Form<NL>::HASN && (e = make_tmap_2d(&mn, a.Nh, (unsigned long long)a.npad, (unsigned long long)a.nt,
                               (unsigned long long)a.npad * 8, 2 * S, NT)) != cudaSuccess)
     return e;
   // the caller's grid (time_fused_grid) is also the number of partial sums it reduces
@@ -915,7 +963,13 @@ static cudaError_t launch_tma(const TimeArgs& a, int grid, cudaStream_t st) {
 
 template <int NT, int RM, int OUTM, int NL>
 static cudaError_t launch_t(const TimeArgs& a, int grid, cudaStream_t st) {
-  if constexpr (TimeGeo<NT>::L > 1) {
+  if constexpr (TimeGeo<NT>::L > 1 && NL == 3) {  // BDF2: TMA kernel, or the register kernel
+    if (pipe_mode() == 3) {
+      if (k1_variant() == 1282) return launch_tma<NT, RM, OUTM, NL, 128, 2>(a, grid, st);
+      if (k1_variant() == 2561) return launch_tma<NT, RM, OUTM, NL, 256, 1>(a, grid, st);
+      return launch_tma<NT, RM, OUTM, NL, 256, 2>(a, grid, st);
+    }
+  } else if constexpr (TimeGeo<NT>::L > 1) {
     if (pipe_mode() == 3) {
       if (k1_variant() == 1282) return launch_tma<NT, RM, OUTM, NL, 128, 2>(a, grid, st);
       if (k1_variant() == 2561) return launch_tma<NT, RM, OUTM, NL, 256, 1>(a, grid, st);
@@ -938,6 +992,13 @@ static cudaError_t launch_t(const TimeArgs& a, int grid, cudaStream_t st) {
 
 template <int NT>
 static cudaError_t dispatch_nt(const TimeArgs& a, int rm, int om, int nl, int grid, cudaStream_t st) {
+  if (nl == 3) {  // BDF2 system (linear)
+    if (rm == RM_RESID && om == OUT_UPDATE) return launch_t<NT, RM_RESID, OUT_UPDATE, 3>(a, grid, st);
+    if (rm == RM_RESID && om == OUT_S) return launch_t<NT, RM_RESID, OUT_S, 3>(a, grid, st);
+    if (rm == RM_INPUT && om == OUT_S) return launch_t<NT, RM_INPUT, OUT_S, 3>(a, grid, st);
+    if (rm == RM_QOP && om == OUT_S) return launch_t<NT, RM_QOP, OUT_S, 3>(a, grid, st);
+    return cudaErrorInvalidValue;
+  }
   if (rm == RM_RESID && om == OUT_UPDATE) {
     if (nl == 0) return launch_t<NT, RM_RESID, OUT_UPDATE, 0>(a, grid, st);
     if (nl == 1) return launch_t<NT, RM_RESID, OUT_UPDATE, 1>(a, grid, st);
@@ -1025,7 +1086,12 @@ __global__ void __launch_bounds__(256) k_resid_only(const TimeArgs a) {
     double2 cur = ld2(a.X + (long)t * a.npad + base);
     double2 prev = t > 0 ? ld2(a.X + (long)(t - 1) * a.npad + base) : ld2(a.u0h + base);
     double2 r = make_double2(fma(E.x, prev.x, -cur.x), fma(E.y, prev.y, -cur.y));
-    if constexpr (NL >= 1) {
+    if constexpr (NL == 3) {  // BDF2: f2 - R v
+      const double2 zero = make_double2(0.0, 0.0);
+      const double2 xm2 = t >= 2 ? ld2(a.X + (long)(t - 2) * a.npad + base) : zero;
+      r = bdf2_form<true>(E, cur, t >= 1 ? prev : zero, xm2, ld2(a.u0h + base), t);
+    }
+    if constexpr (K1Form<NL>::HASN) {
       double2 c1 = ld2(a.C1 + base), nm1 = ld2(a.Nh + (long)t * a.npad + base);
       r.x = fma(c1.x, nm1.x, r.x);
       r.y = fma(c1.y, nm1.y, r.y);
@@ -1052,6 +1118,7 @@ __global__ void __launch_bounds__(256) k_resid_only(const TimeArgs a) {
 cudaError_t launch_resid_only(const TimeArgs& a, int nl, int grid, cudaStream_t st) {
   if (nl == 0) k_resid_only<0><<<grid, 256, 0, st>>>(a);
   else if (nl == 1) k_resid_only<1><<<grid, 256, 0, st>>>(a);
+  else if (nl == 3) k_resid_only<3><<<grid, 256, 0, st>>>(a);
   else k_resid_only<2><<<grid, 256, 0, st>>>(a);
   return cudaGetLastError();
 }

@@ -71,6 +71,10 @@ CONFIGS = {
     # NEXT-1: the paper's own nonlinear iteration -- IF scheme (6.1) solved by
     # the IMEX-type Exp-ParaDiag iteration (7.2)/(7.3) -- on the
     # c3 and c5 problems (not BASELINE.json configs)
+    # NEXT-2: the exponential BDF2 all-at-once system (4.1)-(4.5)
+    # on the c1 / c2 problems (linear; nt unknowns u_2..u_{nt+1})
+    "c1bdf2": Config("c1bdf2", 1, 63, 1.0, 1.0, 1.0, 32, 1e-2, scheme=3, solvers=("fixed_point", "gmres"), seed=1),
+    "c2bdf2": Config("c2bdf2", 2, 255, 0.5, 1.0, 1.0, 64, 1e-3, scheme=3, solvers=("fixed_point", "gmres"), seed=2),
     "c3if": Config("c3if", 2, 511, 1.0, 1.0, 0.5, 128, 1e-3, scheme=2, q=CUBIC, seed=3),
     "c5if": Config("c5if", 2, 2047, 0.1, 0.5, 1.0, 256, 1e-3, scheme=2, q=CUBIC, seed=5),
 }

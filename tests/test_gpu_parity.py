@@ -129,6 +129,7 @@ def test_sweep_full_size_sampled(orc):
 # preconditioner apply (Steps (a)-(c)) and residual
 # ------------------------------------------------------------------------------------------
 PRECOND_CASES = [
+    ("c1bdf2", None, None), ("c2bdf2", 31, 64),  # NEXT-2: BDF2 divisor
     ("c1", None, None),
     ("c2", 31, 64),
     ("c3", 31, 128),
@@ -153,7 +154,8 @@ def test_precond_apply_parity(orc, name, n, nt):
 
 
 @pytest.mark.parametrize("name,n,nt", [("c1", None, None), ("c2", 31, 64), ("c3", 31, 128), ("c4", 7, 64),
-                                       ("c5", 31, 256), ("c5", 7, 4), ("c5if", 31, 256), ("c3if", 255, 8)])
+                                       ("c5", 31, 256), ("c5", 7, 4), ("c5if", 31, 256), ("c3if", 255, 8),
+                                       ("c1bdf2", None, None), ("c2bdf2", 31, 64)])
 def test_residual_parity(orc, name, n, nt):
     cfg = synth.CONFIGS[name] if n is None else cfg_small(name, n, nt)
     plan = Plan(Problem.from_config(cfg))
@@ -183,7 +185,9 @@ def test_precond_zero_and_alias(orc):
 SOLVE_CASES = [("c1", None, None), ("c2", 63, 64), ("c3", 63, 128), ("c5", 63, 256), ("c4", 15, 64),
                ("c3", 255, 16), ("c5", 255, 16),
                # NEXT-1: IF scheme (6.1) by the IMEX-type iteration (7.2)
-               ("c3if", 63, 128), ("c5if", 63, 256), ("c5if", 255, 16)]
+               ("c3if", 63, 128), ("c5if", 63, 256), ("c5if", 255, 16),
+               # NEXT-2: the BDF2 system (4.2) by Richardson (4.4)
+               ("c1bdf2", None, None), ("c2bdf2", 63, 64)]
 
 
 @pytest.mark.parametrize("name,n,nt", SOLVE_CASES)
@@ -201,7 +205,8 @@ def test_fixed_point_parity(orc, name, n, nt):
     assert np.allclose(h[big], hist[big], rtol=1e-6)
 
 
-@pytest.mark.parametrize("name,n,nt", [("c1", None, None), ("c2", 63, 64), ("c4", 15, 64)])
+@pytest.mark.parametrize("name,n,nt", [("c1", None, None), ("c2", 63, 64), ("c4", 15, 64), ("c1bdf2", None, None),
+                                       ("c2bdf2", 63, 64)])
 def test_gmres_parity(orc, name, n, nt):
     cfg = synth.CONFIGS[name] if n is None else cfg_small(name, n, nt)
     plan = Plan(Problem.from_config(cfg), krylov_vectors=21)
@@ -261,7 +266,7 @@ def test_dist1_fixed_point_parity(orc, comm1, name, n, nt):
     assert relmax(H(U), Uo) < 1e-9
 
 
-@pytest.mark.parametrize("name,n,nt", [("c2", 63, 64), ("c4", 15, 64)])
+@pytest.mark.parametrize("name,n,nt", [("c2", 63, 64), ("c4", 15, 64), ("c2bdf2", 63, 64)])
 def test_dist1_gmres_parity(orc, comm1, name, n, nt):
     cfg = cfg_small(name, n, nt)
     plan = Plan(Problem.from_config(cfg), krylov_vectors=21, comm=comm1)
