@@ -143,6 +143,14 @@ expd_status expd_fixed_point_solve(expd_plan* plan, const double* u0, double* U,
 expd_status expd_gmres_solve(expd_plan* plan, const double* u0, double* U, double tol, int restart, int maxit,
                              expd_report* report);
 
+/* Left-preconditioned BiCGStab on Q_alpha^{-1} Q u = Q_alpha^{-1} f (PAPER.md:1088-1114,
+   the paper's other Krylov method; reading R17): the preconditioned residual is iterated,
+   stop when its norm relative to the initial one is < tol (also after the half step).
+   Linear problems only; the workspace must hold >= 6 Krylov vectors.  iterations = BiCGStab
+   steps (2 fused K1 passes each).  Blocking. */
+expd_status expd_bicgstab_solve(expd_plan* plan, const double* u0, double* U, double tol, int maxit,
+                                expd_report* report);
+
 /* ---- multi-GPU ---------------------------------------------------------------------- */
 /* The rank's slabs; INVALID_ARG when nt % nranks != 0 or there are fewer x-lines than ranks.
    Pure host computation (no device needed). */

@@ -102,6 +102,7 @@ def lib():
             "orc_precond": (C.c_double, [pp, dp, dp]),
             "orc_fixed_point": (C.c_int, [pp, dp, dp, C.c_double, C.c_int, dp, C.POINTER(C.c_int)]),
             "orc_gmres": (C.c_int, [pp, dp, dp, C.c_double, C.c_int, C.c_int, dp, C.POINTER(C.c_int)]),
+            "orc_bicgstab": (C.c_int, [pp, dp, dp, C.c_double, C.c_int, dp, C.POINTER(C.c_int)]),
             "orc_mode_residual": (None, [pp, C.c_long, dp, C.c_double, dp, dp]),
             "orc_dst_sample_batch": (None, [pp, dp, C.c_long, C.POINTER(C.c_long), C.c_int, dp]),
             "orc_dst_x_rows": (None, [pp, dp, C.c_long, dp]),
@@ -249,6 +250,16 @@ def gmres(s: Spec, u0, U=None, tol=1e-12, restart=20, maxit=100):
     its = C.c_int()
     p = s.c_struct()
     st = lib().orc_gmres(C.byref(p), _p(u0), _p(U), tol, restart, maxit, _p(hist), C.byref(its))
+    return U, st, its.value, hist[: its.value + 1].copy()
+
+
+def bicgstab(s: Spec, u0, U=None, tol=1e-12, maxit=100):
+    u0 = _f64(u0)
+    U = np.zeros((s.nt,) + u0.shape) if U is None else _f64(U).copy()
+    hist = np.zeros(maxit + 1)
+    its = C.c_int()
+    p = s.c_struct()
+    st = lib().orc_bicgstab(C.byref(p), _p(u0), _p(U), tol, maxit, _p(hist), C.byref(its))
     return U, st, its.value, hist[: its.value + 1].copy()
 
 

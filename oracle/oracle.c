@@ -818,6 +818,77 @@ int orc_gmres(const orc_problem* p, const double* u0, double* U, double tol, int
 /* ------------------------------------------------------------------------------------ */
 /* per-spectral-mode versions (sampled checks at full size)                              */
 /* ------------------------------------------------------------------------------------ */
+/* Left-preconditioned BiCGStab (van der Vorst) on Q_alpha^{-1} Q x = Q_alpha^{-1} f from
+   x_0 = U (zeros), PAPER.md:1088-1114 ("preconditioned BiCGStab" with the same
+   preconditioner), reading R17: the preconditioned residual r = Q_alpha^{-1}(f - Q x) is
+   iterated and the stop is ||r|| / ||r_0|| < tol, also tested after the half step (s);
+   iterations = BiCGStab steps (two operator applications each).  Linear problems. */
+static ld dot_ld(const ld* a, const ld* b, size_t len) {
+  ld s = 0.0L;
+  for (size_t i = 0; i < len; ++i) s += a[i] * b[i];
+  return s;
+}
+int orc_bicgstab(const orc_problem* p, const double* u0, double* U, double tol, int maxit, double* hist,
+                 int* iterations) {
+  if (p->npoly > 0) return 2;
+  ctx_t c;
+  ctx_init(&c, p);
+  size_t N = (size_t)c.N, tot = N * (size_t)p->nt;
+  ld* u0l = (ld*)malloc(sizeof(ld) * N);
+  ld* x = (ld*)malloc(sizeof(ld) * tot);
+  ld* r = (ld*)malloc(sizeof(ld) * tot);
+  ld* rh = (ld*)malloc(sizeof(ld) * tot);
+  ld* pv = (ld*)calloc(tot, sizeof(ld));
+  ld* v = (ld*)calloc(tot, sizeof(ld));
+  ld* s = (ld*)malloc(sizeof(ld) * tot);
+  ld* t = (ld*)malloc(sizeof(ld) * tot);
+  ld* w = (ld*)malloc(sizeof(ld) * tot);
+  for (size_t i = 0; i < N; ++i) u0l[i] = u0[i];
+  for (size_t i = 0; i < tot; ++i) x[i] = U[i];
+  residual_ld(&c, u0l, x, w); /* f - Q x */
+  precond_ld(&c, w, r);       /* r_0 */
+  memcpy(rh, r, sizeof(ld) * tot);
+  ld beta0 = sqrtl(norm2_ld(r, tot));
+  if (hist) hist[0] = 1.0;
+  int status = 7, its = 0;
+  ld rho_prev = 1.0L, al = 1.0L, om = 1.0L;
+  if (beta0 == 0.0L) status = 0;
+  for (int i = 0; status != 0 && i < maxit; ++i) {
+    ld rho = dot_ld(rh, r, tot);
+    ld beta = (rho / rho_prev) * (al / om);
+    for (size_t q = 0; q < tot; ++q) pv[q] = r[q] + beta * (pv[q] - om * v[q]);
+    apply_Qcorner_ld(&c, 0.0L, pv, w);
+    precond_ld(&c, w, v); /* v = Q_a^{-1} Q p */
+    al = rho / dot_ld(rh, v, tot);
+    for (size_t q = 0; q < tot; ++q) s[q] = r[q] - al * v[q];
+    ld sn = sqrtl(norm2_ld(s, tot));
+    if (sn / beta0 < (ld)tol) { /* half step */
+      for (size_t q = 0; q < tot; ++q) x[q] += al * pv[q];
+      its = i + 1;
+      if (hist) hist[its] = (double)(sn / beta0);
+      status = 0;
+      break;
+    }
+    apply_Qcorner_ld(&c, 0.0L, s, w);
+    precond_ld(&c, w, t); /* t = Q_a^{-1} Q s */
+    om = dot_ld(t, s, tot) / dot_ld(t, t, tot);
+    for (size_t q = 0; q < tot; ++q) {
+      x[q] += al * pv[q] + om * s[q];
+      r[q] = s[q] - om * t[q];
+    }
+    rho_prev = rho;
+    its = i + 1;
+    ld rn = sqrtl(norm2_ld(r, tot));
+    if (hist) hist[its] = (double)(rn / beta0);
+    if (rn / beta0 < (ld)tol) { status = 0; break; }
+  }
+  if (iterations) *iterations = its;
+  for (size_t i = 0; i < tot; ++i) U[i] = (double)x[i];
+  free(u0l); free(x); free(r); free(rh); free(pv); free(v); free(s); free(t); free(w);
+  ctx_free(&c);
+  return status;
+}
+
 void orc_mode_residual(const orc_problem* p, long J, const double* uhat, double uhat0, const double* nhat,
                        double* rhat) {
   ld E, f1, f2;

@@ -89,6 +89,11 @@ int orc_fixed_point(const orc_problem* p, const double* u0, double* U, double to
 int orc_gmres(const orc_problem* p, const double* u0, double* U, double tol, int restart, int maxit,
               double* hist, int* iterations);
 
+/* Left-preconditioned BiCGStab on Q_alpha^{-1} Q (reading R17): same
+   contract as orc_gmres (hist[k] = relative preconditioned residual after step k). */
+int orc_bicgstab(const orc_problem* p, const double* u0, double* U, double tol, int maxit, double* hist,
+                 int* iterations);
+
 /* Per-spectral-mode versions (sampled full-size parity; reading R4: in the DST basis
    Step (b) is the divide by 1 - lambda_k E_J).
    uhat: [nt] (u_1..u_Nt of mode J), uhat0 = u_0 of mode J,

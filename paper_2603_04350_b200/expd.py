@@ -39,6 +39,7 @@ EXPORTS = [
     "expd_precond_apply",
     "expd_fixed_point_solve",
     "expd_gmres_solve",
+    "expd_bicgstab_solve",
     "expd_load_state",
     "expd_sweep",
     "expd_sweep_norm2",
@@ -121,6 +122,7 @@ def load_library(path: str = LIB_PATH):
         "expd_precond_apply": (C.c_int, [vp, vp, vp]),
         "expd_fixed_point_solve": (C.c_int, [vp, vp, vp, C.c_double, C.c_int, C.POINTER(_Report)]),
         "expd_gmres_solve": (C.c_int, [vp, vp, vp, C.c_double, C.c_int, C.c_int, C.POINTER(_Report)]),
+        "expd_bicgstab_solve": (C.c_int, [vp, vp, vp, C.c_double, C.c_int, C.POINTER(_Report)]),
         "expd_load_state": (C.c_int, [vp, vp, vp]),
         "expd_sweep": (C.c_int, [vp]),
         "expd_sweep_norm2": (C.c_int, [vp, dp]),
@@ -351,6 +353,14 @@ class Plan:
         U = self._vec().zero_() if U is None else U
         r, hist = self._report(maxit)
         st = self.lib.expd_gmres_solve(self.handle, _ptr(u0), _ptr(U), tol, restart, maxit, C.byref(r))
+        if st not in (EXPD_OK, 7):
+            self._check(st)
+        return U, self._rdict(r, hist, st)
+
+    def bicgstab_solve(self, u0, U=None, tol=1e-12, maxit=100):
+        U = self._vec().zero_() if U is None else U
+        r, hist = self._report(maxit)
+        st = self.lib.expd_bicgstab_solve(self.handle, _ptr(u0), _ptr(U), tol, maxit, C.byref(r))
         if st not in (EXPD_OK, 7):
             self._check(st)
         return U, self._rdict(r, hist, st)

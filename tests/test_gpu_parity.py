@@ -218,6 +218,31 @@ def test_gmres_parity(orc, name, n, nt):
     assert relmax(H(U), Uo) < 1e-9
 
 
+@pytest.mark.parametrize("name,n,nt", [("c1", None, None), ("c2", 63, 64), ("c4", 15, 64), ("c2bdf2", 63, 64)])
+def test_bicgstab_parity(orc, name, n, nt):
+    cfg = synth.CONFIGS[name] if n is None else cfg_small(name, n, nt)
+    plan = Plan(Problem.from_config(cfg), krylov_vectors=6)
+    u0 = synth.initial_condition(cfg)
+    U, rep = plan.bicgstab_solve(T(u0), tol=cfg.tol, maxit=50)
+    Uo, st, its, hist = orc.bicgstab(orc.spec(cfg), u0, tol=cfg.tol, maxit=50)
+    assert st == 0 and rep["converged"]
+    assert rep["iterations"] == its
+    assert relmax(H(U), Uo) < 1e-9
+
+
+def test_bicgstab_slow_convergence_matches_oracle(orc):
+    # alpha = 0.2 on a slowly decaying problem: several BiCGStab steps
+    cfg = synth.Config("b", 1, 15, 0.05, 0.0, 0.5, 16, 0.2)
+    plan = Plan(Problem.from_config(cfg), krylov_vectors=6)
+    u0 = np.random.default_rng(3).standard_normal(15)
+    U, rep = plan.bicgstab_solve(T(u0), tol=1e-12, maxit=60)
+    Uo, st, its, hist = orc.bicgstab(orc.spec(cfg), u0, tol=1e-12, maxit=60)
+    assert rep["iterations"] == its and its >= 3
+    h = np.array(rep["hist"])
+    assert np.allclose(h[hist > 1e-9], hist[hist > 1e-9], rtol=1e-6)
+    assert relmax(H(U), Uo) < 1e-9
+
+
 def test_gmres_small_restart_matches_oracle(orc):
     cfg = synth.Config("g", 1, 15, 0.05, 0.0, 0.5, 16, 0.2)
     plan = Plan(Problem.from_config(cfg), krylov_vectors=3)
@@ -262,6 +287,17 @@ def test_dist1_fixed_point_parity(orc, comm1, name, n, nt):
     u0 = synth.initial_condition(cfg)
     U, rep = plan.fixed_point_solve(T(u0), tol=cfg.tol, maxit=50)
     Uo, st, its, hist = orc.fixed_point(orc.spec(cfg), u0, tol=cfg.tol, maxit=50)
+    assert st == 0 and rep["converged"] and rep["iterations"] == its
+    assert relmax(H(U), Uo) < 1e-9
+
+
+@pytest.mark.parametrize("name,n,nt", [("c2", 63, 64), ("c4", 15, 64), ("c2bdf2", 63, 64)])
+def test_dist1_bicgstab_parity(orc, comm1, name, n, nt):
+    cfg = cfg_small(name, n, nt)
+    plan = Plan(Problem.from_config(cfg), krylov_vectors=6, comm=comm1)
+    u0 = synth.initial_condition(cfg)
+    U, rep = plan.bicgstab_solve(T(u0), tol=cfg.tol, maxit=50)
+    Uo, st, its, hist = orc.bicgstab(orc.spec(cfg), u0, tol=cfg.tol, maxit=50)
     assert st == 0 and rep["converged"] and rep["iterations"] == its
     assert relmax(H(U), Uo) < 1e-9
 
