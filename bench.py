@@ -321,13 +321,18 @@ def run_ours(args):
         f_t = dst_flops_per_line_pair(M) * pairs                      # one axis transform
         f_nl = 2 * f_t + 3.0 * 2 * M * pairs                          # [V, N, V], cubic N
         fam = {}
+        try:
+            tprof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        except Exception:
+            tprof = {}
         for which, label, flops, per_step in ((4, "line_x", f_t, 2), (6, "line_y_nl", f_nl, 1)):
             ms_l = plan.debug_kernel_ms(which, ns, 5)
             tf = flops / (ms_l * 1e-3) / 1e12
             fam[label] = {"bound": "alu", "kernel": f"k_line ({label}: {'x-axis DST-I' if which == 4 else 'fused y [V, N(u), V]'})",
                           "achieved": tf, "peak": FP64_PEAK_TFLOPS,
                           "peak_source": "measured DFMA loop (profiles/r01_probe_fp64_hbm.txt)", "unit": "TFLOP/s",
-                          "frac": tf / FP64_PEAK_TFLOPS, "traffic": None, "algorithmic_flops_per_launch": flops,
+                          "frac": tf / FP64_PEAK_TFLOPS, "traffic": tprof.get(f"{cfg.name}:{label}"),
+                          "algorithmic_flops_per_launch": flops,
                           "launch_ms": ms_l, "slices_per_launch": ns,
                           "ms_per_step": ms_l * per_step * (cfg.nt - 1) / ns}
         kernels.update(fam)
