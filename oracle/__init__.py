@@ -18,6 +18,7 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "oracle.c")
+_SRCS = [_SRC, os.path.join(_HERE, "oracle_cplx.c")]
 _LIB = os.path.join(_HERE, "liboracle.so")
 
 CFLAGS = ["-O2", "-fopenmp", "-ffp-contract=off", "-fPIC", "-shared", "-std=c11"]
@@ -26,9 +27,9 @@ CFLAGS = ["-O2", "-fopenmp", "-ffp-contract=off", "-fPIC", "-shared", "-std=c11"
 def build(force: bool = False) -> str:
     """Compile oracle.c -> liboracle.so (gcc, no FFT/BLAS, -ffp-contract=off)."""
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < max(
-        os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "oracle.h"))
+        *(os.path.getmtime(f) for f in _SRCS), os.path.getmtime(os.path.join(_HERE, "oracle.h"))
     ):
-        subprocess.check_call(["gcc", *CFLAGS, "-o", _LIB, _SRC, "-lm"])
+        subprocess.check_call(["gcc", *CFLAGS, "-o", _LIB, *_SRCS, "-lm"])
     return _LIB
 
 
@@ -44,6 +45,8 @@ class Problem(C.Structure):
         ("scheme", C.c_int),
         ("npoly", C.c_int),
         ("q", C.c_double * 8),
+        ("a_im", C.c_double),
+        ("c_im", C.c_double),
     ]
 
 
@@ -60,6 +63,12 @@ class Spec:
     alpha: float
     scheme: int = 0  # 0 exponential Euler / ETD1, 1 ETD2
     q: tuple = field(default_factory=tuple)  # N(u) = sum_p q[p] u^p
+    a_im: float = 0.0  # imaginary parts of a and c (complex state; oracle_cplx.c)
+    c_im: float = 0.0
+
+    @property
+    def is_complex(self) -> bool:
+        return self.a_im != 0.0 or self.c_im != 0.0
 
     @property
     def dt(self) -> float:
@@ -75,6 +84,7 @@ class Spec:
         p.alpha, p.scheme, p.npoly = self.alpha, self.scheme, len(self.q)
         for i, v in enumerate(self.q):
             p.q[i] = v
+        p.a_im, p.c_im = self.a_im, self.c_im
         return p
 
 
@@ -107,6 +117,12 @@ def lib():
             "orc_dst_sample_batch": (None, [pp, dp, C.c_long, C.POINTER(C.c_long), C.c_int, dp]),
             "orc_dst_x_rows": (None, [pp, dp, C.c_long, dp]),
             "orc_mode_precond": (None, [pp, C.c_long, dp, dp]),
+            "orc_cplx_sequential": (None, [pp, dp, dp]),
+            "orc_cplx_residual": (None, [pp, dp, dp, dp, dp]),
+            "orc_cplx_precond": (None, [pp, dp, dp]),
+            "orc_cplx_apply_Q": (None, [pp, dp, dp]),
+            "orc_cplx_fixed_point": (C.c_int, [pp, dp, dp, C.c_double, C.c_int, dp, C.POINTER(C.c_int)]),
+            "orc_cplx_gmres": (C.c_int, [pp, dp, dp, C.c_double, C.c_int, C.c_int, dp, C.POINTER(C.c_int)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -283,4 +299,70 @@ def mode_precond(s: Spec, J: int, rhat) -> np.ndarray:
 
 def spec(cfg) -> Spec:
     """Spec from any object with the problem fields (e.g. synth.Config)."""
-    return Spec(cfg.dim, cfg.n, cfg.a, cfg.c, cfg.T, cfg.nt, cfg.alpha, cfg.scheme, tuple(cfg.q))
+    return Spec(cfg.dim, cfg.n, cfg.a, cfg.c, cfg.T, cfg.nt, cfg.alpha, cfg.scheme, tuple(cfg.q),
+                getattr(cfg, "a_im", 0.0), getattr(cfg, "c_im", 0.0))
+
+
+# ---- complex coefficients (oracle_cplx.c): complex128 arrays, linear problems only ----------
+
+
+def _c128(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.complex128)
+
+
+def _pc(a: np.ndarray):
+    assert a.dtype == np.complex128 and a.flags.c_contiguous
+    return a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def cplx_sequential(s: Spec, u0) -> np.ndarray:
+    u0 = _c128(u0)
+    U = np.empty((s.nt,) + u0.shape, dtype=np.complex128)
+    p = s.c_struct()
+    lib().orc_cplx_sequential(C.byref(p), _pc(u0), _pc(U))
+    return U
+
+
+def cplx_residual(s: Spec, u0, U):
+    u0, U = _c128(u0), _c128(U)
+    R = np.empty_like(U)
+    r2 = C.c_double()
+    p = s.c_struct()
+    lib().orc_cplx_residual(C.byref(p), _pc(u0), _pc(U), _pc(R), C.byref(r2))
+    return R, r2.value
+
+
+def cplx_precond(s: Spec, R) -> np.ndarray:
+    R = _c128(R)
+    S = np.empty_like(R)
+    p = s.c_struct()
+    lib().orc_cplx_precond(C.byref(p), _pc(R), _pc(S))
+    return S
+
+
+def cplx_apply_Q(s: Spec, V) -> np.ndarray:
+    V = _c128(V)
+    out = np.empty_like(V)
+    p = s.c_struct()
+    lib().orc_cplx_apply_Q(C.byref(p), _pc(V), _pc(out))
+    return out
+
+
+def cplx_fixed_point(s: Spec, u0, U=None, tol=1e-12, maxit=100):
+    u0 = _c128(u0)
+    U = np.zeros((s.nt,) + u0.shape, dtype=np.complex128) if U is None else _c128(U).copy()
+    hist = np.zeros(maxit + 1)
+    its = C.c_int()
+    p = s.c_struct()
+    st = lib().orc_cplx_fixed_point(C.byref(p), _pc(u0), _pc(U), tol, maxit, _p(hist), C.byref(its))
+    return U, st, its.value, hist[: its.value + 1].copy()
+
+
+def cplx_gmres(s: Spec, u0, U=None, tol=1e-12, restart=20, maxit=100):
+    u0 = _c128(u0)
+    U = np.zeros((s.nt,) + u0.shape, dtype=np.complex128) if U is None else _c128(U).copy()
+    hist = np.zeros(maxit + 1)
+    its = C.c_int()
+    p = s.c_struct()
+    st = lib().orc_cplx_gmres(C.byref(p), _pc(u0), _pc(U), tol, restart, maxit, _p(hist), C.byref(its))
+    return U, st, its.value, hist[: its.value + 1].copy()

@@ -36,6 +36,7 @@ typedef struct {
                     *    nt unknowns u_2..u_{nt+1}, u_1 = A u_0 (reading R16)           */
   int npoly;       /* N(u) = sum_{p<npoly} q[p] u^p ; 0 = linear                   */
   double q[8];
+  double a_im, c_im; /* imaginary parts of a and c (oracle_cplx.c only; 0 elsewhere)   */
 } orc_problem;
 
 long orc_nmodes(const orc_problem* p);
@@ -101,6 +102,17 @@ int orc_bicgstab(const orc_problem* p, const double* u0, double* U, double tol, 
 void orc_mode_residual(const orc_problem* p, long J, const double* uhat, double uhat0, const double* nhat,
                        double* rhat);
 void orc_mode_precond(const orc_problem* p, long J, const double* rhat, double* shat);
+
+/* ---- complex coefficients (oracle_cplx.c), linear only (npoly = 0, scheme 0) ----------
+ * Complex vectors are interleaved (re, im) doubles, same slice/time layout as above.     */
+void orc_cplx_sequential(const orc_problem* p, const double* u0, double* U);
+void orc_cplx_residual(const orc_problem* p, const double* u0, const double* U, double* R, double* rnorm2);
+void orc_cplx_precond(const orc_problem* p, const double* R, double* S);
+void orc_cplx_apply_Q(const orc_problem* p, const double* V, double* out);
+int orc_cplx_fixed_point(const orc_problem* p, const double* u0, double* U, double tol, int maxit, double* hist,
+                         int* iterations);
+int orc_cplx_gmres(const orc_problem* p, const double* u0, double* U, double tol, int restart, int maxit,
+                   double* hist, int* iterations);
 
 #ifdef __cplusplus
 }
