@@ -67,6 +67,15 @@ typedef struct {
   expd_scheme scheme;
   int npoly;          /* N(u) = sum_{p < npoly} q[p] u^p; 0 = linear; 0 <= npoly <= 8     */
   double q[8];
+  double a_im, c_im;  /* imaginary parts of a and c (0 for the real problems above).  Either
+                         non-zero makes a COMPLEX plan (the paper's Schroedinger tests, a = i,
+                         c = 2i): u_t = (a Delta - c) u with a = a + i a_im,
+                         c = c + i c_im, Re a >= 0 (a != 0), Re c >= 0; linear only
+                         (npoly = 0), scheme EXPD_EXP_EULER, one GPU (no expd_dist).  Every
+                         space-time / slice argument of a complex plan (u0, U, R, S) is
+                         complex128: interleaved (re, im) doubles, 2 N doubles per slice.
+                         GMRES runs over C with the Hermitian inner product (reading R18);
+                         BiCGStab, expd_dst / expd_nonlin_hat stay real-only.            */
 } expd_problem;
 
 typedef struct {

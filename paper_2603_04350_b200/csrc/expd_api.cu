@@ -7,6 +7,7 @@
 
 #include <chrono>
 #include <cmath>
+#include <complex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -28,7 +29,10 @@ struct expd_plan {
   int sms = 148;
   int nl = 0;      // 0 linear, 1 ETD1 / IF-IMEX, 2 ETD2
   int nshift = 0;  // IF / IMEX-type: K1 reads N-hat of the same slice (one slice later)
-  int k1 = 0;      // K1 form: nl, or 3 for the BDF2 system
+  int k1 = 0;      // K1 form: nl, 3 for the BDF2 system, 4 for complex coefficients
+  bool cx = false; // complex coefficients: spectral entries are (re, im) pairs, mlen = 2 npad
+  std::vector<double> h_Ecx;  // complex E_J table (re, im) [2 npad], long double on the host
+  double *X2 = nullptr, *X3 = nullptr;  // complex plans: planar (re / im) transform staging
   double a1 = 0.0;
   // small device tables owned by the plan
   double* d_lam = nullptr;   // [n]
@@ -117,7 +121,7 @@ static expd_status build_tables(expd_plan* p) {
   CUDA_TRY(p, cudaMalloc(&p->d_ginv, sizeof(double) * nt));
   CUDA_TRY(p, cudaMalloc(&p->d_twM, sizeof(double2) * M));
   CUDA_TRY(p, cudaMalloc(&p->d_sinp, sizeof(double) * M));
-  CUDA_TRY(p, cudaMallocHost(&p->h_pin, sizeof(double) * 256));
+  CUDA_TRY(p, cudaMallocHost(&p->h_pin, sizeof(double) * 512));
   CUDA_TRY(p, cudaMemcpy(p->d_lam, lam.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
   CUDA_TRY(p, cudaMemcpy(p->d_twt, twt.data(), sizeof(double2) * nt, cudaMemcpyHostToDevice));
   CUDA_TRY(p, cudaMemcpy(p->d_g, g.data(), sizeof(double) * nt, cudaMemcpyHostToDevice));
@@ -132,8 +136,13 @@ extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dis
   if (!prob || !out) return EXPD_ERR_INVALID_ARG;
   *out = nullptr;
   const expd_problem& P = *prob;
-  if (P.dim < 1 || P.dim > 3 || P.n < 3 || !is_pow2((long)P.n + 1) || P.n + 1 > 4096 || !(P.a > 0.0) ||
-      !(P.c >= 0.0) || !(P.dt > 0.0) || P.nt < 4 || !is_pow2(P.nt) || !(P.alpha > 0.0) || !(P.alpha <= 1.0) ||
+  const bool cx = P.a_im != 0.0 || P.c_im != 0.0;
+  // real plans: a > 0, c >= 0; complex plans: Re a >= 0, Re c >= 0, a != 0 (|E_J| <= 1)
+  const bool coef_ok = cx ? (P.a >= 0.0 && P.c >= 0.0 && (P.a > 0.0 || P.a_im != 0.0) && std::isfinite(P.a_im) &&
+                             std::isfinite(P.c_im))
+                          : (P.a > 0.0 && P.c >= 0.0);
+  if (P.dim < 1 || P.dim > 3 || P.n < 3 || !is_pow2((long)P.n + 1) || P.n + 1 > 4096 || !coef_ok ||
+      !(P.dt > 0.0) || P.nt < 4 || !is_pow2(P.nt) || !(P.alpha > 0.0) || !(P.alpha <= 1.0) ||
       P.npoly < 0 || P.npoly > 8 ||
       (P.scheme != EXPD_EXP_EULER && P.scheme != EXPD_ETD2 && P.scheme != EXPD_IF_IMEX &&
        P.scheme != EXPD_BDF2) ||
@@ -141,6 +150,8 @@ extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dis
       !std::isfinite(P.a) || !std::isfinite(P.c) || !std::isfinite(P.dt))
     return EXPD_ERR_INVALID_ARG;
   if (P.nt > 256) return EXPD_ERR_UNSUPPORTED;
+  if (cx && (P.npoly > 0 || P.scheme != EXPD_EXP_EULER || (dist && (dist->nranks > 1 || dist->nccl_comm))))
+    return EXPD_ERR_UNSUPPORTED;  // complex plans: linear exponential Euler on one GPU
   int nranks = dist ? dist->nranks : 1;
   if (nranks < 1 || nranks > EXPD_MAX_RANKS || (dist && (dist->rank < 0 || dist->rank >= nranks)))
     return EXPD_ERR_INVALID_ARG;
@@ -171,7 +182,8 @@ extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dis
   // K1 form: 0 linear, 1 one N-hat term (ETD1; IF/IMEX with N of the same slice), 2 ETD2
   p->nl = P.npoly > 0 ? (P.scheme == EXPD_ETD2 ? 2 : 1) : 0;
   p->nshift = (P.npoly > 0 && P.scheme == EXPD_IF_IMEX) ? 1 : 0;
-  p->k1 = P.scheme == EXPD_BDF2 ? 3 : p->nl;  // K1 form (3: the BDF2 system)
+  p->k1 = P.scheme == EXPD_BDF2 ? 3 : (cx ? 4 : p->nl);  // K1 form (3: BDF2 system, 4: complex)
+  p->cx = cx;
   if (cudaSetDevice(device) != cudaSuccess) {
     delete p;
     return EXPD_ERR_CUDA;
@@ -187,7 +199,7 @@ extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dis
     expd_plan_destroy(p);
     return EXPD_ERR_INVALID_ARG;
   }
-  p->mlen = p->L.mode_len[p->L.rank];
+  p->mlen = p->L.mode_len[p->L.rank] * (cx ? 2 : 1);  // doubles per slice of the mode slab
   p->moff = p->L.mode_off[p->L.rank];
   p->ntl = p->L.ntl[p->L.rank];
   p->t0 = p->L.t0[p->L.rank];
@@ -197,6 +209,33 @@ extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dis
     a2a_schedule(p->L, A2A_TIME_TO_MODE, 1, p->t2m1_s, p->t2m1_r);
   }
   p->time_grid = time_fused_grid(P.nt, p->mlen / 2, p->sms, p->nl);
+  if (cx) {
+    // E_J = exp(dt (a mu_J^0 - c)), complex, in long double (the phase dt (Im a mu - Im c) reaches
+    // ~1e5 rad at n = 1023: a double evaluation would lose ~1e-11 of it).  Pads get 0.
+    const int n = P.n, M = n + 1;
+    const long double h = 1.0L / (long double)M;
+    std::vector<long double> lam(n);
+    for (int j = 1; j <= n; ++j) {
+      long double sn = sinl(PI_L * (long double)j / (2.0L * (long double)M));
+      lam[j - 1] = -4.0L / (h * h) * sn * sn;
+    }
+    p->h_Ecx.assign(2 * (size_t)npad, 0.0);
+    for (long J = 0; J < npad; ++J) {
+      const int jx = (int)(J % M);
+      if (jx >= n) continue;
+      long r = J / M;
+      long double mu = lam[jx];
+      for (int ax = 1; ax < P.dim; ++ax) {
+        mu += lam[r % n];
+        r /= n;
+      }
+      const long double re = (long double)P.dt * ((long double)P.a * mu - (long double)P.c);
+      const long double im = (long double)P.dt * ((long double)P.a_im * mu - (long double)P.c_im);
+      const long double mag = expl(re);
+      p->h_Ecx[2 * J] = (double)(mag * cosl(im));
+      p->h_Ecx[2 * J + 1] = (double)(mag * sinl(im));
+    }
+  }
   p->vgrid = vec_grid(p->sms);
   *out = p;
   return EXPD_OK;
@@ -204,7 +243,7 @@ extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dis
 
 // workspace layout (every block 256-byte aligned)
 struct Layout {
-  size_t Uh, Nh, T1, UT, NT, u0h, E, C1, C2, scratch, partial, dscal, krylov, total, vec;
+  size_t Uh, Nh, T1, UT, NT, X2, X3, u0h, E, C1, C2, scratch, partial, dscal, krylov, total, vec;
 };
 static Layout layout(const expd_plan* p, int kv) {
   Layout L{};
@@ -214,7 +253,7 @@ static Layout layout(const expd_plan* p, int kv) {
   const size_t nhv = align_up(sizeof(double) * (size_t)(p->prob.nt + ((p->dist || p->nshift) ? 1 : 0)) *
                               (size_t)p->mlen);
   const size_t tsl = p->dist ? align_up(sizeof(double) * (size_t)p->ntl * (size_t)p->g.npad) : 0;
-  const size_t sl = align_up(sizeof(double) * (size_t)p->g.npad);
+  const size_t sl = align_up(sizeof(double) * (size_t)p->g.npad * (p->cx ? 2 : 1));
   size_t off = 0;
   L.vec = vec;
   L.Uh = off; off += vec;
@@ -222,13 +261,15 @@ static Layout layout(const expd_plan* p, int kv) {
   L.T1 = off; off += vec;
   L.UT = off; off += tsl;
   L.NT = off; off += (p->nl ? tsl : 0);
+  L.X2 = off; off += (p->cx ? vec : 0);
+  L.X3 = off; off += (p->cx ? vec : 0);
   L.u0h = off; off += sl;
   L.E = off; off += sl;
   L.C1 = off; off += sl;
   L.C2 = off; off += sl;
   L.scratch = off; off += align_up(sizeof(double) * dst_scratch_doubles(p->g, nonlin_chunk_slices(p->g)));
   L.partial = off; off += align_up(sizeof(double) * 32 * (size_t)(p->sms * 8 + 64));
-  L.dscal = off; off += align_up(sizeof(double) * 256);
+  L.dscal = off; off += align_up(sizeof(double) * 512);
   L.krylov = off; off += (size_t)kv * vec;
   L.total = off;
   return L;
@@ -256,6 +297,8 @@ extern "C" expd_status expd_plan_set_workspace(expd_plan* p, void* d_ptr, size_t
   p->T1 = at(L.T1);
   p->UT = p->dist ? at(L.UT) : nullptr;
   p->NT = (p->dist && p->nl) ? at(L.NT) : nullptr;
+  p->X2 = p->cx ? at(L.X2) : nullptr;
+  p->X3 = p->cx ? at(L.X3) : nullptr;
   p->u0h = at(L.u0h);
   p->E = at(L.E);
   p->C1 = at(L.C1);
@@ -270,8 +313,13 @@ extern "C" expd_status expd_plan_set_workspace(expd_plan* p, void* d_ptr, size_t
     p->sweep_exec = nullptr;
   }
   CUDA_TRY(p, cudaSetDevice(p->device));
-  CUDA_TRY(p, mode_tables(p->g, p->d_lam, p->prob.a, p->prob.c, p->prob.dt, p->prob.scheme, p->E, p->C1, p->C2,
-                          p->stream));
+  if (p->cx)
+    CUDA_TRY(p, cudaMemcpyAsync(p->E, p->h_Ecx.data(), sizeof(double) * p->h_Ecx.size(), cudaMemcpyHostToDevice,
+                                p->stream));
+  else
+    CUDA_TRY(p, mode_tables(p->g, p->d_lam, p->prob.a, p->prob.c, p->prob.dt, p->prob.scheme, p->E, p->C1, p->C2,
+                            p->stream));
+  CUDA_TRY(p, cudaStreamSynchronize(p->stream));  // the host table outlives the copy
   p->tables_ready = true;
   return EXPD_OK;
 }
@@ -346,7 +394,25 @@ static expd_status allreduce(expd_plan* p, double* buf, long count) {
 
 // spectral u0 (full slice, every rank) and (nonlinear) N-hat_0 = V N(u_0) (this rank's
 // mode slab of it in Nh slice 0)
+// complex plans: ns interleaved complex physical slices <-> interleaved complex spectral
+// slices, through the planar staging X3 (physical) / X2 (spectral) and the real DST
+static expd_status cx_phys_to_mode(expd_plan* p, const double* U, double* mode, long ns) {
+  const long N = p->g.N, np = p->g.npad;
+  CUDA_TRY(p, cx_split(U, 2 * N, N, p->X3, N, ns, p->stream));
+  CUDA_TRY(p, dst_slices(p->g, dst_tables(p), p->X3, false, p->X2, true, 2 * ns, p->scratch, p->stream));
+  CUDA_TRY(p, cx_merge(p->X2, np, np, mode, 2 * np, ns, p->stream));
+  return EXPD_OK;
+}
+static expd_status cx_mode_to_phys(expd_plan* p, const double* mode, double* U, long ns) {
+  const long N = p->g.N, np = p->g.npad;
+  CUDA_TRY(p, cx_split(mode, 2 * np, np, p->X2, np, ns, p->stream));
+  CUDA_TRY(p, dst_slices(p->g, dst_tables(p), p->X2, true, p->X3, false, 2 * ns, p->scratch, p->stream));
+  CUDA_TRY(p, cx_merge(p->X3, N, N, U, 2 * N, ns, p->stream));
+  return EXPD_OK;
+}
+
 static expd_status load_u0(expd_plan* p, const double* u0) {
+  if (p->cx) return cx_phys_to_mode(p, u0, p->u0h, 1);
   CUDA_TRY(p, dst_slices(p->g, dst_tables(p), u0, false, p->u0h, true, 1, p->scratch, p->stream));
   if (p->nl) {
     double* full = p->dist ? p->UT : p->Nh;
@@ -361,6 +427,7 @@ static expd_status load_u0(expd_plan* p, const double* u0) {
 
 // physical time-slab slices (the API layout) <-> the spectral mode slab
 static expd_status phys_to_mode(expd_plan* p, const double* U, double* mode) {
+  if (p->cx) return cx_phys_to_mode(p, U, mode, p->prob.nt);
   if (!p->dist) {
     CUDA_TRY(p, dst_slices(p->g, dst_tables(p), U, false, mode, true, p->prob.nt, p->scratch, p->stream));
     return EXPD_OK;
@@ -369,6 +436,7 @@ static expd_status phys_to_mode(expd_plan* p, const double* U, double* mode) {
   return a2a(p, A2A_T2M, p->UT, mode);
 }
 static expd_status mode_to_phys(expd_plan* p, const double* mode, double* U) {
+  if (p->cx) return cx_mode_to_phys(p, mode, U, p->prob.nt);
   if (!p->dist) {
     CUDA_TRY(p, dst_slices(p->g, dst_tables(p), mode, true, U, false, p->prob.nt, p->scratch, p->stream));
     return EXPD_OK;
@@ -495,7 +563,7 @@ extern "C" expd_status expd_precond_apply(expd_plan* p, const double* R, double*
   if (!R || !S) return fail(p, EXPD_ERR_INVALID_ARG, "expd_precond_apply: bad pointers");
   if ((s = phys_to_mode(p, R, p->T1))) return s;
   TimeArgs a = time_args(p, p->T1, p->T1, false);
-  CUDA_TRY(p, launch_time_fused(a, RM_INPUT, OUT_S, p->k1 == 3 ? 3 : 0, p->time_grid, p->stream));
+  CUDA_TRY(p, launch_time_fused(a, RM_INPUT, OUT_S, p->k1 >= 3 ? p->k1 : 0, p->time_grid, p->stream));
   return mode_to_phys(p, p->T1, S);
 }
 
@@ -689,13 +757,60 @@ extern "C" expd_status expd_fixed_point_solve(expd_plan* p, const double* u0, do
   return conv ? EXPD_OK : EXPD_ERR_NOT_CONVERGED;
 }
 
-extern "C" expd_status expd_gmres_solve(expd_plan* p, const double* u0, double* U, double tol, int restart,
-                                        int maxit, expd_report* report) {
-  expd_status s = ready(p);
-  if (s) return s;
-  if (!u0 || !U || maxit < 0 || restart < 1 || !(tol >= 0.0)) return fail(p, EXPD_ERR_INVALID_ARG, "gmres: bad args");
-  if (p->nl) return fail(p, EXPD_ERR_UNSUPPORTED, "GMRES is for linear problems (npoly == 0)");
-  if (p->krylov_cap < 1) return fail(p, EXPD_ERR_OOM, "workspace holds no Krylov vectors");
+// Scalar traits of the GMRES driver: real plans (double) and complex plans (GMRES over C with
+// the Hermitian inner product, reading R18); K = doubles per coefficient on the device.
+template <class T>
+struct Scal;
+template <>
+struct Scal<double> {
+  static constexpr int K = 1;
+  static double conj(double x) { return x; }
+  static double abs(double x) { return std::fabs(x); }
+  static double get(const double* p) { return p[0]; }
+  static void put(double* p, double v) { p[0] = v; }
+  // Givens rotation zeroing b (real, >= 0) under a: returns the new diagonal entry
+  static double givens(double a, double b, double& cs, double& sn) {
+    const double den = std::sqrt(a * a + b * b);
+    cs = den > 0.0 ? a / den : 1.0;
+    sn = den > 0.0 ? b / den : 0.0;
+    return den;
+  }
+};
+template <>
+struct Scal<std::complex<double>> {
+  using C = std::complex<double>;
+  static constexpr int K = 2;
+  static C conj(C x) { return std::conj(x); }
+  static double abs(C x) { return std::abs(x); }
+  static C get(const double* p) { return C(p[0], p[1]); }
+  static void put(double* p, C v) {
+    p[0] = v.real();
+    p[1] = v.imag();
+  }
+  // complex Givens [c s; -conj(s) c], c real: (a, b) -> (c a + s b, 0)
+  static C givens(C a, double b, double& cs, C& sn) {
+    const double aa = std::abs(a), den = std::sqrt(aa * aa + b * b);
+    if (den == 0.0) {
+      cs = 1.0;
+      sn = 0.0;
+    } else if (aa == 0.0) {
+      cs = 0.0;
+      sn = 1.0;
+    } else {
+      cs = aa / den;
+      sn = (a / aa) * (b / den);
+    }
+    return cs * a + sn * b;
+  }
+};
+
+template <class T>
+static expd_status gmres_impl(expd_plan* p, const double* u0, double* U, double tol, int restart, int maxit,
+                              expd_report* report) {
+  using SC = Scal<T>;
+  constexpr int K = SC::K;
+  constexpr bool CX = K == 2;
+  expd_status s;
   const int m = restart < p->krylov_cap ? restart : p->krylov_cap;
   const long len = (long)p->prob.nt * p->mlen;  // this rank's mode slab of a space-time vector
   const size_t vstride = align_up(sizeof(double) * (size_t)len) / sizeof(double);
@@ -704,11 +819,13 @@ extern "C" expd_status expd_gmres_solve(expd_plan* p, const double* u0, double* 
   if (s) return s;
   CUDA_TRY(p, cudaStreamSynchronize(p->stream));
   std::vector<double> hist{1.0};
-  std::vector<double> H((size_t)(m + 1) * m), cs(m), sn(m), gv(m + 1), y(m), hcol(m + 1), h2(m + 1);
+  std::vector<T> H((size_t)(m + 1) * m), sn(m), gv(m + 1), y(m);
+  std::vector<double> cs(m);
   std::vector<const double*> Vp(m + 1);
   double beta0 = -1.0;
   int its = 0, conv = 0;
-  double* dcoef = p->dscal + 128;  // device coefficient scratch (128 doubles)
+  double* dcoef = p->dscal + 128;  // device coefficient scratch: h [0, 40K), h2 [40K, 80K), ||w||^2 at 80K
+  const int O2 = 40 * K, O3 = 80 * K;
   auto t0 = std::chrono::steady_clock::now();
   while (its < maxit) {
     // z = Q_alpha^{-1}(f - Q x)  [K1: residual -> precondition], beta = ||z||
@@ -727,42 +844,37 @@ extern "C" expd_status expd_gmres_solve(expd_plan* p, const double* u0, double* 
       break;
     }
     CUDA_TRY(p, scale_copy(p->T1, 1.0 / beta, Vk(0), len, p->stream));
-    std::fill(gv.begin(), gv.end(), 0.0);
+    std::fill(gv.begin(), gv.end(), T(0.0));
     gv[0] = beta;
     int j = 0, done = 0;
     for (j = 0; j < m && its < maxit; ++j) {
       for (int i = 0; i <= j; ++i) Vp[i] = Vk(i);
       TimeArgs q = time_args(p, Vk(j), p->T1, false);
       CUDA_TRY(p, launch_time_fused(q, RM_QOP, OUT_S, p->k1, p->time_grid, p->stream));  // w = P Q v_j
-      // CGS2: h = V^T w ; w -= V h ; h2 = V^T w ; w -= V h2 ; ||w||^2
+      // CGS2: h = V^H w ; w -= V h ; h2 = V^H w ; w -= V h2 ; ||w||^2
       // (distributed: every partial inner product is completed by an allreduce before use)
-      CUDA_TRY(p, multi_dot(Vp.data(), j + 1, p->T1, len, p->partial, p->vgrid, dcoef, p->stream));
-      if ((s = allreduce(p, dcoef, j + 1))) return s;
-      CUDA_TRY(p, multi_axpy_dot(Vp.data(), j + 1, dcoef, p->T1, len, p->partial, p->vgrid, dcoef + 40, 1,
-                                 p->stream));
-      if ((s = allreduce(p, dcoef + 40, j + 1))) return s;
-      CUDA_TRY(p, multi_axpy_dot(Vp.data(), j + 1, dcoef + 40, p->T1, len, p->partial, p->vgrid, dcoef + 80, 2,
-                                 p->stream));
-      if ((s = allreduce(p, dcoef + 80, 1))) return s;
-      CUDA_TRY(p, cudaMemcpyAsync(p->h_pin, dcoef, sizeof(double) * 81, cudaMemcpyDeviceToHost, p->stream));
+      CUDA_TRY(p, multi_dot(Vp.data(), j + 1, p->T1, len, p->partial, p->vgrid, dcoef, p->stream, CX));
+      if ((s = allreduce(p, dcoef, K * (j + 1)))) return s;
+      CUDA_TRY(p, multi_axpy_dot(Vp.data(), j + 1, dcoef, p->T1, len, p->partial, p->vgrid, dcoef + O2, 1,
+                                 p->stream, CX));
+      if ((s = allreduce(p, dcoef + O2, K * (j + 1)))) return s;
+      CUDA_TRY(p, multi_axpy_dot(Vp.data(), j + 1, dcoef + O2, p->T1, len, p->partial, p->vgrid, dcoef + O3, 2,
+                                 p->stream, CX));
+      if ((s = allreduce(p, dcoef + O3, 1))) return s;
+      CUDA_TRY(p, cudaMemcpyAsync(p->h_pin, dcoef, sizeof(double) * (O3 + 1), cudaMemcpyDeviceToHost, p->stream));
       CUDA_TRY(p, cudaStreamSynchronize(p->stream));
-      for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = p->h_pin[i] + p->h_pin[40 + i];
-      double hn = std::sqrt(p->h_pin[80]);
-      double hsub = hn;
+      for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = SC::get(p->h_pin + K * i) + SC::get(p->h_pin + O2 + K * i);
+      double hn = std::sqrt(p->h_pin[O3]);
       for (int i = 0; i < j; ++i) {
-        double a0 = H[(size_t)i * m + j], b0 = H[(size_t)(i + 1) * m + j];
+        T a0 = H[(size_t)i * m + j], b0 = H[(size_t)(i + 1) * m + j];
         H[(size_t)i * m + j] = cs[i] * a0 + sn[i] * b0;
-        H[(size_t)(i + 1) * m + j] = -sn[i] * a0 + cs[i] * b0;
+        H[(size_t)(i + 1) * m + j] = -SC::conj(sn[i]) * a0 + cs[i] * b0;
       }
-      double a0 = H[(size_t)j * m + j];
-      double den = std::sqrt(a0 * a0 + hsub * hsub);
-      cs[j] = den > 0.0 ? a0 / den : 1.0;
-      sn[j] = den > 0.0 ? hsub / den : 0.0;
-      H[(size_t)j * m + j] = den;
-      gv[j + 1] = -sn[j] * gv[j];
+      H[(size_t)j * m + j] = SC::givens(H[(size_t)j * m + j], hn, cs[j], sn[j]);
+      gv[j + 1] = -SC::conj(sn[j]) * gv[j];
       gv[j] = cs[j] * gv[j];
       ++its;
-      double rel = std::fabs(gv[j + 1]) / beta0;
+      double rel = SC::abs(gv[j + 1]) / beta0;
       hist.push_back(rel);
       if (rel < tol || hn == 0.0) {
         done = 1;
@@ -772,13 +884,16 @@ extern "C" expd_status expd_gmres_solve(expd_plan* p, const double* u0, double* 
       if (j + 1 < m) CUDA_TRY(p, scale_copy(p->T1, 1.0 / hn, Vk(j + 1), len, p->stream));
     }
     for (int i = j - 1; i >= 0; --i) {
-      double sacc = gv[i];
+      T sacc = gv[i];
       for (int l = i + 1; l < j; ++l) sacc -= H[(size_t)i * m + l] * y[l];
       y[i] = sacc / H[(size_t)i * m + i];
     }
-    for (int i = 0; i < j; ++i) Vp[i] = Vk(i);
-    CUDA_TRY(p, cudaMemcpyAsync(dcoef, y.data(), sizeof(double) * j, cudaMemcpyHostToDevice, p->stream));
-    CUDA_TRY(p, lincomb_add(Vp.data(), j, dcoef, p->Uh, len, p->stream));
+    for (int i = 0; i < j; ++i) {
+      Vp[i] = Vk(i);
+      SC::put(p->h_pin + K * i, y[i]);
+    }
+    CUDA_TRY(p, cudaMemcpyAsync(dcoef, p->h_pin, sizeof(double) * K * j, cudaMemcpyHostToDevice, p->stream));
+    CUDA_TRY(p, lincomb_add(Vp.data(), j, dcoef, p->Uh, len, p->stream, CX));
     CUDA_TRY(p, cudaStreamSynchronize(p->stream));
     if (done) {
       conv = 1;
@@ -793,6 +908,17 @@ extern "C" expd_status expd_gmres_solve(expd_plan* p, const double* u0, double* 
   return conv ? EXPD_OK : EXPD_ERR_NOT_CONVERGED;
 }
 
+extern "C" expd_status expd_gmres_solve(expd_plan* p, const double* u0, double* U, double tol, int restart,
+                                        int maxit, expd_report* report) {
+  expd_status s = ready(p);
+  if (s) return s;
+  if (!u0 || !U || maxit < 0 || restart < 1 || !(tol >= 0.0)) return fail(p, EXPD_ERR_INVALID_ARG, "gmres: bad args");
+  if (p->nl) return fail(p, EXPD_ERR_UNSUPPORTED, "GMRES is for linear problems (npoly == 0)");
+  if (p->krylov_cap < 1) return fail(p, EXPD_ERR_OOM, "workspace holds no Krylov vectors");
+  if (p->cx) return gmres_impl<std::complex<double>>(p, u0, U, tol, restart, maxit, report);
+  return gmres_impl<double>(p, u0, U, tol, restart, maxit, report);
+}
+
 // ---------------------------------------------------------------------------------------
 // left-preconditioned BiCGStab (reading R17, van der Vorst's steps
 // with the half-step test): the operator B v = Q_alpha^{-1} Q v is one K1 pass (RM_QOP); the
@@ -804,6 +930,7 @@ extern "C" expd_status expd_bicgstab_solve(expd_plan* p, const double* u0, doubl
   if (s) return s;
   if (!u0 || !U || maxit < 0 || !(tol >= 0.0)) return fail(p, EXPD_ERR_INVALID_ARG, "bicgstab: bad args");
   if (p->nl) return fail(p, EXPD_ERR_UNSUPPORTED, "BiCGStab is for linear problems (npoly == 0)");
+  if (p->cx) return fail(p, EXPD_ERR_UNSUPPORTED, "BiCGStab: real plans only");
   if (p->krylov_cap < 6) return fail(p, EXPD_ERR_OOM, "BiCGStab needs 6 work vectors in the workspace");
   const long len = (long)p->prob.nt * p->mlen;
   const size_t vstride = align_up(sizeof(double) * (size_t)len) / sizeof(double);

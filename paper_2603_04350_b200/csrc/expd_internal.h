@@ -107,13 +107,19 @@ cudaError_t mode_tables(const Geom& g, const double* lam_axis, double a, double 
                         double* E, double* C1, double* C2, cudaStream_t st);
 cudaError_t reduce_partials(const double* partial, int n, double* out, cudaStream_t st);
 // GMRES / CGS2 helpers over vectors of length len (all 16-byte aligned, len even)
+// (cx: complex vectors, Hermitian inner products, complex coefficients as (re, im) pairs)
 cudaError_t multi_dot(const double* const* V, int nv, const double* w, long len, double* partial, int grid,
-                      double* out, cudaStream_t st);
+                      double* out, cudaStream_t st, bool cx = false);
 cudaError_t multi_axpy_dot(const double* const* V, int nv, const double* coef_dev, double* w, long len,
-                           double* partial, int grid, double* out, int want_dot, cudaStream_t st);
+                           double* partial, int grid, double* out, int want_dot, cudaStream_t st, bool cx = false);
 cudaError_t scale_copy(const double* x, double s, double* y, long len, cudaStream_t st);
 cudaError_t lincomb_add(const double* const* V, int nv, const double* coef_dev, double* x, long len,
-                        cudaStream_t st);
+                        cudaStream_t st, bool cx = false);
+// complex interleaved slices <-> planar (re, im) slice pairs (complex plans)
+cudaError_t cx_split(const double* in, long in_stride, long len, double* out, long out_stride, long nslices,
+                     cudaStream_t st);
+cudaError_t cx_merge(const double* in, long in_stride, long len, double* out, long out_stride, long nslices,
+                     cudaStream_t st);
 int vec_grid(int sms);
 
 // ---- multi-GPU (dist.cu) ----------------------------------------------------------------

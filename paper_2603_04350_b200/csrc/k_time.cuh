@@ -1,0 +1,1066 @@
+// k_time.cuh -- K1, the time-local fused pass of one Exp-ParaDiag sweep (sm_100a, fp64).
+//
+// In the DST basis every spatial mode J is an independent length-Nt problem (V commutes
+// with Q, Q_alpha and F (x) I).  One CTA owns a tile of S mode
+// PAIRS x all Nt time slices; the two real modes of a pair travel as one complex
+// sequence z_t = u_{2p}(t) + i u_{2p+1}(t) (Hermitian packing), which is also exactly
+// how they sit in memory (one 16-byte double2 per pair and slice).  Per tile, in one HBM
+// pass:
+//   stage 1  r_t = E_J u_{t-1} + C1_J N_t - C2_J N_{t-1} - u_t        (R5/R6)
+//            ||r||^2 partials                                         (stage 4 / conv. test)
+//   stage 2  Step (a): y = Gamma_alpha r, Y = F y    (alpha^{t/Nt}, omega = e^{+2 pi i/Nt})
+//            Step (b): X_k = Y_k / (1 - lambda_k E_J), lambda_k = alpha^{1/Nt} omega^k
+//            Step (c): s = Gamma_alpha^{-1} F^* X
+//   update   u_t <- u_t + s_t                                         ((3.2))
+// The length-Nt DFT is a two-level four-step FFT Nt = P x Q: phase A (thread = pair, m2)
+// does the DFT-P over t = Q m1 + m2 in registers and the inter-stage twiddle; phase B
+// (thread = pair, {k1, P-k1}) does both DFT-Q's, so every thread holds each frequency k
+// together with its Hermitian partner Nt-k and unpacks / divides / repacks the two modes
+// in registers, then runs the inverse DFT-Q; phase C inverts the DFT-P and applies the
+// update.  Shared memory carries the two transposes; the divisor's 1/Nt (both unitary
+// 1/sqrt(Nt) factors) is folded into the reciprocal.
+#pragma once
+#include <cstdlib>
+
+#include <cuda.h>
+
+#include "expd_internal.h"
+#include "fft_dev.cuh"
+#include "tma_dev.cuh"
+
+namespace expd {
+
+template <int NT>
+struct TimeCfg;
+// Radix plan of the length-NT time FFT (Stockham stages R_0 .. R_{L-1}); the last stage
+// has a small radix so that a thread can own a frequency set together with its Hermitian
+// partner set; TPS = NT / R_0 threads per mode pair; S = 256 / TPS pairs per CTA.
+#ifndef EXPD_K1_THREADS
+#define EXPD_K1_THREADS 256
+#endif
+template <int NT> struct TimeCfg;
+template <> struct TimeCfg<4>   { static constexpr int L = 1, R0 = 4, R1 = 1, R2 = 1; };
+template <> struct TimeCfg<8>   { static constexpr int L = 1, R0 = 8, R1 = 1, R2 = 1; };
+template <> struct TimeCfg<16>  { static constexpr int L = 2, R0 = 4, R1 = 4, R2 = 1; };
+template <> struct TimeCfg<32>  { static constexpr int L = 2, R0 = 8, R1 = 4, R2 = 1; };
+template <> struct TimeCfg<64>  { static constexpr int L = 2, R0 = 8, R1 = 8, R2 = 1; };
+template <> struct TimeCfg<128> { static constexpr int L = 3, R0 = 8, R1 = 4, R2 = 4; };
+template <> struct TimeCfg<256> { static constexpr int L = 3, R0 = 8, R1 = 8, R2 = 4; };
+template <int NT>
+struct TimeGeo {
+  using C = TimeCfg<NT>;
+  static constexpr int L = C::L, R0 = C::R0;
+  static constexpr int RL = L == 1 ? C::R0 : (L == 2 ? C::R1 : C::R2);  // last forward radix
+  static constexpr int TPS = NT / R0;                                    // threads per pair
+  static constexpr int THREADS = EXPD_K1_THREADS;
+  static constexpr int S = THREADS / TPS;                                // pairs per CTA
+  static constexpr int NSL = NT / RL;                                    // Ns of the last stage
+};
+
+__device__ __forceinline__ double2 ld2(const double* p) { return __ldg(reinterpret_cast<const double2*>(p)); }
+__device__ __forceinline__ double2 ld2cs(const double* p) {  // streaming: read once
+  return __ldcs(reinterpret_cast<const double2*>(p));
+}
+__device__ __forceinline__ void st2(double* p, double2 v) { *reinterpret_cast<double2*>(p) = v; }
+
+// 1/D for D in [(1-beta)^2, 4], beta in (0,1): MUFU reciprocal seed + two Newton steps
+// (relative error < 2^-52; no branchy IEEE division sequence in the hot loop).
+__device__ __forceinline__ double fast_rcp(double D) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(D));
+  double e = fma(-D, r, 1.0);
+  r = fma(r, e, r);
+  e = fma(-D, r, 1.0);
+  return fma(r, e, r);
+}
+
+// d/2 for one real mode: 1/(2 Nt (1 - beta e^{i theta})) = (1 - beta c + i beta s)/(2 Nt D)
+__device__ __forceinline__ double2 half_divisor(double beta, double c, double s, double half_inv_nt) {
+  double u = fma(-beta, c, 1.0);
+  double v = beta * s;
+  double D = fma(u, u, v * v);
+  double r = half_inv_nt * fast_rcp(D);
+  return make_double2(u * r, v * r);
+}
+
+// BDF2: 1 - 4/3 lambda_{0,k} E + 1/3 lambda_{1,k} E^2 with
+// lambda_{1,k} = lambda_{0,k}^2 = (1 - x)(1 - x/3), x = beta e^{i theta}: the product of two
+// first-order reciprocals.
+__device__ __forceinline__ double2 half_divisor_bdf2(double beta, double c, double s, double half_inv_nt) {
+  return cmul(half_divisor(beta, c, s, half_inv_nt), half_divisor(beta * (1.0 / 3.0), c, s, 1.0));
+}
+
+// 1/(Nt (1 - beta e^{i theta})) for a complex beta = a1 E_J (complex coefficients: every
+// mode's time sequence is already complex, so each frequency divides on its own -- no
+// Hermitian unpack; PAPER.md:113-124 with complex E_J, :983)
+__device__ __forceinline__ double2 cx_divisor(double bx, double by, double c, double s, double inv_nt) {
+  const double u = fma(-bx, c, fma(by, s, 1.0));  // Re(1 - beta e^{i theta})
+  const double v = -fma(bx, s, by * c);           // Im(1 - beta e^{i theta})
+  const double D = fma(u, u, v * v);
+  const double r = inv_nt * fast_rcp(D);
+  return make_double2(u * r, -v * r);
+}
+
+// NL == 3 marks the BDF2 system (linear): residual f2 - R v, Q-operator R v, BDF2 divisor.
+// NL == 4 marks a complex-coefficient linear plan: a "pair" is one complex mode (re, im),
+// E_J is complex, residual E z_{t-1} - z_t and Q v = v_t - E v_{t-1} in complex arithmetic.
+template <int NL>
+struct K1Form {
+  static constexpr bool HASN = NL == 1 || NL == 2;  // an N-hat term in the residual
+  static constexpr bool BDF = NL == 3;
+  static constexpr bool CX = NL == 4;
+};
+
+// W_k = A Z_k + B conj(Z_kp),  W_kp = conj(A) Z_kp + conj(B) conj(Z_k)
+// with A = (da + db)/2, B = (da - db)/2 for the two modes of the pair (Hermitian unpack,
+// divide, repack in one step).  tw = e^{2 pi i k/Nt}.
+template <bool BDF = false>
+__device__ __forceinline__ void divide_pair(double2& Zk, double2& Zkp, double2 tw, double ba, double bb,
+                                            double hin, bool self) {
+  double2 da = BDF ? half_divisor_bdf2(ba, tw.x, tw.y, hin) : half_divisor(ba, tw.x, tw.y, hin);
+  double2 db = BDF ? half_divisor_bdf2(bb, tw.x, tw.y, hin) : half_divisor(bb, tw.x, tw.y, hin);
+  double2 A = cadd(da, db), B = csub(da, db);
+  double2 zk = Zk, zkp = Zkp;
+  // A*zk + B*conj(zkp)
+  double2 wk = make_double2(fma(A.x, zk.x, fma(-A.y, zk.y, fma(B.x, zkp.x, B.y * zkp.y))),
+                            fma(A.x, zk.y, fma(A.y, zk.x, fma(B.y, zkp.x, -B.x * zkp.y))));
+  if (self) {
+    Zk = wk;
+    return;
+  }
+  // conj(A)*zkp + conj(B)*conj(zk)
+  double2 wkp = make_double2(fma(A.x, zkp.x, fma(A.y, zkp.y, fma(B.x, zk.x, -B.y * zk.y))),
+                             fma(A.x, zkp.y, fma(-A.y, zkp.x, fma(-B.y, zk.x, -B.x * zk.y))));
+  Zk = wk;
+  Zkp = wkp;
+}
+
+// One Stockham stage between shared buffers: job (s, j), inputs x[j + r NT/R], twiddle
+// w^{r (j mod NS) NT/(NS R)} (w = e^{DIR 2 pi i/NT}), DFT-R, outputs y[(j/NS) NS R + j mod NS + r NS].
+template <int NT, int S, int THREADS, int R, int NS, int DIR>
+__device__ __forceinline__ void tstage(const double2* __restrict__ in, double2* __restrict__ out,
+                                       const double2* __restrict__ stw) {
+  constexpr int JOBS = S * (NT / R);
+#pragma unroll
+  for (int J = threadIdx.x; J < JOBS; J += THREADS) {
+    const int s = J % S, j = J / S, k = j % NS;
+    double2 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = in[(j + r * (NT / R)) * S + s];
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      const double2 w = stw[(r * k * (NT / (NS * R))) & (NT - 1)];
+      v[r] = DIR > 0 ? cmul(v[r], w) : cmulc(v[r], w);
+    }
+    DFT<R, DIR>::run(v);
+    const int base = (j / NS) * NS * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) out[(base + r * NS) * S + s] = v[r];
+  }
+}
+
+// v[r] *= w1^r (DIR > 0) or conj(w1)^r (DIR < 0), r = 1..R-1, powers by products from
+// one base twiddle held in a register (binary splitting, <= 2 log2 R roundings deep): the
+// twiddles cost fp64 products instead of shared-memory table loads.
+template <int R, int DIR>
+__device__ __forceinline__ void twpow_mul(double2* v, double2 w1) {
+  if constexpr (R > 1) {
+    double2 t[R];
+    t[1] = w1;
+#pragma unroll
+    for (int r = 2; r < R; ++r) t[r] = (r % 2 == 0) ? cmul(t[r / 2], t[r / 2]) : cmul(t[r - 1], t[1]);
+#pragma unroll
+    for (int r = 1; r < R; ++r) v[r] = DIR > 0 ? cmul(v[r], t[r]) : cmulc(v[r], t[r]);
+  }
+}
+
+// tstage with the job's base twiddle w^{k NT/(NS R)} in a register (one job per thread).
+template <int NT, int S, int THREADS, int R, int NS, int DIR>
+__device__ __forceinline__ void tstage_pw(const double2* __restrict__ in, double2* __restrict__ out, double2 w1) {
+  constexpr int JOBS = S * (NT / R);
+  static_assert(JOBS == THREADS, "one job per thread");
+  const int J = threadIdx.x;
+  const int s = J % S, j = J / S, k = j % NS;
+  double2 v[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) v[r] = in[(j + r * (NT / R)) * S + s];
+  twpow_mul<R, DIR>(v, w1);
+  DFT<R, DIR>::run(v);
+  const int base = (j / NS) * NS * R + k;
+#pragma unroll
+  for (int r = 0; r < R; ++r) out[(base + r * NS) * S + s] = v[r];
+}
+
+// Last forward stage (radix RL, NS = NT/RL) of two partner jobs ja, jb (their frequency sets
+// k = j + NS r are Hermitian partners), the pair divide, and the first inverse stage
+// (radix RL, NS = 1: no twiddles) on the same sets.
+template <int NT, int RL, bool BDF = false, bool CX = false>
+__device__ __forceinline__ void pair_divide(double2 (&va)[RL], double2 (&vb)[RL], bool pj0, const double2* stw,
+                                            int ja, int jb, double ba, double bb, double hin) {
+  constexpr int NS = NT / RL;
+  if constexpr (CX) {  // (ba, bb) = a1 E_J complex; frequency ja + NS r (and jb + NS r)
+    const double inv_nt = 2.0 * hin;
+#pragma unroll
+    for (int r = 0; r < RL; ++r) {
+      const double2 w = stw[ja + NS * r];
+      va[r] = cmul(va[r], cx_divisor(ba, bb, w.x, w.y, inv_nt));
+    }
+    if (!pj0 || jb != ja) {
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        const double2 w = stw[jb + NS * r];
+        vb[r] = cmul(vb[r], cx_divisor(ba, bb, w.x, w.y, inv_nt));
+      }
+    }
+    return;
+  }
+  if (!pj0) {
+#pragma unroll
+    for (int r = 0; r < RL; ++r) divide_pair<BDF>(va[r], vb[RL - 1 - r], stw[ja + NS * r], ba, bb, hin, false);
+  } else {
+    // ja = 0: frequencies NS r, partner NS (RL - r) mod RL; self at r = 0 and RL/2
+    divide_pair<BDF>(va[0], va[0], stw[0], ba, bb, hin, true);
+#pragma unroll
+    for (int r = 1; r < (RL + 1) / 2; ++r) divide_pair<BDF>(va[r], va[RL - r], stw[NS * r], ba, bb, hin, false);
+    if constexpr (RL % 2 == 0) divide_pair<BDF>(va[RL / 2], va[RL / 2], stw[NS * (RL / 2)], ba, bb, hin, true);
+    if (jb != ja) {
+      // jb = NS/2: frequencies NS/2 + NS r, partner index RL-1-r
+#pragma unroll
+      for (int r = 0; r < RL / 2; ++r)
+        divide_pair<BDF>(vb[r], vb[RL - 1 - r], stw[jb + NS * r], ba, bb, hin, false);
+      if constexpr (RL % 2 == 1)
+        divide_pair<BDF>(vb[RL / 2], vb[RL / 2], stw[jb + NS * (RL / 2)], ba, bb, hin, true);
+    }
+  }
+}
+
+// BDF2 time-local residual / Q-operator of one mode pair at time t:
+// RESID: r_t = 4/3 E p1 - 1/3 E^2 p2 - x_t, p1 = v_{t-1} (u_1 = E u_0 at t = 0), p2 = v_{t-2}
+// (u_1 at t = 1, u_0 at t = 0);  QOP: (R v)_t = v_t - 4/3 E v_{t-1} + 1/3 E^2 v_{t-2}.
+template <bool RESID>
+__device__ __forceinline__ double2 bdf2_form(double2 E, double2 xc, double2 xm1, double2 xm2, double2 u0, int t) {
+  const double2 u1 = make_double2(E.x * u0.x, E.y * u0.y);
+  const double2 zero = make_double2(0.0, 0.0);
+  const double2 p1 = t >= 1 ? xm1 : (RESID ? u1 : zero);
+  const double2 p2 = t >= 2 ? xm2 : (t == 1 ? (RESID ? u1 : zero) : (RESID ? u0 : zero));
+  const double c43 = 4.0 / 3.0, c13 = 1.0 / 3.0;
+  const double2 e2 = make_double2(E.x * E.x, E.y * E.y);
+  double2 r;
+  r.x = fma(c43 * E.x, p1.x, -c13 * e2.x * p2.x);
+  r.y = fma(c43 * E.y, p1.y, -c13 * e2.y * p2.y);
+  return RESID ? make_double2(r.x - xc.x, r.y - xc.y) : make_double2(xc.x - r.x, xc.y - r.y);
+}
+
+#ifndef EXPD_K1_MINB
+#define EXPD_K1_MINB 2
+#endif
+#ifndef EXPD_K1_REREAD
+#define EXPD_K1_REREAD 0
+#endif
+template <int NT, int RM, int OUTM, int NL>
+__global__ void __launch_bounds__(EXPD_K1_THREADS, EXPD_K1_MINB) k_time_fused(const TimeArgs a) {
+  using G = TimeGeo<NT>;
+  using C = TimeCfg<NT>;
+  constexpr int L = G::L, R0 = G::R0, RL = G::RL, TPS = G::TPS, S = G::S, THREADS = G::THREADS;
+  constexpr int NSL = G::NSL;
+  extern __shared__ double2 smem[];
+  double2* buf0 = smem;                      // [NT][S]
+  double2* buf1 = smem + (L > 1 ? NT * S : 0);
+  double2* stw = smem + (L > 1 ? 2 * NT * S : 0);  // [NT] e^{+2 pi i q/NT}
+  double* sg = reinterpret_cast<double*>(stw + NT);  // [NT] alpha^{t/NT}
+  double* sgi = sg + NT;                              // [NT] alpha^{-t/NT}
+
+  const int tid = threadIdx.x;
+  for (int i = tid; i < NT; i += THREADS) {
+    stw[i] = a.tw[i];
+    sg[i] = a.g[i];
+    sgi[i] = a.ginv[i];
+  }
+  __syncthreads();
+
+  const long npad = a.npad;
+  const long ntiles = (a.npairs + S - 1) / S;
+  const double hin = a.half_inv_nt;
+  double nrm = 0.0;
+  const int s = tid % S;   // pair within the tile (fastest: conflict-free shared accesses)
+  const int j = tid / S;   // stage-0 job: times j + r TPS
+
+  for (long tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const long pair = tile * S + s;
+    const bool valid = pair < a.npairs;
+    const long base = 2 * pair;
+
+    // ---- phase A: stage 1 residual (+ ||r||^2), Gamma_alpha, forward stage 0 ----------
+    double2 y[R0];
+    double2 xv[(OUTM == OUT_UPDATE && !EXPD_K1_REREAD) ? R0 : 1];
+    double2 Ej = make_double2(0.0, 0.0), c1 = Ej, c2 = Ej;
+    if (valid && RM != RM_INPUT) Ej = ld2(a.E + base);
+    if (valid && K1Form<NL>::HASN) c1 = ld2(a.C1 + base);
+    if (valid && NL == 2) c2 = ld2(a.C2 + base);
+#pragma unroll
+    for (int r = 0; r < R0; ++r) {
+      const int t = j + r * TPS;
+      double2 cur = make_double2(0.0, 0.0), rr;
+      if (valid) cur = (OUTM == OUT_UPDATE) ? ld2(a.X + (long)t * npad + base) : ld2cs(a.X + (long)t * npad + base);
+      if constexpr (RM == RM_INPUT) {
+        rr = cur;
+      } else if constexpr (K1Form<NL>::BDF) {
+        double2 xm1 = make_double2(0.0, 0.0), xm2 = xm1, u0 = xm1;
+        if (valid) {
+          if (t >= 1) xm1 = ld2(a.X + (long)(t - 1) * npad + base);
+          if (t >= 2) xm2 = ld2(a.X + (long)(t - 2) * npad + base);
+          if (RM == RM_RESID) u0 = ld2(a.u0h + base);
+        }
+        rr = bdf2_form<RM == RM_RESID>(Ej, cur, xm1, xm2, u0, t);
+      } else {
+        double2 prev = make_double2(0.0, 0.0);
+        if (valid) {
+          if (t > 0) prev = ld2(a.X + (long)(t - 1) * npad + base);
+          else if (RM == RM_RESID) prev = ld2(a.u0h + base);
+        }
+        if constexpr (K1Form<NL>::CX) {
+          const double2 ep = cmul(Ej, prev);
+          rr = RM == RM_RESID ? csub(ep, cur) : csub(cur, ep);
+        } else if constexpr (RM == RM_RESID) {
+          rr = make_double2(fma(Ej.x, prev.x, -cur.x), fma(Ej.y, prev.y, -cur.y));
+          if constexpr (K1Form<NL>::HASN) {
+            double2 nm1 = valid ? ld2cs(a.Nh + (long)t * npad + base) : make_double2(0.0, 0.0);
+            rr.x = fma(c1.x, nm1.x, rr.x);
+            rr.y = fma(c1.y, nm1.y, rr.y);
+            if constexpr (NL == 2) {
+              double2 nm2 = valid ? ld2(a.Nh + (long)(t > 0 ? t - 1 : 0) * npad + base) : make_double2(0.0, 0.0);
+              rr.x = fma(-c2.x, nm2.x, rr.x);
+              rr.y = fma(-c2.y, nm2.y, rr.y);
+            }
+          }
+        } else {  // RM_QOP: (Q v)_t = v_t - E v_{t-1}, v_{-1} = 0
+          rr = make_double2(fma(-Ej.x, prev.x, cur.x), fma(-Ej.y, prev.y, cur.y));
+        }
+      }
+      nrm = fma(rr.x, rr.x, fma(rr.y, rr.y, nrm));
+      if constexpr (OUTM == OUT_UPDATE && !EXPD_K1_REREAD) xv[r] = cur;
+      y[r] = cscale(rr, sg[t]);
+    }
+    DFT<R0, +1>::run(y);
+
+    if constexpr (L == 1) {
+      // single stage: job 0 owns every frequency; divide its Hermitian pairs in place
+      const double2 Ep = valid ? ld2(a.E + base) : make_double2(0.0, 0.0);
+      const double ba = a.a1 * Ep.x, bb = a.a1 * Ep.y;
+      double2 dummy[R0];
+      pair_divide<NT, R0, K1Form<NL>::BDF, K1Form<NL>::CX>(y, dummy, true, stw, 0, 0, ba, bb, hin);
+      DFT<R0, -1>::run(y);
+    } else {
+#pragma unroll
+      for (int r = 0; r < R0; ++r) buf0[(j * R0 + r) * S + s] = y[r];
+      __syncthreads();
+      const double2* pin = buf0;
+      double2* pout = buf1;
+      if constexpr (L == 3) {  // forward middle stage
+        tstage<NT, S, THREADS, C::R1, R0, +1>(buf0, buf1, stw);
+        __syncthreads();
+        pin = buf1;
+        pout = buf0;
+      }
+      // ---- pair stage: last forward stage, divide, first inverse stage ---------------
+      for (int PJ = tid; PJ < S * (NSL / 2); PJ += THREADS) {
+        const int ps = PJ % S, pj = PJ / S;
+        const int ja = pj, jb = pj == 0 ? NSL / 2 : NSL - pj;
+        const long jpair = tile * S + ps;
+        double2 va[RL], vb[RL];
+#pragma unroll
+        for (int r = 0; r < RL; ++r) {
+          va[r] = pin[(ja + r * NSL) * S + ps];
+          vb[r] = pin[(jb + r * NSL) * S + ps];
+        }
+#pragma unroll
+        for (int r = 1; r < RL; ++r) {
+          va[r] = cmul(va[r], stw[(r * ja) & (NT - 1)]);
+          vb[r] = cmul(vb[r], stw[(r * jb) & (NT - 1)]);
+        }
+        DFT<RL, +1>::run(va);
+        DFT<RL, +1>::run(vb);
+        const double2 Ep = jpair < a.npairs ? ld2(a.E + 2 * jpair) : make_double2(0.0, 0.0);
+        pair_divide<NT, RL, K1Form<NL>::BDF, K1Form<NL>::CX>(va, vb, pj == 0, stw, ja, jb, a.a1 * Ep.x,
+                                                           a.a1 * Ep.y, hin);
+        DFT<RL, -1>::run(va);
+        DFT<RL, -1>::run(vb);
+#pragma unroll
+        for (int r = 0; r < RL; ++r) {
+          pout[(ja * RL + r) * S + ps] = va[r];
+          pout[(jb * RL + r) * S + ps] = vb[r];
+        }
+      }
+      __syncthreads();
+      if constexpr (L == 3) {  // inverse middle stage (radix R1, NS = RL)
+        tstage<NT, S, THREADS, C::R1, RL, -1>(buf0, buf1, stw);
+        __syncthreads();
+      }
+      const double2* cin = (L == 3) ? buf1 : buf1;
+      // ---- phase C input: inverse last stage (radix R0, NS = TPS) ----------------------
+#pragma unroll
+      for (int r = 0; r < R0; ++r) y[r] = cin[(j + r * TPS) * S + s];
+#pragma unroll
+      for (int r = 1; r < R0; ++r) y[r] = cmulc(y[r], stw[(r * j) & (NT - 1)]);
+      DFT<R0, -1>::run(y);
+    }
+    // ---- phase C: Gamma_alpha^{-1}, update, store (times j + r TPS) -------------------
+    if (valid) {
+#pragma unroll
+      for (int r = 0; r < R0; ++r) {
+        const int t = j + r * TPS;
+        double2 sv = cscale(y[r], sgi[t]);
+        if constexpr (OUTM == OUT_UPDATE) {
+          if constexpr (EXPD_K1_REREAD) sv = cadd(ld2(a.X + (long)t * npad + base), sv);  // L2 hit
+          else sv = cadd(xv[r], sv);
+        }
+        st2(a.Y + (long)t * npad + base, sv);
+      }
+    }
+  }
+
+  if (a.partial) {
+    // fixed-order block reduction (deterministic for a fixed grid)
+    __shared__ double red[THREADS / 32];
+    for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+    if ((tid & 31) == 0) red[tid >> 5] = nrm;
+    __syncthreads();
+    if (tid < 32) {
+      double v = tid < THREADS / 32 ? red[tid] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (tid == 0) a.partial[blockIdx.x] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// K1, software-pipelined: one persistent CTA per SM; while tile i is transformed, the
+// U-hat / N-hat time columns (and the per-mode tables) of tile i+1 stream into the other
+// half of a double-buffered shared-memory stage with cp.async, so phase A never waits on
+// HBM latency.  Phase C takes u_t for the update from the staged tile, not registers.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ void cpa16(void* smem, const void* gmem, bool valid) {
+  unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  int sz = valid ? 16 : 0;  // zero-fill past the last mode pair
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(gmem), "r"(sz));
+}
+__device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cpa_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+// DB: double-buffered stage, one CTA per SM.  !DB: one stage per CTA, two CTAs per SM
+// (the other CTA's math hides this one's cp.async latency); buf0 then aliases the N-hat
+// part of the stage (N-hat is dead once phase A has run).
+template <int NT, int RM, int NL, bool DB>
+struct PipeLayout {
+  using G = TimeGeo<NT>;
+  static constexpr int S = G::S;
+  static constexpr int TILE = NT * S;                   // double2 per staged array
+  static constexpr int NARR = 1 + (NL ? 1 : 0);         // X (+ N-hat)
+  static constexpr int AUX = 4 * S;                     // E, C1, C2, u0-hat per pair
+  static constexpr int STAGE = NARR * TILE + AUX;       // double2 per pipeline stage
+  static constexpr bool ALIAS = !DB && NL;              // buf0 inside the stage's N-hat block
+  static constexpr int NSTAGE = DB ? 2 : 1;
+  static constexpr int FFTBUF = ALIAS ? TILE : 2 * TILE;
+  static constexpr size_t BYTES = sizeof(double2) * (NSTAGE * STAGE + FFTBUF + NT) + sizeof(double) * 2 * NT;
+};
+
+template <int NT, int RM, int NL, bool DB>
+__device__ __forceinline__ void pipe_issue(const TimeArgs& a, long tile, double2* stage) {
+  using PL = PipeLayout<NT, RM, NL, DB>;
+  constexpr int S = PL::S, TILE = PL::TILE, THREADS = TimeGeo<NT>::THREADS;
+  const long npad = a.npad;
+  for (int c = threadIdx.x; c < TILE; c += THREADS) {
+    const int t = c / S, s = c % S;
+    const long pair = tile * S + s;
+    const bool ok = pair < a.npairs;
+    const long off = (long)t * npad + 2 * (ok ? pair : 0);
+    cpa16(stage + c, a.X + off, ok);
+    if constexpr (NL) cpa16(stage + TILE + c, a.Nh + off, ok);
+  }
+  if (threadIdx.x < S) {
+    const int s = threadIdx.x;
+    const long pair = tile * S + s;
+    const bool ok = pair < a.npairs;
+    const long off = 2 * (ok ? pair : 0);
+    double2* aux = stage + PL::NARR * TILE;
+    cpa16(aux + s, a.E + off, ok);
+    if constexpr (NL >= 1) cpa16(aux + S + s, a.C1 + off, ok);
+    if constexpr (NL == 2) cpa16(aux + 2 * S + s, a.C2 + off, ok);
+    if constexpr (RM == RM_RESID) cpa16(aux + 3 * S + s, a.u0h + off, ok);
+  }
+  cpa_commit();
+}
+
+template <int NT, int RM, int OUTM, int NL, bool DB>
+__global__ void __launch_bounds__(EXPD_K1_THREADS, DB ? 1 : 2) k_time_pipe(const TimeArgs a) {
+  using G = TimeGeo<NT>;
+  using C = TimeCfg<NT>;
+  using PL = PipeLayout<NT, RM, NL, DB>;
+  constexpr int L = G::L, R0 = G::R0, RL = G::RL, TPS = G::TPS, S = G::S, THREADS = G::THREADS;
+  constexpr int NSL = G::NSL, TILE = PL::TILE;
+  static_assert(L > 1, "pipelined kernel needs a multi-stage FFT");
+  extern __shared__ double2 smem[];
+  double2* buf0 = PL::ALIAS ? smem + TILE : smem + PL::NSTAGE * PL::STAGE;  // [NT][S]
+  double2* buf1 = PL::ALIAS ? smem + PL::STAGE : buf0 + TILE;
+  double2* stw = smem + PL::NSTAGE * PL::STAGE + PL::FFTBUF;  // [NT] e^{+2 pi i q/NT}
+  double* sg = reinterpret_cast<double*>(stw + NT);
+  double* sgi = sg + NT;
+
+  const int tid = threadIdx.x;
+  for (int i = tid; i < NT; i += THREADS) {
+    stw[i] = a.tw[i];
+    sg[i] = a.g[i];
+    sgi[i] = a.ginv[i];
+  }
+  const long npad = a.npad;
+  const long ntiles = (a.npairs + S - 1) / S;
+  const double hin = a.half_inv_nt;
+  double nrm = 0.0;
+  const int s = tid % S;
+  const int j = tid / S;
+
+  long tile = blockIdx.x;
+  int cur = 0;
+  if (DB && tile < ntiles) pipe_issue<NT, RM, NL, DB>(a, tile, smem);
+  for (; tile < ntiles; tile += gridDim.x, cur ^= (DB ? 1 : 0)) {
+    if constexpr (DB) {
+      const long next = tile + gridDim.x;
+      if (next < ntiles) {
+        pipe_issue<NT, RM, NL, DB>(a, next, smem + (cur ^ 1) * PL::STAGE);
+        cpa_wait<1>();
+      } else {
+        cpa_wait<0>();
+      }
+    } else {
+      pipe_issue<NT, RM, NL, DB>(a, tile, smem);
+      cpa_wait<0>();
+    }
+    __syncthreads();
+    const double2* X = smem + cur * PL::STAGE;
+    const double2* NH = X + TILE;
+    const double2* aux = X + PL::NARR * TILE;
+    const long pair = tile * S + s;
+    const bool valid = pair < a.npairs;
+    const long base = 2 * pair;
+
+    // ---- phase A: residual (+ ||r||^2), Gamma_alpha, forward stage 0 (times j + r TPS) ---
+    double2 y[R0];
+    const double2 Ej = aux[s];
+    const double2 c1 = NL >= 1 ? aux[S + s] : make_double2(0.0, 0.0);
+    const double2 c2 = NL == 2 ? aux[2 * S + s] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int r = 0; r < R0; ++r) {
+      const int t = j + r * TPS;
+      const double2 xc = X[t * S + s];
+      double2 rr;
+      if constexpr (RM == RM_INPUT) {
+        rr = xc;
+      } else {
+        const double2 prev = t > 0 ? X[(t - 1) * S + s] : (RM == RM_RESID ? aux[3 * S + s] : make_double2(0.0, 0.0));
+        if constexpr (K1Form<NL>::CX) {
+          const double2 ep = cmul(Ej, prev);
+          rr = RM == RM_RESID ? csub(ep, xc) : csub(xc, ep);
+        } else if constexpr (RM == RM_RESID) {
+          rr = make_double2(fma(Ej.x, prev.x, -xc.x), fma(Ej.y, prev.y, -xc.y));
+          if constexpr (NL >= 1) {
+            const double2 nm1 = NH[t * S + s];
+            rr.x = fma(c1.x, nm1.x, rr.x);
+            rr.y = fma(c1.y, nm1.y, rr.y);
+            if constexpr (NL == 2) {
+              const double2 nm2 = NH[(t > 0 ? t - 1 : 0) * S + s];
+              rr.x = fma(-c2.x, nm2.x, rr.x);
+              rr.y = fma(-c2.y, nm2.y, rr.y);
+            }
+          }
+        } else {  // RM_QOP
+          rr = make_double2(fma(-Ej.x, prev.x, xc.x), fma(-Ej.y, prev.y, xc.y));
+        }
+      }
+      nrm = fma(rr.x, rr.x, fma(rr.y, rr.y, nrm));
+      y[r] = cscale(rr, sg[t]);
+    }
+    DFT<R0, +1>::run(y);
+    if constexpr (PL::ALIAS) __syncthreads();  // every thread is done reading N-hat
+#pragma unroll
+    for (int r = 0; r < R0; ++r) buf0[(j * R0 + r) * S + s] = y[r];
+    __syncthreads();
+    const double2* pin = buf0;
+    double2* pout = buf1;
+    if constexpr (L == 3) {
+      tstage<NT, S, THREADS, C::R1, R0, +1>(buf0, buf1, stw);
+      __syncthreads();
+      pin = buf1;
+      pout = buf0;
+    }
+    for (int PJ = tid; PJ < S * (NSL / 2); PJ += THREADS) {
+      const int ps = PJ % S, pj = PJ / S;
+      const int ja = pj, jb = pj == 0 ? NSL / 2 : NSL - pj;
+      double2 va[RL], vb[RL];
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        va[r] = pin[(ja + r * NSL) * S + ps];
+        vb[r] = pin[(jb + r * NSL) * S + ps];
+      }
+#pragma unroll
+      for (int r = 1; r < RL; ++r) {
+        va[r] = cmul(va[r], stw[(r * ja) & (NT - 1)]);
+        vb[r] = cmul(vb[r], stw[(r * jb) & (NT - 1)]);
+      }
+      DFT<RL, +1>::run(va);
+      DFT<RL, +1>::run(vb);
+      const double2 Ep = aux[ps];
+#ifdef EXPD_K1_NODIV_EXPERIMENT
+      pair_divide<NT, RL>(va, vb, false, stw, ja, jb, a.a1 * Ep.x, a.a1 * Ep.y, hin);
+#else
+      pair_divide<NT, RL>(va, vb, pj == 0, stw, ja, jb, a.a1 * Ep.x, a.a1 * Ep.y, hin);
+#endif
+      DFT<RL, -1>::run(va);
+      DFT<RL, -1>::run(vb);
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        pout[(ja * RL + r) * S + ps] = va[r];
+        pout[(jb * RL + r) * S + ps] = vb[r];
+      }
+    }
+    __syncthreads();
+    if constexpr (L == 3) {
+      tstage<NT, S, THREADS, C::R1, RL, -1>(buf0, buf1, stw);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < R0; ++r) y[r] = buf1[(j + r * TPS) * S + s];
+#pragma unroll
+    for (int r = 1; r < R0; ++r) y[r] = cmulc(y[r], stw[(r * j) & (NT - 1)]);
+    DFT<R0, -1>::run(y);
+    // ---- phase C: Gamma_alpha^{-1}, update (u_t from the staged tile), store ------------
+    if (valid) {
+#pragma unroll
+      for (int r = 0; r < R0; ++r) {
+        const int t = j + r * TPS;
+        double2 sv = cscale(y[r], sgi[t]);
+        if constexpr (OUTM == OUT_UPDATE) sv = cadd(X[t * S + s], sv);
+        st2(a.Y + (long)t * npad + base, sv);
+      }
+    }
+    __syncthreads();  // stage `cur` is refilled by the next iteration's prefetch
+  }
+
+  if (a.partial) {
+    __shared__ double red[THREADS / 32];
+    for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+    if ((tid & 31) == 0) red[tid >> 5] = nrm;
+    __syncthreads();
+    if (tid < 32) {
+      double v = tid < THREADS / 32 ? red[tid] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (tid == 0) a.partial[blockIdx.x] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------------------
+// K1, TMA-fed: the U-hat / N-hat time columns of a tile (S mode pairs x all NT slices =
+// one {2S doubles, NT rows} box per array) arrive by TMA tensor loads on an mbarrier (one
+// instruction per array instead of 2 NT S / THREADS cp.async per thread); the per-mode
+// tables by cp.async.  NST = 2: the next tile's loads overlap this tile's transform;
+// NST = 1: the overlap comes from the other CTAs on the SM.  THR sets S = THR / TPS.
+// ---------------------------------------------------------------------------------------
+template <int NT, int THR>
+struct TGeo {
+  using C = TimeCfg<NT>;
+  static constexpr int L = C::L, R0 = C::R0;
+  static constexpr int RL = L == 1 ? C::R0 : (L == 2 ? C::R1 : C::R2);
+  static constexpr int TPS = NT / R0;
+  static constexpr int THREADS = THR;
+  static constexpr int S = THR / TPS;
+  static constexpr int NSL = NT / RL;
+  static_assert(S >= 1 && S * TPS == THR, "THR must be a multiple of NT / R0");
+};
+
+template <int NT, int THR, int NL, int NST>
+struct TmaLayout {
+  using G = TGeo<NT, THR>;
+  static constexpr int S = G::S;
+  static constexpr int TILE = NT * S;                  // double2 per staged array
+  static constexpr int NARR = 1 + (K1Form<NL>::HASN ? 1 : 0);
+  static constexpr int AUX = 4 * S;                    // E, C1, C2, u0-hat per pair
+  static constexpr int STAGE = ((NARR * TILE + AUX) + 7) / 8 * 8;  // 128-byte multiple
+  static constexpr bool ALIAS = K1Form<NL>::HASN;      // buf0 in the stage's N-hat block
+  static constexpr int FFTBUF = ALIAS ? TILE : 2 * TILE;
+  static constexpr size_t BYTES =
+      128 + sizeof(double2) * ((size_t)NST * STAGE + FFTBUF + NT) + sizeof(double) * 2 * NT + 16 * NST;
+  static constexpr int MINB_SMEM = (int)((228 * 1024) / (BYTES + 1024));
+  static constexpr int MINB = MINB_SMEM < 1 ? 1 : (MINB_SMEM > 8 ? 8 : MINB_SMEM);
+};
+
+template <int NT, int THR, int RM, int NL, int NST>
+__device__ __forceinline__ void tma_tile_issue(const CUtensorMap* mx, const CUtensorMap* mn, const TimeArgs& a,
+                                               long tile, double2* stage, uint64_t* bar) {
+  using PL = TmaLayout<NT, THR, NL, NST>;
+  constexpr int S = PL::S, TILE = PL::TILE;
+  if (threadIdx.x == 0) {
+    mbar_arrive_expect_tx(bar, (uint32_t)(PL::NARR * TILE * 16));
+    tma_load_2d(stage, mx, bar, (int)(2 * S * tile), 0);
+    if constexpr (K1Form<NL>::HASN) tma_load_2d(stage + TILE, mn, bar, (int)(2 * S * tile), 0);
+  }
+  if (threadIdx.x < S) {
+    const int s = threadIdx.x;
+    const long pair = tile * S + s;
+    const bool ok = pair < a.npairs;
+    const long off = 2 * (ok ? pair : 0);
+    double2* aux = stage + PL::NARR * TILE;
+    cpa16(aux + s, a.E + off, ok);
+    if constexpr (K1Form<NL>::HASN) cpa16(aux + S + s, a.C1 + off, ok);
+    if constexpr (NL == 2) cpa16(aux + 2 * S + s, a.C2 + off, ok);
+    if constexpr (RM == RM_RESID) cpa16(aux + 3 * S + s, a.u0h + off, ok);
+  }
+  cpa_commit();
+}
+
+template <int NT, int RM, int OUTM, int NL, int THR, int NST>
+__global__ void __launch_bounds__(THR, (TmaLayout<NT, THR, NL, NST>::MINB))
+    k_time_tma(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mn,
+               const __grid_constant__ TimeArgs a) {
+  using G = TGeo<NT, THR>;
+  using C = TimeCfg<NT>;
+  using PL = TmaLayout<NT, THR, NL, NST>;
+  constexpr int L = G::L, R0 = G::R0, RL = G::RL, TPS = G::TPS, S = G::S, THREADS = THR;
+  constexpr int NSL = G::NSL, TILE = PL::TILE;
+  static_assert(L > 1, "TMA kernel needs a multi-stage FFT");
+  extern __shared__ unsigned char tsm_raw[];
+  // 128-byte aligned base as an offset from the __shared__ array (keeps LDS/STS)
+  double2* smem = reinterpret_cast<double2*>(tsm_raw + ((128u - (smem_u32(tsm_raw) & 127u)) & 127u));
+  double2* fft = smem + NST * PL::STAGE;
+  double2* stw = fft + PL::FFTBUF;                     // [NT] e^{+2 pi i q/NT}
+  double* sg = reinterpret_cast<double*>(stw + NT);    // [NT] alpha^{t/NT}
+  double* sgi = sg + NT;                               // [NT] alpha^{-t/NT}
+  uint64_t* bar = reinterpret_cast<uint64_t*>(sgi + NT);
+
+  const int tid = threadIdx.x;
+  __builtin_assume(tid < THREADS);
+  for (int i = tid; i < NT; i += THREADS) {
+    stw[i] = a.tw[i];
+    sg[i] = a.g[i];
+    sgi[i] = a.ginv[i];
+  }
+  if (tid == 0) {
+    prefetch_tmap(&mx);
+    if constexpr (K1Form<NL>::HASN) prefetch_tmap(&mn);
+    for (int k = 0; k < NST; ++k) mbar_init(&bar[k], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  const long ntiles = (a.npairs + S - 1) / S;
+  const double hin = a.half_inv_nt;
+  double nrm = 0.0;
+  const int s = tid % S;
+  const int j = tid / S;
+  const long npad = a.npad;
+  // loop-invariant base twiddles of this thread's jobs (each stage has one job per thread
+  // in the L = 3 plans used at NT >= 64; other plans keep the table loads)
+  constexpr bool PW = (L == 3) && (S * (NT / C::R1) == THREADS) && (S * (NSL / 2) == THREADS);
+  double2 w_fm = make_double2(1.0, 0.0), w_im = w_fm, w_pa = w_fm, w_pb = w_fm, w_c = w_fm;
+  if constexpr (PW) {
+    w_fm = stw[((j % R0) * (NT / (R0 * C::R1))) & (NT - 1)];   // forward middle stage, NS = R0
+    w_im = stw[((j % RL) * (NT / (RL * C::R1))) & (NT - 1)];   // inverse middle stage, NS = RL
+    const int pj = tid / S;
+    w_pa = stw[pj & (NT - 1)];
+    w_pb = stw[(pj == 0 ? NSL / 2 : NSL - pj) & (NT - 1)];
+    w_c = stw[j & (NT - 1)];                                     // phase C (inverse stage 0)
+  }
+
+  long tile = blockIdx.x;
+  if (tile < ntiles) tma_tile_issue<NT, THR, RM, NL, NST>(&mx, &mn, a, tile, smem, &bar[0]);
+  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+    const int cur = NST == 2 ? (it & 1) : 0;
+    double2* stg = smem + cur * PL::STAGE;
+    const long next = tile + gridDim.x;
+    if constexpr (NST == 2) {
+      if (next < ntiles) {
+        tma_tile_issue<NT, THR, RM, NL, NST>(&mx, &mn, a, next, smem + (cur ^ 1) * PL::STAGE, &bar[cur ^ 1]);
+        cpa_wait<1>();
+      } else {
+        cpa_wait<0>();
+      }
+    } else {
+      cpa_wait<0>();
+    }
+    mbar_wait(&bar[cur], (uint32_t)((NST == 2 ? (it >> 1) : it) & 1));
+    __syncthreads();  // the cp.async aux of every thread < S is visible
+    const double2* X = stg;
+    const double2* NH = stg + TILE;
+    const double2* aux = stg + PL::NARR * TILE;
+    double2* buf0 = PL::ALIAS ? stg + TILE : fft;
+    double2* buf1 = PL::ALIAS ? fft : fft + TILE;
+    const long pair = tile * S + s;
+    const bool valid = pair < a.npairs;
+    const long base = 2 * pair;
+
+    // ---- phase A: residual (+ ||r||^2), Gamma_alpha, forward stage 0 (times j + r TPS) ---
+    double2 y[R0];
+    double2 xv[OUTM == OUT_UPDATE ? R0 : 1];  // u_t kept in registers for the update
+    const double2 Ej = aux[s];
+    const double2 c1 = K1Form<NL>::HASN ? aux[S + s] : make_double2(0.0, 0.0);
+    const double2 c2 = NL == 2 ? aux[2 * S + s] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int r = 0; r < R0; ++r) {
+      const int t = j + r * TPS;
+      const double2 xc = X[t * S + s];
+      if constexpr (OUTM == OUT_UPDATE) xv[r] = xc;
+      double2 rr;
+      if constexpr (RM == RM_INPUT) {
+        rr = xc;
+      } else if constexpr (K1Form<NL>::BDF) {
+        const double2 zero = make_double2(0.0, 0.0);
+        const double2 xm1 = t >= 1 ? X[(t - 1) * S + s] : zero;
+        const double2 xm2 = t >= 2 ? X[(t - 2) * S + s] : zero;
+        const double2 u0 = RM == RM_RESID ? aux[3 * S + s] : zero;
+        rr = bdf2_form<RM == RM_RESID>(Ej, xc, xm1, xm2, u0, t);
+      } else {
+        const double2 prev = t > 0 ? X[(t - 1) * S + s] : (RM == RM_RESID ? aux[3 * S + s] : make_double2(0.0, 0.0));
+        if constexpr (K1Form<NL>::CX) {
+          const double2 ep = cmul(Ej, prev);
+          rr = RM == RM_RESID ? csub(ep, xc) : csub(xc, ep);
+        } else if constexpr (RM == RM_RESID) {
+          rr = make_double2(fma(Ej.x, prev.x, -xc.x), fma(Ej.y, prev.y, -xc.y));
+          if constexpr (K1Form<NL>::HASN) {
+            const double2 nm1 = NH[t * S + s];
+            rr.x = fma(c1.x, nm1.x, rr.x);
+            rr.y = fma(c1.y, nm1.y, rr.y);
+            if constexpr (NL == 2) {
+              const double2 nm2 = NH[(t > 0 ? t - 1 : 0) * S + s];
+              rr.x = fma(-c2.x, nm2.x, rr.x);
+              rr.y = fma(-c2.y, nm2.y, rr.y);
+            }
+          }
+        } else {  // RM_QOP
+          rr = make_double2(fma(-Ej.x, prev.x, xc.x), fma(-Ej.y, prev.y, xc.y));
+        }
+      }
+      nrm = fma(rr.x, rr.x, fma(rr.y, rr.y, nrm));
+      y[r] = cscale(rr, sg[t]);
+    }
+    DFT<R0, +1>::run(y);
+    if constexpr (PL::ALIAS) __syncthreads();  // every thread is done reading N-hat
+#pragma unroll
+    for (int r = 0; r < R0; ++r) buf0[(j * R0 + r) * S + s] = y[r];
+    __syncthreads();
+    const double2* pin = buf0;
+    double2* pout = buf1;
+    if constexpr (L == 3) {
+      if constexpr (PW) tstage_pw<NT, S, THREADS, C::R1, R0, +1>(buf0, buf1, w_fm);
+      else tstage<NT, S, THREADS, C::R1, R0, +1>(buf0, buf1, stw);
+      __syncthreads();
+      pin = buf1;
+      pout = buf0;
+    }
+    for (int PJ = tid; PJ < S * (NSL / 2); PJ += THREADS) {
+      const int ps = PJ % S, pj = PJ / S;
+      const int ja = pj, jb = pj == 0 ? NSL / 2 : NSL - pj;
+      double2 va[RL], vb[RL];
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        va[r] = pin[(ja + r * NSL) * S + ps];
+        vb[r] = pin[(jb + r * NSL) * S + ps];
+      }
+      if constexpr (PW) {
+        twpow_mul<RL, +1>(va, w_pa);
+        twpow_mul<RL, +1>(vb, w_pb);
+      } else {
+#pragma unroll
+        for (int r = 1; r < RL; ++r) {
+          va[r] = cmul(va[r], stw[(r * ja) & (NT - 1)]);
+          vb[r] = cmul(vb[r], stw[(r * jb) & (NT - 1)]);
+        }
+      }
+      DFT<RL, +1>::run(va);
+      DFT<RL, +1>::run(vb);
+      const double2 Ep = aux[ps];
+      pair_divide<NT, RL, K1Form<NL>::BDF, K1Form<NL>::CX>(va, vb, pj == 0, stw, ja, jb, a.a1 * Ep.x,
+                                                           a.a1 * Ep.y, hin);
+      DFT<RL, -1>::run(va);
+      DFT<RL, -1>::run(vb);
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        pout[(ja * RL + r) * S + ps] = va[r];
+        pout[(jb * RL + r) * S + ps] = vb[r];
+      }
+    }
+    // last generic-proxy writes into the stage (buf0 aliases its N-hat block): order them
+    // before the next TMA write into the stage (the later accesses are reads)
+    if constexpr (PL::ALIAS) fence_proxy_async_smem();
+    __syncthreads();
+    if constexpr (L == 3) {
+      if constexpr (PW) tstage_pw<NT, S, THREADS, C::R1, RL, -1>(buf0, buf1, w_im);
+      else tstage<NT, S, THREADS, C::R1, RL, -1>(buf0, buf1, stw);
+      __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < R0; ++r) y[r] = buf1[(j + r * TPS) * S + s];
+    if constexpr (PW) {
+      twpow_mul<R0, -1>(y, w_c);
+    } else {
+#pragma unroll
+      for (int r = 1; r < R0; ++r) y[r] = cmulc(y[r], stw[(r * j) & (NT - 1)]);
+    }
+    DFT<R0, -1>::run(y);
+    // ---- phase C: Gamma_alpha^{-1}, update (u_t from the staged tile), store ------------
+    if (valid) {
+#pragma unroll
+      for (int r = 0; r < R0; ++r) {
+        const int t = j + r * TPS;
+        double2 sv = cscale(y[r], sgi[t]);
+        if constexpr (OUTM == OUT_UPDATE) sv = cadd(xv[r], sv);
+        st2(a.Y + (long)t * npad + base, sv);
+      }
+    }
+    __syncthreads();  // every read of the stage is done: it may be refilled by TMA
+    if constexpr (NST == 1) {
+      if (next < ntiles) tma_tile_issue<NT, THR, RM, NL, NST>(&mx, &mn, a, next, smem, &bar[0]);
+    }
+  }
+
+  if (a.partial) {
+    __shared__ double red[THREADS / 32];
+    for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+    if ((tid & 31) == 0) red[tid >> 5] = nrm;
+    __syncthreads();
+    if (tid < 32) {
+      double v = tid < THREADS / 32 ? red[tid] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (tid == 0) a.partial[blockIdx.x] = v;
+    }
+  }
+}
+
+template <int NT, int OUTM>
+static size_t time_smem_bytes() {
+  const size_t tile = TimeGeo<NT>::L > 1 ? (size_t)NT * TimeGeo<NT>::S : 0;
+  return sizeof(double2) * (2 * tile + NT) + sizeof(double) * 2 * NT;
+}
+
+// EXPD_K1_PIPE: 0 = register-load kernel, 1 = double-buffered cp.async pipe (1 CTA/SM),
+// 2 = single-stage cp.async pipe with two CTAs per SM, 3 (default) = TMA-fed kernel with
+// the variant EXPD_K1V = <threads><stages> (e.g. 2561, 2562, 1281, 1282)
+static int pipe_mode() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EXPD_K1_PIPE");
+    v = (e && e[0] >= '0' && e[0] <= '3') ? e[0] - '0' : 3;
+    if (v == 3 && !tma_available()) v = 2;
+  }
+  return v;
+}
+// Variants: 2562 (default: 256 threads, double-buffered tiles, 1 CTA/SM), 2561 (single
+// stage, 2 CTAs/SM), 1282 (128 threads = 4 pairs per tile).  c5: 7.02 / 7.10 / 11.2 ms.
+static int k1_variant() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EXPD_K1V");
+    v = e ? atoi(e) : 2562;
+    if (v != 2562 && v != 1282 && v != 2561) v = 2562;
+  }
+  return v;
+}
+static bool use_pipe() { return pipe_mode() > 0; }
+
+template <int NT, int RM, int OUTM, int NL, bool DB>
+static cudaError_t launch_pipe(const TimeArgs& a, int grid, cudaStream_t st) {
+  auto kp = k_time_pipe<NT, RM, OUTM, NL, DB>;
+  const size_t smp = PipeLayout<NT, RM, NL, DB>::BYTES;
+  static bool attr_p = false;
+  if (!attr_p) {
+    cudaError_t e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);
+    if (e != cudaSuccess) return e;
+    attr_p = true;
+  }
+  kp<<<grid, TimeGeo<NT>::THREADS, smp, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int NT, int RM, int OUTM, int NL, int THR, int NST>
+static cudaError_t launch_tma(const TimeArgs& a, int grid, cudaStream_t st) {
+  using PL = TmaLayout<NT, THR, NL, NST>;
+  auto k = k_time_tma<NT, RM, OUTM, NL, THR, NST>;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PL::BYTES);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  constexpr int S = PL::S;
+  CUtensorMap mx, mn;
+  cudaError_t e = make_tmap_2d(&mx, a.X, (unsigned long long)a.npad, (unsigned long long)a.nt,
+                               (unsigned long long)a.npad * 8, 2 * S, NT);
+  if (e != cudaSuccess) return e;
+  mn = mx;
+  if (K1Form<NL>::HASN && (e = make_tmap_2d(&mn, a.Nh, (unsigned long long)a.npad, (unsigned long long)a.nt,
+                              (unsigned long long)a.npad * 8, 2 * S, NT)) != cudaSuccess)
+    return e;
+  // the caller's grid (time_fused_grid) is also the number of partial sums it reduces
+  k<<<(unsigned)grid, THR, PL::BYTES, st>>>(mx, mn, a);
+  return cudaGetLastError();
+}
+
+template <int NT, int RM, int OUTM, int NL>
+static cudaError_t launch_t(const TimeArgs& a, int grid, cudaStream_t st) {
+  if constexpr (TimeGeo<NT>::L > 1 && (NL == 3 || NL == 4)) {  // BDF2 / complex: TMA or register kernel
+    if (pipe_mode() == 3) {
+      if (k1_variant() == 1282) return launch_tma<NT, RM, OUTM, NL, 128, 2>(a, grid, st);
+      if (k1_variant() == 2561) return launch_tma<NT, RM, OUTM, NL, 256, 1>(a, grid, st);
+      return launch_tma<NT, RM, OUTM, NL, 256, 2>(a, grid, st);
+    }
+  } else if constexpr (TimeGeo<NT>::L > 1) {
+    if (pipe_mode() == 3) {
+      if (k1_variant() == 1282) return launch_tma<NT, RM, OUTM, NL, 128, 2>(a, grid, st);
+      if (k1_variant() == 2561) return launch_tma<NT, RM, OUTM, NL, 256, 1>(a, grid, st);
+      return launch_tma<NT, RM, OUTM, NL, 256, 2>(a, grid, st);
+    }
+    if (pipe_mode() == 1) return launch_pipe<NT, RM, OUTM, NL, true>(a, grid, st);
+    if (pipe_mode() == 2) return launch_pipe<NT, RM, OUTM, NL, false>(a, grid, st);
+  }
+  auto k = k_time_fused<NT, RM, OUTM, NL>;
+  size_t sm = time_smem_bytes<NT, OUTM>();
+  static bool attr_done = false;  // per-instantiation, host-side
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  k<<<grid, TimeGeo<NT>::THREADS, sm, st>>>(a);
+  return cudaGetLastError();
+}
+
+template <int NT>
+static cudaError_t dispatch_nt(const TimeArgs& a, int rm, int om, int nl, int grid, cudaStream_t st) {
+  if (nl == 3) {  // BDF2 system (linear)
+    if (rm == RM_RESID && om == OUT_UPDATE) return launch_t<NT, RM_RESID, OUT_UPDATE, 3>(a, grid, st);
+    if (rm == RM_RESID && om == OUT_S) return launch_t<NT, RM_RESID, OUT_S, 3>(a, grid, st);
+    if (rm == RM_INPUT && om == OUT_S) return launch_t<NT, RM_INPUT, OUT_S, 3>(a, grid, st);
+    if (rm == RM_QOP && om == OUT_S) return launch_t<NT, RM_QOP, OUT_S, 3>(a, grid, st);
+    return cudaErrorInvalidValue;
+  }
+  if (nl == 4) {  // complex coefficients (linear)
+    if (rm == RM_RESID && om == OUT_UPDATE) return launch_t<NT, RM_RESID, OUT_UPDATE, 4>(a, grid, st);
+    if (rm == RM_RESID && om == OUT_S) return launch_t<NT, RM_RESID, OUT_S, 4>(a, grid, st);
+    if (rm == RM_INPUT && om == OUT_S) return launch_t<NT, RM_INPUT, OUT_S, 4>(a, grid, st);
+    if (rm == RM_QOP && om == OUT_S) return launch_t<NT, RM_QOP, OUT_S, 4>(a, grid, st);
+    return cudaErrorInvalidValue;
+  }
+  if (rm == RM_RESID && om == OUT_UPDATE) {
+    if (nl == 0) return launch_t<NT, RM_RESID, OUT_UPDATE, 0>(a, grid, st);
+    if (nl == 1) return launch_t<NT, RM_RESID, OUT_UPDATE, 1>(a, grid, st);
+    return launch_t<NT, RM_RESID, OUT_UPDATE, 2>(a, grid, st);
+  }
+  if (rm == RM_RESID && om == OUT_S) {
+    if (nl == 0) return launch_t<NT, RM_RESID, OUT_S, 0>(a, grid, st);
+    if (nl == 1) return launch_t<NT, RM_RESID, OUT_S, 1>(a, grid, st);
+    return launch_t<NT, RM_RESID, OUT_S, 2>(a, grid, st);
+  }
+  if (rm == RM_INPUT && om == OUT_S) return launch_t<NT, RM_INPUT, OUT_S, 0>(a, grid, st);
+  if (rm == RM_QOP && om == OUT_S) return launch_t<NT, RM_QOP, OUT_S, 0>(a, grid, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace expd

@@ -112,36 +112,45 @@ struct VecPtrs {
   const double* v[32];
 };
 
-// h_i = <V_i, w>, i < nv   (K6 pass 1)
-template <int NV>
+// h_i = <V_i, w>, i < nv   (K6 pass 1).  CX: the vectors are complex (interleaved), the
+// inner product is the Hermitian one, h_i = sum conj(V_i) w -> (re, im) = rows 2i, 2i+1
+// (complex GMRES, reading R18).
+template <int NV, bool CX = false>
 __global__ void __launch_bounds__(256) k_multi_dot(VecPtrs V, const double* __restrict__ w, long len2,
                                                    double* partial) {
-  double acc[NV];
+  constexpr int NA = CX ? 2 * NV : NV;
+  double acc[NA];
 #pragma unroll
-  for (int i = 0; i < NV; ++i) acc[i] = 0.0;
+  for (int i = 0; i < NA; ++i) acc[i] = 0.0;
   const double2* w2 = reinterpret_cast<const double2*>(w);
   for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < len2; e += (long)gridDim.x * blockDim.x) {
     double2 x = __ldcs(w2 + e);
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       double2 v = __ldcs(reinterpret_cast<const double2*>(V.v[i]) + e);
-      acc[i] = fma(v.x, x.x, fma(v.y, x.y, acc[i]));
+      if constexpr (CX) {
+        acc[2 * i] = fma(v.x, x.x, fma(v.y, x.y, acc[2 * i]));
+        acc[2 * i + 1] = fma(v.x, x.y, fma(-v.y, x.x, acc[2 * i + 1]));
+      } else {
+        acc[i] = fma(v.x, x.x, fma(v.y, x.y, acc[i]));
+      }
     }
   }
-  block_sum_store<NV>(acc, partial, gridDim.x);
+  block_sum_store<NA>(acc, partial, gridDim.x);
 }
 
-// w <- w - sum_i coef_i V_i ; then (WANT == 1) h2_i = <V_i, w> or (WANT == 2) ||w||^2
-template <int NV, int WANT>
+// w <- w - sum_i coef_i V_i ; then (WANT == 1) h2_i = <V_i, w> or (WANT == 2) ||w||^2.
+// CX: complex coefficients (coef[2i], coef[2i+1]) and the Hermitian h2_i (rows 2i, 2i+1).
+template <int NV, int WANT, bool CX = false>
 __global__ void __launch_bounds__(256) k_axpy_dot(VecPtrs V, const double* __restrict__ coef, double* w, long len2,
                                                   double* partial) {
-  constexpr int NO = WANT == 1 ? NV : 1;
+  constexpr int NO = WANT == 1 ? (CX ? 2 * NV : NV) : 1;
   double acc[NO];
 #pragma unroll
   for (int i = 0; i < NO; ++i) acc[i] = 0.0;
-  double cf[NV];
+  double2 cf[NV];
 #pragma unroll
-  for (int i = 0; i < NV; ++i) cf[i] = coef[i];
+  for (int i = 0; i < NV; ++i) cf[i] = CX ? make_double2(coef[2 * i], coef[2 * i + 1]) : make_double2(coef[i], 0.0);
   double2* w2 = reinterpret_cast<double2*>(w);
   for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < len2; e += (long)gridDim.x * blockDim.x) {
     double2 x = w2[e];
@@ -149,13 +158,25 @@ __global__ void __launch_bounds__(256) k_axpy_dot(VecPtrs V, const double* __res
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       vv[i] = __ldcs(reinterpret_cast<const double2*>(V.v[i]) + e);
-      x.x = fma(-cf[i], vv[i].x, x.x);
-      x.y = fma(-cf[i], vv[i].y, x.y);
+      if constexpr (CX) {  // x -= cf * v (complex)
+        x.x = fma(-cf[i].x, vv[i].x, fma(cf[i].y, vv[i].y, x.x));
+        x.y = fma(-cf[i].x, vv[i].y, fma(-cf[i].y, vv[i].x, x.y));
+      } else {
+        x.x = fma(-cf[i].x, vv[i].x, x.x);
+        x.y = fma(-cf[i].x, vv[i].y, x.y);
+      }
     }
     w2[e] = x;
     if constexpr (WANT == 1) {
 #pragma unroll
-      for (int i = 0; i < NV; ++i) acc[i] = fma(vv[i].x, x.x, fma(vv[i].y, x.y, acc[i]));
+      for (int i = 0; i < NV; ++i) {
+        if constexpr (CX) {
+          acc[2 * i] = fma(vv[i].x, x.x, fma(vv[i].y, x.y, acc[2 * i]));
+          acc[2 * i + 1] = fma(vv[i].x, x.y, fma(-vv[i].y, x.x, acc[2 * i + 1]));
+        } else {
+          acc[i] = fma(vv[i].x, x.x, fma(vv[i].y, x.y, acc[i]));
+        }
+      }
     } else if constexpr (WANT == 2) {
       acc[0] = fma(x.x, x.x, fma(x.y, x.y, acc[0]));
     }
@@ -163,20 +184,25 @@ __global__ void __launch_bounds__(256) k_axpy_dot(VecPtrs V, const double* __res
   if constexpr (WANT > 0) block_sum_store<NO>(acc, partial, gridDim.x);
 }
 
-// x <- x + sum_i coef_i V_i   (K7)
-template <int NV>
+// x <- x + sum_i coef_i V_i   (K7); CX: complex coefficients (coef[2i], coef[2i+1])
+template <int NV, bool CX = false>
 __global__ void __launch_bounds__(256) k_lincomb(VecPtrs V, const double* __restrict__ coef, double* x, long len2) {
-  double cf[NV];
+  double2 cf[NV];
 #pragma unroll
-  for (int i = 0; i < NV; ++i) cf[i] = coef[i];
+  for (int i = 0; i < NV; ++i) cf[i] = CX ? make_double2(coef[2 * i], coef[2 * i + 1]) : make_double2(coef[i], 0.0);
   double2* x2 = reinterpret_cast<double2*>(x);
   for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < len2; e += (long)gridDim.x * blockDim.x) {
     double2 a = x2[e];
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
       double2 v = __ldcs(reinterpret_cast<const double2*>(V.v[i]) + e);
-      a.x = fma(cf[i], v.x, a.x);
-      a.y = fma(cf[i], v.y, a.y);
+      if constexpr (CX) {
+        a.x = fma(cf[i].x, v.x, fma(-cf[i].y, v.y, a.x));
+        a.y = fma(cf[i].x, v.y, fma(cf[i].y, v.x, a.y));
+      } else {
+        a.x = fma(cf[i].x, v.x, a.x);
+        a.y = fma(cf[i].x, v.y, a.y);
+      }
     }
     x2[e] = a;
   }
@@ -212,47 +238,91 @@ static VecPtrs pack(const double* const* V, int nv) {
 
 // For nv > 8 the vectors are processed in groups of up to 8 (one extra pass over w per
 // group); restart <= 8 keeps every CGS2 sweep a single pass.
+// cx: complex vectors / coefficients, every coefficient or inner product is 2 doubles
+// (re, im) in the device arrays (out, coef_dev).
 cudaError_t multi_dot(const double* const* V, int nv, const double* w, long len, double* partial, int grid,
-                      double* out, cudaStream_t st) {
+                      double* out, cudaStream_t st, bool cx) {
   const long len2 = len / 2;
+  const int K = cx ? 2 : 1;
   for (int g0 = 0; g0 < nv; g0 += 8) {
     int ng = nv - g0 < 8 ? nv - g0 : 8;
     VecPtrs p = pack(V + g0, ng);
-    NV_SWITCH(ng, (k_multi_dot<NVc><<<grid, 256, 0, st>>>(p, w, len2, partial)));
-    k_reduce_rows<<<ng, 32, 0, st>>>(partial, grid, ng, out + g0);
+    if (cx) NV_SWITCH(ng, (k_multi_dot<NVc, true><<<grid, 256, 0, st>>>(p, w, len2, partial)))
+    else NV_SWITCH(ng, (k_multi_dot<NVc, false><<<grid, 256, 0, st>>>(p, w, len2, partial)))
+    k_reduce_rows<<<K * ng, 32, 0, st>>>(partial, grid, K * ng, out + K * g0);
   }
   return cudaGetLastError();
 }
 
 cudaError_t multi_axpy_dot(const double* const* V, int nv, const double* coef_dev, double* w, long len,
-                           double* partial, int grid, double* out, int want_dot, cudaStream_t st) {
+                           double* partial, int grid, double* out, int want_dot, cudaStream_t st, bool cx) {
   const long len2 = len / 2;
+  const int K = cx ? 2 : 1;
   for (int g0 = 0; g0 < nv; g0 += 8) {
     int ng = nv - g0 < 8 ? nv - g0 : 8;
     VecPtrs p = pack(V + g0, ng);
     const bool last = g0 + ng >= nv;
+    const double* cf = coef_dev + K * g0;
     if (last && want_dot == 2) {
-      NV_SWITCH(ng, (k_axpy_dot<NVc, 2><<<grid, 256, 0, st>>>(p, coef_dev + g0, w, len2, partial)));
+      if (cx) NV_SWITCH(ng, (k_axpy_dot<NVc, 2, true><<<grid, 256, 0, st>>>(p, cf, w, len2, partial)))
+      else NV_SWITCH(ng, (k_axpy_dot<NVc, 2, false><<<grid, 256, 0, st>>>(p, cf, w, len2, partial)))
       k_reduce_rows<<<1, 32, 0, st>>>(partial, grid, 1, out);
     } else if (last && want_dot == 1 && nv <= 8) {
-      NV_SWITCH(ng, (k_axpy_dot<NVc, 1><<<grid, 256, 0, st>>>(p, coef_dev + g0, w, len2, partial)));
-      k_reduce_rows<<<ng, 32, 0, st>>>(partial, grid, ng, out);
+      if (cx) NV_SWITCH(ng, (k_axpy_dot<NVc, 1, true><<<grid, 256, 0, st>>>(p, cf, w, len2, partial)))
+      else NV_SWITCH(ng, (k_axpy_dot<NVc, 1, false><<<grid, 256, 0, st>>>(p, cf, w, len2, partial)))
+      k_reduce_rows<<<K * ng, 32, 0, st>>>(partial, grid, K * ng, out);
     } else {
-      NV_SWITCH(ng, (k_axpy_dot<NVc, 0><<<grid, 256, 0, st>>>(p, coef_dev + g0, w, len2, partial)));
+      if (cx) NV_SWITCH(ng, (k_axpy_dot<NVc, 0, true><<<grid, 256, 0, st>>>(p, cf, w, len2, partial)))
+      else NV_SWITCH(ng, (k_axpy_dot<NVc, 0, false><<<grid, 256, 0, st>>>(p, cf, w, len2, partial)))
     }
   }
-  if (want_dot == 1 && nv > 8) return multi_dot(V, nv, w, len, partial, grid, out, st);
+  if (want_dot == 1 && nv > 8) return multi_dot(V, nv, w, len, partial, grid, out, st, cx);
   return cudaGetLastError();
 }
 
 cudaError_t lincomb_add(const double* const* V, int nv, const double* coef_dev, double* x, long len,
-                        cudaStream_t st) {
+                        cudaStream_t st, bool cx) {
   const long len2 = len / 2;
+  const int K = cx ? 2 : 1;
   for (int g0 = 0; g0 < nv; g0 += 8) {
     int ng = nv - g0 < 8 ? nv - g0 : 8;
     VecPtrs p = pack(V + g0, ng);
-    NV_SWITCH(ng, (k_lincomb<NVc><<<vec_grid(148), 256, 0, st>>>(p, coef_dev + g0, x, len2)));
+    if (cx) NV_SWITCH(ng, (k_lincomb<NVc, true><<<vec_grid(148), 256, 0, st>>>(p, coef_dev + K * g0, x, len2)))
+    else NV_SWITCH(ng, (k_lincomb<NVc, false><<<vec_grid(148), 256, 0, st>>>(p, coef_dev + K * g0, x, len2)))
   }
+  return cudaGetLastError();
+}
+
+// complex interleaved slices <-> planar (re slice, im slice) pairs: slice t of `in` (len
+// complex entries at stride in_stride doubles) -> slices 2t, 2t+1 of `out` (stride
+// out_stride).  Complex plans run the real DST on the planar pairs (V is real).
+__global__ void k_cx_split(const double* __restrict__ in, long in_stride, long len, double* __restrict__ out,
+                           long out_stride, long nslices) {
+  const long total = len * nslices;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    const long t = e / len, i = e - t * len;
+    const double2 v = __ldcs(reinterpret_cast<const double2*>(in + t * in_stride) + i);
+    out[2 * t * out_stride + i] = v.x;
+    out[(2 * t + 1) * out_stride + i] = v.y;
+  }
+}
+__global__ void k_cx_merge(const double* __restrict__ in, long in_stride, long len, double* __restrict__ out,
+                           long out_stride, long nslices) {
+  const long total = len * nslices;
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < total; e += (long)gridDim.x * blockDim.x) {
+    const long t = e / len, i = e - t * len;
+    const double2 v = make_double2(__ldcs(in + 2 * t * in_stride + i), __ldcs(in + (2 * t + 1) * in_stride + i));
+    reinterpret_cast<double2*>(out + t * out_stride)[i] = v;
+  }
+}
+cudaError_t cx_split(const double* in, long in_stride, long len, double* out, long out_stride, long nslices,
+                     cudaStream_t st) {
+  k_cx_split<<<1184, 256, 0, st>>>(in, in_stride, len, out, out_stride, nslices);
+  return cudaGetLastError();
+}
+cudaError_t cx_merge(const double* in, long in_stride, long len, double* out, long out_stride, long nslices,
+                     cudaStream_t st) {
+  k_cx_merge<<<1184, 256, 0, st>>>(in, in_stride, len, out, out_stride, nslices);
   return cudaGetLastError();
 }
 

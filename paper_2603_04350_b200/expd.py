@@ -76,6 +76,8 @@ class _Problem(C.Structure):
         ("scheme", C.c_int),
         ("npoly", C.c_int),
         ("q", C.c_double * 8),
+        ("a_im", C.c_double),
+        ("c_im", C.c_double),
     ]
 
 
@@ -161,10 +163,21 @@ class Problem:
     alpha: float
     scheme: int = 0
     q: tuple = field(default_factory=tuple)
+    a_im: float = 0.0  # imaginary parts of a, c: a complex plan (complex128 vectors, linear only)
+    c_im: float = 0.0
 
     @classmethod
     def from_config(cls, cfg) -> "Problem":
-        return cls(cfg.dim, cfg.n, cfg.a, cfg.c, cfg.T / cfg.nt, cfg.nt, cfg.alpha, cfg.scheme, tuple(cfg.q))
+        return cls(cfg.dim, cfg.n, cfg.a, cfg.c, cfg.T / cfg.nt, cfg.nt, cfg.alpha, cfg.scheme, tuple(cfg.q),
+                   getattr(cfg, "a_im", 0.0), getattr(cfg, "c_im", 0.0))
+
+    @property
+    def is_complex(self) -> bool:
+        return self.a_im != 0.0 or self.c_im != 0.0
+
+    @property
+    def dtype(self) -> torch.dtype:
+        return torch.complex128 if self.is_complex else torch.float64
 
     @property
     def N(self) -> int:
@@ -180,6 +193,7 @@ class Problem:
         p.scheme, p.npoly = self.scheme, len(self.q)
         for i, v in enumerate(self.q):
             p.q[i] = float(v)
+        p.a_im, p.c_im = float(self.a_im), float(self.c_im)
         return p
 
 
@@ -250,11 +264,11 @@ class Comm:
             pass
 
 
-def _ptr(t: torch.Tensor | None):
+def _ptr(t: torch.Tensor | None, dtype: torch.dtype = torch.float64):
     if t is None:
         return None
-    if not (t.is_cuda and t.dtype == torch.float64 and t.is_contiguous()):
-        raise ValueError("expected a contiguous float64 CUDA tensor")
+    if not (t.is_cuda and t.dtype == dtype and t.is_contiguous()):
+        raise ValueError(f"expected a contiguous {dtype} CUDA tensor")
     return C.c_void_p(t.data_ptr())
 
 
@@ -306,20 +320,24 @@ class Plan:
 
     def _vec(self):
         """A physical space-time vector of this rank: its time slab (all nt slices on one GPU)."""
-        return torch.empty((self.layout["nt_local"],) + self.problem.shape, dtype=torch.float64,
+        return torch.empty((self.layout["nt_local"],) + self.problem.shape, dtype=self.problem.dtype,
                            device=f"cuda:{self.device}")
+
+    def _a(self, t):
+        """A state argument (u0, U, R, S): float64, or complex128 for a complex plan."""
+        return _ptr(t, self.problem.dtype)
 
     # ---- primitives ------------------------------------------------------------------
     def residual(self, u0: torch.Tensor, U: torch.Tensor, R: torch.Tensor | None = None, norm: bool = False):
         R = self._vec() if R is None else R
         rn = C.c_double()
-        self._check(self.lib.expd_residual(self.handle, _ptr(u0), _ptr(U), _ptr(R),
+        self._check(self.lib.expd_residual(self.handle, self._a(u0), self._a(U), self._a(R),
                                            C.pointer(rn) if norm else None))
         return (R, rn.value) if norm else R
 
     def precond_apply(self, R: torch.Tensor, S: torch.Tensor | None = None):
         S = self._vec() if S is None else S
-        self._check(self.lib.expd_precond_apply(self.handle, _ptr(R), _ptr(S)))
+        self._check(self.lib.expd_precond_apply(self.handle, self._a(R), self._a(S)))
         return S
 
     # ---- solvers ---------------------------------------------------------------------
@@ -344,7 +362,7 @@ class Plan:
     def fixed_point_solve(self, u0, U=None, tol=1e-12, maxit=100):
         U = self._vec().zero_() if U is None else U
         r, hist = self._report(maxit)
-        st = self.lib.expd_fixed_point_solve(self.handle, _ptr(u0), _ptr(U), tol, maxit, C.byref(r))
+        st = self.lib.expd_fixed_point_solve(self.handle, self._a(u0), self._a(U), tol, maxit, C.byref(r))
         if st not in (EXPD_OK, 7):
             self._check(st)
         return U, self._rdict(r, hist, st)
@@ -352,7 +370,7 @@ class Plan:
     def gmres_solve(self, u0, U=None, tol=1e-12, restart=20, maxit=100):
         U = self._vec().zero_() if U is None else U
         r, hist = self._report(maxit)
-        st = self.lib.expd_gmres_solve(self.handle, _ptr(u0), _ptr(U), tol, restart, maxit, C.byref(r))
+        st = self.lib.expd_gmres_solve(self.handle, self._a(u0), self._a(U), tol, restart, maxit, C.byref(r))
         if st not in (EXPD_OK, 7):
             self._check(st)
         return U, self._rdict(r, hist, st)
@@ -360,14 +378,14 @@ class Plan:
     def bicgstab_solve(self, u0, U=None, tol=1e-12, maxit=100):
         U = self._vec().zero_() if U is None else U
         r, hist = self._report(maxit)
-        st = self.lib.expd_bicgstab_solve(self.handle, _ptr(u0), _ptr(U), tol, maxit, C.byref(r))
+        st = self.lib.expd_bicgstab_solve(self.handle, self._a(u0), self._a(U), tol, maxit, C.byref(r))
         if st not in (EXPD_OK, 7):
             self._check(st)
         return U, self._rdict(r, hist, st)
 
     # ---- spectral-state sweep (benchmark / fine-grained driving) ----------------------
     def load_state(self, u0, U=None):
-        self._check(self.lib.expd_load_state(self.handle, _ptr(u0), _ptr(U)))
+        self._check(self.lib.expd_load_state(self.handle, self._a(u0), self._a(U)))
 
     def sweep(self):
         self._check(self.lib.expd_sweep(self.handle))
@@ -378,7 +396,7 @@ class Plan:
         return v.value
 
     def store_state(self, U):
-        self._check(self.lib.expd_store_state(self.handle, _ptr(U)))
+        self._check(self.lib.expd_store_state(self.handle, self._a(U)))
 
     def dst(self, x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """V x for a stack of physical slices [..., n, ..., n]."""

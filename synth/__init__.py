@@ -33,6 +33,12 @@ class Config:
     solvers: tuple = ("fixed_point",)
     tol: float = 1e-12  # reading R9
     seed: int = 0
+    a_im: float = 0.0  # imaginary parts of a, c: complex state (NEXT-4, Schroedinger)
+    c_im: float = 0.0
+
+    @property
+    def is_complex(self) -> bool:
+        return self.a_im != 0.0 or self.c_im != 0.0
 
     @property
     def dt(self) -> float:
@@ -77,6 +83,14 @@ CONFIGS = {
     "c2bdf2": Config("c2bdf2", 2, 255, 0.5, 1.0, 1.0, 64, 1e-3, scheme=3, solvers=("fixed_point", "gmres"), seed=2),
     "c3if": Config("c3if", 2, 511, 1.0, 1.0, 0.5, 128, 1e-3, scheme=2, q=CUBIC, seed=3),
     "c5if": Config("c5if", 2, 2047, 0.1, 0.5, 1.0, 256, 1e-3, scheme=2, q=CUBIC, seed=5),
+    # NEXT-4: complex coefficients, the paper's Schroedinger tests.
+    # c6se: 1D, a = i, c = 2i, u0 = sin(pi x), h = 1/128, dt = 0.01
+    "c6se": Config("c6se", 1, 127, 0.0, 0.0, 2.56, 256, 1e-3, solvers=("gmres", "fixed_point"), a_im=1.0,
+                   c_im=2.0, seed=6),
+    # c7se: 2D, a = i, c = 200i, Gaussian wave packet u0 (the paper
+    # runs it with BDF2 on h = 1/40 -- here exponential Euler on a 1023^2 grid)
+    "c7se": Config("c7se", 2, 1023, 0.0, 0.0, 0.64, 128, 1e-3, solvers=("fixed_point", "gmres"), a_im=1.0,
+                   c_im=200.0, seed=7),
 }
 
 
@@ -125,6 +139,15 @@ def initial_condition(cfg: Config) -> np.ndarray:
             nb = p[:-2, 1:-1] + p[2:, 1:-1] + p[1:-1, :-2] + p[1:-1, 2:]
             u = (1.0 - w) * u + w * nb / 4.0
         return u
+    if cfg.name.startswith("c6"):
+        return sine_table(n, 1)[0].astype(np.complex128)  # sin(pi x)
+    if cfg.name.startswith("c7"):
+        # exp(-((x-1/2)^2 + (y-1/2)^2) / (2 mu^2)) exp(-5 i (x - 1/2)), mu = 0.05
+        x = np.arange(1, n + 1) / (n + 1) - 0.5
+        mu = 0.05
+        gx = np.exp(-x * x / (2 * mu * mu)) * np.exp(-5j * x)
+        gy = np.exp(-x * x / (2 * mu * mu))
+        return np.multiply.outer(gy, gx)  # [y][x]
     if cfg.name.startswith("c5"):
         rng = np.random.default_rng(cfg.seed)
         K = min(64, n)
@@ -139,6 +162,9 @@ def initial_condition(cfg: Config) -> np.ndarray:
 def random_spacetime(cfg: Config, seed: int | None = None, scale: float = 1.0) -> np.ndarray:
     """Seeded standard-normal space-time vector [nt][n..n] (parity inputs, seeds 100+cfg)."""
     rng = np.random.default_rng(100 + cfg.seed if seed is None else seed)
+    if cfg.is_complex:  # complex state: independent N(0,1) real and imaginary parts
+        re = rng.standard_normal((cfg.nt,) + cfg.shape)
+        return scale * (re + 1j * rng.standard_normal((cfg.nt,) + cfg.shape))
     return scale * rng.standard_normal((cfg.nt,) + cfg.shape)
 
 
