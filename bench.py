@@ -51,8 +51,29 @@ def dst_flops_per_line_pair(M: int) -> float:
 BYTES_PER_DOF = {  # algorithmic fp64 bytes per space-time dof
     "k1_linear": 16,      # read U-hat, write U-hat
     "k1_nonlinear": 24,   # read U-hat, read N-hat, write U-hat
+    "k1_complex": 32,     # complex dof (NEXT-4): read U-hat (re, im), write U-hat (re, im)
     "stage3": 16,         # read U-hat slice, write N-hat slice
 }
+
+
+def workload_label(cfg) -> str:
+    if getattr(cfg, "is_complex", False):
+        return (f"{cfg.name}: {cfg.dim}D n={cfg.n} Nt={cfg.nt} complex a={cfg.a}+{cfg.a_im}i c={cfg.c}+{cfg.c_im}i "
+                f"exp. Euler fixed-point sweep (Schroedinger, PAPER.md:983/1064; NEXT-4)")
+    src = {"c1": ":7", "c2": ":8", "c3": ":9", "c4": ":10", "c5": ":11"}.get(cfg.name)
+    return (f"{cfg.name}: {cfg.dim}D n={cfg.n} Nt={cfg.nt} "
+            f"{ {0: 'exp. Euler' if not cfg.q else 'ETD1', 1: 'ETD2', 2: 'IF/IMEX', 3: 'BDF2'}[cfg.scheme] } "
+            f"{'Picard' if cfg.q else 'fixed-point'} sweep" + (f" (BASELINE.json{src})" if src else ""))
+
+
+def oracle_dsts_per_slice(cfg) -> float:
+    """Real-DST-equivalent transforms per time slice in one oracle sweep: residual (A = V E V:
+    2; ETD adds the Phi products: 2 each), Step (b) (DST + IDST of the real and imaginary
+    parts of the DFT'd slice: 4).  A complex DST is two real ones."""
+    if getattr(cfg, "is_complex", False):
+        return 8.0
+    res = 2.0 + (2.0 if cfg.q and cfg.scheme == 0 else 0.0) + (4.0 if cfg.q and cfg.scheme == 1 else 0.0)
+    return res + 4.0
 
 
 def parse():
@@ -153,7 +174,7 @@ def oracle_sample_step(cfg, u_rows):
 
     oracle.dst_x_rows(oracle.spec(cfg), u_rows)
     rows_per_slice = cfg.n ** (cfg.dim - 1)
-    return cfg.nst * u_rows.shape[0] / (10.0 * cfg.dim * rows_per_slice * cfg.nt)
+    return cfg.nst * u_rows.shape[0] / (oracle_dsts_per_slice(cfg) * cfg.dim * rows_per_slice * cfg.nt)
 
 
 def cpu_baseline(cfg, nsamples=4):
@@ -205,7 +226,7 @@ def run_reference(args):
         "unit": "DOF-iter/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": 1e3 * dt / max(args.steps, 1), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f80 (long double accumulation)", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: {cfg.dim}D n={cfg.n} Nt={cfg.nt} ETD2 Picard sweep (BASELINE.json:11)"},
+        "config": {"workload": workload_label(cfg)},
         "cpu_baseline": {"value": value, "unit": "DOF-iter/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
                          "kind": "oracle",
                          "sample": f"each step: oracle x-axis DST-I of {REF_ROWS} rows of a {cfg.name} slice = "
@@ -249,6 +270,8 @@ def run_ours(args):
     plan.load_state(u0, None)
     plan.set_profiling(True)
     nl = len(cfg.q) > 0
+    cx = cfg.is_complex
+    esz = 16 if cx else 8  # bytes per state entry (complex128 / float64)
 
     def step():
         plan.sweep()
@@ -289,7 +312,7 @@ def run_ours(args):
     # this rank's share: K1 on its mode slab (nt x mode_len padded entries, of which the
     # n^dim real modes are counted), stage 3 on its time slab
     share = lay["mode_len"] / lay["npad"]
-    k1_bytes = (BYTES_PER_DOF["k1_nonlinear"] if nl else BYTES_PER_DOF["k1_linear"]) * cfg.nst * share
+    k1_bytes = BYTES_PER_DOF["k1_complex" if cx else ("k1_nonlinear" if nl else "k1_linear")] * cfg.nst * share
     s3_slices = (cfg.nt - 1) if ws == 1 else lay["nt_local"]
     s3_bytes = BYTES_PER_DOF["stage3"] * cfg.N * s3_slices if nl else 0
     k1_ms = statistics.mean(ms_k1)
@@ -345,9 +368,9 @@ def run_ours(args):
     e2e = None
     if not args.no_e2e:
         u0_h = torch.from_numpy(synth.initial_condition(cfg)).pin_memory()
-        U_h = torch.empty((lay["nt_local"],) + cfg.shape, dtype=torch.float64).pin_memory()
+        U_h = torch.empty((lay["nt_local"],) + cfg.shape, dtype=prob.dtype).pin_memory()
         u0_d = torch.empty_like(u0_h, device=dev)
-        U_d = torch.empty((lay["nt_local"],) + cfg.shape, dtype=torch.float64, device=dev)
+        U_d = torch.empty((lay["nt_local"],) + cfg.shape, dtype=prob.dtype, device=dev)
         plan.set_profiling(False)
         tot_ms, tot_sweeps = 0.0, 0
         for i in range(args.e2e_steps + 1):
@@ -369,7 +392,7 @@ def run_ours(args):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             tot_ms = float(t.item())
         e2e = {"value": cfg.nst * tot_sweeps / (tot_ms * 1e-3), "unit": "DOF-iter/s",
-               "h2d_bytes_per_step": u0_h.numel() * 8 * ws, "d2h_bytes_per_step": cfg.nst * 8,
+               "h2d_bytes_per_step": u0_h.numel() * esz * ws, "d2h_bytes_per_step": cfg.nst * esz,
                "what": f"full fixed-point solve per step ({rep['sweeps']} sweeps, {rep['iterations']} iterations, "
                        f"rel residual {rep['rel_residual']:.2e}) incl. setup DSTs, final IDST and host copies"}
 
@@ -384,12 +407,12 @@ def run_ours(args):
     line = {
         "metric": "space-time DOF-iterations/s per Exp-ParaDiag sweep", "value": value, "unit": "DOF-iter/s",
         "n_gpus": ws, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"{cfg.name}: {cfg.dim}D n={cfg.n} Nt={cfg.nt} "
-                               f"{'ETD2' if cfg.scheme == 1 else 'exp. Euler'} "
-                               f"{'Picard' if nl else 'fixed-point'} sweep (BASELINE.json:11)",
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "c128" if cx else "f64", "data": "synthetic",
+        "config": {"workload": workload_label(cfg),
                    "n_st": cfg.nst, "alpha": cfg.alpha,
-                   "l2": "inputs 8.6 GB per space-time array >> 126 MB L2 (no flush needed)",
+                   "l2": f"inputs {cfg.nst * esz / 1e9:.1f} GB per space-time array "
+                         f"{'>>' if cfg.nst * esz > 126e6 else '<'} 126 MB L2"
+                         f"{' (no flush needed)' if cfg.nst * esz > 126e6 else ' (L2-resident: not a roofline number)'}",
                    "parallelism": "single GPU" if ws == 1 else
                    f"{ws} GPUs: mode slabs (K1) / time slabs (stage 3), NCCL all-to-all + allreduce"},
         "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
