@@ -74,8 +74,8 @@ typedef struct {
                          (npoly = 0), scheme EXPD_EXP_EULER, one GPU (no expd_dist).  Every
                          space-time / slice argument of a complex plan (u0, U, R, S) is
                          complex128: interleaved (re, im) doubles, 2 N doubles per slice.
-                         GMRES runs over C with the Hermitian inner product (reading R18);
-                         BiCGStab, expd_dst / expd_nonlin_hat stay real-only.            */
+                         GMRES and BiCGStab run over C with the Hermitian inner product
+                         (reading R18); expd_dst / expd_nonlin_hat stay real-only.       */
 } expd_problem;
 
 typedef struct {

@@ -123,6 +123,7 @@ def lib():
             "orc_cplx_apply_Q": (None, [pp, dp, dp]),
             "orc_cplx_fixed_point": (C.c_int, [pp, dp, dp, C.c_double, C.c_int, dp, C.POINTER(C.c_int)]),
             "orc_cplx_gmres": (C.c_int, [pp, dp, dp, C.c_double, C.c_int, C.c_int, dp, C.POINTER(C.c_int)]),
+            "orc_cplx_bicgstab": (C.c_int, [pp, dp, dp, C.c_double, C.c_int, dp, C.POINTER(C.c_int)]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -365,4 +366,14 @@ def cplx_gmres(s: Spec, u0, U=None, tol=1e-12, restart=20, maxit=100):
     its = C.c_int()
     p = s.c_struct()
     st = lib().orc_cplx_gmres(C.byref(p), _pc(u0), _pc(U), tol, restart, maxit, _p(hist), C.byref(its))
+    return U, st, its.value, hist[: its.value + 1].copy()
+
+
+def cplx_bicgstab(s: Spec, u0, U=None, tol=1e-12, maxit=100):
+    u0 = _c128(u0)
+    U = np.zeros((s.nt,) + u0.shape, dtype=np.complex128) if U is None else _c128(U).copy()
+    hist = np.zeros(maxit + 1)
+    its = C.c_int()
+    p = s.c_struct()
+    st = lib().orc_cplx_bicgstab(C.byref(p), _pc(u0), _pc(U), tol, maxit, _p(hist), C.byref(its))
     return U, st, its.value, hist[: its.value + 1].copy()

@@ -113,6 +113,8 @@ int orc_cplx_fixed_point(const orc_problem* p, const double* u0, double* U, doub
                          int* iterations);
 int orc_cplx_gmres(const orc_problem* p, const double* u0, double* U, double tol, int restart, int maxit,
                    double* hist, int* iterations);
+int orc_cplx_bicgstab(const orc_problem* p, const double* u0, double* U, double tol, int maxit, double* hist,
+                      int* iterations);
 
 #ifdef __cplusplus
 }

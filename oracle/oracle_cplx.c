@@ -369,3 +369,59 @@ int orc_cplx_gmres(const orc_problem* p, const double* u0, double* U, double tol
   cctx_free(&c);
   return status;
 }
+
+/* left-preconditioned BiCGStab over C (reading R17 with the Hermitian inner product of
+   R18): the same steps as orc_bicgstab with rho = <r-hat, r>, alpha = rho / <r-hat, v>,
+   omega = <t, s> / <t, t>, <v, w> = sum conj(v) w */
+int orc_cplx_bicgstab(const orc_problem* p, const double* u0, double* U, double tol, int maxit, double* hist,
+                      int* iterations) {
+  cctx c;
+  cctx_init(&c, p);
+  size_t N = (size_t)c.N, tot = N * (size_t)p->nt;
+  lc *u = load_c(u0, N), *x = load_c(U, tot);
+  lc *r = (lc*)malloc(sizeof(lc) * tot), *rh = (lc*)malloc(sizeof(lc) * tot);
+  lc *pv = (lc*)calloc(tot, sizeof(lc)), *v = (lc*)calloc(tot, sizeof(lc));
+  lc *s = (lc*)malloc(sizeof(lc) * tot), *t = (lc*)malloc(sizeof(lc) * tot), *w = (lc*)malloc(sizeof(lc) * tot);
+  cresidual(&c, u, x, w); /* f - Q x */
+  cprecond(&c, w, r);     /* r_0 */
+  memcpy(rh, r, sizeof(lc) * tot);
+  ld beta0 = sqrtl(rdot(r, r, tot));
+  if (hist) hist[0] = 1.0;
+  int status = 7, its = 0;
+  lc rho_prev = 1.0L, al = 1.0L, om = 1.0L;
+  if (beta0 == 0.0L) status = 0;
+  for (int i = 0; status != 0 && i < maxit; ++i) {
+    lc rho = cdot(rh, r, tot);
+    lc beta = (rho / rho_prev) * (al / om);
+    for (size_t q = 0; q < tot; ++q) pv[q] = r[q] + beta * (pv[q] - om * v[q]);
+    capply_Q(&c, pv, w);
+    cprecond(&c, w, v); /* v = Q_a^{-1} Q p */
+    al = rho / cdot(rh, v, tot);
+    for (size_t q = 0; q < tot; ++q) s[q] = r[q] - al * v[q];
+    ld sn = sqrtl(rdot(s, s, tot));
+    if (sn / beta0 < (ld)tol) { /* half step */
+      for (size_t q = 0; q < tot; ++q) x[q] += al * pv[q];
+      its = i + 1;
+      if (hist) hist[its] = (double)(sn / beta0);
+      status = 0;
+      break;
+    }
+    capply_Q(&c, s, w);
+    cprecond(&c, w, t); /* t = Q_a^{-1} Q s */
+    om = cdot(t, s, tot) / rdot(t, t, tot);
+    for (size_t q = 0; q < tot; ++q) {
+      x[q] += al * pv[q] + om * s[q];
+      r[q] = s[q] - om * t[q];
+    }
+    rho_prev = rho;
+    its = i + 1;
+    ld rn = sqrtl(rdot(r, r, tot));
+    if (hist) hist[its] = (double)(rn / beta0);
+    if (rn / beta0 < (ld)tol) { status = 0; break; }
+  }
+  if (iterations) *iterations = its;
+  store_c(x, U, tot);
+  free(u); free(x); free(r); free(rh); free(pv); free(v); free(s); free(t); free(w);
+  cctx_free(&c);
+  return status;
+}

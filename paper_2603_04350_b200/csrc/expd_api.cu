@@ -924,14 +924,13 @@ extern "C" expd_status expd_gmres_solve(expd_plan* p, const double* u0, double* 
 // with the half-step test): the operator B v = Q_alpha^{-1} Q v is one K1 pass (RM_QOP); the
 // inner products are multi-dot partials (allreduced when distributed) read to the host.
 // ---------------------------------------------------------------------------------------
-extern "C" expd_status expd_bicgstab_solve(expd_plan* p, const double* u0, double* U, double tol, int maxit,
-                                           expd_report* report) {
-  expd_status s = ready(p);
-  if (s) return s;
-  if (!u0 || !U || maxit < 0 || !(tol >= 0.0)) return fail(p, EXPD_ERR_INVALID_ARG, "bicgstab: bad args");
-  if (p->nl) return fail(p, EXPD_ERR_UNSUPPORTED, "BiCGStab is for linear problems (npoly == 0)");
-  if (p->cx) return fail(p, EXPD_ERR_UNSUPPORTED, "BiCGStab: real plans only");
-  if (p->krylov_cap < 6) return fail(p, EXPD_ERR_OOM, "BiCGStab needs 6 work vectors in the workspace");
+template <class T>
+static expd_status bicgstab_impl(expd_plan* p, const double* u0, double* U, double tol, int maxit,
+                                 expd_report* report) {
+  using SC = Scal<T>;
+  constexpr int K = SC::K;
+  constexpr bool CX = K == 2;
+  expd_status s;
   const long len = (long)p->prob.nt * p->mlen;
   const size_t vstride = align_up(sizeof(double) * (size_t)len) / sizeof(double);
   double* r = p->krylov;
@@ -944,8 +943,18 @@ extern "C" expd_status expd_bicgstab_solve(expd_plan* p, const double* u0, doubl
   double* dcoef = p->dscal + 128;
   s = expd_load_state(p, u0, U);
   if (s) return s;
-  auto dot = [&](const double* a, const double* b, double* out) -> expd_status {
-    CUDA_TRY(p, multi_dot(&a, 1, b, len, p->partial, p->vgrid, p->dscal, p->stream));
+  // <a, b> (Hermitian for complex plans) and ||a||^2, completed by allreduce, read to the host
+  auto dot = [&](const double* a, const double* b, T* out) -> expd_status {
+    CUDA_TRY(p, multi_dot(&a, 1, b, len, p->partial, p->vgrid, p->dscal, p->stream, CX));
+    expd_status e = allreduce(p, p->dscal, K);
+    if (e) return e;
+    double h[2];
+    if ((e = read_scalars(p, K, h))) return e;
+    *out = SC::get(h);
+    return EXPD_OK;
+  };
+  auto nrm2 = [&](const double* a, double* out) -> expd_status {
+    CUDA_TRY(p, multi_dot(&a, 1, a, len, p->partial, p->vgrid, p->dscal, p->stream));
     expd_status e = allreduce(p, p->dscal, 1);
     if (e) return e;
     return read_scalars(p, 1, out);
@@ -956,14 +965,22 @@ extern "C" expd_status expd_bicgstab_solve(expd_plan* p, const double* u0, doubl
     return EXPD_OK;
   };
   // out += sum_i c_i V_i (coefficients staged through pinned host memory)
-  auto axpy = [&](double* out, std::initializer_list<const double*> V, std::initializer_list<double> c)
-      -> expd_status {
+  auto axpy = [&](double* out, std::initializer_list<const double*> V, std::initializer_list<T> c) -> expd_status {
     std::vector<const double*> vp(V);
-    std::vector<double> cv(c);
+    std::vector<T> cv(c);
     CUDA_TRY(p, cudaStreamSynchronize(p->stream));  // h_pin may still feed an earlier copy
-    for (size_t i = 0; i < cv.size(); ++i) p->h_pin[i] = cv[i];
-    CUDA_TRY(p, cudaMemcpyAsync(dcoef, p->h_pin, sizeof(double) * cv.size(), cudaMemcpyHostToDevice, p->stream));
-    CUDA_TRY(p, lincomb_add(vp.data(), (int)vp.size(), dcoef, out, len, p->stream));
+    for (size_t i = 0; i < cv.size(); ++i) SC::put(p->h_pin + K * i, cv[i]);
+    CUDA_TRY(p, cudaMemcpyAsync(dcoef, p->h_pin, sizeof(double) * K * cv.size(), cudaMemcpyHostToDevice, p->stream));
+    CUDA_TRY(p, lincomb_add(vp.data(), (int)vp.size(), dcoef, out, len, p->stream, CX));
+    return EXPD_OK;
+  };
+  // y = c y (a complex c scales the interleaved (re, im) pairs)
+  auto scale = [&](double* y, T c) -> expd_status {
+    if constexpr (CX) {
+      CUDA_TRY(p, scale_copy_cx(y, c.real(), c.imag(), y, len, p->stream));
+    } else {
+      CUDA_TRY(p, scale_copy(y, c, y, len, p->stream));
+    }
     return EXPD_OK;
   };
   CUDA_TRY(p, cudaMemsetAsync(pv, 0, sizeof(double) * len, p->stream));
@@ -974,25 +991,26 @@ extern "C" expd_status expd_bicgstab_solve(expd_plan* p, const double* u0, doubl
     CUDA_TRY(p, scale_copy(r, 1.0, rh, len, p->stream));
   }
   double b2;
-  if ((s = dot(r, r, &b2))) return s;
+  if ((s = nrm2(r, &b2))) return s;
   const double beta0 = std::sqrt(b2);
   std::vector<double> hist{1.0};
   int its = 0, conv = beta0 == 0.0 ? 1 : 0;
-  double rho_prev = 1.0, al = 1.0, om = 1.0;
+  T rho_prev = 1.0, al = 1.0, om = 1.0;
   auto t0 = std::chrono::steady_clock::now();
   for (int i = 0; !conv && i < maxit; ++i) {
-    double rho, rv, ts, tt, sn2, rn2;
+    T rho, rv, ts;
+    double tt, sn2, rn2;
     if ((s = dot(rh, r, &rho))) return s;
-    const double beta = (rho / rho_prev) * (al / om);
+    const T beta = (rho / rho_prev) * (al / om);
     // p = r + beta (p - om v) = beta p + r - beta om v
-    CUDA_TRY(p, scale_copy(pv, beta, pv, len, p->stream));
-    if ((s = axpy(pv, {r, v}, {1.0, -beta * om}))) return s;
+    if ((s = scale(pv, beta))) return s;
+    if ((s = axpy(pv, {r, v}, {T(1.0), -beta * om}))) return s;
     if ((s = bop(pv, v))) return s;
     if ((s = dot(rh, v, &rv))) return s;
     al = rho / rv;
     CUDA_TRY(p, scale_copy(r, 1.0, sv, len, p->stream));  // s = r - al v
     if ((s = axpy(sv, {v}, {-al}))) return s;
-    if ((s = dot(sv, sv, &sn2))) return s;
+    if ((s = nrm2(sv, &sn2))) return s;
     if (std::sqrt(sn2) / beta0 < tol) {  // half step
       if ((s = axpy(x, {pv}, {al}))) return s;
       its = i + 1;
@@ -1002,14 +1020,14 @@ extern "C" expd_status expd_bicgstab_solve(expd_plan* p, const double* u0, doubl
     }
     if ((s = bop(sv, t))) return s;
     if ((s = dot(t, sv, &ts))) return s;
-    if ((s = dot(t, t, &tt))) return s;
+    if ((s = nrm2(t, &tt))) return s;
     om = ts / tt;
     if ((s = axpy(x, {pv, sv}, {al, om}))) return s;
     CUDA_TRY(p, scale_copy(sv, 1.0, r, len, p->stream));  // r = s - om t
     if ((s = axpy(r, {t}, {-om}))) return s;
     rho_prev = rho;
     its = i + 1;
-    if ((s = dot(r, r, &rn2))) return s;
+    if ((s = nrm2(r, &rn2))) return s;
     hist.push_back(std::sqrt(rn2) / beta0);
     if (hist.back() < tol) conv = 1;
   }
@@ -1019,5 +1037,16 @@ extern "C" expd_status expd_bicgstab_solve(expd_plan* p, const double* u0, doubl
   if (s) return s;
   CUDA_TRY(p, cudaStreamSynchronize(p->stream));
   return conv ? EXPD_OK : EXPD_ERR_NOT_CONVERGED;
+}
+
+extern "C" expd_status expd_bicgstab_solve(expd_plan* p, const double* u0, double* U, double tol, int maxit,
+                                           expd_report* report) {
+  expd_status s = ready(p);
+  if (s) return s;
+  if (!u0 || !U || maxit < 0 || !(tol >= 0.0)) return fail(p, EXPD_ERR_INVALID_ARG, "bicgstab: bad args");
+  if (p->nl) return fail(p, EXPD_ERR_UNSUPPORTED, "BiCGStab is for linear problems (npoly == 0)");
+  if (p->krylov_cap < 6) return fail(p, EXPD_ERR_OOM, "BiCGStab needs 6 work vectors in the workspace");
+  if (p->cx) return bicgstab_impl<std::complex<double>>(p, u0, U, tol, maxit, report);
+  return bicgstab_impl<double>(p, u0, U, tol, maxit, report);
 }
 

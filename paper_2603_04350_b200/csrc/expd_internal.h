@@ -113,6 +113,7 @@ cudaError_t multi_dot(const double* const* V, int nv, const double* w, long len,
 cudaError_t multi_axpy_dot(const double* const* V, int nv, const double* coef_dev, double* w, long len,
                            double* partial, int grid, double* out, int want_dot, cudaStream_t st, bool cx = false);
 cudaError_t scale_copy(const double* x, double s, double* y, long len, cudaStream_t st);
+cudaError_t scale_copy_cx(const double* x, double sr, double si, double* y, long len, cudaStream_t st);
 cudaError_t lincomb_add(const double* const* V, int nv, const double* coef_dev, double* x, long len,
                         cudaStream_t st, bool cx = false);
 // complex interleaved slices <-> planar (re, im) slice pairs (complex plans)

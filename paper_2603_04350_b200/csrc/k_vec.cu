@@ -326,6 +326,21 @@ cudaError_t cx_merge(const double* in, long in_stride, long len, double* out, lo
   return cudaGetLastError();
 }
 
+// y = (s_re + i s_im) x on interleaved complex vectors (complex BiCGStab)
+__global__ void k_scale_copy_cx(const double* __restrict__ x, double sr, double si, double* y, long len2) {
+  const double2* x2 = reinterpret_cast<const double2*>(x);
+  double2* y2 = reinterpret_cast<double2*>(y);
+  for (long e = blockIdx.x * (long)blockDim.x + threadIdx.x; e < len2; e += (long)gridDim.x * blockDim.x) {
+    double2 a = x2[e];
+    y2[e] = make_double2(fma(sr, a.x, -si * a.y), fma(sr, a.y, si * a.x));
+  }
+}
+
+cudaError_t scale_copy_cx(const double* x, double sr, double si, double* y, long len, cudaStream_t st) {
+  k_scale_copy_cx<<<1184, 256, 0, st>>>(x, sr, si, y, len / 2);
+  return cudaGetLastError();
+}
+
 cudaError_t scale_copy(const double* x, double s, double* y, long len, cudaStream_t st) {
   k_scale_copy<<<1184, 256, 0, st>>>(x, s, y, len / 2);
   return cudaGetLastError();

@@ -148,3 +148,61 @@ def test_cplx_gmres_schroedinger_one_iteration(orc):
     U, st, its, hist = orc.cplx_gmres(s, u0, tol=1e-10, restart=20, maxit=20)
     assert st == 0 and its == 1
     assert rel(U, orc.cplx_sequential(s, u0)) < 1e-9
+
+
+def test_cplx_bicgstab_on_dense_system(orc):
+    """BiCGStab over C written out on the dense complex system Q_alpha^{-1} Q (test-side,
+    Hermitian inner products np.vdot) takes the oracle's steps: same history, same x."""
+    s = cspec(orc, 1, 4, 0.3 + 1j, 0.5 + 2j, T=0.5, nt=4, alpha=0.3)
+    rng = np.random.default_rng(4)
+    u0 = crandn(rng, 4)
+    A = sla.expm(s.dt * Lc(s))
+    Q = np.eye(16) - np.kron(alpha_circulant(4, 0.0), A)
+    Qa = dense_Qalpha_c(s, s.alpha)
+    B = np.linalg.solve(Qa, Q)
+    f = np.zeros(16, dtype=complex)
+    f[:4] = A @ u0
+    b = np.linalg.solve(Qa, f)
+    x = np.zeros_like(b)
+    r = b.copy()
+    rh = r.copy()
+    beta0 = np.linalg.norm(r)
+    rho_prev = al = om = 1.0
+    p = np.zeros_like(b)
+    v = np.zeros_like(b)
+    hist = [1.0]
+    for _ in range(30):
+        rho = np.vdot(rh, r)
+        beta = (rho / rho_prev) * (al / om)
+        p = r + beta * (p - om * v)
+        v = B @ p
+        al = rho / np.vdot(rh, v)
+        sv = r - al * v
+        if np.linalg.norm(sv) / beta0 < 1e-13:
+            x = x + al * p
+            hist.append(np.linalg.norm(sv) / beta0)
+            break
+        t = B @ sv
+        om = np.vdot(t, sv) / np.vdot(t, t).real
+        x = x + al * p + om * sv
+        r = sv - om * t
+        rho_prev = rho
+        hist.append(np.linalg.norm(r) / beta0)
+        if hist[-1] < 1e-13:
+            break
+    U, st, its, h = orc.cplx_bicgstab(s, u0, tol=1e-13, maxit=30)
+    assert st == 0 and its == len(hist) - 1 and its >= 2
+    big = np.array(hist) > 1e-10
+    assert np.allclose(h[big], np.array(hist)[big], rtol=1e-8)
+    assert rel(U.reshape(-1), x) < 1e-10
+    assert rel(U, orc.cplx_sequential(s, u0)) < 1e-10
+
+
+@pytest.mark.parametrize("a,c", COEFS)
+def test_cplx_bicgstab_matches_gmres_and_sequential(orc, a, c):
+    s = cspec(orc, 2, 4, a, c, T=0.4, nt=8, alpha=0.2)
+    u0 = crandn(np.random.default_rng(7), (4, 4))
+    Ub, st, its, _ = orc.cplx_bicgstab(s, u0, tol=1e-12, maxit=60)
+    Ug, st2, _, _ = orc.cplx_gmres(s, u0, tol=1e-12, restart=30, maxit=60)
+    assert st == 0 and st2 == 0
+    assert rel(Ub, Ug) < 1e-9 and rel(Ub, orc.cplx_sequential(s, u0)) < 1e-9
