@@ -30,10 +30,10 @@ cudaError_t launch_time_fused(const TimeArgs& a, int rmode, int outmode, int nl,
 // tiles per CTA-slot of the TMA variant: (pairs per tile, resident CTAs per SM)
 template <int NT>
 static void tma_shape(int nl, int& S, int& per_sm) {
-  if (k1_variant() == 1282) {
+  if (k1_variant(NT) == 1282) {
     S = TmaLayout<NT, 128, 1, 2>::S;
     per_sm = nl ? TmaLayout<NT, 128, 1, 2>::MINB : TmaLayout<NT, 128, 0, 2>::MINB;
-  } else if (k1_variant() == 2561) {
+  } else if (k1_variant(NT) == 2561) {
     S = TmaLayout<NT, 256, 1, 1>::S;
     per_sm = nl ? TmaLayout<NT, 256, 1, 1>::MINB : TmaLayout<NT, 256, 0, 1>::MINB;
   } else {

@@ -954,14 +954,17 @@ static int pipe_mode() {
 }
 // Variants: 2562 (default: 256 threads, double-buffered tiles, 1 CTA/SM), 2561 (single
 // stage, 2 CTAs/SM), 1282 (128 threads = 4 pairs per tile).  c5: 7.02 / 7.10 / 11.2 ms.
-static int k1_variant() {
+static int k1_variant(int nt) {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("EXPD_K1V");
-    v = e ? atoi(e) : 2562;
-    if (v != 2562 && v != 1282 && v != 2561) v = 2562;
+    v = e ? atoi(e) : 0;
+    if (v != 2562 && v != 1282 && v != 2561) v = 0;
   }
-  return v;
+  if (v) return v;
+  // default per Nt (measured, profiles/r01/k1_variants.txt): Nt = 128 runs best with
+  // 128-thread CTAs of 8 pairs (more resident CTAs hide the TMA latency), else 2562
+  return nt == 128 ? 1282 : 2562;
 }
 static bool use_pipe() { return pipe_mode() > 0; }
 
@@ -1007,14 +1010,14 @@ template <int NT, int RM, int OUTM, int NL>
 static cudaError_t launch_t(const TimeArgs& a, int grid, cudaStream_t st) {
   if constexpr (TimeGeo<NT>::L > 1 && (NL == 3 || NL == 4)) {  // BDF2 / complex: TMA or register kernel
     if (pipe_mode() == 3) {
-      if (k1_variant() == 1282) return launch_tma<NT, RM, OUTM, NL, 128, 2>(a, grid, st);
-      if (k1_variant() == 2561) return launch_tma<NT, RM, OUTM, NL, 256, 1>(a, grid, st);
+      if (k1_variant(NT) == 1282) return launch_tma<NT, RM, OUTM, NL, 128, 2>(a, grid, st);
+      if (k1_variant(NT) == 2561) return launch_tma<NT, RM, OUTM, NL, 256, 1>(a, grid, st);
       return launch_tma<NT, RM, OUTM, NL, 256, 2>(a, grid, st);
     }
   } else if constexpr (TimeGeo<NT>::L > 1) {
     if (pipe_mode() == 3) {
-      if (k1_variant() == 1282) return launch_tma<NT, RM, OUTM, NL, 128, 2>(a, grid, st);
-      if (k1_variant() == 2561) return launch_tma<NT, RM, OUTM, NL, 256, 1>(a, grid, st);
+      if (k1_variant(NT) == 1282) return launch_tma<NT, RM, OUTM, NL, 128, 2>(a, grid, st);
+      if (k1_variant(NT) == 2561) return launch_tma<NT, RM, OUTM, NL, 256, 1>(a, grid, st);
       return launch_tma<NT, RM, OUTM, NL, 256, 2>(a, grid, st);
     }
     if (pipe_mode() == 1) return launch_pipe<NT, RM, OUTM, NL, true>(a, grid, st);
