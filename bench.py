@@ -32,6 +32,10 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# NCCL prints its version banner to stdout at communicator init (NCCL_DEBUG unset / VERSION):
+# keep stdout to the one JSON line
+if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
+    os.environ["NCCL_DEBUG"] = "WARN"
 
 # fp64 FMA throughput of this pool's B200 (not in MEASURED_PEAKS.json): a DFMA loop measured
 # 34.19 TFLOP/s (profiles/r01_probe_fp64_hbm.txt, tools/probe_fp64.cu); nominal 148 SMs x 64
@@ -263,7 +267,16 @@ def run_ours(args):
     prob = Problem.from_config(cfg)
     stream = torch.cuda.Stream(device=dev)
     torch.cuda.set_stream(stream)
-    comm = Comm(rank, ws, local) if (ws > 1 or args.dist1) else None
+    comm = None
+    if ws > 1 or args.dist1:
+        saved = os.dup(1)  # NCCL's init banner goes to stdout: keep stdout to the JSON line
+        os.dup2(2, 1)
+        try:
+            comm = Comm(rank, ws, local)
+        finally:
+            sys.stdout.flush()
+            os.dup2(saved, 1)
+            os.close(saved)
     plan = Plan(prob, device=local, stream=stream, comm=comm)
     lay = plan.layout
     u0 = torch.from_numpy(synth.initial_condition(cfg)).to(dev)
@@ -335,7 +348,7 @@ def run_ours(args):
                "sweep_algorithmic_gbs": (k1_bytes + s3_bytes) / (ms_step * 1e-3) / 1e9,
                "sweep_frac_of_peak": (k1_bytes + s3_bytes) / (ms_step * 1e-3) / 1e9 / hbm_peak}
     roofline = k1_roof
-    if nl and ws == 1 and cfg.dim == 2:
+    if nl and comm is None and cfg.dim == 2:
         # stage-3 kernel families, timed live with CUDA events on the plan's stream after the
         # timed region (16-slice launches, as in the sweep's chunks); fp64-bound
         ns = min(16, cfg.nt)

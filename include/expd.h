@@ -172,6 +172,12 @@ expd_status expd_layout_query(const expd_problem* prob, int rank, int nranks, ex
    per list (sends and recvs have equal length), or -1 on invalid arguments.  Host only. */
 long expd_a2a_schedule(const expd_problem* prob, int rank, int nranks, int direction, int shift, long* sends,
                        long* recvs, long cap);
+/* The same schedule with stride 4 or 5 longs per message; stride 5 appends the message's
+   slice key (the index of its slice within the time slab it belongs to).  The distributed
+   sweep pipelines its all-to-alls in chunks of slice keys: every
+   rank's slab holds nt / nranks slices, so a key range is one symmetric chunk. */
+long expd_a2a_schedule_keyed(const expd_problem* prob, int rank, int nranks, int direction, int shift,
+                             long* sends, long* recvs, long cap, int stride);
 /* NCCL communicator for a plan (NCCL is loaded at run time: the process's libnccl.so.2).
    Rank 0 creates the 128-byte id, the caller broadcasts it (e.g. torch.distributed), every
    rank calls expd_nccl_comm_init (collective).  The caller owns the communicator. */

@@ -63,18 +63,18 @@ void a2a_schedule(const DistLayout& L, int dir, int shift, std::vector<A2AMsg>& 
     if (dir == A2A_MODE_TO_TIME) {
       for (int i = 0; i < L.ntl[q]; ++i) {  // r -> q: the slices of q's time slab
         const long t = L.t0[q] + i;
-        sends.push_back({q, t * L.mode_len[r], 0, L.mode_len[r]});
+        sends.push_back({q, t * L.mode_len[r], 0, L.mode_len[r], i});
       }
       for (int i = 0; i < L.ntl[r]; ++i) {  // q -> r: q's modes of r's slices
-        recvs.push_back({q, 0, (long)i * L.npad + L.mode_off[q], L.mode_len[q]});
+        recvs.push_back({q, 0, (long)i * L.npad + L.mode_off[q], L.mode_len[q], i});
       }
     } else {
       for (int i = 0; i < L.ntl[r]; ++i) {  // r -> q: q's modes of r's slices
-        sends.push_back({q, (long)i * L.npad + L.mode_off[q], 0, L.mode_len[q]});
+        sends.push_back({q, (long)i * L.npad + L.mode_off[q], 0, L.mode_len[q], i});
       }
       for (int i = 0; i < L.ntl[q]; ++i) {  // q -> r: r's modes of q's slices
         const long t = L.t0[q] + i;
-        recvs.push_back({q, 0, (t + shift) * L.mode_len[r], L.mode_len[r]});
+        recvs.push_back({q, 0, (t + shift) * L.mode_len[r], L.mode_len[r], i});
       }
     }
   }
@@ -129,16 +129,20 @@ static std::string nccl_err(ncclResult_t r) {
   return a.ok ? std::string(a.GetErrorString(r)) : std::string("NCCL not loaded");
 }
 
-// Execute one schedule: NCCL send / recv for peers, cudaMemcpy2DAsync for the self part.
+// Execute one schedule (the messages with slice key in [s_lo, s_hi)): NCCL send / recv for
+// peers, device copies for the self part.  Every message's slice key is the slice index
+// within the time slab it belongs to, and every rank's slab has nt / P slices, so a key
+// range is one symmetric chunk of the all-to-all on every rank.
 int a2a_execute(void* comm, const DistLayout& L, const std::vector<A2AMsg>& sends, const std::vector<A2AMsg>& recvs,
-                const double* src, double* dst, cudaStream_t st, std::string& err) {
+                const double* src, double* dst, cudaStream_t st, std::string& err, int s_lo, int s_hi) {
   NcclApi& a = nccl();
+  auto in = [&](const A2AMsg& m) { return m.slice >= s_lo && m.slice < s_hi; };
   // self part: pair the k-th self send with the k-th self recv
   std::vector<const A2AMsg*> ss, rr;
   for (const auto& m : sends)
-    if (m.peer == L.rank) ss.push_back(&m);
+    if (m.peer == L.rank && in(m)) ss.push_back(&m);
   for (const auto& m : recvs)
-    if (m.peer == L.rank) rr.push_back(&m);
+    if (m.peer == L.rank && in(m)) rr.push_back(&m);
   if (ss.size() != rr.size()) {
     err = "a2a: self schedule mismatch";
     return EXPD_ERR_INVALID_ARG;
@@ -159,9 +163,11 @@ int a2a_execute(void* comm, const DistLayout& L, const std::vector<A2AMsg>& send
   ncclComm_t c = (ncclComm_t)comm;
   ncclResult_t r = a.GroupStart();
   for (const auto& m : sends)
-    if (r == ncclSuccess && m.peer != L.rank) r = a.Send(src + m.src_off, (size_t)m.count, ncclFloat64, m.peer, c, st);
+    if (r == ncclSuccess && m.peer != L.rank && in(m))
+      r = a.Send(src + m.src_off, (size_t)m.count, ncclFloat64, m.peer, c, st);
   for (const auto& m : recvs)
-    if (r == ncclSuccess && m.peer != L.rank) r = a.Recv(dst + m.dst_off, (size_t)m.count, ncclFloat64, m.peer, c, st);
+    if (r == ncclSuccess && m.peer != L.rank && in(m))
+      r = a.Recv(dst + m.dst_off, (size_t)m.count, ncclFloat64, m.peer, c, st);
   ncclResult_t r2 = a.GroupEnd();
   if (r != ncclSuccess || r2 != ncclSuccess) {
     err = "a2a: " + nccl_err(r != ncclSuccess ? r : r2);
@@ -222,6 +228,11 @@ extern "C" expd_status expd_layout_query(const expd_problem* prob, int rank, int
 
 extern "C" long expd_a2a_schedule(const expd_problem* prob, int rank, int nranks, int direction, int shift,
                                   long* sends, long* recvs, long cap) {
+  return expd_a2a_schedule_keyed(prob, rank, nranks, direction, shift, sends, recvs, cap, 4);
+}
+
+extern "C" long expd_a2a_schedule_keyed(const expd_problem* prob, int rank, int nranks, int direction, int shift,
+                                        long* sends, long* recvs, long cap, int stride) {
   Geom g{};
   if (!geom_of(prob, &g)) return -1;
   DistLayout L{};
@@ -231,16 +242,23 @@ extern "C" long expd_a2a_schedule(const expd_problem* prob, int rank, int nranks
   a2a_schedule(L, direction, shift, s, r);
   const long n = (long)s.size();
   if ((long)r.size() != n) return -1;
+  if (stride != 4 && stride != 5) return -1;
   if (sends && recvs && cap >= n) {
     for (long i = 0; i < n; ++i) {
-      sends[4 * i + 0] = s[i].peer;
-      sends[4 * i + 1] = s[i].src_off;
-      sends[4 * i + 2] = s[i].dst_off;
-      sends[4 * i + 3] = s[i].count;
-      recvs[4 * i + 0] = r[i].peer;
-      recvs[4 * i + 1] = r[i].src_off;
-      recvs[4 * i + 2] = r[i].dst_off;
-      recvs[4 * i + 3] = r[i].count;
+      long* o = sends + stride * i;
+      long* q = recvs + stride * i;
+      o[0] = s[i].peer;
+      o[1] = s[i].src_off;
+      o[2] = s[i].dst_off;
+      o[3] = s[i].count;
+      q[0] = r[i].peer;
+      q[1] = r[i].src_off;
+      q[2] = r[i].dst_off;
+      q[3] = r[i].count;
+      if (stride == 5) {
+        o[4] = s[i].slice;
+        q[4] = r[i].slice;
+      }
     }
   }
   return n;

@@ -66,6 +66,10 @@ struct expd_plan {
   // optional stage timing: ev[0] before stage 3, ev[1] before K1, ev[2] after K1
   bool prof = false;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  // distributed sweep pipelining: the all-to-alls run on comm_stream in chunks of the time
+  // slab, overlapped with stage 3 of the neighbouring chunks (events in pev)
+  cudaStream_t comm_stream = nullptr;
+  std::vector<cudaEvent_t> pev;
   std::string err;
 };
 
@@ -329,6 +333,8 @@ extern "C" void expd_plan_destroy(expd_plan* p) {
   cudaSetDevice(p->device);
   if (p->sweep_exec) cudaGraphExecDestroy(p->sweep_exec);
   if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
+  if (p->comm_stream) cudaStreamDestroy(p->comm_stream);
+  for (cudaEvent_t e : p->pev) cudaEventDestroy(e);
   for (int i = 0; i < 3; ++i)
     if (p->ev[i]) cudaEventDestroy(p->ev[i]);
   cudaFree(p->d_lam);
@@ -379,13 +385,15 @@ static expd_status ready(expd_plan* p) {
 // spectral u0 and (nonlinear) N-hat_0 = V N(u_0)
 // ---- distribution helpers (no-ops / local copies on one GPU) ---------------------------
 enum { A2A_M2T = 0, A2A_T2M = 1, A2A_T2M_SHIFT = 2 };
-static expd_status a2a(expd_plan* p, int which, const double* src, double* dst) {
+// one all-to-all (or the chunk of it whose messages carry slice keys in [lo, hi))
+static expd_status a2a(expd_plan* p, int which, const double* src, double* dst, cudaStream_t st = nullptr,
+                       int lo = 0, int hi = 1 << 30) {
   const std::vector<A2AMsg>* s = &p->m2t_s;
   const std::vector<A2AMsg>* r = &p->m2t_r;
   if (which == A2A_T2M) { s = &p->t2m_s; r = &p->t2m_r; }
   if (which == A2A_T2M_SHIFT) { s = &p->t2m1_s; r = &p->t2m1_r; }
-  int st = a2a_execute(p->dinfo.nccl_comm, p->L, *s, *r, src, dst, p->stream, p->err);
-  return (expd_status)st;
+  int e = a2a_execute(p->dinfo.nccl_comm, p->L, *s, *r, src, dst, st ? st : p->stream, p->err, lo, hi);
+  return (expd_status)e;
 }
 static expd_status allreduce(expd_plan* p, double* buf, long count) {
   if (!p->dist) return EXPD_OK;
@@ -474,15 +482,71 @@ static cudaError_t enqueue_sweep(expd_plan* p, cudaStream_t st) {
 // local time slices, all-to-all N-hat back (time slab -> mode slab, shifted one slice:
 // N-hat_m = V N(u_m) sits in slice m while U-hat slice t holds u_{t+1}), K1 on the mode
 // slab, allreduce of ||r||^2.
-static expd_status sweep_dist(expd_plan* p) {
+// Chunks of the time slab in the pipelined distributed sweep (EXPD_DIST_CHUNKS, default 8;
+// 1 = the unpipelined schedule).
+static int dist_chunks(const expd_plan* p) {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EXPD_DIST_CHUNKS");
+    v = e ? atoi(e) : 8;
+    if (v < 1) v = 1;
+  }
+  return v < p->ntl ? v : p->ntl;
+}
+
+// Stage 3 of the distributed sweep, pipelined over chunks of the time slab: the mode ->
+// time all-to-all of every chunk is posted on comm_stream up front; chunk c's stage 3 runs
+// on the plan stream once its slices have landed, and its time -> mode all-to-all follows
+// on comm_stream while stage 3 moves on to chunk c + 1.  Every rank posts the same chunk
+// sequence (slice keys), so the NCCL groups match across ranks.
+static expd_status stage3_dist(expd_plan* p) {
   expd_status s;
-  CUDA_TRY(p, record(p, 0, p->stream));
-  if (p->nl) {
+  const int nch = dist_chunks(p);
+  if (nch <= 1) {
     if ((s = a2a(p, A2A_M2T, p->Uh, p->UT))) return s;
     CUDA_TRY(p, nonlin_slices(p->g, dst_tables(p), p->UT, p->NT, p->ntl, p->prob.npoly, p->prob.q, p->scratch,
                               p->stream));
-    if ((s = a2a(p, A2A_T2M_SHIFT, p->NT, p->Nh))) return s;
+    return a2a(p, A2A_T2M_SHIFT, p->NT, p->Nh);
   }
+  if (!p->comm_stream) {
+    // highest priority: the exchange's kernels take SM slots as soon as a stage-3 kernel
+    // releases them, instead of queueing behind the next persistent stage-3 grid
+    int lo = 0, hi = 0;
+    CUDA_TRY(p, cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CUDA_TRY(p, cudaStreamCreateWithPriority(&p->comm_stream, cudaStreamNonBlocking, hi));
+  }
+  while ((int)p->pev.size() < 2 * nch + 2) {
+    cudaEvent_t e;
+    CUDA_TRY(p, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    p->pev.push_back(e);
+  }
+  const int k = (p->ntl + nch - 1) / nch;
+  cudaStream_t cs = p->comm_stream;
+  CUDA_TRY(p, cudaEventRecord(p->pev[0], p->stream));  // U-hat is final (K1 of the last sweep)
+  CUDA_TRY(p, cudaStreamWaitEvent(cs, p->pev[0], 0));
+  for (int c = 0; c < nch && c * k < p->ntl; ++c) {
+    const int lo = c * k, hi = lo + k < p->ntl ? lo + k : p->ntl;
+    if ((s = a2a(p, A2A_M2T, p->Uh, p->UT, cs, lo, hi))) return s;
+    CUDA_TRY(p, cudaEventRecord(p->pev[2 + c], cs));
+  }
+  for (int c = 0; c < nch && c * k < p->ntl; ++c) {
+    const int lo = c * k, hi = lo + k < p->ntl ? lo + k : p->ntl;
+    CUDA_TRY(p, cudaStreamWaitEvent(p->stream, p->pev[2 + c], 0));
+    CUDA_TRY(p, nonlin_slices(p->g, dst_tables(p), p->UT + (size_t)lo * p->g.npad, p->NT + (size_t)lo * p->g.npad,
+                              hi - lo, p->prob.npoly, p->prob.q, p->scratch, p->stream));
+    CUDA_TRY(p, cudaEventRecord(p->pev[2 + nch + c], p->stream));
+    CUDA_TRY(p, cudaStreamWaitEvent(cs, p->pev[2 + nch + c], 0));
+    if ((s = a2a(p, A2A_T2M_SHIFT, p->NT, p->Nh, cs, lo, hi))) return s;
+  }
+  CUDA_TRY(p, cudaEventRecord(p->pev[1], cs));
+  CUDA_TRY(p, cudaStreamWaitEvent(p->stream, p->pev[1], 0));
+  return EXPD_OK;
+}
+
+static expd_status sweep_dist(expd_plan* p) {
+  expd_status s;
+  CUDA_TRY(p, record(p, 0, p->stream));
+  if (p->nl && (s = stage3_dist(p))) return s;
   CUDA_TRY(p, record(p, 1, p->stream));
   TimeArgs a = time_args(p, p->Uh, p->Uh, true);
   CUDA_TRY(p, launch_time_fused(a, RM_RESID, OUT_UPDATE, p->k1, p->time_grid, p->stream));

@@ -137,12 +137,16 @@ struct DistLayout {
 struct A2AMsg {
   int peer;
   long src_off, dst_off, count;  // doubles
+  int slice;                     // index of the slice within its time slab (pipelining key)
 };
 enum A2ADir { A2A_MODE_TO_TIME = 0, A2A_TIME_TO_MODE = 1 };
 bool dist_layout(const Geom& g, int nt, int rank, int nranks, DistLayout* L);
 void a2a_schedule(const DistLayout& L, int dir, int shift, std::vector<A2AMsg>& sends, std::vector<A2AMsg>& recvs);
+// executes the messages whose slice key lies in [s_lo, s_hi) (one chunk of a pipelined
+// all-to-all; every rank must pass the same range)
 int a2a_execute(void* comm, const DistLayout& L, const std::vector<A2AMsg>& sends, const std::vector<A2AMsg>& recvs,
-                const double* src, double* dst, cudaStream_t st, std::string& err);
+                const double* src, double* dst, cudaStream_t st, std::string& err, int s_lo = 0,
+                int s_hi = 1 << 30);
 int allreduce_sum(void* comm, int nranks, double* buf, long count, cudaStream_t st, std::string& err);
 
 }  // namespace expd

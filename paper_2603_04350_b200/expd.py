@@ -52,6 +52,7 @@ EXPORTS = [
     "expd_debug_kernel_ms",
     "expd_layout_query",
     "expd_a2a_schedule",
+    "expd_a2a_schedule_keyed",
     "expd_nccl_unique_id",
     "expd_nccl_comm_init",
     "expd_nccl_comm_destroy",
@@ -138,6 +139,8 @@ def load_library(path: str = LIB_PATH):
         "expd_layout_query": (C.c_int, [C.POINTER(_Problem), C.c_int, C.c_int, C.POINTER(_Layout)]),
         "expd_a2a_schedule": (C.c_long, [C.POINTER(_Problem), C.c_int, C.c_int, C.c_int, C.c_int,
                                          C.POINTER(C.c_long), C.POINTER(C.c_long), C.c_long]),
+        "expd_a2a_schedule_keyed": (C.c_long, [C.POINTER(_Problem), C.c_int, C.c_int, C.c_int, C.c_int,
+                                               C.POINTER(C.c_long), C.POINTER(C.c_long), C.c_long, C.c_int]),
         "expd_nccl_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),
         "expd_nccl_comm_init": (C.c_int, [C.POINTER(C.c_ubyte), C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
         "expd_nccl_comm_destroy": (None, [vp]),
@@ -207,20 +210,23 @@ def layout(problem: Problem, rank: int, nranks: int) -> dict:
     return {k: getattr(out, k) for k, _ in _Layout._fields_}
 
 
-def a2a_schedule(problem: Problem, rank: int, nranks: int, direction: int, shift: int = 0):
+def a2a_schedule(problem: Problem, rank: int, nranks: int, direction: int, shift: int = 0, keyed: bool = False):
     """The all-to-all messages this rank posts (expd_a2a_schedule): two int64 arrays
-    (sends, recvs) of rows {peer, src_off, dst_off, count}, in posting order."""
+    (sends, recvs) of rows {peer, src_off, dst_off, count} (+ slice key when keyed), in
+    posting order."""
     import numpy as np
 
     lib = load_library()
     p = problem._c()
-    n = lib.expd_a2a_schedule(C.byref(p), rank, nranks, direction, shift, None, None, 0)
+    w = 5 if keyed else 4
+    n = lib.expd_a2a_schedule_keyed(C.byref(p), rank, nranks, direction, shift, None, None, 0, w)
     if n < 0:
         raise ExpdError(1, "expd_a2a_schedule")
-    s = np.zeros((n, 4), dtype=np.int64)
-    r = np.zeros((n, 4), dtype=np.int64)
+    s = np.zeros((n, w), dtype=np.int64)
+    r = np.zeros((n, w), dtype=np.int64)
     lp = C.POINTER(C.c_long)
-    lib.expd_a2a_schedule(C.byref(p), rank, nranks, direction, shift, s.ctypes.data_as(lp), r.ctypes.data_as(lp), n)
+    lib.expd_a2a_schedule_keyed(C.byref(p), rank, nranks, direction, shift, s.ctypes.data_as(lp),
+                                r.ctypes.data_as(lp), n, w)
     return s, r
 
 

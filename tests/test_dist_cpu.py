@@ -258,3 +258,58 @@ def test_distributed_sweep_matches_oracle(tmp_path, P, name, n, nt):
         assert np.array_equal(h, hists[0])  # every rank takes the same decisions
     assert st == 0 and len(hists[0]) - 1 == its  # identical iteration count (R8)
     assert np.abs(U - Uo).max() <= 1e-12 * np.abs(Uo).max()
+
+
+# ------------------------------------------------------------------------------------------
+# the pipelined exchange: chunks of slice keys (expd_api.cu stage3_dist)
+# ------------------------------------------------------------------------------------------
+@pytest.mark.parametrize("name,n,nt", CASES[:5])
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("direction,shift", [(0, 0), (1, 1)])
+def test_keyed_chunks_are_symmetric(name, n, nt, P, direction, shift):
+    """Every slice-key chunk is a complete all-to-all by itself: what r sends q with key i
+    is what q posts to receive from r with key i, in the same order."""
+    cfg = _cfg(name, n, nt)
+    prob = Problem.from_config(cfg)
+    if cfg.nt % P:
+        pytest.skip("nt % P != 0")
+    S = [a2a_schedule(prob, r, P, direction, shift, keyed=True) for r in range(P)]
+    ntl = cfg.nt // P
+    for r in range(P):
+        assert np.array_equal(S[r][0][:, :4], a2a_schedule(prob, r, P, direction, shift)[0])
+        assert set(S[r][0][:, 4]) == set(range(ntl)) == set(S[r][1][:, 4])
+        for q in range(P):
+            for key in range(ntl):
+                sent = S[r][0][(S[r][0][:, 0] == q) & (S[r][0][:, 4] == key)][:, 3]
+                got = S[q][1][(S[q][1][:, 0] == r) & (S[q][1][:, 4] == key)][:, 3]
+                assert list(sent) == list(got), (r, q, key)
+
+
+def _chunked_worker(rank, P, port, name, n, nt, k):
+    _init(rank, P, port)
+    try:
+        cfg = _cfg(name, n, nt)
+        prob = Problem.from_config(cfg)
+        L = layout(prob, rank, P)
+        npad, off, ln, t0, ntl = L["npad"], L["mode_off"], L["mode_len"], L["t0"], L["nt_local"]
+        G = torch.from_numpy(np.random.default_rng(7).standard_normal((cfg.nt, npad)))
+        mode = G[:, off:off + ln].contiguous().reshape(-1)
+        time = torch.full((ntl * npad,), float("nan"), dtype=torch.float64)
+        back = torch.zeros(((cfg.nt + 1) * ln,), dtype=torch.float64)
+        s0, r0 = a2a_schedule(prob, rank, P, 0, 0, keyed=True)
+        s1, r1 = a2a_schedule(prob, rank, P, 1, 1, keyed=True)
+        chunks = [(lo, min(lo + k, ntl)) for lo in range(0, ntl, k)]
+        sel = lambda m, lo, hi: m[(m[:, 4] >= lo) & (m[:, 4] < hi)][:, :4]  # noqa: E731
+        for lo, hi in chunks:  # every mode -> time chunk first (as posted on the comm stream)
+            run_schedule(sel(s0, lo, hi), sel(r0, lo, hi), mode, time, rank)
+        assert torch.equal(time.reshape(ntl, npad), G[t0:t0 + ntl])
+        for lo, hi in chunks:  # then chunk by chunk back, after "stage 3" of the chunk
+            run_schedule(sel(s1, lo, hi), sel(r1, lo, hi), time, back, rank)
+        assert torch.equal(back.reshape(cfg.nt + 1, ln)[1:], G[:, off:off + ln])
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("P,name,n,nt,k", [(2, "c3", 31, 16, 3), (4, "c5", 15, 16, 1), (2, "c4", 7, 8, 2)])
+def test_chunked_a2a_gloo(P, name, n, nt, k):
+    _spawn(_chunked_worker, P, name, n, nt, k)
