@@ -126,13 +126,34 @@ static void cctx_free(cctx* c) {
   free(c->E);
 }
 
-/* u_n = A u_{n-1}, n = 1..Nt */
+/* u_n = A u_{n-1}, n = 1..Nt; scheme 3: exponential BDF2 (4.1)
+   u_n = 4/3 A u_{n-1} - 1/3 A^2 u_{n-2} from u_1 = A u_0 (reading R16), U holding
+   u_2 .. u_{Nt+1} */
 void orc_cplx_sequential(const orc_problem* p, const double* u0, double* U) {
   cctx c;
   cctx_init(&c, p);
   size_t N = (size_t)c.N;
   lc* prev = load_c(u0, N);
   lc* cur = (lc*)malloc(sizeof(lc) * N);
+  if (p->scheme == 3) {
+    lc* um2 = (lc*)malloc(sizeof(lc) * N);
+    lc* t1 = (lc*)malloc(sizeof(lc) * N);
+    lc* t2 = (lc*)malloc(sizeof(lc) * N);
+    memcpy(um2, prev, sizeof(lc) * N);
+    capply_A(p, c.S, c.E, um2, prev); /* u_1 */
+    for (int n = 2; n <= p->nt + 1; ++n) {
+      capply_A(p, c.S, c.E, prev, cur);
+      capply_A(p, c.S, c.E, um2, t1);
+      capply_A(p, c.S, c.E, t1, t2);
+      for (size_t i = 0; i < N; ++i) cur[i] = (4.0L / 3.0L) * cur[i] - (1.0L / 3.0L) * t2[i];
+      store_c(cur, U + 2 * (size_t)(n - 2) * N, N);
+      memcpy(um2, prev, sizeof(lc) * N);
+      memcpy(prev, cur, sizeof(lc) * N);
+    }
+    free(um2); free(t1); free(t2); free(prev); free(cur);
+    cctx_free(&c);
+    return;
+  }
   for (int n = 1; n <= p->nt; ++n) {
     capply_A(p, c.S, c.E, prev, cur);
     store_c(cur, U + 2 * (size_t)(n - 1) * N, N);
@@ -143,9 +164,31 @@ void orc_cplx_sequential(const orc_problem* p, const double* u0, double* U) {
   cctx_free(&c);
 }
 
-/* r_n = A u_{n-1} - u_n (f - Q U) */
+/* r_n = A u_{n-1} - u_n (f - Q U); scheme 3: r = f_2 - R v
+   (PAPER.md:440-442): r_n = 4/3 A v_{n-1} - 1/3 A^2 v_{n-2} - v_n with v_0 = u_1 = A u_0,
+   v_{-1} = u_0 */
 static void cresidual(const cctx* c, const lc* u0, const lc* U, lc* R) {
   size_t N = (size_t)c->N;
+  if (c->p->scheme == 3) {
+    lc* u1 = (lc*)malloc(sizeof(lc) * N);
+    capply_A(c->p, c->S, c->E, u0, u1);
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int n = 1; n <= c->p->nt; ++n) {
+      const lc* p1 = n == 1 ? u1 : U + (size_t)(n - 2) * N;
+      const lc* p2 = n == 1 ? u0 : n == 2 ? u1 : U + (size_t)(n - 3) * N;
+      lc* r = R + (size_t)(n - 1) * N;
+      lc* t1 = (lc*)malloc(sizeof(lc) * N);
+      lc* t2 = (lc*)malloc(sizeof(lc) * N);
+      capply_A(c->p, c->S, c->E, p1, r);
+      capply_A(c->p, c->S, c->E, p2, t1);
+      capply_A(c->p, c->S, c->E, t1, t2);
+      for (size_t i = 0; i < N; ++i)
+        r[i] = (4.0L / 3.0L) * r[i] - (1.0L / 3.0L) * t2[i] - U[(size_t)(n - 1) * N + i];
+      free(t1); free(t2);
+    }
+    free(u1);
+    return;
+  }
 #pragma omp parallel for schedule(dynamic, 1)
   for (int n = 1; n <= c->p->nt; ++n) {
     const lc* prev = n == 1 ? u0 : U + (size_t)(n - 2) * N;
@@ -155,9 +198,30 @@ static void cresidual(const cctx* c, const lc* u0, const lc* U, lc* R) {
   }
 }
 
-/* (Q v)_n = v_n - A v_{n-1}, v_0 = 0 */
+/* (Q v)_n = v_n - A v_{n-1}, v_0 = 0; scheme 3: R v = v - 4/3 (C_0 (x) A) v + 1/3 (C_1 (x) A^2) v
+    */
 static void capply_Q(const cctx* c, const lc* V, lc* out) {
   size_t N = (size_t)c->N;
+  if (c->p->scheme == 3) {
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int n = 1; n <= c->p->nt; ++n) {
+      lc* o = out + (size_t)(n - 1) * N;
+      lc* t1 = (lc*)malloc(sizeof(lc) * N);
+      lc* t2 = (lc*)malloc(sizeof(lc) * N);
+      memcpy(o, V + (size_t)(n - 1) * N, sizeof(lc) * N);
+      if (n >= 2) {
+        capply_A(c->p, c->S, c->E, V + (size_t)(n - 2) * N, t1);
+        for (size_t i = 0; i < N; ++i) o[i] -= (4.0L / 3.0L) * t1[i];
+      }
+      if (n >= 3) {
+        capply_A(c->p, c->S, c->E, V + (size_t)(n - 3) * N, t1);
+        capply_A(c->p, c->S, c->E, t1, t2);
+        for (size_t i = 0; i < N; ++i) o[i] += (1.0L / 3.0L) * t2[i];
+      }
+      free(t1); free(t2);
+    }
+    return;
+  }
 #pragma omp parallel for schedule(dynamic, 1)
   for (int n = 1; n <= c->p->nt; ++n) {
     lc* o = out + (size_t)(n - 1) * N;
@@ -196,7 +260,14 @@ static void cprecond(const cctx* c, const lc* R, lc* Sout) {
     lc* t = (lc*)malloc(sizeof(lc) * N);
     cdst(p, c->S, Y + (size_t)k * N, t);
     lc lam = a1 * w[k];
-    for (size_t J = 0; J < N; ++J) t[J] /= (1.0L - lam * c->E[J]); /* Step (b) */
+    if (p->scheme == 3) { /* BDF2 Step (b) of (4.5): 1 - 4/3 lambda_{0,k} E + 1/3 lambda_{1,k} E^2,
+                             lambda_{1,k} = alpha^{2/Nt} omega^{2k} */
+      lc lam1 = powl((ld)p->alpha, 2.0L / (ld)nt) * w[(2L * k) % nt];
+      for (size_t J = 0; J < N; ++J)
+        t[J] /= (1.0L - (4.0L / 3.0L) * lam * c->E[J] + (1.0L / 3.0L) * lam1 * c->E[J] * c->E[J]);
+    } else {
+      for (size_t J = 0; J < N; ++J) t[J] /= (1.0L - lam * c->E[J]); /* Step (b) */
+    }
     cdst(p, c->S, t, Y + (size_t)k * N);
     free(t);
   }

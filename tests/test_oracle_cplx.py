@@ -206,3 +206,73 @@ def test_cplx_bicgstab_matches_gmres_and_sequential(orc, a, c):
     Ug, st2, _, _ = orc.cplx_gmres(s, u0, tol=1e-12, restart=30, maxit=60)
     assert st == 0 and st2 == 0
     assert rel(Ub, Ug) < 1e-9 and rel(Ub, orc.cplx_sequential(s, u0)) < 1e-9
+
+
+# ------------------------------------------------------------------------------------------
+# complex exponential BDF2 (scheme 3, the 2D Schroedinger test of :1064)
+# ------------------------------------------------------------------------------------------
+def cspec3(orc, dim, n, a, c, T=0.5, nt=8, alpha=1e-2):
+    a, c = complex(a), complex(c)
+    return orc.Spec(dim, n, a.real, c.real, T, nt, alpha, 3, (), a.imag, c.imag)
+
+
+def dense_R_c(s, alpha):
+    """R_alpha = I - 4/3 (C_0^alpha (x) A) + 1/3 (C_1^alpha (x) A^2) (PAPER.md:440-458);
+    alpha = 0 gives R."""
+    A = sla.expm(s.dt * Lc(s))
+    L = s.nt
+    C0 = np.diag(np.ones(L - 1), -1)
+    C1 = np.diag(np.ones(L - 2), -2)
+    C0[0, L - 1] = alpha
+    C1[0, L - 2] = alpha
+    C1[1, L - 1] = alpha
+    return np.eye(L * s.N) - 4 / 3 * np.kron(C0, A) + 1 / 3 * np.kron(C1, A @ A)
+
+
+@pytest.mark.parametrize("a,c", COEFS)
+def test_cplx_bdf2_sequential_is_exact(orc, a, c):
+    """(4.1) from u_1 = A u_0 gives 4/3 A^n - 1/3 A^2 A^{n-2} = A^n exactly (R16)."""
+    s = cspec3(orc, 1, 9, a, c, T=0.3, nt=6)
+    u0 = crandn(np.random.default_rng(21), 9)
+    U = orc.cplx_sequential(s, u0)
+    for i in range(s.nt):
+        assert rel(U[i], sla.expm((i + 2) * s.dt * Lc(s)) @ u0) < 1e-11
+
+
+@pytest.mark.parametrize("a,c", COEFS)
+def test_cplx_bdf2_residual_and_R_vs_dense(orc, a, c):
+    s = cspec3(orc, 2, 3, a, c, T=0.3, nt=5)
+    rng = np.random.default_rng(22)
+    u0, U = crandn(rng, (3, 3)), crandn(rng, (5, 3, 3))
+    A = sla.expm(s.dt * Lc(s))
+    u1 = A @ u0.reshape(-1)
+    f = np.zeros(45, dtype=complex)
+    f[:9] = 4 / 3 * A @ u1 - 1 / 3 * A @ A @ u0.reshape(-1)
+    f[9:18] = -1 / 3 * A @ A @ u1
+    R, _ = orc.cplx_residual(s, u0, U)
+    assert rel(R.reshape(-1), f - dense_R_c(s, 0.0) @ U.reshape(-1)) < 1e-12
+    assert rel(orc.cplx_apply_Q(s, U).reshape(-1), dense_R_c(s, 0.0) @ U.reshape(-1)) < 1e-12
+
+
+@pytest.mark.parametrize("alpha", [0.3, 1e-2, 1e-4])
+@pytest.mark.parametrize("a,c", COEFS)
+@pytest.mark.parametrize("dim,n,nt", [(1, 5, 8), (2, 3, 6)])
+def test_cplx_bdf2_precond_vs_dense_solve(orc, alpha, a, c, dim, n, nt):
+    s = cspec3(orc, dim, n, a, c, T=0.5, nt=nt, alpha=alpha)
+    R = crandn(np.random.default_rng(23), (nt,) + (n,) * dim)
+    S = orc.cplx_precond(s, R)
+    want = np.linalg.solve(dense_R_c(s, alpha), R.reshape(-1))
+    kappa = alpha ** (-(nt - 1) / nt)
+    assert rel(S.reshape(-1), want) < 1e-15 * kappa * 200
+
+
+@pytest.mark.parametrize("a,c", COEFS)
+def test_cplx_bdf2_solvers_reach_sequential(orc, a, c):
+    s = cspec3(orc, 2, 4, a, c, T=0.4, nt=8, alpha=0.05)
+    u0 = crandn(np.random.default_rng(24), (4, 4))
+    Us = orc.cplx_sequential(s, u0)
+    for solve in (lambda: orc.cplx_fixed_point(s, u0, tol=1e-13, maxit=80),
+                  lambda: orc.cplx_gmres(s, u0, tol=1e-13, restart=40, maxit=80),
+                  lambda: orc.cplx_bicgstab(s, u0, tol=1e-13, maxit=80)):
+        U, st, its, _ = solve()
+        assert st == 0 and rel(U, Us) < 1e-10
