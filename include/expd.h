@@ -71,7 +71,8 @@ typedef struct {
                          non-zero makes a COMPLEX plan (the paper's Schroedinger tests, a = i,
                          c = 2i): u_t = (a Delta - c) u with a = a + i a_im,
                          c = c + i c_im, Re a >= 0 (a != 0), Re c >= 0; linear only
-                         (npoly = 0), scheme EXPD_EXP_EULER, one GPU (no expd_dist).  Every
+                         (npoly = 0), scheme EXPD_EXP_EULER or EXPD_BDF2, one GPU (no
+                         expd_dist).  Every
                          space-time / slice argument of a complex plan (u0, U, R, S) is
                          complex128: interleaved (re, im) doubles, 2 N doubles per slice.
                          GMRES and BiCGStab run over C with the Hermitian inner product

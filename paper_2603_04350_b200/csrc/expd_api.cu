@@ -154,8 +154,9 @@ extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dis
       !std::isfinite(P.a) || !std::isfinite(P.c) || !std::isfinite(P.dt))
     return EXPD_ERR_INVALID_ARG;
   if (P.nt > 256) return EXPD_ERR_UNSUPPORTED;
-  if (cx && (P.npoly > 0 || P.scheme != EXPD_EXP_EULER || (dist && (dist->nranks > 1 || dist->nccl_comm))))
-    return EXPD_ERR_UNSUPPORTED;  // complex plans: linear exponential Euler on one GPU
+  if (cx && (P.npoly > 0 || (P.scheme != EXPD_EXP_EULER && P.scheme != EXPD_BDF2) ||
+             (dist && (dist->nranks > 1 || dist->nccl_comm))))
+    return EXPD_ERR_UNSUPPORTED;  // complex plans: linear exponential Euler or BDF2, one GPU
   int nranks = dist ? dist->nranks : 1;
   if (nranks < 1 || nranks > EXPD_MAX_RANKS || (dist && (dist->rank < 0 || dist->rank >= nranks)))
     return EXPD_ERR_INVALID_ARG;
@@ -186,7 +187,8 @@ extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dis
   // K1 form: 0 linear, 1 one N-hat term (ETD1; IF/IMEX with N of the same slice), 2 ETD2
   p->nl = P.npoly > 0 ? (P.scheme == EXPD_ETD2 ? 2 : 1) : 0;
   p->nshift = (P.npoly > 0 && P.scheme == EXPD_IF_IMEX) ? 1 : 0;
-  p->k1 = P.scheme == EXPD_BDF2 ? 3 : (cx ? 4 : p->nl);  // K1 form (3: BDF2 system, 4: complex)
+  // K1 form: 3 BDF2 system, 4 complex coefficients, 5 complex BDF2
+  p->k1 = P.scheme == EXPD_BDF2 ? (cx ? 5 : 3) : (cx ? 4 : p->nl);
   p->cx = cx;
   if (cudaSetDevice(device) != cudaSuccess) {
     delete p;

@@ -85,10 +85,10 @@ __global__ void __launch_bounds__(256) k_resid_only(const TimeArgs a) {
     double2 prev = t > 0 ? ld2(a.X + (long)(t - 1) * a.npad + base) : ld2(a.u0h + base);
     double2 r = make_double2(fma(E.x, prev.x, -cur.x), fma(E.y, prev.y, -cur.y));
     if constexpr (NL == 4) r = csub(cmul(E, prev), cur);  // complex mode: E z_{t-1} - z_t
-    if constexpr (NL == 3) {  // BDF2: f2 - R v
+    if constexpr (K1Form<NL>::BDF) {  // BDF2: f2 - R v (NL 5: complex)
       const double2 zero = make_double2(0.0, 0.0);
       const double2 xm2 = t >= 2 ? ld2(a.X + (long)(t - 2) * a.npad + base) : zero;
-      r = bdf2_form<true>(E, cur, t >= 1 ? prev : zero, xm2, ld2(a.u0h + base), t);
+      r = bdf2_form<true, K1Form<NL>::CX>(E, cur, t >= 1 ? prev : zero, xm2, ld2(a.u0h + base), t);
     }
     if constexpr (K1Form<NL>::HASN) {
       double2 c1 = ld2(a.C1 + base), nm1 = ld2(a.Nh + (long)t * a.npad + base);
@@ -119,6 +119,7 @@ cudaError_t launch_resid_only(const TimeArgs& a, int nl, int grid, cudaStream_t 
   else if (nl == 1) k_resid_only<1><<<grid, 256, 0, st>>>(a);
   else if (nl == 3) k_resid_only<3><<<grid, 256, 0, st>>>(a);
   else if (nl == 4) k_resid_only<4><<<grid, 256, 0, st>>>(a);
+  else if (nl == 5) k_resid_only<5><<<grid, 256, 0, st>>>(a);
   else k_resid_only<2><<<grid, 256, 0, st>>>(a);
   return cudaGetLastError();
 }

@@ -104,11 +104,12 @@ __device__ __forceinline__ double2 cx_divisor(double bx, double by, double c, do
 // NL == 3 marks the BDF2 system (linear): residual f2 - R v, Q-operator R v, BDF2 divisor.
 // NL == 4 marks a complex-coefficient linear plan: a "pair" is one complex mode (re, im),
 // E_J is complex, residual E z_{t-1} - z_t and Q v = v_t - E v_{t-1} in complex arithmetic.
+// NL == 5: the BDF2 system with complex coefficients (both of the above).
 template <int NL>
 struct K1Form {
   static constexpr bool HASN = NL == 1 || NL == 2;  // an N-hat term in the residual
-  static constexpr bool BDF = NL == 3;
-  static constexpr bool CX = NL == 4;
+  static constexpr bool BDF = NL == 3 || NL == 5;
+  static constexpr bool CX = NL == 4 || NL == 5;
 };
 
 // W_k = A Z_k + B conj(Z_kp),  W_kp = conj(A) Z_kp + conj(B) conj(Z_k)
@@ -200,17 +201,16 @@ __device__ __forceinline__ void pair_divide(double2 (&va)[RL], double2 (&vb)[RL]
   constexpr int NS = NT / RL;
   if constexpr (CX) {  // (ba, bb) = a1 E_J complex; frequency ja + NS r (and jb + NS r)
     const double inv_nt = 2.0 * hin;
+    // BDF2: 1 - 4/3 lambda E + 1/3 lambda^2 E^2 = (1 - lambda E)(1 - lambda E / 3)
+    auto div = [&](double2 w) {
+      const double2 d = cx_divisor(ba, bb, w.x, w.y, inv_nt);
+      return BDF ? cmul(d, cx_divisor(ba * (1.0 / 3.0), bb * (1.0 / 3.0), w.x, w.y, 1.0)) : d;
+    };
 #pragma unroll
-    for (int r = 0; r < RL; ++r) {
-      const double2 w = stw[ja + NS * r];
-      va[r] = cmul(va[r], cx_divisor(ba, bb, w.x, w.y, inv_nt));
-    }
+    for (int r = 0; r < RL; ++r) va[r] = cmul(va[r], div(stw[ja + NS * r]));
     if (!pj0 || jb != ja) {
 #pragma unroll
-      for (int r = 0; r < RL; ++r) {
-        const double2 w = stw[jb + NS * r];
-        vb[r] = cmul(vb[r], cx_divisor(ba, bb, w.x, w.y, inv_nt));
-      }
+      for (int r = 0; r < RL; ++r) vb[r] = cmul(vb[r], div(stw[jb + NS * r]));
     }
     return;
   }
@@ -237,8 +237,17 @@ __device__ __forceinline__ void pair_divide(double2 (&va)[RL], double2 (&vb)[RL]
 // BDF2 time-local residual / Q-operator of one mode pair at time t:
 // RESID: r_t = 4/3 E p1 - 1/3 E^2 p2 - x_t, p1 = v_{t-1} (u_1 = E u_0 at t = 0), p2 = v_{t-2}
 // (u_1 at t = 1, u_0 at t = 0);  QOP: (R v)_t = v_t - 4/3 E v_{t-1} + 1/3 E^2 v_{t-2}.
-template <bool RESID>
+template <bool RESID, bool CX = false>
 __device__ __forceinline__ double2 bdf2_form(double2 E, double2 xc, double2 xm1, double2 xm2, double2 u0, int t) {
+  if constexpr (CX) {  // one complex mode: E, the states and u0 are complex numbers
+    const double2 zero = make_double2(0.0, 0.0);
+    const double2 u1 = cmul(E, u0);
+    const double2 p1 = t >= 1 ? xm1 : (RESID ? u1 : zero);
+    const double2 p2 = t >= 2 ? xm2 : (t == 1 ? (RESID ? u1 : zero) : (RESID ? u0 : zero));
+    const double2 a = cmul(E, p1), b = cmul(E, cmul(E, p2));
+    const double2 r = make_double2((4.0 / 3.0) * a.x - (1.0 / 3.0) * b.x, (4.0 / 3.0) * a.y - (1.0 / 3.0) * b.y);
+    return RESID ? csub(r, xc) : csub(xc, r);
+  }
   const double2 u1 = make_double2(E.x * u0.x, E.y * u0.y);
   const double2 zero = make_double2(0.0, 0.0);
   const double2 p1 = t >= 1 ? xm1 : (RESID ? u1 : zero);
@@ -311,7 +320,7 @@ __global__ void __launch_bounds__(EXPD_K1_THREADS, EXPD_K1_MINB) k_time_fused(co
           if (t >= 2) xm2 = ld2(a.X + (long)(t - 2) * npad + base);
           if (RM == RM_RESID) u0 = ld2(a.u0h + base);
         }
-        rr = bdf2_form<RM == RM_RESID>(Ej, cur, xm1, xm2, u0, t);
+        rr = bdf2_form<RM == RM_RESID, K1Form<NL>::CX>(Ej, cur, xm1, xm2, u0, t);
       } else {
         double2 prev = make_double2(0.0, 0.0);
         if (valid) {
@@ -816,7 +825,7 @@ __global__ void __launch_bounds__(THR, (TmaLayout<NT, THR, NL, NST>::MINB))
         const double2 xm1 = t >= 1 ? X[(t - 1) * S + s] : zero;
         const double2 xm2 = t >= 2 ? X[(t - 2) * S + s] : zero;
         const double2 u0 = RM == RM_RESID ? aux[3 * S + s] : zero;
-        rr = bdf2_form<RM == RM_RESID>(Ej, xc, xm1, xm2, u0, t);
+        rr = bdf2_form<RM == RM_RESID, K1Form<NL>::CX>(Ej, xc, xm1, xm2, u0, t);
       } else {
         const double2 prev = t > 0 ? X[(t - 1) * S + s] : (RM == RM_RESID ? aux[3 * S + s] : make_double2(0.0, 0.0));
         if constexpr (K1Form<NL>::CX) {
@@ -1008,7 +1017,7 @@ static cudaError_t launch_tma(const TimeArgs& a, int grid, cudaStream_t st) {
 
 template <int NT, int RM, int OUTM, int NL>
 static cudaError_t launch_t(const TimeArgs& a, int grid, cudaStream_t st) {
-  if constexpr (TimeGeo<NT>::L > 1 && (NL == 3 || NL == 4)) {  // BDF2 / complex: TMA or register kernel
+  if constexpr (TimeGeo<NT>::L > 1 && NL >= 3) {  // BDF2 / complex: TMA or register kernel
     if (pipe_mode() == 3) {
       if (k1_variant(NT) == 1282) return launch_tma<NT, RM, OUTM, NL, 128, 2>(a, grid, st);
       if (k1_variant(NT) == 2561) return launch_tma<NT, RM, OUTM, NL, 256, 1>(a, grid, st);
@@ -1049,6 +1058,13 @@ static cudaError_t dispatch_nt(const TimeArgs& a, int rm, int om, int nl, int gr
     if (rm == RM_RESID && om == OUT_S) return launch_t<NT, RM_RESID, OUT_S, 4>(a, grid, st);
     if (rm == RM_INPUT && om == OUT_S) return launch_t<NT, RM_INPUT, OUT_S, 4>(a, grid, st);
     if (rm == RM_QOP && om == OUT_S) return launch_t<NT, RM_QOP, OUT_S, 4>(a, grid, st);
+    return cudaErrorInvalidValue;
+  }
+  if (nl == 5) {  // complex BDF2 system
+    if (rm == RM_RESID && om == OUT_UPDATE) return launch_t<NT, RM_RESID, OUT_UPDATE, 5>(a, grid, st);
+    if (rm == RM_RESID && om == OUT_S) return launch_t<NT, RM_RESID, OUT_S, 5>(a, grid, st);
+    if (rm == RM_INPUT && om == OUT_S) return launch_t<NT, RM_INPUT, OUT_S, 5>(a, grid, st);
+    if (rm == RM_QOP && om == OUT_S) return launch_t<NT, RM_QOP, OUT_S, 5>(a, grid, st);
     return cudaErrorInvalidValue;
   }
   if (rm == RM_RESID && om == OUT_UPDATE) {

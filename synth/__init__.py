@@ -91,6 +91,10 @@ CONFIGS = {
     # runs it with BDF2 on h = 1/40 -- here exponential Euler on a 1023^2 grid)
     "c7se": Config("c7se", 2, 1023, 0.0, 0.0, 0.64, 128, 1e-3, solvers=("fixed_point", "gmres"), a_im=1.0,
                    c_im=200.0, seed=7),
+    # c7bdf2: the same packet with the paper's own setup for it -- exponential BDF2 (scheme 3),
+    # dt = 0.05, alpha_opt = 0.0001953125, GMRES; h = 1/1024
+    "c7bdf2": Config("c7bdf2", 2, 1023, 0.0, 0.0, 6.4, 128, 0.0001953125, scheme=3,
+                     solvers=("gmres", "fixed_point"), tol=1e-10, a_im=1.0, c_im=200.0, seed=7),
 }
 
 

@@ -171,6 +171,73 @@ def test_cplx_full_size_sampled_modes(orc):
         assert np.abs(got[i] - want.astype(np.complex128)).max() < 1e-9 * np.linalg.norm(u0)
 
 
+# ------------------------------------------------------------------------------------------
+# complex BDF2 (K1 form 5; the paper's 2D Schroedinger setup)
+# ------------------------------------------------------------------------------------------
+BDF_CASES = [("c7bdf2", 31, 32), ("c7bdf2", 15, 8), ("c7bdf2", 7, 256), ("c7bdf2", 15, 128)]
+
+
+@pytest.mark.parametrize("name,n,nt", BDF_CASES)
+def test_cplx_bdf2_precond_and_residual_parity(orc, name, n, nt):
+    cfg = cfg_of(name, n, nt)
+    s = orc.spec(cfg)
+    plan = Plan(Problem.from_config(cfg))
+    R = synth.random_spacetime(cfg)
+    assert relmax(H(plan.precond_apply(TC(R))), orc.cplx_precond(s, R)) < 1e-11
+    u0 = synth.initial_condition(cfg)
+    U = synth.random_spacetime(cfg, scale=0.5)
+    Rg, rn2 = plan.residual(TC(u0), TC(U), norm=True)
+    want, wn2 = orc.cplx_residual(s, u0, U)
+    assert relmax(H(Rg), want) < 1e-11
+    assert abs(rn2 - wn2) < 1e-11 * wn2
+
+
+@pytest.mark.parametrize("solver", ["fixed_point", "gmres", "bicgstab"])
+def test_cplx_bdf2_solver_parity(orc, solver):
+    cfg = cfg_of("c7bdf2", 31, 32)
+    s = orc.spec(cfg)
+    plan = Plan(Problem.from_config(cfg), krylov_vectors=21)
+    u0 = synth.initial_condition(cfg)
+    if solver == "fixed_point":
+        U, rep = plan.fixed_point_solve(TC(u0), tol=cfg.tol, maxit=50)
+        Uo, st, its, _ = orc.cplx_fixed_point(s, u0, tol=cfg.tol, maxit=50)
+    elif solver == "gmres":
+        U, rep = plan.gmres_solve(TC(u0), tol=cfg.tol, restart=20, maxit=50)
+        Uo, st, its, _ = orc.cplx_gmres(s, u0, tol=cfg.tol, restart=20, maxit=50)
+        assert its == 3
+    else:
+        U, rep = plan.bicgstab_solve(TC(u0), tol=cfg.tol, maxit=50)
+        Uo, st, its, _ = orc.cplx_bicgstab(s, u0, tol=cfg.tol, maxit=50)
+    assert st == 0 and rep["converged"] and rep["iterations"] == its
+    assert relmax(H(U), Uo) < 1e-9
+
+
+def test_cplx_bdf2_full_size_sampled_modes(orc):
+    """c7bdf2 at full size (1023^2 x 128, complex, BDF2): GMRES converges in 3 iterations and
+    the solution's DST modes are E_J^{t+2} u-hat_J(0) (BDF2 is exact on the linear problem,
+    reading R16)."""
+    cfg = synth.CONFIGS["c7bdf2"]
+    s = orc.spec(cfg)
+    plan = Plan(Problem.from_config(cfg), krylov_vectors=5)
+    u0 = synth.initial_condition(cfg)
+    U, rep = plan.gmres_solve(TC(u0), tol=cfg.tol, restart=4, maxit=20)
+    assert rep["converged"] and rep["iterations"] == 3
+    Uh = H(U)
+    rng = np.random.default_rng(12)
+    kx = rng.integers(1, 40, 6)
+    ky = 2 * rng.integers(0, 20, 6) + 1
+    idx = (ky - 1) * cfg.n + (kx - 1)
+    ts = np.array([0, 5, 127])
+    uh0 = orc.dst_sample(s, u0.real, idx) + 1j * orc.dst_sample(s, u0.imag, idx)
+    got = orc.dst_sample_batch(s, Uh[ts].real, idx) + 1j * orc.dst_sample_batch(s, Uh[ts].imag, idx)
+    lam = orc.axis_eigs(cfg.n).astype(np.longdouble)
+    mu = lam[kx - 1] + lam[ky - 1]
+    z = np.longdouble(cfg.dt) * (np.clongdouble(complex(cfg.a, cfg.a_im)) * mu - np.clongdouble(complex(cfg.c, cfg.c_im)))
+    for i, t in enumerate(ts):
+        want = np.exp(z * (t + 2)) * uh0
+        assert np.abs(got[i] - want.astype(np.complex128)).max() < 1e-9 * np.linalg.norm(u0)
+
+
 def test_cplx_invalid_problems():
     base = dict(dim=1, n=15, a=0.0, c=0.0, dt=0.01, nt=8, alpha=1e-2, a_im=1.0, c_im=2.0)
     with pytest.raises(ExpdError) as e:  # nonlinear complex: not built

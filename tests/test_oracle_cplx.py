@@ -276,3 +276,19 @@ def test_cplx_bdf2_solvers_reach_sequential(orc, a, c):
                   lambda: orc.cplx_bicgstab(s, u0, tol=1e-13, maxit=80)):
         U, st, its, _ = solve()
         assert st == 0 and rel(U, Us) < 1e-10
+
+
+@pytest.mark.parametrize("n,nt", [(31, 16), (31, 32), (31, 64), (63, 16)])
+def test_cplx_bdf2_gmres_three_iterations(orc, n, nt):
+    """the 2D Schroedinger equation (a = i, c = 200i, the Gaussian packet of
+    :1066, dt = 0.05, alpha_opt = 0.0001953125) with the BDF2 preconditioner: GMRES
+    "consistently converges in just three iterations, regardless of the window size" (the
+    tolerance is not printed: any tol in [1e-11, 1e-8] gives 3 here; h = 1/32, 1/64 instead
+    of 1/40, which the power-of-two DST does not take)."""
+    s = cspec3(orc, 2, n, 1j, 200j, T=0.05 * nt, nt=nt, alpha=0.0001953125)
+    x = np.arange(1, n + 1) / (n + 1) - 0.5
+    g = np.exp(-x * x / (2 * 0.05 ** 2))
+    u0 = np.multiply.outer(g, g * np.exp(-5j * x))
+    U, st, its, hist = orc.cplx_gmres(s, u0, tol=1e-10, restart=20, maxit=20)
+    assert st == 0 and its == 3
+    assert rel(U, orc.cplx_sequential(s, u0)) < 1e-9
