@@ -12,7 +12,7 @@ import torch  # noqa: E402
 import synth  # noqa: E402
 from paper_2603_04350_b200 import Plan, Problem  # noqa: E402
 
-names = sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5"]
+names = sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5", "c3if", "c5if", "c1bdf2", "c2bdf2", "c6se", "c7se", "c7bdf2"]
 for name in names:
     cfg = synth.CONFIGS[name]
     u0 = torch.from_numpy(synth.initial_condition(cfg)).cuda()
@@ -20,7 +20,8 @@ for name in names:
         kv = 0 if solver != "gmres" else (21 if cfg.nst < 2e8 else 4)
         tol = cfg.tol
         plan = Plan(Problem.from_config(cfg), krylov_vectors=kv)
-        U = torch.zeros((cfg.nt,) + cfg.shape, dtype=torch.float64, device="cuda")
+        prob = Problem.from_config(cfg)
+        U = torch.zeros((cfg.nt,) + cfg.shape, dtype=prob.dtype, device="cuda")
         run = (lambda: plan.fixed_point_solve(u0, U, tol=tol, maxit=100)) if solver != "gmres" else \
               (lambda: plan.gmres_solve(u0, U, tol=tol, restart=min(20, kv - 1), maxit=100))
         run()  # warm-up (first solve builds the sweep graph)
