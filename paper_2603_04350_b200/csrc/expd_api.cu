@@ -691,6 +691,7 @@ extern "C" expd_status expd_nonlin_hat(expd_plan* p, const double* uhat, double*
   const size_t row = sizeof(double) * p->g.n, prow = sizeof(double) * p->g.M;
   const size_t rows = (size_t)(p->g.N / p->g.n);
   if (p->dist && !p->nl) return fail(p, EXPD_ERR_UNSUPPORTED, "expd_nonlin_hat: linear distributed plan");
+  if (p->cx) return fail(p, EXPD_ERR_UNSUPPORTED, "expd_nonlin_hat: real plans only");
   double* tin = p->dist ? p->UT : p->T1;
   double* tout = p->dist ? p->NT : p->T1 + chunk * p->g.npad;
   for (long s0 = 0; s0 < nslices; s0 += chunk) {
