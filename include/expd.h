@@ -71,10 +71,10 @@ typedef struct {
                          non-zero makes a COMPLEX plan (the paper's Schroedinger tests, a = i,
                          c = 2i): u_t = (a Delta - c) u with a = a + i a_im,
                          c = c + i c_im, Re a >= 0 (a != 0), Re c >= 0; linear only
-                         (npoly = 0), scheme EXPD_EXP_EULER or EXPD_BDF2, one GPU (no
-                         expd_dist).  Every
-                         space-time / slice argument of a complex plan (u0, U, R, S) is
-                         complex128: interleaved (re, im) doubles, 2 N doubles per slice.
+                         (npoly = 0), scheme EXPD_EXP_EULER or EXPD_BDF2, one or more
+                         GPUs.  Every space-time / slice argument of a complex plan (u0,
+                         U, R, S) is complex128: interleaved (re, im) doubles, 2 N doubles
+                         per slice.
                          GMRES and BiCGStab run over C with the Hermitian inner product
                          (reading R18); expd_dst / expd_nonlin_hat stay real-only.       */
 } expd_problem;
@@ -90,7 +90,8 @@ typedef struct {
    time slab = slices [t0, t0 + nt_local) (physical API vectors U, R, S and stage 3);
    mode slab = padded spectral entries [mode_off, mode_off + mode_len) of every slice
    (the time-local fused kernel K1).  npad = entries of a padded spectral slice
-   (n^{dim-1} (n+1)). */
+   (n^{dim-1} (n+1)); complex problems count doubles of the interleaved (re, im) slice, so
+   npad, mode_off and mode_len are twice the real ones. */
 typedef struct {
   int rank, nranks;
   long npad, mode_off, mode_len;

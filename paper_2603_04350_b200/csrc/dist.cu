@@ -198,6 +198,7 @@ using namespace expd;
 // ---------------------------------------------------------------------------------------
 // C-ABI (include/expd.h "Multi-GPU")
 // ---------------------------------------------------------------------------------------
+// the geometry the partition is computed on (complex problems: doubled, as in the plan)
 static bool geom_of(const expd_problem* p, Geom* g) {
   if (!p || p->dim < 1 || p->dim > 3 || p->n < 3) return false;
   g->dim = p->dim;
@@ -208,6 +209,7 @@ static bool geom_of(const expd_problem* p, Geom* g) {
   for (int i = 1; i < p->dim; ++i) npad *= p->n;
   g->N = N;
   g->npad = npad;
+  if (p->a_im != 0.0 || p->c_im != 0.0) *g = complex_layout_geom(*g);
   return true;
 }
 

@@ -154,9 +154,8 @@ extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dis
       !std::isfinite(P.a) || !std::isfinite(P.c) || !std::isfinite(P.dt))
     return EXPD_ERR_INVALID_ARG;
   if (P.nt > 256) return EXPD_ERR_UNSUPPORTED;
-  if (cx && (P.npoly > 0 || (P.scheme != EXPD_EXP_EULER && P.scheme != EXPD_BDF2) ||
-             (dist && (dist->nranks > 1 || dist->nccl_comm))))
-    return EXPD_ERR_UNSUPPORTED;  // complex plans: linear exponential Euler or BDF2, one GPU
+  if (cx && (P.npoly > 0 || (P.scheme != EXPD_EXP_EULER && P.scheme != EXPD_BDF2)))
+    return EXPD_ERR_UNSUPPORTED;  // complex plans: linear exponential Euler or BDF2
   int nranks = dist ? dist->nranks : 1;
   if (nranks < 1 || nranks > EXPD_MAX_RANKS || (dist && (dist->rank < 0 || dist->rank >= nranks)))
     return EXPD_ERR_INVALID_ARG;
@@ -201,11 +200,14 @@ extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dis
     return st;
   }
   p->dist = nranks > 1 || (dist && dist->nccl_comm);
-  if (!dist_layout(p->g, P.nt, p->dist ? dist->rank : 0, p->dist ? nranks : 1, &p->L)) {
+  // the partition is computed in doubles of a spectral slice: a complex slice has 2 npad
+  // (interleaved (re, im) per mode, whole padded x-lines of 2 M doubles per slab unit)
+  if (!dist_layout(cx ? complex_layout_geom(p->g) : p->g, P.nt, p->dist ? dist->rank : 0, p->dist ? nranks : 1,
+                   &p->L)) {
     expd_plan_destroy(p);
     return EXPD_ERR_INVALID_ARG;
   }
-  p->mlen = p->L.mode_len[p->L.rank] * (cx ? 2 : 1);  // doubles per slice of the mode slab
+  p->mlen = p->L.mode_len[p->L.rank];  // doubles per slice of the mode slab
   p->moff = p->L.mode_off[p->L.rank];
   p->ntl = p->L.ntl[p->L.rank];
   p->t0 = p->L.t0[p->L.rank];
@@ -258,7 +260,8 @@ static Layout layout(const expd_plan* p, int kv) {
   const size_t vec = align_up(sizeof(double) * (size_t)p->prob.nt * (size_t)p->mlen);
   const size_t nhv = align_up(sizeof(double) * (size_t)(p->prob.nt + ((p->dist || p->nshift) ? 1 : 0)) *
                               (size_t)p->mlen);
-  const size_t tsl = p->dist ? align_up(sizeof(double) * (size_t)p->ntl * (size_t)p->g.npad) : 0;
+  const size_t tsl =
+      p->dist ? align_up(sizeof(double) * (size_t)p->ntl * (size_t)p->g.npad * (p->cx ? 2 : 1)) : 0;
   const size_t sl = align_up(sizeof(double) * (size_t)p->g.npad * (p->cx ? 2 : 1));
   size_t off = 0;
   L.vec = vec;
@@ -437,7 +440,12 @@ static expd_status load_u0(expd_plan* p, const double* u0) {
 
 // physical time-slab slices (the API layout) <-> the spectral mode slab
 static expd_status phys_to_mode(expd_plan* p, const double* U, double* mode) {
-  if (p->cx) return cx_phys_to_mode(p, U, mode, p->prob.nt);
+  if (p->cx && !p->dist) return cx_phys_to_mode(p, U, mode, p->prob.nt);
+  if (p->cx) {  // the local time slab -> interleaved complex spectral slices -> mode slab
+    expd_status s = cx_phys_to_mode(p, U, p->UT, p->ntl);
+    if (s) return s;
+    return a2a(p, A2A_T2M, p->UT, mode);
+  }
   if (!p->dist) {
     CUDA_TRY(p, dst_slices(p->g, dst_tables(p), U, false, mode, true, p->prob.nt, p->scratch, p->stream));
     return EXPD_OK;
@@ -446,7 +454,12 @@ static expd_status phys_to_mode(expd_plan* p, const double* U, double* mode) {
   return a2a(p, A2A_T2M, p->UT, mode);
 }
 static expd_status mode_to_phys(expd_plan* p, const double* mode, double* U) {
-  if (p->cx) return cx_mode_to_phys(p, mode, U, p->prob.nt);
+  if (p->cx && !p->dist) return cx_mode_to_phys(p, mode, U, p->prob.nt);
+  if (p->cx) {
+    expd_status s = a2a(p, A2A_M2T, mode, p->UT);
+    if (s) return s;
+    return cx_mode_to_phys(p, p->UT, U, p->ntl);
+  }
   if (!p->dist) {
     CUDA_TRY(p, dst_slices(p->g, dst_tables(p), mode, true, U, false, p->prob.nt, p->scratch, p->stream));
     return EXPD_OK;

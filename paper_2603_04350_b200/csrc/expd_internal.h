@@ -141,6 +141,14 @@ struct A2AMsg {
 };
 enum A2ADir { A2A_MODE_TO_TIME = 0, A2A_TIME_TO_MODE = 1 };
 bool dist_layout(const Geom& g, int nt, int rank, int nranks, DistLayout* L);
+// the geometry the partition of a complex plan is computed on: a spectral slice of 2 npad
+// doubles with x-lines of 2 M doubles (interleaved (re, im) per mode)
+inline Geom complex_layout_geom(const Geom& g) {
+  Geom c = g;
+  c.npad = 2 * g.npad;
+  c.M = 2 * g.M;
+  return c;
+}
 void a2a_schedule(const DistLayout& L, int dir, int shift, std::vector<A2AMsg>& sends, std::vector<A2AMsg>& recvs);
 // executes the messages whose slice key lies in [s_lo, s_hi) (one chunk of a pipelined
 // all-to-all; every rank must pass the same range)

@@ -313,3 +313,25 @@ def _chunked_worker(rank, P, port, name, n, nt, k):
 @pytest.mark.parametrize("P,name,n,nt,k", [(2, "c3", 31, 16, 3), (4, "c5", 15, 16, 1), (2, "c4", 7, 8, 2)])
 def test_chunked_a2a_gloo(P, name, n, nt, k):
     _spawn(_chunked_worker, P, name, n, nt, k)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+@pytest.mark.parametrize("dim,n,nt", [(1, 15, 8), (2, 15, 8), (3, 7, 8)])
+def test_complex_layout_is_the_real_one_doubled(P, dim, n, nt):
+    """A complex problem partitions the interleaved (re, im) spectral slice: the same padded
+    x-lines per rank as the real problem (dim >= 2), every offset and length doubled."""
+    base = dict(dim=dim, n=n, a=1.0, c=0.0, dt=0.01, nt=nt, alpha=1e-2)
+    real = Problem(**base)
+    cplx = Problem(**{**base, "a": 0.0, "a_im": 1.0, "c_im": 2.0})
+    for r in range(P):
+        lr, lc = layout(real, r, P), layout(cplx, r, P)
+        assert lc["npad"] == 2 * lr["npad"] and lc["nt_local"] == lr["nt_local"]
+        assert lc["mode_len"] % 2 == 0 and lc["mode_off"] % 2 == 0
+        if dim >= 2:
+            assert lc["mode_off"] == 2 * lr["mode_off"] and lc["mode_len"] == 2 * lr["mode_len"]
+    off = 0
+    for r in range(P):
+        lc = layout(cplx, r, P)
+        assert lc["mode_off"] == off
+        off += lc["mode_len"]
+    assert off == 2 * layout(real, 0, P)["npad"]

@@ -238,6 +238,43 @@ def test_cplx_bdf2_full_size_sampled_modes(orc):
         assert np.abs(got[i] - want.astype(np.complex128)).max() < 1e-9 * np.linalg.norm(u0)
 
 
+# ------------------------------------------------------------------------------------------
+# complex plans on the distributed schedule (a 1-rank NCCL communicator: the all-to-alls
+# become local copies, the mode / time slab code path runs)
+# ------------------------------------------------------------------------------------------
+@pytest.fixture(scope="module")
+def comm1():
+    from paper_2603_04350_b200 import Comm
+
+    c = Comm(0, 1, 0)
+    yield c
+    c.close()
+
+
+@pytest.mark.parametrize("name,n,nt", [("c6se", 63, 32), ("c7se", 31, 64), ("c7bdf2", 31, 32)])
+def test_cplx_dist1_parity(orc, comm1, name, n, nt):
+    cfg = cfg_of(name, n, nt)
+    s = orc.spec(cfg)
+    plan = Plan(Problem.from_config(cfg), krylov_vectors=21, comm=comm1)
+    R = synth.random_spacetime(cfg)
+    assert relmax(H(plan.precond_apply(TC(R))), orc.cplx_precond(s, R)) < 1e-11
+    u0 = synth.initial_condition(cfg)
+    U = synth.random_spacetime(cfg, scale=0.5)
+    Rg, rn2 = plan.residual(TC(u0), TC(U), norm=True)
+    want, wn2 = orc.cplx_residual(s, u0, U)
+    assert relmax(H(Rg), want) < 1e-11 and abs(rn2 - wn2) < 1e-11 * wn2
+    for solve, ref in ((lambda: plan.fixed_point_solve(TC(u0), tol=cfg.tol, maxit=50),
+                        lambda: orc.cplx_fixed_point(s, u0, tol=cfg.tol, maxit=50)),
+                       (lambda: plan.gmres_solve(TC(u0), tol=cfg.tol, restart=20, maxit=50),
+                        lambda: orc.cplx_gmres(s, u0, tol=cfg.tol, restart=20, maxit=50)),
+                       (lambda: plan.bicgstab_solve(TC(u0), tol=cfg.tol, maxit=50),
+                        lambda: orc.cplx_bicgstab(s, u0, tol=cfg.tol, maxit=50))):
+        Ug, rep = solve()
+        Uo, st, its, _ = ref()
+        assert st == 0 and rep["converged"] and rep["iterations"] == its
+        assert relmax(H(Ug), Uo) < 1e-9
+
+
 def test_cplx_invalid_problems():
     base = dict(dim=1, n=15, a=0.0, c=0.0, dt=0.01, nt=8, alpha=1e-2, a_im=1.0, c_im=2.0)
     with pytest.raises(ExpdError) as e:  # nonlinear complex: not built
