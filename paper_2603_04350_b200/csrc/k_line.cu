@@ -9,8 +9,9 @@
 //   * persistent CTAs, one line pair per work item, two shared-memory buffers: the TMA
 //     brings item i+1 while item i is transformed (no exposed HBM / L2 latency);
 //   * x-axis (ROW) items: the two rows are loaded / stored as TMA tensor boxes
-//     {16 doubles, M/16} with the 128-byte swizzle, so the mirror reads of the
-//     pre-processing and the per-thread chunk writes of the result are bank-conflict free;
+//     {16 doubles, M/16}: loaded linear (the stage-0 reads of x_i and of the mirror x_{M-i}
+//     are runs of consecutive doubles per half-warp), stored with the 128-byte swizzle (the
+//     per-thread chunk writes of the result, 128 bytes apart per lane, hit distinct banks);
 //   * strided-axis (COL) items: one column pair (16 B per grid row) moved as TMA boxes
 //     of {2 doubles, 256 rows} into / out of a linear layout (the result is compacted
 //     from the padded work layout before the store);
@@ -416,7 +417,10 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
         if (i == 0) {
           v[r] = make_double2(0.0, 0.0);
         } else if (AX == AX_ROW) {
-          const uint32_t o1 = row_sw(i - 1), o2 = row_sw(M - i - 1);
+          // the input rows land UNswizzled (linear): a half-warp's 16 reads of x_i at i - 1
+          // and of the mirror at M - i - 1 each cover 16 consecutive doubles, i.e. 32
+          // distinct banks (the 128-byte swizzle splits the i - 1 run over two lines)
+          const uint32_t o1 = (uint32_t)(i - 1) * 8u, o2 = (uint32_t)(M - i - 1) * 8u;
           const double2 z = make_double2(*reinterpret_cast<const double*>(cb + o1),
                                          *reinterpret_cast<const double*>(cb + M * 8 + o1));
           const double2 zm = make_double2(*reinterpret_cast<const double*>(cb + o2),
@@ -532,7 +536,10 @@ cudaError_t make_tmap_2d(CUtensorMap* m, const double* ptr, unsigned long long c
 bool tma_available() { return encode_fn() != nullptr; }
 
 // Tensor map of nslices padded spectral slices for one axis pass (COL: G column pairs).
-static cudaError_t axis_map(CUtensorMap* m, const Geom& g, int ax, const double* ptr, long nslices, int G) {
+// ROW: sw = true for the output map (the per-thread chunk writes need the 128-byte swizzle
+// to be conflict free), false for the input map (linear, see k_line's stage-0 reads)
+static cudaError_t axis_map(CUtensorMap* m, const Geom& g, int ax, const double* ptr, long nslices, int G,
+                            bool sw = true) {
   const cuuint64_t M = (cuuint64_t)g.M, n = (cuuint64_t)g.n;
   const cuuint64_t rows = (cuuint64_t)(g.npad / g.M);  // spectral rows per slice
   const cuuint64_t sl = (cuuint64_t)g.npad * 8;
@@ -540,7 +547,7 @@ static cudaError_t axis_map(CUtensorMap* m, const Geom& g, int ax, const double*
     const cuuint64_t d[4] = {16, M / 16, rows, (cuuint64_t)nslices};
     const cuuint64_t s[3] = {128, M * 8, sl};
     const cuuint32_t b[4] = {16, (cuuint32_t)(M / 16), 1, 1};
-    return make_map(m, ptr, d, s, b, true);
+    return make_map(m, ptr, d, s, b, sw);
   }
   const cuuint64_t nz = g.dim == 3 ? n : 1;
   const cuuint64_t d[4] = {M, n, nz, (cuuint64_t)nslices};
@@ -578,7 +585,7 @@ static cudaError_t launch_line(const Geom& g, const DstTables& t, const Poly& P,
     if (per_sm < 1) per_sm = 1;
   }
   CUtensorMap mi, mo;
-  cudaError_t e = axis_map(&mi, g, AX, in, nslices, G);
+  cudaError_t e = axis_map(&mi, g, AX, in, nslices, G, /*sw=*/false);
   if (e != cudaSuccess) return e;
   if ((e = axis_map(&mo, g, AX, out, nslices, G)) != cudaSuccess) return e;
   LineArgs a{};
