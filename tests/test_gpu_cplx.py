@@ -39,7 +39,8 @@ def cfg_of(name, n=None, nt=None):
 
 # nt 4 / 8: single-stage register K1; 16..256: the TMA K1 (L = 2, 3); dims 1..3
 CASES = [("c6se", None, None), ("c6se", 63, 4), ("c6se", 31, 8), ("c7se", 31, 16), ("c7se", 15, 64),
-         ("c7se", 31, 128), ("c7se", 7, 256)]
+         ("c7se", 31, 128), ("c7se", 7, 256),
+         ("c6se", 3, 4), ("c7se", 3, 8), ("c6se", 4095, 4), ("c7se", 255, 4)]  # smallest / largest lines
 CASES3 = [("c7se", 7, 32)]
 
 
