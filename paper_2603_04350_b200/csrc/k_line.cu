@@ -140,7 +140,25 @@ template <int M, int G>
 struct LPre {
   double sp[LGeo<M, G, 1>::R0];
   double2 tmid, ta, tb;
+  int pj;  // this thread's partner job of the last stage (see partner_job)
 };
+
+// Lane -> partner job of the last FFT stage.  With one pair job per thread (G = 1, NSL / 2 =
+// T) any bijection works; the tables (tools/partner_lanes.py) group the jobs so that each
+// 8-lane phase of the partner reads and unpack writes hits distinct bank groups (the
+// identity walks the mirrored frequencies downwards and straddles a padding slot in half
+// of the phases).  Other configurations: the identity.
+#include "partner_lanes.inc"
+template <int M, int G>
+__device__ __forceinline__ int partner_job(int tid) {
+  using D = LGeo<M, G, 1>;
+  if constexpr (G == 1 && D::NSL / 2 == D::THREADS && (M == 512 || M == 1024 || M == 2048)) {
+    if constexpr (M == 512) return __ldg(kPartnerJob512 + tid);
+    else if constexpr (M == 1024) return __ldg(kPartnerJob1024 + tid);
+    else return __ldg(kPartnerJob2048 + tid);
+  }
+  return tid;
+}
 
 // position p of line pair g in the padded work layout [SW][G]
 template <int M, int G>
@@ -208,7 +226,7 @@ __device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* 
   double2 va[PJT][RL], vb[PJT][RL];
 #pragma unroll
   for (int pt = 0; pt < PJT; ++pt) {
-    const int PJ = threadIdx.x + pt * D::THREADS;
+    const int PJ = PJT == 1 ? pre.pj : threadIdx.x + pt * D::THREADS;
     if (PJOBS % D::THREADS == 0 || PJ < PJOBS) {
       const int gg = PJ % G, pj = PJ / G;
       const int ja = pj, jb = pj == 0 ? NSL / 2 : NSL - pj;
@@ -236,7 +254,7 @@ __device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* 
   double2* Eb = buf + D::WS * G;
 #pragma unroll
   for (int pt = 0; pt < PJT; ++pt) {
-    const int PJ = threadIdx.x + pt * D::THREADS;
+    const int PJ = PJT == 1 ? pre.pj : threadIdx.x + pt * D::THREADS;
     if (PJOBS % D::THREADS == 0 || PJ < PJOBS) {
       const int gg = PJ % G, pj = PJ / G;
       const int ja = pj, jb = pj == 0 ? NSL / 2 : NSL - pj;
@@ -364,6 +382,7 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
   __builtin_assume(tid < D::THREADS);
   const int g = tid % G, j = tid / G;
   const double scale = sqrt(2.0 / (double)M);
+  const int my_pj = partner_job<M, G>(tid);
 
   if (tid == 0) {
     prefetch_tmap(&in_map);
@@ -391,14 +410,16 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
     const double* sinp = a.sinp;
     asm volatile("" : "+l"(tw), "+l"(sinp));
     LPre<M, G> pre;
+    pre.pj = my_pj;
     {
 #pragma unroll
       for (int r = 0; r < R0; ++r) pre.sp[r] = __ldg(sinp + j + T * r);  // sinp[0] = 0
       constexpr int NS1 = R0, TWS1 = M / (NS1 * D::RM1);
       pre.tmid = __ldg(tw + (j % NS1) * TWS1);
       constexpr int NSL = D::NSL;
-      pre.ta = __ldg(tw + (j < NSL / 2 ? j : 0));
-      pre.tb = __ldg(tw + (j == 0 ? NSL / 2 : (j < NSL / 2 ? NSL - j : 0)));
+      const int pj = pre.pj / G;  // the partner job's frequency set (G = 1: the table entry)
+      pre.ta = __ldg(tw + (pj < NSL / 2 ? pj : 0));
+      pre.tb = __ldg(tw + (pj == 0 ? NSL / 2 : (pj < NSL / 2 ? NSL - pj : 0)));
     }
     mbar_wait(&bar[cur], (uint32_t)((NBUF == 2 ? (it >> 1) : it) & 1));
 
