@@ -304,12 +304,14 @@ def run_ours(args):
     ev1 = torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize(dev)
     ev0.record(stream)
-    ms_nl, ms_k1, norms = [], [], []
+    ms_nl, ms_k1, norms, passes = [], [], [], []
     for _ in range(args.steps):
         norms.append(step())
         a, b = plan.sweep_stage_ms()
         ms_nl.append(a)
         ms_k1.append(b)
+        if nl and comm is None and cfg.dim == 2:
+            passes.append(plan.sweep_pass_ms())  # stage-3 passes, events inside the sweep
     ev1.record(stream)
     torch.cuda.synchronize(dev)
     ck = clocks.stop()
@@ -351,29 +353,34 @@ def run_ours(args):
                "sweep_algorithmic_gbs": (k1_bytes + s3_bytes) / (ms_step * 1e-3) / 1e9,
                "sweep_frac_of_peak": (k1_bytes + s3_bytes) / (ms_step * 1e-3) / 1e9 / hbm_peak}
     roofline = k1_roof
-    if nl and comm is None and cfg.dim == 2:
-        # stage-3 kernel families, timed live with CUDA events on the plan's stream after the
-        # timed region (16-slice launches, as in the sweep's chunks); fp64-bound
-        ns = min(16, cfg.nt)
+    if passes:
+        # stage-3 kernel families, timed live INSIDE the timed sweeps: CUDA events recorded on
+        # the plan's stream between consecutive passes of stage 3 (expd_sweep_pass_ms), summed
+        # per family and averaged over the steps; fp64-bound
         M = cfg.n + 1
-        pairs = ((cfg.n + 1) // 2) * ns
-        f_t = dst_flops_per_line_pair(M) * pairs                      # one axis transform
-        f_nl = 2 * f_t + 3.0 * 2 * M * pairs                          # [V, N, V], cubic N
+        s3 = cfg.nt - 1                                               # slices per sweep
+        pairs = (cfg.n + 1) // 2                                      # line pairs per slice
+        f_t = dst_flops_per_line_pair(M) * pairs                      # one axis transform / slice
+        f_nl = 2 * f_t + 3.0 * 2 * M * pairs                          # [V, N, V], cubic N / slice
         fam = {}
         try:
             tprof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
         except Exception:
             tprof = {}
-        for which, label, flops, per_step in ((4, "line_x", f_t, 2), (6, "line_y_nl", f_nl, 1)):
-            ms_l = plan.debug_kernel_ms(which, ns, 5)
-            tf = flops / (ms_l * 1e-3) / 1e12
-            fam[label] = {"bound": "alu", "kernel": f"k_line ({label}: {'x-axis DST-I' if which == 4 else 'fused y [V, N(u), V]'})",
+        for label, key, nkey, flops, slices in (("line_x", "x_ms", "x_launches", f_t, 2 * s3),
+                                                ("line_y_nl", "fused_ms", "fused_launches", f_nl, s3)):
+            ms_sweep = statistics.mean(p_[key] for p_ in passes)
+            nlaunch = passes[-1][nkey]
+            tf = flops * slices / (ms_sweep * 1e-3) / 1e12
+            fam[label] = {"bound": "alu", "kernel": f"k_line ({label}: {'x-axis DST-I' if label == 'line_x' else 'fused y [V, N(u), V]'})",
                           "achieved": tf, "peak": FP64_PEAK_TFLOPS,
                           "peak_source": "measured DFMA loop (profiles/r01_probe_fp64_hbm.txt)", "unit": "TFLOP/s",
                           "frac": tf / FP64_PEAK_TFLOPS, "traffic": tprof.get(f"{cfg.name}:{label}"),
-                          "algorithmic_flops_per_launch": flops,
-                          "launch_ms": ms_l, "slices_per_launch": ns,
-                          "ms_per_step": ms_l * per_step * (cfg.nt - 1) / ns}
+                          "traffic_note": "ncu dram bytes of one 16-slice launch",
+                          "algorithmic_flops_per_launch": flops * slices / max(nlaunch, 1),
+                          "launch_ms": ms_sweep / max(nlaunch, 1), "launches_per_step": nlaunch,
+                          "slices_per_step": slices, "ms_per_step": ms_sweep,
+                          "timing": "CUDA events between the passes inside the timed sweeps"}
         kernels.update(fam)
         # the dominant kernel of the step by device time
         cand = [(k1_ms, k1_roof)] + [(v["ms_per_step"], v) for v in fam.values()]

@@ -211,6 +211,14 @@ expd_status expd_nonlin_hat(expd_plan* plan, const double* uhat, double* nhat, l
    the fused time-local kernel K1, in milliseconds. */
 expd_status expd_set_profiling(expd_plan* plan, int enable);
 expd_status expd_sweep_stage_ms(expd_plan* plan, double* ms_nonlin, double* ms_time);
+/* Stage-3 pass times of the last sweep (set_profiling on, single-GPU nonlinear plans with
+   the TMA line kernels): device ms summed over the sweep's x-passes, plain strided passes
+   (3-D) and fused strided [V, N(u), V] passes, measured by CUDA events recorded on the
+   plan's stream between consecutive passes inside the sweep, and the launch counts.
+   UNSUPPORTED when no such timing exists.  Diagnostics for bench.py's per-kernel
+   rooflines. */
+expd_status expd_sweep_pass_ms(expd_plan* plan, double* ms_x, double* ms_strided, double* ms_fused, int* n_x,
+                               int* n_strided, int* n_fused);
 /* Diagnostics for tuning: average device time (ms, CUDA events) of `reps` back-to-back
    launches of one kernel family on the workspace's spectral state: which = 0 x-axis DST
    pass, 1 strided-axis DST pass, 2 fused strided IDST -> N -> DST pass (each over nslices

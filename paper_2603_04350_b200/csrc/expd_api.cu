@@ -66,6 +66,8 @@ struct expd_plan {
   // optional stage timing: ev[0] before stage 3, ev[1] before K1, ev[2] after K1
   bool prof = false;
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
+  std::vector<cudaEvent_t> tev;  // per-pass events of stage 3 (profiling, single GPU)
+  PassTimer timer{};
   // distributed sweep pipelining: the all-to-alls run on comm_stream in chunks of the time
   // slab, overlapped with stage 3 of the neighbouring chunks (events in pev)
   cudaStream_t comm_stream = nullptr;
@@ -342,6 +344,7 @@ extern "C" void expd_plan_destroy(expd_plan* p) {
   for (cudaEvent_t e : p->pev) cudaEventDestroy(e);
   for (int i = 0; i < 3; ++i)
     if (p->ev[i]) cudaEventDestroy(p->ev[i]);
+  for (cudaEvent_t e : p->tev) cudaEventDestroy(e);
   cudaFree(p->d_lam);
   cudaFree(p->d_twt);
   cudaFree(p->d_g);
@@ -481,8 +484,15 @@ static cudaError_t enqueue_sweep(expd_plan* p, cudaStream_t st) {
   cudaError_t e = record(p, 0, st);
   if (e != cudaSuccess) return e;
   if (p->nl) {
+    PassTimer* tm = nullptr;
+    if (p->prof && !p->tev.empty()) {
+      p->timer.ev = p->tev.data();
+      p->timer.cap = (int)p->tev.size();
+      p->timer.ext = p->capturing;
+      tm = &p->timer;
+    }
     e = nonlin_slices(p->g, dst_tables(p), p->Uh, p->Nh + p->g.npad, p->prob.nt - 1 + p->nshift, p->prob.npoly,
-                      p->prob.q, p->scratch, st);
+                      p->prob.q, p->scratch, st, tm);
     if (e != cudaSuccess) return e;
   }
   if ((e = record(p, 1, st)) != cudaSuccess) return e;
@@ -724,6 +734,12 @@ extern "C" expd_status expd_set_profiling(expd_plan* p, int enable) {
   if (s) return s;
   for (int i = 0; i < 3; ++i)
     if (!p->ev[i]) CUDA_TRY(p, cudaEventCreate(&p->ev[i]));
+  if (p->tev.empty() && p->nl && !p->dist) {  // one event per stage-3 pass + the end
+    const long ns = p->prob.nt - 1 + p->nshift, ch = nonlin_chunk_slices(p->g);
+    const long cap = ((ns + ch - 1) / ch) * 5 + 2;
+    p->tev.resize(cap < 512 ? cap : 512);
+    for (auto& e : p->tev) CUDA_TRY(p, cudaEventCreate(&e));
+  }
   if (p->prof != (enable != 0) && p->sweep_exec) {
     cudaGraphExecDestroy(p->sweep_exec);  // recapture with / without the event nodes
     p->sweep_exec = nullptr;
@@ -740,6 +756,32 @@ extern "C" expd_status expd_sweep_stage_ms(expd_plan* p, double* ms_nonlin, doub
   CUDA_TRY(p, cudaEventElapsedTime(&b, p->ev[1], p->ev[2]));
   if (ms_nonlin) *ms_nonlin = a;
   if (ms_time) *ms_time = b;
+  return EXPD_OK;
+}
+
+extern "C" expd_status expd_sweep_pass_ms(expd_plan* p, double* ms_x, double* ms_strided, double* ms_fused,
+                                          int* n_x, int* n_strided, int* n_fused) {
+  if (!p || !p->prof) return fail(p, EXPD_ERR_INVALID_ARG, "profiling not enabled");
+  if (p->tev.empty() || p->timer.used < 2)
+    return fail(p, EXPD_ERR_UNSUPPORTED, "no stage-3 pass timing (linear, distributed or non-TMA plan)");
+  double t[3] = {0.0, 0.0, 0.0};
+  int n[3] = {0, 0, 0};
+  CUDA_TRY(p, cudaEventSynchronize(p->tev[p->timer.used - 1]));
+  for (int k = 0; k + 1 < p->timer.used; ++k) {
+    float m = 0.f;
+    CUDA_TRY(p, cudaEventElapsedTime(&m, p->tev[k], p->tev[k + 1]));
+    const int kind = p->timer.kind[k];
+    if (kind >= 0 && kind < 3) {
+      t[kind] += m;
+      ++n[kind];
+    }
+  }
+  if (ms_x) *ms_x = t[0];
+  if (ms_strided) *ms_strided = t[1];
+  if (ms_fused) *ms_fused = t[2];
+  if (n_x) *n_x = n[0];
+  if (n_strided) *n_strided = n[1];
+  if (n_fused) *n_fused = n[2];
   return EXPD_OK;
 }
 

@@ -83,8 +83,19 @@ struct DstTables {
 cudaError_t dst_slices(const Geom& g, const DstTables& t, const double* src, bool src_spectral, double* dst,
                        bool dst_spectral, long nslices, double* scratch, cudaStream_t st);
 // N-hat = V N(V u-hat) for nslices spectral slices (stage 3 of the sweep, K4).
+// Optional in-stream timing of stage 3's passes (profiling runs): an event is recorded
+// before every axis pass and after the last one; kind[k] says which pass interval k is
+// (0 x-pass, 1 plain strided pass, 2 fused strided [V, N, V] pass).  ext: recording inside
+// a CUDA-graph capture.
+struct PassTimer {
+  cudaEvent_t* ev;
+  int cap;
+  bool ext;
+  int used;
+  int kind[512];
+};
 cudaError_t nonlin_slices(const Geom& g, const DstTables& t, const double* uhat, double* nhat, long nslices,
-                          int npoly, const double* q, double* scratch, cudaStream_t st);
+                          int npoly, const double* q, double* scratch, cudaStream_t st, struct PassTimer* timer = nullptr);
 // N-hat = V N(u) for physical slices u (row stride n).
 cudaError_t nonlin_phys_slices(const Geom& g, const DstTables& t, const double* u, double* nhat, long nslices,
                                int npoly, const double* q, double* scratch, cudaStream_t st);

@@ -639,22 +639,40 @@ static bool use_line(const Geom& g) {
   return v && g.dim >= 2 && line_supported(g);
 }
 
+static cudaError_t mark(PassTimer* tm, int kind, cudaStream_t st) {
+  if (!tm || tm->used >= tm->cap) return cudaSuccess;
+  cudaEvent_t e = tm->ev[tm->used];
+  if (kind >= 0 && tm->used < 512) tm->kind[tm->used] = kind;
+  ++tm->used;
+  return tm->ext ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal) : cudaEventRecord(e, st);
+}
+
 cudaError_t nonlin_slices(const Geom& g, const DstTables& t, const double* uhat, double* nhat, long nslices,
-                          int npoly, const double* q, double* scratch, cudaStream_t st) {
+                          int npoly, const double* q, double* scratch, cudaStream_t st, PassTimer* tm) {
   Poly P = make_poly(npoly, q);
   const int rows_ps = (int)(g.N / g.n);
   const long chunk = nonlin_chunk_slices(g);
   const bool tl = use_line(g);
+  if (tm) tm->used = 0;
   for (long s0 = 0; s0 < nslices; s0 += chunk) {
     long ns = nslices - s0 < chunk ? nslices - s0 : chunk;
     const double* in = uhat + s0 * g.npad;
     double* out = nhat + s0 * g.npad;
     if (tl) {
       // x (inverse) -> scratch ; [dim 3: y] ; last axis fused [V, N, V] ; [dim 3: y] ; x -> out
+      CK(mark(tm, 0, st));
       CK(line_pass(g, t, P, 0, false, in, scratch, ns, st));
-      if (g.dim == 3) CK(line_pass(g, t, P, 1, false, scratch, scratch, ns, st));
+      if (g.dim == 3) {
+        CK(mark(tm, 1, st));
+        CK(line_pass(g, t, P, 1, false, scratch, scratch, ns, st));
+      }
+      CK(mark(tm, 2, st));
       CK(line_pass(g, t, P, g.dim - 1, true, scratch, scratch, ns, st));
-      if (g.dim == 3) CK(line_pass(g, t, P, 1, false, scratch, scratch, ns, st));
+      if (g.dim == 3) {
+        CK(mark(tm, 1, st));
+        CK(line_pass(g, t, P, 1, false, scratch, scratch, ns, st));
+      }
+      CK(mark(tm, 0, st));
       CK(line_pass(g, t, P, 0, false, scratch, out, ns, st));
       continue;
     }
@@ -672,6 +690,7 @@ cudaError_t nonlin_slices(const Geom& g, const DstTables& t, const double* uhat,
     RowsOp r2{scratch, g.npad, g.M, out, g.npad, g.M, rows_ps, ns, false, false};
     CK(rows(g.M, r2, t, P, st));
   }
+  if (tl) CK(mark(tm, -1, st));  // end of the last pass
   return cudaSuccess;
 }
 

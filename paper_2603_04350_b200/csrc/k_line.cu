@@ -645,8 +645,10 @@ template <int M, int AX, bool NL>
 static cudaError_t launch_col(const Geom& g, const DstTables& t, const Poly& P, const double* in, double* out,
                               long nslices, cudaStream_t st) {
   if constexpr (M == 2048) {
-    // measured on c5 (profiles/r01): plain strided pass fastest with 2 column pairs per item
-    // (32-byte TMA rows), the fused [V, N, V] pass with 1 pair and 1 buffer (more CTAs / SM)
+    // measured on c5 inside the sweep (profiles/r01): plain strided pass fastest with 2
+    // column pairs per item (32-byte TMA rows), the fused [V, N, V] pass with 1 pair and 2
+    // buffers (22.93 vs 23.02 ms per sweep with 1 buffer once the partner-lane tables made
+    // its transforms faster and the exposed TMA wait grew to 21 % of its samples)
     switch (colv()) {
       case 11: return launch_line<M, AX, NL, 1, 1>(g, t, P, in, out, nslices, st);
       case 12: return launch_line<M, AX, NL, 1, 2>(g, t, P, in, out, nslices, st);
@@ -654,7 +656,7 @@ static cudaError_t launch_col(const Geom& g, const DstTables& t, const Poly& P, 
       case 22: return launch_line<M, AX, NL, 2, 2>(g, t, P, in, out, nslices, st);
       case 41: return launch_line<M, AX, NL, 4, 1>(g, t, P, in, out, nslices, st);
       default:
-        if constexpr (NL) return launch_line<M, AX, NL, 1, 1>(g, t, P, in, out, nslices, st);
+        if constexpr (NL) return launch_line<M, AX, NL, 1, 2>(g, t, P, in, out, nslices, st);
         else return launch_line<M, AX, NL, 2, 2>(g, t, P, in, out, nslices, st);
     }
   } else if constexpr (M == 4096) {

@@ -50,6 +50,7 @@ EXPORTS = [
     "expd_set_profiling",
     "expd_sweep_stage_ms",
     "expd_debug_kernel_ms",
+    "expd_sweep_pass_ms",
     "expd_layout_query",
     "expd_a2a_schedule",
     "expd_a2a_schedule_keyed",
@@ -136,6 +137,8 @@ def load_library(path: str = LIB_PATH):
         "expd_set_profiling": (C.c_int, [vp, C.c_int]),
         "expd_sweep_stage_ms": (C.c_int, [vp, dp, dp]),
         "expd_debug_kernel_ms": (C.c_int, [vp, C.c_int, C.c_long, C.c_int, dp]),
+        "expd_sweep_pass_ms": (C.c_int, [vp, dp, dp, dp, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                         C.POINTER(C.c_int)]),
         "expd_layout_query": (C.c_int, [C.POINTER(_Problem), C.c_int, C.c_int, C.POINTER(_Layout)]),
         "expd_a2a_schedule": (C.c_long, [C.POINTER(_Problem), C.c_int, C.c_int, C.c_int, C.c_int,
                                          C.POINTER(C.c_long), C.POINTER(C.c_long), C.c_long]),
@@ -426,6 +429,14 @@ class Plan:
         a, b = C.c_double(), C.c_double()
         self._check(self.lib.expd_sweep_stage_ms(self.handle, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    def sweep_pass_ms(self) -> dict:
+        """Stage-3 pass times of the last sweep, from events inside the sweep (profiling on)."""
+        t = [C.c_double() for _ in range(3)]
+        n = [C.c_int() for _ in range(3)]
+        self._check(self.lib.expd_sweep_pass_ms(self.handle, *(C.byref(x) for x in t), *(C.byref(x) for x in n)))
+        return {"x_ms": t[0].value, "strided_ms": t[1].value, "fused_ms": t[2].value,
+                "x_launches": n[0].value, "strided_launches": n[1].value, "fused_launches": n[2].value}
 
     def debug_kernel_ms(self, which: int, nslices: int = 1, reps: int = 10) -> float:
         v = C.c_double()
