@@ -206,12 +206,13 @@ expd_status expd_dst(expd_plan* plan, const double* in, double* out, long nslice
    Uses the workspace's spectral temporary and transform scratch.  Async. */
 expd_status expd_nonlin_hat(expd_plan* plan, const double* uhat, double* nhat, long nslices);
 /* Stage timing of expd_sweep with CUDA events recorded on the plan's stream (inside the
-   sweep's CUDA graph): enable != 0 turns it on.  expd_sweep_stage_ms waits for the last
-   sweep and returns the device time of stage 3 (N-hat of all slices; 0 when linear) and of
-   the fused time-local kernel K1, in milliseconds. */
+   sweep's CUDA graph): enable = 1 turns it on, 2 also records an event between every
+   stage-3 pass (for expd_sweep_pass_ms; ~50 more graph nodes per sweep), 0 off.
+   expd_sweep_stage_ms waits for the last sweep and returns the device time of stage 3
+   (N-hat of all slices; 0 when linear) and of the fused time-local kernel K1, in ms. */
 expd_status expd_set_profiling(expd_plan* plan, int enable);
 expd_status expd_sweep_stage_ms(expd_plan* plan, double* ms_nonlin, double* ms_time);
-/* Stage-3 pass times of the last sweep (set_profiling on, single-GPU nonlinear plans with
+/* Stage-3 pass times of the last sweep (set_profiling level 2, single-GPU nonlinear plans with
    the TMA line kernels): device ms summed over the sweep's x-passes, plain strided passes
    (3-D) and fused strided [V, N(u), V] passes, measured by CUDA events recorded on the
    plan's stream between consecutive passes inside the sweep, and the launch counts.

@@ -65,6 +65,7 @@ struct expd_plan {
   bool eager_done = false;  // one eager sweep (kernel attributes) before the first capture
   // optional stage timing: ev[0] before stage 3, ev[1] before K1, ev[2] after K1
   bool prof = false;
+  int prof_level = 0;  // 1: stage events; 2: + an event between every stage-3 pass
   cudaEvent_t ev[3] = {nullptr, nullptr, nullptr};
   std::vector<cudaEvent_t> tev;  // per-pass events of stage 3 (profiling, single GPU)
   PassTimer timer{};
@@ -485,7 +486,7 @@ static cudaError_t enqueue_sweep(expd_plan* p, cudaStream_t st) {
   if (e != cudaSuccess) return e;
   if (p->nl) {
     PassTimer* tm = nullptr;
-    if (p->prof && !p->tev.empty()) {
+    if (p->prof_level >= 2 && !p->tev.empty()) {
       p->timer.ev = p->tev.data();
       p->timer.cap = (int)p->tev.size();
       p->timer.ext = p->capturing;
@@ -740,11 +741,13 @@ extern "C" expd_status expd_set_profiling(expd_plan* p, int enable) {
     p->tev.resize(cap < 512 ? cap : 512);
     for (auto& e : p->tev) CUDA_TRY(p, cudaEventCreate(&e));
   }
-  if (p->prof != (enable != 0) && p->sweep_exec) {
+  const int level = enable <= 0 ? 0 : (enable >= 2 ? 2 : 1);
+  if (p->prof_level != level && p->sweep_exec) {
     cudaGraphExecDestroy(p->sweep_exec);  // recapture with / without the event nodes
     p->sweep_exec = nullptr;
   }
-  p->prof = enable != 0;
+  p->prof = level != 0;
+  p->prof_level = level;
   return EXPD_OK;
 }
 
@@ -761,7 +764,7 @@ extern "C" expd_status expd_sweep_stage_ms(expd_plan* p, double* ms_nonlin, doub
 
 extern "C" expd_status expd_sweep_pass_ms(expd_plan* p, double* ms_x, double* ms_strided, double* ms_fused,
                                           int* n_x, int* n_strided, int* n_fused) {
-  if (!p || !p->prof) return fail(p, EXPD_ERR_INVALID_ARG, "profiling not enabled");
+  if (!p || p->prof_level < 2) return fail(p, EXPD_ERR_INVALID_ARG, "pass profiling (level 2) not enabled");
   if (p->tev.empty() || p->timer.used < 2)
     return fail(p, EXPD_ERR_UNSUPPORTED, "no stage-3 pass timing (linear, distributed or non-TMA plan)");
   double t[3] = {0.0, 0.0, 0.0};

@@ -311,12 +311,15 @@ __device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* 
 // ---------------------------------------------------------------------------------------
 template <int AX, int G>
 __device__ __forceinline__ void line_coords(const LineArgs& a, long item, int& c0, int& c1, int& c2, int& c3) {
-  const long s = item / a.per_slice;
-  const int w = (int)(item % a.per_slice);
+  // 32-bit unsigned arithmetic (item counts stay far below 2^32): a 64-bit division is a
+  // long software sequence on the issuing thread's critical path to the TMA
+  const unsigned it = (unsigned)item, ps = (unsigned)a.per_slice;
+  const unsigned s = it / ps;
+  const int w = (int)(it - s * ps);
   if constexpr (AX == AX_ROW) {
     c0 = 0; c1 = 0; c2 = 2 * w; c3 = (int)s;  // rows 2w, 2w+1 of slice s
   } else {
-    const int o = w / a.inner, cg = w % a.inner;
+    const int o = (int)((unsigned)w / (unsigned)a.inner), cg = w - o * a.inner;
     c0 = 2 * G * cg;
     if constexpr (AX == AX_COL_Y) { c1 = 0; c2 = o; }
     else { c1 = o; c2 = 0; }

@@ -421,7 +421,8 @@ class Plan:
         self._check(self.lib.expd_nonlin_hat(self.handle, _ptr(uhat), _ptr(out), ns))
         return out
 
-    def set_profiling(self, enable: bool = True):
+    def set_profiling(self, enable: bool | int = True):
+        """0 off, 1 (True) stage events, 2 stage events + an event between stage-3 passes."""
         self._check(self.lib.expd_set_profiling(self.handle, int(enable)))
 
     def sweep_stage_ms(self):
