@@ -338,3 +338,31 @@ def test_dist1_matches_single_gpu_schedule(comm1):
     U2, r2 = Plan(Problem.from_config(cfg), comm=comm1).fixed_point_solve(u0, tol=cfg.tol, maxit=50)
     assert r1["iterations"] == r2["iterations"]
     assert relmax(H(U2), H(U1)) < 1e-13
+
+
+def test_dist1_uneven_pipeline_chunks(tmp_path):
+    """The pipelined exchange with chunks that do not divide the time slab (EXPD_DIST_CHUNKS
+    = 3 over 8 slices: 3 + 3 + 2), in a fresh process (the setting is read once)."""
+    import subprocess
+    import sys
+
+    code = """
+import sys; sys.path.insert(0, '.')
+import numpy as np, torch, synth, oracle
+from paper_2603_04350_b200 import Comm, Plan, Problem
+cfg = synth.CONFIGS['c5'].scaled(63, 8)
+comm = Comm(0, 1, 0)
+plan = Plan(Problem.from_config(cfg), comm=comm)
+u0 = synth.initial_condition(cfg)
+U, rep = plan.fixed_point_solve(torch.from_numpy(u0).cuda(), tol=cfg.tol, maxit=50)
+Uo, st, its, _ = oracle.fixed_point(oracle.spec(cfg), u0, tol=cfg.tol, maxit=50)
+err = np.abs(U.cpu().numpy() - Uo).max() / np.abs(Uo).max()
+assert rep['converged'] and rep['iterations'] == its and err < 1e-9, (rep['iterations'], its, err)
+print('ok', its, err)
+"""
+    import os
+
+    env = dict(os.environ, EXPD_DIST_CHUNKS="3")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
