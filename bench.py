@@ -349,8 +349,13 @@ def run_ours(args):
         traffic = prof.get(f"{cfg.name}:k1", None)
     except Exception:
         pass
+    try:
+        k1_ncu = (json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json"))).get("counters") or {}).get(
+            f"{cfg.name}:k1")
+    except Exception:
+        k1_ncu = None
     k1_roof = {"bound": "hbm", "kernel": "k_time_tma (K1: residual + ||r||^2 + alpha-circulant preconditioner + "
-                                        "update, one HBM pass)",
+                                        "update, one HBM pass)", "ncu": k1_ncu,
                "achieved": k1_gbs, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
                "frac": k1_gbs / hbm_peak, "traffic": traffic,
                "algorithmic_bytes_per_launch": k1_bytes, "launch_ms": k1_ms, "launches_per_step": 1}
@@ -384,6 +389,7 @@ def run_ours(args):
                           "peak_source": "measured DFMA loop (profiles/r01_probe_fp64_hbm.txt)", "unit": "TFLOP/s",
                           "frac": tf / FP64_PEAK_TFLOPS, "traffic": tprof.get(f"{cfg.name}:{label}"),
                           "traffic_note": "ncu dram bytes of one 16-slice launch",
+                          "ncu": (tprof.get("counters") or {}).get(f"{cfg.name}:{label}"),
                           "algorithmic_flops_per_launch": flops * slices / max(nlaunch, 1),
                           "launch_ms": ms_sweep / max(nlaunch, 1), "launches_per_step": nlaunch,
                           "slices_per_step": slices, "ms_per_step": ms_sweep,
