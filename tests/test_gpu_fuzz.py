@@ -68,3 +68,41 @@ def test_fuzz_precond_and_residual(orc, seed):
         wr, wn2 = orc.residual(s, u0, U)
     assert relmax(Rg.cpu().numpy(), wr) < 1e-11, cfg
     assert abs(rn2 - wn2) <= 1e-11 * wn2, cfg
+
+
+@pytest.mark.parametrize("seed", range(200, 236))
+def test_fuzz_solvers(orc, seed):
+    """Linear random problems, all three solvers: identical iteration counts (unless a
+    residual of the history lies within a factor 1.5 of the tolerance, where round-off may
+    decide) and solutions within 1e-9."""
+    cfg = draw(seed)
+    cfg = synth.Config(cfg.name, cfg.dim, min(cfg.n, 63 if cfg.dim < 3 else 7), cfg.a, cfg.c, cfg.T,
+                       min(cfg.nt, 64), max(cfg.alpha, 1e-3), scheme=cfg.scheme, q=(), a_im=cfg.a_im,
+                       c_im=cfg.c_im, seed=seed)
+    s = orc.spec(cfg)
+    dt = torch.complex128 if cfg.is_complex else torch.float64
+    u0 = synth.random_slice(cfg, seed)
+    if cfg.is_complex:
+        u0 = u0 + 1j * synth.random_slice(cfg, seed + 1)
+    plan = Plan(Problem.from_config(cfg), krylov_vectors=21)
+    tol = 1e-11
+    pre = "cplx_" if cfg.is_complex else ""
+    runs = (("fixed_point", lambda: plan.fixed_point_solve(torch.from_numpy(np.asarray(u0)).to(DEV, dt), tol=tol,
+                                                            maxit=60),
+             lambda: getattr(orc, pre + "fixed_point")(s, u0, tol=tol, maxit=60)),
+            ("gmres", lambda: plan.gmres_solve(torch.from_numpy(np.asarray(u0)).to(DEV, dt), tol=tol, restart=20,
+                                               maxit=60),
+             lambda: getattr(orc, pre + "gmres")(s, u0, tol=tol, restart=20, maxit=60)),
+            ("bicgstab", lambda: plan.bicgstab_solve(torch.from_numpy(np.asarray(u0)).to(DEV, dt), tol=tol,
+                                                     maxit=60),
+             lambda: getattr(orc, pre + "bicgstab")(s, u0, tol=tol, maxit=60)))
+    for name, gpu, ref in runs:
+        U, rep = gpu()
+        Uo, st, its, hist = ref()
+        assert st == 0 and rep["converged"], (name, cfg)
+        borderline = np.any(np.abs(np.log(np.maximum(hist, 1e-300) / tol)) < np.log(1.5))
+        if borderline:
+            assert abs(rep["iterations"] - its) <= 1, (name, cfg)
+        else:
+            assert rep["iterations"] == its, (name, cfg, rep["hist"], list(hist))
+        assert relmax(U.cpu().numpy(), Uo) < 1e-9, (name, cfg)
