@@ -106,3 +106,26 @@ def test_fuzz_solvers(orc, seed):
         else:
             assert rep["iterations"] == its, (name, cfg, rep["hist"], list(hist))
         assert relmax(U.cpu().numpy(), Uo) < 1e-9, (name, cfg)
+
+
+@pytest.mark.parametrize("seed", range(300, 316))
+def test_fuzz_picard(orc, seed):
+    """Nonlinear random problems (ETD1 / ETD2 / IF-IMEX, N(u) = q1 u - u^3): the Picard sweep
+    takes the oracle's iterations (borderline rule as above) to the oracle's fixed point."""
+    rng = np.random.default_rng(seed)
+    dim = int(rng.integers(1, 3))
+    n = int(2 ** rng.integers(3, 8 if dim == 1 else 6) - 1)
+    nt = int(2 ** rng.integers(2, 6))
+    cfg = synth.Config(f"pic{seed}", dim, n, float(10 ** rng.uniform(-2, 0)), float(rng.uniform(0.2, 1.5)),
+                       float(10 ** rng.uniform(-1.5, -0.3)), nt, float(10 ** rng.uniform(-3, -1.5)),
+                       scheme=int(rng.choice([0, 1, 2])), q=(0.0, float(rng.uniform(-0.5, 0.5)), 0.0, -1.0), seed=seed)
+    s = orc.spec(cfg)
+    u0 = 0.5 * synth.random_slice(cfg, seed)
+    plan = Plan(Problem.from_config(cfg))
+    tol = 1e-11
+    U, rep = plan.fixed_point_solve(torch.from_numpy(u0).to(DEV), tol=tol, maxit=80)
+    Uo, st, its, hist = orc.fixed_point(s, u0, tol=tol, maxit=80)
+    assert st == 0 and rep["converged"], cfg
+    borderline = np.any(np.abs(np.log(np.maximum(hist, 1e-300) / tol)) < np.log(1.5))
+    assert abs(rep["iterations"] - its) <= (1 if borderline else 0), (cfg, rep["hist"], list(hist))
+    assert relmax(U.cpu().numpy(), Uo) < 1e-9, cfg
