@@ -49,6 +49,8 @@ def _nccl_include():
 
 
 NVCC_FLAGS += _nccl_include()
+# tuning aid: extra nvcc flags (e.g. -DEXPD_LINE_REGS=128); rebuild with build(force=True)
+NVCC_FLAGS += os.environ.get("EXPD_NVCC_EXTRA", "").split()
 
 
 def _sources():
