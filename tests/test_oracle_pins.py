@@ -823,3 +823,41 @@ def test_bicgstab_on_dense_system(orc):
     big = np.array(hist) > 1e-10
     assert np.allclose(h[big], np.array(hist)[big], rtol=1e-8)
     assert rel(U.reshape(-1), x) < 1e-10
+
+
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_etd_picard_history_exact(orc, scheme):
+    """The lagged Picard sweep of ETD1 / ETD2 (north_star's iteration, readings R5 / R6) with
+    N = -M u is Richardson on the linear system Q' U = f; per DST mode J
+    Q' = I - (E - c1 M) C_0 (ETD1) or I - (E - (c1 + c2) M) C_0 - c2 M C_0^2 (ETD2),
+    c1 = dt phi1(dt mu), c2 = dt phi2(dt mu), f = ((E - c1 M) u0-hat, [ETD2: c2 M u0-hat], 0, ...)
+    (N(u_{-1}) := N(u_0)).  The residual then follows r^k = (I - Q' Q_alpha^{-1})^k f exactly:
+    the oracle's whole relative history must match these dense nt x nt products (built here
+    from the closed forms; the asymptotic rate is the spectral radius, but the short window is
+    transient-dominated, so the history itself is the pin)."""
+    n, k, M, nt = 7, 2, 3.0, 8
+    s = spec(orc, 1, n, a=0.5, c=0.3, T=1.0, nt=nt, alpha=0.05, scheme=scheme, q=(0.0, -M))
+    u0 = synth.sine_table(n, k)[k - 1]
+    mu = np.sort(np.linalg.eigvalsh(Lh(s)))[::-1][k - 1]
+    z = s.dt * mu
+    E = np.exp(z)
+    c1 = s.dt * np.expm1(z) / z
+    c2 = s.dt * (np.expm1(z) - z) / z**2
+    C0 = np.diag(np.ones(nt - 1), -1)
+    f = np.zeros(nt)
+    f[0] = E - c1 * M
+    if scheme == 0:
+        Qp = np.eye(nt) - (E - c1 * M) * C0
+    else:
+        Qp = np.eye(nt) - (E - (c1 + c2) * M) * C0 - c2 * M * (C0 @ C0)
+        f[1] = c2 * M
+    Qa = np.eye(nt) - E * alpha_circulant(nt, s.alpha)
+    G = np.eye(nt) - Qp @ np.linalg.inv(Qa)
+    U, st, its, hist = orc.fixed_point(s, u0, tol=1e-13, maxit=80)
+    assert st == 0 and its >= 6
+    r = f.copy()
+    for kk in range(1, len(hist)):
+        r = G @ r
+        want = np.linalg.norm(r) / np.linalg.norm(f)
+        assert abs(hist[kk] - want) < 1e-8 * want + 1e-15, (kk, hist[kk], want)
+    assert rel(U, orc.sequential(s, u0)) < 1e-11
