@@ -56,7 +56,7 @@ def test_dst_matches_oracle(orc, dim, n):
         assert relmax(got[i], orc.dst(s, x[i])) < 1e-13
 
 
-@pytest.mark.parametrize("dim,n", [(2, 2047), (3, 255)])
+@pytest.mark.parametrize("dim,n", [(2, 2047), (3, 255), (2, 4095)])  # 4095: the largest line
 def test_dst_full_size_sampled(orc, dim, n):
     cfg = synth.Config("t", dim, n, 1.0, 1.0, 1.0, 4, 1e-2)
     plan = Plan(Problem.from_config(cfg))
@@ -366,3 +366,15 @@ print('ok', its, err)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+def test_max_line_length_picard_converges():
+    """n + 1 = 4096 (the largest line the kernels take) in 2D: the ETD2 Picard solve converges
+    and its solution satisfies the all-at-once system (residual at round-off relative to U)."""
+    cfg = synth.CONFIGS["c5"].scaled(4095, 4)
+    plan = Plan(Problem.from_config(cfg))
+    u0 = T(synth.initial_condition(cfg))
+    U, rep = plan.fixed_point_solve(u0, tol=1e-12, maxit=30)
+    assert rep["converged"]
+    _, rn2 = plan.residual(u0, U, norm=True)
+    assert rn2 ** 0.5 < 1e-12 * float(U.norm())
