@@ -273,8 +273,13 @@ static Layout layout(const expd_plan* p, int kv) {
   L.T1 = off; off += vec;
   L.UT = off; off += tsl;
   L.NT = off; off += (p->nl ? tsl : 0);
-  L.X2 = off; off += (p->cx ? vec : 0);
-  L.X3 = off; off += (p->cx ? vec : 0);
+  // complex planar staging (cx_phys_to_mode / cx_mode_to_phys): up to ns = nt (one GPU) or
+  // ntl (the time slab) slices, i.e. 2 ns npad doubles in X2 and 2 ns N <= 2 ns npad in X3 --
+  // NOT the mode-slab vector size, which is smaller on ranks with a short mode slab
+  const size_t cxs =
+      p->cx ? align_up(sizeof(double) * 2 * (size_t)(p->dist ? p->ntl : p->prob.nt) * (size_t)p->g.npad) : 0;
+  L.X2 = off; off += cxs;
+  L.X3 = off; off += cxs;
   L.u0h = off; off += sl;
   L.E = off; off += sl;
   L.C1 = off; off += sl;

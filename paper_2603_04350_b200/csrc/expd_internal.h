@@ -3,12 +3,44 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstddef>
 #include <cstdint>
 #include <string>
 #include <vector>
 
 namespace expd {
+
+// One-time setup of a kernel per DEVICE (the dynamic shared-memory opt-in is a property of
+// the device context, so a plan on a second GPU of the same process needs its own): a bitmask
+// of the devices already done plus the occupancy found there, one object per call site.
+// Concurrent first calls may both run the (idempotent) setup; the atomics keep it race free.
+struct DevOnce {
+  std::atomic<unsigned long long> done{0};
+  std::atomic<int> per_sm[64];
+};
+template <typename K>
+inline cudaError_t smem_optin(DevOnce& o, K k, size_t smem_bytes, int threads = 0, int* per_sm = nullptr) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  dev &= 63;
+  const unsigned long long bit = 1ull << dev;
+  if (!(o.done.load(std::memory_order_acquire) & bit)) {
+    e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_bytes);
+    if (e != cudaSuccess) return e;
+    int v = 1;
+    if (threads > 0) {
+      e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&v, k, threads, smem_bytes);
+      if (e != cudaSuccess) return e;
+      if (v < 1) v = 1;
+    }
+    o.per_sm[dev].store(v, std::memory_order_relaxed);
+    o.done.fetch_or(bit, std::memory_order_release);
+  }
+  if (per_sm) *per_sm = o.per_sm[dev].load(std::memory_order_relaxed);
+  return cudaSuccess;
+}
 
 // Spectral layout: every x-line of a spectral slice is padded
 // from n to n+1 doubles (n+1 = 2^m), so a spectral slice holds n^{dim-1} (n+1) doubles,

@@ -437,13 +437,8 @@ static size_t dst_smem() {
   return sizeof(double2) * (size_t)(DGeo<M, G>::SW * G + DGeo<M, G>::NWB * G + 1);
 }
 template <typename K>
-static cudaError_t smem_attr(K k, size_t bytes, bool& done) {
-  if (!done) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
-    if (e != cudaSuccess) return e;
-    done = true;
-  }
-  return cudaSuccess;
+static cudaError_t smem_attr(K k, size_t bytes, DevOnce& done) {
+  return smem_optin(done, k, bytes);
 }
 
 template <int M, int MODE>
@@ -452,7 +447,7 @@ static cudaError_t rows_launch(const RowsOp& o, const DstTables& t, const Poly& 
   int pairs = (o.rows + 1) / 2;
   dim3 grid((pairs + G - 1) / G, (unsigned)o.nslices);
   const size_t sm = dst_smem<M, G>();
-  static bool done = false;  // per instantiation
+  static DevOnce done;  // per instantiation and device
   cudaError_t e = smem_attr(k_rows<M, G, MODE>, sm, done);
   if (e != cudaSuccess) return e;
   k_rows<M, G, MODE><<<grid, DGeo<M, G>::THREADS, sm, st>>>(o.in, o.in_slice, o.in_rs, o.out, o.out_slice, o.out_rs,
@@ -470,7 +465,7 @@ static cudaError_t run_cols_g(const ColsOp& o, const DstTables& t, const Poly& P
   dim3 grid((unsigned)(o.nouter * ((M / 2) / G)), (unsigned)o.nslices);
   const size_t sm = dst_smem<M, G>();
   cudaError_t e;
-  static bool done_nl = false, done_pl = false;  // per instantiation
+  static DevOnce done_nl, done_pl;  // per instantiation and device
   if (o.nl) {
     if ((e = smem_attr(k_cols<M, G, true>, sm, done_nl)) != cudaSuccess) return e;
     k_cols<M, G, true><<<grid, DGeo<M, G>::THREADS, sm, st>>>(o.in, o.in_slice, o.out, o.out_slice, o.stride,

@@ -585,14 +585,10 @@ static cudaError_t axis_map(CUtensorMap* m, const Geom& g, int ax, const double*
 }
 
 static int sm_count() {
-  static int n = 0;
-  if (!n) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
+  int dev = 0, n = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  return n > 0 ? n : 148;
 }
 
 template <int M, int AX, bool NL, int G, int NBUF>
@@ -600,14 +596,9 @@ static cudaError_t launch_line(const Geom& g, const DstTables& t, const Poly& P,
                                long nslices, cudaStream_t st) {
   using D = LGeo<M, G, NBUF>;
   auto k = k_line<M, AX, NL, G, NBUF>;
-  static int per_sm = 0;  // per instantiation
-  if (!per_sm) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)D::SMEM);
-    if (e != cudaSuccess) return e;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k, D::THREADS, D::SMEM);
-    if (e != cudaSuccess) return e;
-    if (per_sm < 1) per_sm = 1;
-  }
+  static DevOnce once;  // per instantiation and device
+  int per_sm = 1;
+  if (cudaError_t e = smem_optin(once, k, D::SMEM, D::THREADS, &per_sm); e != cudaSuccess) return e;
   CUtensorMap mi, mo;
   cudaError_t e = axis_map(&mi, g, AX, in, nslices, G, /*sw=*/false);
   if (e != cudaSuccess) return e;

@@ -981,12 +981,8 @@ template <int NT, int RM, int OUTM, int NL, bool DB>
 static cudaError_t launch_pipe(const TimeArgs& a, int grid, cudaStream_t st) {
   auto kp = k_time_pipe<NT, RM, OUTM, NL, DB>;
   const size_t smp = PipeLayout<NT, RM, NL, DB>::BYTES;
-  static bool attr_p = false;
-  if (!attr_p) {
-    cudaError_t e = cudaFuncSetAttribute(kp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smp);
-    if (e != cudaSuccess) return e;
-    attr_p = true;
-  }
+  static DevOnce attr_p;  // per instantiation and device
+  if (cudaError_t e = smem_optin(attr_p, kp, smp); e != cudaSuccess) return e;
   kp<<<grid, TimeGeo<NT>::THREADS, smp, st>>>(a);
   return cudaGetLastError();
 }
@@ -995,12 +991,8 @@ template <int NT, int RM, int OUTM, int NL, int THR, int NST>
 static cudaError_t launch_tma(const TimeArgs& a, int grid, cudaStream_t st) {
   using PL = TmaLayout<NT, THR, NL, NST>;
   auto k = k_time_tma<NT, RM, OUTM, NL, THR, NST>;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PL::BYTES);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static DevOnce attr;  // per instantiation and device
+  if (cudaError_t e = smem_optin(attr, k, PL::BYTES); e != cudaSuccess) return e;
   constexpr int S = PL::S;
   CUtensorMap mx, mn;
   cudaError_t e = make_tmap_2d(&mx, a.X, (unsigned long long)a.npad, (unsigned long long)a.nt,
@@ -1034,12 +1026,8 @@ static cudaError_t launch_t(const TimeArgs& a, int grid, cudaStream_t st) {
   }
   auto k = k_time_fused<NT, RM, OUTM, NL>;
   size_t sm = time_smem_bytes<NT, OUTM>();
-  static bool attr_done = false;  // per-instantiation, host-side
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
+  static DevOnce attr_done;  // per instantiation and device
+  if (cudaError_t e = smem_optin(attr_done, k, sm); e != cudaSuccess) return e;
   k<<<grid, TimeGeo<NT>::THREADS, sm, st>>>(a);
   return cudaGetLastError();
 }

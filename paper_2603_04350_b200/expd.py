@@ -332,15 +332,30 @@ class Plan:
         return torch.empty((self.layout["nt_local"],) + self.problem.shape, dtype=self.problem.dtype,
                            device=f"cuda:{self.device}")
 
-    def _a(self, t):
-        """A state argument (u0, U, R, S): float64, or complex128 for a complex plan."""
-        return _ptr(t, self.problem.dtype)
+    def _a(self, t, slices: int | None = None):
+        """A state argument (u0, U, R, S): float64, or complex128 for a complex plan, on the
+        plan's device, holding `slices` spatial slices (default: this rank's time slab; 1 for
+        u0).  The C-ABI reads / writes exactly that many elements through the raw pointer, so
+        a wrong shape or device is rejected here instead of faulting on the device."""
+        if t is None:
+            return None
+        want = (self.layout["nt_local"] if slices is None else slices) * self.problem.N
+        return self._chk(t, self.problem.dtype, want)
+
+    def _chk(self, t, dtype, numel: int):
+        if not isinstance(t, torch.Tensor):
+            raise ValueError("expected a torch tensor")
+        if t.device.type != "cuda" or t.device.index != self.device:
+            raise ValueError(f"tensor on {t.device}, plan on cuda:{self.device}")
+        if t.numel() != numel:
+            raise ValueError(f"tensor holds {t.numel()} elements, expected {numel}")
+        return _ptr(t, dtype)
 
     # ---- primitives ------------------------------------------------------------------
     def residual(self, u0: torch.Tensor, U: torch.Tensor, R: torch.Tensor | None = None, norm: bool = False):
         R = self._vec() if R is None else R
         rn = C.c_double()
-        self._check(self.lib.expd_residual(self.handle, self._a(u0), self._a(U), self._a(R),
+        self._check(self.lib.expd_residual(self.handle, self._a(u0, 1), self._a(U), self._a(R),
                                            C.pointer(rn) if norm else None))
         return (R, rn.value) if norm else R
 
@@ -371,7 +386,7 @@ class Plan:
     def fixed_point_solve(self, u0, U=None, tol=1e-12, maxit=100):
         U = self._vec().zero_() if U is None else U
         r, hist = self._report(maxit)
-        st = self.lib.expd_fixed_point_solve(self.handle, self._a(u0), self._a(U), tol, maxit, C.byref(r))
+        st = self.lib.expd_fixed_point_solve(self.handle, self._a(u0, 1), self._a(U), tol, maxit, C.byref(r))
         if st not in (EXPD_OK, 7):
             self._check(st)
         return U, self._rdict(r, hist, st)
@@ -379,7 +394,7 @@ class Plan:
     def gmres_solve(self, u0, U=None, tol=1e-12, restart=20, maxit=100):
         U = self._vec().zero_() if U is None else U
         r, hist = self._report(maxit)
-        st = self.lib.expd_gmres_solve(self.handle, self._a(u0), self._a(U), tol, restart, maxit, C.byref(r))
+        st = self.lib.expd_gmres_solve(self.handle, self._a(u0, 1), self._a(U), tol, restart, maxit, C.byref(r))
         if st not in (EXPD_OK, 7):
             self._check(st)
         return U, self._rdict(r, hist, st)
@@ -387,14 +402,14 @@ class Plan:
     def bicgstab_solve(self, u0, U=None, tol=1e-12, maxit=100):
         U = self._vec().zero_() if U is None else U
         r, hist = self._report(maxit)
-        st = self.lib.expd_bicgstab_solve(self.handle, self._a(u0), self._a(U), tol, maxit, C.byref(r))
+        st = self.lib.expd_bicgstab_solve(self.handle, self._a(u0, 1), self._a(U), tol, maxit, C.byref(r))
         if st not in (EXPD_OK, 7):
             self._check(st)
         return U, self._rdict(r, hist, st)
 
     # ---- spectral-state sweep (benchmark / fine-grained driving) ----------------------
     def load_state(self, u0, U=None):
-        self._check(self.lib.expd_load_state(self.handle, self._a(u0), self._a(U)))
+        self._check(self.lib.expd_load_state(self.handle, self._a(u0, 1), self._a(U)))
 
     def sweep(self):
         self._check(self.lib.expd_sweep(self.handle))
@@ -411,14 +426,20 @@ class Plan:
         """V x for a stack of physical slices [..., n, ..., n]."""
         out = torch.empty_like(x) if out is None else out
         ns = x.numel() // self.problem.N
-        self._check(self.lib.expd_dst(self.handle, _ptr(x), _ptr(out), ns))
+        if ns * self.problem.N != x.numel():
+            raise ValueError("x must hold whole slices of n^dim points")
+        self._check(self.lib.expd_dst(self.handle, self._chk(x, torch.float64, x.numel()),
+                                      self._chk(out, torch.float64, x.numel()), ns))
         return out
 
     def nonlin_hat(self, uhat: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
         """V N(V uhat) for a stack of DST-coefficient slices [..., n, ..., n] (stage 3)."""
         out = torch.empty_like(uhat) if out is None else out
         ns = uhat.numel() // self.problem.N
-        self._check(self.lib.expd_nonlin_hat(self.handle, _ptr(uhat), _ptr(out), ns))
+        if ns * self.problem.N != uhat.numel():
+            raise ValueError("uhat must hold whole slices of n^dim points")
+        self._check(self.lib.expd_nonlin_hat(self.handle, self._chk(uhat, torch.float64, uhat.numel()),
+                                             self._chk(out, torch.float64, uhat.numel()), ns))
         return out
 
     def set_profiling(self, enable: bool | int = True):
