@@ -45,11 +45,13 @@ FP64_PEAK_TFLOPS = 34.19
 
 def dst_flops_per_line_pair(M: int) -> float:
     """Algorithmic fp64 flops of one DST-I transform of two real lines of length M-1
-    (DESIGN.md "K2/K3"): complex FFT of length M (5 M log2 M, the radix-2 count) + the
-    sinft pre-processing, Hermitian unpack, prefix sum and scaling (15 flops per point)."""
+    ("4 DST-I via half-length complex FFTs at ~25-30 flop/point/axis"): the
+    split-radix count of the complex FFT of length M, 4 M log2 M - 6 M, plus the sinft
+    pre-processing, Hermitian unpack and prefix sum, 12 flops per complex point:
+    (4 log2 M + 6) M, i.e. 25 flops per real point per axis at M = 2048."""
     import math
 
-    return 5.0 * M * math.log2(M) + 15.0 * M
+    return (4.0 * math.log2(M) + 6.0) * M
 
 
 BYTES_PER_DOF = {  # algorithmic fp64 bytes per space-time dof (DESIGN.md "Byte model")
@@ -62,8 +64,9 @@ BYTES_PER_DOF = {  # algorithmic fp64 bytes per space-time dof (DESIGN.md "Byte 
 
 def workload_label(cfg) -> str:
     if getattr(cfg, "is_complex", False):
+        scheme = "BDF2" if cfg.scheme == 3 else "exp. Euler"
         return (f"{cfg.name}: {cfg.dim}D n={cfg.n} Nt={cfg.nt} complex a={cfg.a}+{cfg.a_im}i c={cfg.c}+{cfg.c_im}i "
-                f"exp. Euler fixed-point sweep (Schroedinger, PAPER.md:983/1064; NEXT-4)")
+                f"{scheme} fixed-point sweep (Schroedinger, PAPER.md:983/1064; NEXT-4)")
     src = {"c1": ":7", "c2": ":8", "c3": ":9", "c4": ":10", "c5": ":11"}.get(cfg.name)
     return (f"{cfg.name}: {cfg.dim}D n={cfg.n} Nt={cfg.nt} "
             f"{ {0: 'exp. Euler' if not cfg.q else 'ETD1', 1: 'ETD2', 2: 'IF/IMEX', 3: 'BDF2'}[cfg.scheme] } "
@@ -92,7 +95,48 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--dist1", action="store_true",
                     help="N = 1: run the distributed schedule (1-rank NCCL communicator) instead")
+    ap.add_argument("--solver", default="sweep", choices=["sweep", "gmres"],
+                    help="sweep: one fixed-point / Picard sweep per step; gmres: one Arnoldi step of "
+                         "left-preconditioned GMRES per step (linear configs, e.g. c4; SURVEY §8(d.3))")
+    ap.add_argument("--launch-check", action="store_true",
+                    help="only check the multi-rank launch (gloo without a GPU): ranks, world size, one allreduce")
     return ap.parse_args()
+
+
+def free_port() -> int:
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(args) -> int:
+    """--gpus N > 1 without a torchrun environment: start N ranks of this script on this node
+    (one process per GPU, rendezvous on 127.0.0.1) and return their exit status."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()), os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def launch_check(args) -> int:
+    import torch
+    import torch.distributed as dist
+
+    ws, rank, local = dist_env()
+    backend = "nccl" if torch.cuda.is_available() else "gloo"
+    if ws > 1:
+        dist.init_process_group(backend, init_method="env://")
+    dev = torch.device(f"cuda:{local}") if backend == "nccl" else torch.device("cpu")
+    t = torch.ones(1, device=dev)
+    if ws > 1:
+        dist.all_reduce(t)
+    if rank == 0:
+        print(json.dumps({"launch_check": True, "n_gpus": ws, "backend": backend if ws > 1 else "none",
+                          "allreduce_sum": float(t.item()), "world_size_ok": ws == args.gpus}), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
 
 
 def dist_env():
@@ -164,16 +208,16 @@ class ClockSampler:
 # ------------------------------------------------------------------------------------------
 # CPU oracle baseline (oracle/ as it stands; rank 0, N = 1 only)
 # ------------------------------------------------------------------------------------------
-REF_ROWS = 256  # rows per CPU-baseline sample
+REF_ROWS = 2048  # rows per CPU-baseline sample (about one whole x-axis pass of a c5 slice)
 
 
 def oracle_sample_step(cfg, u_rows):
     """One bounded sample of the oracle's sweep: the x-axis DST-I (plain O(n) long-double
-    sums per output) of REF_ROWS rows of a c5 slice.  The oracle's sweep applies 10 DSTs per
-    time slice (residual: A and the two Phi products = 6; Step (b): DST and IDST of the real
-    and imaginary parts = 4), each dim axis passes over the slice's n^{dim-1} rows, plus
-    O(Nt) DFT sums per point (< 3 % of its work at c5): one sample is
-    REF_ROWS / (10 dim n^{dim-1} Nt) of a sweep, i.e. that fraction of N_st DOF-iterations."""
+    sums per output; the sine table is built once per n) of REF_ROWS rows of a slice.  The
+    oracle's sweep applies oracle_dsts_per_slice(cfg) DSTs per time slice, each dim axis passes
+    over the slice's n^{dim-1} rows, plus O(Nt) DFT sums per point (< 3 % of its work at c5):
+    one sample is REF_ROWS / (dsts dim n^{dim-1} Nt) of a sweep, i.e. that fraction of N_st
+    DOF-iterations."""
     import oracle
 
     oracle.dst_x_rows(oracle.spec(cfg), u_rows)
@@ -181,28 +225,68 @@ def oracle_sample_step(cfg, u_rows):
     return cfg.nst * u_rows.shape[0] / (oracle_dsts_per_slice(cfg) * cfg.dim * rows_per_slice * cfg.nt)
 
 
-def cpu_baseline(cfg, nsamples=4):
+def oracle_sweep(cfg):
+    """One WHOLE oracle sweep (orc_residual + orc_precond: stages 1 and 2 with the nonlinear
+    terms, exactly what an oracle Picard / fixed-point iteration computes per sweep) on a
+    seeded state; returns (DOF-iter/s, seconds)."""
+    import oracle
+    import synth
+
+    s = oracle.spec(cfg)
+    u0 = synth.initial_condition(cfg)
+    U = synth.random_spacetime(cfg, seed=1, scale=0.3)
+    t0 = time.perf_counter()
+    R, _ = oracle.residual(s, u0, U)
+    oracle.precond(s, R)
+    dt = time.perf_counter() - t0
+    return cfg.nst / dt, dt
+
+
+def host_cpu_model() -> str:
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_baseline(cfg, sweep_cfgs=("c2", "c3")):
+    """The oracle as it stands on this host's cores (rank 0, N = 1): whole oracle sweeps of
+    the configs the oracle finishes in seconds (c2, c3), plus the bounded sample of the
+    benchmarked config (a scaled addendum: a whole c5 oracle sweep takes minutes)."""
     import numpy as np
 
     import oracle
+    import synth
 
     oracle.build()
     cores = os.cpu_count() or 1
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    sweeps = {}
+    for name in sweep_cfgs:
+        rate, sec = oracle_sweep(synth.CONFIGS[name])
+        sweeps[name] = {"value": rate, "unit": "DOF-iter/s", "seconds": sec,
+                        "workload": workload_label(synth.CONFIGS[name])}
     u = np.random.default_rng(0).standard_normal((REF_ROWS, cfg.n))
-    oracle_sample_step(cfg, u)  # warm-up (library load, OpenMP pool)
+    oracle_sample_step(cfg, u)  # warm-up (library load, OpenMP pool, sine table)
     t0 = time.perf_counter()
-    dofs = 0.0
-    done = 0
-    while done < nsamples or time.perf_counter() - t0 < 10.0:  # >= 10 s of oracle work
+    dofs, done = 0.0, 0
+    while done < 3 or time.perf_counter() - t0 < 5.0:
         dofs += oracle_sample_step(cfg, u)
         done += 1
     dt = time.perf_counter() - t0
-    nsamples = done
-    return {"value": dofs / dt, "unit": "DOF-iter/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
-            "kind": "oracle",
-            "sample": f"{nsamples} x oracle x-axis DST-I of {REF_ROWS} rows of a {cfg.name} slice (plain long-double "
-                      f"sums) = {REF_ROWS}/(10 dim n^(dim-1) Nt) of an oracle sweep each; {dt:.1f} s"}
+    head = sweep_cfgs[-1]
+    return {"value": sweeps[head]["value"], "unit": "DOF-iter/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
+            "cpu_model": host_cpu_model(), "kind": "oracle",
+            "sample": f"one whole oracle sweep (orc_residual + orc_precond, long double, naive O(n) sine and O(Nt) "
+                      f"DFT sums) of {head} ({sweeps[head]['seconds']:.1f} s); c2 and the {cfg.name} sample below",
+            "sweeps": sweeps,
+            f"{cfg.name}_sample": {"value": dofs / dt, "unit": "DOF-iter/s", "seconds": dt,
+                                   "sample": f"{done} x oracle x-axis DST-I of {REF_ROWS} rows of a {cfg.name} slice = "
+                                             f"{REF_ROWS}/({oracle_dsts_per_slice(cfg):.0f} dim n^(dim-1) Nt) of an "
+                                             f"oracle sweep each (scaled by that work ratio)"}}
 
 
 def run_reference(args):
@@ -216,9 +300,11 @@ def run_reference(args):
 
     import oracle
 
-    oracle.build()
     cores = os.cpu_count() or 1
+    if ws > 1:  # torchrun pins OMP_NUM_THREADS=1 per rank; rank 0 alone runs the oracle here
+        os.environ["OMP_NUM_THREADS"] = str(cores)
     os.environ.setdefault("OMP_NUM_THREADS", str(cores))
+    oracle.build()
     u = np.random.default_rng(0).standard_normal((REF_ROWS, cfg.n))
     for _ in range(args.warmup):
         oracle_sample_step(cfg, u)
@@ -236,8 +322,10 @@ def run_reference(args):
         "config": {"workload": workload_label(cfg)},
         "cpu_baseline": {"value": value, "unit": "DOF-iter/s", "cores": int(os.environ["OMP_NUM_THREADS"]),
                          "kind": "oracle",
+                         "cpu_model": host_cpu_model(),
                          "sample": f"each step: oracle x-axis DST-I of {REF_ROWS} rows of a {cfg.name} slice = "
-                                   f"{REF_ROWS}/(10 dim n^(dim-1) Nt) of an oracle sweep"},
+                                   f"{REF_ROWS}/({oracle_dsts_per_slice(cfg):.0f} dim n^(dim-1) Nt) of an oracle "
+                                   f"sweep (scaled by that work ratio)"},
         "e2e": {"value": value, "unit": "DOF-iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -360,11 +448,28 @@ def run_ours(args):
                "frac": k1_gbs / hbm_peak, "traffic": traffic,
                "algorithmic_bytes_per_launch": k1_bytes, "launch_ms": k1_ms, "launches_per_step": 1}
     kernels = {"k1": k1_roof, "stage3_ms": s3_ms,
-               "stage3_gbs": (s3_bytes / (s3_ms * 1e-3) / 1e9) if s3_ms > 0 else None,
-               "sweep_ms": ms_step,
-               "sweep_algorithmic_gbs": (k1_bytes + s3_bytes) / (ms_step * 1e-3) / 1e9,
-               "sweep_frac_of_peak": (k1_bytes + s3_bytes) / (ms_step * 1e-3) / 1e9 / hbm_peak}
-    roofline = k1_roof
+               "stage3_gbs": (s3_bytes / (s3_ms * 1e-3) / 1e9) if s3_ms > 0 else None}
+    # north_star's quantity: "achieved fraction of the HBM roofline (bytes moved per iteration
+    # over peak bandwidth)" -- the whole sweep's algorithmic bytes (40 B/dof
+    # for a nonlinear sweep, 16 for a linear one) over the step's device time
+    sweep_bytes = k1_bytes + s3_bytes
+    sweep_gbs = sweep_bytes / (ms_step * 1e-3) / 1e9
+    sweep_traffic = None
+    try:
+        tp = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
+        sweep_traffic = tp.get(f"{cfg.name}:sweep")
+    except Exception:
+        pass
+    roofline = {"bound": "hbm", "scope": "whole sweep (north_star: bytes moved per iteration over peak bandwidth)",
+                "kernel": ("sweep = stage 3 (k_line passes: x-IDST, fused y [V, N(u), V], x-DST) + K1 (k_time_tma) + "
+                           "norm reduction" if nl else "sweep = K1 (k_time_tma) + norm reduction"),
+                "achieved": sweep_gbs, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
+                "frac": sweep_gbs / hbm_peak, "traffic": sweep_traffic,
+                "traffic_note": "ncu dram read+write bytes of one whole sweep (profiles/ncu_traffic.json)",
+                "algorithmic_bytes_per_step": sweep_bytes,
+                "bytes_per_dof": BYTES_PER_DOF["k1_complex" if cx else ("k1_nonlinear" if nl else "k1_linear")]
+                + (BYTES_PER_DOF["stage3"] if nl else 0),
+                "ms_per_step": ms_step}
     if passes:
         # stage-3 kernel families, timed live in full sweeps right after the timed region: CUDA
         # events recorded on the plan's stream between consecutive passes of stage 3 inside the
@@ -397,8 +502,9 @@ def run_ours(args):
         kernels.update(fam)
         # the dominant kernel of the step by device time
         cand = [(k1_ms, k1_roof)] + [(v["ms_per_step"], v) for v in fam.values()]
-        roofline = max(cand, key=lambda x: x[0])[1]
-        kernels["dominant"] = roofline["kernel"]
+        kernels["dominant"] = max(cand, key=lambda x: x[0])[1]["kernel"]
+    else:
+        kernels["dominant"] = k1_roof["kernel"]
 
     # e2e: full solve through the C-ABI with host buffers (H2D u0, solve, final IDST, D2H U)
     e2e = None
@@ -465,10 +571,119 @@ def run_ours(args):
     return 0
 
 
+def run_gmres(args):
+    """--solver gmres: a step is one Arnoldi step j of left-preconditioned GMRES:
+    the K1 operator pass w = Q_alpha^{-1} Q v_j (16 B/dof) and CGS2 -- multi-dot over j+1 basis
+    vectors, fused w -= V h + second multi-dot, fused w -= V h2 + ||w||^2 (8(3j+5) B/dof) --
+    SURVEY §8(d.3): 16 + 8(3j+5) B/dof.  K steps = one GMRES(K) cycle run with tol 0 from U = 0,
+    each step's device time taken by CUDA events on the plan's stream around its kernels
+    (expd_solver_step_ms); the whole solve (setup, K steps with their host Givens round trips,
+    x += V y, final IDST) is also timed end to end."""
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2603_04350_b200 import Comm, Plan, Problem
+    from paper_2603_04350_b200 import build as pbuild
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if rank == 0:
+        pbuild.build()
+    if ws > 1:
+        dist.barrier()
+    cfg = synth.CONFIGS[args.config]
+    if cfg.q:
+        raise SystemExit("--solver gmres: linear configs only (GMRES is for npoly == 0)")
+    prob = Problem.from_config(cfg)
+    stream = torch.cuda.Stream(device=dev)
+    torch.cuda.set_stream(stream)
+    comm = Comm(rank, ws, local) if ws > 1 else None
+    K = args.steps
+    plan = Plan(prob, device=local, stream=stream, comm=comm, krylov_vectors=K + 1)
+    lay = plan.layout
+    cx = cfg.is_complex
+    esz = 16 if cx else 8
+    u0 = torch.from_numpy(synth.initial_condition(cfg)).to(dev)
+    U = torch.zeros((lay["nt_local"],) + cfg.shape, dtype=prob.dtype, device=dev)
+    plan.set_profiling(True)
+    for _ in range(max(1, args.warmup // 3)):
+        U.zero_()
+        plan.gmres_solve(u0, U, tol=0.0, restart=K, maxit=K)
+    torch.cuda.synchronize(dev)
+    if ws > 1:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    U.zero_()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize(dev)
+    ev0.record(stream)
+    _, rep = plan.gmres_solve(u0, U, tol=0.0, restart=K, maxit=K)
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    ck = clocks.stop()
+    steps_ms = plan.solver_step_ms()
+    solve_ms = ev0.elapsed_time(ev1)
+    dev_ms = sum(steps_ms)
+    if ws > 1:
+        t = torch.tensor([dev_ms, solve_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dev_ms, solve_ms = (float(x) for x in t.tolist())
+    pk = peaks()
+    hbm_peak = pk["hbm_gbs"] if pk else 6650.0
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if pk else "fallback (B200_PROFILING.md)"
+    share = lay["mode_len"] / lay["npad"]
+    dof_bytes = esz * cfg.nst * share  # one space-time vector of this rank, in bytes
+    per_step = [(16 + 8 * (3 * j + 5)) / 8 * dof_bytes for j in range(1, len(steps_ms) + 1)]
+    gbs = sum(per_step) / (dev_ms * 1e-3) / 1e9
+    value = cfg.nst * len(steps_ms) / (dev_ms * 1e-3)
+    roofline = {"bound": "hbm", "scope": "GMRES Arnoldi steps j = 1..K (SURVEY §8(d.3): 16 + 8(3j+5) B/dof)",
+                "kernel": "k_time_tma (RM_QOP: w = Q_alpha^{-1} Q v_j) + k_multi_dot + 2 x k_axpy_dot (CGS2, ||w||^2)",
+                "achieved": gbs, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s", "frac": gbs / hbm_peak,
+                "traffic": None, "algorithmic_bytes_per_step": per_step,
+                "step_ms": steps_ms}
+    line = {
+        "metric": "space-time DOF-iterations/s per Exp-ParaDiag GMRES (Arnoldi) step", "value": value,
+        "unit": "DOF-iter/s", "n_gpus": ws, "steps": len(steps_ms), "warmup": args.warmup,
+        "ms_per_step": dev_ms / max(len(steps_ms), 1), "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "c128" if cx else "f64", "data": "synthetic",
+        "config": {"workload": f"{cfg.name}: {cfg.dim}D n={cfg.n} Nt={cfg.nt} GMRES({K}) Arnoldi steps, tol 0 "
+                               f"(BASELINE.json{ {'c2': ':8', 'c4': ':10'}.get(cfg.name, '') })",
+                   "n_st": cfg.nst, "alpha": cfg.alpha,
+                   "l2": f"basis vectors {cfg.nst * esz / 1e9:.2f} GB each vs 126 MB L2"},
+        "roofline": roofline,
+        "e2e_solve_ms": solve_ms, "e2e_note": "the whole GMRES(K) solve on resident data incl. setup DSTs, the "
+                                             "host Givens round trip per step, x += V y and the final IDST",
+        "clocks": ck, "hist": rep["hist"], "iterations": rep["iterations"],
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    plan.close()
+    if comm is not None:
+        comm.close()
+    if ws > 1:
+        dist.destroy_process_group()
+    return 0
+
+
 def main():
     args = parse()
+    env_ws = os.environ.get("WORLD_SIZE")
+    if args.gpus > 1 and env_ws is None:
+        return self_launch(args)
+    if int(env_ws or 1) != args.gpus:
+        print(f"bench.py: WORLD_SIZE={env_ws} but --gpus {args.gpus}", file=sys.stderr)
+        return 2
+    if args.launch_check:
+        return launch_check(args)
     if args.impl == "reference":
         return run_reference(args)
+    if args.solver == "gmres":
+        return run_gmres(args)
     return run_ours(args)
 
 

@@ -227,6 +227,12 @@ expd_status expd_sweep_pass_ms(expd_plan* plan, double* ms_x, double* ms_strided
    the TMA line kernels (x-axis, strided axis, fused strided [V, N, V]).  The
    workspace contents are overwritten with transformed data. */
 expd_status expd_debug_kernel_ms(expd_plan* plan, int which, long nslices, int reps, double* ms);
+/* Device time (ms) of every Arnoldi step of the last expd_gmres_solve run with profiling on
+   (expd_set_profiling >= 1): CUDA events on the plan's stream before the step's K1 operator
+   pass and after its CGS2 / norm kernels (and allreduces), i.e. w = Q_alpha^{-1} Q v_j and the
+   orthogonalisation of PAPER.md:284-289, without the host's Givens update.  Writes up to cap
+   values to ms (caller-owned host buffer) and the number of steps to *count. */
+expd_status expd_solver_step_ms(const expd_plan* plan, double* ms, int cap, int* count);
 /* Number of kernels one expd_sweep launches (for the benchmark's launch count). */
 int expd_sweep_kernel_launches(const expd_plan* plan);
 

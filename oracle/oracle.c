@@ -172,9 +172,18 @@ void orc_dst(const orc_problem* p, const double* in, double* out) {
 }
 
 /* The x-axis factor of V on nrows rows of n points (plain O(n) sums per output, the first
-   axis pass of orc_dst): the bounded CPU-baseline sample of bench.py. */
+   axis pass of orc_dst): the bounded CPU-baseline sample of bench.py.  The sine table is
+   built once per n and kept (a whole sweep builds it once too; rebuilding its n^2 sinl
+   values on every call made the sample mostly table construction).  Not thread safe:
+   callers are sequential. */
 void orc_dst_x_rows(const orc_problem* p, const double* in, long nrows, double* out) {
-  ld* S = sine_table(p->n);
+  static ld* S = NULL;
+  static int Sn = -1;
+  if (Sn != p->n) {
+    free(S);
+    S = sine_table(p->n);
+    Sn = p->n;
+  }
   long n = p->n;
 #pragma omp parallel for schedule(static)
   for (long r = 0; r < nrows; ++r) {
@@ -185,7 +194,6 @@ void orc_dst_x_rows(const orc_problem* p, const double* in, long nrows, double* 
       out[r * n + j] = (double)acc;
     }
   }
-  free(S);
 }
 
 /* One entry of V in: sum over all grid points of prod_axes S[j_ax][i_ax] in[i]. */

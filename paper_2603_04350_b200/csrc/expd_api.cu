@@ -73,6 +73,10 @@ struct expd_plan {
   // slab, overlapped with stage 3 of the neighbouring chunks (events in pev)
   cudaStream_t comm_stream = nullptr;
   std::vector<cudaEvent_t> pev;
+  // Krylov step timing (profiling on): device ms of every Arnoldi / BiCGStab step of the last
+  // solve, from two events on the plan's stream around the step's kernels
+  cudaEvent_t kev[2] = {nullptr, nullptr};
+  std::vector<double> kstep_ms;
   std::string err;
 };
 
@@ -351,6 +355,8 @@ extern "C" void expd_plan_destroy(expd_plan* p) {
   for (int i = 0; i < 3; ++i)
     if (p->ev[i]) cudaEventDestroy(p->ev[i]);
   for (cudaEvent_t e : p->tev) cudaEventDestroy(e);
+  for (cudaEvent_t e : p->kev)
+    if (e) cudaEventDestroy(e);
   cudaFree(p->d_lam);
   cudaFree(p->d_twt);
   cudaFree(p->d_g);
@@ -740,6 +746,8 @@ extern "C" expd_status expd_set_profiling(expd_plan* p, int enable) {
   if (s) return s;
   for (int i = 0; i < 3; ++i)
     if (!p->ev[i]) CUDA_TRY(p, cudaEventCreate(&p->ev[i]));
+  for (int i = 0; i < 2; ++i)
+    if (!p->kev[i]) CUDA_TRY(p, cudaEventCreate(&p->kev[i]));
   if (p->tev.empty() && p->nl && !p->dist) {  // one event per stage-3 pass + the end
     const long ns = p->prob.nt - 1 + p->nshift, ch = nonlin_chunk_slices(p->g);
     const long cap = ((ns + ch - 1) / ch) * 5 + 2;
@@ -790,6 +798,14 @@ extern "C" expd_status expd_sweep_pass_ms(expd_plan* p, double* ms_x, double* ms
   if (n_x) *n_x = n[0];
   if (n_strided) *n_strided = n[1];
   if (n_fused) *n_fused = n[2];
+  return EXPD_OK;
+}
+
+extern "C" expd_status expd_solver_step_ms(const expd_plan* p, double* ms, int cap, int* count) {
+  if (!p || !count || cap < 0 || (cap > 0 && !ms)) return EXPD_ERR_INVALID_ARG;
+  const int n = (int)p->kstep_ms.size();
+  for (int i = 0; i < n && i < cap; ++i) ms[i] = p->kstep_ms[i];
+  *count = n;
   return EXPD_OK;
 }
 
@@ -949,6 +965,7 @@ static expd_status gmres_impl(expd_plan* p, const double* u0, double* U, double 
   if (s) return s;
   CUDA_TRY(p, cudaStreamSynchronize(p->stream));
   std::vector<double> hist{1.0};
+  p->kstep_ms.clear();
   std::vector<T> H((size_t)(m + 1) * m), sn(m), gv(m + 1), y(m);
   std::vector<double> cs(m);
   std::vector<const double*> Vp(m + 1);
@@ -979,6 +996,7 @@ static expd_status gmres_impl(expd_plan* p, const double* u0, double* U, double 
     int j = 0, done = 0;
     for (j = 0; j < m && its < maxit; ++j) {
       for (int i = 0; i <= j; ++i) Vp[i] = Vk(i);
+      if (p->prof) CUDA_TRY(p, cudaEventRecord(p->kev[0], p->stream));
       TimeArgs q = time_args(p, Vk(j), p->T1, false);
       CUDA_TRY(p, launch_time_fused(q, RM_QOP, OUT_S, p->k1, p->time_grid, p->stream));  // w = P Q v_j
       // CGS2: h = V^H w ; w -= V h ; h2 = V^H w ; w -= V h2 ; ||w||^2
@@ -991,8 +1009,14 @@ static expd_status gmres_impl(expd_plan* p, const double* u0, double* U, double 
       CUDA_TRY(p, multi_axpy_dot(Vp.data(), j + 1, dcoef + O2, p->T1, len, p->partial, p->vgrid, dcoef + O3, 2,
                                  p->stream, CX));
       if ((s = allreduce(p, dcoef + O3, 1))) return s;
+      if (p->prof) CUDA_TRY(p, cudaEventRecord(p->kev[1], p->stream));
       CUDA_TRY(p, cudaMemcpyAsync(p->h_pin, dcoef, sizeof(double) * (O3 + 1), cudaMemcpyDeviceToHost, p->stream));
       CUDA_TRY(p, cudaStreamSynchronize(p->stream));
+      if (p->prof) {
+        float km = 0.f;
+        CUDA_TRY(p, cudaEventElapsedTime(&km, p->kev[0], p->kev[1]));
+        p->kstep_ms.push_back(km);
+      }
       for (int i = 0; i <= j; ++i) H[(size_t)i * m + j] = SC::get(p->h_pin + K * i) + SC::get(p->h_pin + O2 + K * i);
       double hn = std::sqrt(p->h_pin[O3]);
       for (int i = 0; i < j; ++i) {

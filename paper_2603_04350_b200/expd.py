@@ -51,6 +51,7 @@ EXPORTS = [
     "expd_sweep_stage_ms",
     "expd_debug_kernel_ms",
     "expd_sweep_pass_ms",
+    "expd_solver_step_ms",
     "expd_layout_query",
     "expd_a2a_schedule",
     "expd_a2a_schedule_keyed",
@@ -139,6 +140,7 @@ def load_library(path: str = LIB_PATH):
         "expd_debug_kernel_ms": (C.c_int, [vp, C.c_int, C.c_long, C.c_int, dp]),
         "expd_sweep_pass_ms": (C.c_int, [vp, dp, dp, dp, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                          C.POINTER(C.c_int)]),
+        "expd_solver_step_ms": (C.c_int, [vp, dp, C.c_int, C.POINTER(C.c_int)]),
         "expd_layout_query": (C.c_int, [C.POINTER(_Problem), C.c_int, C.c_int, C.POINTER(_Layout)]),
         "expd_a2a_schedule": (C.c_long, [C.POINTER(_Problem), C.c_int, C.c_int, C.c_int, C.c_int,
                                          C.POINTER(C.c_long), C.POINTER(C.c_long), C.c_long]),
@@ -459,6 +461,14 @@ class Plan:
         self._check(self.lib.expd_sweep_pass_ms(self.handle, *(C.byref(x) for x in t), *(C.byref(x) for x in n)))
         return {"x_ms": t[0].value, "strided_ms": t[1].value, "fused_ms": t[2].value,
                 "x_launches": n[0].value, "strided_launches": n[1].value, "fused_launches": n[2].value}
+
+    def solver_step_ms(self) -> list:
+        """Device ms of every Arnoldi step of the last GMRES solve (profiling on)."""
+        n = C.c_int()
+        self._check(self.lib.expd_solver_step_ms(self.handle, None, 0, C.byref(n)))
+        buf = (C.c_double * max(n.value, 1))()
+        self._check(self.lib.expd_solver_step_ms(self.handle, buf, n.value, C.byref(n)))
+        return [buf[i] for i in range(n.value)]
 
     def debug_kernel_ms(self, which: int, nslices: int = 1, reps: int = 10) -> float:
         v = C.c_double()

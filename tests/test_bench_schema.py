@@ -46,3 +46,29 @@ def test_reference_line():
     d = line("bench_reference_final.json")
     assert d["impl"] == "reference" and d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
+
+
+def _run_bench(*argv, env=None):
+    import subprocess
+    import sys
+
+    e = dict(os.environ)
+    e.pop("WORLD_SIZE", None)
+    e.update(env or {})
+    p = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), *argv], capture_output=True, text=True,
+                       timeout=300, env=e, cwd=ROOT)
+    return p
+
+
+def test_bench_self_launches_n_ranks():
+    """bench.py --gpus 2 without a torchrun environment starts 2 ranks itself (gloo here, NCCL
+    on a GPU box): every rank joins one process group and rank 0 reports n_gpus = 2."""
+    p = _run_bench("--gpus", "2", "--launch-check")
+    assert p.returncode == 0, p.stderr
+    d = json.loads([l for l in p.stdout.splitlines() if l.startswith("{")][-1])
+    assert d["n_gpus"] == 2 and d["world_size_ok"] and d["allreduce_sum"] == 2.0
+
+
+def test_bench_rejects_world_size_mismatch():
+    p = _run_bench("--gpus", "1", "--launch-check", env={"WORLD_SIZE": "2", "RANK": "0", "LOCAL_RANK": "0"})
+    assert p.returncode != 0 and "WORLD_SIZE" in p.stderr

@@ -55,8 +55,7 @@ def test_fuzz_precond_and_residual(orc, seed):
     R = synth.random_spacetime(cfg)
     S = plan.precond_apply(torch.from_numpy(R).to(DEV, dt)).cpu().numpy()
     want = orc.cplx_precond(s, R) if cfg.is_complex else orc.precond(s, R)[0]
-    kappa = cfg.alpha ** (-(cfg.nt - 1) / cfg.nt)  # cond(Gamma_alpha): the apply's round-off scale
-    assert relmax(S, want) < 1e-11 * max(1.0, kappa / 1e3), cfg
+    assert relmax(S, want) < 1e-11, cfg  # north_star's tolerance, for every draw
     u0 = synth.random_slice(cfg, seed + 1000)
     if cfg.is_complex:
         u0 = u0 + 1j * synth.random_slice(cfg, seed + 2000)
@@ -73,8 +72,8 @@ def test_fuzz_precond_and_residual(orc, seed):
 @pytest.mark.parametrize("seed", range(200, 236))
 def test_fuzz_solvers(orc, seed):
     """Linear random problems, all three solvers: identical iteration counts (unless a
-    residual of the history lies within a factor 1.5 of the tolerance, where round-off may
-    decide) and solutions within 1e-9."""
+    residual of the history lies within 12 % of the tolerance, where round-off may decide) and
+    solutions within 1e-9."""
     cfg = draw(seed)
     cfg = synth.Config(cfg.name, cfg.dim, min(cfg.n, 63 if cfg.dim < 3 else 7), cfg.a, cfg.c, cfg.T,
                        min(cfg.nt, 64), max(cfg.alpha, 1e-3), scheme=cfg.scheme, q=(), a_im=cfg.a_im,
@@ -100,7 +99,7 @@ def test_fuzz_solvers(orc, seed):
         U, rep = gpu()
         Uo, st, its, hist = ref()
         assert st == 0 and rep["converged"], (name, cfg)
-        borderline = np.any(np.abs(np.log(np.maximum(hist, 1e-300) / tol)) < np.log(1.5))
+        borderline = np.any(np.abs(np.log(np.maximum(hist, 1e-300) / tol)) < np.log(1.12))
         if borderline:
             assert abs(rep["iterations"] - its) <= 1, (name, cfg)
         else:
@@ -126,6 +125,6 @@ def test_fuzz_picard(orc, seed):
     U, rep = plan.fixed_point_solve(torch.from_numpy(u0).to(DEV), tol=tol, maxit=80)
     Uo, st, its, hist = orc.fixed_point(s, u0, tol=tol, maxit=80)
     assert st == 0 and rep["converged"], cfg
-    borderline = np.any(np.abs(np.log(np.maximum(hist, 1e-300) / tol)) < np.log(1.5))
+    borderline = np.any(np.abs(np.log(np.maximum(hist, 1e-300) / tol)) < np.log(1.12))
     assert abs(rep["iterations"] - its) <= (1 if borderline else 0), (cfg, rep["hist"], list(hist))
     assert relmax(U.cpu().numpy(), Uo) < 1e-9, cfg

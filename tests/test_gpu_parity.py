@@ -366,15 +366,3 @@ print('ok', its, err)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
-
-
-def test_max_line_length_picard_converges():
-    """n + 1 = 4096 (the largest line the kernels take) in 2D: the ETD2 Picard solve converges
-    and its solution satisfies the all-at-once system (residual at round-off relative to U)."""
-    cfg = synth.CONFIGS["c5"].scaled(4095, 4)
-    plan = Plan(Problem.from_config(cfg))
-    u0 = T(synth.initial_condition(cfg))
-    U, rep = plan.fixed_point_solve(u0, tol=1e-12, maxit=30)
-    assert rep["converged"]
-    _, rn2 = plan.residual(u0, U, norm=True)
-    assert rn2 ** 0.5 < 1e-12 * float(U.norm())
