@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <chrono>
+#include <cstddef>
 #include <cmath>
 #include <complex>
 #include <cstdio>
@@ -41,6 +42,7 @@ struct expd_plan {
   double* d_ginv = nullptr;  // [nt]
   double2* d_twM = nullptr;  // [M]   e^{-2 pi i q/M}
   double* d_sinp = nullptr;  // [M]   sin(pi i/M)
+  double* d_pa = nullptr;    // [M]   c (sin(pi i/M) + 1/2), c = sqrt(2/M)/2
   double* h_pin = nullptr;   // pinned host scalars [256]
   // workspace (caller-owned)
   char* ws = nullptr;
@@ -61,6 +63,11 @@ struct expd_plan {
   // CUDA graph of one sweep (captured on a private stream, launched on `stream`)
   cudaStream_t cap_stream = nullptr;
   cudaGraphExec_t sweep_exec = nullptr;
+  // the fixed-point solve's device-side loop: WHILE (not converged) { sweep; reduce; test }
+  cudaGraphExec_t loop_exec = nullptr;
+  FpLoopState* loopst = nullptr;  // device state in the workspace
+  FpLoopState* h_loopst = nullptr;  // pinned host copy
+  bool loop_failed = false;         // the graph could not be built: host-driven loop
   bool capturing = false;
   bool eager_done = false;  // one eager sweep (kernel attributes) before the first capture
   // optional stage timing: ev[0] before stage 3, ev[1] before K1, ev[2] after K1
@@ -107,6 +114,7 @@ static expd_status build_tables(expd_plan* p) {
   const int n = P.n, M = n + 1, nt = P.nt;
   std::vector<double> lam(n), g(nt), gi(nt), sinp(M);
   std::vector<double2> twt(nt), twM(M);
+  std::vector<double> pa(M);
   const long double h = 1.0L / (long double)M;
   for (int j = 1; j <= n; ++j) {
     long double s = sinl(PI_L * (long double)j / (2.0L * (long double)M));
@@ -123,6 +131,11 @@ static expd_status build_tables(expd_plan* p) {
     long double ang = 2.0L * PI_L * (long double)q / (long double)M;
     twM[q] = make_double2((double)cosl(ang), (double)(-sinl(ang)));
     sinp[q] = (double)sinl(PI_L * (long double)q / (long double)M);
+    // the line kernels' pre-processing y_i = s_i (x_i + x_{M-i}) + (x_i - x_{M-i})/2 written as
+    // y_i = a_i x_i + b_i x_{M-i}, a = c (s + 1/2), b = a - c, with the orthonormal scale
+    // sqrt(2/M) and the 1/2 of the Hermitian unpack folded in as c (the transform is linear)
+    const long double cq = 0.5L * sqrtl(2.0L / (long double)M), sq = sinl(PI_L * (long double)q / (long double)M);
+    pa[q] = (double)(cq * (sq + 0.5L));
   }
   p->a1 = (double)powl((long double)P.alpha, 1.0L / (long double)nt);
   CUDA_TRY(p, cudaSetDevice(p->device));
@@ -132,6 +145,7 @@ static expd_status build_tables(expd_plan* p) {
   CUDA_TRY(p, cudaMalloc(&p->d_ginv, sizeof(double) * nt));
   CUDA_TRY(p, cudaMalloc(&p->d_twM, sizeof(double2) * M));
   CUDA_TRY(p, cudaMalloc(&p->d_sinp, sizeof(double) * M));
+  CUDA_TRY(p, cudaMalloc(&p->d_pa, sizeof(double) * M));
   CUDA_TRY(p, cudaMallocHost(&p->h_pin, sizeof(double) * 512));
   CUDA_TRY(p, cudaMemcpy(p->d_lam, lam.data(), sizeof(double) * n, cudaMemcpyHostToDevice));
   CUDA_TRY(p, cudaMemcpy(p->d_twt, twt.data(), sizeof(double2) * nt, cudaMemcpyHostToDevice));
@@ -139,6 +153,7 @@ static expd_status build_tables(expd_plan* p) {
   CUDA_TRY(p, cudaMemcpy(p->d_ginv, gi.data(), sizeof(double) * nt, cudaMemcpyHostToDevice));
   CUDA_TRY(p, cudaMemcpy(p->d_twM, twM.data(), sizeof(double2) * M, cudaMemcpyHostToDevice));
   CUDA_TRY(p, cudaMemcpy(p->d_sinp, sinp.data(), sizeof(double) * M, cudaMemcpyHostToDevice));
+  CUDA_TRY(p, cudaMemcpy(p->d_pa, pa.data(), sizeof(double) * M, cudaMemcpyHostToDevice));
   return EXPD_OK;
 }
 
@@ -258,7 +273,7 @@ extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dis
 
 // workspace layout (every block 256-byte aligned)
 struct Layout {
-  size_t Uh, Nh, T1, UT, NT, X2, X3, u0h, E, C1, C2, scratch, partial, dscal, krylov, total, vec;
+  size_t Uh, Nh, T1, UT, NT, X2, X3, u0h, E, C1, C2, scratch, partial, dscal, loopst, krylov, total, vec;
 };
 static Layout layout(const expd_plan* p, int kv) {
   Layout L{};
@@ -291,6 +306,7 @@ static Layout layout(const expd_plan* p, int kv) {
   L.scratch = off; off += align_up(sizeof(double) * dst_scratch_doubles(p->g, nonlin_chunk_slices(p->g)));
   L.partial = off; off += align_up(sizeof(double) * 32 * (size_t)(p->sms * 8 + 64));
   L.dscal = off; off += align_up(sizeof(double) * 512);
+  L.loopst = off; off += align_up(sizeof(FpLoopState));
   L.krylov = off; off += (size_t)kv * vec;
   L.total = off;
   return L;
@@ -327,11 +343,16 @@ extern "C" expd_status expd_plan_set_workspace(expd_plan* p, void* d_ptr, size_t
   p->scratch = at(L.scratch);
   p->partial = at(L.partial);
   p->dscal = at(L.dscal);
+  p->loopst = reinterpret_cast<FpLoopState*>(p->ws + L.loopst);
   p->krylov = kv ? at(L.krylov) : nullptr;
   p->krylov_cap = kv;
   if (p->sweep_exec) {
     cudaGraphExecDestroy(p->sweep_exec);
     p->sweep_exec = nullptr;
+  }
+  if (p->loop_exec) {  // both graphs hold workspace pointers
+    cudaGraphExecDestroy(p->loop_exec);
+    p->loop_exec = nullptr;
   }
   CUDA_TRY(p, cudaSetDevice(p->device));
   if (p->cx)
@@ -349,6 +370,8 @@ extern "C" void expd_plan_destroy(expd_plan* p) {
   if (!p) return;
   cudaSetDevice(p->device);
   if (p->sweep_exec) cudaGraphExecDestroy(p->sweep_exec);
+  if (p->loop_exec) cudaGraphExecDestroy(p->loop_exec);
+  if (p->h_loopst) cudaFreeHost(p->h_loopst);
   if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
   if (p->comm_stream) cudaStreamDestroy(p->comm_stream);
   for (cudaEvent_t e : p->pev) cudaEventDestroy(e);
@@ -363,6 +386,7 @@ extern "C" void expd_plan_destroy(expd_plan* p) {
   cudaFree(p->d_ginv);
   cudaFree(p->d_twM);
   cudaFree(p->d_sinp);
+  cudaFree(p->d_pa);
   if (p->h_pin) cudaFreeHost(p->h_pin);
   delete p;
 }
@@ -372,7 +396,7 @@ extern "C" const char* expd_plan_last_error(const expd_plan* p) { return p ? p->
 // ---------------------------------------------------------------------------------------
 // internal helpers
 // ---------------------------------------------------------------------------------------
-static DstTables dst_tables(const expd_plan* p) { return DstTables{p->d_twM, p->d_sinp}; }
+static DstTables dst_tables(const expd_plan* p) { return DstTables{p->d_twM, p->d_sinp, p->d_pa}; }
 
 static TimeArgs time_args(const expd_plan* p, const double* X, double* Y, bool with_partial) {
   TimeArgs a{};
@@ -759,6 +783,10 @@ extern "C" expd_status expd_set_profiling(expd_plan* p, int enable) {
     cudaGraphExecDestroy(p->sweep_exec);  // recapture with / without the event nodes
     p->sweep_exec = nullptr;
   }
+  if (p->prof_level != level && p->loop_exec) {
+    cudaGraphExecDestroy(p->loop_exec);
+    p->loop_exec = nullptr;
+  }
   p->prof = level != 0;
   p->prof_level = level;
   return EXPD_OK;
@@ -862,6 +890,85 @@ static void fill_report(expd_report* r, int its, int sweeps, int conv, const std
     for (size_t i = 0; i < hist.size(); ++i) r->hist[i] = hist[i];
 }
 
+// The device-side fixed-point loop (single-GPU plans): one CUDA graph holding a WHILE
+// conditional node whose body is the captured sweep (stage 3, K1, the norm reduction) and
+// k_fp_conv, which records rho_k and sets the loop condition -- the iteration runs without a
+// host round trip per sweep; the host reads the loop state once at the end.
+static bool device_loop_enabled() {
+  const char* s = getenv("EXPD_DEVICE_LOOP");
+  return !(s && s[0] == '0');
+}
+
+static expd_status build_loop_graph(expd_plan* p) {
+  if (!p->cap_stream) CUDA_TRY(p, cudaStreamCreateWithFlags(&p->cap_stream, cudaStreamNonBlocking));
+  cudaGraph_t g = nullptr;
+  CUDA_TRY(p, cudaGraphCreate(&g, 0));
+  cudaGraphConditionalHandle h;
+  cudaError_t e = cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault);
+  cudaGraphNodeParams cp{};
+  cudaGraphNode_t node;
+  if (e == cudaSuccess) {
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    e = cudaGraphAddNode(&node, g, nullptr, 0, &cp);
+  }
+  if (e == cudaSuccess) {
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    e = cudaStreamBeginCaptureToGraph(p->cap_stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (e == cudaSuccess) {
+      const bool prof = p->prof;
+      p->prof = false;  // no event records inside the conditional body
+      p->capturing = true;
+      cudaError_t e1 = enqueue_sweep(p, p->cap_stream);
+      if (e1 == cudaSuccess) e1 = launch_fp_conv(h, p->loopst, p->dscal, p->cap_stream);
+      p->capturing = false;
+      p->prof = prof;
+      cudaError_t e2 = cudaStreamEndCapture(p->cap_stream, &body);
+      e = e1 != cudaSuccess ? e1 : e2;
+    }
+  }
+  if (e == cudaSuccess) e = cudaGraphInstantiate(&p->loop_exec, g, 0);
+  cudaGraphDestroy(g);
+  if (e != cudaSuccess) {
+    p->loop_exec = nullptr;
+    return fail(p, EXPD_ERR_CUDA, std::string("device loop graph: ") + cudaGetErrorString(e));
+  }
+  return EXPD_OK;
+}
+
+static expd_status fixed_point_device_loop(expd_plan* p, double tol, int maxit, expd_report* report) {
+  if (!p->h_loopst) CUDA_TRY(p, cudaMallocHost(&p->h_loopst, sizeof(FpLoopState)));
+  if (!p->loop_exec) {
+    expd_status s = build_loop_graph(p);
+    if (s) return s;
+  }
+  FpLoopState* hs = p->h_loopst;
+  hs->k = 0;
+  hs->status = -1;
+  hs->maxit = maxit;
+  hs->r0 = 0.0;
+  hs->tol = tol;
+  CUDA_TRY(p, cudaMemcpyAsync(p->loopst, hs, offsetof(FpLoopState, hist), cudaMemcpyHostToDevice, p->stream));
+  auto t0 = std::chrono::steady_clock::now();
+  CUDA_TRY(p, cudaGraphLaunch(p->loop_exec, p->stream));
+  CUDA_TRY(p, cudaMemcpyAsync(hs, p->loopst, sizeof(FpLoopState), cudaMemcpyDeviceToHost, p->stream));
+  CUDA_TRY(p, cudaStreamSynchronize(p->stream));
+  const double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  const int k = hs->k;
+  std::vector<double> hist(hs->hist, hs->hist + k + 1);
+  if (hs->status == 6) {
+    fill_report(report, k, k + 1, 0, hist, 0.0);
+    return fail(p, EXPD_ERR_BREAKDOWN, "non-finite residual norm");
+  }
+  if (hs->status != 0 && hs->status != 7)
+    return fail(p, EXPD_ERR_CUDA, "device loop ended without a verdict");
+  const int conv = hs->status == 0;
+  fill_report(report, conv ? k : maxit, conv ? k + 1 : maxit + 1, conv, hist, secs);
+  return conv ? EXPD_OK : EXPD_ERR_NOT_CONVERGED;
+}
+
 extern "C" expd_status expd_fixed_point_solve(expd_plan* p, const double* u0, double* U, double tol, int maxit,
                                               expd_report* report) {
   expd_status s = ready(p);
@@ -869,6 +976,21 @@ extern "C" expd_status expd_fixed_point_solve(expd_plan* p, const double* u0, do
   if (!u0 || !U || maxit < 0 || !(tol >= 0.0)) return fail(p, EXPD_ERR_INVALID_ARG, "fixed_point: bad args");
   s = expd_load_state(p, u0, U);
   if (s) return s;
+  if (!p->dist && graphs_enabled() && device_loop_enabled() && !p->loop_failed && maxit < kFpLoopHist) {
+    if (!p->loop_exec && build_loop_graph(p) != EXPD_OK) {
+      p->loop_failed = true;  // no conditional-node support: the host-driven loop below
+      if (getenv("EXPD_DEBUG")) fprintf(stderr, "expd: %s; host loop\n", p->err.c_str());
+      cudaGetLastError();
+    }
+  }
+  if (!p->dist && graphs_enabled() && device_loop_enabled() && !p->loop_failed && maxit < kFpLoopHist) {
+    s = fixed_point_device_loop(p, tol, maxit, report);
+    if (s && s != EXPD_ERR_NOT_CONVERGED) return s;
+    expd_status s2 = expd_store_state(p, U);
+    if (s2) return s2;
+    CUDA_TRY(p, cudaStreamSynchronize(p->stream));
+    return s;
+  }
   CUDA_TRY(p, cudaStreamSynchronize(p->stream));
   const bool graphs = graphs_enabled();
   std::vector<double> hist;

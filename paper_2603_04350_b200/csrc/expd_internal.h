@@ -109,6 +109,7 @@ cudaError_t launch_resid_only(const TimeArgs& a, int nl, int grid, cudaStream_t 
 struct DstTables {
   const double2* tw;   // [M] exp(-2 pi i q / M)
   const double* sinp;  // [M] sin(pi i / M)
+  const double* pa;    // [M] a_i = c (sin(pi i/M) + 1/2), c = sqrt(2/M)/2 (the line kernels' folded pre-processing)
 };
 // Orthonormal DST-I of every slice along every axis: physical (row stride n) <-> spectral
 // (row stride n+1).  src/dst may alias only when both are spectral.
@@ -165,6 +166,14 @@ cudaError_t cx_split(const double* in, long in_stride, long len, double* out, lo
 cudaError_t cx_merge(const double* in, long in_stride, long len, double* out, long out_stride, long nslices,
                      cudaStream_t st);
 int vec_grid(int sms);
+// device-side fixed-point loop state (expd_fixed_point_solve's CUDA-graph WHILE loop)
+constexpr int kFpLoopHist = 1024;  // history entries: the device loop takes maxit < kFpLoopHist
+struct FpLoopState {
+  int k, status, maxit, pad;
+  double r0, tol;
+  double hist[kFpLoopHist];
+};
+cudaError_t launch_fp_conv(cudaGraphConditionalHandle h, FpLoopState* st, const double* norm2, cudaStream_t s);
 
 // ---- multi-GPU (dist.cu) ----------------------------------------------------------------
 constexpr int EXPD_MAX_RANKS = 64;

@@ -82,7 +82,8 @@ struct LineArgs {
   int inner;       // ROW: row pairs per slice; COL: column-pair groups per outer index
   int rows;        // ROW: rows per slice (for the incomplete last pair)
   const double2* tw;   // [M] exp(-2 pi i q / M)
-  const double* sinp;  // [M] sin(pi i / M)
+  const double* pa;    // [M] a_i = c (sin(pi i/M) + 1/2), c = sqrt(2/M)/2 (b_i = a_i - c)
+  double c;            // sqrt(2/M)/2
   Poly poly;
 };
 
@@ -95,13 +96,17 @@ __device__ __forceinline__ uint32_t row_sw(int x) {
   return (uint32_t)(o * 128 + ((((c >> 1) ^ (o & 7))) << 4) + ((c & 1) << 3));
 }
 
-__device__ __forceinline__ double2 lpre(double2 z, double2 zm, double s) {
-  double2 sum = cadd(z, zm), dif = csub(z, zm);
-  return make_double2(fma(s, sum.x, 0.5 * dif.x), fma(s, sum.y, 0.5 * dif.y));
+// y_i = s_i (x_i + x_{M-i}) + (x_i - x_{M-i})/2 = a_i x_i + b_i x_{M-i} (times the folded scale
+// c): a = c (s + 1/2), b = a - c
+__device__ __forceinline__ double2 lpre(double2 z, double2 zm, double a, double c) {
+  const double b = a - c;
+  return make_double2(fma(a, z.x, b * zm.x), fma(a, z.y, b * zm.y));
 }
+// Hermitian unpack of the two real lines' transforms; the 1/2 of the textbook formulas and
+// the orthonormal scale are folded into the pre-processing table (a_i, b_i)
 __device__ __forceinline__ void lunpack(double2 Zk, double2 Zm, bool k0, double2& e, double2& w) {
-  e = make_double2(-0.5 * (Zk.y - Zm.y), 0.5 * (Zk.x - Zm.x));
-  w = make_double2(0.5 * (Zk.x + Zm.x), 0.5 * (Zk.y + Zm.y));
+  e = make_double2(Zm.y - Zk.y, Zk.x - Zm.x);
+  w = make_double2(Zk.x + Zm.x, Zk.y + Zm.y);
   if (k0) w = make_double2(0.5 * w.x, 0.5 * w.y);
 }
 // v[r] *= w^{r b}, r = 1..R-1, from the single table entry w^b.  EXPD_LINE_TWSEQ: running
@@ -138,7 +143,7 @@ __device__ __forceinline__ void ltwmul(const double2* __restrict__ tw, int b, do
 // each thread owns exactly one such job, the configurations used here).
 template <int M, int G>
 struct LPre {
-  double sp[LGeo<M, G, 1>::R0];
+  double pa[LGeo<M, G, 1>::R0];
   double2 tmid, ta, tb;
   int pj;  // this thread's partner job of the last stage (see partner_job)
 };
@@ -200,7 +205,7 @@ __device__ __forceinline__ void lmid(double2* buf, const double2* __restrict__ t
 }
 
 // DST core of G line pairs: thread (g, j) holds the stage-0 inputs y_i (i = j + T r) of
-// line pair g in v; leaves the unscaled F at natural positions [2jL, 2jL + 2L) in out
+// line pair g in v; leaves F (already scaled: V x) at natural positions [2jL, 2jL + 2L) in out
 // (F_m sits at position m-1; position M-1 is the spectral pad and returns 0).  Starts with
 // a barrier (buf may still be read by the caller's stage-0 loads).
 template <int M, int G>
@@ -384,7 +389,6 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
   const int tid = threadIdx.x;
   __builtin_assume(tid < D::THREADS);
   const int g = tid % G, j = tid / G;
-  const double scale = sqrt(2.0 / (double)M);
   const int my_pj = partner_job<M, G>(tid);
 
   if (tid == 0) {
@@ -410,13 +414,13 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
     // the twiddle / sine tables are re-read every item: an opaque copy of the pointers keeps
     // the compiler from hoisting ~30 loop-invariant twiddles into registers for the whole loop
     const double2* tw = a.tw;
-    const double* sinp = a.sinp;
-    asm volatile("" : "+l"(tw), "+l"(sinp));
+    const double* pa = a.pa;
+    asm volatile("" : "+l"(tw), "+l"(pa));
     LPre<M, G> pre;
     pre.pj = my_pj;
     {
 #pragma unroll
-      for (int r = 0; r < R0; ++r) pre.sp[r] = __ldg(sinp + j + T * r);  // sinp[0] = 0
+      for (int r = 0; r < R0; ++r) pre.pa[r] = __ldg(pa + j + T * r);
       constexpr int NS1 = R0, TWS1 = M / (NS1 * D::RM1);
       pre.tmid = __ldg(tw + (j % NS1) * TWS1);
       constexpr int NSL = D::NSL;
@@ -449,12 +453,12 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
                                          *reinterpret_cast<const double*>(cb + M * 8 + o1));
           const double2 zm = make_double2(*reinterpret_cast<const double*>(cb + o2),
                                           *reinterpret_cast<const double*>(cb + M * 8 + o2));
-          v[r] = lpre(z, zm, pre.sp[r]);
+          v[r] = lpre(z, zm, pre.pa[r], a.c);
         } else {
           // pass 0: raw [row][G] linear; pass 1: the padded layout written by the N step
           const int p1 = i - 1, p2 = M - i - 1;
           const int q1 = pass ? lswz<PADP>(p1) : p1, q2 = pass ? lswz<PADP>(p2) : p2;
-          v[r] = lpre(buf[q1 * G + g], buf[q2 * G + g], pre.sp[r]);
+          v[r] = lpre(buf[q1 * G + g], buf[q2 * G + g], pre.pa[r], a.c);
         }
       }
       lcore<M, G>(v, buf, wt, tw, out, pre);
@@ -463,7 +467,7 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
 #pragma unroll
         for (int q = 0; q < 2 * L; ++q)
           lat<M, G>(buf, 2 * j * L + q, g) =
-              make_double2(poly_eval(a.poly, scale * out[q].x), poly_eval(a.poly, scale * out[q].y));
+              make_double2(poly_eval(a.poly, out[q].x), poly_eval(a.poly, out[q].y));
         __syncthreads();
       }
     }
@@ -474,14 +478,14 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
       for (int l = 0; l < L; ++l) {
         const int x = 2 * j * L + 2 * l;
         const uint32_t off = row_sw(x);
-        *reinterpret_cast<double2*>(cb + off) = make_double2(scale * out[2 * l].x, scale * out[2 * l + 1].x);
-        *reinterpret_cast<double2*>(cb + M * 8 + off) = make_double2(scale * out[2 * l].y, scale * out[2 * l + 1].y);
+        *reinterpret_cast<double2*>(cb + off) = make_double2(out[2 * l].x, out[2 * l + 1].x);
+        *reinterpret_cast<double2*>(cb + M * 8 + off) = make_double2(out[2 * l].y, out[2 * l + 1].y);
       }
     } else {
       // chunk -> padded layout (conflict free), then compact in place to the linear [row][G]
       // layout the TMA store reads; thread (g, j) moves positions j + T r of pair g
 #pragma unroll
-      for (int q = 0; q < 2 * L; ++q) lat<M, G>(buf, 2 * j * L + q, g) = make_double2(scale * out[q].x, scale * out[q].y);
+      for (int q = 0; q < 2 * L; ++q) lat<M, G>(buf, 2 * j * L + q, g) = out[q];
       __syncthreads();
       double2 c[R0];
 #pragma unroll
@@ -615,7 +619,8 @@ static cudaError_t launch_line(const Geom& g, const DstTables& t, const Poly& P,
   a.rows = rows;
   a.nitems = (long)a.per_slice * nslices;
   a.tw = t.tw;
-  a.sinp = t.sinp;
+  a.pa = t.pa;
+  a.c = 0.5 * sqrt(2.0 / (double)g.M);
   a.poly = P;
   long grid = (long)sm_count() * per_sm;
   if (grid > a.nitems) grid = a.nitems;

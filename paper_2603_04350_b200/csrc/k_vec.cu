@@ -108,6 +108,40 @@ cudaError_t reduce_partials(const double* partial, int n, double* out, cudaStrea
 
 int vec_grid(int sms) { return sms * 4; }
 
+// The convergence test of the fixed-point / Picard iteration (R8) on the device: the body of
+// the CUDA-graph WHILE loop of expd_fixed_point_solve (one sweep, the norm reduction, then
+// this kernel).  rho_k = ||r^k|| / ||r^0||; stop on rho_k < tol (converged), on a non-finite
+// norm (breakdown) or after sweep maxit; otherwise k += 1 and the loop runs another sweep.
+__global__ void k_fp_conv(cudaGraphConditionalHandle h, FpLoopState* st, const double* norm2) {
+  if (threadIdx.x != 0) return;
+  const int k = st->k;
+  const double n2 = norm2[0];
+  unsigned int again = 0;
+  if (!isfinite(n2)) {
+    st->hist[k] = n2;
+    st->status = 6;  // EXPD_ERR_BREAKDOWN
+  } else {
+    const double rn = sqrt(n2);
+    if (k == 0) st->r0 = rn;
+    const double rho = st->r0 > 0.0 ? rn / st->r0 : 0.0;
+    st->hist[k] = rho;
+    if (rho < st->tol) {
+      st->status = 0;
+    } else if (k >= st->maxit) {
+      st->status = 7;  // EXPD_ERR_NOT_CONVERGED
+    } else {
+      st->k = k + 1;
+      again = 1;
+    }
+  }
+  cudaGraphSetConditional(h, again);
+}
+
+cudaError_t launch_fp_conv(cudaGraphConditionalHandle h, FpLoopState* st, const double* norm2, cudaStream_t s) {
+  k_fp_conv<<<1, 32, 0, s>>>(h, st, norm2);
+  return cudaGetLastError();
+}
+
 struct VecPtrs {
   const double* v[32];
 };

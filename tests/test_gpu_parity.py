@@ -366,3 +366,33 @@ print('ok', its, err)
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     r = subprocess.run([sys.executable, "-c", code], cwd=root, env=env, capture_output=True, text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
+
+
+@pytest.mark.parametrize("name,n,nt", [("c1", None, None), ("c2", 63, 64), ("c5", 255, 16), ("c3if", 63, 128)])
+def test_device_loop_matches_host_loop(orc, name, n, nt, monkeypatch):
+    """The fixed-point / Picard solve's device-side loop (CUDA-graph WHILE node, one host sync)
+    takes the same iterations, history and solution as the host-driven loop and the oracle."""
+    cfg = synth.CONFIGS[name] if n is None else cfg_small(name, n, nt)
+    u0 = synth.initial_condition(cfg)
+    plan = Plan(Problem.from_config(cfg))
+    Ud, rd = plan.fixed_point_solve(T(u0), tol=cfg.tol, maxit=50)
+    Ud2, rd2 = plan.fixed_point_solve(T(u0), tol=cfg.tol, maxit=50)  # the graph is reused
+    monkeypatch.setenv("EXPD_DEVICE_LOOP", "0")
+    Uh, rh = plan.fixed_point_solve(T(u0), tol=cfg.tol, maxit=50)
+    Uo, st, its, hist = orc.fixed_point(orc.spec(cfg), u0, tol=cfg.tol, maxit=50)
+    assert rd["converged"] and rh["converged"] and rd["iterations"] == rh["iterations"] == its
+    assert rd["sweeps"] == rh["sweeps"] == its + 1
+    assert rd["hist"] == rh["hist"] == rd2["hist"]  # the same kernels in the same order: bitwise
+    assert float((Ud - Uh).abs().max()) == 0.0 and float((Ud2 - Uh).abs().max()) == 0.0
+    assert relmax(H(Ud), Uo) < 1e-9
+
+
+def test_device_loop_not_converged_and_maxit(orc):
+    cfg = cfg_small("c5", 63, 32)
+    plan = Plan(Problem.from_config(cfg))
+    u0 = T(synth.initial_condition(cfg))
+    U, rep = plan.fixed_point_solve(u0, tol=1e-30, maxit=3)
+    assert rep["status"] == "EXPD_ERR_NOT_CONVERGED" and not rep["converged"]
+    assert rep["iterations"] == 3 and rep["sweeps"] == 4 and len(rep["hist"]) == 4
+    U0, rep0 = plan.fixed_point_solve(u0, tol=1e-30, maxit=0)
+    assert rep0["sweeps"] == 1 and len(rep0["hist"]) == 1
