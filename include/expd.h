@@ -180,6 +180,28 @@ long expd_a2a_schedule(const expd_problem* prob, int rank, int nranks, int direc
    rank's slab holds nt / nranks slices, so a key range is one symmetric chunk. */
 long expd_a2a_schedule_keyed(const expd_problem* prob, int rank, int nranks, int direction, int shift,
                              long* sends, long* recvs, long cap, int stride);
+/* A point-to-point transport for expd_a2a_execute_host: send / recv post one message of
+   `count` doubles to / from `peer` (host memory, valid until group_end returns); group_start /
+   group_end (nullable) bracket the messages of one all-to-all chunk, and group_end returns
+   when all of them are complete.  Each returns 0 on success.  ctx is passed through. */
+typedef struct {
+  void* ctx;
+  int (*group_start)(void* ctx);
+  int (*send)(void* ctx, const double* buf, long count, int peer);
+  int (*recv)(void* ctx, double* buf, long count, int peer);
+  int (*group_end)(void* ctx);
+} expd_transport;
+/* Executes this rank's all-to-all schedule (direction, shift as expd_a2a_schedule) for the
+   slice keys [s_lo, s_hi) on HOST buffers through `transport`: self messages are host
+   copies, the others one group of sends then receives in the schedule's order.  It is the
+   very routine the distributed sweep runs on the device, where the transport is
+   cudaMemcpyAsync + ncclSend / ncclRecv inside ncclGroupStart / ncclGroupEnd -- exposed so
+   the message selection, self pairing, ordering and chunking run under a CPU transport
+   (tests/test_dist_cpu.py: torch.distributed gloo) without GPUs.  src / dst: the layouts of
+   expd_a2a_schedule (doubles).  INVALID_ARG on bad arguments or a schedule mismatch,
+   EXPD_ERR_NCCL if the transport fails. */
+expd_status expd_a2a_execute_host(const expd_problem* prob, int rank, int nranks, int direction, int shift, int s_lo,
+                                  int s_hi, const double* src, double* dst, const expd_transport* transport);
 /* NCCL communicator for a plan (NCCL is loaded at run time: the process's libnccl.so.2).
    Rank 0 creates the 128-byte id, the caller broadcasts it (e.g. torch.distributed), every
    rank calls expd_nccl_comm_init (collective).  The caller owns the communicator. */

@@ -129,15 +129,18 @@ static std::string nccl_err(ncclResult_t r) {
   return a.ok ? std::string(a.GetErrorString(r)) : std::string("NCCL not loaded");
 }
 
-// Execute one schedule (the messages with slice key in [s_lo, s_hi)): NCCL send / recv for
-// peers, device copies for the self part.  Every message's slice key is the slice index
-// within the time slab it belongs to, and every rank's slab has nt / P slices, so a key
-// range is one symmetric chunk of the all-to-all on every rank.
-int a2a_execute(void* comm, const DistLayout& L, const std::vector<A2AMsg>& sends, const std::vector<A2AMsg>& recvs,
-                const double* src, double* dst, cudaStream_t st, std::string& err, int s_lo, int s_hi) {
-  NcclApi& a = nccl();
+// Execute one schedule (the messages with slice key in [s_lo, s_hi)) through a transport:
+// the self part as local copies (the k-th self send paired with the k-th self recv), then
+// one group of point-to-point sends and receives in the schedule's order.  Every message's
+// slice key is the slice index within the time slab it belongs to, and every rank's slab
+// has nt / P slices, so a key range is one symmetric chunk of the all-to-all on every rank.
+// The device path runs it with NcclTransport (cudaMemcpyAsync + ncclSend / ncclRecv); the
+// CPU tests run the SAME function with a host transport (expd_a2a_execute_host: memcpy +
+// the caller's send / recv, torch.distributed gloo in tests/test_dist_cpu.py).
+template <class Tr>
+static int a2a_run(Tr& tr, const DistLayout& L, const std::vector<A2AMsg>& sends, const std::vector<A2AMsg>& recvs,
+                   const double* src, double* dst, std::string& err, int s_lo, int s_hi) {
   auto in = [&](const A2AMsg& m) { return m.slice >= s_lo && m.slice < s_hi; };
-  // self part: pair the k-th self send with the k-th self recv
   std::vector<const A2AMsg*> ss, rr;
   for (const auto& m : sends)
     if (m.peer == L.rank && in(m)) ss.push_back(&m);
@@ -148,32 +151,78 @@ int a2a_execute(void* comm, const DistLayout& L, const std::vector<A2AMsg>& send
     return EXPD_ERR_INVALID_ARG;
   }
   for (size_t k = 0; k < ss.size(); ++k) {
-    cudaError_t e = cudaMemcpyAsync(dst + rr[k]->dst_off, src + ss[k]->src_off, sizeof(double) * ss[k]->count,
-                                    cudaMemcpyDeviceToDevice, st);
-    if (e != cudaSuccess) {
-      err = std::string("a2a self copy: ") + cudaGetErrorString(e);
-      return EXPD_ERR_CUDA;
+    if (ss[k]->count != rr[k]->count) {
+      err = "a2a: self message sizes differ";
+      return EXPD_ERR_INVALID_ARG;
     }
+    if (int e = tr.self_copy(dst + rr[k]->dst_off, src + ss[k]->src_off, ss[k]->count, err)) return e;
   }
   if (L.nranks == 1) return EXPD_OK;
-  if (!a.ok || !comm) {
-    err = "a2a: NCCL unavailable";
-    return EXPD_ERR_NCCL;
-  }
-  ncclComm_t c = (ncclComm_t)comm;
-  ncclResult_t r = a.GroupStart();
+  if (int e = tr.group_start(err)) return e;
+  int st = EXPD_OK;
   for (const auto& m : sends)
-    if (r == ncclSuccess && m.peer != L.rank && in(m))
-      r = a.Send(src + m.src_off, (size_t)m.count, ncclFloat64, m.peer, c, st);
+    if (st == EXPD_OK && m.peer != L.rank && in(m)) st = tr.send(src + m.src_off, m.count, m.peer, err);
   for (const auto& m : recvs)
-    if (r == ncclSuccess && m.peer != L.rank && in(m))
-      r = a.Recv(dst + m.dst_off, (size_t)m.count, ncclFloat64, m.peer, c, st);
-  ncclResult_t r2 = a.GroupEnd();
-  if (r != ncclSuccess || r2 != ncclSuccess) {
-    err = "a2a: " + nccl_err(r != ncclSuccess ? r : r2);
+    if (st == EXPD_OK && m.peer != L.rank && in(m)) st = tr.recv(dst + m.dst_off, m.count, m.peer, err);
+  const int st2 = tr.group_end(err);  // always close the group
+  return st != EXPD_OK ? st : st2;
+}
+
+struct NcclTransport {
+  void* comm;
+  cudaStream_t st;
+  int self_copy(double* d, const double* s, long n, std::string& err) {
+    cudaError_t e = cudaMemcpyAsync(d, s, sizeof(double) * n, cudaMemcpyDeviceToDevice, st);
+    if (e == cudaSuccess) return EXPD_OK;
+    err = std::string("a2a self copy: ") + cudaGetErrorString(e);
+    return EXPD_ERR_CUDA;
+  }
+  int check(ncclResult_t r, std::string& err) {
+    if (r == ncclSuccess) return EXPD_OK;
+    err = "a2a: " + nccl_err(r);
     return EXPD_ERR_NCCL;
   }
-  return EXPD_OK;
+  int group_start(std::string& err) {
+    NcclApi& a = nccl();
+    if (!a.ok || !comm) {
+      err = "a2a: NCCL unavailable";
+      return EXPD_ERR_NCCL;
+    }
+    return check(a.GroupStart(), err);
+  }
+  int send(const double* b, long n, int peer, std::string& err) {
+    return check(nccl().Send(b, (size_t)n, ncclFloat64, peer, (ncclComm_t)comm, st), err);
+  }
+  int recv(double* b, long n, int peer, std::string& err) {
+    return check(nccl().Recv(b, (size_t)n, ncclFloat64, peer, (ncclComm_t)comm, st), err);
+  }
+  int group_end(std::string& err) {
+    NcclApi& a = nccl();
+    return a.ok ? check(a.GroupEnd(), err) : EXPD_ERR_NCCL;
+  }
+};
+
+struct HostTransport {
+  const expd_transport* t;
+  int self_copy(double* d, const double* s, long n, std::string&) {
+    memmove(d, s, sizeof(double) * n);
+    return EXPD_OK;
+  }
+  int wrap(int r, const char* what, std::string& err) {
+    if (r == 0) return EXPD_OK;
+    err = std::string("a2a host transport: ") + what + " failed";
+    return EXPD_ERR_NCCL;
+  }
+  int group_start(std::string& err) { return wrap(t->group_start ? t->group_start(t->ctx) : 0, "group_start", err); }
+  int send(const double* b, long n, int peer, std::string& err) { return wrap(t->send(t->ctx, b, n, peer), "send", err); }
+  int recv(double* b, long n, int peer, std::string& err) { return wrap(t->recv(t->ctx, b, n, peer), "recv", err); }
+  int group_end(std::string& err) { return wrap(t->group_end ? t->group_end(t->ctx) : 0, "group_end", err); }
+};
+
+int a2a_execute(void* comm, const DistLayout& L, const std::vector<A2AMsg>& sends, const std::vector<A2AMsg>& recvs,
+                const double* src, double* dst, cudaStream_t st, std::string& err, int s_lo, int s_hi) {
+  NcclTransport tr{comm, st};
+  return a2a_run(tr, L, sends, recvs, src, dst, err, s_lo, s_hi);
 }
 
 int allreduce_sum(void* comm, int nranks, double* buf, long count, cudaStream_t st, std::string& err) {
@@ -264,6 +313,22 @@ extern "C" long expd_a2a_schedule_keyed(const expd_problem* prob, int rank, int 
     }
   }
   return n;
+}
+
+extern "C" expd_status expd_a2a_execute_host(const expd_problem* prob, int rank, int nranks, int direction,
+                                             int shift, int s_lo, int s_hi, const double* src, double* dst,
+                                             const expd_transport* transport) {
+  Geom g{};
+  if (!src || !dst || !transport || !transport->send || !transport->recv || !geom_of(prob, &g))
+    return EXPD_ERR_INVALID_ARG;
+  DistLayout L{};
+  if (!dist_layout(g, prob->nt, rank, nranks, &L)) return EXPD_ERR_INVALID_ARG;
+  if (direction != A2A_MODE_TO_TIME && direction != A2A_TIME_TO_MODE) return EXPD_ERR_INVALID_ARG;
+  std::vector<A2AMsg> s, r;
+  a2a_schedule(L, direction, shift, s, r);
+  HostTransport tr{transport};
+  std::string err;
+  return (expd_status)a2a_run(tr, L, s, r, src, dst, err, s_lo, s_hi);
 }
 
 extern "C" expd_status expd_nccl_unique_id(unsigned char id[128]) {

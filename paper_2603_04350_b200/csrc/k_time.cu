@@ -29,7 +29,14 @@ cudaError_t launch_time_fused(const TimeArgs& a, int rmode, int outmode, int nl,
 // by the number of tiles.
 // tiles per CTA-slot of the TMA variant: (pairs per tile, resident CTAs per SM)
 template <int NT>
-static void tma_shape(int nl, int& S, int& per_sm) {
+static void tma_shape(int nl, int& S, int& per_sm, long npairs) {
+  if constexpr (ring_capable<NT>()) {
+    if (k1_variant(NT) == 5123 && ring_ok<NT>(npairs)) {  // one 512-thread CTA per SM
+      S = RingLayout<NT, 1>::S;
+      per_sm = 1;
+      return;
+    }
+  }
   if (k1_variant(NT) == 1282) {
     S = TmaLayout<NT, 128, 1, 2>::S;
     per_sm = nl ? TmaLayout<NT, 128, 1, 2>::MINB : TmaLayout<NT, 128, 0, 2>::MINB;
@@ -58,11 +65,11 @@ int time_fused_grid(int nt, long npairs, int sms, int nl) {
   if (nt >= 16 && use_pipe()) per_sm = pipe_mode() == 1 ? 1 : 2;
   if (nt >= 16 && pipe_mode() == 3) {
     switch (nt) {
-      case 16: tma_shape<16>(nl, S, per_sm); break;
-      case 32: tma_shape<32>(nl, S, per_sm); break;
-      case 64: tma_shape<64>(nl, S, per_sm); break;
-      case 128: tma_shape<128>(nl, S, per_sm); break;
-      default: tma_shape<256>(nl, S, per_sm);
+      case 16: tma_shape<16>(nl, S, per_sm, npairs); break;
+      case 32: tma_shape<32>(nl, S, per_sm, npairs); break;
+      case 64: tma_shape<64>(nl, S, per_sm, npairs); break;
+      case 128: tma_shape<128>(nl, S, per_sm, npairs); break;
+      default: tma_shape<256>(nl, S, per_sm, npairs);
     }
   }
   long ntiles = (npairs + S - 1) / S;

@@ -177,10 +177,10 @@ __device__ __forceinline__ void twpow_mul(double2* v, double2 w1) {
 
 // tstage with the job's base twiddle w^{k NT/(NS R)} in a register (one job per thread).
 template <int NT, int S, int THREADS, int R, int NS, int DIR>
-__device__ __forceinline__ void tstage_pw(const double2* __restrict__ in, double2* __restrict__ out, double2 w1) {
+__device__ __forceinline__ void tstage_pw(const double2* __restrict__ in, double2* __restrict__ out, double2 w1,
+                                          int J = threadIdx.x) {
   constexpr int JOBS = S * (NT / R);
   static_assert(JOBS == THREADS, "one job per thread");
-  const int J = threadIdx.x;
   const int s = J % S, j = J / S, k = j % NS;
   double2 v[R];
 #pragma unroll
@@ -943,6 +943,239 @@ __global__ void __launch_bounds__(THR, (TmaLayout<NT, THR, NL, NST>::MINB))
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// K1 "ring" variant (EXPD_K1V = 5123, the default for Nt = 128 / 256): one persistent CTA of
+// TWO 256-thread warp groups per SM sharing a ring of THREE staged tiles.  Each group runs the
+// same per-tile pipeline as k_time_tma (phase A, the Stockham stages, the Hermitian-pair
+// divide, phase C) on every other tile of the CTA's sequence, synchronising on its own named
+// barrier, so two tiles are transformed at once (16 warps per SM instead of 8: the latency
+// that left k_time_tma issue-bound at 25 %) while the third buffer streams in.  A group that
+// finishes tile i refills the tile's buffer with tile i + 3 (TMA tensor boxes for U-hat /
+// N-hat, 1-D bulk copies for the per-mode tables, all on the buffer's mbarrier).  FFT scratch
+// lives inside the tile's own buffer after phase A has read it (u_t stays in registers for the
+// update): N-hat block and U-hat block (nonlinear forms), U-hat block and a per-group buffer
+// (linear forms).  Requires npairs % S == 0 (full tiles).
+// ---------------------------------------------------------------------------------------
+// the plans with one job per thread in every stage of a 256-thread group (Nt = 256)
+template <int NT>
+constexpr bool ring_capable() {
+  using G = TGeo<NT, 256>;
+  return G::L == 3 && G::S * (NT / TimeCfg<NT>::R1) == 256 && G::S * (G::NSL / 2) == 256;
+}
+
+template <int NT, int NL>
+struct RingLayout {
+  using G = TGeo<NT, 256>;
+  static constexpr int S = G::S;
+  static constexpr int TILE = NT * S;                      // double2 per staged array
+  static constexpr int NARR = 1 + (K1Form<NL>::HASN ? 1 : 0);
+  static constexpr int AUX = 4 * S;                        // E, C1, C2, u0-hat per pair
+  static constexpr int STAGE = ((NARR * TILE + AUX) + 7) / 8 * 8;
+  static constexpr int NBUF = 3;
+  static constexpr int XBUF = K1Form<NL>::HASN ? 0 : TILE;  // per-group FFT buffer (linear forms)
+  static constexpr size_t BYTES =
+      128 + sizeof(double2) * ((size_t)NBUF * STAGE + 2 * XBUF + NT) + sizeof(double) * 2 * NT + 8 * NBUF + 16;
+};
+
+template <int NT, int RM, int NL>
+__device__ __forceinline__ void ring_issue(const CUtensorMap* mx, const CUtensorMap* mn, const TimeArgs& a,
+                                           long tile, double2* stage, uint64_t* bar) {
+  using PL = RingLayout<NT, NL>;
+  constexpr int S = PL::S, TILE = PL::TILE;
+  constexpr uint32_t AUXB = 16 * S;
+  constexpr int NAUX = 1 + (K1Form<NL>::HASN ? 1 : 0) + (NL == 2 ? 1 : 0) + (RM == RM_RESID ? 1 : 0);
+  mbar_arrive_expect_tx(bar, (uint32_t)(PL::NARR * TILE * 16) + NAUX * AUXB);
+  tma_load_2d(stage, mx, bar, (int)(2 * S * tile), 0);
+  if constexpr (K1Form<NL>::HASN) tma_load_2d(stage + TILE, mn, bar, (int)(2 * S * tile), 0);
+  double2* aux = stage + PL::NARR * TILE;
+  const long off = 2 * S * tile;  // doubles
+  bulk_load_1d(aux, a.E + off, AUXB, bar);
+  if constexpr (K1Form<NL>::HASN) bulk_load_1d(aux + S, a.C1 + off, AUXB, bar);
+  if constexpr (NL == 2) bulk_load_1d(aux + 2 * S, a.C2 + off, AUXB, bar);
+  if constexpr (RM == RM_RESID) bulk_load_1d(aux + 3 * S, a.u0h + off, AUXB, bar);
+}
+
+template <int NT, int RM, int OUTM, int NL>
+__global__ void __launch_bounds__(512, 1)
+    k_time_ring(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mn,
+                const __grid_constant__ TimeArgs a) {
+  using G = TGeo<NT, 256>;
+  using C = TimeCfg<NT>;
+  using PL = RingLayout<NT, NL>;
+  constexpr int L = G::L, R0 = G::R0, RL = G::RL, TPS = G::TPS, S = G::S, GT = 256;
+  constexpr int NSL = G::NSL, TILE = PL::TILE, NBUF = PL::NBUF;
+  static_assert(L == 3 && S * (NT / C::R1) == GT && S * (NSL / 2) == GT, "ring kernel: the one-job-per-thread plans");
+  extern __shared__ unsigned char rsm_raw[];
+  double2* smem = reinterpret_cast<double2*>(rsm_raw + ((128u - (smem_u32(rsm_raw) & 127u)) & 127u));
+  double2* xbuf = smem + NBUF * PL::STAGE;             // [2][XBUF] (linear forms)
+  double2* stw = xbuf + 2 * PL::XBUF;                  // [NT] e^{+2 pi i q/NT}
+  double* sg = reinterpret_cast<double*>(stw + NT);    // [NT] alpha^{t/NT}
+  double* sgi = sg + NT;                               // [NT] alpha^{-t/NT}
+  uint64_t* full = reinterpret_cast<uint64_t*>(sgi + NT);
+
+  const int grp = threadIdx.x / GT;
+  const int tid = threadIdx.x % GT;
+  for (int i = threadIdx.x; i < NT; i += 2 * GT) {
+    stw[i] = a.tw[i];
+    sg[i] = a.g[i];
+    sgi[i] = a.ginv[i];
+  }
+  const long ntiles = a.npairs / S;
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&mx);
+    if constexpr (K1Form<NL>::HASN) prefetch_tmap(&mn);
+    for (int k = 0; k < NBUF; ++k) mbar_init(&full[k], 1);
+    mbar_fence_init();
+    for (int k = 0; k < NBUF; ++k) {
+      const long t = blockIdx.x + (long)k * gridDim.x;
+      if (t < ntiles) ring_issue<NT, RM, NL>(&mx, &mn, a, t, smem + k * PL::STAGE, &full[k]);
+    }
+  }
+  __syncthreads();
+  const double hin = a.half_inv_nt;
+  double nrm = 0.0;
+  const int s = tid % S;
+  const int j = tid / S;
+  const long npad = a.npad;
+  const int pj = tid / S;
+  // this thread's base twiddles, re-read from shared memory where used (an opaque copy of
+  // the table pointer keeps the compiler from holding all five in registers for the loop)
+  const int i_fm = ((j % R0) * (NT / (R0 * C::R1))) & (NT - 1);
+  const int i_im = ((j % RL) * (NT / (RL * C::R1))) & (NT - 1);
+  const int i_pa = pj & (NT - 1);
+  const int i_pb = (pj == 0 ? NSL / 2 : NSL - pj) & (NT - 1);
+  const int i_c = j & (NT - 1);
+  const int barid = 1 + grp;
+
+  for (long i = grp;; i += 2) {
+    const long tile = blockIdx.x + i * gridDim.x;
+    if (tile >= ntiles) break;
+    const int b = (int)(i % NBUF);
+    double2* stg = smem + b * PL::STAGE;
+    mbar_wait(&full[b], (uint32_t)((i / NBUF) & 1));
+    const double2* X = stg;
+    const double2* NH = stg + TILE;
+    const double2* aux = stg + PL::NARR * TILE;
+    double2* buf0 = K1Form<NL>::HASN ? stg + TILE : stg;            // after phase A
+    double2* buf1 = K1Form<NL>::HASN ? stg : xbuf + grp * PL::XBUF;
+    const long pair = tile * S + s;
+    const long base = 2 * pair;
+    const double2* tw = stw;
+    asm volatile("" : "+l"(tw));
+
+    // ---- phase A: residual (+ ||r||^2), Gamma_alpha, forward stage 0 -------------------
+    double2 y[R0];
+    double2 xv[OUTM == OUT_UPDATE ? R0 : 1];
+    const double2 Ej = aux[s];
+    const double2 c1 = K1Form<NL>::HASN ? aux[S + s] : make_double2(0.0, 0.0);
+    const double2 c2 = NL == 2 ? aux[2 * S + s] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int r = 0; r < R0; ++r) {
+      const int t = j + r * TPS;
+      const double2 xc = X[t * S + s];
+      if constexpr (OUTM == OUT_UPDATE) xv[r] = xc;
+      double2 rr;
+      if constexpr (RM == RM_INPUT) {
+        rr = xc;
+      } else if constexpr (K1Form<NL>::BDF) {
+        const double2 zero = make_double2(0.0, 0.0);
+        const double2 xm1 = t >= 1 ? X[(t - 1) * S + s] : zero;
+        const double2 xm2 = t >= 2 ? X[(t - 2) * S + s] : zero;
+        const double2 u0 = RM == RM_RESID ? aux[3 * S + s] : zero;
+        rr = bdf2_form<RM == RM_RESID, K1Form<NL>::CX>(Ej, xc, xm1, xm2, u0, t);
+      } else {
+        const double2 prev = t > 0 ? X[(t - 1) * S + s] : (RM == RM_RESID ? aux[3 * S + s] : make_double2(0.0, 0.0));
+        if constexpr (K1Form<NL>::CX) {
+          const double2 ep = cmul(Ej, prev);
+          rr = RM == RM_RESID ? csub(ep, xc) : csub(xc, ep);
+        } else if constexpr (RM == RM_RESID) {
+          rr = make_double2(fma(Ej.x, prev.x, -xc.x), fma(Ej.y, prev.y, -xc.y));
+          if constexpr (K1Form<NL>::HASN) {
+            const double2 nm1 = NH[t * S + s];
+            rr.x = fma(c1.x, nm1.x, rr.x);
+            rr.y = fma(c1.y, nm1.y, rr.y);
+            if constexpr (NL == 2) {
+              const double2 nm2 = NH[(t > 0 ? t - 1 : 0) * S + s];
+              rr.x = fma(-c2.x, nm2.x, rr.x);
+              rr.y = fma(-c2.y, nm2.y, rr.y);
+            }
+          }
+        } else {  // RM_QOP
+          rr = make_double2(fma(-Ej.x, prev.x, xc.x), fma(-Ej.y, prev.y, xc.y));
+        }
+      }
+      nrm = fma(rr.x, rr.x, fma(rr.y, rr.y, nrm));
+      y[r] = cscale(rr, sg[t]);
+    }
+    DFT<R0, +1>::run(y);
+    named_bar(barid, GT);  // the group is done reading the tile (U-hat, N-hat)
+#pragma unroll
+    for (int r = 0; r < R0; ++r) buf0[(j * R0 + r) * S + s] = y[r];
+    named_bar(barid, GT);
+    tstage_pw<NT, S, GT, C::R1, R0, +1>(buf0, buf1, tw[i_fm], tid);
+    named_bar(barid, GT);
+    {
+      const int ps = s;
+      const int ja = pj, jb = pj == 0 ? NSL / 2 : NSL - pj;
+      double2 va[RL], vb[RL];
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        va[r] = buf1[(ja + r * NSL) * S + ps];
+        vb[r] = buf1[(jb + r * NSL) * S + ps];
+      }
+      twpow_mul<RL, +1>(va, tw[i_pa]);
+      twpow_mul<RL, +1>(vb, tw[i_pb]);
+      DFT<RL, +1>::run(va);
+      DFT<RL, +1>::run(vb);
+      // one partner job per thread: its pair is this thread's pair s (Ej)
+      pair_divide<NT, RL, K1Form<NL>::BDF, K1Form<NL>::CX>(va, vb, pj == 0, stw, ja, jb, a.a1 * Ej.x, a.a1 * Ej.y,
+                                                           hin);
+      DFT<RL, -1>::run(va);
+      DFT<RL, -1>::run(vb);
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        buf0[(ja * RL + r) * S + ps] = va[r];
+        buf0[(jb * RL + r) * S + ps] = vb[r];
+      }
+    }
+    named_bar(barid, GT);
+    tstage_pw<NT, S, GT, C::R1, RL, -1>(buf0, buf1, tw[i_im], tid);
+    named_bar(barid, GT);
+#pragma unroll
+    for (int r = 0; r < R0; ++r) y[r] = buf1[(j + r * TPS) * S + s];
+    // every generic write into the buffer is ordered before the refill's async-proxy writes;
+    // after the barrier no thread of the group reads it again
+    fence_proxy_async_smem();
+    named_bar(barid, GT);
+    if (tid == 0) {
+      const long nxt = blockIdx.x + (i + NBUF) * gridDim.x;
+      if (nxt < ntiles) ring_issue<NT, RM, NL>(&mx, &mn, a, nxt, stg, &full[b]);
+    }
+    twpow_mul<R0, -1>(y, tw[i_c]);
+    DFT<R0, -1>::run(y);
+    // ---- phase C: Gamma_alpha^{-1}, update, store ----------------------------------------
+#pragma unroll
+    for (int r = 0; r < R0; ++r) {
+      const int t = j + r * TPS;
+      double2 sv = cscale(y[r], sgi[t]);
+      if constexpr (OUTM == OUT_UPDATE) sv = cadd(xv[r], sv);
+      st2(a.Y + (long)t * npad + base, sv);
+    }
+  }
+
+  if (a.partial) {
+    __shared__ double red[2 * GT / 32];
+    for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      double v = threadIdx.x < 2 * GT / 32 ? red[threadIdx.x] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (threadIdx.x == 0) a.partial[blockIdx.x] = v;
+    }
+  }
+}
+
 template <int NT, int OUTM>
 static size_t time_smem_bytes() {
   const size_t tile = TimeGeo<NT>::L > 1 ? (size_t)NT * TimeGeo<NT>::S : 0;
@@ -968,7 +1201,7 @@ static int k1_variant(int nt) {
   if (v < 0) {
     const char* e = getenv("EXPD_K1V");
     v = e ? atoi(e) : 0;
-    if (v != 2562 && v != 1282 && v != 2561) v = 0;
+    if (v != 2562 && v != 1282 && v != 2561 && v != 5123) v = 0;
   }
   if (v) return v;
   // default per Nt (measured, profiles/r01/k1_variants.txt): Nt = 128 runs best with
@@ -1008,7 +1241,35 @@ static cudaError_t launch_tma(const TimeArgs& a, int grid, cudaStream_t st) {
 }
 
 template <int NT, int RM, int OUTM, int NL>
+static cudaError_t launch_ring(const TimeArgs& a, int grid, cudaStream_t st) {
+  using PL = RingLayout<NT, NL>;
+  auto k = k_time_ring<NT, RM, OUTM, NL>;
+  static DevOnce attr;  // per instantiation and device
+  if (cudaError_t e = smem_optin(attr, k, PL::BYTES); e != cudaSuccess) return e;
+  constexpr int S = PL::S;
+  CUtensorMap mx, mn;
+  cudaError_t e = make_tmap_2d(&mx, a.X, (unsigned long long)a.npad, (unsigned long long)a.nt,
+                               (unsigned long long)a.npad * 8, 2 * S, NT);
+  if (e != cudaSuccess) return e;
+  mn = mx;
+  if (K1Form<NL>::HASN && (e = make_tmap_2d(&mn, a.Nh, (unsigned long long)a.npad, (unsigned long long)a.nt,
+                              (unsigned long long)a.npad * 8, 2 * S, NT)) != cudaSuccess)
+    return e;
+  k<<<(unsigned)grid, 512, PL::BYTES, st>>>(mx, mn, a);
+  return cudaGetLastError();
+}
+// the ring kernel takes full tiles only
+template <int NT>
+static bool ring_ok(long npairs) {
+  if constexpr (ring_capable<NT>()) return npairs % RingLayout<NT, 1>::S == 0;
+  return false;
+}
+
+template <int NT, int RM, int OUTM, int NL>
 static cudaError_t launch_t(const TimeArgs& a, int grid, cudaStream_t st) {
+  if constexpr (ring_capable<NT>()) {
+    if (pipe_mode() == 3 && k1_variant(NT) == 5123 && ring_ok<NT>(a.npairs)) return launch_ring<NT, RM, OUTM, NL>(a, grid, st);
+  }
   if constexpr (TimeGeo<NT>::L > 1 && NL >= 3) {  // BDF2 / complex: TMA or register kernel
     if (pipe_mode() == 3) {
       if (k1_variant(NT) == 1282) return launch_tma<NT, RM, OUTM, NL, 128, 2>(a, grid, st);

@@ -55,6 +55,7 @@ EXPORTS = [
     "expd_layout_query",
     "expd_a2a_schedule",
     "expd_a2a_schedule_keyed",
+    "expd_a2a_execute_host",
     "expd_nccl_unique_id",
     "expd_nccl_comm_init",
     "expd_nccl_comm_destroy",
@@ -91,6 +92,15 @@ class _Dist(C.Structure):
 class _Layout(C.Structure):
     _fields_ = [("rank", C.c_int), ("nranks", C.c_int), ("npad", C.c_long), ("mode_off", C.c_long),
                 ("mode_len", C.c_long), ("t0", C.c_int), ("nt_local", C.c_int)]
+
+
+_GroupFn = C.CFUNCTYPE(C.c_int, C.c_void_p)
+_SendFn = C.CFUNCTYPE(C.c_int, C.c_void_p, C.POINTER(C.c_double), C.c_long, C.c_int)
+
+
+class _Transport(C.Structure):
+    _fields_ = [("ctx", C.c_void_p), ("group_start", _GroupFn), ("send", _SendFn), ("recv", _SendFn),
+                ("group_end", _GroupFn)]
 
 
 class _Report(C.Structure):
@@ -146,6 +156,8 @@ def load_library(path: str = LIB_PATH):
                                          C.POINTER(C.c_long), C.POINTER(C.c_long), C.c_long]),
         "expd_a2a_schedule_keyed": (C.c_long, [C.POINTER(_Problem), C.c_int, C.c_int, C.c_int, C.c_int,
                                                C.POINTER(C.c_long), C.POINTER(C.c_long), C.c_long, C.c_int]),
+        "expd_a2a_execute_host": (C.c_int, [C.POINTER(_Problem), C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                             C.c_int, dp, dp, C.POINTER(_Transport)]),
         "expd_nccl_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),
         "expd_nccl_comm_init": (C.c_int, [C.POINTER(C.c_ubyte), C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
         "expd_nccl_comm_destroy": (None, [vp]),
@@ -233,6 +245,32 @@ def a2a_schedule(problem: Problem, rank: int, nranks: int, direction: int, shift
     lib.expd_a2a_schedule_keyed(C.byref(p), rank, nranks, direction, shift, s.ctypes.data_as(lp),
                                 r.ctypes.data_as(lp), n, w)
     return s, r
+
+
+def a2a_execute_host(problem: Problem, rank: int, nranks: int, direction: int, shift: int, src, dst,
+                     send, recv, group_start=None, group_end=None, s_lo: int = 0, s_hi: int = 1 << 30):
+    """Run this rank's all-to-all (expd_a2a_execute_host) on host float64 numpy arrays with a
+    Python transport: send(view, peer) / recv(view, peer) get numpy views of the message
+    buffers (valid until group_end() returns); group_start() / group_end() bracket a chunk.
+    The library selects, pairs and orders the messages exactly as on the GPU (NCCL)."""
+    import numpy as np
+
+    lib = load_library()
+    assert src.dtype == np.float64 and dst.dtype == np.float64 and src.flags.c_contiguous and dst.flags.c_contiguous
+
+    def view(ptr, n):
+        return np.ctypeslib.as_array(ptr, shape=(int(n),))
+
+    cb = [_GroupFn(lambda ctx: int(group_start() or 0) if group_start else 0),
+          _SendFn(lambda ctx, ptr, n, peer: int(send(view(ptr, n), int(peer)) or 0)),
+          _SendFn(lambda ctx, ptr, n, peer: int(recv(view(ptr, n), int(peer)) or 0)),
+          _GroupFn(lambda ctx: int(group_end() or 0) if group_end else 0)]
+    tr = _Transport(None, *cb)
+    dp = C.POINTER(C.c_double)
+    st = lib.expd_a2a_execute_host(C.byref(problem._c()), rank, nranks, direction, shift, s_lo, s_hi,
+                                   src.ctypes.data_as(dp), dst.ctypes.data_as(dp), C.byref(tr))
+    if st != EXPD_OK:
+        raise ExpdError(st, "expd_a2a_execute_host")
 
 
 class Comm:

@@ -1,6 +1,8 @@
 """Multi-GPU host logic on CPU: the mode-slab /
 time-slab partition and the all-to-all message schedules that libexpd.so executes with NCCL,
-checked here as data and executed with torch.distributed (gloo, world size 2 and 4).
+checked here as data and executed by the library's own all-to-all routine (the one the GPU
+sweep runs with NCCL) through a host transport over torch.distributed (gloo, world size 2
+and 4).
 
 The last test runs the whole distributed Picard / fixed-point schedule of one sweep --
 all-to-all U-hat to time slabs, stage 3 on the local slices, all-to-all N-hat back shifted
@@ -22,6 +24,7 @@ import torch.multiprocessing as mp
 
 import synth
 from paper_2603_04350_b200 import Problem, a2a_schedule, layout
+from paper_2603_04350_b200.expd import a2a_execute_host
 
 CASES = [("c1", None, None), ("c2", 15, 8), ("c3", 31, 16), ("c4", 7, 8), ("c5", 15, 16), ("c5", 2047, 256),
          ("c4", 255, 64)]
@@ -125,6 +128,47 @@ def run_schedule(sends, recvs, src: torch.Tensor, dst: torch.Tensor, rank: int):
         dst[do:do + c] = b
 
 
+class GlooTransport:
+    """expd_transport over torch.distributed (gloo): isend / irecv per message, tagged by the
+    message's position in its (sender, receiver) stream within the chunk; group_end waits
+    for every request and copies the received buffers into the library's destination views."""
+
+    def __init__(self):
+        self.reqs, self.pending, self.tags = [], [], {}
+
+    def group_start(self):
+        self.reqs, self.pending, self.tags = [], [], {}
+
+    def _tag(self, kind, peer):
+        t = self.tags.get((kind, peer), 0)
+        self.tags[(kind, peer)] = t + 1
+        return t
+
+    def send(self, view, peer):
+        self.reqs.append(dist.isend(torch.from_numpy(view.copy()), dst=peer, tag=self._tag("s", peer)))
+
+    def recv(self, view, peer):
+        b = torch.empty(len(view), dtype=torch.float64)
+        self.reqs.append(dist.irecv(b, src=peer, tag=self._tag("r", peer)))
+        self.pending.append((view, b))
+
+    def group_end(self):
+        for r in self.reqs:
+            r.wait()
+        for v, b in self.pending:
+            v[:] = b.numpy()
+
+
+def lib_a2a(prob, rank, P, direction, shift, src, dst, s_lo=0, s_hi=1 << 30):
+    """The library's all-to-all (expd_a2a_execute_host) on torch / numpy float64 buffers."""
+    tr = GlooTransport()
+    s = np.ascontiguousarray(src.numpy() if isinstance(src, torch.Tensor) else src)
+    d = dst.numpy() if isinstance(dst, torch.Tensor) else dst
+    assert d.flags.c_contiguous
+    a2a_execute_host(prob, rank, P, direction, shift, s, d, tr.send, tr.recv, tr.group_start, tr.group_end,
+                     s_lo=s_lo, s_hi=s_hi)
+
+
 def _spawn(fn, P, *args):
     port = _free_port()
     mp.spawn(fn, args=(P, port) + args, nprocs=P, join=True)
@@ -147,14 +191,17 @@ def _a2a_worker(rank, P, port, name, n, nt):
         # mode slab -> time slab
         mode = G[:, off:off + ln].contiguous().reshape(-1)
         time = torch.full((ntl * npad,), float("nan"), dtype=torch.float64)
-        s, r = a2a_schedule(prob, rank, P, 0, 0)
-        run_schedule(s, r, mode, time, rank)
+        lib_a2a(prob, rank, P, 0, 0, mode, time)
         assert torch.equal(time.reshape(ntl, npad), G[t0:t0 + ntl])
         # time slab -> mode slab, shifted one slice (the N-hat exchange)
         back = torch.zeros(((cfg.nt + 1) * ln,), dtype=torch.float64)
-        s, r = a2a_schedule(prob, rank, P, 1, 1)
-        run_schedule(s, r, time, back, rank)
+        lib_a2a(prob, rank, P, 1, 1, time, back)
         assert torch.equal(back.reshape(cfg.nt + 1, ln)[1:], G[:, off:off + ln])
+        # the test-side executor of the message lists agrees with the library's
+        time2 = torch.full((ntl * npad,), float("nan"), dtype=torch.float64)
+        s, r = a2a_schedule(prob, rank, P, 0, 0)
+        run_schedule(s, r, mode, time2, rank)
+        assert torch.equal(time2, time)
     finally:
         dist.destroy_process_group()
 
@@ -203,21 +250,19 @@ def _dist_picard_worker(rank, P, port, name, n, nt, out_dir):
         Nh = np.zeros((cfg.nt + 1, ln))
         if nl:
             Nh[0] = _pad(oracle.dst(s, oracle.nonlin(s, u0))[None], cfg)[0][off:off + ln]
-        m2t = a2a_schedule(prob, rank, P, 0, 0)
-        t2m1 = a2a_schedule(prob, rank, P, 1, 1)
         hist, r0 = [], None
         for k in range(60):
             if nl:  # stage 3 on the time slab
-                UT = torch.zeros(ntl * npad, dtype=torch.float64)
-                run_schedule(*m2t, torch.from_numpy(Uh.reshape(-1).copy()), UT, rank)
-                UT = UT.numpy().reshape(ntl, npad)
+                UT = np.zeros(ntl * npad)
+                lib_a2a(prob, rank, P, 0, 0, Uh.reshape(-1), UT)
+                UT = UT.reshape(ntl, npad)
                 NT = np.zeros((ntl, npad))
                 for i in range(ntl):
                     uh = _unpad(UT[i], cfg)
                     NT[i] = _pad(oracle.dst(s, oracle.nonlin(s, oracle.dst(s, uh)))[None], cfg)[0]
-                nh = torch.from_numpy(Nh.reshape(-1).copy())
-                run_schedule(*t2m1, torch.from_numpy(NT.reshape(-1)), nh, rank)
-                Nh = nh.numpy().reshape(cfg.nt + 1, ln)
+                nh = Nh.reshape(-1).copy()
+                lib_a2a(prob, rank, P, 1, 1, NT.reshape(-1), nh)
+                Nh = nh.reshape(cfg.nt + 1, ln)
             rn2 = 0.0
             for e in modes:  # K1 on the mode slab: residual, ||r||^2, preconditioner, update
                 c = e - off
@@ -234,9 +279,9 @@ def _dist_picard_worker(rank, P, port, name, n, nt, out_dir):
             hist.append(rn / r0)
             if hist[-1] < cfg.tol:
                 break
-        UT = torch.zeros(ntl * npad, dtype=torch.float64)
-        run_schedule(*m2t, torch.from_numpy(Uh.reshape(-1).copy()), UT, rank)
-        U = np.stack([oracle.dst(s, _unpad(x, cfg)) for x in UT.numpy().reshape(ntl, npad)])
+        UT = np.zeros(ntl * npad)
+        lib_a2a(prob, rank, P, 0, 0, Uh.reshape(-1), UT)
+        U = np.stack([oracle.dst(s, _unpad(x, cfg)) for x in UT.reshape(ntl, npad)])
         np.save(os.path.join(out_dir, f"U{rank}.npy"), U)
         np.save(os.path.join(out_dir, f"hist{rank}.npy"), np.array(hist))
     finally:
@@ -306,6 +351,15 @@ def _chunked_worker(rank, P, port, name, n, nt, k):
         for lo, hi in chunks:  # then chunk by chunk back, after "stage 3" of the chunk
             run_schedule(sel(s1, lo, hi), sel(r1, lo, hi), time, back, rank)
         assert torch.equal(back.reshape(cfg.nt + 1, ln)[1:], G[:, off:off + ln])
+        # the library's chunked execution (slice-key ranges, expd_api.cu stage3_dist's order)
+        time2 = torch.full((ntl * npad,), float("nan"), dtype=torch.float64)
+        back2 = torch.zeros(((cfg.nt + 1) * ln,), dtype=torch.float64)
+        for lo, hi in chunks:
+            lib_a2a(prob, rank, P, 0, 0, mode, time2, lo, hi)
+        assert torch.equal(time2, time)
+        for lo, hi in chunks:
+            lib_a2a(prob, rank, P, 1, 1, time2, back2, lo, hi)
+        assert torch.equal(back2, back)
     finally:
         dist.destroy_process_group()
 
