@@ -1204,8 +1204,10 @@ static int k1_variant(int nt) {
     if (v != 2562 && v != 1282 && v != 2561 && v != 5123) v = 0;
   }
   if (v) return v;
-  // default per Nt (measured, profiles/r01/k1_variants.txt): Nt = 128 runs best with
-  // 128-thread CTAs of 8 pairs (more resident CTAs hide the TMA latency), else 2562
+  // default per Nt (measured): Nt = 256 the ring of two warp groups (c5 K1 6.69 -> 6.02 ms,
+  // profiles/r02/), Nt = 128 128-thread CTAs of 8 pairs (more resident CTAs hide the TMA
+  // latency), else 2562; the ring falls back to 2562 for partial tiles
+  if (nt == 256) return 5123;
   return nt == 128 ? 1282 : 2562;
 }
 static bool use_pipe() { return pipe_mode() > 0; }
