@@ -482,18 +482,6 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
         *reinterpret_cast<double2*>(cb + M * 8 + off) = make_double2(out[2 * l].y, out[2 * l + 1].y);
       }
     } else {
-#ifndef EXPD_COL_COMPACT
-      // straight into the [row][G] layout the TMA store reads, 128-byte swizzled (the output
-      // map has CU_TENSOR_MAP_SWIZZLE_128B): thread (g, j)'s 2L consecutive rows are 16 B x G
-      // apart, which the swizzle spreads over 4 bank groups per quarter warp (2-way instead of
-      // the linear layout's 8-way conflict) -- no padded round trip and compaction
-#pragma unroll
-      for (int q = 0; q < 2 * L; ++q) {
-        uint32_t off = (uint32_t)(((2 * j * L + q) * G + g) * 16);
-        off ^= ((off >> 7) & 7u) << 4;
-        *reinterpret_cast<double2*>(cb + off) = out[q];
-      }
-#else
       // chunk -> padded layout (conflict free), then compact in place to the linear [row][G]
       // layout the TMA store reads; thread (g, j) moves positions j + T r of pair g
 #pragma unroll
@@ -505,7 +493,6 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
       __syncthreads();
 #pragma unroll
       for (int r = 0; r < R0; ++r) buf[(j + T * r) * G + g] = c[r];
-#endif
     }
     fence_proxy_async_smem();
     __syncthreads();
@@ -595,10 +582,10 @@ static cudaError_t axis_map(CUtensorMap* m, const Geom& g, int ax, const double*
   const cuuint64_t s[3] = {M * 8, n * M * 8, sl};
   if (ax == AX_COL_Y) {
     const cuuint32_t b[4] = {(cuuint32_t)(2 * G), (cuuint32_t)CBR, 1, 1};
-    return make_map(m, ptr, d, s, b, sw);
+    return make_map(m, ptr, d, s, b, false);
   }
   const cuuint32_t b[4] = {(cuuint32_t)(2 * G), 1, (cuuint32_t)CBR, 1};
-  return make_map(m, ptr, d, s, b, sw);
+  return make_map(m, ptr, d, s, b, false);
 }
 
 static int sm_count() {
@@ -607,14 +594,6 @@ static int sm_count() {
   cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
   return n > 0 ? n : 148;
 }
-
-// strided-axis results go into a 128B-swizzled store box (default) or, built with
-// -DEXPD_COL_COMPACT, through the padded layout and a compaction into a linear one
-#ifndef EXPD_COL_COMPACT
-static bool col_swizzle() { return true; }
-#else
-static bool col_swizzle() { return false; }
-#endif
 
 template <int M, int AX, bool NL, int G, int NBUF>
 static cudaError_t launch_line(const Geom& g, const DstTables& t, const Poly& P, const double* in, double* out,
@@ -625,10 +604,9 @@ static cudaError_t launch_line(const Geom& g, const DstTables& t, const Poly& P,
   int per_sm = 1;
   if (cudaError_t e = smem_optin(once, k, D::SMEM, D::THREADS, &per_sm); e != cudaSuccess) return e;
   CUtensorMap mi, mo;
-  const bool colswz = AX != AX_ROW && col_swizzle();
   cudaError_t e = axis_map(&mi, g, AX, in, nslices, G, /*sw=*/false);
   if (e != cudaSuccess) return e;
-  if ((e = axis_map(&mo, g, AX, out, nslices, G, /*sw=*/AX == AX_ROW || colswz)) != cudaSuccess) return e;
+  if ((e = axis_map(&mo, g, AX, out, nslices, G, /*sw=*/AX == AX_ROW)) != cudaSuccess) return e;
   LineArgs a{};
   const int rows = (int)(g.npad / g.M);
   if (AX == AX_ROW) {

@@ -4,9 +4,9 @@
 tag=${1:-r02d}
 O=gpurun_out; mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/${tag}_build.log 2>&1 || { echo BUILD FAILED; exit 1; }
-bash tools/build_variant.sh k_line.cu /tmp/libexpd_compact.so -DEXPD_COL_COMPACT > $O/${tag}_variant.log 2>&1 || echo VARIANT BUILD FAILED
+
 timeout 1800 python -m pytest tests -q -m gpu -p no:cacheprovider > $O/${tag}_pytest_gpu.log 2>&1; echo "pytest gpu exit $?"; tail -3 $O/${tag}_pytest_gpu.log
-for lib in default compact default compact; do
+for lib in default default; do
   if [ $lib = compact ]; then export EXPD_LIB=/tmp/libexpd_compact.so; else unset EXPD_LIB; fi
   timeout 600 python bench.py --no-cpu --no-e2e > $O/${tag}_bench_$lib.json 2>$O/${tag}_bench_$lib.err
   python -c "
