@@ -508,6 +508,279 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
 }
 
 // ---------------------------------------------------------------------------------------
+// k_line2: the M = 2048 line transform with TWO threads per radix-16 job (256 threads per
+// line pair).  Same arithmetic and data layout as k_line (sinft pre-processing, complex FFT
+// 16 x 16 x 8 of the two packed lines, Hermitian unpack on partner jobs, prefix sum), but a
+// thread holds 8 complex values instead of 16: each radix-16 DFT is split by decimation in
+// time into the DFT-8 of the even inputs (lane half h = 0) and of the odd inputs (h = 1),
+// joined by one register exchange with the partner lane (lane ^ 16, four complex values) and
+// the last radix-2 butterfly; the Hermitian partner jobs (ja, jb) of the last stage sit in
+// the same two lanes.  Half the registers per thread -> twice the resident warps per SM for
+// the latency-bound transform (k_line: 168 registers, 12 warps per SM).
+// Lane mapping inside a warp w: h = lane >> 4, job j = 16 w + (lane & 15): each half warp
+// reads one contiguous run of a stage's inputs.
+// ---------------------------------------------------------------------------------------
+struct L2Geo {
+  static constexpr int M = 2048, T = 256, RL = 8, NSL = M / RL;  // last stage: 256 jobs of 8
+  static constexpr int L = (M / 2) / T;                           // k-values per thread (4)
+  static constexpr int PADP = 16;
+  static constexpr int SW = M + M / PADP;                         // padded positions
+  static constexpr size_t BUFB = ((size_t)SW * 16 + 1023) / 1024 * 1024;
+  static constexpr int NW = T / 32;
+};
+template <int NBUF>
+constexpr size_t line2_smem() {
+  return 1024 + NBUF * L2Geo::BUFB + 16 * L2Geo::NW + 16;
+}
+#ifndef EXPD_LINE2_MINB
+#define EXPD_LINE2_MINB 2
+#endif
+
+// W / E arrays of the unpack without padding: a 2-bit XOR inside each 8-entry block makes
+// the prefix reads (thread t: entries 4t .. 4t+3) conflict free
+__device__ __forceinline__ int l2we(int k) { return k ^ ((k >> 3) & 3); }
+
+// the partner lane's value (lane ^ 16)
+__device__ __forceinline__ double2 xch16(double2 v) {
+  return make_double2(__shfl_xor_sync(0xffffffffu, v.x, 16), __shfl_xor_sync(0xffffffffu, v.y, 16));
+}
+
+// Two-lane radix-16 DFT (DIR = -1, X_k = sum_r x_r W16^{rk}), in place: this lane holds
+// x_{2m+h} (m = 0..7) in v; on return v[q] = X_{4h+q}, v[4+q] = X_{4h+q+8} (q = 0..3).
+__device__ __forceinline__ void dft16_2lane(double2 (&v)[8], int h) {
+  DFT<8, -1>::run(v);  // h = 0: E_k = DFT8(x_even), h = 1: O_k = DFT8(x_odd)
+  // h = 1: O'_k = W16^k O_k (compile-time twiddles; the select keeps the warp converged)
+  sfor<8>([&](auto kk) {
+    constexpr int k = decltype(kk)::value;
+    double2 t = v[k];
+    twid<k, 16, -1>(t);
+    v[k] = h ? t : v[k];
+  });
+  // h = 0 keeps E_0..3 and needs O'_0..3; h = 1 keeps O'_4..7 and needs E_4..7
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const double2 give = h ? v[q] : v[4 + q];
+    const double2 got = xch16(give);
+    const double2 E = h ? got : v[q];
+    const double2 Op = h ? v[4 + q] : got;
+    v[q] = cadd(E, Op);
+    v[4 + q] = csub(E, Op);
+  }
+}
+
+template <int AX, bool NL, int NBUF>
+__global__ void __launch_bounds__(L2Geo::T, EXPD_LINE2_MINB)
+    k_line2(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
+            const __grid_constant__ LineArgs a) {
+  using D = L2Geo;
+  constexpr int M = D::M, T = D::T, L = D::L, NSL = D::NSL, PADP = D::PADP;
+  extern __shared__ unsigned char lsm2_raw[];
+  char* base = reinterpret_cast<char*>(lsm2_raw + ((1024u - (smem_u32(lsm2_raw) & 1023u)) & 1023u));
+  double2* wt = reinterpret_cast<double2*>(base + NBUF * D::BUFB);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wt + D::NW);
+  const int tid = threadIdx.x;
+  __builtin_assume(tid < T);
+  const int lane = tid & 31, w = tid >> 5;
+  const int h = lane >> 4;                   // half of the radix-16 job / partner job
+  const int j = (w << 4) | (lane & 15);      // stage-0 / middle job, partner-pair index
+  const int pj = j;
+  const int ja = pj, jb = pj == 0 ? NSL / 2 : NSL - pj;
+  const int J = h ? jb : ja;                 // this lane's last-stage job
+
+  if (tid == 0) {
+    prefetch_tmap(&in_map);
+    prefetch_tmap(&out_map);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  long item = blockIdx.x;
+  if (tid == 0 && item < a.nitems) line_issue_load<M, AX, 1>(&in_map, a, item, base, &bar[0]);
+
+  for (int it = 0; item < a.nitems; ++it, item += gridDim.x) {
+    const int cur = NBUF == 2 ? (it & 1) : 0;
+    char* cb = base + cur * D::BUFB;
+    double2* buf = reinterpret_cast<double2*>(cb);
+    const long next = item + gridDim.x;
+    if (NBUF == 2 && tid == 0 && next < a.nitems) {
+      bulk_wait_read0();
+      line_issue_load<M, AX, 1>(&in_map, a, next, base + (cur ^ 1) * D::BUFB, &bar[cur ^ 1]);
+    }
+    const double2* tw = a.tw;
+    const double* pa = a.pa;
+    asm volatile("" : "+l"(tw), "+l"(pa));
+#ifndef EXPD_LINE2_LAZY_A
+    double pre_a[8];  // loaded before the TMA wait (their latency hides behind it)
+#pragma unroll
+    for (int m = 0; m < 8; ++m) pre_a[m] = __ldg(pa + j + 128 * (2 * m + h));
+#define L2_PRE_A(m) pre_a[m]
+#else
+#define L2_PRE_A(m) __ldg(pa + j + 128 * (2 * (m) + h))
+#endif
+    const double2 tmid = __ldg(tw + (j & 15) * 8);  // middle stage (NS = 16): w^{(j mod 16) M/256}
+    const double2 tlast = __ldg(tw + J);
+    mbar_wait(&bar[cur], (uint32_t)((NBUF == 2 ? (it >> 1) : it) & 1));
+
+    double2 out[2 * L];
+    int npass = NL ? 2 : 1;
+    asm volatile("" : "+r"(npass));
+#pragma unroll 1
+    for (int pass = 0; pass < npass; ++pass) {
+      // ---- stage 0: pre-processing + two-lane radix 16 over i = j + 128 r ------------
+      double2 v[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const int i = j + 128 * (2 * m + h);
+        if (i == 0) {
+          v[m] = make_double2(0.0, 0.0);
+        } else if (AX == AX_ROW) {
+          const uint32_t o1 = (uint32_t)(i - 1) * 8u, o2 = (uint32_t)(M - i - 1) * 8u;
+          const double2 z = make_double2(*reinterpret_cast<const double*>(cb + o1),
+                                         *reinterpret_cast<const double*>(cb + M * 8 + o1));
+          const double2 zm = make_double2(*reinterpret_cast<const double*>(cb + o2),
+                                          *reinterpret_cast<const double*>(cb + M * 8 + o2));
+          v[m] = lpre(z, zm, L2_PRE_A(m), a.c);
+        } else {
+          const int p1 = i - 1, p2 = M - i - 1;
+          const int q1 = pass ? lswz<PADP>(p1) : p1, q2 = pass ? lswz<PADP>(p2) : p2;
+          v[m] = lpre(buf[q1], buf[q2], L2_PRE_A(m), a.c);
+        }
+      }
+      dft16_2lane(v, h);
+      __syncthreads();  // stage-0 reads of buf done
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        buf[lswz<PADP>(j * 16 + 4 * h + q)] = v[q];
+        buf[lswz<PADP>(j * 16 + 4 * h + 8 + q)] = v[4 + q];
+      }
+      __syncthreads();
+      // ---- middle stage (radix 16, NS = 16): inputs jm + 128 r, twiddle w^{r (jm mod 16) 8}
+#pragma unroll
+      for (int m = 0; m < 8; ++m) v[m] = buf[lswz<PADP>(j + 128 * (2 * m + h))];
+      {
+        const double2 w2 = cmul(tmid, tmid);
+        double2 tp = h ? tmid : make_double2(1.0, 0.0);  // w^{(2m + h) b}
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          if (m > 0 || h) v[m] = cmul(v[m], tp);
+          if (m + 1 < 8) tp = cmul(tp, w2);
+        }
+      }
+      dft16_2lane(v, h);
+      __syncthreads();
+      {
+        const int mbase = (j >> 4) * 256 + (j & 15);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          buf[lswz<PADP>(mbase + 16 * (4 * h + q))] = v[q];
+          buf[lswz<PADP>(mbase + 16 * (4 * h + 8 + q))] = v[4 + q];
+        }
+      }
+      __syncthreads();
+      // ---- last stage (radix 8, NS = 256) on this lane's job J ------------------------
+#pragma unroll
+      for (int r = 0; r < 8; ++r) v[r] = buf[lswz<PADP>(J + NSL * r)];
+#ifdef EXPD_LINE2_TWSEQ
+      {  // running product: two live twiddles (register-light, 7 roundings deep)
+        double2 tp = tlast;
+#pragma unroll
+        for (int r = 1; r < 8; ++r) {
+          v[r] = cmul(v[r], tp);
+          if (r + 1 < 8) tp = cmul(tp, tlast);
+        }
+      }
+#else
+      ltwmul_w<8>(tlast, v);
+#endif
+      DFT<8, -1>::run(v);
+      __syncthreads();  // every read of buf done: the unpack arrays overwrite it
+      // ---- Hermitian unpack: k = J + 256 r pairs with M - k = partner's J' + 256 (7 - r)
+      {
+        double2 rcv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) rcv[q] = xch16(v[4 + q]);
+        double2* Wb = buf;
+        double2* Eb = buf + M / 2;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const int k = J + NSL * r;
+          const double2 own = pj == 0 ? (h == 0 ? v[(8 - r) & 7] : v[7 - r]) : rcv[3 - r];
+          double2 e, wv;
+          lunpack(v[r], own, h == 0 && pj == 0 && r == 0, e, wv);
+          if (k >= 1) Eb[l2we(k - 1)] = e;  // E[k - 1] = e_k, k = 1 .. M/2 - 1
+          Wb[l2we(k)] = wv;
+        }
+      }
+      __syncthreads();
+      // ---- prefix sum: thread t owns k in [4t, 4t + 4) -> positions [8t, 8t + 8) --------
+      double2 tot = make_double2(0.0, 0.0);
+      {
+        const double2* Wb = buf;
+        const double2* Eb = buf + M / 2;
+#pragma unroll
+        for (int l = 0; l < L; ++l) {
+          const int k = 4 * tid + l;
+          tot = cadd(tot, Wb[l2we(k)]);
+          out[2 * l] = tot;
+          out[2 * l + 1] = (k == M / 2 - 1) ? make_double2(0.0, 0.0) : Eb[l2we(k)];  // e_{k+1}
+        }
+      }
+      double2 inc = tot;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const double ox = __shfl_up_sync(0xffffffffu, inc.x, d);
+        const double oy = __shfl_up_sync(0xffffffffu, inc.y, d);
+        if (lane >= d) inc = cadd(inc, make_double2(ox, oy));
+      }
+      double2 off = csub(inc, tot);
+      if (lane == 31) wt[w] = inc;
+      __syncthreads();
+      for (int b = 0; b < w; ++b) off = cadd(off, wt[b]);
+#pragma unroll
+      for (int l = 0; l < L; ++l) out[2 * l] = cadd(out[2 * l], off);
+      if (NL && pass + 1 < npass) {
+        __syncthreads();  // the (e, w) reads are done
+#pragma unroll
+        for (int q = 0; q < 2 * L; ++q)
+          buf[lswz<PADP>(8 * tid + q)] = make_double2(poly_eval(a.poly, out[q].x), poly_eval(a.poly, out[q].y));
+        __syncthreads();
+      }
+    }
+    __syncthreads();  // (e, w) reads and the cross-warp offsets done before the output
+    if constexpr (AX == AX_ROW) {
+#pragma unroll
+      for (int l = 0; l < L; ++l) {
+        const int x = 8 * tid + 2 * l;
+        const uint32_t off = row_sw(x);
+        *reinterpret_cast<double2*>(cb + off) = make_double2(out[2 * l].x, out[2 * l + 1].x);
+        *reinterpret_cast<double2*>(cb + M * 8 + off) = make_double2(out[2 * l].y, out[2 * l + 1].y);
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 2 * L; ++q) buf[lswz<PADP>(8 * tid + q)] = out[q];
+      __syncthreads();
+      double2 c[8];
+#pragma unroll
+      for (int r = 0; r < 8; ++r) c[r] = buf[lswz<PADP>(tid + T * r)];
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < 8; ++r) buf[tid + T * r] = c[r];
+    }
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      line_issue_store<M, AX, 1>(&out_map, a, item, cb);
+      if (NBUF == 1 && next < a.nitems) {
+        bulk_wait_read0();
+        line_issue_load<M, AX, 1>(&in_map, a, next, base, &bar[0]);
+      }
+    }
+  }
+  if (tid == 0) bulk_wait0();
+}
+
+// ---------------------------------------------------------------------------------------
 // host side: tensor maps and launches
 // ---------------------------------------------------------------------------------------
 typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -665,9 +938,58 @@ static cudaError_t launch_col(const Geom& g, const DstTables& t, const Poly& P, 
   }
 }
 
+template <int AX, bool NL, int NBUF>
+static cudaError_t launch_line2(const Geom& g, const DstTables& t, const Poly& P, const double* in, double* out,
+                                long nslices, cudaStream_t st) {
+  auto k = k_line2<AX, NL, NBUF>;
+  constexpr size_t SMEM = line2_smem<NBUF>();
+  static DevOnce once;  // per instantiation and device
+  int per_sm = 1;
+  if (cudaError_t e = smem_optin(once, k, SMEM, L2Geo::T, &per_sm); e != cudaSuccess) return e;
+  CUtensorMap mi, mo;
+  cudaError_t e = axis_map(&mi, g, AX, in, nslices, 1, /*sw=*/false);
+  if (e != cudaSuccess) return e;
+  if ((e = axis_map(&mo, g, AX, out, nslices, 1, /*sw=*/AX == AX_ROW)) != cudaSuccess) return e;
+  LineArgs a{};
+  const int rows = (int)(g.npad / g.M);
+  if (AX == AX_ROW) {
+    a.inner = (rows + 1) / 2;
+    a.per_slice = a.inner;
+  } else {
+    a.inner = g.M / 2;
+    a.per_slice = a.inner * (g.dim == 3 ? g.n : 1);
+  }
+  a.rows = rows;
+  a.nitems = (long)a.per_slice * nslices;
+  a.tw = t.tw;
+  a.pa = t.pa;
+  a.c = 0.5 * sqrt(2.0 / (double)g.M);
+  a.poly = P;
+  long grid = (long)sm_count() * per_sm;
+  if (grid > a.nitems) grid = a.nitems;
+  if (grid < 1) return cudaSuccess;
+  k<<<(unsigned)grid, L2Geo::T, SMEM, st>>>(mi, mo, a);
+  return cudaGetLastError();
+}
+// EXPD_LINE2=0 keeps the one-thread-per-job k_line at M = 2048
+static bool use_line2() {
+  const char* e = getenv("EXPD_LINE2");
+  return !(e && e[0] == '0');
+}
+
 template <int M>
 static cudaError_t line_pass_m(const Geom& g, const DstTables& t, const Poly& P, int ax, bool nl, const double* in,
                                double* out, long nslices, cudaStream_t st) {
+  if constexpr (M == 2048) {
+    if (use_line2()) {
+      if (ax == AX_ROW) return launch_line2<AX_ROW, false, 2>(g, t, P, in, out, nslices, st);
+      if (ax == AX_COL_Y)
+        return nl ? launch_line2<AX_COL_Y, true, 2>(g, t, P, in, out, nslices, st)
+                  : launch_line2<AX_COL_Y, false, 2>(g, t, P, in, out, nslices, st);
+      return nl ? launch_line2<AX_COL_Z, true, 2>(g, t, P, in, out, nslices, st)
+                : launch_line2<AX_COL_Z, false, 2>(g, t, P, in, out, nslices, st);
+    }
+  }
   if (ax == AX_ROW) {
     static int rv = -1;  // EXPD_ROWV=1: one buffer per CTA (more CTAs per SM)
     if (rv < 0) {
