@@ -515,8 +515,12 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
 // time into the DFT-8 of the even inputs (lane half h = 0) and of the odd inputs (h = 1),
 // joined by one register exchange with the partner lane (lane ^ 16, four complex values) and
 // the last radix-2 butterfly; the Hermitian partner jobs (ja, jb) of the last stage sit in
-// the same two lanes.  Half the registers per thread -> twice the resident warps per SM for
-// the latency-bound transform (k_line: 168 registers, 12 warps per SM).
+// the same two lanes.  Half the registers per thread -> more resident warps per SM (16
+// instead of 12).  MEASURED SLOWER on c5 (profiles/r02/bench_line2_ab_*.json): x-passes
+// 7.53 -> 9.89 ms, fused y-pass 8.17 -> 10.74 ms per sweep (3 CTAs/SM at 80 registers with
+// spills: 10.8 / 10.9): the line kernels are bound by the LSU data pipe (75 % busy with the
+// shared-memory wavefronts of the exchanges), not by latency, and the partner-lane shuffles
+// and selects add to it.  Kept as an opt-in record of the experiment (EXPD_LINE2=1).
 // Lane mapping inside a warp w: h = lane >> 4, job j = 16 w + (lane & 15): each half warp
 // reads one contiguous run of a stage's inputs.
 // ---------------------------------------------------------------------------------------
@@ -971,10 +975,10 @@ static cudaError_t launch_line2(const Geom& g, const DstTables& t, const Poly& P
   k<<<(unsigned)grid, L2Geo::T, SMEM, st>>>(mi, mo, a);
   return cudaGetLastError();
 }
-// EXPD_LINE2=0 keeps the one-thread-per-job k_line at M = 2048
+// EXPD_LINE2=1 selects k_line2 at M = 2048 (measured slower than k_line, see above)
 static bool use_line2() {
   const char* e = getenv("EXPD_LINE2");
-  return !(e && e[0] == '0');
+  return e && e[0] == '1';
 }
 
 template <int M>
