@@ -484,16 +484,23 @@ def run_ours(args):
             tprof = json.load(open(os.path.join(ROOT, "profiles", "ncu_traffic.json")))
         except Exception:
             tprof = {}
-        for label, key, nkey, flops, slices in (("line_x", "x_ms", "x_launches", f_t, 2 * s3),
-                                                ("line_y_nl", "fused_ms", "fused_launches", f_nl, s3)):
+        persistent = passes[-1]["x_launches"] == 0 and passes[-1]["fused_launches"] >= 1
+        fams = ((("stage3_persistent", "fused_ms", "fused_launches", 2 * f_t + f_nl, s3),) if persistent else
+                (("line_x", "x_ms", "x_launches", f_t, 2 * s3), ("line_y_nl", "fused_ms", "fused_launches", f_nl, s3)))
+        for label, key, nkey, flops, slices in fams:
             ms_sweep = statistics.mean(p_[key] for p_ in passes)
             nlaunch = passes[-1][nkey]
             tf = flops * slices / (ms_sweep * 1e-3) / 1e12
-            fam[label] = {"bound": "alu", "kernel": f"k_line ({label}: {'x-axis DST-I' if label == 'line_x' else 'fused y [V, N(u), V]'})",
+            kname = {"line_x": "k_line (line_x: x-axis DST-I)", "line_y_nl": "k_line (line_y_nl: fused y [V, N(u), V])",
+                     "stage3_persistent": "k_stage3p (persistent stage 3: x-IDST -> fused y [V, N(u), V] -> x-DST, "
+                                          "intermediate in an L2-resident ring)"}[label]
+            fam[label] = {"bound": "alu", "kernel": kname,
                           "achieved": tf, "peak": FP64_PEAK_TFLOPS,
                           "peak_source": "measured DFMA loop (profiles/r01_probe_fp64_hbm.txt)", "unit": "TFLOP/s",
                           "frac": tf / FP64_PEAK_TFLOPS, "traffic": tprof.get(f"{cfg.name}:{label}"),
-                          "traffic_note": "ncu dram bytes of one 16-slice launch",
+                          "traffic_note": ("ncu dram bytes of the one launch per sweep" if persistent else
+                                           "ncu dram bytes of one 16-slice launch"),
+                          "hbm_gbs": 16.0 * cfg.N * slices / (ms_sweep * 1e-3) / 1e9 if persistent else None,
                           "ncu": (tprof.get("counters") or {}).get(f"{cfg.name}:{label}"),
                           "algorithmic_flops_per_launch": flops * slices / max(nlaunch, 1),
                           "launch_ms": ms_sweep / max(nlaunch, 1), "launches_per_step": nlaunch,

@@ -237,7 +237,9 @@ expd_status expd_sweep_stage_ms(expd_plan* plan, double* ms_nonlin, double* ms_t
 /* Stage-3 pass times of the last sweep (set_profiling level 2, single-GPU nonlinear plans with
    the TMA line kernels): device ms summed over the sweep's x-passes, plain strided passes
    (3-D) and fused strided [V, N(u), V] passes, measured by CUDA events recorded on the
-   plan's stream between consecutive passes inside the sweep, and the launch counts.
+   plan's stream between consecutive passes inside the sweep, and the launch counts.  With
+   the persistent stage 3 (one launch carrying all passes, 2-D) the whole stage is reported
+   in ms_fused with n_fused = 1 and n_x = 0.
    UNSUPPORTED when no such timing exists.  Diagnostics for bench.py's per-kernel
    rooflines. */
 expd_status expd_sweep_pass_ms(expd_plan* plan, double* ms_x, double* ms_strided, double* ms_fused, int* n_x,

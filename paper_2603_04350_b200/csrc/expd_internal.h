@@ -128,7 +128,15 @@ struct PassTimer {
   int kind[512];
 };
 cudaError_t nonlin_slices(const Geom& g, const DstTables& t, const double* uhat, double* nhat, long nslices,
-                          int npoly, const double* q, double* scratch, cudaStream_t st, struct PassTimer* timer = nullptr);
+                          int npoly, const double* q, double* scratch, cudaStream_t st, struct PassTimer* timer = nullptr,
+                          void* s3ctl = nullptr);
+// persistent stage 3 (k_line.cu): one launch for all slices, intermediate in a ring of K
+// slices (ring: K npad doubles), dependency counters in ctl (stage3p_ctl_bytes(), zeroed by the
+// launch).  PassTimer kind 3 marks it.
+size_t stage3p_ctl_bytes();
+bool stage3p_supported(const Geom& g, long nslices);
+cudaError_t stage3p(const Geom& g, const DstTables& t, const Poly& P, const double* uhat, double* ring, int K,
+                    double* nhat, long nslices, void* ctl, cudaStream_t st);
 // N-hat = V N(u) for physical slices u (row stride n).
 cudaError_t nonlin_phys_slices(const Geom& g, const DstTables& t, const double* u, double* nhat, long nslices,
                                int npoly, const double* q, double* scratch, cudaStream_t st);

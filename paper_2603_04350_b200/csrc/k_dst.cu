@@ -619,6 +619,7 @@ int nonlin_chunk_slices(const Geom& g) {
 }
 
 int nonlin_kernel_launches(const Geom& g, long nslices) {
+  if (use_line(g) && nonlin_chunk_slices(g) >= 2 && stage3p_supported(g, nslices)) return 1;
   long chunk = nonlin_chunk_slices(g);
   long nch = (nslices + chunk - 1) / chunk;
   int per = g.dim == 1 ? 1 : (g.dim == 2 ? 3 : 5);
@@ -642,13 +643,28 @@ static cudaError_t mark(PassTimer* tm, int kind, cudaStream_t st) {
   return tm->ext ? cudaEventRecordWithFlags(e, st, cudaEventRecordExternal) : cudaEventRecord(e, st);
 }
 
+// ring slots of the persistent stage 3's intermediate (EXPD_S3P_K, default 4: 134 MB at c5)
+static int s3p_ring(long chunk) {
+  const char* e = getenv("EXPD_S3P_K");
+  long k = e ? atol(e) : 4;
+  if (k < 2) k = 2;
+  if (k > chunk) k = chunk;
+  return (int)k;
+}
+
 cudaError_t nonlin_slices(const Geom& g, const DstTables& t, const double* uhat, double* nhat, long nslices,
-                          int npoly, const double* q, double* scratch, cudaStream_t st, PassTimer* tm) {
+                          int npoly, const double* q, double* scratch, cudaStream_t st, PassTimer* tm, void* s3ctl) {
   Poly P = make_poly(npoly, q);
   const int rows_ps = (int)(g.N / g.n);
   const long chunk = nonlin_chunk_slices(g);
   const bool tl = use_line(g);
   if (tm) tm->used = 0;
+  if (tl && s3ctl && chunk >= 2 && stage3p_supported(g, nslices)) {
+    CK(mark(tm, 3, st));
+    CK(stage3p(g, t, P, uhat, scratch, s3p_ring(chunk), nhat, nslices, s3ctl, st));
+    CK(mark(tm, -1, st));
+    return cudaSuccess;
+  }
   for (long s0 = 0; s0 < nslices; s0 += chunk) {
     long ns = nslices - s0 < chunk ? nslices - s0 : chunk;
     const double* in = uhat + s0 * g.npad;

@@ -315,7 +315,8 @@ __device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* 
 // the persistent line kernel
 // ---------------------------------------------------------------------------------------
 template <int AX, int G>
-__device__ __forceinline__ void line_coords(const LineArgs& a, long item, int& c0, int& c1, int& c2, int& c3) {
+__device__ __forceinline__ void line_coords(const LineArgs& a, long item, int& c0, int& c1, int& c2, int& c3,
+                                            int smod = 0) {
   // 32-bit unsigned arithmetic (item counts stay far below 2^32): a 64-bit division is a
   // long software sequence on the issuing thread's critical path to the TMA
   const unsigned it = (unsigned)item, ps = (unsigned)a.per_slice;
@@ -330,13 +331,14 @@ __device__ __forceinline__ void line_coords(const LineArgs& a, long item, int& c
     else { c1 = o; c2 = 0; }
     c3 = (int)s;
   }
+  if (smod) c3 %= smod;  // a ring of smod slices (the persistent stage 3's intermediate)
 }
 
 template <int M, int AX, int G>
 __device__ __forceinline__ void line_issue_load(const CUtensorMap* map, const LineArgs& a, long item, char* buf,
-                                                uint64_t* bar) {
+                                                uint64_t* bar, int smod = 0) {
   int c0, c1, c2, c3;
-  line_coords<AX, G>(a, item, c0, c1, c2, c3);
+  line_coords<AX, G>(a, item, c0, c1, c2, c3, smod);
   mbar_arrive_expect_tx(bar, (uint32_t)(G * M * 16));
   if constexpr (AX == AX_ROW) {
     tma_load_4d(buf, map, bar, 0, 0, c2, c3);
@@ -354,9 +356,9 @@ __device__ __forceinline__ void line_issue_load(const CUtensorMap* map, const Li
 
 template <int M, int AX, int G>
 __device__ __forceinline__ void line_issue_store(const CUtensorMap* map, const LineArgs& a, long item,
-                                                 const char* buf) {
+                                                 const char* buf, int smod = 0) {
   int c0, c1, c2, c3;
-  line_coords<AX, G>(a, item, c0, c1, c2, c3);
+  line_coords<AX, G>(a, item, c0, c1, c2, c3, smod);
   if constexpr (AX == AX_ROW) {
     tma_store_4d(map, buf, 0, 0, c2, c3);
     if (c2 + 1 < a.rows) tma_store_4d(map, buf + M * 8, 0, 0, c2 + 1, c3);
@@ -371,46 +373,17 @@ __device__ __forceinline__ void line_issue_store(const CUtensorMap* map, const L
   bulk_commit();
 }
 
-// G line pairs per item, NBUF shared-memory buffers (2: the next item's TMA load overlaps
-// this item's transform; 1: overlap comes from the other CTAs on the SM).
-template <int M, int AX, bool NL, int G, int NBUF>
-__global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::MINB)
-    k_line(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
-           const __grid_constant__ LineArgs a) {
-  using D = LGeo<M, G, NBUF>;
-  static_assert(AX != AX_ROW || G == 1, "row items are one row pair");
+// The transform of one item (G line pairs) whose input the TMA is bringing into cb (arrival
+// on bar, phase parity): table values, the wait, [V] or [V, N, V], and the result written in
+// the layout the item's TMA store reads.  Every thread of the CTA calls it.
+template <int M, int AX, bool NL, int G>
+__device__ __forceinline__ void line_item(char* cb, double2* wt, const LineArgs& a, int my_pj, uint64_t* bar,
+                                          uint32_t parity) {
+  using D = LGeo<M, G, 1>;
   constexpr int R0 = D::R0, T = D::T, L = D::L, PADP = D::PADP;
-  extern __shared__ unsigned char lsm_raw[];
-  // 1 KB-aligned base as an offset from the __shared__ array (pointer arithmetic on the
-  // array keeps the shared address space: LDS/STS, not generic LD/ST)
-  char* base = reinterpret_cast<char*>(lsm_raw + ((1024u - (smem_u32(lsm_raw) & 1023u)) & 1023u));
-  double2* wt = reinterpret_cast<double2*>(base + NBUF * D::BUFB);
-  uint64_t* bar = reinterpret_cast<uint64_t*>(wt + D::NWB * G);
   const int tid = threadIdx.x;
-  __builtin_assume(tid < D::THREADS);
   const int g = tid % G, j = tid / G;
-  const int my_pj = partner_job<M, G>(tid);
-
-  if (tid == 0) {
-    prefetch_tmap(&in_map);
-    prefetch_tmap(&out_map);
-    mbar_init(&bar[0], 1);
-    mbar_init(&bar[1], 1);
-    mbar_fence_init();
-  }
-  __syncthreads();
-  long item = blockIdx.x;
-  if (tid == 0 && item < a.nitems) line_issue_load<M, AX, G>(&in_map, a, item, base, &bar[0]);
-
-  for (int it = 0; item < a.nitems; ++it, item += gridDim.x) {
-    const int cur = NBUF == 2 ? (it & 1) : 0;
-    char* cb = base + cur * D::BUFB;
-    double2* buf = reinterpret_cast<double2*>(cb);
-    const long next = item + gridDim.x;
-    if (NBUF == 2 && tid == 0 && next < a.nitems) {
-      bulk_wait_read0();  // the previous item's stores have left the other buffer
-      line_issue_load<M, AX, G>(&in_map, a, next, base + (cur ^ 1) * D::BUFB, &bar[cur ^ 1]);
-    }
+  double2* buf = reinterpret_cast<double2*>(cb);
     // the twiddle / sine tables are re-read every item: an opaque copy of the pointers keeps
     // the compiler from hoisting ~30 loop-invariant twiddles into registers for the whole loop
     const double2* tw = a.tw;
@@ -428,7 +401,7 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
       pre.ta = __ldg(tw + (pj < NSL / 2 ? pj : 0));
       pre.tb = __ldg(tw + (pj == 0 ? NSL / 2 : (pj < NSL / 2 ? NSL - pj : 0)));
     }
-    mbar_wait(&bar[cur], (uint32_t)((NBUF == 2 ? (it >> 1) : it) & 1));
+    mbar_wait(bar, parity);
 
     double2 out[2 * L];
     // NL: two passes [V, N, V] through ONE copy of the transform code (the trip count is
@@ -494,6 +467,49 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
 #pragma unroll
       for (int r = 0; r < R0; ++r) buf[(j + T * r) * G + g] = c[r];
     }
+}
+
+// G line pairs per item, NBUF shared-memory buffers (2: the next item's TMA load overlaps
+// this item's transform; 1: overlap comes from the other CTAs on the SM).
+template <int M, int AX, bool NL, int G, int NBUF>
+__global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::MINB)
+    k_line(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
+           const __grid_constant__ LineArgs a) {
+  using D = LGeo<M, G, NBUF>;
+  static_assert(AX != AX_ROW || G == 1, "row items are one row pair");
+  constexpr int R0 = D::R0, T = D::T, L = D::L, PADP = D::PADP;
+  extern __shared__ unsigned char lsm_raw[];
+  // 1 KB-aligned base as an offset from the __shared__ array (pointer arithmetic on the
+  // array keeps the shared address space: LDS/STS, not generic LD/ST)
+  char* base = reinterpret_cast<char*>(lsm_raw + ((1024u - (smem_u32(lsm_raw) & 1023u)) & 1023u));
+  double2* wt = reinterpret_cast<double2*>(base + NBUF * D::BUFB);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wt + D::NWB * G);
+  const int tid = threadIdx.x;
+  __builtin_assume(tid < D::THREADS);
+  const int g = tid % G, j = tid / G;
+  const int my_pj = partner_job<M, G>(tid);
+
+  if (tid == 0) {
+    prefetch_tmap(&in_map);
+    prefetch_tmap(&out_map);
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  long item = blockIdx.x;
+  if (tid == 0 && item < a.nitems) line_issue_load<M, AX, G>(&in_map, a, item, base, &bar[0]);
+
+  for (int it = 0; item < a.nitems; ++it, item += gridDim.x) {
+    const int cur = NBUF == 2 ? (it & 1) : 0;
+    char* cb = base + cur * D::BUFB;
+    double2* buf = reinterpret_cast<double2*>(cb);
+    const long next = item + gridDim.x;
+    if (NBUF == 2 && tid == 0 && next < a.nitems) {
+      bulk_wait_read0();  // the previous item's stores have left the other buffer
+      line_issue_load<M, AX, G>(&in_map, a, next, base + (cur ^ 1) * D::BUFB, &bar[cur ^ 1]);
+    }
+    line_item<M, AX, NL, G>(cb, wt, a, my_pj, &bar[cur], (uint32_t)((NBUF == 2 ? (it >> 1) : it) & 1));
     fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
@@ -505,6 +521,166 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
     }
   }
   if (tid == 0) bulk_wait0();
+}
+
+// ---------------------------------------------------------------------------------------
+// Persistent stage 3 (2-D; SURVEY §7 "Hard parts"): ONE launch carries
+// every slice through x-IDST -> fused y [V, N(u), V] -> x-DST with no kernel boundary.  The
+// CTAs take one of three roles by (blockIdx mod #SMs) -- the three CTAs of an SM share a role,
+// so an SM runs one code path -- and each role takes its items in slice order from its own
+// ticket counter.  Dependencies are per slice and counted in global memory: y(s) waits until
+// all x-IDST(s) items are stored, x-DST(s) until all y(s) items are, and x-IDST(s) until
+// ring slot s mod K of the intermediate is free (x-DST(s - K) stored).  The intermediate is
+// a ring of K slices (K x 33.5 MB at c5) that stays in the 126 MB L2, so HBM sees U-hat read
+// once and N-hat written once (16 B per dof) instead of three round trips per slice, and the
+// per-chunk launch tails disappear.  Progress: the pending item of the smallest slice always
+// has its dependencies met (every earlier item of the producer role has been taken by a
+// resident CTA, which finishes it without waiting), so the spin waits cannot deadlock for
+// K >= 2; a CTA that must wait first completes and signals its own pending store.
+// ---------------------------------------------------------------------------------------
+constexpr int kS3MaxSlices = 272;
+struct S3Ctl {
+  unsigned int ticket[4];
+  unsigned int done[3][kS3MaxSlices];
+};
+struct S3Args {
+  LineArgs row, col;  // item geometry of the x passes / the fused y pass (tables, poly shared)
+  S3Ctl* ctl;
+  int nslices, K, sms, split0, split1;
+};
+
+__device__ __forceinline__ unsigned ld_acquire_u32(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_proxy_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait1() { asm volatile("cp.async.bulk.wait_group 1;" ::: "memory"); }
+
+// sh: shared scratch of the issuing thread's state (keeps it out of the transform's registers):
+// sh[0], sh[1] next items (double-buffered broadcast), sh[2] current item, sh[3] pending
+// (stored, not yet signalled) item, sh[4] "current item's load issued", sh[5] "next issued"
+template <int M, int AX, bool NL>
+__device__ __forceinline__ void s3_role(const CUtensorMap* in_map, const CUtensorMap* out_map, const LineArgs& a,
+                                     const S3Args& s3, int pass, char* base, double2* wt, uint64_t* bar,
+                                     volatile long* sh, int my_pj) {
+  using D = LGeo<M, 1, 2>;
+  const int tid = threadIdx.x;
+  S3Ctl* ctl = s3.ctl;
+  const unsigned per = (unsigned)a.per_slice;
+  const unsigned total = per * (unsigned)s3.nslices;
+  const int K = s3.K;
+  const int smod_in = pass == 0 ? 0 : K, smod_out = pass == 2 ? 0 : K;
+  auto grab = [&]() -> long {
+    const unsigned t = atomicAdd(&ctl->ticket[pass], 1u);
+    return t < total ? (long)t : -1;
+  };
+  auto ready = [&](long item) -> bool {
+    const int s = (int)((unsigned)item / per);
+    if (pass == 0) return s < K || ld_acquire_u32(&ctl->done[2][s - K]) == per;
+    return ld_acquire_u32(&ctl->done[pass - 1][s]) == per;
+  };
+  auto signal = [&](long item) {
+    fence_proxy_async_global();
+    __threadfence();
+    atomicAdd(&ctl->done[pass][(unsigned)item / per], 1u);
+  };
+  if (tid == 0) {
+    const long item = grab();
+    sh[4] = 0;
+    if (item >= 0 && ready(item)) {
+      fence_proxy_async_global();
+      line_issue_load<M, AX, 1>(in_map, a, item, base, &bar[0], smod_in);
+      sh[4] = 1;
+    }
+    sh[2] = item;
+    sh[3] = -1;
+  }
+  __syncthreads();
+  for (int it = 0; sh[2] >= 0; ++it) {
+    const int cur = it & 1;
+    char* cb = base + cur * D::BUFB;
+    if (tid == 0) {
+      const long item = sh[2];
+      if (!sh[4]) {  // deferred: complete and signal our own pending store, then wait
+        if (sh[3] >= 0) {
+          bulk_wait0();
+          signal(sh[3]);
+          sh[3] = -1;
+        }
+        while (!ready(item)) __nanosleep(128);
+        fence_proxy_async_global();
+        line_issue_load<M, AX, 1>(in_map, a, item, cb, &bar[cur], smod_in);
+      }
+      const long nxt = grab();
+      bulk_wait_read0();  // the previous item's store has left the other buffer
+      sh[5] = 0;
+      if (nxt >= 0 && ready(nxt)) {
+        fence_proxy_async_global();
+        line_issue_load<M, AX, 1>(in_map, a, nxt, base + (cur ^ 1) * D::BUFB, &bar[cur ^ 1], smod_in);
+        sh[5] = 1;
+      }
+      sh[it & 1] = nxt;
+    }
+    line_item<M, AX, NL, 1>(cb, wt, a, my_pj, &bar[cur], (uint32_t)((it >> 1) & 1));
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      const long item = sh[2];
+      line_issue_store<M, AX, 1>(out_map, a, item, cb, smod_out);
+      if (sh[3] >= 0) {
+        bulk_wait1();  // the previous item's store is complete
+        signal(sh[3]);
+      }
+      sh[3] = item;
+      sh[4] = sh[5];
+      sh[2] = sh[it & 1];
+    }
+    __syncthreads();  // sh[2] (the next item) is visible
+  }
+  if (tid == 0) {
+    bulk_wait0();
+    if (sh[3] >= 0) signal(sh[3]);
+  }
+}
+
+template <int M>
+__global__ void __launch_bounds__(LGeo<M, 1, 2>::THREADS, LGeo<M, 1, 2>::MINB)
+    k_stage3p(const __grid_constant__ CUtensorMap m_u, const __grid_constant__ CUtensorMap m_trow_out,
+              const __grid_constant__ CUtensorMap m_tcol, const __grid_constant__ CUtensorMap m_trow_in,
+              const __grid_constant__ CUtensorMap m_n, const __grid_constant__ S3Args s3) {
+  using D = LGeo<M, 1, 2>;
+  extern __shared__ unsigned char s3sm_raw[];
+  char* base = reinterpret_cast<char*>(s3sm_raw + ((1024u - (smem_u32(s3sm_raw) & 1023u)) & 1023u));
+  double2* wt = reinterpret_cast<double2*>(base + 2 * D::BUFB);
+  uint64_t* bar = reinterpret_cast<uint64_t*>(wt + D::NWB);
+  __shared__ long sh[6];
+  const int tid = threadIdx.x;
+  const int my_pj = partner_job<M, 1>(tid);
+  const int b = (int)(blockIdx.x % (unsigned)s3.sms);
+  const int role = b < s3.split0 ? 0 : (b < s3.split0 + s3.split1 ? 1 : 2);
+  if (tid == 0) {
+    mbar_init(&bar[0], 1);
+    mbar_init(&bar[1], 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  if (role == 0) {
+    if (tid == 0) {
+      prefetch_tmap(&m_u);
+      prefetch_tmap(&m_trow_out);
+    }
+    s3_role<M, AX_ROW, false>(&m_u, &m_trow_out, s3.row, s3, 0, base, wt, bar, sh, my_pj);
+  } else if (role == 1) {
+    if (tid == 0) prefetch_tmap(&m_tcol);
+    s3_role<M, AX_COL_Y, true>(&m_tcol, &m_tcol, s3.col, s3, 1, base, wt, bar, sh, my_pj);
+  } else {
+    if (tid == 0) {
+      prefetch_tmap(&m_trow_in);
+      prefetch_tmap(&m_n);
+    }
+    s3_role<M, AX_ROW, false>(&m_trow_in, &m_n, s3.row, s3, 2, base, wt, bar, sh, my_pj);
+  }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1008,6 +1184,85 @@ static cudaError_t line_pass_m(const Geom& g, const DstTables& t, const Poly& P,
               : launch_col<M, AX_COL_Y, false>(g, t, P, in, out, nslices, st);
   return nl ? launch_col<M, AX_COL_Z, true>(g, t, P, in, out, nslices, st)
             : launch_col<M, AX_COL_Z, false>(g, t, P, in, out, nslices, st);
+}
+
+// ---- persistent stage 3 (host) ----------------------------------------------------------
+size_t stage3p_ctl_bytes() { return sizeof(S3Ctl); }
+
+// roles (x-IDST : fused y : x-DST) of the SMs: EXPD_S3P_SPLIT="n0,n1" overrides; default by
+// the measured per-slice costs of the passes (fused y ~ 2.2 x one x pass at M = 2048)
+static void s3p_split(int sms, int& n0, int& n1) {
+  const char* e = getenv("EXPD_S3P_SPLIT");
+  if (e && sscanf(e, "%d,%d", &n0, &n1) == 2 && n0 > 0 && n1 > 0 && n0 + n1 < sms) return;
+  const double ry = 2.2;
+  n0 = (int)(sms / (2.0 + ry) + 0.5);
+  if (n0 < 1) n0 = 1;
+  n1 = sms - 2 * n0;
+}
+
+template <int M>
+static cudaError_t launch_s3p(const Geom& g, const DstTables& t, const Poly& P, const double* uhat, double* ring,
+                              int K, double* nhat, long nslices, void* ctl, cudaStream_t st) {
+  using D = LGeo<M, 1, 2>;
+  auto k = k_stage3p<M>;
+  static DevOnce once;
+  int per_sm = 1;
+  if (cudaError_t e = smem_optin(once, k, D::SMEM, D::THREADS, &per_sm); e != cudaSuccess) return e;
+  CUtensorMap mu, mto, mtc, mti, mn;
+  cudaError_t e;
+  if ((e = axis_map(&mu, g, AX_ROW, uhat, nslices, 1, false)) != cudaSuccess) return e;
+  if ((e = axis_map(&mto, g, AX_ROW, ring, K, 1, true)) != cudaSuccess) return e;
+  if ((e = axis_map(&mtc, g, AX_COL_Y, ring, K, 1, false)) != cudaSuccess) return e;
+  if ((e = axis_map(&mti, g, AX_ROW, ring, K, 1, false)) != cudaSuccess) return e;
+  if ((e = axis_map(&mn, g, AX_ROW, nhat, nslices, 1, true)) != cudaSuccess) return e;
+  S3Args s{};
+  const int rows = (int)(g.npad / g.M);
+  s.row.inner = (rows + 1) / 2;
+  s.row.per_slice = s.row.inner;
+  s.row.rows = rows;
+  s.col.inner = g.M / 2;
+  s.col.per_slice = s.col.inner;
+  s.col.rows = rows;
+  for (LineArgs* la : {&s.row, &s.col}) {
+    la->nitems = (long)la->per_slice * nslices;
+    la->tw = t.tw;
+    la->pa = t.pa;
+    la->c = 0.5 * sqrt(2.0 / (double)g.M);
+    la->poly = P;
+  }
+  s.ctl = reinterpret_cast<S3Ctl*>(ctl);
+  s.nslices = (int)nslices;
+  s.K = K;
+  s.sms = sm_count();
+  s3p_split(s.sms, s.split0, s.split1);
+  if ((e = cudaMemsetAsync(ctl, 0, sizeof(S3Ctl), st)) != cudaSuccess) return e;
+  k<<<(unsigned)(s.sms * per_sm), D::THREADS, D::SMEM, st>>>(mu, mto, mtc, mti, mn, s);
+  return cudaGetLastError();
+}
+
+// Is the persistent stage 3 selected for this geometry (2-D, TMA line kernels, slices <=
+// kS3MaxSlices)?  Opt-in (EXPD_S3P=1): measured on c5 (profiles/r02/) it takes 17.6 ms against
+// the chunked passes' 15.9 ms per sweep, and ncu counts 49.7 GB of DRAM traffic per launch --
+// as much as the chunked passes.  A slice is 33.5 MB and every slice moves ~200 MB through the
+// L2 (U-hat, the intermediate's write / in-place pass / read, N-hat) between the x-IDST that
+// writes its intermediate and the x-DST that reads it, so the ring cannot stay in the 126 MB
+// L2 at this size, and the per-role SM split idles SMs whenever a role waits.
+bool stage3p_supported(const Geom& g, long nslices) {
+  const char* e = getenv("EXPD_S3P");
+  if (!(e && e[0] == '1')) return false;
+  return g.dim == 2 && line_supported(g) && g.M >= 512 && nslices <= kS3MaxSlices;
+}
+
+cudaError_t stage3p(const Geom& g, const DstTables& t, const Poly& P, const double* uhat, double* ring, int K,
+                    double* nhat, long nslices, void* ctl, cudaStream_t st) {
+  if (nslices <= 0) return cudaSuccess;
+  switch (g.M) {
+    case 512: return launch_s3p<512>(g, t, P, uhat, ring, K, nhat, nslices, ctl, st);
+    case 1024: return launch_s3p<1024>(g, t, P, uhat, ring, K, nhat, nslices, ctl, st);
+    case 2048: return launch_s3p<2048>(g, t, P, uhat, ring, K, nhat, nslices, ctl, st);
+    case 4096: return launch_s3p<4096>(g, t, P, uhat, ring, K, nhat, nslices, ctl, st);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 // One axis pass (ax: 0 = x rows, 1 = y, 2 = z) of nslices padded spectral slices; nl
