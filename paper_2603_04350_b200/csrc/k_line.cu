@@ -83,6 +83,7 @@ struct LineArgs {
   int rows;        // ROW: rows per slice (for the incomplete last pair)
   const double2* tw;   // [M] exp(-2 pi i q / M)
   const double* pa;    // [M] a_i = c (sin(pi i/M) + 1/2), c = sqrt(2/M)/2 (b_i = a_i - c)
+  const double* sinp;  // [M] sin(pi i/M)
   double c;            // sqrt(2/M)/2
   Poly poly;
 };
@@ -143,10 +144,60 @@ __device__ __forceinline__ void ltwmul(const double2* __restrict__ tw, int b, do
 // each thread owns exactly one such job, the configurations used here).
 template <int M, int G>
 struct LPre {
-  double pa[LGeo<M, G, 1>::R0];
-  double2 tmid, ta, tb;
+  double sj, cj;       // sin / cos (pi j / M) of this thread's stage-0 job j (kept for the kernel)
+  double2 tmid, ta, tb;  // base twiddles (re-loaded per item: held, they cost spills)
   int pj;  // this thread's partner job of the last stage (see partner_job)
 };
+
+// cos (2 pi e / 32) (exact decimal expansions to 20 digits)
+__host__ __device__ constexpr double cos32(int e) {
+  constexpr double c[9] = {1.0,
+                           0.98078528040323044913,
+                           0.92387953251128675613,
+                           0.83146961230254523708,
+                           0.70710678118654752440,
+                           0.55557023301960222474,
+                           0.38268343236508977173,
+                           0.19509032201612826785,
+                           0.0};
+  e &= 31;
+  return e <= 8 ? c[e] : (e <= 16 ? -c[16 - e] : (e <= 24 ? -c[e - 16] : c[32 - e]));
+}
+__host__ __device__ constexpr double sin32(int e) { return cos32(8 - e); }
+
+// The per-thread constants of the line transform, computed ONCE per kernel (they depend only
+// on the thread): the stage-0 angle pi j / M (the pre-processing weights sin(pi i / M), i = j +
+// T r, follow by the addition theorem with the compile-time angles pi r / R0 -- no per-item
+// table loads through the LSU, which is the line kernels' bottleneck) and the base twiddles
+// of the middle stage and of the last stage's partner jobs.
+template <int M, int G>
+__device__ __forceinline__ LPre<M, G> line_pre(const LineArgs& a, int my_pj) {
+  const int j = threadIdx.x / G;
+  LPre<M, G> pre;
+  pre.pj = my_pj;
+  pre.sj = __ldg(a.sinp + j);
+  pre.cj = __ldg(a.sinp + M / 2 - j);  // cos(pi j / M) = sin(pi (M/2 - j) / M), j <= M / 2
+  return pre;
+}
+template <int M, int G>
+__device__ __forceinline__ void line_pre_tw(LPre<M, G>& pre, const double2* __restrict__ tw) {
+  using D = LGeo<M, G, 1>;
+  constexpr int R0 = D::R0, NSL = D::NSL;
+  const int j = threadIdx.x / G;
+  constexpr int NS1 = R0, TWS1 = M / (NS1 * D::RM1);
+  pre.tmid = __ldg(tw + (j % NS1) * TWS1);
+  const int pj = pre.pj / G;  // the partner job's frequency set (G = 1: the table entry)
+  pre.ta = __ldg(tw + (pj < NSL / 2 ? pj : 0));
+  pre.tb = __ldg(tw + (pj == 0 ? NSL / 2 : (pj < NSL / 2 ? NSL - pj : 0)));
+}
+
+// a_i = c (sin(pi i/M) + 1/2) for i = j + T r: sin(pi j/M + pi r/R0) by the addition theorem
+template <int R0, int r>
+__device__ __forceinline__ double pre_a(double sj, double cj, double c) {
+  constexpr int e = 16 * r / R0;  // pi r / R0 = 2 pi e / 32
+  const double s = fma(sj, cos32(e), cj * sin32(e));
+  return fma(c, s, 0.5 * c);
+}
 
 // Lane -> partner job of the last FFT stage.  With one pair job per thread (G = 1, NSL / 2 =
 // T) any bijection works; the tables (tools/partner_lanes.py) group the jobs so that each
@@ -377,30 +428,19 @@ __device__ __forceinline__ void line_issue_store(const CUtensorMap* map, const L
 // on bar, phase parity): table values, the wait, [V] or [V, N, V], and the result written in
 // the layout the item's TMA store reads.  Every thread of the CTA calls it.
 template <int M, int AX, bool NL, int G>
-__device__ __forceinline__ void line_item(char* cb, double2* wt, const LineArgs& a, int my_pj, uint64_t* bar,
-                                          uint32_t parity) {
+__device__ __forceinline__ void line_item(char* cb, double2* wt, const LineArgs& a, const LPre<M, G>& pre0,
+                                          uint64_t* bar, uint32_t parity) {
   using D = LGeo<M, G, 1>;
   constexpr int R0 = D::R0, T = D::T, L = D::L, PADP = D::PADP;
   const int tid = threadIdx.x;
   const int g = tid % G, j = tid / G;
   double2* buf = reinterpret_cast<double2*>(cb);
-    // the twiddle / sine tables are re-read every item: an opaque copy of the pointers keeps
-    // the compiler from hoisting ~30 loop-invariant twiddles into registers for the whole loop
+    // the twiddle table is re-read every item: an opaque copy of the pointer keeps the
+    // compiler from hoisting loop-invariant twiddles into registers for the whole loop
     const double2* tw = a.tw;
-    const double* pa = a.pa;
-    asm volatile("" : "+l"(tw), "+l"(pa));
-    LPre<M, G> pre;
-    pre.pj = my_pj;
-    {
-#pragma unroll
-      for (int r = 0; r < R0; ++r) pre.pa[r] = __ldg(pa + j + T * r);
-      constexpr int NS1 = R0, TWS1 = M / (NS1 * D::RM1);
-      pre.tmid = __ldg(tw + (j % NS1) * TWS1);
-      constexpr int NSL = D::NSL;
-      const int pj = pre.pj / G;  // the partner job's frequency set (G = 1: the table entry)
-      pre.ta = __ldg(tw + (pj < NSL / 2 ? pj : 0));
-      pre.tb = __ldg(tw + (pj == 0 ? NSL / 2 : (pj < NSL / 2 ? NSL - pj : 0)));
-    }
+    asm volatile("" : "+l"(tw));
+    LPre<M, G> pre = pre0;
+    line_pre_tw<M, G>(pre, tw);
     mbar_wait(bar, parity);
 
     double2 out[2 * L];
@@ -412,9 +452,14 @@ __device__ __forceinline__ void line_item(char* cb, double2* wt, const LineArgs&
 #pragma unroll 1
     for (int pass = 0; pass < npass; ++pass) {
       double2 v[R0];
-#pragma unroll
-      for (int r = 0; r < R0; ++r) {
+      // opaque copies: the weights are recomputed in each pass instead of being hoisted out of
+      // the pass loop (16 live doubles)
+      double sj = pre.sj, cj = pre.cj;
+      asm volatile("" : "+d"(sj), "+d"(cj));
+      sfor<R0>([&](auto rr) {
+        constexpr int r = decltype(rr)::value;
         const int i = j + T * r;
+        const double av = pre_a<R0, r>(sj, cj, a.c);
         if (i == 0) {
           v[r] = make_double2(0.0, 0.0);
         } else if (AX == AX_ROW) {
@@ -426,14 +471,14 @@ __device__ __forceinline__ void line_item(char* cb, double2* wt, const LineArgs&
                                          *reinterpret_cast<const double*>(cb + M * 8 + o1));
           const double2 zm = make_double2(*reinterpret_cast<const double*>(cb + o2),
                                           *reinterpret_cast<const double*>(cb + M * 8 + o2));
-          v[r] = lpre(z, zm, pre.pa[r], a.c);
+          v[r] = lpre(z, zm, av, a.c);
         } else {
           // pass 0: raw [row][G] linear; pass 1: the padded layout written by the N step
           const int p1 = i - 1, p2 = M - i - 1;
           const int q1 = pass ? lswz<PADP>(p1) : p1, q2 = pass ? lswz<PADP>(p2) : p2;
-          v[r] = lpre(buf[q1 * G + g], buf[q2 * G + g], pre.pa[r], a.c);
+          v[r] = lpre(buf[q1 * G + g], buf[q2 * G + g], av, a.c);
         }
-      }
+      });
       lcore<M, G>(v, buf, wt, tw, out, pre);
       if (NL && pass + 1 < npass) {
         __syncthreads();  // everyone has read (e, w) of pass 0
@@ -488,6 +533,7 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
   __builtin_assume(tid < D::THREADS);
   const int g = tid % G, j = tid / G;
   const int my_pj = partner_job<M, G>(tid);
+  const LPre<M, G> pre = line_pre<M, G>(a, my_pj);
 
   if (tid == 0) {
     prefetch_tmap(&in_map);
@@ -509,7 +555,7 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
       bulk_wait_read0();  // the previous item's stores have left the other buffer
       line_issue_load<M, AX, G>(&in_map, a, next, base + (cur ^ 1) * D::BUFB, &bar[cur ^ 1]);
     }
-    line_item<M, AX, NL, G>(cb, wt, a, my_pj, &bar[cur], (uint32_t)((NBUF == 2 ? (it >> 1) : it) & 1));
+    line_item<M, AX, NL, G>(cb, wt, a, pre, &bar[cur], (uint32_t)((NBUF == 2 ? (it >> 1) : it) & 1));
     fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
@@ -571,6 +617,7 @@ __device__ __forceinline__ void s3_role(const CUtensorMap* in_map, const CUtenso
   const unsigned total = per * (unsigned)s3.nslices;
   const int K = s3.K;
   const int smod_in = pass == 0 ? 0 : K, smod_out = pass == 2 ? 0 : K;
+  const LPre<M, 1> pre = line_pre<M, 1>(a, my_pj);
   auto grab = [&]() -> long {
     const unsigned t = atomicAdd(&ctl->ticket[pass], 1u);
     return t < total ? (long)t : -1;
@@ -622,7 +669,7 @@ __device__ __forceinline__ void s3_role(const CUtensorMap* in_map, const CUtenso
       }
       sh[it & 1] = nxt;
     }
-    line_item<M, AX, NL, 1>(cb, wt, a, my_pj, &bar[cur], (uint32_t)((it >> 1) & 1));
+    line_item<M, AX, NL, 1>(cb, wt, a, pre, &bar[cur], (uint32_t)((it >> 1) & 1));
     fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
@@ -1073,6 +1120,7 @@ static cudaError_t launch_line(const Geom& g, const DstTables& t, const Poly& P,
   a.nitems = (long)a.per_slice * nslices;
   a.tw = t.tw;
   a.pa = t.pa;
+  a.sinp = t.sinp;
   a.c = 0.5 * sqrt(2.0 / (double)g.M);
   a.poly = P;
   long grid = (long)sm_count() * per_sm;
@@ -1143,6 +1191,7 @@ static cudaError_t launch_line2(const Geom& g, const DstTables& t, const Poly& P
   a.nitems = (long)a.per_slice * nslices;
   a.tw = t.tw;
   a.pa = t.pa;
+  a.sinp = t.sinp;
   a.c = 0.5 * sqrt(2.0 / (double)g.M);
   a.poly = P;
   long grid = (long)sm_count() * per_sm;
@@ -1227,6 +1276,7 @@ static cudaError_t launch_s3p(const Geom& g, const DstTables& t, const Poly& P, 
     la->nitems = (long)la->per_slice * nslices;
     la->tw = t.tw;
     la->pa = t.pa;
+    la->sinp = t.sinp;
     la->c = 0.5 * sqrt(2.0 / (double)g.M);
     la->poly = P;
   }

@@ -396,3 +396,29 @@ def test_device_loop_not_converged_and_maxit(orc):
     assert rep["iterations"] == 3 and rep["sweeps"] == 4 and len(rep["hist"]) == 4
     U0, rep0 = plan.fixed_point_solve(u0, tol=1e-30, maxit=0)
     assert rep0["sweeps"] == 1 and len(rep0["hist"]) == 1
+
+
+@pytest.mark.parametrize("env", [{"EXPD_LINE2": "1"}, {"EXPD_S3P": "1"}, {"EXPD_S3P": "1", "EXPD_S3P_K": "2"},
+                                 {"EXPD_K1V": "2562"}])
+def test_opt_in_variants_match_default(orc, env, monkeypatch):
+    """The measured-and-kept-opt-in kernel variants (k_line2, the
+    persistent stage 3 with rings of 4 and 2 slices, the previous K1 default) give the default
+    path's Picard iterations and solution at n + 1 = 2048 (their launch size), and k_line2's
+    stage 3 matches the oracle at sampled modes."""
+    cfg = synth.CONFIGS["c5"].scaled(2047, 8)
+    u0 = T(synth.initial_condition(cfg))
+    plan = Plan(Problem.from_config(cfg))
+    Ud, rd = plan.fixed_point_solve(u0, tol=1e-12, maxit=30)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    plan2 = Plan(Problem.from_config(cfg))
+    Uv, rv = plan2.fixed_point_solve(u0, tol=1e-12, maxit=30)
+    assert rd["converged"] and rv["converged"] and rv["iterations"] == rd["iterations"]
+    assert relmax(H(Uv), H(Ud)) < 1e-12
+    if "EXPD_LINE2" in env:
+        s = orc.spec(cfg)
+        uh = np.random.default_rng(57).standard_normal((1,) + cfg.shape) / np.sqrt(cfg.N)
+        got = H(plan2.nonlin_hat(T(uh))).reshape(1, -1)
+        idx = np.random.default_rng(58).integers(0, cfg.N, 16)
+        want = orc.dst_sample(s, orc.nonlin(s, orc.dst(s, uh[0])), idx)
+        assert np.abs(got[0][idx] - want).max() < 1e-12 * np.abs(got[0]).max()
