@@ -1197,12 +1197,9 @@ static int pipe_mode() {
 // Variants: 2562 (default: 256 threads, double-buffered tiles, 1 CTA/SM), 2561 (single
 // stage, 2 CTAs/SM), 1282 (128 threads = 4 pairs per tile).  c5: 7.02 / 7.10 / 11.2 ms.
 static int k1_variant(int nt) {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("EXPD_K1V");
-    v = e ? atoi(e) : 0;
-    if (v != 2562 && v != 1282 && v != 2561 && v != 5123) v = 0;
-  }
+  const char* e = getenv("EXPD_K1V");  // read per launch (a tuning / A-B switch)
+  int v = e ? atoi(e) : 0;
+  if (v != 2562 && v != 1282 && v != 2561 && v != 5123) v = 0;
   if (v) return v;
   // default per Nt (measured): Nt = 256 the ring of two warp groups (c5 K1 6.69 -> 6.02 ms,
   // profiles/r02/), Nt = 128 128-thread CTAs of 8 pairs (more resident CTAs hide the TMA
