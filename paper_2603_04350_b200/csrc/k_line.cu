@@ -1047,6 +1047,17 @@ static cudaError_t make_map(CUtensorMap* m, const double* ptr, const cuuint64_t 
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
+// L2 promotion of the K1 tile loads (EXPD_K1_PROMO: 0 none, 1 64B, 2 128B, 3 256B = default)
+static CUtensorMapL2promotion k1_promotion() {
+  const char* e = getenv("EXPD_K1_PROMO");
+  switch (e ? atoi(e) : 3) {
+    case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
+    case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
+    case 2: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
+    default: return CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+  }
+}
+
 // 2-D fp64 tensor map (no swizzle): rows of `cols` doubles at byte stride row_bytes.
 cudaError_t make_tmap_2d(CUtensorMap* m, const double* ptr, unsigned long long cols, unsigned long long rows,
                          unsigned long long row_bytes, unsigned box_cols, unsigned box_rows) {
@@ -1057,7 +1068,7 @@ cudaError_t make_tmap_2d(CUtensorMap* m, const double* ptr, unsigned long long c
   const cuuint32_t b[2] = {box_cols, box_rows};
   const cuuint32_t es[2] = {1, 1};
   CUresult r = f(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(ptr), d, s, b, es,
-                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, k1_promotion(),
                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
