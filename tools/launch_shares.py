@@ -10,10 +10,11 @@ def shares(path):
     h = rows[hi]
     ki, vi = h.index("Kernel Name"), h.index("Metric Value")
     ui = h.index("Metric Unit") if "Metric Unit" in h else None
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     tot, cnt = collections.defaultdict(float), collections.Counter()
     unit = "?"
     for r in rows[hi + 1:]:
-        if len(r) <= vi:
+        if len(r) <= vi or (mi is not None and r[mi] != "gpu__time_duration.sum"):
             continue
         name = r[ki].split("(")[0]
         tot[name] += float(r[vi].replace(",", ""))
