@@ -1047,10 +1047,13 @@ static cudaError_t make_map(CUtensorMap* m, const double* ptr, const cuuint64_t 
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 
-// L2 promotion of the K1 tile loads (EXPD_K1_PROMO: 0 none, 1 64B, 2 128B, 3 256B = default)
+// L2 promotion of the K1 tile loads (EXPD_K1_PROMO: 0 none = default, 1 64B, 2 128B, 3 256B).
+// Measured on c5 (profiles/r02/ncu_k1_promo_*.csv): 256B promotion over-fetches 0.7-1.5 GB of
+// DRAM reads per K1 launch (each 128-byte box row is a different time slice) at the same
+// duration; without promotion the reads equal the algorithmic 17.3 GB.
 static CUtensorMapL2promotion k1_promotion() {
   const char* e = getenv("EXPD_K1_PROMO");
-  switch (e ? atoi(e) : 3) {
+  switch (e ? atoi(e) : 0) {
     case 0: return CU_TENSOR_MAP_L2_PROMOTION_NONE;
     case 1: return CU_TENSOR_MAP_L2_PROMOTION_L2_64B;
     case 2: return CU_TENSOR_MAP_L2_PROMOTION_L2_128B;
