@@ -468,6 +468,8 @@ class Plan:
         ns = x.numel() // self.problem.N
         if ns * self.problem.N != x.numel():
             raise ValueError("x must hold whole slices of n^dim points")
+        if ns == 0:
+            return out
         self._check(self.lib.expd_dst(self.handle, self._chk(x, torch.float64, x.numel()),
                                       self._chk(out, torch.float64, x.numel()), ns))
         return out
@@ -478,6 +480,8 @@ class Plan:
         ns = uhat.numel() // self.problem.N
         if ns * self.problem.N != uhat.numel():
             raise ValueError("uhat must hold whole slices of n^dim points")
+        if ns == 0:
+            return out
         self._check(self.lib.expd_nonlin_hat(self.handle, self._chk(uhat, torch.float64, uhat.numel()),
                                              self._chk(out, torch.float64, uhat.numel()), ns))
         return out

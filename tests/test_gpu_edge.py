@@ -1,0 +1,86 @@
+"""Edge cases of the CUDA path against the oracle and the C-ABI's documented behaviour:
+empty inputs, the zero problem, the largest alpha, the smallest grids and time windows, and
+the binding's argument checks."""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2603_04350_b200 import Plan, Problem  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def T(x):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float64)).to(DEV)
+
+
+def H(t):
+    return t.detach().cpu().numpy()
+
+
+def relmax(got, want):
+    return float(np.abs(got - want).max() / max(np.abs(want).max(), 1e-300))
+
+
+def test_empty_slices_leave_output_untouched():
+    cfg = synth.CONFIGS["c5"].scaled(63, 4)
+    plan = Plan(Problem.from_config(cfg))
+    x = torch.empty((0,) + cfg.shape, dtype=torch.float64, device=DEV)
+    assert plan.dst(x).numel() == 0 and plan.nonlin_hat(x).numel() == 0
+
+
+@pytest.mark.parametrize("name,n,nt", [("c2", 31, 16), ("c5", 63, 8)])
+def test_zero_problem(orc, name, n, nt):
+    """u0 = 0: F(0) = 0, so r^0 = 0; both the oracle and the GPU stop at once (rho := 0 when
+    ||r^0|| = 0, reading R8) with U = 0."""
+    cfg = synth.CONFIGS[name].scaled(n, nt)
+    u0 = np.zeros(cfg.shape)
+    plan = Plan(Problem.from_config(cfg), krylov_vectors=4)
+    U, rep = plan.fixed_point_solve(T(u0), tol=1e-12)
+    Uo, st, its, hist = orc.fixed_point(orc.spec(cfg), u0, tol=1e-12)
+    assert st == 0 and rep["converged"] and rep["iterations"] == its == 0
+    assert float(U.abs().max()) == 0.0
+    if not cfg.q:
+        U, rep = plan.gmres_solve(T(u0), tol=1e-12, restart=3)
+        assert rep["converged"] and rep["iterations"] == 0 and float(U.abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("dim,n,nt", [(1, 3, 4), (2, 3, 4), (3, 3, 4), (1, 7, 256)])
+def test_alpha_one_and_smallest_grids(orc, dim, n, nt):
+    """alpha = 1 (the largest the ABI takes: the periodic, circulant preconditioner, cond = 1)
+    on the smallest grids (n + 1 = 4) and windows (Nt = 4)."""
+    cfg = synth.Config("e", dim, n, 0.5, 0.3, 0.5, nt, 1.0)
+    plan = Plan(Problem.from_config(cfg))
+    R = synth.random_spacetime(cfg, seed=7)
+    want, leak = orc.precond(orc.spec(cfg), R)
+    assert leak < 1e-8 and relmax(H(plan.precond_apply(T(R))), want) < 1e-11
+    u0 = synth.random_slice(cfg, 8)
+    U = synth.random_spacetime(cfg, seed=9)
+    Rg, rn2 = plan.residual(T(u0), T(U), norm=True)
+    wr, wn2 = orc.residual(orc.spec(cfg), u0, U)
+    assert relmax(H(Rg), wr) < 1e-11 and abs(rn2 - wn2) < 1e-11 * wn2
+
+
+def test_binding_rejects_wrong_shapes_and_devices():
+    cfg = synth.CONFIGS["c2"].scaled(15, 8)
+    plan = Plan(Problem.from_config(cfg))
+    u0 = torch.zeros(cfg.shape, dtype=torch.float64, device=DEV)
+    with pytest.raises(ValueError):
+        plan.fixed_point_solve(u0, torch.zeros((cfg.nt - 1,) + cfg.shape, dtype=torch.float64, device=DEV))
+    with pytest.raises(ValueError):
+        plan.fixed_point_solve(torch.zeros(cfg.N + 1, dtype=torch.float64, device=DEV))
+    with pytest.raises(ValueError):
+        plan.precond_apply(torch.zeros((cfg.nt,) + cfg.shape, dtype=torch.float64))  # host tensor
+    with pytest.raises(ValueError):
+        plan.precond_apply(torch.zeros((cfg.nt,) + cfg.shape, dtype=torch.float32, device=DEV))
+    with pytest.raises(ValueError):
+        plan.dst(torch.zeros(cfg.N + 3, dtype=torch.float64, device=DEV))
