@@ -138,19 +138,32 @@ expd_status expd_residual(expd_plan* plan, const double* u0, const double* U, do
    Async. */
 expd_status expd_precond_apply(expd_plan* plan, const double* R, double* S);
 
+/* Solver buffers (expd_fixed_point_solve, expd_gmres_solve, expd_bicgstab_solve): u0 and U
+   are device pointers on the plan's device, or -- single-GPU plans -- HOST pointers (pinned
+   for asynchronous copies, pageable accepted): u0 and the initial guess are then copied in
+   inside the call, and the solution's inverse DST runs chunk by chunk while the finished
+   chunks stream to the host, so the copy-out overlaps the transform.  Host buffers on a
+   distributed plan: INVALID_ARG. */
+/* With on != 0 the solvers ignore the contents of U on entry and start from U = 0 (the
+   paper's zero initial guess), skipping the transform (and, for host U, the
+   copy) of the guess; U is still written with the solution. */
+expd_status expd_set_zero_guess(expd_plan* plan, int on);
+
 /* Preconditioned Richardson / Picard (3.2) from the initial guess in
    U (zeros per PAPER.md:895): sweep k computes r^k = F(U^k) - Q U^k, rho_k =
    ||r^k|| / ||r^0||, U^{k+1} = U^k + Q_alpha^{-1} r^k; stops after the first sweep with
-   rho_k < tol (R8), returning U^{k+1} in U.  Blocking.  report (nullable). */
+   rho_k < tol (R8), returning U^{k+1} in U.  Blocking.  report (nullable).  On one GPU
+   the iteration runs as a CUDA graph with a device-side WHILE loop (the convergence test on
+   the device, one synchronisation per solve). */
 expd_status expd_fixed_point_solve(expd_plan* plan, const double* u0, double* U, double tol, int maxit,
                                    expd_report* report);
 
 /* Left-preconditioned restarted GMRES(restart) on Q_alpha^{-1} Q u = Q_alpha^{-1} f
    (PAPER.md:284-289), classical Gram-Schmidt applied twice (R11), Givens rotations;
    stops when ||Q_alpha^{-1}(f - Q x)|| / ||Q_alpha^{-1}(f - Q x_0)|| < tol.
-   Linear problems only (npoly == 0, else UNSUPPORTED).  The effective restart is
-   min(restart, krylov vectors in the workspace - 1).  U: initial guess in, solution out.
-   Blocking. */
+   Linear problems only (npoly == 0, else UNSUPPORTED).  The workspace must hold >= restart
+   Krylov vectors (expd_plan_workspace_bytes(plan, restart)), else EXPD_ERR_OOM.  U: initial
+   guess in, solution out.  Blocking. */
 expd_status expd_gmres_solve(expd_plan* plan, const double* u0, double* U, double tol, int restart, int maxit,
                              expd_report* report);
 

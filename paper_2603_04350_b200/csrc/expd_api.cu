@@ -69,6 +69,12 @@ struct expd_plan {
   void* s3ctl = nullptr;            // persistent stage 3's dependency counters (workspace)
   FpLoopState* h_loopst = nullptr;  // pinned host copy
   bool loop_failed = false;         // the graph could not be built: host-driven loop
+  // solver I/O: zero initial guess (expd_set_zero_guess) and host u0 / U (staged, the final
+  // inverse DST streamed out chunk by chunk with the device-to-host copy)
+  bool zero_guess = false;
+  double* hstage = nullptr;          // [N] (x2 complex) device staging of a host u0
+  cudaStream_t copy_stream = nullptr;
+  std::vector<cudaEvent_t> cev;
   bool capturing = false;
   bool eager_done = false;  // one eager sweep (kernel attributes) before the first capture
   // optional stage timing: ev[0] before stage 3, ev[1] before K1, ev[2] after K1
@@ -274,7 +280,8 @@ extern "C" expd_status expd_plan_create(const expd_problem* prob, const expd_dis
 
 // workspace layout (every block 256-byte aligned)
 struct Layout {
-  size_t Uh, Nh, T1, UT, NT, X2, X3, u0h, E, C1, C2, scratch, partial, dscal, loopst, s3ctl, krylov, total, vec;
+  size_t Uh, Nh, T1, UT, NT, X2, X3, u0h, E, C1, C2, scratch, partial, dscal, loopst, s3ctl, hstage, krylov, total,
+      vec;
 };
 static Layout layout(const expd_plan* p, int kv) {
   Layout L{};
@@ -309,6 +316,7 @@ static Layout layout(const expd_plan* p, int kv) {
   L.dscal = off; off += align_up(sizeof(double) * 512);
   L.loopst = off; off += align_up(sizeof(FpLoopState));
   L.s3ctl = off; off += align_up(stage3p_ctl_bytes());
+  L.hstage = off; off += align_up(sizeof(double) * (size_t)p->g.N * (p->cx ? 2 : 1));
   L.krylov = off; off += (size_t)kv * vec;
   L.total = off;
   return L;
@@ -347,6 +355,7 @@ extern "C" expd_status expd_plan_set_workspace(expd_plan* p, void* d_ptr, size_t
   p->dscal = at(L.dscal);
   p->loopst = reinterpret_cast<FpLoopState*>(p->ws + L.loopst);
   p->s3ctl = p->ws + L.s3ctl;
+  p->hstage = at(L.hstage);
   p->krylov = kv ? at(L.krylov) : nullptr;
   p->krylov_cap = kv;
   if (p->sweep_exec) {
@@ -375,6 +384,8 @@ extern "C" void expd_plan_destroy(expd_plan* p) {
   if (p->sweep_exec) cudaGraphExecDestroy(p->sweep_exec);
   if (p->loop_exec) cudaGraphExecDestroy(p->loop_exec);
   if (p->h_loopst) cudaFreeHost(p->h_loopst);
+  if (p->copy_stream) cudaStreamDestroy(p->copy_stream);
+  for (cudaEvent_t e : p->cev) cudaEventDestroy(e);
   if (p->cap_stream) cudaStreamDestroy(p->cap_stream);
   if (p->comm_stream) cudaStreamDestroy(p->comm_stream);
   for (cudaEvent_t e : p->pev) cudaEventDestroy(e);
@@ -701,7 +712,7 @@ extern "C" expd_status expd_load_state(expd_plan* p, const double* u0, const dou
   if (!u0) return fail(p, EXPD_ERR_INVALID_ARG, "expd_load_state: u0 is null");
   s = load_u0(p, u0);
   if (s) return s;
-  if (U) return phys_to_mode(p, U, p->Uh);
+  if (U && !p->zero_guess) return phys_to_mode(p, U, p->Uh);
   CUDA_TRY(p, cudaMemsetAsync(p->Uh, 0, sizeof(double) * p->prob.nt * p->mlen, p->stream));
   return EXPD_OK;
 }
@@ -894,6 +905,95 @@ static void fill_report(expd_report* r, int its, int sweeps, int conv, const std
     for (size_t i = 0; i < hist.size(); ++i) r->hist[i] = hist[i];
 }
 
+// ---------------------------------------------------------------------------------------
+// solver I/O with host buffers: u0 / U may be host pointers (pinned or pageable) on a
+// single-GPU plan.  u0 is staged to the device; the initial guess (unless zero_guess) is
+// copied into T1 and transformed from there; the solution's inverse DST runs chunk by chunk
+// into T1 while the previous chunk streams to the host on a copy stream.
+// ---------------------------------------------------------------------------------------
+static bool is_host_ptr(const void* ptr) {
+  cudaPointerAttributes at{};
+  if (cudaPointerGetAttributes(&at, ptr) != cudaSuccess) {
+    cudaGetLastError();
+    return true;  // unknown to CUDA: pageable host memory
+  }
+  return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
+}
+
+struct SolveIO {
+  bool host_u0 = false, host_U = false;
+  const double* u0 = nullptr;  // device u0 (staged if host)
+  const double* Uin = nullptr; // device initial guess (T1 if host), nullptr if zero_guess
+};
+
+static expd_status solve_in(expd_plan* p, const double* u0, const double* U, SolveIO& io) {
+  io.host_u0 = is_host_ptr(u0);
+  io.host_U = is_host_ptr(U);
+  io.u0 = u0;
+  io.Uin = U;
+  if ((io.host_u0 || io.host_U) && p->dist)
+    return fail(p, EXPD_ERR_INVALID_ARG, "host u0 / U: single-GPU plans only (distributed: device buffers)");
+  const size_t slice = sizeof(double) * (size_t)p->g.N * (p->cx ? 2 : 1);
+  if (io.host_u0) {
+    CUDA_TRY(p, cudaMemcpyAsync(p->hstage, u0, slice, cudaMemcpyHostToDevice, p->stream));
+    io.u0 = p->hstage;
+  }
+  if (p->zero_guess) {
+    io.Uin = nullptr;
+  } else if (io.host_U) {
+    CUDA_TRY(p, cudaMemcpyAsync(p->T1, U, slice * p->prob.nt, cudaMemcpyHostToDevice, p->stream));
+    io.Uin = p->T1;
+  }
+  return EXPD_OK;
+}
+
+// U = V U-hat into the caller's U: device pointer -> expd_store_state; host pointer -> the
+// inverse DST of slice chunks into T1, each chunk copied out on copy_stream as soon as it is
+// done (the copy of chunk c overlaps the transform of chunk c + 1).  Synchronises.
+static expd_status solve_out(expd_plan* p, double* U, const SolveIO& io) {
+  if (!io.host_U) {
+    expd_status s = expd_store_state(p, U);
+    if (s) return s;
+    CUDA_TRY(p, cudaStreamSynchronize(p->stream));
+    return EXPD_OK;
+  }
+  const long nt = p->prob.nt;
+  const long per = (long)p->g.N * (p->cx ? 2 : 1);  // doubles per physical slice
+  const int nch = nt >= 8 ? 8 : (int)nt;
+  const long ck = (nt + nch - 1) / nch;
+  if (!p->copy_stream) CUDA_TRY(p, cudaStreamCreateWithFlags(&p->copy_stream, cudaStreamNonBlocking));
+  while ((int)p->cev.size() < nch + 1) {
+    cudaEvent_t e;
+    CUDA_TRY(p, cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    p->cev.push_back(e);
+  }
+  int c = 0;
+  for (long t0 = 0; t0 < nt; t0 += ck, ++c) {
+    const long ns = nt - t0 < ck ? nt - t0 : ck;
+    double* dst = p->T1 + t0 * per;
+    if (p->cx) {
+      expd_status s = cx_mode_to_phys(p, p->Uh + t0 * p->mlen, dst, ns);
+      if (s) return s;
+    } else {
+      CUDA_TRY(p, dst_slices(p->g, dst_tables(p), p->Uh + t0 * p->mlen, true, dst, false, ns, p->scratch, p->stream));
+    }
+    CUDA_TRY(p, cudaEventRecord(p->cev[c], p->stream));
+    CUDA_TRY(p, cudaStreamWaitEvent(p->copy_stream, p->cev[c], 0));
+    CUDA_TRY(p, cudaMemcpyAsync(U + t0 * per, dst, sizeof(double) * ns * per, cudaMemcpyDeviceToHost, p->copy_stream));
+  }
+  CUDA_TRY(p, cudaEventRecord(p->cev[nch], p->copy_stream));
+  CUDA_TRY(p, cudaStreamWaitEvent(p->stream, p->cev[nch], 0));  // later work on the plan stream follows
+  CUDA_TRY(p, cudaStreamSynchronize(p->copy_stream));
+  CUDA_TRY(p, cudaStreamSynchronize(p->stream));
+  return EXPD_OK;
+}
+
+extern "C" expd_status expd_set_zero_guess(expd_plan* p, int on) {
+  if (!p) return EXPD_ERR_INVALID_ARG;
+  p->zero_guess = on != 0;
+  return EXPD_OK;
+}
+
 // The device-side fixed-point loop (single-GPU plans): one CUDA graph holding a WHILE
 // conditional node whose body is the captured sweep (stage 3, K1, the norm reduction) and
 // k_fp_conv, which records rho_k and sets the loop condition -- the iteration runs without a
@@ -978,7 +1078,9 @@ extern "C" expd_status expd_fixed_point_solve(expd_plan* p, const double* u0, do
   expd_status s = ready(p);
   if (s) return s;
   if (!u0 || !U || maxit < 0 || !(tol >= 0.0)) return fail(p, EXPD_ERR_INVALID_ARG, "fixed_point: bad args");
-  s = expd_load_state(p, u0, U);
+  SolveIO io;
+  if ((s = solve_in(p, u0, U, io))) return s;
+  s = expd_load_state(p, io.u0, io.Uin);
   if (s) return s;
   if (!p->dist && graphs_enabled() && device_loop_enabled() && !p->loop_failed && maxit < kFpLoopHist) {
     if (!p->loop_exec && build_loop_graph(p) != EXPD_OK) {
@@ -990,10 +1092,8 @@ extern "C" expd_status expd_fixed_point_solve(expd_plan* p, const double* u0, do
   if (!p->dist && graphs_enabled() && device_loop_enabled() && !p->loop_failed && maxit < kFpLoopHist) {
     s = fixed_point_device_loop(p, tol, maxit, report);
     if (s && s != EXPD_ERR_NOT_CONVERGED) return s;
-    expd_status s2 = expd_store_state(p, U);
-    if (s2) return s2;
-    CUDA_TRY(p, cudaStreamSynchronize(p->stream));
-    return s;
+    expd_status s2 = solve_out(p, U, io);
+    return s2 ? s2 : s;
   }
   CUDA_TRY(p, cudaStreamSynchronize(p->stream));
   const bool graphs = graphs_enabled();
@@ -1023,9 +1123,8 @@ extern "C" expd_status expd_fixed_point_solve(expd_plan* p, const double* u0, do
   double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   int its = conv ? k : maxit;
   fill_report(report, its, conv ? k + 1 : maxit + 1, conv, hist, secs);
-  s = expd_store_state(p, U);
+  s = solve_out(p, U, io);
   if (s) return s;
-  CUDA_TRY(p, cudaStreamSynchronize(p->stream));
   return conv ? EXPD_OK : EXPD_ERR_NOT_CONVERGED;
 }
 
@@ -1083,11 +1182,15 @@ static expd_status gmres_impl(expd_plan* p, const double* u0, double* U, double 
   constexpr int K = SC::K;
   constexpr bool CX = K == 2;
   expd_status s;
-  const int m = restart < p->krylov_cap ? restart : p->krylov_cap;
+  if (restart > p->krylov_cap)
+    return fail(p, EXPD_ERR_OOM, "GMRES restart exceeds the Krylov vectors in the workspace");
+  const int m = restart;
   const long len = (long)p->prob.nt * p->mlen;  // this rank's mode slab of a space-time vector
   const size_t vstride = align_up(sizeof(double) * (size_t)len) / sizeof(double);
   auto Vk = [&](int i) { return p->krylov + (size_t)i * vstride; };
-  s = expd_load_state(p, u0, U);
+  SolveIO io;
+  if ((s = solve_in(p, u0, U, io))) return s;
+  s = expd_load_state(p, io.u0, io.Uin);
   if (s) return s;
   CUDA_TRY(p, cudaStreamSynchronize(p->stream));
   std::vector<double> hist{1.0};
@@ -1182,9 +1285,8 @@ static expd_status gmres_impl(expd_plan* p, const double* u0, double* U, double 
   }
   double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   fill_report(report, its, its, conv, hist, secs);
-  s = expd_store_state(p, U);
+  s = solve_out(p, U, io);
   if (s) return s;
-  CUDA_TRY(p, cudaStreamSynchronize(p->stream));
   return conv ? EXPD_OK : EXPD_ERR_NOT_CONVERGED;
 }
 
@@ -1221,7 +1323,9 @@ static expd_status bicgstab_impl(expd_plan* p, const double* u0, double* U, doub
   double* t = sv + vstride;
   double* x = p->Uh;
   double* dcoef = p->dscal + 128;
-  s = expd_load_state(p, u0, U);
+  SolveIO io;
+  if ((s = solve_in(p, u0, U, io))) return s;
+  s = expd_load_state(p, io.u0, io.Uin);
   if (s) return s;
   // <a, b> (Hermitian for complex plans) and ||a||^2, completed by allreduce, read to the host
   auto dot = [&](const double* a, const double* b, T* out) -> expd_status {
@@ -1313,9 +1417,8 @@ static expd_status bicgstab_impl(expd_plan* p, const double* u0, double* U, doub
   }
   double secs = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
   fill_report(report, its, 2 * its + 1, conv, hist, secs);
-  s = expd_store_state(p, U);
+  s = solve_out(p, U, io);
   if (s) return s;
-  CUDA_TRY(p, cudaStreamSynchronize(p->stream));
   return conv ? EXPD_OK : EXPD_ERR_NOT_CONVERGED;
 }
 

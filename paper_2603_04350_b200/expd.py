@@ -52,6 +52,7 @@ EXPORTS = [
     "expd_debug_kernel_ms",
     "expd_sweep_pass_ms",
     "expd_solver_step_ms",
+    "expd_set_zero_guess",
     "expd_layout_query",
     "expd_a2a_schedule",
     "expd_a2a_schedule_keyed",
@@ -151,6 +152,7 @@ def load_library(path: str = LIB_PATH):
         "expd_sweep_pass_ms": (C.c_int, [vp, dp, dp, dp, C.POINTER(C.c_int), C.POINTER(C.c_int),
                                          C.POINTER(C.c_int)]),
         "expd_solver_step_ms": (C.c_int, [vp, dp, C.c_int, C.POINTER(C.c_int)]),
+        "expd_set_zero_guess": (C.c_int, [vp, C.c_int]),
         "expd_layout_query": (C.c_int, [C.POINTER(_Problem), C.c_int, C.c_int, C.POINTER(_Layout)]),
         "expd_a2a_schedule": (C.c_long, [C.POINTER(_Problem), C.c_int, C.c_int, C.c_int, C.c_int,
                                          C.POINTER(C.c_long), C.POINTER(C.c_long), C.c_long]),
@@ -382,14 +384,28 @@ class Plan:
         want = (self.layout["nt_local"] if slices is None else slices) * self.problem.N
         return self._chk(t, self.problem.dtype, want)
 
-    def _chk(self, t, dtype, numel: int):
+    def _chk(self, t, dtype, numel: int, host_ok: bool = False):
         if not isinstance(t, torch.Tensor):
             raise ValueError("expected a torch tensor")
-        if t.device.type != "cuda" or t.device.index != self.device:
-            raise ValueError(f"tensor on {t.device}, plan on cuda:{self.device}")
         if t.numel() != numel:
             raise ValueError(f"tensor holds {t.numel()} elements, expected {numel}")
+        if host_ok and t.device.type == "cpu":  # solver I/O with host buffers (single-GPU plans)
+            if not (t.dtype == dtype and t.is_contiguous()):
+                raise ValueError(f"expected a contiguous {dtype} tensor")
+            return C.c_void_p(t.data_ptr())
+        if t.device.type != "cuda" or t.device.index != self.device:
+            raise ValueError(f"tensor on {t.device}, plan on cuda:{self.device}")
         return _ptr(t, dtype)
+
+    def _io(self, t, slices: int | None = None):
+        """A solver argument (u0, U): on the plan's device, or a host tensor (pinned for
+        overlapped copies) that the library copies in / streams out itself."""
+        want = (self.layout["nt_local"] if slices is None else slices) * self.problem.N
+        return self._chk(t, self.problem.dtype, want, host_ok=self.comm is None)
+
+    def set_zero_guess(self, on: bool = True):
+        """Solvers start from U = 0 and ignore U's contents on entry."""
+        self._check(self.lib.expd_set_zero_guess(self.handle, int(bool(on))))
 
     # ---- primitives ------------------------------------------------------------------
     def residual(self, u0: torch.Tensor, U: torch.Tensor, R: torch.Tensor | None = None, norm: bool = False):
@@ -426,7 +442,7 @@ class Plan:
     def fixed_point_solve(self, u0, U=None, tol=1e-12, maxit=100):
         U = self._vec().zero_() if U is None else U
         r, hist = self._report(maxit)
-        st = self.lib.expd_fixed_point_solve(self.handle, self._a(u0, 1), self._a(U), tol, maxit, C.byref(r))
+        st = self.lib.expd_fixed_point_solve(self.handle, self._io(u0, 1), self._io(U), tol, maxit, C.byref(r))
         if st not in (EXPD_OK, 7):
             self._check(st)
         return U, self._rdict(r, hist, st)
@@ -434,7 +450,7 @@ class Plan:
     def gmres_solve(self, u0, U=None, tol=1e-12, restart=20, maxit=100):
         U = self._vec().zero_() if U is None else U
         r, hist = self._report(maxit)
-        st = self.lib.expd_gmres_solve(self.handle, self._a(u0, 1), self._a(U), tol, restart, maxit, C.byref(r))
+        st = self.lib.expd_gmres_solve(self.handle, self._io(u0, 1), self._io(U), tol, restart, maxit, C.byref(r))
         if st not in (EXPD_OK, 7):
             self._check(st)
         return U, self._rdict(r, hist, st)
@@ -442,7 +458,7 @@ class Plan:
     def bicgstab_solve(self, u0, U=None, tol=1e-12, maxit=100):
         U = self._vec().zero_() if U is None else U
         r, hist = self._report(maxit)
-        st = self.lib.expd_bicgstab_solve(self.handle, self._a(u0, 1), self._a(U), tol, maxit, C.byref(r))
+        st = self.lib.expd_bicgstab_solve(self.handle, self._io(u0, 1), self._io(U), tol, maxit, C.byref(r))
         if st not in (EXPD_OK, 7):
             self._check(st)
         return U, self._rdict(r, hist, st)

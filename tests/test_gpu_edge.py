@@ -84,3 +84,42 @@ def test_binding_rejects_wrong_shapes_and_devices():
         plan.precond_apply(torch.zeros((cfg.nt,) + cfg.shape, dtype=torch.float32, device=DEV))
     with pytest.raises(ValueError):
         plan.dst(torch.zeros(cfg.N + 3, dtype=torch.float64, device=DEV))
+
+
+@pytest.mark.parametrize("name,n,nt,solver", [("c5", 63, 16, "fixed_point"), ("c2", 31, 16, "gmres"),
+                                              ("c2", 31, 16, "bicgstab"), ("c7se", 31, 16, "gmres")])
+def test_host_buffers_and_zero_guess(orc, name, n, nt, solver):
+    """The solvers with host u0 / U (pinned and pageable): the library copies in and streams the
+    solution out chunk by chunk; results identical to the device-buffer call.  With the zero
+    guess set, garbage in U on entry is ignored."""
+    cfg = synth.CONFIGS[name].scaled(n, nt)
+    prob = Problem.from_config(cfg)
+    plan = Plan(prob, krylov_vectors=6)
+    u0 = torch.from_numpy(np.asarray(synth.initial_condition(cfg))).to(prob.dtype)
+    kw = {"gmres": dict(restart=5)}.get(solver, {})
+    solve = getattr(plan, solver + "_solve")
+    Ud, rd = solve(u0.to(DEV), torch.zeros((cfg.nt,) + cfg.shape, dtype=prob.dtype, device=DEV), tol=cfg.tol, **kw)
+    for pin in (True, False):
+        Uh = torch.zeros((cfg.nt,) + cfg.shape, dtype=prob.dtype)
+        u0h = u0.clone()
+        if pin:
+            Uh, u0h = Uh.pin_memory(), u0h.pin_memory()
+        Uh2, rh = solve(u0h, Uh, tol=cfg.tol, **kw)
+        assert Uh2.device.type == "cpu" and rh["iterations"] == rd["iterations"]
+        assert float((Uh2 - Ud.cpu()).abs().max()) == 0.0
+    plan.set_zero_guess(True)
+    garbage = torch.full((cfg.nt,) + cfg.shape, 1e30, dtype=prob.dtype, device=DEV)
+    Uz, rz = solve(u0.to(DEV), garbage, tol=cfg.tol, **kw)
+    assert rz["iterations"] == rd["iterations"] and float((Uz - Ud).abs().max()) == 0.0
+
+
+def test_gmres_restart_beyond_workspace_is_an_error():
+    from paper_2603_04350_b200 import ExpdError
+
+    cfg = synth.CONFIGS["c2"].scaled(15, 8)
+    plan = Plan(Problem.from_config(cfg), krylov_vectors=3)
+    u0 = torch.from_numpy(synth.initial_condition(cfg)).to(DEV)
+    with pytest.raises(ExpdError):
+        plan.gmres_solve(u0, tol=1e-12, restart=4)
+    U, rep = plan.gmres_solve(u0, tol=1e-12, restart=3)
+    assert rep["converged"]
