@@ -17,6 +17,7 @@ for name in sys.argv[1:] or ["c1", "c2"]:
     plan = Plan(Problem.from_config(cfg))
     u0 = torch.from_numpy(synth.initial_condition(cfg)).cuda()
     U = torch.zeros((cfg.nt,) + cfg.shape, dtype=torch.float64, device="cuda")
+    plan.set_zero_guess(True)  # PAPER.md:895's zero initial guess, no transform of U on entry
     res = {}
     for mode in ("1", "0"):
         os.environ["EXPD_DEVICE_LOOP"] = mode
