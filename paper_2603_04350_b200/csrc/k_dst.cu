@@ -603,7 +603,9 @@ cudaError_t dst_slices(const Geom& g, const DstTables& t, const double* src, boo
 
 int nonlin_chunk_slices(const Geom& g) {
   // slices per stage-3 chunk: the chunk's intermediate (npad doubles per slice) is about
-  // EXPD_CHUNK_MB (default 512) MB.  Measured on c5 (profiles/r01): 2-slice chunks that fit
+  // EXPD_CHUNK_MB (default 512) MB.  Re-measured in round 2 (profiles/r02/chunk_sweep.txt):
+  // 64 / 128 / 256 / 512 / 1024 / 2048 MB -> 23.5 / 22.3 / 21.9 / 21.7 / 21.7 / 21.9 ms per
+  // sweep; at 4 GB and the whole 8.6 GB state the fused y-pass slows from 8.3 to 13-17 ms.  Measured on c5 (profiles/r01): 2-slice chunks that fit
   // the 126 MB L2 lose more to launch tails than the L2 residency saves -- the axis passes
   // are shared-memory / fp64 bound and the extra HBM round trip of the intermediate
   // overlaps them (64 MB: 21.7 ms stage 3, 512 MB: 18.9 ms)
