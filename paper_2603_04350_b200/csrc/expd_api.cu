@@ -542,7 +542,7 @@ static cudaError_t enqueue_sweep(expd_plan* p, cudaStream_t st) {
       tm = &p->timer;
     }
     e = nonlin_slices(p->g, dst_tables(p), p->Uh, p->Nh + p->g.npad, p->prob.nt - 1 + p->nshift, p->prob.npoly,
-                      p->prob.q, p->scratch, st, tm, p->s3ctl);
+                      p->prob.q, p->scratch, st, tm, p->s3ctl, p->T1);  // T1 is free during a sweep
     if (e != cudaSuccess) return e;
   }
   if ((e = record(p, 1, st)) != cudaSuccess) return e;
@@ -885,7 +885,7 @@ extern "C" expd_status expd_debug_kernel_ms(expd_plan* p, int which, long nslice
 extern "C" int expd_sweep_kernel_launches(const expd_plan* p) {
   if (!p) return 0;
   int k = 2;  // fused time pass + norm reduction
-  if (p->nl) k += nonlin_kernel_launches(p->g, p->prob.nt - 1 + p->nshift);
+  if (p->nl) k += nonlin_kernel_launches(p->g, p->prob.nt - 1 + p->nshift, !p->dist);
   return k;
 }
 

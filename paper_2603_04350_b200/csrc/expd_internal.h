@@ -129,7 +129,7 @@ struct PassTimer {
 };
 cudaError_t nonlin_slices(const Geom& g, const DstTables& t, const double* uhat, double* nhat, long nslices,
                           int npoly, const double* q, double* scratch, cudaStream_t st, struct PassTimer* timer = nullptr,
-                          void* s3ctl = nullptr);
+                          void* s3ctl = nullptr, double* full_tmp = nullptr);
 // persistent stage 3 (k_line.cu): one launch for all slices, intermediate in a ring of K
 // slices (ring: K npad doubles), dependency counters in ctl (stage3p_ctl_bytes(), zeroed by the
 // launch).  PassTimer kind 3 marks it.
@@ -152,7 +152,7 @@ cudaError_t make_tmap_2d(CUtensorMap* m, const double* ptr, unsigned long long c
                          unsigned long long row_bytes, unsigned box_cols, unsigned box_rows);
 cudaError_t line_pass(const Geom& g, const DstTables& t, const Poly& P, int ax, bool nl, const double* in,
                       double* out, long nslices, cudaStream_t st);
-int nonlin_kernel_launches(const Geom& g, long nslices);
+int nonlin_kernel_launches(const Geom& g, long nslices, bool full_tmp = false);
 
 // vector kernels (k_vec.cu)
 cudaError_t mode_tables(const Geom& g, const double* lam_axis, double a, double c, double dt, int scheme,

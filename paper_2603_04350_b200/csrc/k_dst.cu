@@ -620,7 +620,15 @@ int nonlin_chunk_slices(const Geom& g) {
   return (int)(c < 1 ? 1 : (c > 64 ? 64 : c));
 }
 
-int nonlin_kernel_launches(const Geom& g, long nslices) {
+// EXPD_S3_FULLX=0 keeps the x passes chunked too when a whole-state intermediate is available
+static bool s3_full_x() {
+  const char* e = getenv("EXPD_S3_FULLX");
+  return !(e && e[0] == '0');
+}
+
+int nonlin_kernel_launches(const Geom& g, long nslices, bool full_tmp) {
+  if (full_tmp && use_line(g) && g.dim == 2 && s3_full_x())
+    return 2 + (int)((nslices + nonlin_chunk_slices(g) - 1) / nonlin_chunk_slices(g));
   if (use_line(g) && nonlin_chunk_slices(g) >= 2 && stage3p_supported(g, nslices)) return 1;
   long chunk = nonlin_chunk_slices(g);
   long nch = (nslices + chunk - 1) / chunk;
@@ -655,12 +663,29 @@ static int s3p_ring(long chunk) {
 }
 
 cudaError_t nonlin_slices(const Geom& g, const DstTables& t, const double* uhat, double* nhat, long nslices,
-                          int npoly, const double* q, double* scratch, cudaStream_t st, PassTimer* tm, void* s3ctl) {
+                          int npoly, const double* q, double* scratch, cudaStream_t st, PassTimer* tm, void* s3ctl,
+                          double* full_tmp) {
   Poly P = make_poly(npoly, q);
   const int rows_ps = (int)(g.N / g.n);
   const long chunk = nonlin_chunk_slices(g);
   const bool tl = use_line(g);
   if (tm) tm->used = 0;
+  if (tl && full_tmp && g.dim == 2 && s3_full_x()) {
+    // the x passes over ALL slices in one launch each (an intermediate of the whole state):
+    // no per-chunk launch tails (measured: x passes 7.7 -> 7.2 ms per c5 sweep); the fused
+    // y pass stays in ~512 MB chunks (whole-state launches of it measured 1.6-2x slower)
+    CK(mark(tm, 0, st));
+    CK(line_pass(g, t, P, 0, false, uhat, full_tmp, nslices, st));
+    for (long s0 = 0; s0 < nslices; s0 += chunk) {
+      const long ns = nslices - s0 < chunk ? nslices - s0 : chunk;
+      CK(mark(tm, 2, st));
+      CK(line_pass(g, t, P, 1, true, full_tmp + s0 * g.npad, full_tmp + s0 * g.npad, ns, st));
+    }
+    CK(mark(tm, 0, st));
+    CK(line_pass(g, t, P, 0, false, full_tmp, nhat, nslices, st));
+    CK(mark(tm, -1, st));
+    return cudaSuccess;
+  }
   if (tl && s3ctl && chunk >= 2 && stage3p_supported(g, nslices)) {
     CK(mark(tm, 3, st));
     CK(stage3p(g, t, P, uhat, scratch, s3p_ring(chunk), nhat, nslices, s3ctl, st));
