@@ -144,9 +144,9 @@ expd_status expd_precond_apply(expd_plan* plan, const double* R, double* S);
    inside the call, and the solution's inverse DST runs chunk by chunk while the finished
    chunks stream to the host, so the copy-out overlaps the transform.  Host buffers on a
    distributed plan: INVALID_ARG. */
-/* With on != 0 the solvers ignore the contents of U on entry and start from U = 0 (the
-   paper's zero initial guess), skipping the transform (and, for host U, the
-   copy) of the guess; U is still written with the solution. */
+/* With on != 0 the solvers (and expd_load_state) ignore the contents of U on entry and start
+   from U = 0 (the paper's zero initial guess), skipping the transform (and, for
+   host U, the copy) of the guess; U is still written with the solution.  Sticky per plan. */
 expd_status expd_set_zero_guess(expd_plan* plan, int on);
 
 /* Preconditioned Richardson / Picard (3.2) from the initial guess in
