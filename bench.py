@@ -499,7 +499,7 @@ def run_ours(args):
                           "peak_source": "measured DFMA loop (profiles/r01_probe_fp64_hbm.txt)", "unit": "TFLOP/s",
                           "frac": tf / FP64_PEAK_TFLOPS, "traffic": tprof.get(f"{cfg.name}:{label}"),
                           "traffic_note": ("ncu dram bytes of the one launch per sweep" if persistent else
-                                           "ncu dram bytes of one 16-slice launch"),
+                                           f"ncu dram bytes of one launch ({slices / max(nlaunch, 1):.0f} slices)"),
                           "hbm_gbs": 16.0 * cfg.N * slices / (ms_sweep * 1e-3) / 1e9 if persistent else None,
                           "ncu": (tprof.get("counters") or {}).get(f"{cfg.name}:{label}"),
                           "algorithmic_flops_per_launch": flops * slices / max(nlaunch, 1),
