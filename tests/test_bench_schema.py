@@ -7,11 +7,11 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def line(name):
-    return json.loads(open(os.path.join(ROOT, "profiles", "r01", name)).read().strip().splitlines()[-1])
+def line(name, rnd="r02"):
+    return json.loads(open(os.path.join(ROOT, "profiles", rnd, name)).read().strip().splitlines()[-1])
 
 
-@pytest.mark.parametrize("name", ["bench_final.json", "bench_final_c4.json", "bench_final_c7se.json"])
+@pytest.mark.parametrize("name", ["bench_final.json", "bench_final_c3.json", "bench_final_c7se.json"])
 def test_bench_line_schema(name):
     d = line(name)
     for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
@@ -37,13 +37,33 @@ def test_bench_line_schema(name):
 def test_default_bench_line_has_cpu_baseline():
     d = line("bench_final.json")
     cb = d["cpu_baseline"]
-    for k in ("value", "unit", "cores", "kind", "sample"):
+    for k in ("value", "unit", "cores", "kind", "sample", "cpu_model", "sweeps"):
         assert k in cb, k
     assert cb["kind"] == "oracle" and cb["cores"] >= 1
+    # whole oracle sweeps (c2, c3), not a scaled sample, carry the value
+    assert set(cb["sweeps"]) == {"c2", "c3"} and cb["value"] == cb["sweeps"]["c3"]["value"]
+
+
+def test_default_roofline_is_the_whole_sweep():
+    """north_star's quantity: the sweep's algorithmic bytes (40 B/dof for c5) over the
+    measured HBM peak; per-kernel lines under `kernels`."""
+    d = line("bench_final.json")
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and r["scope"].startswith("whole sweep") and r["bytes_per_dof"] == 40
+    assert abs(r["achieved"] - r["algorithmic_bytes_per_step"] / (d["ms_per_step"] * 1e-3) / 1e9) < 1e-6 * r["achieved"]
+    assert "k1" in d["kernels"] and "dominant" in d["kernels"]
+
+
+def test_gmres_step_line():
+    d = line("bench_final_c4_gmres.json")
+    r = d["roofline"]
+    assert r["bound"] == "hbm" and len(r["step_ms"]) == d["steps"] == 3
+    assert 0 < r["frac"] <= 1
 
 
 def test_reference_line():
     d = line("bench_reference_final.json")
+    assert d["config"]["workload"] == line("bench_final.json")["config"]["workload"]
     assert d["impl"] == "reference" and d["cpu_baseline"]["kind"] == "oracle"
     assert d["e2e"]["h2d_bytes_per_step"] == 0 and d["e2e"]["d2h_bytes_per_step"] == 0
 
