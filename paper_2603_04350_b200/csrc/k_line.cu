@@ -655,7 +655,14 @@ __device__ __forceinline__ void s3_role(const CUtensorMap* in_map, const CUtenso
           signal(sh[3]);
           sh[3] = -1;
         }
-        while (!ready(item)) __nanosleep(128);
+        const uint64_t t0 = global_ns();  // bounded: a dependency that never completes traps
+        while (!ready(item)) {
+          __nanosleep(128);
+          if (global_ns() - t0 > 4000000000ull) {
+            printf("expd: stage-3 dependency wait timed out (pass %d item %ld)\n", pass, item);
+            __trap();
+          }
+        }
         fence_proxy_async_global();
         line_issue_load<M, AX, 1>(in_map, a, item, cb, &bar[cur], smod_in);
       }
