@@ -748,9 +748,7 @@ extern "C" expd_status expd_dst(expd_plan* p, const double* in, double* out, lon
     long ns = nslices - s0 < chunk ? nslices - s0 : chunk;
     CUDA_TRY(p, dst_slices(p->g, dst_tables(p), in + s0 * p->g.N, false, tmp, true, ns, p->scratch, p->stream));
     // drop the pad column: spectral rows of n+1 doubles -> rows of n doubles
-    CUDA_TRY(p, cudaMemcpy2DAsync(out + s0 * p->g.N, sizeof(double) * p->g.n, tmp, sizeof(double) * p->g.M,
-                                  sizeof(double) * p->g.n, (size_t)ns * (p->g.N / p->g.n),
-                                  cudaMemcpyDeviceToDevice, p->stream));
+    CUDA_TRY(p, repitch(tmp, p->g.M, out + s0 * p->g.N, p->g.n, p->g.n, ns * (p->g.N / p->g.n), p->stream));
   }
   return EXPD_OK;
 }
@@ -761,7 +759,6 @@ extern "C" expd_status expd_nonlin_hat(expd_plan* p, const double* uhat, double*
   if (!uhat || !nhat || nslices < 0) return fail(p, EXPD_ERR_INVALID_ARG, "expd_nonlin_hat: bad args");
   // T1 (nt padded slices: input half, output half) on one GPU; UT / NT when distributed
   const long chunk = p->dist ? p->ntl : p->prob.nt / 2;
-  const size_t row = sizeof(double) * p->g.n, prow = sizeof(double) * p->g.M;
   const size_t rows = (size_t)(p->g.N / p->g.n);
   if (p->dist && !p->nl) return fail(p, EXPD_ERR_UNSUPPORTED, "expd_nonlin_hat: linear distributed plan");
   if (p->cx) return fail(p, EXPD_ERR_UNSUPPORTED, "expd_nonlin_hat: real plans only");
@@ -769,12 +766,9 @@ extern "C" expd_status expd_nonlin_hat(expd_plan* p, const double* uhat, double*
   double* tout = p->dist ? p->NT : p->T1 + chunk * p->g.npad;
   for (long s0 = 0; s0 < nslices; s0 += chunk) {
     const long ns = nslices - s0 < chunk ? nslices - s0 : chunk;
-    CUDA_TRY(p, cudaMemsetAsync(tin, 0, sizeof(double) * ns * p->g.npad, p->stream));
-    CUDA_TRY(p, cudaMemcpy2DAsync(tin, prow, uhat + s0 * p->g.N, row, row, (size_t)ns * rows, cudaMemcpyDeviceToDevice,
-                                  p->stream));
+    CUDA_TRY(p, repitch(uhat + s0 * p->g.N, p->g.n, tin, p->g.M, p->g.n, (long)(ns * rows), p->stream));
     CUDA_TRY(p, nonlin_slices(p->g, dst_tables(p), tin, tout, ns, p->prob.npoly, p->prob.q, p->scratch, p->stream));
-    CUDA_TRY(p, cudaMemcpy2DAsync(nhat + s0 * p->g.N, row, tout, prow, row, (size_t)ns * rows, cudaMemcpyDeviceToDevice,
-                                  p->stream));
+    CUDA_TRY(p, repitch(tout, p->g.M, nhat + s0 * p->g.N, p->g.n, p->g.n, (long)(ns * rows), p->stream));
   }
   return EXPD_OK;
 }

@@ -169,6 +169,8 @@ cudaError_t scale_copy_cx(const double* x, double sr, double si, double* y, long
 cudaError_t lincomb_add(const double* const* V, int nv, const double* coef_dev, double* x, long len,
                         cudaStream_t st, bool cx = false);
 // complex interleaved slices <-> planar (re, im) slice pairs (complex plans)
+// physical rows (stride n) <-> padded spectral rows (stride M), zeroing the pad (k_vec.cu)
+cudaError_t repitch(const double* in, long in_rs, double* out, long out_rs, int width, long rows, cudaStream_t st);
 cudaError_t cx_split(const double* in, long in_stride, long len, double* out, long out_stride, long nslices,
                      cudaStream_t st);
 cudaError_t cx_merge(const double* in, long in_stride, long len, double* out, long out_stride, long nslices,

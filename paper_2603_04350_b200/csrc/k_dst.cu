@@ -562,16 +562,34 @@ static cudaError_t colpass(const Geom& g, const DstTables& t, const Poly& P, int
   return cols(g.M, col_op(g, ax, in, out, nslices, false), t, P, st);
 }
 
+// EXPD_PHYS_ROWS=1: the physical <-> spectral x pass through k_rows (the round-1 kernel that
+// re-pitches inside the transform) instead of re-pitch copy + TMA row pass (A/B switch)
+static bool phys_rows_kernel() {
+  const char* e = getenv("EXPD_PHYS_ROWS");
+  return e && e[0] == '1';
+}
+
 cudaError_t dst_slices(const Geom& g, const DstTables& t, const double* src, bool src_spectral, double* dst,
                        bool dst_spectral, long nslices, double* scratch, cudaStream_t st) {
   if (nslices <= 0) return cudaSuccess;
   Poly P = make_poly(0, nullptr);
   const int rows_ps = (int)(g.N / g.n);
   const long phys_slice = g.N;
+  // dim >= 2 with the TMA line kernels: the x pass runs as the spectral TMA row pass in place
+  // on padded rows and the physical <-> padded re-pitch is a plain copy pass (physical rows of
+  // n doubles, n odd, are not 16-byte aligned, so TMA cannot read or write them).  Measured
+  // (profiles/r02/phys_x_ab.txt): c5 precond_apply 31.6 -> 30.7 ms, c2 solve 0.197 -> 0.188 ms
+  // against k_rows, which re-pitches inside its (non-TMA) transform.
+  const bool tma_x = use_line(g) && g.dim >= 2 && !phys_rows_kernel();
   if (!src_spectral && dst_spectral) {
     // physical -> spectral: x first (into dst), then strided axes in place
-    RowsOp r{src, phys_slice, g.n, dst, g.npad, g.M, rows_ps, nslices, false, false};
-    CK(rows(g.M, r, t, P, st));
+    if (tma_x) {
+      CK(repitch(src, g.n, dst, g.M, g.n, (long)rows_ps * nslices, st));
+      CK(line_pass(g, t, P, 0, false, dst, dst, nslices, st));
+    } else {
+      RowsOp r{src, phys_slice, g.n, dst, g.npad, g.M, rows_ps, nslices, false, false};
+      CK(rows(g.M, r, t, P, st));
+    }
     for (int ax = 1; ax < g.dim; ++ax) CK(colpass(g, t, P, ax, dst, dst, nslices, st));
     return cudaSuccess;
   }
@@ -585,6 +603,11 @@ cudaError_t dst_slices(const Geom& g, const DstTables& t, const double* src, boo
       for (int ax = 1; ax < g.dim; ++ax) {
         CK(colpass(g, t, P, ax, cur, scratch, ns, st));
         cur = scratch;
+      }
+      if (tma_x) {
+        CK(line_pass(g, t, P, 0, false, cur, scratch, ns, st));
+        CK(repitch(scratch, g.M, dst + s0 * phys_slice, g.n, g.n, (long)rows_ps * ns, st));
+        continue;
       }
       RowsOp r{cur, g.npad, g.M, dst + s0 * phys_slice, phys_slice, g.n, rows_ps, ns, false, false};
       CK(rows(g.M, r, t, P, st));

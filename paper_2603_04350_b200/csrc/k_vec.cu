@@ -327,6 +327,26 @@ cudaError_t lincomb_add(const double* const* V, int nv, const double* coef_dev, 
   return cudaGetLastError();
 }
 
+// rows of `width` doubles at stride in_rs -> stride out_rs (physical <-> padded spectral
+// rows); the pad columns [width, out_rs) of the output are zeroed when out_rs > width.  Each
+// block walks whole rows: coalesced 8-byte accesses (n odd: rows are not 16-byte aligned).
+__global__ void __launch_bounds__(256) k_repitch(const double* __restrict__ in, long in_rs, double* __restrict__ out,
+                                                 long out_rs, int width, long rows) {
+  const int ow = out_rs > width ? (int)out_rs : width;
+  for (long r = blockIdx.x; r < rows; r += gridDim.x) {
+    const double* a = in + r * in_rs;
+    double* b = out + r * out_rs;
+#pragma unroll 4
+    for (int i = threadIdx.x; i < ow; i += blockDim.x) b[i] = i < width ? __ldcs(a + i) : 0.0;
+  }
+}
+cudaError_t repitch(const double* in, long in_rs, double* out, long out_rs, int width, long rows, cudaStream_t st) {
+  if (rows <= 0) return cudaSuccess;
+  const long grid = rows < 148L * 16 ? rows : 148L * 16;
+  k_repitch<<<(unsigned)grid, 256, 0, st>>>(in, in_rs, out, out_rs, width, rows);
+  return cudaGetLastError();
+}
+
 // complex interleaved slices <-> planar (re slice, im slice) pairs: slice t of `in` (len
 // complex entries at stride in_stride doubles) -> slices 2t, 2t+1 of `out` (stride
 // out_stride).  Complex plans run the real DST on the planar pairs (V is real).
