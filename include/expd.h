@@ -81,7 +81,8 @@ typedef struct {
 
 typedef struct {
   int rank, nranks;   /* 1 <= nranks <= 64, nt % nranks == 0                  */
-  void* nccl_comm;    /* ncclComm_t (expd_nccl_comm_init) or NULL when nranks == 1; with
+  void* nccl_comm;    /* ncclComm_t (expd_nccl_comm_init), a host communicator
+                         (expd_host_comm_create), or NULL when nranks == 1; with
                          nranks == 1 and a communicator the distributed schedule runs on one
                          GPU (all-to-alls become local copies) -- used by the GPU tests     */
 } expd_dist;
@@ -221,6 +222,20 @@ expd_status expd_a2a_execute_host(const expd_problem* prob, int rank, int nranks
 expd_status expd_nccl_unique_id(unsigned char id[128]);
 expd_status expd_nccl_comm_init(const unsigned char id[128], int nranks, int rank, int device, void** comm);
 void expd_nccl_comm_destroy(void* comm);
+/* A HOST communicator for expd_dist.nccl_comm: the distributed plan's all-to-alls and
+   allreduces run through host staging buffers and `transport` (the expd_transport of
+   expd_a2a_execute_host, copied; ctx and the callbacks must outlive the communicator)
+   instead of NCCL.  Every exchange blocks the calling thread: group_start synchronizes the
+   stream, sends are staged device -> host and posted, receives land host -> device after
+   group_end.  Allreduces send every rank's partial sums to every other rank and add them
+   in rank order (all ranks hold the same bits).  It exists so the multi-rank plan runs
+   with several processes on ONE GPU (NCCL refuses two ranks per device) and their kernels
+   never wait on one another (tests/test_gpu_multirank.py); NVLink runs use NCCL.
+   INVALID_ARG on a null transport / send / recv / comm or a bad rank. */
+expd_status expd_host_comm_create(const expd_transport* transport, int rank, int nranks, void** comm);
+/* Frees a host communicator (no-op for anything else).  expd_nccl_comm_destroy ignores host
+   communicators. */
+void expd_host_comm_destroy(void* comm);
 
 /* ---- lower-level entry points used by the solver loop and the benchmark -------------- */
 /* Spectral-state sweep, the hot path of one Exp-ParaDiag iteration on data already in

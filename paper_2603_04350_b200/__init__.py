@@ -3,6 +3,6 @@
 libexpd.so (csrc/, C-ABI include/expd.h) holds every kernel; expd.py is the ctypes
 binding.  See DESIGN.md.
 """
-from .expd import EXPORTS, Comm, ExpdError, Plan, Problem, a2a_schedule, layout, load_library  # noqa: F401
+from .expd import EXPORTS, Comm, ExpdError, HostComm, Plan, Problem, a2a_schedule, layout, load_library  # noqa: F401
 
-__all__ = ["Plan", "Problem", "Comm", "ExpdError", "load_library", "layout", "a2a_schedule", "EXPORTS"]
+__all__ = ["Plan", "Problem", "Comm", "HostComm", "ExpdError", "load_library", "layout", "a2a_schedule", "EXPORTS"]

@@ -13,14 +13,20 @@
 //     problem ("naturally parallelizable"), so K1 needs no
 //     communication; norms and GMRES inner products are partial sums + one allreduce.
 // A schedule is plain data (a list of messages), so the same list is executed by NCCL
-// here and by torch.distributed (gloo) in the CPU tests (tests/test_dist_cpu.py).
+// here and by torch.distributed (gloo) in the CPU tests (tests/test_dist_cpu.py).  A host
+// communicator (expd_host_comm_create) runs the device plan's exchanges through host
+// staging buffers and a caller transport instead of NCCL: the multi-rank plan can then be
+// exercised by several processes sharing one GPU (tests/test_gpu_multirank.py), whose
+// kernels never wait on one another -- the hosts exchange the data.
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
 #include <cstdio>
 #include <cstring>
+#include <memory>
 #include <mutex>
+#include <unordered_set>
 #include <vector>
 
 #include "../../include/expd.h"
@@ -219,14 +225,115 @@ struct HostTransport {
   int group_end(std::string& err) { return wrap(t->group_end ? t->group_end(t->ctx) : 0, "group_end", err); }
 };
 
+// ---- host communicators -----------------------------------------------------------------
+struct HostComm {
+  expd_transport t;
+  int rank, nranks;
+};
+static std::mutex g_hc_mu;
+static std::unordered_set<const void*> g_hc;  // live host communicators
+static HostComm* host_comm(void* comm) {
+  std::lock_guard<std::mutex> lk(g_hc_mu);
+  return comm && g_hc.count(comm) ? static_cast<HostComm*>(comm) : nullptr;
+}
+
+static int cuda_fail(cudaError_t e, const char* what, std::string& err) {
+  if (e == cudaSuccess) return EXPD_OK;
+  err = std::string(what) + ": " + cudaGetErrorString(e);
+  return EXPD_ERR_CUDA;
+}
+
+// Device buffers through host staging and a host transport (blocking): group_start waits
+// for the stream (the sources are final), each send copies its device range to a host
+// buffer and posts it, each receive posts a host buffer, and group_end -- once the transport
+// has completed every message -- copies the received buffers to their device ranges.
+struct StagedTransport {
+  HostComm* hc;
+  cudaStream_t st;
+  std::vector<std::unique_ptr<double[]>> bufs;  // alive until group_end returns
+  std::vector<std::pair<double*, std::pair<const double*, long>>> landing;  // device dst, host src, count
+  int self_copy(double* d, const double* s, long n, std::string& err) {
+    return cuda_fail(cudaMemcpyAsync(d, s, sizeof(double) * n, cudaMemcpyDeviceToDevice, st), "a2a self copy", err);
+  }
+  int wrap(int r, const char* what, std::string& err) {
+    if (r == 0) return EXPD_OK;
+    err = std::string("a2a host communicator: ") + what + " failed";
+    return EXPD_ERR_NCCL;
+  }
+  int group_start(std::string& err) {
+    bufs.clear();
+    landing.clear();
+    if (int e = cuda_fail(cudaStreamSynchronize(st), "a2a host communicator", err)) return e;
+    return wrap(hc->t.group_start ? hc->t.group_start(hc->t.ctx) : 0, "group_start", err);
+  }
+  int send(const double* b, long n, int peer, std::string& err) {
+    bufs.emplace_back(new double[n > 0 ? n : 1]);
+    double* h = bufs.back().get();
+    if (int e = cuda_fail(cudaMemcpy(h, b, sizeof(double) * n, cudaMemcpyDeviceToHost), "a2a stage out", err))
+      return e;
+    return wrap(hc->t.send(hc->t.ctx, h, n, peer), "send", err);
+  }
+  int recv(double* b, long n, int peer, std::string& err) {
+    bufs.emplace_back(new double[n > 0 ? n : 1]);
+    double* h = bufs.back().get();
+    landing.push_back({b, {h, n}});
+    return wrap(hc->t.recv(hc->t.ctx, h, n, peer), "recv", err);
+  }
+  int group_end(std::string& err) {
+    if (int e = wrap(hc->t.group_end ? hc->t.group_end(hc->t.ctx) : 0, "group_end", err)) return e;
+    for (const auto& l : landing)
+      if (int e = cuda_fail(cudaMemcpyAsync(l.first, l.second.first, sizeof(double) * l.second.second,
+                                            cudaMemcpyHostToDevice, st), "a2a stage in", err))
+        return e;
+    return cuda_fail(cudaStreamSynchronize(st), "a2a stage in", err);  // before bufs are released
+  }
+};
+
+// Sum over the ranks through a host communicator: every rank sends its count values to
+// every other rank and adds the P contributions in rank order, so all ranks hold the same
+// bits (as NCCL's allreduce guarantees).
+static int host_allreduce(HostComm* hc, double* buf, long count, cudaStream_t st, std::string& err) {
+  const int P = hc->nranks, me = hc->rank;
+  std::vector<double> all((size_t)P * count);
+  if (int e = cuda_fail(cudaMemcpyAsync(all.data() + (size_t)me * count, buf, sizeof(double) * count,
+                                        cudaMemcpyDeviceToHost, st), "allreduce stage out", err))
+    return e;
+  if (int e = cuda_fail(cudaStreamSynchronize(st), "allreduce stage out", err)) return e;
+  const expd_transport& t = hc->t;
+  if (P > 1) {
+    int r = t.group_start ? t.group_start(t.ctx) : 0;
+    for (int q = 0; q < P && r == 0; ++q)
+      if (q != me) r = t.send(t.ctx, all.data() + (size_t)me * count, count, q);
+    for (int q = 0; q < P && r == 0; ++q)
+      if (q != me) r = t.recv(t.ctx, all.data() + (size_t)q * count, count, q);
+    const int r2 = t.group_end ? t.group_end(t.ctx) : 0;
+    if (r || r2) {
+      err = "allreduce: host communicator transport failed";
+      return EXPD_ERR_NCCL;
+    }
+  }
+  std::vector<double> sum(count, 0.0);
+  for (int q = 0; q < P; ++q)
+    for (long i = 0; i < count; ++i) sum[i] += all[(size_t)q * count + i];
+  if (int e = cuda_fail(cudaMemcpyAsync(buf, sum.data(), sizeof(double) * count, cudaMemcpyHostToDevice, st),
+                        "allreduce stage in", err))
+    return e;
+  return cuda_fail(cudaStreamSynchronize(st), "allreduce stage in", err);
+}
+
 int a2a_execute(void* comm, const DistLayout& L, const std::vector<A2AMsg>& sends, const std::vector<A2AMsg>& recvs,
                 const double* src, double* dst, cudaStream_t st, std::string& err, int s_lo, int s_hi) {
+  if (HostComm* hc = host_comm(comm)) {
+    StagedTransport tr{hc, st, {}, {}};
+    return a2a_run(tr, L, sends, recvs, src, dst, err, s_lo, s_hi);
+  }
   NcclTransport tr{comm, st};
   return a2a_run(tr, L, sends, recvs, src, dst, err, s_lo, s_hi);
 }
 
 int allreduce_sum(void* comm, int nranks, double* buf, long count, cudaStream_t st, std::string& err) {
   if (nranks == 1 && !comm) return EXPD_OK;
+  if (HostComm* hc = host_comm(comm)) return host_allreduce(hc, buf, count, st, err);
   NcclApi& a = nccl();
   if (!a.ok || !comm) {
     err = "allreduce: NCCL unavailable";
@@ -357,6 +464,22 @@ extern "C" expd_status expd_nccl_comm_init(const unsigned char id[128], int nran
 }
 
 extern "C" void expd_nccl_comm_destroy(void* comm) {
+  if (host_comm(comm)) return;  // not an NCCL communicator (expd_host_comm_destroy owns it)
   NcclApi& a = nccl();
   if (comm && a.ok) a.CommDestroy((ncclComm_t)comm);
+}
+
+extern "C" expd_status expd_host_comm_create(const expd_transport* transport, int rank, int nranks, void** comm) {
+  if (!transport || !transport->send || !transport->recv || !comm || nranks < 1 || rank < 0 || rank >= nranks)
+    return EXPD_ERR_INVALID_ARG;
+  HostComm* hc = new HostComm{*transport, rank, nranks};
+  std::lock_guard<std::mutex> lk(g_hc_mu);
+  g_hc.insert(hc);
+  *comm = hc;
+  return EXPD_OK;
+}
+
+extern "C" void expd_host_comm_destroy(void* comm) {
+  std::lock_guard<std::mutex> lk(g_hc_mu);
+  if (comm && g_hc.erase(comm)) delete static_cast<HostComm*>(comm);
 }

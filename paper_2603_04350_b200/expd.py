@@ -60,6 +60,8 @@ EXPORTS = [
     "expd_nccl_unique_id",
     "expd_nccl_comm_init",
     "expd_nccl_comm_destroy",
+    "expd_host_comm_create",
+    "expd_host_comm_destroy",
 ]
 
 
@@ -163,6 +165,8 @@ def load_library(path: str = LIB_PATH):
         "expd_nccl_unique_id": (C.c_int, [C.POINTER(C.c_ubyte)]),
         "expd_nccl_comm_init": (C.c_int, [C.POINTER(C.c_ubyte), C.c_int, C.c_int, C.c_int, C.POINTER(vp)]),
         "expd_nccl_comm_destroy": (None, [vp]),
+        "expd_host_comm_create": (C.c_int, [C.POINTER(_Transport), C.c_int, C.c_int, C.POINTER(vp)]),
+        "expd_host_comm_destroy": (None, [vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -249,6 +253,33 @@ def a2a_schedule(problem: Problem, rank: int, nranks: int, direction: int, shift
     return s, r
 
 
+def _make_transport(send, recv, group_start=None, group_end=None):
+    """An expd_transport over Python callables (numpy views of the message buffers); returns
+    the struct and the ctypes callbacks, which must stay referenced while it is in use.  A
+    callable that raises reports failure (status 1) to the library."""
+    import numpy as np
+
+    def view(ptr, n):
+        return np.ctypeslib.as_array(ptr, shape=(int(n),))
+
+    def guard(f):
+        def g(*a):
+            try:
+                return int(f(*a) or 0)
+            except Exception:  # an exception must not cross the C frames
+                import traceback
+
+                traceback.print_exc()
+                return 1
+        return g
+
+    cb = [_GroupFn(guard(lambda ctx: group_start() if group_start else 0)),
+          _SendFn(guard(lambda ctx, ptr, n, peer: send(view(ptr, n), int(peer)))),
+          _SendFn(guard(lambda ctx, ptr, n, peer: recv(view(ptr, n), int(peer)))),
+          _GroupFn(guard(lambda ctx: group_end() if group_end else 0))]
+    return _Transport(None, *cb), cb
+
+
 def a2a_execute_host(problem: Problem, rank: int, nranks: int, direction: int, shift: int, src, dst,
                      send, recv, group_start=None, group_end=None, s_lo: int = 0, s_hi: int = 1 << 30):
     """Run this rank's all-to-all (expd_a2a_execute_host) on host float64 numpy arrays with a
@@ -260,14 +291,7 @@ def a2a_execute_host(problem: Problem, rank: int, nranks: int, direction: int, s
     lib = load_library()
     assert src.dtype == np.float64 and dst.dtype == np.float64 and src.flags.c_contiguous and dst.flags.c_contiguous
 
-    def view(ptr, n):
-        return np.ctypeslib.as_array(ptr, shape=(int(n),))
-
-    cb = [_GroupFn(lambda ctx: int(group_start() or 0) if group_start else 0),
-          _SendFn(lambda ctx, ptr, n, peer: int(send(view(ptr, n), int(peer)) or 0)),
-          _SendFn(lambda ctx, ptr, n, peer: int(recv(view(ptr, n), int(peer)) or 0)),
-          _GroupFn(lambda ctx: int(group_end() or 0) if group_end else 0)]
-    tr = _Transport(None, *cb)
+    tr, cb = _make_transport(send, recv, group_start, group_end)
     dp = C.POINTER(C.c_double)
     st = lib.expd_a2a_execute_host(C.byref(problem._c()), rank, nranks, direction, shift, s_lo, s_hi,
                                    src.ctypes.data_as(dp), dst.ctypes.data_as(dp), C.byref(tr))
@@ -306,6 +330,36 @@ class Comm:
     def close(self):
         if getattr(self, "ptr", None):
             self.lib.expd_nccl_comm_destroy(self.ptr)
+            self.ptr = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class HostComm:
+    """A host communicator (expd_host_comm_create) for distributed plans: the plan's
+    all-to-alls and allreduces go through host buffers and `transport`, an object with
+    send(view, peer), recv(view, peer), group_start(), group_end() (e.g. torch.distributed
+    gloo; tests/test_gpu_multirank.py).  Lets several ranks share one GPU; NVLink runs use
+    Comm (NCCL)."""
+
+    def __init__(self, rank: int, nranks: int, device: int, transport):
+        self.lib = load_library()
+        self.rank, self.nranks, self.device = rank, nranks, device
+        self._tr, self._cb = _make_transport(transport.send, transport.recv, getattr(transport, "group_start", None),
+                                             getattr(transport, "group_end", None))
+        h = C.c_void_p()
+        st = self.lib.expd_host_comm_create(C.byref(self._tr), rank, nranks, C.byref(h))
+        if st != EXPD_OK:
+            raise ExpdError(st, "expd_host_comm_create")
+        self.ptr = h
+
+    def close(self):
+        if getattr(self, "ptr", None):
+            self.lib.expd_host_comm_destroy(self.ptr)
             self.ptr = None
 
     def __del__(self):

@@ -389,3 +389,28 @@ def test_complex_layout_is_the_real_one_doubled(P, dim, n, nt):
         assert lc["mode_off"] == off
         off += lc["mode_len"]
     assert off == 2 * layout(real, 0, P)["npad"]
+
+
+# ------------------------------------------------------------------------------------------
+# the host communicator (expd_host_comm_create): host-only lifecycle and argument checks;
+# tests/test_gpu_multirank.py runs distributed plans through it on the GPU
+# ------------------------------------------------------------------------------------------
+def test_host_comm_lifecycle():
+    import ctypes as C
+
+    from paper_2603_04350_b200 import ExpdError, HostComm
+    from paper_2603_04350_b200.expd import _make_transport, load_library
+
+    tr = GlooTransport()
+    c = HostComm(1, 2, 0, tr)
+    assert c.ptr
+    lib = load_library()
+    lib.expd_nccl_comm_destroy(c.ptr)  # not an NCCL communicator: ignored
+    c.close()
+    c.close()  # idempotent
+    with pytest.raises(ExpdError):
+        HostComm(2, 2, 0, tr)  # rank out of range
+    t, cb = _make_transport(tr.send, tr.recv)
+    h = C.c_void_p()
+    assert lib.expd_host_comm_create(C.byref(t), 0, 0, C.byref(h)) == 1  # nranks < 1
+    assert lib.expd_host_comm_create(None, 0, 1, C.byref(h)) == 1

@@ -1,0 +1,110 @@
+"""The distributed plan with 2 and 4 ranks on the GPU.
+
+NCCL refuses two ranks on one device and this pool gives one GPU, so the ranks here are
+processes sharing cuda:0 whose plans exchange through a HOST communicator
+(expd_host_comm_create over torch.distributed gloo): the same mode-slab K1, time-slab stage 3,
+pipelined all-to-all schedule (message lists, chunking, self pairing) and allreduces as on
+NVLink, with every exchange staged through host memory.  No rank's kernel waits on another's
+-- the hosts move the data between the launches.  Each rank returns its time slab; the
+concatenation is compared with the oracle: the preconditioner apply and the residual at
+1e-11, the solvers with identical iteration counts and solutions within 1e-9.
+
+The shapes keep the solution well above round-off of u0 (at n = 31, nt = 8 the linear c2
+problems decay to 1e-19 of u0 within one step, where a relative comparison means nothing).
+The uneven mode splits are the point: n odd and P a power of two, so the x-line units never
+divide evenly (31 lines over 2 ranks: 16 + 15), incl. the complex 2D case whose staging
+buffers once overflowed on ranks with the short slab.
+"""
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+
+import synth
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import torch.distributed as dist  # noqa: E402
+
+from test_dist_cpu import GlooTransport, _cfg, _init, _spawn  # noqa: E402
+
+SOLVERS = {"fixed_point": {}, "gmres": {"restart": 20}, "bicgstab": {}}
+
+
+def _worker(rank, P, port, name, n, nt, solvers, out_dir):
+    _init(rank, P, port)
+    try:
+        from paper_2603_04350_b200 import HostComm, Plan, Problem
+
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda:0")
+        cfg = _cfg(name, n, nt)
+        prob = Problem.from_config(cfg)
+        comm = HostComm(rank, P, 0, GlooTransport())
+        plan = Plan(prob, krylov_vectors=21, comm=comm)
+        t0, ntl = plan.layout["t0"], plan.layout["nt_local"]
+
+        def T(x):
+            return torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+
+        out = {}
+        R = synth.random_spacetime(cfg)
+        out["S"] = plan.precond_apply(T(R[t0:t0 + ntl])).cpu().numpy()
+        u0 = synth.initial_condition(cfg)
+        U = synth.random_spacetime(cfg, scale=0.5)
+        Rg, rn2 = plan.residual(T(u0), T(U[t0:t0 + ntl]), norm=True)
+        out["R"], out["rn2"] = Rg.cpu().numpy(), np.array(rn2)
+        for sv in solvers:
+            Us, rep = getattr(plan, sv + "_solve")(T(u0), tol=cfg.tol, maxit=50, **SOLVERS[sv])
+            out["U_" + sv] = Us.cpu().numpy()
+            out["its_" + sv] = np.array([rep["iterations"], int(rep["converged"])])
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), **out)
+        del plan
+        comm.close()
+    finally:
+        dist.destroy_process_group()
+
+
+def relmax(got, want):
+    return float(np.abs(got - want).max() / max(np.abs(want).max(), 1e-300))
+
+
+@pytest.mark.parametrize("P,name,n,nt,solvers", [
+    (2, "c7se", 31, 8, ("fixed_point", "gmres", "bicgstab")),  # complex 2D, 16 + 15 x-lines
+    (2, "c5", 63, 8, ("fixed_point",)),                         # ETD2 Picard: stage 3 on time slabs
+    (2, "c2bdf2", 63, 64, ("fixed_point", "gmres")),            # exponential BDF2 (NEXT-2)
+    (2, "c2", 63, 64, ("bicgstab",)),                           # real BiCGStab (NEXT-4)
+    (2, "c5if", 31, 8, ("fixed_point",)),                       # IMEX-type iteration (NEXT-1)
+    (4, "c5", 31, 8, ("fixed_point",)),                         # 4 ranks: 8 + 8 + 8 + 7 lines
+    (4, "c4", 15, 64, ("gmres",)),                              # 3D GMRES over 4 mode slabs
+    (2, "c1", None, None, ("fixed_point", "gmres")),            # 1D: mode pairs, not x-lines
+])
+def test_multirank_parity(orc, tmp_path, P, name, n, nt, solvers):
+    _spawn(_worker, P, name, n, nt, solvers, str(tmp_path))
+    cfg = _cfg(name, n, nt)
+    s = orc.spec(cfg)
+    got = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(P)]
+    cat = lambda key: np.concatenate([g[key] for g in got])  # noqa: E731
+    cx = cfg.is_complex
+    R = synth.random_spacetime(cfg)
+    want = orc.cplx_precond(s, R) if cx else orc.precond(s, R)[0]
+    assert relmax(cat("S"), want) < 1e-11
+    u0 = synth.initial_condition(cfg)
+    U = synth.random_spacetime(cfg, scale=0.5)
+    want, wn2 = orc.cplx_residual(s, u0, U) if cx else orc.residual(s, u0, U)
+    assert relmax(cat("R"), want) < 1e-11
+    for g in got:  # the allreduced norm: the same bits on every rank
+        assert float(g["rn2"]) == float(got[0]["rn2"]) and abs(float(g["rn2"]) - wn2) < 1e-11 * wn2
+    for sv in solvers:
+        kw = SOLVERS[sv]
+        ref = getattr(orc, ("cplx_" if cx else "") + sv)
+        Uo, st, its, _ = ref(s, u0, tol=cfg.tol, maxit=50, **kw)
+        for g in got:
+            assert g["its_" + sv][1] == 1 and g["its_" + sv][0] == its, sv
+        assert st == 0 and relmax(cat("U_" + sv), Uo) < 1e-9, sv
