@@ -175,21 +175,27 @@ __device__ __forceinline__ void twpow_mul(double2* v, double2 w1) {
   }
 }
 
-// tstage with the job's base twiddle w^{k NT/(NS R)} in a register (one job per thread).
-template <int NT, int S, int THREADS, int R, int NS, int DIR>
+// tstage with the job's base twiddle w^{k NT/(NS R)} in a register: JPT jobs per thread
+// (J, J + THREADS, ...), which share k = j mod NS when THREADS / S is a multiple of NS.
+template <int NT, int S, int THREADS, int R, int NS, int DIR, int JPT = 1>
 __device__ __forceinline__ void tstage_pw(const double2* __restrict__ in, double2* __restrict__ out, double2 w1,
                                           int J = threadIdx.x) {
   constexpr int JOBS = S * (NT / R);
-  static_assert(JOBS == THREADS, "one job per thread");
-  const int s = J % S, j = J / S, k = j % NS;
-  double2 v[R];
+  static_assert(JOBS == THREADS * JPT, "JPT jobs per thread");
+  static_assert(JPT == 1 || (THREADS / S) % NS == 0, "the jobs of a thread share their twiddle");
 #pragma unroll
-  for (int r = 0; r < R; ++r) v[r] = in[(j + r * (NT / R)) * S + s];
-  twpow_mul<R, DIR>(v, w1);
-  DFT<R, DIR>::run(v);
-  const int base = (j / NS) * NS * R + k;
+  for (int jt = 0; jt < JPT; ++jt) {
+    const int Jj = J + jt * THREADS;
+    const int s = Jj % S, j = Jj / S, k = j % NS;
+    double2 v[R];
 #pragma unroll
-  for (int r = 0; r < R; ++r) out[(base + r * NS) * S + s] = v[r];
+    for (int r = 0; r < R; ++r) v[r] = in[(j + r * (NT / R)) * S + s];
+    twpow_mul<R, DIR>(v, w1);
+    DFT<R, DIR>::run(v);
+    const int base = (j / NS) * NS * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) out[(base + r * NS) * S + s] = v[r];
+  }
 }
 
 // Last forward stage (radix RL, NS = NT/RL) of two partner jobs ja, jb (their frequency sets
@@ -956,11 +962,20 @@ __global__ void __launch_bounds__(THR, (TmaLayout<NT, THR, NL, NST>::MINB))
 // update): N-hat block and U-hat block (nonlinear forms), U-hat block and a per-group buffer
 // (linear forms).  Requires npairs % S == 0 (full tiles).
 // ---------------------------------------------------------------------------------------
-// the plans with one job per thread in every stage of a 256-thread group (Nt = 256)
+// the plans with one job per thread in the first and partner stages of a 256-thread group
+// and one or two in the middle stages (Nt = 256: 8 x 8 x 4, one; Nt = 128: 8 x 4 x 4, two,
+// whose twiddles coincide)
+template <int NT>
+constexpr int ring_mid_jobs() {
+  using G = TGeo<NT, 256>;
+  return G::S * (NT / TimeCfg<NT>::R1) / 256;
+}
 template <int NT>
 constexpr bool ring_capable() {
   using G = TGeo<NT, 256>;
-  return G::L == 3 && G::S * (NT / TimeCfg<NT>::R1) == 256 && G::S * (G::NSL / 2) == 256;
+  constexpr int jm = ring_mid_jobs<NT>();
+  return G::L == 3 && G::S * G::TPS == 256 && (jm == 1 || jm == 2) && G::S * (NT / TimeCfg<NT>::R1) == 256 * jm &&
+         G::S * (G::NSL / 2) == 256 && (jm == 1 || ((256 / G::S) % G::R0 == 0 && (256 / G::S) % G::RL == 0));
 }
 
 template <int NT, int NL>
@@ -1004,7 +1019,8 @@ __global__ void __launch_bounds__(512, 1)
   using PL = RingLayout<NT, NL>;
   constexpr int L = G::L, R0 = G::R0, RL = G::RL, TPS = G::TPS, S = G::S, GT = 256;
   constexpr int NSL = G::NSL, TILE = PL::TILE, NBUF = PL::NBUF;
-  static_assert(L == 3 && S * (NT / C::R1) == GT && S * (NSL / 2) == GT, "ring kernel: the one-job-per-thread plans");
+  static_assert(ring_capable<NT>(), "ring kernel: one job per thread outside the middle stages");
+  constexpr int JM = ring_mid_jobs<NT>();
   extern __shared__ unsigned char rsm_raw[];
   double2* smem = reinterpret_cast<double2*>(rsm_raw + ((128u - (smem_u32(rsm_raw) & 127u)) & 127u));
   double2* xbuf = smem + NBUF * PL::STAGE;             // [2][XBUF] (linear forms)
@@ -1112,7 +1128,7 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
     for (int r = 0; r < R0; ++r) buf0[(j * R0 + r) * S + s] = y[r];
     named_bar(barid, GT);
-    tstage_pw<NT, S, GT, C::R1, R0, +1>(buf0, buf1, tw[i_fm], tid);
+    tstage_pw<NT, S, GT, C::R1, R0, +1, JM>(buf0, buf1, tw[i_fm], tid);
     named_bar(barid, GT);
     {
       const int ps = s;
@@ -1139,7 +1155,7 @@ __global__ void __launch_bounds__(512, 1)
       }
     }
     named_bar(barid, GT);
-    tstage_pw<NT, S, GT, C::R1, RL, -1>(buf0, buf1, tw[i_im], tid);
+    tstage_pw<NT, S, GT, C::R1, RL, -1, JM>(buf0, buf1, tw[i_im], tid);
     named_bar(barid, GT);
 #pragma unroll
     for (int r = 0; r < R0; ++r) y[r] = buf1[(j + r * TPS) * S + s];
@@ -1202,11 +1218,11 @@ static int k1_variant(int nt) {
   int v = e ? atoi(e) : 0;
   if (v != 2562 && v != 1282 && v != 2561 && v != 5123) v = 0;
   if (v) return v;
-  // default per Nt (measured): Nt = 256 the ring of two warp groups (c5 K1 6.69 -> 6.02 ms,
-  // profiles/r02/), Nt = 128 128-thread CTAs of 8 pairs (more resident CTAs hide the TMA
-  // latency), else 2562; the ring falls back to 2562 for partial tiles
-  if (nt == 256) return 5123;
-  return nt == 128 ? 1282 : 2562;
+  // default per Nt (measured): the ring of two warp groups at Nt = 256 (c5 K1 6.69 -> 6.02 ms)
+  // and Nt = 128 (two middle-stage jobs per thread; c3 K1 0.184 -> 0.167 ms, c7se 1.124 ->
+  // 1.115 ms against 1282, profiles/r02/k1_ring128_ab.txt), else 2562; the ring falls back
+  // to 2562 for partial tiles
+  return nt == 256 || nt == 128 ? 5123 : 2562;
 }
 static bool use_pipe() { return pipe_mode() > 0; }
 
