@@ -43,6 +43,16 @@ if os.environ.get("NCCL_DEBUG", "VERSION").upper() == "VERSION":
 FP64_PEAK_TFLOPS = 34.19
 
 
+def k1_kernel(cfg, lay) -> str:
+    """The K1 kernel the library launches for this plan (csrc/k_time.cuh k1_variant / ring_ok):
+    the ring variant at Nt = 128 / 256 when the mode slab holds whole tiles (16 / 8 pairs),
+    unless EXPD_K1V picks another variant; else the TMA-fed kernel."""
+    v = os.environ.get("EXPD_K1V")
+    ring = v == "5123" if v in ("2562", "1282", "2561", "5123") else cfg.nt in (128, 256)
+    tile = {128: 16, 256: 8}.get(cfg.nt)
+    return "k_time_ring" if ring and tile and (lay["mode_len"] // 2) % tile == 0 else "k_time_tma"
+
+
 def dst_flops_per_line_pair(M: int) -> float:
     """Algorithmic fp64 flops of one DST-I transform of two real lines of length M-1
     ("4 DST-I via half-length complex FFTs at ~25-30 flop/point/axis"): the
@@ -442,8 +452,8 @@ def run_ours(args):
             f"{cfg.name}:k1")
     except Exception:
         k1_ncu = None
-    k1_roof = {"bound": "hbm", "kernel": "k_time_tma (K1: residual + ||r||^2 + alpha-circulant preconditioner + "
-                                        "update, one HBM pass)", "ncu": k1_ncu,
+    k1_roof = {"bound": "hbm", "kernel": f"{k1_kernel(cfg, lay)} (K1: residual + ||r||^2 + alpha-circulant "
+                                        "preconditioner + update, one HBM pass)", "ncu": k1_ncu,
                "achieved": k1_gbs, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
                "frac": k1_gbs / hbm_peak, "traffic": traffic,
                "algorithmic_bytes_per_launch": k1_bytes, "launch_ms": k1_ms, "launches_per_step": 1}
@@ -461,8 +471,9 @@ def run_ours(args):
     except Exception:
         pass
     roofline = {"bound": "hbm", "scope": "whole sweep (north_star: bytes moved per iteration over peak bandwidth)",
-                "kernel": ("sweep = stage 3 (k_line passes: x-IDST, fused y [V, N(u), V], x-DST) + K1 (k_time_tma) + "
-                           "norm reduction" if nl else "sweep = K1 (k_time_tma) + norm reduction"),
+                "kernel": (f"sweep = stage 3 (k_line passes: x-IDST, fused y [V, N(u), V], x-DST) + K1 "
+                           f"({k1_kernel(cfg, lay)}) + norm reduction" if nl
+                           else f"sweep = K1 ({k1_kernel(cfg, lay)}) + norm reduction"),
                 "achieved": sweep_gbs, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s",
                 "frac": sweep_gbs / hbm_peak, "traffic": sweep_traffic,
                 "traffic_note": "ncu dram read+write bytes of one whole sweep (profiles/ncu_traffic.json)",
@@ -657,7 +668,8 @@ def run_gmres(args):
     gbs = sum(per_step) / (dev_ms * 1e-3) / 1e9
     value = cfg.nst * len(steps_ms) / (dev_ms * 1e-3)
     roofline = {"bound": "hbm", "scope": "GMRES Arnoldi steps j = 1..K (SURVEY §8(d.3): 16 + 8(3j+5) B/dof)",
-                "kernel": "k_time_tma (RM_QOP: w = Q_alpha^{-1} Q v_j) + k_multi_dot + 2 x k_axpy_dot (CGS2, ||w||^2)",
+                "kernel": f"{k1_kernel(cfg, lay)} (RM_QOP: w = Q_alpha^{{-1}} Q v_j) + k_multi_dot + 2 x k_axpy_dot "
+                          "(CGS2, ||w||^2)",
                 "achieved": gbs, "peak": hbm_peak, "peak_source": peak_src, "unit": "GB/s", "frac": gbs / hbm_peak,
                 "traffic": None, "algorithmic_bytes_per_step": per_step,
                 "step_ms": steps_ms}

@@ -87,6 +87,20 @@ def relmax(got, want):
 ])
 def test_multirank_parity(orc, tmp_path, P, name, n, nt, solvers):
     _spawn(_worker, P, name, n, nt, solvers, str(tmp_path))
+    _check(orc, tmp_path, P, name, n, nt, solvers)
+
+
+@pytest.mark.parametrize("chunks", ["3", "1", "64"])
+def test_multirank_pipeline_chunks(orc, tmp_path, monkeypatch, chunks):
+    """The pipelined exchange of stage 3 with key ranges that do not divide the time slab
+    (3 over 8 slices: 3 + 3 + 2), one range, and more ranges than slices (read by the
+    spawned ranks from the environment)."""
+    monkeypatch.setenv("EXPD_DIST_CHUNKS", chunks)
+    _spawn(_worker, 2, "c5", 31, 16, ("fixed_point",), str(tmp_path))
+    _check(orc, tmp_path, 2, "c5", 31, 16, ("fixed_point",))
+
+
+def _check(orc, tmp_path, P, name, n, nt, solvers):
     cfg = _cfg(name, n, nt)
     s = orc.spec(cfg)
     got = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(P)]
