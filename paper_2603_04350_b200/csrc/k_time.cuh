@@ -1076,8 +1076,16 @@ __global__ void __launch_bounds__(512, 1)
     double2* buf1 = K1Form<NL>::HASN ? stg : xbuf + grp * PL::XBUF;
     const long pair = tile * S + s;
     const long base = 2 * pair;
+    // an opaque zero OFFSET (not an opaque pointer, which would lose the shared address
+    // space and turn the five twiddle reads into generic LD.E)
+#ifdef EXPD_RING_GENERIC_TW  // A/B: the former opaque pointer
     const double2* tw = stw;
     asm volatile("" : "+l"(tw));
+#else
+    int two = 0;
+    asm volatile("" : "+r"(two));
+    const double2* tw = stw + two;
+#endif
 
     // ---- phase A: residual (+ ||r||^2), Gamma_alpha, forward stage 0 -------------------
     double2 y[R0];
