@@ -62,7 +62,8 @@ struct LGeo {
   static constexpr int JW = 32 / G;           // threads of one line pair inside a warp
   static constexpr int NWB = T / JW;          // warp blocks per line pair
   static constexpr size_t BUFB = ((size_t)G * SWB * 16 + 1023) / 1024 * 1024;  // bytes per buffer
-  static constexpr size_t SMEM = 1024 + NBUF * BUFB + 16 * (size_t)(NWB * G) + 16;
+  // + the two TMA mbarriers and the kWarPoints write-after-read mbarriers
+  static constexpr size_t SMEM = 1024 + NBUF * BUFB + 16 * (size_t)(NWB * G) + 48;
   // resident CTAs per SM: shared memory (228 KB, 1 KB reserved per CTA) and >= EXPD_LINE_REGS
   // registers per thread
 #ifndef EXPD_LINE_REGS
@@ -87,6 +88,42 @@ struct LineArgs {
   double c;            // sqrt(2/M)/2
   Poly poly;
 };
+
+// The write-after-read points of the line transform (a stage reads the buffer, transforms in
+// registers, writes the buffer).  WarSync (default): one __syncthreads before the writes.
+// WarMbar (-DEXPD_WAR_MODE=1): a split barrier on an mbarrier per point -- each warp ARRIVES
+// as soon as its reads are done (release) and WAITS (acquire) only before its writes, so the
+// stage's DFT could overlap the slower warps' reads.  Measured (profiles/r02/war_barrier_ab.txt):
+// dropping the three WAR barriers altogether (wrong results, timing only) would take stage 3
+// from 15.8 to 14.8 ms on c5, but the split barrier is no faster than __syncthreads on c5 and
+// 2 % slower on c3 (the mbarrier arrive / poll traffic goes through the same LSU pipe the
+// transform is bound by).  Point k completes once per use; `ph` carries each point's phase
+// parity (a point cannot complete twice before a warp waits on it: its next completion
+// needs that warp's next arrival).
+struct WarSync {
+  __device__ __forceinline__ void arrive(int) {}
+#ifdef EXPD_EXP_NOWAR  // timing experiment only (tools/gpu_r02s.sh): WRONG results
+  __device__ __forceinline__ void wait(int) {}
+#else
+  __device__ __forceinline__ void wait(int) { __syncthreads(); }
+#endif
+};
+struct WarMbar {
+  uint64_t* b;  // kWarPoints mbarriers, count = warps of the CTA
+  uint32_t ph;
+  __device__ __forceinline__ void arrive(int k) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&b[k]);
+  }
+  __device__ __forceinline__ void wait(int k) {
+    mbar_wait(&b[k], (ph >> k) & 1u);
+    ph ^= 1u << k;
+  }
+};
+constexpr int kWarPoints = 3;  // 0: middle stage, 1: stage 0, 2: last stage -> unpack
+#ifndef EXPD_WAR_MODE
+#define EXPD_WAR_MODE 0  // 0: WarSync in k_line, 1: WarMbar (A/B)
+#endif
 
 template <int PADP>
 __device__ __forceinline__ int lswz(int p) { return p + p / PADP; }
@@ -223,8 +260,8 @@ __device__ __forceinline__ double2& lat(double2* buf, int p, int g) {
 }
 
 // In-place middle Stockham stage (radix R, NS) of the G line pairs in buf.
-template <int M, int G, int R, int NS>
-__device__ __forceinline__ void lmid(double2* buf, const double2* __restrict__ tw, double2 tpre) {
+template <int M, int G, int R, int NS, class W>
+__device__ __forceinline__ void lmid(double2* buf, const double2* __restrict__ tw, double2 tpre, W& war) {
   using D = LGeo<M, G, 1>;
   constexpr int JOBS = G * (M / R);
   constexpr int JT = (JOBS + D::THREADS - 1) / D::THREADS;
@@ -234,15 +271,23 @@ __device__ __forceinline__ void lmid(double2* buf, const double2* __restrict__ t
   for (int jt = 0; jt < JT; ++jt) {
     const int J = threadIdx.x + jt * D::THREADS;
     if (JOBS % D::THREADS == 0 || J < JOBS) {
-      const int g = J % G, jm = J / G, k = jm % NS;
+      const int g = J % G, jm = J / G;
 #pragma unroll
       for (int r = 0; r < R; ++r) v[jt][r] = lat<M, G>(buf, jm + r * (M / R), g);
+    }
+  }
+  war.arrive(0);
+#pragma unroll
+  for (int jt = 0; jt < JT; ++jt) {
+    const int J = threadIdx.x + jt * D::THREADS;
+    if (JOBS % D::THREADS == 0 || J < JOBS) {
+      const int k = (J / G) % NS;
       if (JT == 1) ltwmul_w<R>(tpre, v[jt]);
       else ltwmul<R>(tw, k * TWS, v[jt]);
       DFT<R, -1>::run(v[jt]);
     }
   }
-  __syncthreads();
+  war.wait(0);  // WAR: every warp's reads of buf are done before the writes
 #pragma unroll
   for (int jt = 0; jt < JT; ++jt) {
     const int J = threadIdx.x + jt * D::THREADS;
@@ -259,22 +304,23 @@ __device__ __forceinline__ void lmid(double2* buf, const double2* __restrict__ t
 // line pair g in v; leaves F (already scaled: V x) at natural positions [2jL, 2jL + 2L) in out
 // (F_m sits at position m-1; position M-1 is the spectral pad and returns 0).  Starts with
 // a barrier (buf may still be read by the caller's stage-0 loads).
-template <int M, int G>
+template <int M, int G, class W>
 __device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* buf, double2* wt,
                                       const double2* __restrict__ tw, double2 (&out)[2 * LGeo<M, G, 1>::L],
-                                      const LPre<M, G>& pre) {
+                                      const LPre<M, G>& pre, W& war) {
   using D = LGeo<M, G, 1>;
   constexpr int R0 = D::R0, RL = D::RL, NSL = D::NSL, T = D::T, L = D::L, PADP = D::PADP;
   const int g = threadIdx.x % G, j = threadIdx.x / G;
+  war.arrive(1);  // this warp's stage-0 reads (the caller's) are done
   DFT<R0, -1>::run(v);
-  __syncthreads();
+  war.wait(1);  // WAR: every warp's stage-0 reads are done before the writes
   {
     double2* o0 = buf + lswz<PADP>(j * R0) * G + g;  // R0 = PADP consecutive positions: linear
 #pragma unroll
     for (int r = 0; r < R0; ++r) o0[r * G] = v[r];
   }
   __syncthreads();
-  lmid<M, G, D::RM1, R0>(buf, tw, pre.tmid);
+  lmid<M, G, D::RM1, R0>(buf, tw, pre.tmid, war);
   // last stage on Hermitian partner jobs (ja, jb): frequency sets k = ja + NSL r and
   // jb + NSL r pair up as k <-> M - k; then the unpack into e_k (position 2k-1), w_k (2k)
   constexpr int PJOBS = G * (NSL / 2);
@@ -291,6 +337,15 @@ __device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* 
         va[pt][r] = lat<M, G>(buf, ja + r * NSL, gg);
         vb[pt][r] = lat<M, G>(buf, jb + r * NSL, gg);
       }
+    }
+  }
+  war.arrive(2);
+#pragma unroll
+  for (int pt = 0; pt < PJT; ++pt) {
+    const int PJ = PJT == 1 ? pre.pj : threadIdx.x + pt * D::THREADS;
+    if (PJOBS % D::THREADS == 0 || PJ < PJOBS) {
+      const int pj = PJ / G;
+      const int ja = pj, jb = pj == 0 ? NSL / 2 : NSL - pj;
       if (PJT == 1) {
         ltwmul_w<RL>(pre.ta, va[pt]);
         ltwmul_w<RL>(pre.tb, vb[pt]);
@@ -302,7 +357,7 @@ __device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* 
       DFT<RL, -1>::run(vb[pt]);
     }
   }
-  __syncthreads();
+  war.wait(2);  // WAR: every warp's partner reads are done before the unpack writes
   // unpack into two arrays W[k] = w_k (k = 0..M/2-1) and E[k] = e_k (k = 1..M/2), each
   // padded with one slot per L entries: consecutive threads write consecutive k and the
   // prefix below reads L consecutive entries per thread, both without bank conflicts
@@ -427,9 +482,9 @@ __device__ __forceinline__ void line_issue_store(const CUtensorMap* map, const L
 // The transform of one item (G line pairs) whose input the TMA is bringing into cb (arrival
 // on bar, phase parity): table values, the wait, [V] or [V, N, V], and the result written in
 // the layout the item's TMA store reads.  Every thread of the CTA calls it.
-template <int M, int AX, bool NL, int G>
+template <int M, int AX, bool NL, int G, class W>
 __device__ __forceinline__ void line_item(char* cb, double2* wt, const LineArgs& a, const LPre<M, G>& pre0,
-                                          uint64_t* bar, uint32_t parity) {
+                                          uint64_t* bar, uint32_t parity, W& war) {
   using D = LGeo<M, G, 1>;
   constexpr int R0 = D::R0, T = D::T, L = D::L, PADP = D::PADP;
   const int tid = threadIdx.x;
@@ -479,7 +534,7 @@ __device__ __forceinline__ void line_item(char* cb, double2* wt, const LineArgs&
           v[r] = lpre(buf[q1 * G + g], buf[q2 * G + g], av, a.c);
         }
       });
-      lcore<M, G>(v, buf, wt, tw, out, pre);
+      lcore<M, G>(v, buf, wt, tw, out, pre, war);
       if (NL && pass + 1 < npass) {
         __syncthreads();  // everyone has read (e, w) of pass 0
 #pragma unroll
@@ -540,9 +595,16 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
     prefetch_tmap(&out_map);
     mbar_init(&bar[0], 1);
     mbar_init(&bar[1], 1);
+    if (EXPD_WAR_MODE)
+      for (int k = 0; k < kWarPoints; ++k) mbar_init(&bar[2 + k], D::THREADS / 32);
     mbar_fence_init();
   }
   __syncthreads();
+#if EXPD_WAR_MODE
+  WarMbar war{bar + 2, 0u};
+#else
+  WarSync war;
+#endif
   long item = blockIdx.x;
   if (tid == 0 && item < a.nitems) line_issue_load<M, AX, G>(&in_map, a, item, base, &bar[0]);
 
@@ -555,7 +617,7 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
       bulk_wait_read0();  // the previous item's stores have left the other buffer
       line_issue_load<M, AX, G>(&in_map, a, next, base + (cur ^ 1) * D::BUFB, &bar[cur ^ 1]);
     }
-    line_item<M, AX, NL, G>(cb, wt, a, pre, &bar[cur], (uint32_t)((NBUF == 2 ? (it >> 1) : it) & 1));
+    line_item<M, AX, NL, G>(cb, wt, a, pre, &bar[cur], (uint32_t)((NBUF == 2 ? (it >> 1) : it) & 1), war);
     fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
@@ -612,6 +674,7 @@ __device__ __forceinline__ void s3_role(const CUtensorMap* in_map, const CUtenso
                                      volatile long* sh, int my_pj) {
   using D = LGeo<M, 1, 2>;
   const int tid = threadIdx.x;
+  WarSync war;  // (the persistent kernel's shared memory carries no WAR mbarriers)
   S3Ctl* ctl = s3.ctl;
   const unsigned per = (unsigned)a.per_slice;
   const unsigned total = per * (unsigned)s3.nslices;
@@ -676,7 +739,7 @@ __device__ __forceinline__ void s3_role(const CUtensorMap* in_map, const CUtenso
       }
       sh[it & 1] = nxt;
     }
-    line_item<M, AX, NL, 1>(cb, wt, a, pre, &bar[cur], (uint32_t)((it >> 1) & 1));
+    line_item<M, AX, NL, 1>(cb, wt, a, pre, &bar[cur], (uint32_t)((it >> 1) & 1), war);
     fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
