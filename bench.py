@@ -562,7 +562,8 @@ def run_ours(args):
                "h2d_bytes_per_step": u0_h.numel() * esz * ws, "d2h_bytes_per_step": cfg.nst * esz,
                "what": f"full fixed-point solve per step ({rep['sweeps']} sweeps, {rep['iterations']} iterations, "
                        f"rel residual {rep['rel_residual']:.2e}) through the C-ABI call with host buffers: H2D of u0, "
-                       f"setup DST, the sweeps, the final IDST streamed to the pinned host U (overlapped D2H)"}
+                       f"setup DST, the sweeps (from the zero guess: the first sweep's stage 3 is skipped, N-hat of "
+                       f"U = 0 being exactly 0), the final IDST streamed to the pinned host U (overlapped D2H)"}
 
     cpu = None
     if rank == 0 and ws == 1 and not args.no_cpu:

@@ -155,7 +155,10 @@ expd_status expd_set_zero_guess(expd_plan* plan, int on);
    ||r^k|| / ||r^0||, U^{k+1} = U^k + Q_alpha^{-1} r^k; stops after the first sweep with
    rho_k < tol (R8), returning U^{k+1} in U.  Blocking.  report (nullable).  On one GPU
    the iteration runs as a CUDA graph with a device-side WHILE loop (the convergence test on
-   the device, one synchronisation per solve). */
+   the device, one synchronisation per solve).  With the zero guess
+   (expd_set_zero_guess) and N(0) = 0 (q[0] = 0) the first sweep's stage 3 is skipped: from
+   U = 0 it would compute N-hat = V N(0) = 0 exactly, so N-hat is zeroed instead (one-GPU
+   plans; bitwise the same iterates; EXPD_S3_SKIP0=0 disables). */
 expd_status expd_fixed_point_solve(expd_plan* plan, const double* u0, double* U, double tol, int maxit,
                                    expd_report* report);
 

@@ -530,6 +530,20 @@ static cudaError_t record(expd_plan* p, int i, cudaStream_t st) {
   return p->capturing ? cudaEventRecordWithFlags(p->ev[i], st, cudaEventRecordExternal) : cudaEventRecord(p->ev[i], st);
 }
 
+// K1 (residual, ||r||^2, preconditioner, update) and the norm reduction of one sweep
+static cudaError_t enqueue_k1(expd_plan* p, cudaStream_t st) {
+  TimeArgs a = time_args(p, p->Uh, p->Uh, true);
+  cudaError_t e = launch_time_fused(a, RM_RESID, OUT_UPDATE, p->k1, p->time_grid, st);
+  if (e != cudaSuccess) return e;
+  if ((e = record(p, 2, st)) != cudaSuccess) return e;
+  return reduce_partials(p->partial, p->time_grid, p->dscal, st);
+}
+
+static bool s3_skip0_enabled() {
+  const char* e = getenv("EXPD_S3_SKIP0");
+  return !(e && e[0] == '0');
+}
+
 static cudaError_t enqueue_sweep(expd_plan* p, cudaStream_t st) {
   cudaError_t e = record(p, 0, st);
   if (e != cudaSuccess) return e;
@@ -546,11 +560,7 @@ static cudaError_t enqueue_sweep(expd_plan* p, cudaStream_t st) {
     if (e != cudaSuccess) return e;
   }
   if ((e = record(p, 1, st)) != cudaSuccess) return e;
-  TimeArgs a = time_args(p, p->Uh, p->Uh, true);
-  e = launch_time_fused(a, RM_RESID, OUT_UPDATE, p->k1, p->time_grid, st);
-  if (e != cudaSuccess) return e;
-  if ((e = record(p, 2, st)) != cudaSuccess) return e;
-  return reduce_partials(p->partial, p->time_grid, p->dscal, st);
+  return enqueue_k1(p, st);
 }
 
 // The distributed sweep: all-to-all U-hat (mode -> time slab), stage 3 on the
@@ -1019,7 +1029,11 @@ static expd_status build_loop_graph(expd_plan* p) {
       const bool prof = p->prof;
       p->prof = false;  // no event records inside the conditional body
       p->capturing = true;
-      cudaError_t e1 = enqueue_sweep(p, p->cap_stream);
+      cudaError_t e1;
+      {
+        LineSkipScope skip(&p->loopst->s3skip);  // stage 3 of the first sweep of a zero-guess solve
+        e1 = enqueue_sweep(p, p->cap_stream);
+      }
       if (e1 == cudaSuccess) e1 = launch_fp_conv(h, p->loopst, p->dscal, p->cap_stream);
       p->capturing = false;
       p->prof = prof;
@@ -1036,7 +1050,13 @@ static expd_status build_loop_graph(expd_plan* p) {
   return EXPD_OK;
 }
 
-static expd_status fixed_point_device_loop(expd_plan* p, double tol, int maxit, expd_report* report) {
+// N-hat of every slice stage 3 writes, zeroed: the first sweep from U-hat = 0 with N(0) = 0
+static cudaError_t zero_stage3_nhat(expd_plan* p) {
+  return cudaMemsetAsync(p->Nh + p->g.npad, 0, sizeof(double) * (size_t)(p->prob.nt - 1 + p->nshift) * p->g.npad,
+                         p->stream);
+}
+
+static expd_status fixed_point_device_loop(expd_plan* p, double tol, int maxit, expd_report* report, bool skip0) {
   if (!p->h_loopst) CUDA_TRY(p, cudaMallocHost(&p->h_loopst, sizeof(FpLoopState)));
   if (!p->loop_exec) {
     expd_status s = build_loop_graph(p);
@@ -1048,6 +1068,8 @@ static expd_status fixed_point_device_loop(expd_plan* p, double tol, int maxit, 
   hs->maxit = maxit;
   hs->r0 = 0.0;
   hs->tol = tol;
+  hs->s3skip = skip0 ? 1 : 0;
+  if (skip0) CUDA_TRY(p, zero_stage3_nhat(p));
   CUDA_TRY(p, cudaMemcpyAsync(p->loopst, hs, offsetof(FpLoopState, hist), cudaMemcpyHostToDevice, p->stream));
   auto t0 = std::chrono::steady_clock::now();
   CUDA_TRY(p, cudaGraphLaunch(p->loop_exec, p->stream));
@@ -1076,6 +1098,10 @@ extern "C" expd_status expd_fixed_point_solve(expd_plan* p, const double* u0, do
   if ((s = solve_in(p, u0, U, io))) return s;
   s = expd_load_state(p, io.u0, io.Uin);
   if (s) return s;
+  // From U-hat = 0 (the zero guess: expd_load_state zeroed it) and N(0) = 0, stage 3 of the
+  // first sweep would compute N-hat = V N(V 0) = 0 exactly: it is skipped and N-hat zeroed
+  // (bitwise the same iterates; EXPD_S3_SKIP0=0 disables, read per solve)
+  const bool skip0 = p->nl && !p->dist && !io.Uin && !(p->prob.npoly > 0 && p->prob.q[0] != 0.0) && s3_skip0_enabled();
   if (!p->dist && graphs_enabled() && device_loop_enabled() && !p->loop_failed && maxit < kFpLoopHist) {
     if (!p->loop_exec && build_loop_graph(p) != EXPD_OK) {
       p->loop_failed = true;  // no conditional-node support: the host-driven loop below
@@ -1084,7 +1110,7 @@ extern "C" expd_status expd_fixed_point_solve(expd_plan* p, const double* u0, do
     }
   }
   if (!p->dist && graphs_enabled() && device_loop_enabled() && !p->loop_failed && maxit < kFpLoopHist) {
-    s = fixed_point_device_loop(p, tol, maxit, report);
+    s = fixed_point_device_loop(p, tol, maxit, report, skip0);
     if (s && s != EXPD_ERR_NOT_CONVERGED) return s;
     expd_status s2 = solve_out(p, U, io);
     return s2 ? s2 : s;
@@ -1096,8 +1122,13 @@ extern "C" expd_status expd_fixed_point_solve(expd_plan* p, const double* u0, do
   int k = 0, conv = 0;
   auto t0 = std::chrono::steady_clock::now();
   for (k = 0; k <= maxit; ++k) {
-    s = sweep(p, graphs);  // the first sweep of a plan runs eagerly, then the captured graph
-    if (s) return s;
+    if (k == 0 && skip0) {  // the first sweep without stage 3 (see skip0)
+      CUDA_TRY(p, zero_stage3_nhat(p));
+      CUDA_TRY(p, enqueue_k1(p, p->stream));
+    } else {
+      s = sweep(p, graphs);  // the first sweep of a plan runs eagerly, then the captured graph
+      if (s) return s;
+    }
     double rn2;
     s = read_scalars(p, 1, &rn2);
     if (s) return s;

@@ -153,6 +153,14 @@ cudaError_t make_tmap_2d(CUtensorMap* m, const double* ptr, unsigned long long c
 cudaError_t line_pass(const Geom& g, const DstTables& t, const Poly& P, int ax, bool nl, const double* in,
                       double* out, long nslices, cudaStream_t st);
 int nonlin_kernel_launches(const Geom& g, long nslices, bool full_tmp = false);
+// While in scope, every k_line launch of this host thread (stage 3 included) reads the device
+// int `flag` first and does nothing if it is non-zero: the device loop skips stage 3 of its
+// first sweep when N-hat is known to be zero (zero guess, N(0) = 0), without a second graph.
+struct LineSkipScope {
+  explicit LineSkipScope(const int* flag);
+  ~LineSkipScope();
+  const int* prev;
+};
 
 // vector kernels (k_vec.cu)
 cudaError_t mode_tables(const Geom& g, const double* lam_axis, double a, double c, double dt, int scheme,
@@ -179,7 +187,8 @@ int vec_grid(int sms);
 // device-side fixed-point loop state (expd_fixed_point_solve's CUDA-graph WHILE loop)
 constexpr int kFpLoopHist = 1024;  // history entries: the device loop takes maxit < kFpLoopHist
 struct FpLoopState {
-  int k, status, maxit, pad;
+  int k, status, maxit;
+  int s3skip;  // stage 3 of the next sweep is skipped (N-hat known to be 0); k_fp_conv clears it
   double r0, tol;
   double hist[kFpLoopHist];
 };

@@ -87,6 +87,7 @@ struct LineArgs {
   const double* sinp;  // [M] sin(pi i/M)
   double c;            // sqrt(2/M)/2
   Poly poly;
+  const int* skip;     // device flag: non-zero -> the launch does nothing (nullable)
 };
 
 // The write-after-read points of the line transform (a stage reads the buffer, transforms in
@@ -578,6 +579,7 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
   using D = LGeo<M, G, NBUF>;
   static_assert(AX != AX_ROW || G == 1, "row items are one row pair");
   constexpr int R0 = D::R0, T = D::T, L = D::L, PADP = D::PADP;
+  if (a.skip && *a.skip) return;  // stage 3 of a sweep whose result is known (line_skip_scope)
   extern __shared__ unsigned char lsm_raw[];
   // 1 KB-aligned base as an offset from the __shared__ array (pointer arithmetic on the
   // array keeps the shared address space: LDS/STS, not generic LD/ST)
@@ -1179,6 +1181,11 @@ static int sm_count() {
   return n > 0 ? n : 148;
 }
 
+// The skip flag the k_line launches of this host thread carry (line_skip_scope).
+static thread_local const int* t_line_skip = nullptr;
+LineSkipScope::LineSkipScope(const int* flag) : prev(t_line_skip) { t_line_skip = flag; }
+LineSkipScope::~LineSkipScope() { t_line_skip = prev; }
+
 template <int M, int AX, bool NL, int G, int NBUF>
 static cudaError_t launch_line(const Geom& g, const DstTables& t, const Poly& P, const double* in, double* out,
                                long nslices, cudaStream_t st) {
@@ -1207,6 +1214,7 @@ static cudaError_t launch_line(const Geom& g, const DstTables& t, const Poly& P,
   a.sinp = t.sinp;
   a.c = 0.5 * sqrt(2.0 / (double)g.M);
   a.poly = P;
+  a.skip = t_line_skip;
   long grid = (long)sm_count() * per_sm;
   if (grid > a.nitems) grid = a.nitems;
   if (grid < 1) return cudaSuccess;

@@ -134,6 +134,7 @@ __global__ void k_fp_conv(cudaGraphConditionalHandle h, FpLoopState* st, const d
       again = 1;
     }
   }
+  st->s3skip = 0;  // only the first sweep of a zero-guess solve skips stage 3
   cudaGraphSetConditional(h, again);
 }
 

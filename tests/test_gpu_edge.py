@@ -123,3 +123,36 @@ def test_gmres_restart_beyond_workspace_is_an_error():
         plan.gmres_solve(u0, tol=1e-12, restart=4)
     U, rep = plan.gmres_solve(u0, tol=1e-12, restart=3)
     assert rep["converged"]
+
+
+@pytest.mark.parametrize("name,n,nt,scheme_note", [("c5", 255, 16, "ETD2"), ("c3", 127, 32, "ETD1"),
+                                                   ("c5if", 127, 16, "IF / IMEX"), ("c5", 63, 256, "Nt = 256")])
+@pytest.mark.parametrize("device_loop", ["1", "0"])
+def test_zero_guess_first_sweep_skips_stage3_bitwise(orc, monkeypatch, name, n, nt, scheme_note, device_loop):
+    """From the zero guess with N(0) = 0 the first sweep's stage 3 is skipped (N-hat = V N(0) =
+    0 exactly): the iterates, the history and the solution are bitwise those of the full first
+    sweep (EXPD_S3_SKIP0=0), on the device loop and on the host loop, and match the oracle."""
+    monkeypatch.setenv("EXPD_DEVICE_LOOP", device_loop)
+    cfg = synth.CONFIGS[name].scaled(n, nt)
+    plan = Plan(Problem.from_config(cfg))
+    plan.set_zero_guess(True)
+    u0 = T(synth.initial_condition(cfg))
+    U1, r1 = plan.fixed_point_solve(u0, tol=cfg.tol, maxit=50)
+    monkeypatch.setenv("EXPD_S3_SKIP0", "0")
+    U2, r2 = plan.fixed_point_solve(u0, tol=cfg.tol, maxit=50)
+    assert r1["iterations"] == r2["iterations"] and r1["hist"] == r2["hist"]
+    assert torch.equal(U1, U2)
+    Uo, st, its, _ = orc.fixed_point(orc.spec(cfg), synth.initial_condition(cfg), tol=cfg.tol, maxit=50)
+    assert st == 0 and r1["iterations"] == its and relmax(H(U1), Uo) < 1e-9
+
+
+def test_nonzero_constant_term_does_not_skip(orc):
+    """N(0) = q0 != 0: the first sweep's N-hat is not zero, so nothing is skipped (matches the
+    oracle)."""
+    cfg = synth.Config("q0", 2, 63, 0.5, 1.0, 0.2, 8, 0.05, scheme=1, q=(0.3, 0.0, 0.0, -1.0))
+    plan = Plan(Problem.from_config(cfg))
+    plan.set_zero_guess(True)
+    u0 = synth.initial_condition(synth.CONFIGS["c5"].scaled(63, 8))
+    U, rep = plan.fixed_point_solve(T(u0), tol=1e-12, maxit=60)
+    Uo, st, its, _ = orc.fixed_point(orc.spec(cfg), u0, tol=1e-12, maxit=60)
+    assert st == 0 and rep["iterations"] == its and relmax(H(U), Uo) < 1e-9
