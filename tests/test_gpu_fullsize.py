@@ -13,6 +13,9 @@
   (orc_dst_sample of orc_nonlin of each physical slice).
 * the largest line (n + 1 = 4096): the converged GPU Picard solution satisfies the oracle's
   all-at-once equations at sampled modes.
+* c4 (255^3 x 64, :10): the preconditioner apply and the residual on inputs made of a few
+  separable sine modes, against the oracle's per-mode formulas at those modes, every other
+  mode at round-off.
 """
 from __future__ import annotations
 
@@ -145,3 +148,52 @@ def test_max_line_length_picard_solution_satisfies_oracle_equations(orc):
     for m, j in enumerate(J):
         r = orc.mode_residual(s, j, uh[:, m], uh0[m], nh[:, m])
         assert np.abs(r).max() < 1e-11 * scale, j
+
+
+
+def test_c4_full_size_primitives_sampled(orc):
+    """c4 (255^3 x 64, BASELINE.json:10, 3-D, the GMRES config) at full size: the
+    preconditioner apply and the residual on inputs made of a few separable sine modes, whose
+    DST coefficients are known, against the oracle's per-mode Steps (a)-(c)
+    and per-mode residual; the outputs are taken to the DST basis by the
+    plan's own DST (parity-tested separately) and every other mode must stay at round-off.
+    (c4's own u0 decays by ~1e-17 per step, so its GMRES solution is checked at reduced size.)"""
+    cfg = synth.CONFIGS["c4"]
+    s = orc.spec(cfg)
+    n, nt = cfg.n, cfg.nt
+    ks = [(1, 1, 1), (2, 3, 1), (5, 1, 7), (40, 90, 3)]  # (k_x, k_y, k_z)
+    x = np.arange(1, n + 1) / (n + 1)
+    Sk = lambda k: np.sin(np.pi * k * x)  # noqa: E731
+    J = [(kz - 1) * n * n + (ky - 1) * n + (kx - 1) for kx, ky, kz in ks]
+    # the orthonormal DST's coefficient of one separable mode (oracle sums, one call per mode)
+    unit = np.array([orc.dst_sample(s, np.multiply.outer(Sk(kz), np.multiply.outer(Sk(ky), Sk(kx))), [j])[0]
+                     for (kx, ky, kz), j in zip(ks, J)])
+    F = [torch.from_numpy(np.stack([Sk(k[a]) for k in ks])).to(DEV) for a in range(3)]  # [mode][n] per axis
+    rng = np.random.default_rng(44)
+
+    def field(C):  # sum_m C[m, t] phi_m as [t][z][y][x] on the device
+        return torch.einsum("mt,mz,my,mx->tzyx", T(C), F[2], F[1], F[0]).contiguous()
+
+    def spectral_at(Y):  # the plan's DST of every slice, at the sampled modes; + the rest
+        Yh = plan.dst(Y).reshape(Y.shape[0], -1)
+        at = H(Yh[:, J])
+        Yh[:, J] = 0.0
+        return at, float(Yh.abs().max())
+
+    plan = Plan(Problem.from_config(cfg))
+    C = rng.standard_normal((len(ks), nt))
+    S = plan.precond_apply(field(C))
+    got, rest = spectral_at(S)
+    want = np.stack([orc.mode_precond(s, j, C[m] * unit[m]) for m, j in enumerate(J)], 1)
+    scale = np.abs(want).max()
+    assert np.abs(got - want).max() < 1e-11 * scale and rest < 1e-11 * scale
+    del S
+    D = 0.5 * rng.standard_normal((len(ks), nt))
+    e0 = rng.standard_normal(len(ks))
+    u0 = field(e0[:, None])[0]
+    R, rn2 = plan.residual(u0, field(D), norm=True)
+    got, rest = spectral_at(R)
+    want = np.stack([orc.mode_residual(s, j, D[m] * unit[m], e0[m] * unit[m]) for m, j in enumerate(J)], 1)
+    scale = np.abs(want).max()
+    assert np.abs(got - want).max() < 1e-11 * scale and rest < 1e-11 * scale
+    assert abs(rn2 - float((want ** 2).sum())) < 1e-11 * rn2
