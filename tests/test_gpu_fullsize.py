@@ -15,7 +15,7 @@
   all-at-once equations at sampled modes.
 * c4 (255^3 x 64, :10): the preconditioner apply and the residual on inputs made of a few
   separable sine modes, against the oracle's per-mode formulas at those modes, every other
-  mode at round-off.
+  mode at round-off; GMRES(3) from a separable u0 against the sequential solution E_J^t u-hat_0.
 """
 from __future__ import annotations
 
@@ -197,3 +197,31 @@ def test_c4_full_size_primitives_sampled(orc):
     scale = np.abs(want).max()
     assert np.abs(got - want).max() < 1e-11 * scale and rest < 1e-11 * scale
     assert abs(rn2 - float((want ** 2).sum())) < 1e-11 * rn2
+
+
+def test_c4_full_size_gmres_separable_modes(orc):
+    """GMRES(3) at c4's full size (the bench's GMRES configuration) from a u0 made of three
+    slowly decaying separable modes: the solution of the all-at-once system is the sequential
+    one, u-hat_t(J) = E_J^(t+1) u-hat_0(J) (slice t holds u_{t+1}), with the
+    oracle's E_J; every other mode stays at round-off."""
+    cfg = synth.CONFIGS["c4"]
+    s = orc.spec(cfg)
+    n, nt = cfg.n, cfg.nt
+    ks = [(1, 1, 1), (2, 1, 1), (1, 2, 2)]
+    x = np.arange(1, n + 1) / (n + 1)
+    Sk = lambda k: np.sin(np.pi * k * x)  # noqa: E731
+    J = [(kz - 1) * n * n + (ky - 1) * n + (kx - 1) for kx, ky, kz in ks]
+    e0 = np.array([1.0, -0.7, 0.4])
+    u0 = sum(c * np.multiply.outer(Sk(kz), np.multiply.outer(Sk(ky), Sk(kx))) for c, (kx, ky, kz) in zip(e0, ks))
+    uh0 = orc.dst_sample(s, u0, J)
+    E = orc.mode_tables(s)[1].reshape(-1)[J]
+    plan = Plan(Problem.from_config(cfg), krylov_vectors=4)
+    plan.set_zero_guess(True)
+    U, rep = plan.gmres_solve(T(u0), tol=cfg.tol, restart=3, maxit=20)
+    assert rep["converged"]
+    Uh = plan.dst(U).reshape(nt, -1)
+    got = H(Uh[:, J])
+    Uh[:, J] = 0.0
+    want = np.stack([E ** (t + 1) * uh0 for t in range(nt)])
+    scale = np.abs(uh0).max()
+    assert np.abs(got - want).max() < 1e-9 * scale and float(Uh.abs().max()) < 1e-11 * scale
