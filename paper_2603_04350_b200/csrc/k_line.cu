@@ -30,6 +30,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <mutex>
+#include <type_traits>
 
 #include "expd_internal.h"
 #include "fft_dev.cuh"
@@ -120,6 +121,12 @@ struct WarMbar {
     mbar_wait(&b[k], (ph >> k) & 1u);
     ph ^= 1u << k;
   }
+};
+// WarNone: the stages read and write different buffers (the ping-pong kernel k_line_pp): no
+// write-after-read hazard, no barrier.
+struct WarNone {
+  __device__ __forceinline__ void arrive(int) {}
+  __device__ __forceinline__ void wait(int) {}
 };
 constexpr int kWarPoints = 3;  // 0: middle stage, 1: stage 0, 2: last stage -> unpack
 #ifndef EXPD_WAR_MODE
@@ -260,9 +267,11 @@ __device__ __forceinline__ double2& lat(double2* buf, int p, int g) {
   return buf[lswz<LGeo<M, G, 1>::PADP>(p) * G + g];
 }
 
-// In-place middle Stockham stage (radix R, NS) of the G line pairs in buf.
+// Middle Stockham stage (radix R, NS) of the G line pairs: reads in, writes buf (in place when
+// they are the same buffer).
 template <int M, int G, int R, int NS, class W>
-__device__ __forceinline__ void lmid(double2* buf, const double2* __restrict__ tw, double2 tpre, W& war) {
+__device__ __forceinline__ void lmid(double2* in, double2* buf, const double2* __restrict__ tw, double2 tpre,
+                                     W& war) {
   using D = LGeo<M, G, 1>;
   constexpr int JOBS = G * (M / R);
   constexpr int JT = (JOBS + D::THREADS - 1) / D::THREADS;
@@ -274,7 +283,7 @@ __device__ __forceinline__ void lmid(double2* buf, const double2* __restrict__ t
     if (JOBS % D::THREADS == 0 || J < JOBS) {
       const int g = J % G, jm = J / G;
 #pragma unroll
-      for (int r = 0; r < R; ++r) v[jt][r] = lat<M, G>(buf, jm + r * (M / R), g);
+      for (int r = 0; r < R; ++r) v[jt][r] = lat<M, G>(in, jm + r * (M / R), g);
     }
   }
   war.arrive(0);
@@ -305,10 +314,13 @@ __device__ __forceinline__ void lmid(double2* buf, const double2* __restrict__ t
 // line pair g in v; leaves F (already scaled: V x) at natural positions [2jL, 2jL + 2L) in out
 // (F_m sits at position m-1; position M-1 is the spectral pad and returns 0).  Starts with
 // a barrier (buf may still be read by the caller's stage-0 loads).
+// Buffers: X takes the stage-0 results (read by the middle stage), Y the middle stage's (read
+// by the last stage), Z the unpacked arrays (read by the prefix scan); one buffer for all three
+// with the WarSync / WarMbar policies, X = Z != Y with WarNone (k_line_pp).
 template <int M, int G, class W>
-__device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* buf, double2* wt,
-                                      const double2* __restrict__ tw, double2 (&out)[2 * LGeo<M, G, 1>::L],
-                                      const LPre<M, G>& pre, W& war) {
+__device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* X, double2* Y, double2* Z,
+                                      double2* wt, const double2* __restrict__ tw,
+                                      double2 (&out)[2 * LGeo<M, G, 1>::L], const LPre<M, G>& pre, W& war) {
   using D = LGeo<M, G, 1>;
   constexpr int R0 = D::R0, RL = D::RL, NSL = D::NSL, T = D::T, L = D::L, PADP = D::PADP;
   const int g = threadIdx.x % G, j = threadIdx.x / G;
@@ -316,12 +328,12 @@ __device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* 
   DFT<R0, -1>::run(v);
   war.wait(1);  // WAR: every warp's stage-0 reads are done before the writes
   {
-    double2* o0 = buf + lswz<PADP>(j * R0) * G + g;  // R0 = PADP consecutive positions: linear
+    double2* o0 = X + lswz<PADP>(j * R0) * G + g;  // R0 = PADP consecutive positions: linear
 #pragma unroll
     for (int r = 0; r < R0; ++r) o0[r * G] = v[r];
   }
   __syncthreads();
-  lmid<M, G, D::RM1, R0>(buf, tw, pre.tmid, war);
+  lmid<M, G, D::RM1, R0>(X, Y, tw, pre.tmid, war);
   // last stage on Hermitian partner jobs (ja, jb): frequency sets k = ja + NSL r and
   // jb + NSL r pair up as k <-> M - k; then the unpack into e_k (position 2k-1), w_k (2k)
   constexpr int PJOBS = G * (NSL / 2);
@@ -335,8 +347,8 @@ __device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* 
       const int ja = pj, jb = pj == 0 ? NSL / 2 : NSL - pj;
 #pragma unroll
       for (int r = 0; r < RL; ++r) {
-        va[pt][r] = lat<M, G>(buf, ja + r * NSL, gg);
-        vb[pt][r] = lat<M, G>(buf, jb + r * NSL, gg);
+        va[pt][r] = lat<M, G>(Y, ja + r * NSL, gg);
+        vb[pt][r] = lat<M, G>(Y, jb + r * NSL, gg);
       }
     }
   }
@@ -362,8 +374,8 @@ __device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* 
   // unpack into two arrays W[k] = w_k (k = 0..M/2-1) and E[k] = e_k (k = 1..M/2), each
   // padded with one slot per L entries: consecutive threads write consecutive k and the
   // prefix below reads L consecutive entries per thread, both without bank conflicts
-  double2* Wb = buf;
-  double2* Eb = buf + D::WS * G;
+  double2* Wb = Z;
+  double2* Eb = Z + D::WS * G;
 #pragma unroll
   for (int pt = 0; pt < PJT; ++pt) {
     const int PJ = PJT == 1 ? pre.pj : threadIdx.x + pt * D::THREADS;
@@ -483,14 +495,19 @@ __device__ __forceinline__ void line_issue_store(const CUtensorMap* map, const L
 // The transform of one item (G line pairs) whose input the TMA is bringing into cb (arrival
 // on bar, phase parity): table values, the wait, [V] or [V, N, V], and the result written in
 // the layout the item's TMA store reads.  Every thread of the CTA calls it.
-template <int M, int AX, bool NL, int G, class W>
-__device__ __forceinline__ void line_item(char* cb, double2* wt, const LineArgs& a, const LPre<M, G>& pre0,
-                                          uint64_t* bar, uint32_t parity, W& war) {
+// PP (ping-pong, k_line_pp): the result goes to a second buffer cbo and the transform's stages
+// alternate between the two (lcore's X = Z = cbo, Y = cb), so no stage writes a buffer that
+// another warp may still be reading: the write-after-read barriers disappear (WarNone).
+// Otherwise cbo == cb and the policy W places them.
+template <int M, int AX, bool NL, int G, class W, bool PP = false>
+__device__ __forceinline__ void line_item(char* cb, char* cbo, double2* wt, const LineArgs& a,
+                                          const LPre<M, G>& pre0, uint64_t* bar, uint32_t parity, W& war) {
   using D = LGeo<M, G, 1>;
   constexpr int R0 = D::R0, T = D::T, L = D::L, PADP = D::PADP;
   const int tid = threadIdx.x;
   const int g = tid % G, j = tid / G;
   double2* buf = reinterpret_cast<double2*>(cb);
+  double2* bufo = reinterpret_cast<double2*>(cbo);
     // the twiddle table is re-read every item: an opaque copy of the pointer keeps the
     // compiler from hoisting loop-invariant twiddles into registers for the whole loop
     const double2* tw = a.tw;
@@ -535,9 +552,9 @@ __device__ __forceinline__ void line_item(char* cb, double2* wt, const LineArgs&
           v[r] = lpre(buf[q1 * G + g], buf[q2 * G + g], av, a.c);
         }
       });
-      lcore<M, G>(v, buf, wt, tw, out, pre, war);
+      lcore<M, G>(v, PP ? bufo : buf, buf, PP ? bufo : buf, wt, tw, out, pre, war);
       if (NL && pass + 1 < npass) {
-        __syncthreads();  // everyone has read (e, w) of pass 0
+        if (!PP) __syncthreads();  // everyone has read (e, w) of pass 0
 #pragma unroll
         for (int q = 0; q < 2 * L; ++q)
           lat<M, G>(buf, 2 * j * L + q, g) =
@@ -545,15 +562,17 @@ __device__ __forceinline__ void line_item(char* cb, double2* wt, const LineArgs&
         __syncthreads();
       }
     }
-    __syncthreads();  // (e, w) reads done before the result overwrites the buffer
+    // (e, w) reads done before the result overwrites their buffer (PP: only the row result
+    // goes to it, and the prefix's cross-warp barrier already ordered them unless NWB == 1)
+    if (!PP || (AX == AX_ROW && D::NWB == 1)) __syncthreads();
     if constexpr (AX == AX_ROW) {
       // rows a / b in the 128B-swizzled box layout: positions [2jL, 2jL+2L) as 16-byte pairs
 #pragma unroll
       for (int l = 0; l < L; ++l) {
         const int x = 2 * j * L + 2 * l;
         const uint32_t off = row_sw(x);
-        *reinterpret_cast<double2*>(cb + off) = make_double2(out[2 * l].x, out[2 * l + 1].x);
-        *reinterpret_cast<double2*>(cb + M * 8 + off) = make_double2(out[2 * l].y, out[2 * l + 1].y);
+        *reinterpret_cast<double2*>(cbo + off) = make_double2(out[2 * l].x, out[2 * l + 1].x);
+        *reinterpret_cast<double2*>(cbo + M * 8 + off) = make_double2(out[2 * l].y, out[2 * l + 1].y);
       }
     } else {
       // chunk -> padded layout (conflict free), then compact in place to the linear [row][G]
@@ -564,20 +583,25 @@ __device__ __forceinline__ void line_item(char* cb, double2* wt, const LineArgs&
       double2 c[R0];
 #pragma unroll
       for (int r = 0; r < R0; ++r) c[r] = lat<M, G>(buf, j + T * r, g);
-      __syncthreads();
+      if (!PP) __syncthreads();
 #pragma unroll
-      for (int r = 0; r < R0; ++r) buf[(j + T * r) * G + g] = c[r];
+      for (int r = 0; r < R0; ++r) bufo[(j + T * r) * G + g] = c[r];
     }
 }
 
 // G line pairs per item, NBUF shared-memory buffers (2: the next item's TMA load overlaps
 // this item's transform; 1: overlap comes from the other CTAs on the SM).
-template <int M, int AX, bool NL, int G, int NBUF>
+// PP: two buffers whose roles alternate per item (input of item i = output of item i - 1);
+// the next item's load is issued once the store has read the output buffer (no prefetch
+// during the transform -- the other CTAs of the SM cover the wait), and the transform runs
+// without write-after-read barriers (line_item PP).
+template <int M, int AX, bool NL, int G, int NBUF, bool PP = false>
 __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::MINB)
     k_line(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
            const __grid_constant__ LineArgs a) {
   using D = LGeo<M, G, NBUF>;
   static_assert(AX != AX_ROW || G == 1, "row items are one row pair");
+  static_assert(!PP || NBUF == 2, "ping-pong needs two buffers");
   constexpr int R0 = D::R0, T = D::T, L = D::L, PADP = D::PADP;
   if (a.skip && *a.skip) return;  // stage 3 of a sweep whose result is known (line_skip_scope)
   extern __shared__ unsigned char lsm_raw[];
@@ -603,27 +627,36 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
   }
   __syncthreads();
 #if EXPD_WAR_MODE
-  WarMbar war{bar + 2, 0u};
+  using WarP = WarMbar;
 #else
-  WarSync war;
+  using WarP = WarSync;
 #endif
+  using WarT = std::conditional_t<PP, WarNone, WarP>;
+  WarT war{};
+  if constexpr (std::is_same_v<WarT, WarMbar>) war = WarMbar{bar + 2, 0u};
   long item = blockIdx.x;
   if (tid == 0 && item < a.nitems) line_issue_load<M, AX, G>(&in_map, a, item, base, &bar[0]);
 
   for (int it = 0; item < a.nitems; ++it, item += gridDim.x) {
     const int cur = NBUF == 2 ? (it & 1) : 0;
     char* cb = base + cur * D::BUFB;
+    char* cbo = PP ? base + (cur ^ 1) * D::BUFB : cb;
     double2* buf = reinterpret_cast<double2*>(cb);
     const long next = item + gridDim.x;
-    if (NBUF == 2 && tid == 0 && next < a.nitems) {
+    if (!PP && NBUF == 2 && tid == 0 && next < a.nitems) {
       bulk_wait_read0();  // the previous item's stores have left the other buffer
       line_issue_load<M, AX, G>(&in_map, a, next, base + (cur ^ 1) * D::BUFB, &bar[cur ^ 1]);
     }
-    line_item<M, AX, NL, G>(cb, wt, a, pre, &bar[cur], (uint32_t)((NBUF == 2 ? (it >> 1) : it) & 1), war);
+    line_item<M, AX, NL, G, WarT, PP>(cb, cbo, wt, a, pre, &bar[cur],
+                                      (uint32_t)((NBUF == 2 ? (it >> 1) : it) & 1), war);
     fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
-      line_issue_store<M, AX, G>(&out_map, a, item, cb);
+      line_issue_store<M, AX, G>(&out_map, a, item, cbo);
+      if (PP && next < a.nitems) {
+        bulk_wait_read0();  // the store has read the output buffer: it is the next input
+        line_issue_load<M, AX, G>(&in_map, a, next, cbo, &bar[cur ^ 1]);
+      }
       if (NBUF == 1 && next < a.nitems) {
         bulk_wait_read0();  // the store has read the buffer: refill it
         line_issue_load<M, AX, G>(&in_map, a, next, base, &bar[0]);
@@ -741,7 +774,7 @@ __device__ __forceinline__ void s3_role(const CUtensorMap* in_map, const CUtenso
       }
       sh[it & 1] = nxt;
     }
-    line_item<M, AX, NL, 1>(cb, wt, a, pre, &bar[cur], (uint32_t)((it >> 1) & 1), war);
+    line_item<M, AX, NL, 1>(cb, cb, wt, a, pre, &bar[cur], (uint32_t)((it >> 1) & 1), war);
     fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
@@ -1186,11 +1219,11 @@ static thread_local const int* t_line_skip = nullptr;
 LineSkipScope::LineSkipScope(const int* flag) : prev(t_line_skip) { t_line_skip = flag; }
 LineSkipScope::~LineSkipScope() { t_line_skip = prev; }
 
-template <int M, int AX, bool NL, int G, int NBUF>
+template <int M, int AX, bool NL, int G, int NBUF, bool PP = false>
 static cudaError_t launch_line(const Geom& g, const DstTables& t, const Poly& P, const double* in, double* out,
                                long nslices, cudaStream_t st) {
   using D = LGeo<M, G, NBUF>;
-  auto k = k_line<M, AX, NL, G, NBUF>;
+  auto k = k_line<M, AX, NL, G, NBUF, PP>;
   static DevOnce once;  // per instantiation and device
   int per_sm = 1;
   if (cudaError_t e = smem_optin(once, k, D::SMEM, D::THREADS, &per_sm); e != cudaSuccess) return e;
@@ -1247,6 +1280,8 @@ static cudaError_t launch_col(const Geom& g, const DstTables& t, const Poly& P, 
       case 21: return launch_line<M, AX, NL, 2, 1>(g, t, P, in, out, nslices, st);
       case 22: return launch_line<M, AX, NL, 2, 2>(g, t, P, in, out, nslices, st);
       case 41: return launch_line<M, AX, NL, 4, 1>(g, t, P, in, out, nslices, st);
+      case 13: return launch_line<M, AX, NL, 1, 2, true>(g, t, P, in, out, nslices, st);  // ping-pong
+      case 23: return launch_line<M, AX, NL, 2, 2, true>(g, t, P, in, out, nslices, st);
       default:
         if constexpr (NL) return launch_line<M, AX, NL, 1, 2>(g, t, P, in, out, nslices, st);
         else return launch_line<M, AX, NL, 2, 2>(g, t, P, in, out, nslices, st);
@@ -1318,6 +1353,7 @@ static cudaError_t line_pass_m(const Geom& g, const DstTables& t, const Poly& P,
       rv = e ? atoi(e) : 2;
     }
     if (rv == 1) return launch_line<M, AX_ROW, false, 1, 1>(g, t, P, in, out, nslices, st);
+    if (rv == 3) return launch_line<M, AX_ROW, false, 1, 2, true>(g, t, P, in, out, nslices, st);  // ping-pong
     return launch_line<M, AX_ROW, false, 1, 2>(g, t, P, in, out, nslices, st);
   }
   if (ax == AX_COL_Y)
