@@ -422,3 +422,43 @@ def test_opt_in_variants_match_default(orc, env, monkeypatch):
         idx = np.random.default_rng(58).integers(0, cfg.N, 16)
         want = orc.dst_sample(s, orc.nonlin(s, orc.dst(s, uh[0])), idx)
         assert np.abs(got[0][idx] - want).max() < 1e-12 * np.abs(got[0]).max()
+
+
+@pytest.mark.parametrize("env", [{"EXPD_COLV": "13", "EXPD_ROWV": "3"}, {"EXPD_COLV": "11", "EXPD_ROWV": "1"},
+                                 {"EXPD_COLV": "22"}])
+def test_line_launch_variants_match_oracle(tmp_path, env):
+    """The line kernels' launch variants read once per process (EXPD_COLV / EXPD_ROWV: the
+    ping-pong buffers, one buffer per CTA, two column pairs per item), each in a fresh process:
+    the c5 Picard solve at n + 1 = 2048 takes the oracle's iterations, and stage 3 matches the
+    oracle at sampled modes."""
+    import os
+    import subprocess
+    import sys
+
+    code = """
+import sys; sys.path.insert(0, '.')
+import numpy as np, torch, synth, oracle
+from paper_2603_04350_b200 import Plan, Problem
+cfg = synth.CONFIGS['c5'].scaled(2047, 4)
+s = oracle.spec(cfg)
+plan = Plan(Problem.from_config(cfg))
+uh = np.random.default_rng(57).standard_normal((1,) + cfg.shape) / np.sqrt(cfg.N)
+got = plan.nonlin_hat(torch.from_numpy(uh).cuda()).cpu().numpy().reshape(1, -1)
+idx = np.random.default_rng(58).integers(0, cfg.N, 16)
+want = oracle.dst_sample(s, oracle.nonlin(s, oracle.dst(s, uh[0])), idx)
+err = np.abs(got[0][idx] - want).max() / np.abs(got[0]).max()
+assert err < 1e-12, err
+small = synth.CONFIGS['c5'].scaled(255, 8)
+p2 = Plan(Problem.from_config(small))
+u0 = synth.initial_condition(small)
+U, rep = p2.fixed_point_solve(torch.from_numpy(u0).cuda(), tol=small.tol, maxit=50)
+Uo, st, its, _ = oracle.fixed_point(oracle.spec(small), u0, tol=small.tol, maxit=50)
+e2 = np.abs(U.cpu().numpy() - Uo).max() / np.abs(Uo).max()
+assert rep['converged'] and rep['iterations'] == its and e2 < 1e-9, (rep['iterations'], its, e2)
+print('ok', err, e2)
+"""
+    full_env = dict(os.environ, **env)
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], cwd=root, env=full_env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stdout + r.stderr
