@@ -70,7 +70,18 @@ def _stale(target, deps):
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
+def build(force: bool = False, verbose: bool = False, checked: bool = False) -> str:
+    """checked: the bounds-checked library (-DEXPD_CHECKS, device-side EXPD_CHECK asserts that
+    print and trap) -> libexpd_checked.so next to libexpd.so; load it with EXPD_LIB."""
+    global BUILD, LIB, NVCC_FLAGS
+    if checked:
+        saved = BUILD, LIB, NVCC_FLAGS
+        BUILD, LIB = BUILD + "_checked", LIB.replace("libexpd.so", "libexpd_checked.so")
+        NVCC_FLAGS = NVCC_FLAGS + ["-DEXPD_CHECKS"]
+        try:
+            return build(force, verbose)
+        finally:
+            BUILD, LIB, NVCC_FLAGS = saved
     os.makedirs(BUILD, exist_ok=True)
     hdrs = _headers()
     jobs = []
@@ -104,4 +115,4 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    print(build(force="--force" in sys.argv, verbose=True, checked="--checked" in sys.argv))

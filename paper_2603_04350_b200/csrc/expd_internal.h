@@ -5,9 +5,27 @@
 
 #include <atomic>
 #include <cstddef>
+#include <cstdio>
 #include <cstdint>
 #include <string>
 #include <vector>
+
+// Device-side bounds checks of the checked build (python -m paper_2603_04350_b200.build
+// --checked -> libexpd_checked.so, compiled with -DEXPD_CHECKS; the default build compiles
+// them out).  A failed check prints what and where, then traps -- the stand-in for
+// compute-sanitizer, which this GPU pool does not allow.
+#ifdef EXPD_CHECKS
+#define EXPD_CHECK(cond, what)                                                                              \
+  do {                                                                                                      \
+    if (!(cond)) {                                                                                          \
+      printf("expd check failed: %s (%s:%d) block %d thread %d\n", what, __FILE__, __LINE__, (int)blockIdx.x, \
+             (int)threadIdx.x);                                                                             \
+      __trap();                                                                                             \
+    }                                                                                                       \
+  } while (0)
+#else
+#define EXPD_CHECK(cond, what) ((void)0)
+#endif
 
 namespace expd {
 

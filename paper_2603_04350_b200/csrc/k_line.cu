@@ -264,6 +264,7 @@ __device__ __forceinline__ int partner_job(int tid) {
 // position p of line pair g in the padded work layout [SW][G]
 template <int M, int G>
 __device__ __forceinline__ double2& lat(double2* buf, int p, int g) {
+  EXPD_CHECK(p >= 0 && p < M && g >= 0 && g < G, "line: padded position");
   return buf[lswz<LGeo<M, G, 1>::PADP>(p) * G + g];
 }
 
@@ -387,6 +388,7 @@ __device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* 
         double2 e, w;
         const int ka = ja + NSL * r;
         lunpack(va[pt][r], pj == 0 ? va[pt][(RL - r) % RL] : vb[pt][RL - 1 - r], ka == 0, e, w);
+        EXPD_CHECK(lswz<L>(ka) < D::WS && lswz<L>(jb + NSL * r) < D::WS, "line: unpack index");
         if (ka >= 1) Eb[lswz<L>(ka) * G + gg] = e;
         Wb[lswz<L>(ka) * G + gg] = w;
         const int kb = jb + NSL * r;
@@ -438,6 +440,7 @@ __device__ __forceinline__ void line_coords(const LineArgs& a, long item, int& c
                                             int smod = 0) {
   // 32-bit unsigned arithmetic (item counts stay far below 2^32): a 64-bit division is a
   // long software sequence on the issuing thread's critical path to the TMA
+  EXPD_CHECK(item >= 0 && item < a.nitems, "line: item index");
   const unsigned it = (unsigned)item, ps = (unsigned)a.per_slice;
   const unsigned s = it / ps;
   const int w = (int)(it - s * ps);
@@ -540,6 +543,7 @@ __device__ __forceinline__ void line_item(char* cb, char* cbo, double2* wt, cons
           // and of the mirror at M - i - 1 each cover 16 consecutive doubles, i.e. 32
           // distinct banks (the 128-byte swizzle splits the i - 1 run over two lines)
           const uint32_t o1 = (uint32_t)(i - 1) * 8u, o2 = (uint32_t)(M - i - 1) * 8u;
+          EXPD_CHECK(o1 < M * 8u && o2 < M * 8u, "line: row stage-0 read");
           const double2 z = make_double2(*reinterpret_cast<const double*>(cb + o1),
                                          *reinterpret_cast<const double*>(cb + M * 8 + o1));
           const double2 zm = make_double2(*reinterpret_cast<const double*>(cb + o2),
@@ -549,6 +553,7 @@ __device__ __forceinline__ void line_item(char* cb, char* cbo, double2* wt, cons
           // pass 0: raw [row][G] linear; pass 1: the padded layout written by the N step
           const int p1 = i - 1, p2 = M - i - 1;
           const int q1 = pass ? lswz<PADP>(p1) : p1, q2 = pass ? lswz<PADP>(p2) : p2;
+          EXPD_CHECK(q1 >= 0 && q2 >= 0 && q1 < D::SWB && q2 < D::SWB, "line: column stage-0 read");
           v[r] = lpre(buf[q1 * G + g], buf[q2 * G + g], av, a.c);
         }
       });
@@ -571,6 +576,7 @@ __device__ __forceinline__ void line_item(char* cb, char* cbo, double2* wt, cons
       for (int l = 0; l < L; ++l) {
         const int x = 2 * j * L + 2 * l;
         const uint32_t off = row_sw(x);
+        EXPD_CHECK(off + 16u <= M * 8u, "line: row result slot");
         *reinterpret_cast<double2*>(cbo + off) = make_double2(out[2 * l].x, out[2 * l + 1].x);
         *reinterpret_cast<double2*>(cbo + M * 8 + off) = make_double2(out[2 * l].y, out[2 * l + 1].y);
       }

@@ -429,7 +429,9 @@ __global__ void __launch_bounds__(EXPD_K1_THREADS, EXPD_K1_MINB) k_time_fused(co
           if constexpr (EXPD_K1_REREAD) sv = cadd(ld2(a.X + (long)t * npad + base), sv);  // L2 hit
           else sv = cadd(xv[r], sv);
         }
-        st2(a.Y + (long)t * npad + base, sv);
+        EXPD_CHECK(base >= 0 && base + 1 < npad && t < NT, "K1: store index");
+        EXPD_CHECK(base >= 0 && base + 1 < npad && t < NT, "K1 ring: store index");
+      st2(a.Y + (long)t * npad + base, sv);
       }
     }
   }
@@ -655,6 +657,7 @@ __global__ void __launch_bounds__(EXPD_K1_THREADS, DB ? 1 : 2) k_time_pipe(const
         const int t = j + r * TPS;
         double2 sv = cscale(y[r], sgi[t]);
         if constexpr (OUTM == OUT_UPDATE) sv = cadd(X[t * S + s], sv);
+        EXPD_CHECK(base >= 0 && base + 1 < npad && t < NT, "K1: store index");
         st2(a.Y + (long)t * npad + base, sv);
       }
     }
@@ -927,6 +930,7 @@ __global__ void __launch_bounds__(THR, (TmaLayout<NT, THR, NL, NST>::MINB))
         const int t = j + r * TPS;
         double2 sv = cscale(y[r], sgi[t]);
         if constexpr (OUTM == OUT_UPDATE) sv = cadd(xv[r], sv);
+        EXPD_CHECK(base >= 0 && base + 1 < npad && t < NT, "K1: store index");
         st2(a.Y + (long)t * npad + base, sv);
       }
     }

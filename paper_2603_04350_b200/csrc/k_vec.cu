@@ -338,7 +338,10 @@ __global__ void __launch_bounds__(256) k_repitch(const double* __restrict__ in, 
     const double* a = in + r * in_rs;
     double* b = out + r * out_rs;
 #pragma unroll 4
-    for (int i = threadIdx.x; i < ow; i += blockDim.x) b[i] = i < width ? __ldcs(a + i) : 0.0;
+    for (int i = threadIdx.x; i < ow; i += blockDim.x) {
+      EXPD_CHECK(i < out_rs && (i >= width || i < in_rs), "repitch: row index");
+      b[i] = i < width ? __ldcs(a + i) : 0.0;
+    }
   }
 }
 cudaError_t repitch(const double* in, long in_rs, double* out, long out_rs, int width, long rows, cudaStream_t st) {
