@@ -44,13 +44,20 @@ FP64_PEAK_TFLOPS = 34.19
 
 
 def k1_kernel(cfg, lay) -> str:
-    """The K1 kernel the library launches for this plan (csrc/k_time.cuh k1_variant / ring_ok):
-    the ring variant at Nt = 128 / 256 when the mode slab holds whole tiles (16 / 8 pairs),
-    unless EXPD_K1V picks another variant; else the TMA-fed kernel."""
+    """The K1 kernel the library launches for this plan (csrc/k_time.cuh use_ring): the ring
+    when the mode slab holds whole tiles, at Nt = 128 / 256 always and at Nt = 16 / 32 / 64
+    with at least 16 tiles per SM, unless EXPD_K1V picks a variant; else the TMA-fed kernel."""
+    tile = {16: 64, 32: 64, 64: 32, 128: 16, 256: 8}.get(cfg.nt)
+    npairs = lay["mode_len"] // 2
+    if not tile or npairs % tile:
+        return "k_time_tma"
     v = os.environ.get("EXPD_K1V")
-    ring = v == "5123" if v in ("2562", "1282", "2561", "5123") else cfg.nt in (128, 256)
-    tile = {128: 16, 256: 8}.get(cfg.nt)
-    return "k_time_ring" if ring and tile and (lay["mode_len"] // 2) % tile == 0 else "k_time_tma"
+    if v in ("2562", "1282", "2561", "5123"):
+        return "k_time_ring" if v == "5123" else "k_time_tma"
+    import torch
+
+    sms = torch.cuda.get_device_properties(0).multi_processor_count if torch.cuda.is_available() else 148
+    return "k_time_ring" if cfg.nt >= 128 or npairs // tile >= 16 * sms else "k_time_tma"
 
 
 def dst_flops_per_line_pair(M: int) -> float:

@@ -31,7 +31,7 @@ cudaError_t launch_time_fused(const TimeArgs& a, int rmode, int outmode, int nl,
 template <int NT>
 static void tma_shape(int nl, int& S, int& per_sm, long npairs) {
   if constexpr (ring_capable<NT>()) {
-    if (k1_variant(NT) == 5123 && ring_ok<NT>(npairs)) {  // one 512-thread CTA per SM
+    if (use_ring<NT>(npairs)) {  // one 512-thread CTA per SM
       S = RingLayout<NT, 1>::S;
       per_sm = 1;
       return;

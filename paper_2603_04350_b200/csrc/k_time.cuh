@@ -978,6 +978,8 @@ template <int NT>
 constexpr bool ring_capable() {
   using G = TGeo<NT, 256>;
   constexpr int jm = ring_mid_jobs<NT>();
+  // two-stage plans (Nt = 16 / 32 / 64): one stage-0 job per thread, at most one partner job
+  if (G::L == 2) return G::S * G::TPS == 256 && G::S * (G::NSL / 2) <= 256;
   return G::L == 3 && G::S * G::TPS == 256 && (jm == 1 || jm == 2) && G::S * (NT / TimeCfg<NT>::R1) == 256 * jm &&
          G::S * (G::NSL / 2) == 256 && (jm == 1 || ((256 / G::S) % G::R0 == 0 && (256 / G::S) % G::RL == 0));
 }
@@ -1140,16 +1142,24 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
     for (int r = 0; r < R0; ++r) buf0[(j * R0 + r) * S + s] = y[r];
     named_bar(barid, GT);
-    tstage_pw<NT, S, GT, C::R1, R0, +1, JM>(buf0, buf1, tw[i_fm], tid);
-    named_bar(barid, GT);
-    {
+    // three-stage plans: the forward middle stage buf0 -> buf1, the partner stage reads buf1
+    // and writes buf0; two-stage plans: the partner stage reads buf0 and writes buf1
+    double2* pin = buf0;
+    double2* pout = buf1;
+    if constexpr (L == 3) {
+      tstage_pw<NT, S, GT, C::R1, R0, +1, JM>(buf0, buf1, tw[i_fm], tid);
+      named_bar(barid, GT);
+      pin = buf1;
+      pout = buf0;
+    }
+    if (S * (NSL / 2) == GT || pj < NSL / 2) {
       const int ps = s;
       const int ja = pj, jb = pj == 0 ? NSL / 2 : NSL - pj;
       double2 va[RL], vb[RL];
 #pragma unroll
       for (int r = 0; r < RL; ++r) {
-        va[r] = buf1[(ja + r * NSL) * S + ps];
-        vb[r] = buf1[(jb + r * NSL) * S + ps];
+        va[r] = pin[(ja + r * NSL) * S + ps];
+        vb[r] = pin[(jb + r * NSL) * S + ps];
       }
       twpow_mul<RL, +1>(va, tw[i_pa]);
       twpow_mul<RL, +1>(vb, tw[i_pb]);
@@ -1162,13 +1172,15 @@ __global__ void __launch_bounds__(512, 1)
       DFT<RL, -1>::run(vb);
 #pragma unroll
       for (int r = 0; r < RL; ++r) {
-        buf0[(ja * RL + r) * S + ps] = va[r];
-        buf0[(jb * RL + r) * S + ps] = vb[r];
+        pout[(ja * RL + r) * S + ps] = va[r];
+        pout[(jb * RL + r) * S + ps] = vb[r];
       }
     }
     named_bar(barid, GT);
-    tstage_pw<NT, S, GT, C::R1, RL, -1, JM>(buf0, buf1, tw[i_im], tid);
-    named_bar(barid, GT);
+    if constexpr (L == 3) {
+      tstage_pw<NT, S, GT, C::R1, RL, -1, JM>(buf0, buf1, tw[i_im], tid);
+      named_bar(barid, GT);
+    }
 #pragma unroll
     for (int r = 0; r < R0; ++r) y[r] = buf1[(j + r * TPS) * S + s];
     // every generic write into the buffer is ordered before the refill's async-proxy writes;
@@ -1223,18 +1235,20 @@ static int pipe_mode() {
   }
   return v;
 }
-// Variants: 2562 (default: 256 threads, double-buffered tiles, 1 CTA/SM), 2561 (single
-// stage, 2 CTAs/SM), 1282 (128 threads = 4 pairs per tile).  c5: 7.02 / 7.10 / 11.2 ms.
-static int k1_variant(int nt) {
-  const char* e = getenv("EXPD_K1V");  // read per launch (a tuning / A-B switch)
+// EXPD_K1V (read per launch, a tuning / A-B switch): 5123 the ring, 2562 / 2561 / 1282 the
+// TMA kernel with <threads><stages>; 0 = automatic (use_ring, k1_variant).
+static int k1_env() {
+  const char* e = getenv("EXPD_K1V");
   int v = e ? atoi(e) : 0;
-  if (v != 2562 && v != 1282 && v != 2561 && v != 5123) v = 0;
-  if (v) return v;
-  // default per Nt (measured): the ring of two warp groups at Nt = 256 (c5 K1 6.69 -> 6.02 ms)
-  // and Nt = 128 (two middle-stage jobs per thread; c3 K1 0.184 -> 0.167 ms, c7se 1.124 ->
-  // 1.115 ms against 1282, profiles/r02/k1_ring128_ab.txt), else 2562; the ring falls back
-  // to 2562 for partial tiles
-  return nt == 256 || nt == 128 ? 5123 : 2562;
+  return (v == 2562 || v == 1282 || v == 2561 || v == 5123) ? v : 0;
+}
+// The TMA-kernel variant when the ring is not used: 2562 (256 threads, double-buffered tiles,
+// 1 CTA/SM), 2561 (single stage, 2 CTAs/SM), 1282 (128 threads; round 1's Nt = 128 default).
+// c5: 7.02 / 7.10 / 11.2 ms.
+static int k1_variant(int nt) {
+  const int v = k1_env();
+  if (v && v != 5123) return v;
+  return nt == 128 ? 1282 : 2562;
 }
 static bool use_pipe() { return pipe_mode() > 0; }
 
@@ -1292,11 +1306,36 @@ static bool ring_ok(long npairs) {
   if constexpr (ring_capable<NT>()) return npairs % RingLayout<NT, 1>::S == 0;
   return false;
 }
+static long k1_sms() {
+  static int n[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  dev &= 63;
+  if (!n[dev]) cudaDeviceGetAttribute(&n[dev], cudaDevAttrMultiProcessorCount, dev);
+  return n[dev] > 0 ? n[dev] : 148;
+}
+// The ring (one CTA of two warp groups per SM) or the TMA kernel, measured per plan shape:
+// Nt = 128 / 256 always (c5 K1 6.69 -> 6.02 ms, c3 0.184 -> 0.167, c7se 1.124 -> 1.115 against
+// 1282, profiles/r02/k1_ring128_ab.txt); the two-stage plans (Nt = 16 / 32 / 64) only with at
+// least 16 tiles per SM (c4 GMRES steps 18.66 -> 18.09 ms; c2's 1020 tiles: 0.030 -> 0.033 ms,
+// too few to fill the persistent grid; profiles/r02/k1_ring64_ab.txt).  Partial tiles: TMA.
+template <int NT>
+static bool use_ring(long npairs) {
+  if constexpr (!ring_capable<NT>()) {
+    return false;
+  } else {
+    if (pipe_mode() != 3 || !ring_ok<NT>(npairs)) return false;
+    const int v = k1_env();
+    if (v) return v == 5123;
+    if (NT >= 128) return true;
+    return npairs / RingLayout<NT, 1>::S >= 16L * k1_sms();
+  }
+}
 
 template <int NT, int RM, int OUTM, int NL>
 static cudaError_t launch_t(const TimeArgs& a, int grid, cudaStream_t st) {
   if constexpr (ring_capable<NT>()) {
-    if (pipe_mode() == 3 && k1_variant(NT) == 5123 && ring_ok<NT>(a.npairs)) return launch_ring<NT, RM, OUTM, NL>(a, grid, st);
+    if (use_ring<NT>(a.npairs)) return launch_ring<NT, RM, OUTM, NL>(a, grid, st);
   }
   if constexpr (TimeGeo<NT>::L > 1 && NL >= 3) {  // BDF2 / complex: TMA or register kernel
     if (pipe_mode() == 3) {
