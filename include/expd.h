@@ -240,6 +240,22 @@ expd_status expd_host_comm_create(const expd_transport* transport, int rank, int
    communicators. */
 void expd_host_comm_destroy(void* comm);
 
+/* Peer stores (the fused "NVLink-store transpose" of SURVEY §8(f)):
+   a distributed nonlinear plan's stage 3 can write every row of its x-DST result straight
+   into the N-hat mode slab of the rank that owns the row -- another GPU's memory over NVLink,
+   or another process's on the same GPU -- instead of a local slab plus a time -> mode
+   all-to-all.  Setup, collective over the ranks: every rank exports its slab
+   (expd_plan_nhat_ipc_handle: a CUDA IPC handle of the allocation holding it and the slab's
+   byte offset), the handles are exchanged by the caller (e.g. torch.distributed all_gather),
+   every rank registers every rank's (expd_plan_set_peer_nhat; its own rank maps its own slab),
+   then expd_plan_enable_peer_stores(plan, 1).  Requirements: real coefficients, npoly > 0,
+   dim >= 2, n + 1 >= 256 (the TMA line kernels), <= 16 ranks, mode slabs of whole x-lines.
+   A new workspace disables the peer stores (register again).  UNSUPPORTED / INVALID_ARG /
+   EXPD_ERR_CUDA (e.g. a caching allocator without IPC-able segments). */
+expd_status expd_plan_nhat_ipc_handle(expd_plan* plan, unsigned char handle[64], long* offset_bytes);
+expd_status expd_plan_set_peer_nhat(expd_plan* plan, int rank, const unsigned char handle[64], long offset_bytes);
+expd_status expd_plan_enable_peer_stores(expd_plan* plan, int on);
+
 /* ---- lower-level entry points used by the solver loop and the benchmark -------------- */
 /* Spectral-state sweep, the hot path of one Exp-ParaDiag iteration on data already in
    the workspace (after expd_load_state): [nonlinear: N-hat of every slice (stage 3)] ->

@@ -91,6 +91,12 @@ struct expd_plan {
   // solve, from two events on the plan's stream around the step's kernels
   cudaEvent_t kev[2] = {nullptr, nullptr};
   std::vector<double> kstep_ms;
+  // peer stores of the distributed stage 3 (expd_plan_enable_peer_stores): every rank's N-hat
+  // mode slab (its own, or another process's opened through CUDA IPC) and their tensor maps
+  std::vector<double*> peer_nh;
+  std::vector<void*> peer_ipc;  // IPC-opened allocation bases (closed at destroy)
+  PeerMaps* d_peer = nullptr;
+  bool peer_on = false;
   std::string err;
 };
 
@@ -330,6 +336,7 @@ extern "C" expd_status expd_plan_workspace_bytes(const expd_plan* p, int krylov_
 
 extern "C" expd_status expd_plan_set_workspace(expd_plan* p, void* d_ptr, size_t bytes) {
   if (!p || !d_ptr) return EXPD_ERR_INVALID_ARG;
+  p->peer_on = false;  // the N-hat slab moves: peers register again
   if (((uintptr_t)d_ptr) % kAlign) return fail(p, EXPD_ERR_INVALID_ARG, "workspace must be 256-byte aligned");
   Layout L0 = layout(p, 0);
   if (bytes < L0.total) return fail(p, EXPD_ERR_OOM, "workspace smaller than expd_plan_workspace_bytes(plan, 0)");
@@ -394,6 +401,8 @@ extern "C" void expd_plan_destroy(expd_plan* p) {
   for (cudaEvent_t e : p->tev) cudaEventDestroy(e);
   for (cudaEvent_t e : p->kev)
     if (e) cudaEventDestroy(e);
+  for (void* b : p->peer_ipc) cudaIpcCloseMemHandle(b);
+  cudaFree(p->d_peer);
   cudaFree(p->d_lam);
   cudaFree(p->d_twt);
   cudaFree(p->d_g);
@@ -584,8 +593,25 @@ static int dist_chunks(const expd_plan* p) {
 // on the plan stream once its slices have landed, and its time -> mode all-to-all follows
 // on comm_stream while stage 3 moves on to chunk c + 1.  Every rank posts the same chunk
 // sequence (slice keys), so the NCCL groups match across ranks.
+static expd_status allreduce(expd_plan* p, double* buf, long count);
+
+// Stage 3 with peer stores: the mode -> time all-to-all as usual, then stage 3 of the time slab
+// whose final x-DST pass stores every row straight into its owner's N-hat slab (slot t + 1)
+// -- no local N-hat slab, no time -> mode all-to-all -- and one allreduce as the barrier that
+// orders every rank's stores before any rank's K1 reads them.
+static expd_status stage3_peer(expd_plan* p) {
+  expd_status s;
+  if ((s = a2a(p, A2A_M2T, p->Uh, p->UT))) return s;
+  PeerOut po{p->d_peer, p->t0 + 1};
+  CUDA_TRY(p, nonlin_slices(p->g, dst_tables(p), p->UT, nullptr, p->ntl, p->prob.npoly, p->prob.q, p->scratch,
+                            p->stream, nullptr, nullptr, nullptr, &po));
+  CUDA_TRY(p, cudaMemsetAsync(p->dscal + 500, 0, sizeof(double), p->stream));
+  return allreduce(p, p->dscal + 500, 1);
+}
+
 static expd_status stage3_dist(expd_plan* p) {
   expd_status s;
+  if (p->peer_on) return stage3_peer(p);
   const int nch = dist_chunks(p);
   if (nch <= 1) {
     if ((s = a2a(p, A2A_M2T, p->Uh, p->UT))) return s;
@@ -1458,3 +1484,77 @@ extern "C" expd_status expd_bicgstab_solve(expd_plan* p, const double* u0, doubl
   return bicgstab_impl<double>(p, u0, U, tol, maxit, report);
 }
 
+// ---------------------------------------------------------------------------------------
+// Peer stores of the distributed stage 3 (include/expd.h "Multi-GPU")
+// ---------------------------------------------------------------------------------------
+typedef CUresult (*PFN_addr_range)(CUdeviceptr*, size_t*, CUdeviceptr);
+
+extern "C" expd_status expd_plan_nhat_ipc_handle(expd_plan* p, unsigned char handle[64], long* offset_bytes) {
+  expd_status s = ready(p);
+  if (s) return s;
+  if (!handle || !offset_bytes) return fail(p, EXPD_ERR_INVALID_ARG, "nhat_ipc_handle: bad args");
+  if (!p->dist || !p->Nh) return fail(p, EXPD_ERR_UNSUPPORTED, "nhat_ipc_handle: distributed nonlinear plans only");
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+    return fail(p, EXPD_ERR_CUDA, "cuMemGetAddressRange unavailable");
+  CUdeviceptr base = 0;
+  size_t size = 0;
+  if (((PFN_addr_range)fn)(&base, &size, (CUdeviceptr)p->Nh) != CUDA_SUCCESS)
+    return fail(p, EXPD_ERR_CUDA, "cuMemGetAddressRange failed");
+  cudaIpcMemHandle_t h;
+  CUDA_TRY(p, cudaIpcGetMemHandle(&h, (void*)base));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
+  memcpy(handle, &h, 64);
+  *offset_bytes = (long)((CUdeviceptr)p->Nh - base);
+  return EXPD_OK;
+}
+
+extern "C" expd_status expd_plan_set_peer_nhat(expd_plan* p, int rank, const unsigned char handle[64],
+                                               long offset_bytes) {
+  expd_status s = ready(p);
+  if (s) return s;
+  if (!p->dist || !p->Nh || rank < 0 || rank >= p->L.nranks || p->L.nranks > kMaxPeers || !handle ||
+      offset_bytes < 0)
+    return fail(p, EXPD_ERR_INVALID_ARG, "set_peer_nhat: bad args");
+  if ((int)p->peer_nh.size() != p->L.nranks) p->peer_nh.assign(p->L.nranks, nullptr);
+  if (rank == p->L.rank) {
+    p->peer_nh[rank] = p->Nh;
+    return EXPD_OK;
+  }
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, 64);
+  void* base = nullptr;
+  CUDA_TRY(p, cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  p->peer_ipc.push_back(base);
+  p->peer_nh[rank] = reinterpret_cast<double*>(static_cast<char*>(base) + offset_bytes);
+  return EXPD_OK;
+}
+
+extern "C" expd_status expd_plan_enable_peer_stores(expd_plan* p, int on) {
+  expd_status s = ready(p);
+  if (s) return s;
+  if (!on) {
+    p->peer_on = false;
+    return EXPD_OK;
+  }
+  if (!p->dist || !p->nl || p->cx || p->g.dim < 2 || !line_supported(p->g))
+    return fail(p, EXPD_ERR_UNSUPPORTED, "peer stores: distributed nonlinear real plans, dim >= 2, n + 1 >= 256");
+  if ((int)p->peer_nh.size() != p->L.nranks) return fail(p, EXPD_ERR_INVALID_ARG, "peer stores: peers not set");
+  PeerMaps h{};
+  h.nranks = p->L.nranks;
+  for (int q = 0; q < p->L.nranks; ++q) {
+    if (!p->peer_nh[q]) return fail(p, EXPD_ERR_INVALID_ARG, "peer stores: peer " + std::to_string(q) + " not set");
+    const long M = p->g.M;
+    if (p->L.mode_off[q] % M || p->L.mode_len[q] % M)
+      return fail(p, EXPD_ERR_UNSUPPORTED, "peer stores: mode slabs are not whole x-lines");
+    h.unit_off[q] = (int)(p->L.mode_off[q] / M);
+    h.units[q] = (int)(p->L.mode_len[q] / M);
+    CUDA_TRY(p, peer_nhat_map(&h.m[q], p->g, p->peer_nh[q], h.units[q], p->prob.nt + 1, p->L.mode_len[q]));
+  }
+  if (!p->d_peer) CUDA_TRY(p, cudaMalloc(&p->d_peer, sizeof(PeerMaps)));
+  CUDA_TRY(p, cudaMemcpyAsync(p->d_peer, &h, sizeof(PeerMaps), cudaMemcpyHostToDevice, p->stream));
+  CUDA_TRY(p, cudaStreamSynchronize(p->stream));
+  p->peer_on = true;
+  return EXPD_OK;
+}

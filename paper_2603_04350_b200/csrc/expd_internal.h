@@ -145,9 +145,25 @@ struct PassTimer {
   int used;
   int kind[512];
 };
+// Peer stores of the distributed stage 3 (the fused "NVLink-store transpose"):
+// the final x-DST pass stores each spectral row straight into the N-hat mode slab of the rank
+// that owns it (device memory of another process / GPU, opened through CUDA IPC), at slot
+// slot0 + (slice), instead of a local N-hat slab followed by an all-to-all.  One tensor map
+// per rank (in device memory, 64-byte aligned), rows [unit_off[q], unit_off[q] + units[q]).
+constexpr int kMaxPeers = 16;
+struct PeerMaps {
+  CUtensorMap m[kMaxPeers];
+  int nranks;
+  int unit_off[kMaxPeers];
+  int units[kMaxPeers];
+};
+struct PeerOut {
+  const PeerMaps* maps;  // device
+  int slot0;             // N-hat slot of the launch's first slice
+};
 cudaError_t nonlin_slices(const Geom& g, const DstTables& t, const double* uhat, double* nhat, long nslices,
                           int npoly, const double* q, double* scratch, cudaStream_t st, struct PassTimer* timer = nullptr,
-                          void* s3ctl = nullptr, double* full_tmp = nullptr);
+                          void* s3ctl = nullptr, double* full_tmp = nullptr, const PeerOut* peer = nullptr);
 // persistent stage 3 (k_line.cu): one launch for all slices, intermediate in a ring of K
 // slices (ring: K npad doubles), dependency counters in ctl (stage3p_ctl_bytes(), zeroed by the
 // launch).  PassTimer kind 3 marks it.
@@ -169,7 +185,10 @@ bool tma_available();
 cudaError_t make_tmap_2d(CUtensorMap* m, const double* ptr, unsigned long long cols, unsigned long long rows,
                          unsigned long long row_bytes, unsigned box_cols, unsigned box_rows);
 cudaError_t line_pass(const Geom& g, const DstTables& t, const Poly& P, int ax, bool nl, const double* in,
-                      double* out, long nslices, cudaStream_t st);
+                      double* out, long nslices, cudaStream_t st, const PeerOut* peer = nullptr);
+// the tensor map of one rank's N-hat slab for PeerMaps: units x-lines of M doubles per slot,
+// slots slots, slot stride slot_doubles (the mode-slab length)
+cudaError_t peer_nhat_map(CUtensorMap* m, const Geom& g, double* base, long units, long slots, long slot_doubles);
 int nonlin_kernel_launches(const Geom& g, long nslices, bool full_tmp = false);
 // While in scope, every k_line launch of this host thread (stage 3 included) reads the device
 // int `flag` first and does nothing if it is non-zero: the device loop skips stage 3 of its

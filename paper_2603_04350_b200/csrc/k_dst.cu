@@ -687,13 +687,14 @@ static int s3p_ring(long chunk) {
 
 cudaError_t nonlin_slices(const Geom& g, const DstTables& t, const double* uhat, double* nhat, long nslices,
                           int npoly, const double* q, double* scratch, cudaStream_t st, PassTimer* tm, void* s3ctl,
-                          double* full_tmp) {
+                          double* full_tmp, const PeerOut* peer) {
   Poly P = make_poly(npoly, q);
   const int rows_ps = (int)(g.N / g.n);
   const long chunk = nonlin_chunk_slices(g);
   const bool tl = use_line(g);
   if (tm) tm->used = 0;
-  if (tl && full_tmp && g.dim == 2 && s3_full_x()) {
+  if (peer && (!tl || g.dim < 2)) return cudaErrorInvalidValue;  // peer stores: the line-kernel path
+  if (tl && full_tmp && g.dim == 2 && s3_full_x() && !peer) {
     // the x passes over ALL slices in one launch each (an intermediate of the whole state):
     // no per-chunk launch tails (measured: x passes 7.7 -> 7.2 ms per c5 sweep); the fused
     // y pass stays in ~512 MB chunks (whole-state launches of it measured 1.6-2x slower)
@@ -709,7 +710,7 @@ cudaError_t nonlin_slices(const Geom& g, const DstTables& t, const double* uhat,
     CK(mark(tm, -1, st));
     return cudaSuccess;
   }
-  if (tl && s3ctl && chunk >= 2 && stage3p_supported(g, nslices)) {
+  if (tl && s3ctl && chunk >= 2 && stage3p_supported(g, nslices) && !peer) {
     CK(mark(tm, 3, st));
     CK(stage3p(g, t, P, uhat, scratch, s3p_ring(chunk), nhat, nslices, s3ctl, st));
     CK(mark(tm, -1, st));
@@ -734,7 +735,12 @@ cudaError_t nonlin_slices(const Geom& g, const DstTables& t, const double* uhat,
         CK(line_pass(g, t, P, 1, false, scratch, scratch, ns, st));
       }
       CK(mark(tm, 0, st));
-      CK(line_pass(g, t, P, 0, false, scratch, out, ns, st));
+      if (peer) {
+        PeerOut po{peer->maps, peer->slot0 + (int)s0};
+        CK(line_pass(g, t, P, 0, false, scratch, nullptr, ns, st, &po));
+      } else {
+        CK(line_pass(g, t, P, 0, false, scratch, out, ns, st));
+      }
       continue;
     }
     if (g.dim == 1) {

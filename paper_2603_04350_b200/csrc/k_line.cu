@@ -89,6 +89,8 @@ struct LineArgs {
   double c;            // sqrt(2/M)/2
   Poly poly;
   const int* skip;     // device flag: non-zero -> the launch does nothing (nullable)
+  const PeerMaps* peer;  // ROW only: store each row into its owner's N-hat slab (nullable)
+  int peer_slot0;        // ... at slot peer_slot0 + slice
 };
 
 // The write-after-read points of the line transform (a stage reads the buffer, transforms in
@@ -482,8 +484,21 @@ __device__ __forceinline__ void line_issue_store(const CUtensorMap* map, const L
   int c0, c1, c2, c3;
   line_coords<AX, G>(a, item, c0, c1, c2, c3, smod);
   if constexpr (AX == AX_ROW) {
-    tma_store_4d(map, buf, 0, 0, c2, c3);
-    if (c2 + 1 < a.rows) tma_store_4d(map, buf + M * 8, 0, 0, c2 + 1, c3);
+    if (a.peer) {  // each row to the rank that owns its x-line (PeerMaps)
+      const PeerMaps* pm = a.peer;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = c2 + h;
+        if (row >= a.rows) break;
+        int q = 0;
+        while (q + 1 < pm->nranks && row >= pm->unit_off[q + 1]) ++q;
+        EXPD_CHECK(row - pm->unit_off[q] < pm->units[q], "line: peer row");
+        tma_store_4d(&pm->m[q], buf + h * M * 8, 0, 0, row - pm->unit_off[q], a.peer_slot0 + c3);
+      }
+    } else {
+      tma_store_4d(map, buf, 0, 0, c2, c3);
+      if (c2 + 1 < a.rows) tma_store_4d(map, buf + M * 8, 0, 0, c2 + 1, c3);
+    }
   } else {
 #pragma unroll
     for (int b = 0; b < M / CBR; ++b) {
@@ -669,7 +684,10 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
       }
     }
   }
-  if (tid == 0) bulk_wait0();
+  if (tid == 0) {
+    bulk_wait0();
+    if (a.peer) __threadfence_system();  // the peer stores are complete before the kernel ends
+  }
 }
 
 // ---------------------------------------------------------------------------------------
@@ -1213,6 +1231,14 @@ static cudaError_t axis_map(CUtensorMap* m, const Geom& g, int ax, const double*
   return make_map(m, ptr, d, s, b, false);
 }
 
+cudaError_t peer_nhat_map(CUtensorMap* m, const Geom& g, double* base, long units, long slots, long slot_doubles) {
+  const cuuint64_t M = (cuuint64_t)g.M;
+  const cuuint64_t d[4] = {16, M / 16, (cuuint64_t)units, (cuuint64_t)slots};
+  const cuuint64_t s[3] = {128, M * 8, (cuuint64_t)slot_doubles * 8};
+  const cuuint32_t b[4] = {16, (cuuint32_t)(M / 16), 1, 1};
+  return make_map(m, base, d, s, b, /*sw=*/true);  // the row kernel's swizzled result layout
+}
+
 static int sm_count() {
   int dev = 0, n = 0;
   cudaGetDevice(&dev);
@@ -1227,7 +1253,7 @@ LineSkipScope::~LineSkipScope() { t_line_skip = prev; }
 
 template <int M, int AX, bool NL, int G, int NBUF, bool PP = false>
 static cudaError_t launch_line(const Geom& g, const DstTables& t, const Poly& P, const double* in, double* out,
-                               long nslices, cudaStream_t st) {
+                               long nslices, cudaStream_t st, const PeerOut* peer = nullptr) {
   using D = LGeo<M, G, NBUF>;
   auto k = k_line<M, AX, NL, G, NBUF, PP>;
   static DevOnce once;  // per instantiation and device
@@ -1236,7 +1262,7 @@ static cudaError_t launch_line(const Geom& g, const DstTables& t, const Poly& P,
   CUtensorMap mi, mo;
   cudaError_t e = axis_map(&mi, g, AX, in, nslices, G, /*sw=*/false);
   if (e != cudaSuccess) return e;
-  if ((e = axis_map(&mo, g, AX, out, nslices, G, /*sw=*/AX == AX_ROW)) != cudaSuccess) return e;
+  if ((e = axis_map(&mo, g, AX, peer ? in : out, nslices, G, /*sw=*/AX == AX_ROW)) != cudaSuccess) return e;
   LineArgs a{};
   const int rows = (int)(g.npad / g.M);
   if (AX == AX_ROW) {
@@ -1254,6 +1280,11 @@ static cudaError_t launch_line(const Geom& g, const DstTables& t, const Poly& P,
   a.c = 0.5 * sqrt(2.0 / (double)g.M);
   a.poly = P;
   a.skip = t_line_skip;
+  if (peer) {
+    if (AX != AX_ROW) return cudaErrorInvalidValue;
+    a.peer = peer->maps;
+    a.peer_slot0 = peer->slot0;
+  }
   long grid = (long)sm_count() * per_sm;
   if (grid > a.nitems) grid = a.nitems;
   if (grid < 1) return cudaSuccess;
@@ -1341,7 +1372,11 @@ static bool use_line2() {
 
 template <int M>
 static cudaError_t line_pass_m(const Geom& g, const DstTables& t, const Poly& P, int ax, bool nl, const double* in,
-                               double* out, long nslices, cudaStream_t st) {
+                               double* out, long nslices, cudaStream_t st, const PeerOut* peer = nullptr) {
+  if (peer) {  // the peer-store x pass: the default row kernel only
+    if (ax != AX_ROW || nl) return cudaErrorInvalidValue;
+    return launch_line<M, AX_ROW, false, 1, 2>(g, t, P, in, out, nslices, st, peer);
+  }
   if constexpr (M == 2048) {
     if (use_line2()) {
       if (ax == AX_ROW) return launch_line2<AX_ROW, false, 2>(g, t, P, in, out, nslices, st);
@@ -1453,15 +1488,15 @@ cudaError_t stage3p(const Geom& g, const DstTables& t, const Poly& P, const doub
 // (strided axes only) fuses [V, N, V].  in and out may alias (each item reads and writes
 // only its own lines).
 cudaError_t line_pass(const Geom& g, const DstTables& t, const Poly& P, int ax, bool nl, const double* in,
-                      double* out, long nslices, cudaStream_t st) {
+                      double* out, long nslices, cudaStream_t st, const PeerOut* peer) {
   if (nslices <= 0) return cudaSuccess;
   if (ax == AX_ROW && nl) return cudaErrorInvalidValue;
   switch (g.M) {
-    case 256: return line_pass_m<256>(g, t, P, ax, nl, in, out, nslices, st);
-    case 512: return line_pass_m<512>(g, t, P, ax, nl, in, out, nslices, st);
-    case 1024: return line_pass_m<1024>(g, t, P, ax, nl, in, out, nslices, st);
-    case 2048: return line_pass_m<2048>(g, t, P, ax, nl, in, out, nslices, st);
-    case 4096: return line_pass_m<4096>(g, t, P, ax, nl, in, out, nslices, st);
+    case 256: return line_pass_m<256>(g, t, P, ax, nl, in, out, nslices, st, peer);
+    case 512: return line_pass_m<512>(g, t, P, ax, nl, in, out, nslices, st, peer);
+    case 1024: return line_pass_m<1024>(g, t, P, ax, nl, in, out, nslices, st, peer);
+    case 2048: return line_pass_m<2048>(g, t, P, ax, nl, in, out, nslices, st, peer);
+    case 4096: return line_pass_m<4096>(g, t, P, ax, nl, in, out, nslices, st, peer);
     default: return cudaErrorInvalidValue;
   }
 }

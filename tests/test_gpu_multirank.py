@@ -122,3 +122,68 @@ def _check(orc, tmp_path, P, name, n, nt, solvers):
         for g in got:
             assert g["its_" + sv][1] == 1 and g["its_" + sv][0] == its, sv
         assert st == 0 and relmax(cat("U_" + sv), Uo) < 1e-9, sv
+
+
+def _peer_worker(rank, P, port, name, n, nt, out_dir):
+    _init(rank, P, port)
+    try:
+        from paper_2603_04350_b200 import HostComm, Plan, Problem
+
+        torch.cuda.set_device(0)
+        dev = torch.device("cuda:0")
+        cfg = _cfg(name, n, nt)
+        comm = HostComm(rank, P, 0, GlooTransport())
+        u0 = torch.from_numpy(np.ascontiguousarray(synth.initial_condition(cfg))).to(dev)
+        res = {}
+        for peer in (False, True):
+            plan = Plan(Problem.from_config(cfg), comm=comm)
+            if peer:
+                plan.enable_peer_stores()
+            t0, ntl = plan.layout["t0"], plan.layout["nt_local"]
+            U = torch.from_numpy(np.ascontiguousarray(synth.random_spacetime(cfg, scale=0.5)[t0:t0 + ntl])).to(dev)
+            R, rn2 = plan.residual(u0, U, norm=True)
+            Us, rep = plan.fixed_point_solve(u0, tol=cfg.tol, maxit=50)
+            res[peer] = (R.cpu().numpy(), rn2, Us.cpu().numpy(), rep["iterations"], rep["hist"])
+            del plan
+        assert np.array_equal(res[False][0], res[True][0]) and res[False][1] == res[True][1]
+        assert np.array_equal(res[False][2], res[True][2]) and res[False][3] == res[True][3]
+        assert res[False][4] == res[True][4]
+        # the stores really go through the registered slabs: peers registered one x-line off
+        # (a plan's own slab stays right) give a different solution
+        import ctypes as C
+
+        plan = Plan(Problem.from_config(cfg), comm=comm)
+        h = (C.c_ubyte * 64)()
+        off = C.c_long()
+        plan._check(plan.lib.expd_plan_nhat_ipc_handle(plan.handle, h, C.byref(off)))
+        allh = [None] * P
+        dist.all_gather_object(allh, (bytes(h), off.value))
+        for q, (hb, o) in enumerate(allh):
+            shifted = o + 8 * (cfg.n + 1) if q != rank else o
+            plan._check(plan.lib.expd_plan_set_peer_nhat(plan.handle, q, (C.c_ubyte * 64)(*hb), shifted))
+        plan._check(plan.lib.expd_plan_enable_peer_stores(plan.handle, 1))
+        Ub, repb = plan.fixed_point_solve(u0, tol=cfg.tol, maxit=50)
+        differs = not np.array_equal(Ub.cpu().numpy(), res[True][2])
+        del plan
+        np.savez(os.path.join(out_dir, f"rank{rank}.npz"), U=res[True][2], its=np.array([res[True][3]]),
+                 sabotage_differs=np.array([differs]))
+        comm.close()
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("P,name,n,nt", [(2, "c5", 255, 8), (4, "c5", 255, 8), (2, "c5if", 255, 8),
+                                         (2, "c3", 255, 16)])
+def test_multirank_peer_stores(orc, tmp_path, P, name, n, nt):
+    """Stage 3 with peer stores (each rank's x-DST rows stored straight into the owners' N-hat
+    slabs through CUDA IPC -- here other processes on the same GPU): the residual, the
+    iterations, the history and the solution are bitwise those of the all-to-all schedule,
+    and the solution matches the oracle (255 x-lines over 2 / 4 ranks: 128 + 127, 64 x 3 + 63)."""
+    _spawn(_peer_worker, P, name, n, nt, str(tmp_path))
+    cfg = _cfg(name, n, nt)
+    got = [dict(np.load(tmp_path / f"rank{r}.npz")) for r in range(P)]
+    U = np.concatenate([g["U"] for g in got])
+    Uo, st, its, _ = orc.fixed_point(orc.spec(cfg), synth.initial_condition(cfg), tol=cfg.tol, maxit=50)
+    assert st == 0 and all(int(g["its"][0]) == its for g in got)
+    assert relmax(U, Uo) < 1e-9
+    assert any(bool(g["sabotage_differs"][0]) for g in got)
