@@ -240,20 +240,23 @@ expd_status expd_host_comm_create(const expd_transport* transport, int rank, int
    communicators. */
 void expd_host_comm_destroy(void* comm);
 
-/* Peer stores (the fused "NVLink-store transpose" of SURVEY §8(f)):
-   a distributed nonlinear plan's stage 3 can write every row of its x-DST result straight
-   into the N-hat mode slab of the rank that owns the row -- another GPU's memory over NVLink,
-   or another process's on the same GPU -- instead of a local slab plus a time -> mode
-   all-to-all.  Setup, collective over the ranks: every rank exports its slab
-   (expd_plan_nhat_ipc_handle: a CUDA IPC handle of the allocation holding it and the slab's
-   byte offset), the handles are exchanged by the caller (e.g. torch.distributed all_gather),
-   every rank registers every rank's (expd_plan_set_peer_nhat; its own rank maps its own slab),
-   then expd_plan_enable_peer_stores(plan, 1).  Requirements: real coefficients, npoly > 0,
-   dim >= 2, n + 1 >= 256 (the TMA line kernels), <= 16 ranks, mode slabs of whole x-lines.
-   A new workspace disables the peer stores (register again).  UNSUPPORTED / INVALID_ARG /
-   EXPD_ERR_CUDA (e.g. a caching allocator without IPC-able segments). */
-expd_status expd_plan_nhat_ipc_handle(expd_plan* plan, unsigned char handle[64], long* offset_bytes);
-expd_status expd_plan_set_peer_nhat(expd_plan* plan, int rank, const unsigned char handle[64], long offset_bytes);
+/* Peer access (the fused "NVLink-store transposes" of SURVEY §8(f)): a
+   distributed nonlinear plan's stage 3 can load every row of its time slab straight from the
+   U-hat mode slab of the rank that owns the row and store every row of its result straight
+   into the owner's N-hat slab -- another GPU's memory over NVLink, or another process's on the
+   same GPU -- instead of two all-to-alls through time-slab staging.  Setup, collective over
+   the ranks: every rank exports its slabs (expd_plan_slab_ipc_handle: a CUDA IPC handle of
+   the workspace allocation and the two slabs' byte offsets), the caller exchanges them
+   (e.g. torch.distributed all_gather), every rank registers every rank's
+   (expd_plan_set_peer_slabs; its own rank maps its own slabs), then
+   expd_plan_enable_peer_stores(plan, 1) (0 switches back to the all-to-alls).  Requirements:
+   real coefficients, npoly > 0, dim >= 2, n + 1 >= 256 (the TMA line kernels), <= 16 ranks,
+   mode slabs of whole x-lines.  A new workspace disables it (register again).  UNSUPPORTED /
+   INVALID_ARG / EXPD_ERR_CUDA (e.g. a caching allocator without IPC-able segments). */
+expd_status expd_plan_slab_ipc_handle(expd_plan* plan, unsigned char handle[64], long* nhat_offset,
+                                      long* uhat_offset);
+expd_status expd_plan_set_peer_slabs(expd_plan* plan, int rank, const unsigned char handle[64], long nhat_offset,
+                                     long uhat_offset);
 expd_status expd_plan_enable_peer_stores(expd_plan* plan, int on);
 
 /* ---- lower-level entry points used by the solver loop and the benchmark -------------- */

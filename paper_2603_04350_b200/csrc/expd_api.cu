@@ -93,9 +93,9 @@ struct expd_plan {
   std::vector<double> kstep_ms;
   // peer stores of the distributed stage 3 (expd_plan_enable_peer_stores): every rank's N-hat
   // mode slab (its own, or another process's opened through CUDA IPC) and their tensor maps
-  std::vector<double*> peer_nh;
+  std::vector<double*> peer_nh, peer_uh;
   std::vector<void*> peer_ipc;  // IPC-opened allocation bases (closed at destroy)
-  PeerMaps* d_peer = nullptr;
+  PeerMaps* d_peer = nullptr;   // [0]: the N-hat slabs (stores), [1]: the U-hat slabs (loads)
   bool peer_on = false;
   std::string err;
 };
@@ -595,18 +595,23 @@ static int dist_chunks(const expd_plan* p) {
 // sequence (slice keys), so the NCCL groups match across ranks.
 static expd_status allreduce(expd_plan* p, double* buf, long count);
 
-// Stage 3 with peer stores: the mode -> time all-to-all as usual, then stage 3 of the time slab
-// whose final x-DST pass stores every row straight into its owner's N-hat slab (slot t + 1)
-// -- no local N-hat slab, no time -> mode all-to-all -- and one allreduce as the barrier that
-// orders every rank's stores before any rank's K1 reads them.
-static expd_status stage3_peer(expd_plan* p) {
-  expd_status s;
-  if ((s = a2a(p, A2A_M2T, p->Uh, p->UT))) return s;
-  PeerOut po{p->d_peer, p->t0 + 1};
-  CUDA_TRY(p, nonlin_slices(p->g, dst_tables(p), p->UT, nullptr, p->ntl, p->prob.npoly, p->prob.q, p->scratch,
-                            p->stream, nullptr, nullptr, nullptr, &po));
+// Stage 3 with peer access: the x-IDST pass loads every row of the time slab straight from its
+// owner's U-hat slab (slot t) and the x-DST pass stores every row straight into its owner's
+// N-hat slab (slot t + 1) -- no all-to-all, no time-slab staging.  Two allreduces are the
+// barriers: every rank's U-hat is final before any rank loads it (after K1 of the last sweep
+// or expd_load_state's all-to-all), and every rank's stores are done before any rank's K1.
+static expd_status peer_barrier(expd_plan* p) {
   CUDA_TRY(p, cudaMemsetAsync(p->dscal + 500, 0, sizeof(double), p->stream));
   return allreduce(p, p->dscal + 500, 1);
+}
+
+static expd_status stage3_peer(expd_plan* p) {
+  expd_status s;
+  if ((s = peer_barrier(p))) return s;
+  PeerOut po{p->d_peer, p->t0 + 1, p->d_peer + 1, p->t0};
+  CUDA_TRY(p, nonlin_slices(p->g, dst_tables(p), nullptr, nullptr, p->ntl, p->prob.npoly, p->prob.q, p->scratch,
+                            p->stream, nullptr, nullptr, nullptr, &po));
+  return peer_barrier(p);
 }
 
 static expd_status stage3_dist(expd_plan* p) {
@@ -1489,11 +1494,12 @@ extern "C" expd_status expd_bicgstab_solve(expd_plan* p, const double* u0, doubl
 // ---------------------------------------------------------------------------------------
 typedef CUresult (*PFN_addr_range)(CUdeviceptr*, size_t*, CUdeviceptr);
 
-extern "C" expd_status expd_plan_nhat_ipc_handle(expd_plan* p, unsigned char handle[64], long* offset_bytes) {
+extern "C" expd_status expd_plan_slab_ipc_handle(expd_plan* p, unsigned char handle[64], long* nhat_offset,
+                                                 long* uhat_offset) {
   expd_status s = ready(p);
   if (s) return s;
-  if (!handle || !offset_bytes) return fail(p, EXPD_ERR_INVALID_ARG, "nhat_ipc_handle: bad args");
-  if (!p->dist || !p->Nh) return fail(p, EXPD_ERR_UNSUPPORTED, "nhat_ipc_handle: distributed nonlinear plans only");
+  if (!handle || !nhat_offset || !uhat_offset) return fail(p, EXPD_ERR_INVALID_ARG, "slab_ipc_handle: bad args");
+  if (!p->dist || !p->Nh) return fail(p, EXPD_ERR_UNSUPPORTED, "slab_ipc_handle: distributed nonlinear plans only");
   void* fn = nullptr;
   cudaDriverEntryPointQueryResult q;
   if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
@@ -1502,24 +1508,31 @@ extern "C" expd_status expd_plan_nhat_ipc_handle(expd_plan* p, unsigned char han
   size_t size = 0;
   if (((PFN_addr_range)fn)(&base, &size, (CUdeviceptr)p->Nh) != CUDA_SUCCESS)
     return fail(p, EXPD_ERR_CUDA, "cuMemGetAddressRange failed");
+  if ((CUdeviceptr)p->Uh < base || (CUdeviceptr)p->Uh >= base + size)
+    return fail(p, EXPD_ERR_UNSUPPORTED, "slab_ipc_handle: U-hat and N-hat in different allocations");
   cudaIpcMemHandle_t h;
   CUDA_TRY(p, cudaIpcGetMemHandle(&h, (void*)base));
   static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t size");
   memcpy(handle, &h, 64);
-  *offset_bytes = (long)((CUdeviceptr)p->Nh - base);
+  *nhat_offset = (long)((CUdeviceptr)p->Nh - base);
+  *uhat_offset = (long)((CUdeviceptr)p->Uh - base);
   return EXPD_OK;
 }
 
-extern "C" expd_status expd_plan_set_peer_nhat(expd_plan* p, int rank, const unsigned char handle[64],
-                                               long offset_bytes) {
+extern "C" expd_status expd_plan_set_peer_slabs(expd_plan* p, int rank, const unsigned char handle[64],
+                                                long nhat_offset, long uhat_offset) {
   expd_status s = ready(p);
   if (s) return s;
   if (!p->dist || !p->Nh || rank < 0 || rank >= p->L.nranks || p->L.nranks > kMaxPeers || !handle ||
-      offset_bytes < 0)
-    return fail(p, EXPD_ERR_INVALID_ARG, "set_peer_nhat: bad args");
-  if ((int)p->peer_nh.size() != p->L.nranks) p->peer_nh.assign(p->L.nranks, nullptr);
+      nhat_offset < 0 || uhat_offset < 0)
+    return fail(p, EXPD_ERR_INVALID_ARG, "set_peer_slabs: bad args");
+  if ((int)p->peer_nh.size() != p->L.nranks) {
+    p->peer_nh.assign(p->L.nranks, nullptr);
+    p->peer_uh.assign(p->L.nranks, nullptr);
+  }
   if (rank == p->L.rank) {
     p->peer_nh[rank] = p->Nh;
+    p->peer_uh[rank] = p->Uh;
     return EXPD_OK;
   }
   cudaIpcMemHandle_t h;
@@ -1527,7 +1540,8 @@ extern "C" expd_status expd_plan_set_peer_nhat(expd_plan* p, int rank, const uns
   void* base = nullptr;
   CUDA_TRY(p, cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
   p->peer_ipc.push_back(base);
-  p->peer_nh[rank] = reinterpret_cast<double*>(static_cast<char*>(base) + offset_bytes);
+  p->peer_nh[rank] = reinterpret_cast<double*>(static_cast<char*>(base) + nhat_offset);
+  p->peer_uh[rank] = reinterpret_cast<double*>(static_cast<char*>(base) + uhat_offset);
   return EXPD_OK;
 }
 
@@ -1541,19 +1555,24 @@ extern "C" expd_status expd_plan_enable_peer_stores(expd_plan* p, int on) {
   if (!p->dist || !p->nl || p->cx || p->g.dim < 2 || !line_supported(p->g))
     return fail(p, EXPD_ERR_UNSUPPORTED, "peer stores: distributed nonlinear real plans, dim >= 2, n + 1 >= 256");
   if ((int)p->peer_nh.size() != p->L.nranks) return fail(p, EXPD_ERR_INVALID_ARG, "peer stores: peers not set");
-  PeerMaps h{};
-  h.nranks = p->L.nranks;
+  PeerMaps h[2]{};  // [0] N-hat slabs (stores, the swizzled result layout), [1] U-hat slabs (loads)
+  for (int k = 0; k < 2; ++k) h[k].nranks = p->L.nranks;
   for (int q = 0; q < p->L.nranks; ++q) {
-    if (!p->peer_nh[q]) return fail(p, EXPD_ERR_INVALID_ARG, "peer stores: peer " + std::to_string(q) + " not set");
+    if (!p->peer_nh[q] || !p->peer_uh[q])
+      return fail(p, EXPD_ERR_INVALID_ARG, "peer stores: peer " + std::to_string(q) + " not set");
     const long M = p->g.M;
     if (p->L.mode_off[q] % M || p->L.mode_len[q] % M)
       return fail(p, EXPD_ERR_UNSUPPORTED, "peer stores: mode slabs are not whole x-lines");
-    h.unit_off[q] = (int)(p->L.mode_off[q] / M);
-    h.units[q] = (int)(p->L.mode_len[q] / M);
-    CUDA_TRY(p, peer_nhat_map(&h.m[q], p->g, p->peer_nh[q], h.units[q], p->prob.nt + 1, p->L.mode_len[q]));
+    for (int k = 0; k < 2; ++k) {
+      h[k].unit_off[q] = (int)(p->L.mode_off[q] / M);
+      h[k].units[q] = (int)(p->L.mode_len[q] / M);
+    }
+    CUDA_TRY(p, peer_slab_map(&h[0].m[q], p->g, p->peer_nh[q], h[0].units[q], p->prob.nt + 1, p->L.mode_len[q],
+                              true));
+    CUDA_TRY(p, peer_slab_map(&h[1].m[q], p->g, p->peer_uh[q], h[1].units[q], p->prob.nt, p->L.mode_len[q], false));
   }
-  if (!p->d_peer) CUDA_TRY(p, cudaMalloc(&p->d_peer, sizeof(PeerMaps)));
-  CUDA_TRY(p, cudaMemcpyAsync(p->d_peer, &h, sizeof(PeerMaps), cudaMemcpyHostToDevice, p->stream));
+  if (!p->d_peer) CUDA_TRY(p, cudaMalloc(&p->d_peer, 2 * sizeof(PeerMaps)));
+  CUDA_TRY(p, cudaMemcpyAsync(p->d_peer, h, 2 * sizeof(PeerMaps), cudaMemcpyHostToDevice, p->stream));
   CUDA_TRY(p, cudaStreamSynchronize(p->stream));
   p->peer_on = true;
   return EXPD_OK;

@@ -145,11 +145,12 @@ struct PassTimer {
   int used;
   int kind[512];
 };
-// Peer stores of the distributed stage 3 (the fused "NVLink-store transpose"):
-// the final x-DST pass stores each spectral row straight into the N-hat mode slab of the rank
-// that owns it (device memory of another process / GPU, opened through CUDA IPC), at slot
-// slot0 + (slice), instead of a local N-hat slab followed by an all-to-all.  One tensor map
-// per rank (in device memory, 64-byte aligned), rows [unit_off[q], unit_off[q] + units[q]).
+// Peer access of the distributed stage 3 (the fused "NVLink-store transposes"):
+// the first x pass (x-IDST) loads each spectral row straight from the U-hat mode slab of the
+// rank that owns it and the final x pass (x-DST) stores each row straight into the owner's
+// N-hat slab (device memory of another process / GPU, opened through CUDA IPC), instead of
+// two all-to-alls through time-slab staging.  One tensor map per rank and slab (in device
+// memory, 64-byte aligned), rows [unit_off[q], unit_off[q] + units[q]).
 constexpr int kMaxPeers = 16;
 struct PeerMaps {
   CUtensorMap m[kMaxPeers];
@@ -158,8 +159,10 @@ struct PeerMaps {
   int units[kMaxPeers];
 };
 struct PeerOut {
-  const PeerMaps* maps;  // device
-  int slot0;             // N-hat slot of the launch's first slice
+  const PeerMaps* maps;     // device, nullable: the x-DST rows -> the owners' N-hat slabs
+  int slot0;                // N-hat slot of the launch's first slice
+  const PeerMaps* in_maps;  // device, nullable: the x-IDST rows <- the owners' U-hat slabs
+  int in_slot0;             // U-hat slot of the launch's first slice
 };
 cudaError_t nonlin_slices(const Geom& g, const DstTables& t, const double* uhat, double* nhat, long nslices,
                           int npoly, const double* q, double* scratch, cudaStream_t st, struct PassTimer* timer = nullptr,
@@ -186,9 +189,11 @@ cudaError_t make_tmap_2d(CUtensorMap* m, const double* ptr, unsigned long long c
                          unsigned long long row_bytes, unsigned box_cols, unsigned box_rows);
 cudaError_t line_pass(const Geom& g, const DstTables& t, const Poly& P, int ax, bool nl, const double* in,
                       double* out, long nslices, cudaStream_t st, const PeerOut* peer = nullptr);
-// the tensor map of one rank's N-hat slab for PeerMaps: units x-lines of M doubles per slot,
-// slots slots, slot stride slot_doubles (the mode-slab length)
-cudaError_t peer_nhat_map(CUtensorMap* m, const Geom& g, double* base, long units, long slots, long slot_doubles);
+// the tensor map of one rank's slab for PeerMaps: units x-lines of M doubles per slot, slots
+// slots, slot stride slot_doubles (the mode-slab length); swizzled = the row kernel's result
+// layout (N-hat stores), else its linear input layout (U-hat loads)
+cudaError_t peer_slab_map(CUtensorMap* m, const Geom& g, double* base, long units, long slots, long slot_doubles,
+                          bool swizzled);
 int nonlin_kernel_launches(const Geom& g, long nslices, bool full_tmp = false);
 // While in scope, every k_line launch of this host thread (stage 3 included) reads the device
 // int `flag` first and does nothing if it is non-zero: the device loop skips stage 3 of its

@@ -723,7 +723,12 @@ cudaError_t nonlin_slices(const Geom& g, const DstTables& t, const double* uhat,
     if (tl) {
       // x (inverse) -> scratch ; [dim 3: y] ; last axis fused [V, N, V] ; [dim 3: y] ; x -> out
       CK(mark(tm, 0, st));
-      CK(line_pass(g, t, P, 0, false, in, scratch, ns, st));
+      if (peer && peer->in_maps) {
+        PeerOut pi{nullptr, 0, peer->in_maps, peer->in_slot0 + (int)s0};
+        CK(line_pass(g, t, P, 0, false, nullptr, scratch, ns, st, &pi));
+      } else {
+        CK(line_pass(g, t, P, 0, false, in, scratch, ns, st));
+      }
       if (g.dim == 3) {
         CK(mark(tm, 1, st));
         CK(line_pass(g, t, P, 1, false, scratch, scratch, ns, st));
@@ -735,8 +740,8 @@ cudaError_t nonlin_slices(const Geom& g, const DstTables& t, const double* uhat,
         CK(line_pass(g, t, P, 1, false, scratch, scratch, ns, st));
       }
       CK(mark(tm, 0, st));
-      if (peer) {
-        PeerOut po{peer->maps, peer->slot0 + (int)s0};
+      if (peer && peer->maps) {
+        PeerOut po{peer->maps, peer->slot0 + (int)s0, nullptr, 0};
         CK(line_pass(g, t, P, 0, false, scratch, nullptr, ns, st, &po));
       } else {
         CK(line_pass(g, t, P, 0, false, scratch, out, ns, st));

@@ -91,6 +91,8 @@ struct LineArgs {
   const int* skip;     // device flag: non-zero -> the launch does nothing (nullable)
   const PeerMaps* peer;  // ROW only: store each row into its owner's N-hat slab (nullable)
   int peer_slot0;        // ... at slot peer_slot0 + slice
+  const PeerMaps* peer_in;  // ROW only: load each row from its owner's U-hat slab (nullable)
+  int peer_in_slot0;        // ... at slot peer_in_slot0 + slice
 };
 
 // The write-after-read points of the line transform (a stage reads the buffer, transforms in
@@ -465,8 +467,20 @@ __device__ __forceinline__ void line_issue_load(const CUtensorMap* map, const Li
   line_coords<AX, G>(a, item, c0, c1, c2, c3, smod);
   mbar_arrive_expect_tx(bar, (uint32_t)(G * M * 16));
   if constexpr (AX == AX_ROW) {
-    tma_load_4d(buf, map, bar, 0, 0, c2, c3);
-    tma_load_4d(buf + M * 8, map, bar, 0, 0, c2 + 1, c3);
+    if (a.peer_in) {  // each row from the rank that owns its x-line (PeerMaps); a row past the
+      // slice (odd row count) reads out of the last rank's box: zero-filled, bytes counted
+      const PeerMaps* pm = a.peer_in;
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int row = c2 + h;
+        int q = 0;
+        while (q + 1 < pm->nranks && row >= pm->unit_off[q + 1]) ++q;
+        tma_load_4d(buf + h * M * 8, &pm->m[q], bar, 0, 0, row - pm->unit_off[q], a.peer_in_slot0 + c3);
+      }
+    } else {
+      tma_load_4d(buf, map, bar, 0, 0, c2, c3);
+      tma_load_4d(buf + M * 8, map, bar, 0, 0, c2 + 1, c3);
+    }
   } else {
     // linear raw layout [row][G]: grid row p of pair g at double2 p*G + g (boxes of CBR rows)
 #pragma unroll
@@ -1231,12 +1245,13 @@ static cudaError_t axis_map(CUtensorMap* m, const Geom& g, int ax, const double*
   return make_map(m, ptr, d, s, b, false);
 }
 
-cudaError_t peer_nhat_map(CUtensorMap* m, const Geom& g, double* base, long units, long slots, long slot_doubles) {
+cudaError_t peer_slab_map(CUtensorMap* m, const Geom& g, double* base, long units, long slots, long slot_doubles,
+                          bool swizzled) {
   const cuuint64_t M = (cuuint64_t)g.M;
   const cuuint64_t d[4] = {16, M / 16, (cuuint64_t)units, (cuuint64_t)slots};
   const cuuint64_t s[3] = {128, M * 8, (cuuint64_t)slot_doubles * 8};
   const cuuint32_t b[4] = {16, (cuuint32_t)(M / 16), 1, 1};
-  return make_map(m, base, d, s, b, /*sw=*/true);  // the row kernel's swizzled result layout
+  return make_map(m, base, d, s, b, swizzled);
 }
 
 static int sm_count() {
@@ -1260,9 +1275,12 @@ static cudaError_t launch_line(const Geom& g, const DstTables& t, const Poly& P,
   int per_sm = 1;
   if (cudaError_t e = smem_optin(once, k, D::SMEM, D::THREADS, &per_sm); e != cudaSuccess) return e;
   CUtensorMap mi, mo;
-  cudaError_t e = axis_map(&mi, g, AX, in, nslices, G, /*sw=*/false);
+  // (a peer side's own map is unused: any valid pointer of the launch describes it)
+  const double* in_m = (peer && peer->in_maps) ? out : in;
+  double* out_m = (peer && peer->maps) ? const_cast<double*>(in) : out;
+  cudaError_t e = axis_map(&mi, g, AX, in_m, nslices, G, /*sw=*/false);
   if (e != cudaSuccess) return e;
-  if ((e = axis_map(&mo, g, AX, peer ? in : out, nslices, G, /*sw=*/AX == AX_ROW)) != cudaSuccess) return e;
+  if ((e = axis_map(&mo, g, AX, out_m, nslices, G, /*sw=*/AX == AX_ROW)) != cudaSuccess) return e;
   LineArgs a{};
   const int rows = (int)(g.npad / g.M);
   if (AX == AX_ROW) {
@@ -1284,6 +1302,8 @@ static cudaError_t launch_line(const Geom& g, const DstTables& t, const Poly& P,
     if (AX != AX_ROW) return cudaErrorInvalidValue;
     a.peer = peer->maps;
     a.peer_slot0 = peer->slot0;
+    a.peer_in = peer->in_maps;
+    a.peer_in_slot0 = peer->in_slot0;
   }
   long grid = (long)sm_count() * per_sm;
   if (grid > a.nitems) grid = a.nitems;

@@ -62,8 +62,8 @@ EXPORTS = [
     "expd_nccl_comm_destroy",
     "expd_host_comm_create",
     "expd_host_comm_destroy",
-    "expd_plan_nhat_ipc_handle",
-    "expd_plan_set_peer_nhat",
+    "expd_plan_slab_ipc_handle",
+    "expd_plan_set_peer_slabs",
     "expd_plan_enable_peer_stores",
 ]
 
@@ -170,8 +170,8 @@ def load_library(path: str = LIB_PATH):
         "expd_nccl_comm_destroy": (None, [vp]),
         "expd_host_comm_create": (C.c_int, [C.POINTER(_Transport), C.c_int, C.c_int, C.POINTER(vp)]),
         "expd_host_comm_destroy": (None, [vp]),
-        "expd_plan_nhat_ipc_handle": (C.c_int, [vp, C.POINTER(C.c_ubyte), C.POINTER(C.c_long)]),
-        "expd_plan_set_peer_nhat": (C.c_int, [vp, C.c_int, C.POINTER(C.c_ubyte), C.c_long]),
+        "expd_plan_slab_ipc_handle": (C.c_int, [vp, C.POINTER(C.c_ubyte), C.POINTER(C.c_long), C.POINTER(C.c_long)]),
+        "expd_plan_set_peer_slabs": (C.c_int, [vp, C.c_int, C.POINTER(C.c_ubyte), C.c_long, C.c_long]),
         "expd_plan_enable_peer_stores": (C.c_int, [vp, C.c_int]),
     }
     for name, (res, args) in sig.items():
@@ -464,19 +464,18 @@ class Plan:
         return self._chk(t, self.problem.dtype, want, host_ok=self.comm is None)
 
     def enable_peer_stores(self, group=None):
-        """Stage 3 of this distributed plan stores its rows straight into the owners' N-hat
-        slabs (expd_plan_*peer*: CUDA IPC handles exchanged over torch.distributed, collective
-        over the plan's ranks)."""
+        """Stage 3 of this distributed plan loads its rows straight from the owners' U-hat slabs
+        and stores them straight into the owners' N-hat slabs (expd_plan_*slab* / *peer*: CUDA
+        IPC handles exchanged over torch.distributed, collective over the plan's ranks)."""
         import torch.distributed as dist
 
         h = (C.c_ubyte * 64)()
-        off = C.c_long()
-        self._check(self.lib.expd_plan_nhat_ipc_handle(self.handle, h, C.byref(off)))
-        mine = (bytes(h), off.value)
+        offn, offu = C.c_long(), C.c_long()
+        self._check(self.lib.expd_plan_slab_ipc_handle(self.handle, h, C.byref(offn), C.byref(offu)))
         allh = [None] * self.comm.nranks
-        dist.all_gather_object(allh, mine, group=group)
-        for q, (hb, o) in enumerate(allh):
-            self._check(self.lib.expd_plan_set_peer_nhat(self.handle, q, (C.c_ubyte * 64)(*hb), o))
+        dist.all_gather_object(allh, (bytes(h), offn.value, offu.value), group=group)
+        for q, (hb, on, ou) in enumerate(allh):
+            self._check(self.lib.expd_plan_set_peer_slabs(self.handle, q, (C.c_ubyte * 64)(*hb), on, ou))
         self._check(self.lib.expd_plan_enable_peer_stores(self.handle, 1))
 
     def set_zero_guess(self, on: bool = True):

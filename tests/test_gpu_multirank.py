@@ -152,21 +152,25 @@ def _peer_worker(rank, P, port, name, n, nt, out_dir):
         # (a plan's own slab stays right) give a different solution
         import ctypes as C
 
-        plan = Plan(Problem.from_config(cfg), comm=comm)
-        h = (C.c_ubyte * 64)()
-        off = C.c_long()
-        plan._check(plan.lib.expd_plan_nhat_ipc_handle(plan.handle, h, C.byref(off)))
-        allh = [None] * P
-        dist.all_gather_object(allh, (bytes(h), off.value))
-        for q, (hb, o) in enumerate(allh):
-            shifted = o + 8 * (cfg.n + 1) if q != rank else o
-            plan._check(plan.lib.expd_plan_set_peer_nhat(plan.handle, q, (C.c_ubyte * 64)(*hb), shifted))
-        plan._check(plan.lib.expd_plan_enable_peer_stores(plan.handle, 1))
-        Ub, repb = plan.fixed_point_solve(u0, tol=cfg.tol, maxit=50)
-        differs = not np.array_equal(Ub.cpu().numpy(), res[True][2])
-        del plan
+        differs = []
+        for which in (0, 1):  # 0: the N-hat stores one x-line off, 1: the U-hat loads
+            plan = Plan(Problem.from_config(cfg), comm=comm)
+            h = (C.c_ubyte * 64)()
+            offn, offu = C.c_long(), C.c_long()
+            plan._check(plan.lib.expd_plan_slab_ipc_handle(plan.handle, h, C.byref(offn), C.byref(offu)))
+            allh = [None] * P
+            dist.all_gather_object(allh, (bytes(h), offn.value, offu.value))
+            line = 8 * (cfg.n + 1)
+            for q, (hb, on, ou) in enumerate(allh):
+                if q != rank:
+                    on, ou = (on + line, ou) if which == 0 else (on, ou + line)
+                plan._check(plan.lib.expd_plan_set_peer_slabs(plan.handle, q, (C.c_ubyte * 64)(*hb), on, ou))
+            plan._check(plan.lib.expd_plan_enable_peer_stores(plan.handle, 1))
+            Ub, repb = plan.fixed_point_solve(u0, tol=cfg.tol, maxit=50)
+            differs.append(not np.array_equal(Ub.cpu().numpy(), res[True][2]))
+            del plan
         np.savez(os.path.join(out_dir, f"rank{rank}.npz"), U=res[True][2], its=np.array([res[True][3]]),
-                 sabotage_differs=np.array([differs]))
+                 sabotage_differs=np.array(differs))
         comm.close()
     finally:
         dist.destroy_process_group()
@@ -175,8 +179,9 @@ def _peer_worker(rank, P, port, name, n, nt, out_dir):
 @pytest.mark.parametrize("P,name,n,nt", [(2, "c5", 255, 8), (4, "c5", 255, 8), (2, "c5if", 255, 8),
                                          (2, "c3", 255, 16)])
 def test_multirank_peer_stores(orc, tmp_path, P, name, n, nt):
-    """Stage 3 with peer stores (each rank's x-DST rows stored straight into the owners' N-hat
-    slabs through CUDA IPC -- here other processes on the same GPU): the residual, the
+    """Stage 3 with peer access (each rank's x-IDST rows loaded straight from the owners' U-hat
+    slabs and its x-DST rows stored straight into the owners' N-hat slabs, through CUDA IPC --
+    here other processes on the same GPU): the residual, the
     iterations, the history and the solution are bitwise those of the all-to-all schedule,
     and the solution matches the oracle (255 x-lines over 2 / 4 ranks: 128 + 127, 64 x 3 + 63)."""
     _spawn(_peer_worker, P, name, n, nt, str(tmp_path))
@@ -186,4 +191,4 @@ def test_multirank_peer_stores(orc, tmp_path, P, name, n, nt):
     Uo, st, its, _ = orc.fixed_point(orc.spec(cfg), synth.initial_condition(cfg), tol=cfg.tol, maxit=50)
     assert st == 0 and all(int(g["its"][0]) == its for g in got)
     assert relmax(U, Uo) < 1e-9
-    assert any(bool(g["sabotage_differs"][0]) for g in got)
+    assert any(bool(g["sabotage_differs"][0]) for g in got) and any(bool(g["sabotage_differs"][1]) for g in got)
