@@ -115,6 +115,9 @@ def parse():
     ap.add_argument("--solver", default="sweep", choices=["sweep", "gmres"],
                     help="sweep: one fixed-point / Picard sweep per step; gmres: one Arnoldi step of "
                          "left-preconditioned GMRES per step (linear configs, e.g. c4; SURVEY §8(d.3))")
+    ap.add_argument("--peer", action="store_true",
+                    help="N > 1, nonlinear: stage 3 loads / stores its rows through peer memory (CUDA IPC) "
+                         "instead of the NCCL all-to-alls (Plan.enable_peer_stores)")
     ap.add_argument("--launch-check", action="store_true",
                     help="only check the multi-rank launch (gloo without a GPU): ranks, world size, one allreduce")
     return ap.parse_args()
@@ -386,6 +389,9 @@ def run_ours(args):
             os.dup2(saved, 1)
             os.close(saved)
     plan = Plan(prob, device=local, stream=stream, comm=comm)
+    peer = bool(args.peer and ws > 1 and cfg.q)
+    if peer:
+        plan.enable_peer_stores()
     lay = plan.layout
     u0 = torch.from_numpy(synth.initial_condition(cfg)).to(dev)
     plan.load_state(u0, None)
@@ -590,7 +596,8 @@ def run_ours(args):
                          f"{'>>' if cfg.nst * esz > 126e6 else '<'} 126 MB L2"
                          f"{' (no flush needed)' if cfg.nst * esz > 126e6 else ' (L2-resident: not a roofline number)'}",
                    "parallelism": "single GPU" if ws == 1 else
-                   f"{ws} GPUs: mode slabs (K1) / time slabs (stage 3), NCCL all-to-all + allreduce"},
+                   f"{ws} GPUs: mode slabs (K1) / time slabs (stage 3), "
+                   f"{'peer-memory row loads / stores' if peer else 'NCCL all-to-all'} + allreduce"},
         "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches, "clocks": ck,
         "residual_norm_last": float(np.sqrt(norms[-1])) if norms else None,
