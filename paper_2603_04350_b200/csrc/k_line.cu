@@ -93,6 +93,7 @@ struct LineArgs {
   int peer_slot0;        // ... at slot peer_slot0 + slice
   const PeerMaps* peer_in;  // ROW only: load each row from its owner's U-hat slab (nullable)
   int peer_in_slot0;        // ... at slot peer_in_slot0 + slice
+  double* outp;  // COL with the transposed store (TS): the output array (the tail rows' stores)
 };
 
 // The write-after-read points of the line transform (a stage reads the buffer, transforms in
@@ -492,12 +493,16 @@ __device__ __forceinline__ void line_issue_load(const CUtensorMap* map, const Li
   }
 }
 
-template <int M, int AX, int G>
+template <int M, int AX, int G, bool TS = false>
 __device__ __forceinline__ void line_issue_store(const CUtensorMap* map, const LineArgs& a, long item,
                                                  const char* buf, int smod = 0) {
   int c0, c1, c2, c3;
   line_coords<AX, G>(a, item, c0, c1, c2, c3, smod);
-  if constexpr (AX == AX_ROW) {
+  if constexpr (AX != AX_ROW && TS) {
+    // ONE box of the transposed view (col_ts_map): rows 0 .. M - 2L - 1 of the G pairs
+    if constexpr (AX == AX_COL_Y) tma_store_5d(map, buf, c0, 0, 0, c2, c3);
+    else tma_store_5d(map, buf, c0, c1, 0, 0, c3);
+  } else if constexpr (AX == AX_ROW) {
     if (a.peer) {  // each row to the rank that owns its x-line (PeerMaps)
       const PeerMaps* pm = a.peer;
 #pragma unroll
@@ -531,9 +536,10 @@ __device__ __forceinline__ void line_issue_store(const CUtensorMap* map, const L
 // alternate between the two (lcore's X = Z = cbo, Y = cb), so no stage writes a buffer that
 // another warp may still be reading: the write-after-read barriers disappear (WarNone).
 // Otherwise cbo == cb and the policy W places them.
-template <int M, int AX, bool NL, int G, class W, bool PP = false>
+template <int M, int AX, bool NL, int G, class W, bool PP = false, bool TS = false>
 __device__ __forceinline__ void line_item(char* cb, char* cbo, double2* wt, const LineArgs& a,
-                                          const LPre<M, G>& pre0, uint64_t* bar, uint32_t parity, W& war) {
+                                          const LPre<M, G>& pre0, uint64_t* bar, uint32_t parity, W& war,
+                                          long item = 0) {
   using D = LGeo<M, G, 1>;
   constexpr int R0 = D::R0, T = D::T, L = D::L, PADP = D::PADP;
   const int tid = threadIdx.x;
@@ -598,8 +604,31 @@ __device__ __forceinline__ void line_item(char* cb, char* cbo, double2* wt, cons
     }
     // (e, w) reads done before the result overwrites their buffer (PP: only the row result
     // goes to it, and the prefix's cross-warp barrier already ordered them unless NWB == 1)
-    if (!PP || (AX == AX_ROW && D::NWB == 1)) __syncthreads();
-    if constexpr (AX == AX_ROW) {
+    if (!PP || TS || (AX == AX_ROW && D::NWB == 1)) __syncthreads();
+    if constexpr (AX != AX_ROW && TS) {
+      // transposed store (TS): position p = 2L a + q of pair g goes to slot (q (T-1) + a) G + g,
+      // the smem layout of the transposed TMA view (col_ts_map, box a < T-1): in each write
+      // instruction consecutive threads hit consecutive 16-byte slots (conflict free), and the
+      // result needs no compaction pass.  The last thread's rows M-2L .. M-2 (M-1 is the
+      // spectral pad) lie outside that box: it stores them to global memory itself.
+      if (j < T - 1) {
+        double2* o = bufo + j * G + g;
+#pragma unroll
+        for (int q = 0; q < 2 * L; ++q) o[q * (T - 1) * G] = out[q];
+      } else {
+        int c0, c1, c2, c3;
+        line_coords<AX, G>(a, item, c0, c1, c2, c3);
+        const long npad = (long)a.rows * M;
+        double* gp = a.outp + (long)c3 * npad + c0 + 2 * g;
+#pragma unroll
+        for (int q = 0; q < 2 * L - 1; ++q) {
+          const int p = 2 * j * L + q;
+          const long row = AX == AX_COL_Y ? (long)c2 * (M - 1) + p : (long)p * (M - 1) + c1;
+          EXPD_CHECK(row * M + c0 + 2 * g + 1 < npad, "line: TS tail row");
+          *reinterpret_cast<double2*>(gp + row * M) = out[q];
+        }
+      }
+    } else if constexpr (AX == AX_ROW) {
       // rows a / b in the 128B-swizzled box layout: positions [2jL, 2jL+2L) as 16-byte pairs
 #pragma unroll
       for (int l = 0; l < L; ++l) {
@@ -630,7 +659,7 @@ __device__ __forceinline__ void line_item(char* cb, char* cbo, double2* wt, cons
 // the next item's load is issued once the store has read the output buffer (no prefetch
 // during the transform -- the other CTAs of the SM cover the wait), and the transform runs
 // without write-after-read barriers (line_item PP).
-template <int M, int AX, bool NL, int G, int NBUF, bool PP = false>
+template <int M, int AX, bool NL, int G, int NBUF, bool PP = false, bool TS = false>
 __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::MINB)
     k_line(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
            const __grid_constant__ LineArgs a) {
@@ -682,12 +711,12 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
       bulk_wait_read0();  // the previous item's stores have left the other buffer
       line_issue_load<M, AX, G>(&in_map, a, next, base + (cur ^ 1) * D::BUFB, &bar[cur ^ 1]);
     }
-    line_item<M, AX, NL, G, WarT, PP>(cb, cbo, wt, a, pre, &bar[cur],
-                                      (uint32_t)((NBUF == 2 ? (it >> 1) : it) & 1), war);
+    line_item<M, AX, NL, G, WarT, PP, TS>(cb, cbo, wt, a, pre, &bar[cur],
+                                          (uint32_t)((NBUF == 2 ? (it >> 1) : it) & 1), war, item);
     fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
-      line_issue_store<M, AX, G>(&out_map, a, item, cbo);
+      line_issue_store<M, AX, G, TS>(&out_map, a, item, cbo);
       if (PP && next < a.nitems) {
         bulk_wait_read0();  // the store has read the output buffer: it is the next input
         line_issue_load<M, AX, G>(&in_map, a, next, cbo, &bar[cur ^ 1]);
@@ -1245,6 +1274,44 @@ static cudaError_t axis_map(CUtensorMap* m, const Geom& g, int ax, const double*
   return make_map(m, ptr, d, s, b, false);
 }
 
+// 5-D fp64 tensor map (no swizzle), the COL result's transposed view: dims d[0..4] (d[0]
+// contiguous), byte strides s[1..4] in any order, box b[0..4]
+static cudaError_t make_map5(CUtensorMap* m, const double* ptr, const cuuint64_t d[5], const cuuint64_t s[4],
+                             const cuuint32_t b[5]) {
+  EncodeTiledFn f = encode_fn();
+  if (!f) return cudaErrorNotSupported;
+  const cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = f(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(ptr), d, s, b, es,
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS && getenv("EXPD_DEBUG"))
+    fprintf(stderr, "expd: cuTensorMapEncodeTiled (5-D) failed (%d)\n", (int)r);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+// The transposed store view of a COL pass (k_line TS): grid row p = 2L a + q along the
+// transformed axis becomes the pair of dims (a, q) with a INNER in shared memory, so the box
+// {2G doubles, a < T-1, q < 2L} lands at slot (q (T-1) + a) G + g -- the layout the threads
+// write without bank conflicts.  Rows 2L (T-1) .. M-2 are the last thread's (stored directly).
+template <int M, int G>
+static cudaError_t col_ts_map(CUtensorMap* m, const Geom& g, int ax, const double* ptr, long nslices) {
+  using D = LGeo<M, G, 1>;
+  const cuuint64_t n = (cuuint64_t)g.n, L2 = 2 * D::L, T = D::T;
+  const cuuint64_t sl = (cuuint64_t)g.npad * 8, row = (cuuint64_t)M * 8;
+  const cuuint64_t nz = g.dim == 3 ? n : 1;
+  if (ax == AX_COL_Y) {  // dims {x, a, q, z, slice}
+    const cuuint64_t d[5] = {(cuuint64_t)M, T, L2, nz, (cuuint64_t)nslices};
+    const cuuint64_t s[4] = {L2 * row, row, n * row, sl};
+    const cuuint32_t b[5] = {(cuuint32_t)(2 * G), (cuuint32_t)(T - 1), (cuuint32_t)L2, 1, 1};
+    return make_map5(m, ptr, d, s, b);
+  }
+  // AX_COL_Z: dims {x, y, a, q, slice}
+  const cuuint64_t d[5] = {(cuuint64_t)M, n, T, L2, (cuuint64_t)nslices};
+  const cuuint64_t s[4] = {row, L2 * n * row, n * row, sl};
+  const cuuint32_t b[5] = {(cuuint32_t)(2 * G), 1, (cuuint32_t)(T - 1), (cuuint32_t)L2, 1};
+  return make_map5(m, ptr, d, s, b);
+}
+
 cudaError_t peer_slab_map(CUtensorMap* m, const Geom& g, double* base, long units, long slots, long slot_doubles,
                           bool swizzled) {
   const cuuint64_t M = (cuuint64_t)g.M;
@@ -1266,11 +1333,12 @@ static thread_local const int* t_line_skip = nullptr;
 LineSkipScope::LineSkipScope(const int* flag) : prev(t_line_skip) { t_line_skip = flag; }
 LineSkipScope::~LineSkipScope() { t_line_skip = prev; }
 
-template <int M, int AX, bool NL, int G, int NBUF, bool PP = false>
+template <int M, int AX, bool NL, int G, int NBUF, bool PP = false, bool TS = false>
 static cudaError_t launch_line(const Geom& g, const DstTables& t, const Poly& P, const double* in, double* out,
                                long nslices, cudaStream_t st, const PeerOut* peer = nullptr) {
   using D = LGeo<M, G, NBUF>;
-  auto k = k_line<M, AX, NL, G, NBUF, PP>;
+  static_assert(!TS || AX != AX_ROW, "the transposed store is a COL layout");
+  auto k = k_line<M, AX, NL, G, NBUF, PP, TS>;
   static DevOnce once;  // per instantiation and device
   int per_sm = 1;
   if (cudaError_t e = smem_optin(once, k, D::SMEM, D::THREADS, &per_sm); e != cudaSuccess) return e;
@@ -1280,8 +1348,11 @@ static cudaError_t launch_line(const Geom& g, const DstTables& t, const Poly& P,
   double* out_m = (peer && peer->maps) ? const_cast<double*>(in) : out;
   cudaError_t e = axis_map(&mi, g, AX, in_m, nslices, G, /*sw=*/false);
   if (e != cudaSuccess) return e;
-  if ((e = axis_map(&mo, g, AX, out_m, nslices, G, /*sw=*/AX == AX_ROW)) != cudaSuccess) return e;
+  if constexpr (TS) e = col_ts_map<M, G>(&mo, g, AX, out_m, nslices);
+  else e = axis_map(&mo, g, AX, out_m, nslices, G, /*sw=*/AX == AX_ROW);
+  if (e != cudaSuccess) return e;
   LineArgs a{};
+  a.outp = out;
   const int rows = (int)(g.npad / g.M);
   if (AX == AX_ROW) {
     a.inner = (rows + 1) / 2;
@@ -1322,6 +1393,16 @@ static int colv() {
   }
   return v;
 }
+// EXPD_COLTS=0: the strided-axis result compacted in shared memory and stored as boxes of
+// CBR rows (the round-1/2 layout) instead of the transposed store (A/B at M = 2048)
+static bool colts() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EXPD_COLTS");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
 
 template <int M, int AX, bool NL>
 static cudaError_t launch_col(const Geom& g, const DstTables& t, const Poly& P, const double* in, double* out,
@@ -1340,13 +1421,17 @@ static cudaError_t launch_col(const Geom& g, const DstTables& t, const Poly& P, 
       case 13: return launch_line<M, AX, NL, 1, 2, true>(g, t, P, in, out, nslices, st);  // ping-pong
       case 23: return launch_line<M, AX, NL, 2, 2, true>(g, t, P, in, out, nslices, st);
       default:
-        if constexpr (NL) return launch_line<M, AX, NL, 1, 2>(g, t, P, in, out, nslices, st);
-        else return launch_line<M, AX, NL, 2, 2>(g, t, P, in, out, nslices, st);
+        if (!colts()) {
+          if constexpr (NL) return launch_line<M, AX, NL, 1, 2>(g, t, P, in, out, nslices, st);
+          else return launch_line<M, AX, NL, 2, 2>(g, t, P, in, out, nslices, st);
+        }
+        if constexpr (NL) return launch_line<M, AX, NL, 1, 2, false, true>(g, t, P, in, out, nslices, st);
+        else return launch_line<M, AX, NL, 2, 2, false, true>(g, t, P, in, out, nslices, st);
     }
   } else if constexpr (M == 4096) {
-    return launch_line<M, AX, NL, 1, 2>(g, t, P, in, out, nslices, st);
+    return launch_line<M, AX, NL, 1, 2, false, true>(g, t, P, in, out, nslices, st);
   } else {
-    return launch_line<M, AX, NL, 2, 2>(g, t, P, in, out, nslices, st);
+    return launch_line<M, AX, NL, 2, 2, false, true>(g, t, P, in, out, nslices, st);
   }
 }
 
