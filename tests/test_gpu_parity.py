@@ -67,6 +67,48 @@ def test_dst_full_size_sampled(orc, dim, n):
     assert relmax(got[idx], want) < 1e-12 * np.sqrt(cfg.N) / np.abs(want).max() + 1e-12
 
 
+def _tail_idx(cfg, seed, per=3):
+    """flat indices whose strided-axis position is in the last thread's rows of the line
+    transform (the transposed store writes them with direct global stores): y rows n-17..n-1
+    (2-D / 3-D) and, in 3-D, z planes n-17..n-1 too (the z pass)."""
+    n, rng = cfg.n, np.random.default_rng(seed)
+    tail = np.arange(max(0, n - 17), n)
+    out = []
+    for y in tail:
+        for x in rng.integers(0, n, per):
+            if cfg.dim == 2:
+                out.append(y * n + x)
+            else:
+                out.append(rng.integers(0, n) * n * n + y * n + x)  # y tail, any z
+                out.append(y * n * n + rng.integers(0, n) * n + x)  # z tail, any y
+    return np.array(out)
+
+
+@pytest.mark.parametrize("dim,n", [(2, 255), (2, 2047), (2, 4095), (3, 255)])
+def test_dst_tail_rows_sampled(orc, dim, n):
+    """The strided passes' last rows (stored outside the transposed TMA box) at every line
+    length class the bench and the fuzz use: sampled DST outputs against the oracle."""
+    cfg = synth.Config("t", dim, n, 1.0, 1.0, 1.0, 4, 1e-2)
+    plan = Plan(Problem.from_config(cfg))
+    x = np.random.default_rng(15).standard_normal(cfg.shape)
+    got = H(plan.dst(T(x))).reshape(-1)
+    idx = _tail_idx(cfg, 16)
+    want = orc.dst_sample(orc.spec(cfg), x, idx)
+    assert relmax(got[idx], want) < 1e-12 * np.sqrt(cfg.N) / np.abs(want).max() + 1e-12
+
+
+def test_nonlin_hat_tail_rows_sampled(orc):
+    """The fused [V, N, V] pass's last rows at c5's slice size (2047^2)."""
+    cfg = synth.CONFIGS["c5"].scaled(2047, 4)
+    plan = Plan(Problem.from_config(cfg))
+    s = orc.spec(cfg)
+    uh = np.random.default_rng(65).standard_normal((1,) + cfg.shape) / np.sqrt(cfg.N)
+    got = H(plan.nonlin_hat(T(uh))).reshape(-1)
+    idx = _tail_idx(cfg, 66)
+    want = orc.dst_sample(s, orc.nonlin(s, orc.dst(s, uh[0])), idx)
+    assert np.abs(got[idx] - want).max() < 1e-12 * np.abs(got).max()
+
+
 # ------------------------------------------------------------------------------------------
 # stage 3: N-hat = V N(V u-hat) (K4; the TMA line kernels for n+1 >= 256)
 # ------------------------------------------------------------------------------------------
