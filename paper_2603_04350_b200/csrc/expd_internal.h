@@ -186,7 +186,7 @@ int nonlin_chunk_slices(const Geom& g);
 bool line_supported(const Geom& g);
 bool tma_available();
 cudaError_t make_tmap_2d(CUtensorMap* m, const double* ptr, unsigned long long cols, unsigned long long rows,
-                         unsigned long long row_bytes, unsigned box_cols, unsigned box_rows);
+                         unsigned long long row_bytes, unsigned box_cols, unsigned box_rows, bool sw128 = false);
 cudaError_t line_pass(const Geom& g, const DstTables& t, const Poly& P, int ax, bool nl, const double* in,
                       double* out, long nslices, cudaStream_t st, const PeerOut* peer = nullptr);
 // the tensor map of one rank's slab for PeerMaps: units x-lines of M doubles per slot, slots

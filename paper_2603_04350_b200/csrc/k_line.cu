@@ -1235,7 +1235,7 @@ static CUtensorMapL2promotion k1_promotion() {
 
 // 2-D fp64 tensor map (no swizzle): rows of `cols` doubles at byte stride row_bytes.
 cudaError_t make_tmap_2d(CUtensorMap* m, const double* ptr, unsigned long long cols, unsigned long long rows,
-                         unsigned long long row_bytes, unsigned box_cols, unsigned box_rows) {
+                         unsigned long long row_bytes, unsigned box_cols, unsigned box_rows, bool sw128) {
   EncodeTiledFn f = encode_fn();
   if (!f) return cudaErrorNotSupported;
   const cuuint64_t d[2] = {cols, rows};
@@ -1243,8 +1243,8 @@ cudaError_t make_tmap_2d(CUtensorMap* m, const double* ptr, unsigned long long c
   const cuuint32_t b[2] = {box_cols, box_rows};
   const cuuint32_t es[2] = {1, 1};
   CUresult r = f(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(ptr), d, s, b, es,
-                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, k1_promotion(),
-                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                 CU_TENSOR_MAP_INTERLEAVE_NONE, sw128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                 k1_promotion(), CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
 bool tma_available() { return encode_fn() != nullptr; }

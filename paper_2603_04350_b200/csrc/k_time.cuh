@@ -1240,7 +1240,7 @@ static int pipe_mode() {
 static int k1_env() {
   const char* e = getenv("EXPD_K1V");
   int v = e ? atoi(e) : 0;
-  return (v == 2562 || v == 1282 || v == 2561 || v == 5123) ? v : 0;
+  return (v == 2562 || v == 1282 || v == 2561 || v == 5123 || v == 5124) ? v : 0;
 }
 // The TMA-kernel variant when the ring is not used: 2562 (256 threads, double-buffered tiles,
 // 1 CTA/SM), 2561 (single stage, 2 CTAs/SM), 1282 (128 threads; round 1's Nt = 128 default).
@@ -1279,6 +1279,269 @@ static cudaError_t launch_tma(const TimeArgs& a, int grid, cudaStream_t st) {
     return e;
   // the caller's grid (time_fused_grid) is also the number of partial sums it reduces
   k<<<(unsigned)grid, THR, PL::BYTES, st>>>(mx, mn, a);
+  return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------------------------------
+// K1 warp-per-pair ring (EXPD_K1V = 5124; Nt = 256, the Picard forms ETD1 / ETD2 with
+// residual + update): the ring above with the thread mapping turned around -- warp s of a
+// 256-thread group owns mode pair s of the tile and lane j its stage-0 / middle / partner
+// jobs, so every FFT exchange stays inside one warp (__syncwarp) and a tile needs two group
+// barriers (tile read, scratch released, result staged) instead of six.  Consequences of the mapping:
+//  * the Û / N̂ tiles land with the 128-byte TMA swizzle (element (t, s) at chunk s ^ (t & 7)
+//    of row t), so the lanes' reads of one pair down the time column are conflict free;
+//  * warp s's FFT scratch is its own padded 4.5 KB slice of the tile's Û + N̂ blocks (free once
+//    the group has read the tile); each stage's layout (one pad slot per 8 or per 32
+//    positions) and a lane -> partner-job table keep every access affine and conflict free;
+//  * the result is staged into the tile's Û block (swizzled like the input: conflict free) and
+//    leaves as ONE TMA store per tile (a lane-per-slice register store would touch 32 rows per
+//    instruction), after which the issuing thread waits for the store to read the buffer and
+//    refills it.
+// Same arithmetic in the same order per mode as k_time_ring (identical results).
+// ---------------------------------------------------------------------------------------
+template <int NT, int NL>
+struct WpLayout {
+  static constexpr int S = 8;
+  static constexpr int TILE = NT * S;                        // double2 per staged array
+  static constexpr int AUX = 4 * S;
+  static constexpr int STAGE = ((2 * TILE + AUX) + 63) / 64 * 64;  // 1 KB multiple (swizzle atoms)
+  static constexpr int NBUF = 3;
+  static constexpr int WSLOTS = NT + NT / 8;                // a warp's scratch: 256 positions + pads
+  static constexpr size_t BYTES =
+      1024 + sizeof(double2) * ((size_t)NBUF * STAGE + NT + 16 + NT + NT / 8) + sizeof(double) * 2 * NT + 8 * NBUF + 16;
+};
+
+// (t, s) of a staged tile with the 128-byte swizzle: row t of 8 pairs (16-byte chunks)
+__device__ __forceinline__ int wp_sw(int t, int s) { return t * 8 + (s ^ (t & 7)); }
+
+// Lane -> partner job (ja; jb = 64 - ja, 32 for ja = 0) of the last stage: any bijection is
+// valid; this one (a search over lane groupings, tools/wp_lanes.py) makes the partner reads of
+// layout L2 and the partner writes of layout L3 bank-conflict free for both ja and jb.
+__device__ const unsigned char kWpPj[32] = {8, 0, 25, 7, 13, 24, 16, 19, 22, 21, 2, 26, 1, 27, 10, 11,
+                                            20, 30, 15, 17, 5, 4, 31, 14, 28, 3, 23, 12, 29, 9, 6, 18};
+
+template <int NT, int RM, int OUTM, int NL>
+__global__ void __launch_bounds__(512, 1)
+    k_time_wp(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mn,
+              const __grid_constant__ CUtensorMap my, const __grid_constant__ TimeArgs a) {
+  static_assert(NT == 256 && (NL == 1 || NL == 2) && RM == RM_RESID && OUTM == OUT_UPDATE,
+                "warp-per-pair K1: Nt = 256, Picard residual + update");
+  using C = TimeCfg<NT>;
+  using PL = WpLayout<NT, NL>;
+  constexpr int R0 = C::R0, R1 = C::R1, RL = C::R2, TPS = NT / R0, S = PL::S, GT = 256;
+  constexpr int NSL = NT / RL, TILE = PL::TILE, NBUF = PL::NBUF, WS = PL::WSLOTS;
+  static_assert(R0 == 8 && R1 == 8 && RL == 4 && TPS == 32 && NSL / 2 == 32, "plan 8 x 8 x 4, one job per lane");
+  static_assert(S * WS <= 2 * TILE, "the warps' scratch fits the tile's two blocks");
+  extern __shared__ unsigned char wsm_raw[];
+  double2* smem = reinterpret_cast<double2*>(wsm_raw + ((1024u - (smem_u32(wsm_raw) & 1023u)) & 1023u));
+  double2* stw = smem + NBUF * PL::STAGE;              // [NT] e^{+2 pi i q/NT}
+  double2* tmid = stw + NT;                            // [8] forward / [4] inverse middle twiddles
+  double2* stwp = tmid + 16;                           // [NT + NT/8] stw padded (slot q + q/8)
+  double* sg = reinterpret_cast<double*>(stwp + NT + NT / 8);  // [NT] alpha^{t/NT}
+  double* sgi = sg + NT;                               // [NT] alpha^{-t/NT}
+  uint64_t* full = reinterpret_cast<uint64_t*>(sgi + NT);
+
+  const int grp = threadIdx.x / GT;
+  const int tid = threadIdx.x % GT;
+  for (int i = threadIdx.x; i < NT; i += 2 * GT) {
+    stw[i] = a.tw[i];
+    stwp[i + (i >> 3)] = a.tw[i];
+    sg[i] = a.g[i];
+    sgi[i] = a.ginv[i];
+  }
+  // the middle stages' base twiddles w^{4q} (forward, q < 8) and w^{8q} (inverse, q < 4) packed
+  // into one 128-byte line each: a warp's eight distinct values are one wavefront
+  if (threadIdx.x < 8) tmid[threadIdx.x] = a.tw[(threadIdx.x * (NT / (R0 * R1))) & (NT - 1)];
+  else if (threadIdx.x < 12) tmid[threadIdx.x] = a.tw[((threadIdx.x - 8) * (NT / (RL * R1))) & (NT - 1)];
+  const long ntiles = a.npairs / S;
+  if (threadIdx.x == 0) {
+    prefetch_tmap(&mx);
+    prefetch_tmap(&mn);
+    prefetch_tmap(&my);
+    for (int k = 0; k < NBUF; ++k) mbar_init(&full[k], 1);
+    mbar_fence_init();
+    for (int k = 0; k < NBUF; ++k) {
+      const long t = blockIdx.x + (long)k * gridDim.x;
+      if (t < ntiles) ring_issue<NT, RM, NL>(&mx, &mn, a, t, smem + k * PL::STAGE, &full[k]);
+    }
+  }
+  __syncthreads();
+  const double hin = a.half_inv_nt;
+  double nrm = 0.0;
+  const int s = tid >> 5;   // this warp's mode pair
+  const int j = tid & 31;   // lane: stage-0 / middle job
+  const int ja = kWpPj[j];  // partner jobs
+  const int jb = ja == 0 ? NSL / 2 : NSL - ja;
+  const int barid = 1 + grp;
+  // scratch layouts (16-byte slots of the warp's region): L1 / L2 / L4 one pad slot per 8
+  // positions (p + p/8), L3 one per 32 (p + p/32); every stage's reads and writes are
+  // affine in r with a per-lane base and hit eight distinct bank groups per quarter warp
+  const int l1w = 9 * j;                                   // stage-0 write  (p = 8j + r)
+  const int lrd = j + (j >> 3);                            // reads p = j + 32r (L1, L4): + 36r
+  const int l2w = (j >> 3) * 72 + (j & 7);                 // forward middle write: + 9r
+  const int l2a = ja + (ja >> 3), l2b = jb + (jb >> 3);    // partner reads: + 72r
+  const int l3a = 4 * ja + (ja >> 3), l3b = 4 * jb + (jb >> 3);  // partner writes: + r
+  const int l4w = (j >> 2) * 36 + (j & 3);                 // inverse middle write: + 4r + r/2
+
+  for (long i = grp;; i += 2) {
+    const long tile = blockIdx.x + i * gridDim.x;
+    if (tile >= ntiles) break;
+    const int b = (int)(i % NBUF);
+    double2* stg = smem + b * PL::STAGE;
+    mbar_wait(&full[b], (uint32_t)((i / NBUF) & 1));
+    double2* X = stg;                              // Û tile (swizzled); later the staged result
+    const double2* NH = stg + TILE;                // N̂ tile (swizzled)
+    const double2* aux = stg + 2 * TILE;
+    double2* W = stg + s * WS;                     // this warp's FFT scratch (after phase A)
+    int two = 0;
+    asm volatile("" : "+r"(two));
+    const double2* tw = stw + two;
+
+    // ---- phase A: residual (+ ||r||^2), Gamma_alpha, forward stage 0 -------------------
+    double2 y[R0], xv[R0];
+    const double2 Ej = aux[s];
+    const double2 c1 = aux[S + s];
+    const double2 c2 = NL == 2 ? aux[2 * S + s] : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int r = 0; r < R0; ++r) {
+      const int t = j + r * TPS;
+      const double2 xc = X[wp_sw(t, s)];
+      xv[r] = xc;
+      const double2 prev = t > 0 ? X[wp_sw(t - 1, s)] : aux[3 * S + s];
+      double2 rr = make_double2(fma(Ej.x, prev.x, -xc.x), fma(Ej.y, prev.y, -xc.y));
+      const double2 nm1 = NH[wp_sw(t, s)];
+      rr.x = fma(c1.x, nm1.x, rr.x);
+      rr.y = fma(c1.y, nm1.y, rr.y);
+      if constexpr (NL == 2) {
+        const double2 nm2 = NH[wp_sw(t > 0 ? t - 1 : 0, s)];
+        rr.x = fma(-c2.x, nm2.x, rr.x);
+        rr.y = fma(-c2.y, nm2.y, rr.y);
+      }
+      nrm = fma(rr.x, rr.x, fma(rr.y, rr.y, nrm));
+      y[r] = cscale(rr, sg[t]);
+    }
+    DFT<R0, +1>::run(y);
+    named_bar(barid, GT);  // the group has read the tile: both blocks become the warps' scratch
+#pragma unroll
+    for (int r = 0; r < R0; ++r) W[l1w + r] = y[r];
+    __syncwarp();
+    {  // forward middle stage (radix R1, NS = R0), in place
+      double2 v[R1];
+#pragma unroll
+      for (int r = 0; r < R1; ++r) v[r] = W[lrd + 36 * r];
+      twpow_mul<R1, +1>(v, tmid[j & 7]);
+      DFT<R1, +1>::run(v);
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < R1; ++r) W[l2w + 9 * r] = v[r];
+      __syncwarp();
+    }
+    {  // last forward stage on Hermitian partner jobs, the divide, first inverse stage
+      double2 va[RL], vb[RL];
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        va[r] = W[l2a + 72 * r];
+        vb[r] = W[l2b + 72 * r];
+      }
+      // partner twiddles and the divide's e^{2 pi i k/NT} from the padded copy: the reads at
+      // q = x + 64 r hit bank (x + x/8) mod 8, distinct over a quarter warp (kWpPj)
+      const double2* twp = stwp + two;
+      twpow_mul<RL, +1>(va, twp[l2a]);
+      twpow_mul<RL, +1>(vb, twp[l2b]);
+      DFT<RL, +1>::run(va);
+      DFT<RL, +1>::run(vb);
+      {  // pair_divide (k_time_ring) with the padded table
+        const double ba = a.a1 * Ej.x, bb = a.a1 * Ej.y;
+        if (ja != 0) {
+#pragma unroll
+          for (int r = 0; r < RL; ++r)
+            divide_pair<false>(va[r], vb[RL - 1 - r], twp[l2a + 72 * r], ba, bb, hin, false);
+        } else {
+          // ja = 0: frequencies NSL r, partner NSL (RL - r) mod RL; self at r = 0 and RL/2;
+          // jb = NSL/2: frequencies NSL/2 + NSL r, partner index RL-1-r
+          divide_pair<false>(va[0], va[0], twp[0], ba, bb, hin, true);
+#pragma unroll
+          for (int r = 1; r < (RL + 1) / 2; ++r)
+            divide_pair<false>(va[r], va[RL - r], twp[72 * r], ba, bb, hin, false);
+          divide_pair<false>(va[RL / 2], va[RL / 2], twp[72 * (RL / 2)], ba, bb, hin, true);
+#pragma unroll
+          for (int r = 0; r < RL / 2; ++r)
+            divide_pair<false>(vb[r], vb[RL - 1 - r], twp[l2b + 72 * r], ba, bb, hin, false);
+        }
+      }
+      DFT<RL, -1>::run(va);
+      DFT<RL, -1>::run(vb);
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        W[l3a + r] = va[r];
+        W[l3b + r] = vb[r];
+      }
+      __syncwarp();
+    }
+    {  // inverse middle stage (radix R1, NS = RL), in place
+      double2 v[R1];
+#pragma unroll
+      for (int r = 0; r < R1; ++r) v[r] = W[j + 33 * r];
+      twpow_mul<R1, -1>(v, tmid[8 + (j & 3)]);
+      DFT<R1, -1>::run(v);
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < R1; ++r) W[l4w + 4 * r + (r >> 1)] = v[r];
+      __syncwarp();
+    }
+#pragma unroll
+    for (int r = 0; r < R0; ++r) y[r] = W[lrd + 36 * r];
+    named_bar(barid, GT);  // every warp is done with its scratch: the Û block takes the result
+    twpow_mul<R0, -1>(y, tw[j]);
+    DFT<R0, -1>::run(y);
+    // ---- phase C: Gamma_alpha^{-1}, update, staged into the Û block, one TMA store ------
+#pragma unroll
+    for (int r = 0; r < R0; ++r) {
+      const int t = j + r * TPS;
+      X[wp_sw(t, s)] = cadd(xv[r], cscale(y[r], sgi[t]));
+    }
+    fence_proxy_async_smem();
+    named_bar(barid, GT);
+    if (tid == 0) {
+      tma_store_2d(&my, X, (int)(2 * S * tile), 0);
+      bulk_commit();
+      const long nxt = blockIdx.x + (i + NBUF) * gridDim.x;
+      if (nxt < ntiles) {
+        bulk_wait_read0();  // the store has read the staged result: refill the buffer
+        ring_issue<NT, RM, NL>(&mx, &mn, a, nxt, stg, &full[b]);
+      }
+    }
+  }
+  if (tid == 0) bulk_wait0();
+
+  if (a.partial) {
+    __shared__ double red[2 * GT / 32];
+    for (int o = 16; o > 0; o >>= 1) nrm += __shfl_xor_sync(0xffffffffu, nrm, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = nrm;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      double v = threadIdx.x < 2 * GT / 32 ? red[threadIdx.x] : 0.0;
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (threadIdx.x == 0) a.partial[blockIdx.x] = v;
+    }
+  }
+}
+
+template <int NT, int RM, int OUTM, int NL>
+static cudaError_t launch_wp(const TimeArgs& a, int grid, cudaStream_t st) {
+  using PL = WpLayout<NT, NL>;
+  auto k = k_time_wp<NT, RM, OUTM, NL>;
+  static DevOnce attr;  // per instantiation and device
+  if (cudaError_t e = smem_optin(attr, k, PL::BYTES); e != cudaSuccess) return e;
+  constexpr int S = PL::S;
+  CUtensorMap mx, mn, my;
+  const unsigned long long np = (unsigned long long)a.npad, nt = (unsigned long long)a.nt, rb = np * 8;
+  cudaError_t e = make_tmap_2d(&mx, a.X, np, nt, rb, 2 * S, NT, true);
+  if (e == cudaSuccess) e = make_tmap_2d(&mn, a.Nh, np, nt, rb, 2 * S, NT, true);
+  if (e == cudaSuccess) e = make_tmap_2d(&my, a.Y, np, nt, rb, 2 * S, NT, true);
+  if (e != cudaSuccess) return e;
+  k<<<(unsigned)grid, 512, PL::BYTES, st>>>(mx, mn, my, a);
   return cudaGetLastError();
 }
 
@@ -1332,8 +1595,21 @@ static bool use_ring(long npairs) {
   }
 }
 
+// the warp-per-pair K1 (EXPD_K1V=5124): Nt = 256 Picard sweeps with full tiles
+template <int NT, int RM, int OUTM, int NL>
+static bool use_wp(long npairs) {
+  if constexpr (NT == 256 && (NL == 1 || NL == 2) && RM == RM_RESID && OUTM == OUT_UPDATE) {
+    return pipe_mode() == 3 && npairs % WpLayout<NT, NL>::S == 0 && k1_env() == 5124;
+  } else {
+    return false;
+  }
+}
+
 template <int NT, int RM, int OUTM, int NL>
 static cudaError_t launch_t(const TimeArgs& a, int grid, cudaStream_t st) {
+  if constexpr (NT == 256 && (NL == 1 || NL == 2) && RM == RM_RESID && OUTM == OUT_UPDATE) {
+    if (use_wp<NT, RM, OUTM, NL>(a.npairs)) return launch_wp<NT, RM, OUTM, NL>(a, grid, st);
+  }
   if constexpr (ring_capable<NT>()) {
     if (use_ring<NT>(a.npairs)) return launch_ring<NT, RM, OUTM, NL>(a, grid, st);
   }

@@ -247,6 +247,14 @@ def test_fixed_point_parity(orc, name, n, nt):
     assert np.allclose(h[big], hist[big], rtol=1e-6)
 
 
+@pytest.mark.parametrize("name,n,nt", [("c5", 63, 256), ("c5if", 63, 256), ("c3", 63, 256)])
+def test_k1_warp_per_pair_matches_oracle(orc, name, n, nt, monkeypatch):
+    """The warp-per-pair K1 (EXPD_K1V=5124, opt-in) on the Nt = 256 Picard
+    forms it serves (ETD2, IF/IMEX, ETD1): the oracle's iterations, history and solution."""
+    monkeypatch.setenv("EXPD_K1V", "5124")
+    test_fixed_point_parity(orc, name, n, nt)
+
+
 @pytest.mark.parametrize("name,n,nt", [("c1", None, None), ("c2", 63, 64), ("c4", 15, 64), ("c1bdf2", None, None),
                                        ("c2bdf2", 63, 64)])
 def test_gmres_parity(orc, name, n, nt):
