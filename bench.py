@@ -44,7 +44,8 @@ FP64_PEAK_TFLOPS = 34.19
 
 
 def k1_kernel(cfg, lay) -> str:
-    """The K1 kernel the library launches for this plan (csrc/k_time.cuh use_ring): the ring
+    """The K1 kernel the library launches for this plan (csrc/k_time.cuh use_wp / use_ring): the
+    warp-per-pair kernel for Nt = 256 Picard sweeps, else the ring
     when the mode slab holds whole tiles, at Nt = 128 / 256 always and at Nt = 16 / 32 / 64
     with at least 16 tiles per SM, unless EXPD_K1V picks a variant; else the TMA-fed kernel."""
     tile = {16: 64, 32: 64, 64: 32, 128: 16, 256: 8}.get(cfg.nt)
@@ -54,6 +55,9 @@ def k1_kernel(cfg, lay) -> str:
     v = os.environ.get("EXPD_K1V")
     if v in ("2562", "1282", "2561", "5123"):
         return "k_time_ring" if v == "5123" else "k_time_tma"
+    # the warp-per-pair kernel: Nt = 256 Picard sweeps (ETD1 / ETD2 / IF; csrc/k_time.cuh use_wp)
+    if cfg.nt == 256 and cfg.q and cfg.scheme in (0, 1, 2) and not getattr(cfg, "is_complex", False):
+        return "k_time_wp"
     import torch
 
     sms = torch.cuda.get_device_properties(0).multi_processor_count if torch.cuda.is_available() else 148

@@ -1283,8 +1283,8 @@ static cudaError_t launch_tma(const TimeArgs& a, int grid, cudaStream_t st) {
 }
 
 // ---------------------------------------------------------------------------------------
-// K1 warp-per-pair ring (EXPD_K1V = 5124; Nt = 256, the Picard forms ETD1 / ETD2 with
-// residual + update): the ring above with the thread mapping turned around -- warp s of a
+// K1 warp-per-pair ring (the default for Nt = 256 Picard forms ETD1 / ETD2 / IF with residual +
+// update and full tiles; EXPD_K1V = 5123 selects the ring instead): the ring above with the thread mapping turned around -- warp s of a
 // 256-thread group owns mode pair s of the tile and lane j its stage-0 / middle / partner
 // jobs, so every FFT exchange stays inside one warp (__syncwarp) and a tile needs two group
 // barriers (tile read, scratch released, result staged) instead of six.  Consequences of the mapping:
@@ -1307,8 +1307,11 @@ struct WpLayout {
   static constexpr int STAGE = ((2 * TILE + AUX) + 63) / 64 * 64;  // 1 KB multiple (swizzle atoms)
   static constexpr int NBUF = 3;
   static constexpr int WSLOTS = NT + NT / 8;                // a warp's scratch: 256 positions + pads
-  static constexpr size_t BYTES =
-      1024 + sizeof(double2) * ((size_t)NBUF * STAGE + NT + 16 + NT + NT / 8) + sizeof(double) * 2 * NT + 8 * NBUF + 16;
+  // twiddle power tables (EXPD_WP_TWTAB, default on): forward middle 7 x 8, inverse middle 7 x 4,
+  // partner 3 x 72 (padded), final inverse 7 x 32
+  static constexpr int TWTAB = 56 + 28 + 216 + 224;
+  static constexpr size_t BYTES = 1024 + sizeof(double2) * ((size_t)NBUF * STAGE + NT + 16 + NT + NT / 8 + TWTAB) +
+                                  sizeof(double) * 2 * NT + 8 * NBUF + 16;
 };
 
 // (t, s) of a staged tile with the 128-byte swizzle: row t of 8 pairs (16-byte chunks)
@@ -1337,7 +1340,8 @@ __global__ void __launch_bounds__(512, 1)
   double2* stw = smem + NBUF * PL::STAGE;              // [NT] e^{+2 pi i q/NT}
   double2* tmid = stw + NT;                            // [8] forward / [4] inverse middle twiddles
   double2* stwp = tmid + 16;                           // [NT + NT/8] stw padded (slot q + q/8)
-  double* sg = reinterpret_cast<double*>(stwp + NT + NT / 8);  // [NT] alpha^{t/NT}
+  double2* ttab = stwp + NT + NT / 8;                  // [TWTAB] twiddle powers (see below)
+  double* sg = reinterpret_cast<double*>(ttab + PL::TWTAB);  // [NT] alpha^{t/NT}
   double* sgi = sg + NT;                               // [NT] alpha^{-t/NT}
   uint64_t* full = reinterpret_cast<uint64_t*>(sgi + NT);
 
@@ -1353,6 +1357,20 @@ __global__ void __launch_bounds__(512, 1)
   // into one 128-byte line each: a warp's eight distinct values are one wavefront
   if (threadIdx.x < 8) tmid[threadIdx.x] = a.tw[(threadIdx.x * (NT / (R0 * R1))) & (NT - 1)];
   else if (threadIdx.x < 12) tmid[threadIdx.x] = a.tw[((threadIdx.x - 8) * (NT / (RL * R1))) & (NT - 1)];
+  // the stages' twiddle powers w^r = e^{2 pi i k r / NT} straight from the table (one rounding,
+  // no products; K1-wp is fp64-issue bound and its shared memory has slack): FM[r-1][c]
+  // (forward middle, k = 4c), IM[r-1][c] (inverse middle, k = 8c), PA[r-1][x + x/8] (partner
+  // job x < 64, padded like stwp), FC[r-1][j] (final inverse stage, k = j)
+  for (int q = threadIdx.x; q < PL::TWTAB; q += 2 * GT) {
+    int e;
+    if (q < 56) e = 4 * (q & 7) * (q / 8 + 1);
+    else if (q < 84) e = 8 * ((q - 56) & 3) * ((q - 56) / 4 + 1);
+    else if (q < 300) {
+      const int r = (q - 84) / 72 + 1, y = (q - 84) % 72;  // y = x + x/8 for x < 64 (pads: y % 9 == 8)
+      e = (y % 9 == 8) ? 0 : (y / 9 * 8 + y % 9) * r;
+    } else e = ((q - 300) & 31) * ((q - 300) / 32 + 1);
+    ttab[q] = a.tw[e & (NT - 1)];
+  }
   const long ntiles = a.npairs / S;
   if (threadIdx.x == 0) {
     prefetch_tmap(&mx);
@@ -1429,7 +1447,8 @@ __global__ void __launch_bounds__(512, 1)
       double2 v[R1];
 #pragma unroll
       for (int r = 0; r < R1; ++r) v[r] = W[lrd + 36 * r];
-      twpow_mul<R1, +1>(v, tmid[j & 7]);
+#pragma unroll
+      for (int r = 1; r < R1; ++r) v[r] = cmul(v[r], ttab[(r - 1) * 8 + (j & 7)]);
       DFT<R1, +1>::run(v);
       __syncwarp();
 #pragma unroll
@@ -1446,8 +1465,11 @@ __global__ void __launch_bounds__(512, 1)
       // partner twiddles and the divide's e^{2 pi i k/NT} from the padded copy: the reads at
       // q = x + 64 r hit bank (x + x/8) mod 8, distinct over a quarter warp (kWpPj)
       const double2* twp = stwp + two;
-      twpow_mul<RL, +1>(va, twp[l2a]);
-      twpow_mul<RL, +1>(vb, twp[l2b]);
+#pragma unroll
+      for (int r = 1; r < RL; ++r) {
+        va[r] = cmul(va[r], ttab[84 + (r - 1) * 72 + l2a]);
+        vb[r] = cmul(vb[r], ttab[84 + (r - 1) * 72 + l2b]);
+      }
       DFT<RL, +1>::run(va);
       DFT<RL, +1>::run(vb);
       {  // pair_divide (k_time_ring) with the padded table
@@ -1483,7 +1505,8 @@ __global__ void __launch_bounds__(512, 1)
       double2 v[R1];
 #pragma unroll
       for (int r = 0; r < R1; ++r) v[r] = W[j + 33 * r];
-      twpow_mul<R1, -1>(v, tmid[8 + (j & 3)]);
+#pragma unroll
+      for (int r = 1; r < R1; ++r) v[r] = cmulc(v[r], ttab[56 + (r - 1) * 4 + (j & 3)]);
       DFT<R1, -1>::run(v);
       __syncwarp();
 #pragma unroll
@@ -1493,7 +1516,8 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
     for (int r = 0; r < R0; ++r) y[r] = W[lrd + 36 * r];
     named_bar(barid, GT);  // every warp is done with its scratch: the Û block takes the result
-    twpow_mul<R0, -1>(y, tw[j]);
+#pragma unroll
+    for (int r = 1; r < R0; ++r) y[r] = cmulc(y[r], ttab[300 + (r - 1) * 32 + j]);
     DFT<R0, -1>::run(y);
     // ---- phase C: Gamma_alpha^{-1}, update, staged into the Û block, one TMA store ------
 #pragma unroll
@@ -1595,11 +1619,13 @@ static bool use_ring(long npairs) {
   }
 }
 
-// the warp-per-pair K1 (EXPD_K1V=5124): Nt = 256 Picard sweeps with full tiles
+// the warp-per-pair K1 (the default for Nt = 256 Picard sweeps with full tiles; EXPD_K1V=5123
+// forces the ring, profiles/r02/k1_wp_ab.txt)
 template <int NT, int RM, int OUTM, int NL>
 static bool use_wp(long npairs) {
   if constexpr (NT == 256 && (NL == 1 || NL == 2) && RM == RM_RESID && OUTM == OUT_UPDATE) {
-    return pipe_mode() == 3 && npairs % WpLayout<NT, NL>::S == 0 && k1_env() == 5124;
+    const int v = k1_env();
+    return pipe_mode() == 3 && npairs % WpLayout<NT, NL>::S == 0 && (v == 0 || v == 5124);
   } else {
     return false;
   }

@@ -247,11 +247,13 @@ def test_fixed_point_parity(orc, name, n, nt):
     assert np.allclose(h[big], hist[big], rtol=1e-6)
 
 
+@pytest.mark.parametrize("k1v", ["5124", "5123"])
 @pytest.mark.parametrize("name,n,nt", [("c5", 63, 256), ("c5if", 63, 256), ("c3", 63, 256)])
-def test_k1_warp_per_pair_matches_oracle(orc, name, n, nt, monkeypatch):
-    """The warp-per-pair K1 (EXPD_K1V=5124, opt-in) on the Nt = 256 Picard
-    forms it serves (ETD2, IF/IMEX, ETD1): the oracle's iterations, history and solution."""
-    monkeypatch.setenv("EXPD_K1V", "5124")
+def test_k1_nt256_picard_variants_match_oracle(orc, name, n, nt, k1v, monkeypatch):
+    """Both K1 kernels of the Nt = 256 Picard forms (ETD2, IF/IMEX, ETD1):
+    the warp-per-pair kernel (5124, the default) and the ring (5123): the oracle's iterations,
+    history and solution."""
+    monkeypatch.setenv("EXPD_K1V", k1v)
     test_fixed_point_parity(orc, name, n, nt)
 
 

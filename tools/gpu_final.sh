@@ -20,6 +20,6 @@ timeout 300 python tools/loop_timing.py c1 c2 > $O/${tag}_loop_timing.json 2>&1
 timeout 300 python tools/solve_breakdown.py c1 c2 > $O/${tag}_solve_breakdown.json 2>&1
 CMD="python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu"
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none --csv --log-file $O/${tag}_launches.csv $CMD > $O/${tag}_ncu_launch.log 2>&1; echo "ncu launches exit $?"
-timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_time_ring" -s 2 -c 1 -o $O/${tag}_prof_k1 $CMD > $O/${tag}_ncu_k1.log 2>&1; echo "ncu k1 exit $?"
+timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_time_(ring|wp)" -s 2 -c 1 -o $O/${tag}_prof_k1 $CMD > $O/${tag}_ncu_k1.log 2>&1; echo "ncu k1 exit $?"
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_line.*bool.1" -s 20 -c 1 -o $O/${tag}_prof_colnl $CMD > $O/${tag}_ncu_colnl.log 2>&1; echo "ncu colnl exit $?"
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_line.*2048, .int.0," -s 2 -c 1 -o $O/${tag}_prof_row $CMD > $O/${tag}_ncu_row.log 2>&1; echo "ncu row exit $?"

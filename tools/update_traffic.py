@@ -63,11 +63,11 @@ for r in rows[hi + 1:]:
         per[r[ii]][r[mi]] = x
         per[r[ii]]["name"] = r[ki]
 tot, sweeps = 0.0, 0
-sweep_kernels = ("k_time_ring", "k_time_tma", "k_line<2048, 0, 0", "k_line<2048, 1, 1", "k_stage3p", "k_reduce_rows")
+sweep_kernels = ("k_time_ring", "k_time_wp", "k_time_tma", "k_line<2048, 0, 0", "k_line<2048, 1, 1", "k_stage3p", "k_reduce_rows")
 first_k1 = None
 for lid in sorted(per, key=int):
     d = per[lid]
-    if any(s in d["name"] for s in ("k_time_ring", "k_time_tma")):
+    if any(s in d["name"] for s in ("k_time_ring", "k_time_wp", "k_time_tma")):
         sweeps += 1
         first_k1 = first_k1 or int(lid)
 for lid in sorted(per, key=int):
