@@ -78,6 +78,7 @@ def relmax(got, want):
 @pytest.mark.parametrize("P,name,n,nt,solvers", [
     (2, "c7se", 31, 8, ("fixed_point", "gmres", "bicgstab")),  # complex 2D, 16 + 15 x-lines
     (2, "c5", 63, 8, ("fixed_point",)),                         # ETD2 Picard: stage 3 on time slabs
+    (2, "c5", 63, 256, ("fixed_point",)),                       # Nt = 256: the warp-per-pair K1 on mode slabs
     (2, "c2bdf2", 63, 64, ("fixed_point", "gmres")),            # exponential BDF2 (NEXT-2)
     (2, "c2", 63, 64, ("bicgstab",)),                           # real BiCGStab (NEXT-4)
     (2, "c5if", 31, 8, ("fixed_point",)),                       # IMEX-type iteration (NEXT-1)
