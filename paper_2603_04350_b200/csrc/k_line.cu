@@ -1413,7 +1413,7 @@ static cudaError_t launch_col(const Geom& g, const DstTables& t, const Poly& P, 
     // buffers (22.93 vs 23.02 ms per sweep with 1 buffer once the partner-lane tables made
     // its transforms faster and the exposed TMA wait grew to 21 % of its samples)
     switch (colv()) {
-      case 11: return launch_line<M, AX, NL, 1, 1>(g, t, P, in, out, nslices, st);
+      case 11: return launch_line<M, AX, NL, 1, 1, false, true>(g, t, P, in, out, nslices, st);
       case 12: return launch_line<M, AX, NL, 1, 2>(g, t, P, in, out, nslices, st);
       case 21: return launch_line<M, AX, NL, 2, 1>(g, t, P, in, out, nslices, st);
       case 22: return launch_line<M, AX, NL, 2, 2>(g, t, P, in, out, nslices, st);
