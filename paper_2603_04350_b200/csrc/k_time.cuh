@@ -1287,11 +1287,12 @@ static cudaError_t launch_tma(const TimeArgs& a, int grid, cudaStream_t st) {
 // update and full tiles; EXPD_K1V = 5123 selects the ring instead): the ring above with the thread mapping turned around -- warp s of a
 // 256-thread group owns mode pair s of the tile and lane j its stage-0 / middle / partner
 // jobs, so every FFT exchange stays inside one warp (__syncwarp) and a tile needs two group
-// barriers (tile read, scratch released, result staged) instead of six.  Consequences of the mapping:
+// barriers (tile read, result staged) instead of six.  Consequences of the mapping:
 //  * the Û / N̂ tiles land with the 128-byte TMA swizzle (element (t, s) at chunk s ^ (t & 7)
 //    of row t), so the lanes' reads of one pair down the time column are conflict free;
-//  * warp s's FFT scratch is its own padded 4.5 KB slice of the tile's Û + N̂ blocks (free once
-//    the group has read the tile); each stage's layout (one pad slot per 8 or per 32
+//  * warp s's FFT scratch is its own padded 4.5 KB slice of the N̂ tile plus a pad area after it
+//    (free once the group has read the tile; the Û tile stays intact, so u_t is re-read for the
+//    update instead of held in registers); each stage's layout (one pad slot per 8 or per 32
 //    positions) and a lane -> partner-job table keep every access affine and conflict free;
 //  * the result is staged into the tile's Û block (swizzled like the input: conflict free) and
 //    leaves as ONE TMA store per tile (a lane-per-slice register store would touch 32 rows per
@@ -1304,13 +1305,16 @@ struct WpLayout {
   static constexpr int S = 8;
   static constexpr int TILE = NT * S;                        // double2 per staged array
   static constexpr int AUX = 4 * S;
-  static constexpr int STAGE = ((2 * TILE + AUX) + 63) / 64 * 64;  // 1 KB multiple (swizzle atoms)
-  static constexpr int NBUF = 3;
   static constexpr int WSLOTS = NT + NT / 8;                // a warp's scratch: 256 positions + pads
+  // stage: [Û tile][N̂ tile][pad area][aux]: the warps' scratch runs from the N̂ tile into the pad
+  // area (S WSLOTS = TILE + S NT/8 slots), so the Û tile stays intact until phase C
+  static constexpr int AUXOFF = 2 * TILE + S * (NT / 8);
+  static constexpr int STAGE = ((AUXOFF + AUX) + 63) / 64 * 64;  // 1 KB multiple (swizzle atoms)
+  static constexpr int NBUF = 3;
   // twiddle power tables (EXPD_WP_TWTAB, default on): forward middle 7 x 8, inverse middle 7 x 4,
   // partner 3 x 72 (padded), final inverse 7 x 32
   static constexpr int TWTAB = 56 + 28 + 216 + 224;
-  static constexpr size_t BYTES = 1024 + sizeof(double2) * ((size_t)NBUF * STAGE + NT + 16 + NT + NT / 8 + TWTAB) +
+  static constexpr size_t BYTES = 1024 + sizeof(double2) * ((size_t)NBUF * STAGE + NT + NT / 8 + TWTAB) +
                                   sizeof(double) * 2 * NT + 8 * NBUF + 16;
 };
 
@@ -1323,6 +1327,25 @@ __device__ __forceinline__ int wp_sw(int t, int s) { return t * 8 + (s ^ (t & 7)
 __device__ const unsigned char kWpPj[32] = {8, 0, 25, 7, 13, 24, 16, 19, 22, 21, 2, 26, 1, 27, 10, 11,
                                             20, 30, 15, 17, 5, 4, 31, 14, 28, 3, 23, 12, 29, 9, 6, 18};
 
+// ring_issue with the warp-per-pair stage layout (aux after the pad area)
+template <int NT, int RM, int NL>
+__device__ __forceinline__ void wp_issue(const CUtensorMap* mx, const CUtensorMap* mn, const TimeArgs& a, long tile,
+                                         double2* stage, uint64_t* bar) {
+  using PL = WpLayout<NT, NL>;
+  constexpr int S = PL::S, TILE = PL::TILE;
+  constexpr uint32_t AUXB = 16 * S;
+  constexpr int NAUX = 2 + (NL == 2 ? 1 : 0) + 1;  // E, C1, (C2), u0-hat
+  mbar_arrive_expect_tx(bar, (uint32_t)(2 * TILE * 16) + NAUX * AUXB);
+  tma_load_2d(stage, mx, bar, (int)(2 * S * tile), 0);
+  tma_load_2d(stage + TILE, mn, bar, (int)(2 * S * tile), 0);
+  double2* aux = stage + PL::AUXOFF;
+  const long off = 2 * S * tile;  // doubles
+  bulk_load_1d(aux, a.E + off, AUXB, bar);
+  bulk_load_1d(aux + S, a.C1 + off, AUXB, bar);
+  if constexpr (NL == 2) bulk_load_1d(aux + 2 * S, a.C2 + off, AUXB, bar);
+  bulk_load_1d(aux + 3 * S, a.u0h + off, AUXB, bar);
+}
+
 template <int NT, int RM, int OUTM, int NL>
 __global__ void __launch_bounds__(512, 1)
     k_time_wp(const __grid_constant__ CUtensorMap mx, const __grid_constant__ CUtensorMap mn,
@@ -1334,12 +1357,11 @@ __global__ void __launch_bounds__(512, 1)
   constexpr int R0 = C::R0, R1 = C::R1, RL = C::R2, TPS = NT / R0, S = PL::S, GT = 256;
   constexpr int NSL = NT / RL, TILE = PL::TILE, NBUF = PL::NBUF, WS = PL::WSLOTS;
   static_assert(R0 == 8 && R1 == 8 && RL == 4 && TPS == 32 && NSL / 2 == 32, "plan 8 x 8 x 4, one job per lane");
-  static_assert(S * WS <= 2 * TILE, "the warps' scratch fits the tile's two blocks");
+  static_assert(TILE + S * WS <= PL::AUXOFF, "the warps' scratch fits the N-hat tile and the pad area");
+  static_assert(PL::BYTES + 2 * 256 / 32 * 8 <= 232448, "shared memory");
   extern __shared__ unsigned char wsm_raw[];
   double2* smem = reinterpret_cast<double2*>(wsm_raw + ((1024u - (smem_u32(wsm_raw) & 1023u)) & 1023u));
-  double2* stw = smem + NBUF * PL::STAGE;              // [NT] e^{+2 pi i q/NT}
-  double2* tmid = stw + NT;                            // [8] forward / [4] inverse middle twiddles
-  double2* stwp = tmid + 16;                           // [NT + NT/8] stw padded (slot q + q/8)
+  double2* stwp = smem + NBUF * PL::STAGE;             // [NT + NT/8] e^{+2 pi i q/NT} padded (slot q + q/8)
   double2* ttab = stwp + NT + NT / 8;                  // [TWTAB] twiddle powers (see below)
   double* sg = reinterpret_cast<double*>(ttab + PL::TWTAB);  // [NT] alpha^{t/NT}
   double* sgi = sg + NT;                               // [NT] alpha^{-t/NT}
@@ -1348,15 +1370,10 @@ __global__ void __launch_bounds__(512, 1)
   const int grp = threadIdx.x / GT;
   const int tid = threadIdx.x % GT;
   for (int i = threadIdx.x; i < NT; i += 2 * GT) {
-    stw[i] = a.tw[i];
     stwp[i + (i >> 3)] = a.tw[i];
     sg[i] = a.g[i];
     sgi[i] = a.ginv[i];
   }
-  // the middle stages' base twiddles w^{4q} (forward, q < 8) and w^{8q} (inverse, q < 4) packed
-  // into one 128-byte line each: a warp's eight distinct values are one wavefront
-  if (threadIdx.x < 8) tmid[threadIdx.x] = a.tw[(threadIdx.x * (NT / (R0 * R1))) & (NT - 1)];
-  else if (threadIdx.x < 12) tmid[threadIdx.x] = a.tw[((threadIdx.x - 8) * (NT / (RL * R1))) & (NT - 1)];
   // the stages' twiddle powers w^r = e^{2 pi i k r / NT} straight from the table (one rounding,
   // no products; K1-wp is fp64-issue bound and its shared memory has slack): FM[r-1][c]
   // (forward middle, k = 4c), IM[r-1][c] (inverse middle, k = 8c), PA[r-1][x + x/8] (partner
@@ -1380,7 +1397,7 @@ __global__ void __launch_bounds__(512, 1)
     mbar_fence_init();
     for (int k = 0; k < NBUF; ++k) {
       const long t = blockIdx.x + (long)k * gridDim.x;
-      if (t < ntiles) ring_issue<NT, RM, NL>(&mx, &mn, a, t, smem + k * PL::STAGE, &full[k]);
+      if (t < ntiles) wp_issue<NT, RM, NL>(&mx, &mn, a, t, smem + k * PL::STAGE, &full[k]);
     }
   }
   __syncthreads();
@@ -1409,14 +1426,13 @@ __global__ void __launch_bounds__(512, 1)
     mbar_wait(&full[b], (uint32_t)((i / NBUF) & 1));
     double2* X = stg;                              // Û tile (swizzled); later the staged result
     const double2* NH = stg + TILE;                // N̂ tile (swizzled)
-    const double2* aux = stg + 2 * TILE;
-    double2* W = stg + s * WS;                     // this warp's FFT scratch (after phase A)
+    const double2* aux = stg + PL::AUXOFF;
+    double2* W = stg + TILE + s * WS;              // this warp's FFT scratch (N̂ tile + pad area)
     int two = 0;
     asm volatile("" : "+r"(two));
-    const double2* tw = stw + two;
 
     // ---- phase A: residual (+ ||r||^2), Gamma_alpha, forward stage 0 -------------------
-    double2 y[R0], xv[R0];
+    double2 y[R0];
     const double2 Ej = aux[s];
     const double2 c1 = aux[S + s];
     const double2 c2 = NL == 2 ? aux[2 * S + s] : make_double2(0.0, 0.0);
@@ -1424,7 +1440,6 @@ __global__ void __launch_bounds__(512, 1)
     for (int r = 0; r < R0; ++r) {
       const int t = j + r * TPS;
       const double2 xc = X[wp_sw(t, s)];
-      xv[r] = xc;
       const double2 prev = t > 0 ? X[wp_sw(t - 1, s)] : aux[3 * S + s];
       double2 rr = make_double2(fma(Ej.x, prev.x, -xc.x), fma(Ej.y, prev.y, -xc.y));
       const double2 nm1 = NH[wp_sw(t, s)];
@@ -1439,7 +1454,7 @@ __global__ void __launch_bounds__(512, 1)
       y[r] = cscale(rr, sg[t]);
     }
     DFT<R0, +1>::run(y);
-    named_bar(barid, GT);  // the group has read the tile: both blocks become the warps' scratch
+    named_bar(barid, GT);  // the group has read the N̂ tile: it becomes the warps' scratch
 #pragma unroll
     for (int r = 0; r < R0; ++r) W[l1w + r] = y[r];
     __syncwarp();
@@ -1515,7 +1530,6 @@ __global__ void __launch_bounds__(512, 1)
     }
 #pragma unroll
     for (int r = 0; r < R0; ++r) y[r] = W[lrd + 36 * r];
-    named_bar(barid, GT);  // every warp is done with its scratch: the Û block takes the result
 #pragma unroll
     for (int r = 1; r < R0; ++r) y[r] = cmulc(y[r], ttab[300 + (r - 1) * 32 + j]);
     DFT<R0, -1>::run(y);
@@ -1523,7 +1537,8 @@ __global__ void __launch_bounds__(512, 1)
 #pragma unroll
     for (int r = 0; r < R0; ++r) {
       const int t = j + r * TPS;
-      X[wp_sw(t, s)] = cadd(xv[r], cscale(y[r], sgi[t]));
+      const int q = wp_sw(t, s);
+      X[q] = cadd(X[q], cscale(y[r], sgi[t]));  // u_t re-read from the intact Û tile
     }
     fence_proxy_async_smem();
     named_bar(barid, GT);
@@ -1533,7 +1548,7 @@ __global__ void __launch_bounds__(512, 1)
       const long nxt = blockIdx.x + (i + NBUF) * gridDim.x;
       if (nxt < ntiles) {
         bulk_wait_read0();  // the store has read the staged result: refill the buffer
-        ring_issue<NT, RM, NL>(&mx, &mn, a, nxt, stg, &full[b]);
+        wp_issue<NT, RM, NL>(&mx, &mn, a, nxt, stg, &full[b]);
       }
     }
   }
