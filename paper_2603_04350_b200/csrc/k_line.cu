@@ -133,6 +133,15 @@ struct WarNone {
   __device__ __forceinline__ void arrive(int) {}
   __device__ __forceinline__ void wait(int) {}
 };
+// WarMask: the barrier of point k only where bit k is set (the hybrid buffer schedule of
+// line_item HY, where a stage's output buffer is not the buffer its input is read from)
+struct WarMask {
+  unsigned m;
+  __device__ __forceinline__ void arrive(int) {}
+  __device__ __forceinline__ void wait(int k) {
+    if ((m >> k) & 1u) __syncthreads();
+  }
+};
 constexpr int kWarPoints = 3;  // 0: middle stage, 1: stage 0, 2: last stage -> unpack
 #ifndef EXPD_WAR_MODE
 #define EXPD_WAR_MODE 0  // 0: WarSync in k_line, 1: WarMbar (A/B)
@@ -536,10 +545,11 @@ __device__ __forceinline__ void line_issue_store(const CUtensorMap* map, const L
 // alternate between the two (lcore's X = Z = cbo, Y = cb), so no stage writes a buffer that
 // another warp may still be reading: the write-after-read barriers disappear (WarNone).
 // Otherwise cbo == cb and the policy W places them.
-template <int M, int AX, bool NL, int G, class W, bool PP = false, bool TS = false>
+template <int M, int AX, bool NL, int G, class W, bool PP = false, bool TS = false, bool HY = false>
 __device__ __forceinline__ void line_item(char* cb, char* cbo, double2* wt, const LineArgs& a,
                                           const LPre<M, G>& pre0, uint64_t* bar, uint32_t parity, W& war,
-                                          long item = 0) {
+                                          long item = 0, char* coth = nullptr, const CUtensorMap* in_map = nullptr,
+                                          uint64_t* bar_oth = nullptr, long next = -1) {
   using D = LGeo<M, G, 1>;
   constexpr int R0 = D::R0, T = D::T, L = D::L, PADP = D::PADP;
   const int tid = threadIdx.x;
@@ -560,8 +570,15 @@ __device__ __forceinline__ void line_item(char* cb, char* cbo, double2* wt, cons
     // thrash the instruction cache)
     int npass = NL ? 2 : 1;
     asm volatile("" : "+r"(npass));
+    // HY (hybrid buffer schedule, EXPD_LINE_HY): the middle stage writes the OTHER buffer (free:
+    // the previous item's store has read it; the next item's load goes there only after this
+    // item's last unpack), so its write-after-read barrier and the unpack's go; in the fused
+    // pass the N step writes the other buffer too (no barrier before it) and pass 1 reads it,
+    // which makes every barrier of pass 1's transform a read-after-write one
+    double2* oth = reinterpret_cast<double2*>(coth);
 #pragma unroll 1
     for (int pass = 0; pass < npass; ++pass) {
+      double2* src = (HY && pass) ? oth : buf;  // stage-0 input of this pass
       double2 v[R0];
       // opaque copies: the weights are recomputed in each pass instead of being hoisted out of
       // the pass loop (16 live doubles)
@@ -589,18 +606,30 @@ __device__ __forceinline__ void line_item(char* cb, char* cbo, double2* wt, cons
           const int p1 = i - 1, p2 = M - i - 1;
           const int q1 = pass ? lswz<PADP>(p1) : p1, q2 = pass ? lswz<PADP>(p2) : p2;
           EXPD_CHECK(q1 >= 0 && q2 >= 0 && q1 < D::SWB && q2 < D::SWB, "line: column stage-0 read");
-          v[r] = lpre(buf[q1 * G + g], buf[q2 * G + g], av, a.c);
+          v[r] = lpre(src[q1 * G + g], src[q2 * G + g], av, a.c);
         }
       });
-      lcore<M, G>(v, PP ? bufo : buf, buf, PP ? bufo : buf, wt, tw, out, pre, war);
+      if constexpr (HY) {
+        // X = buf (in place over pass 0's input: its stage-0 reads are ordered by point 1; pass
+        // 1's input is in oth), Y = oth, Z = buf
+        WarMask wm{pass ? 0u : 2u};
+        lcore<M, G>(v, buf, oth, buf, wt, tw, out, pre, wm);
+      } else {
+        lcore<M, G>(v, PP ? bufo : buf, buf, PP ? bufo : buf, wt, tw, out, pre, war);
+      }
       if (NL && pass + 1 < npass) {
-        if (!PP) __syncthreads();  // everyone has read (e, w) of pass 0
+        if (!PP && !HY) __syncthreads();  // everyone has read (e, w) of pass 0
+        double2* nb = HY ? oth : buf;
 #pragma unroll
         for (int q = 0; q < 2 * L; ++q)
-          lat<M, G>(buf, 2 * j * L + q, g) =
+          lat<M, G>(nb, 2 * j * L + q, g) =
               make_double2(poly_eval(a.poly, out[q].x), poly_eval(a.poly, out[q].y));
         __syncthreads();
       }
+    }
+    if constexpr (HY) {
+      // every thread has passed the last unpack barrier: nobody reads oth again -> prefetch
+      if (threadIdx.x == 0 && next >= 0 && next < a.nitems) line_issue_load<M, AX, G>(in_map, a, next, coth, bar_oth);
     }
     // (e, w) reads done before the result overwrites their buffer (PP: only the row result
     // goes to it, and the prefix's cross-warp barrier already ordered them unless NWB == 1)
@@ -659,13 +688,14 @@ __device__ __forceinline__ void line_item(char* cb, char* cbo, double2* wt, cons
 // the next item's load is issued once the store has read the output buffer (no prefetch
 // during the transform -- the other CTAs of the SM cover the wait), and the transform runs
 // without write-after-read barriers (line_item PP).
-template <int M, int AX, bool NL, int G, int NBUF, bool PP = false, bool TS = false>
+template <int M, int AX, bool NL, int G, int NBUF, bool PP = false, bool TS = false, bool HY = false>
 __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::MINB)
     k_line(const __grid_constant__ CUtensorMap in_map, const __grid_constant__ CUtensorMap out_map,
            const __grid_constant__ LineArgs a) {
   using D = LGeo<M, G, NBUF>;
   static_assert(AX != AX_ROW || G == 1, "row items are one row pair");
   static_assert(!PP || NBUF == 2, "ping-pong needs two buffers");
+  static_assert(!HY || (NBUF == 2 && !PP), "the hybrid schedule needs two buffers");
   constexpr int R0 = D::R0, T = D::T, L = D::L, PADP = D::PADP;
   if (a.skip && *a.skip) return;  // stage 3 of a sweep whose result is known (line_skip_scope)
   extern __shared__ unsigned char lsm_raw[];
@@ -707,12 +737,13 @@ __global__ void __launch_bounds__(LGeo<M, G, NBUF>::THREADS, LGeo<M, G, NBUF>::M
     char* cbo = PP ? base + (cur ^ 1) * D::BUFB : cb;
     double2* buf = reinterpret_cast<double2*>(cb);
     const long next = item + gridDim.x;
-    if (!PP && NBUF == 2 && tid == 0 && next < a.nitems) {
+    if (!PP && NBUF == 2 && tid == 0 && (HY || next < a.nitems)) {
       bulk_wait_read0();  // the previous item's stores have left the other buffer
-      line_issue_load<M, AX, G>(&in_map, a, next, base + (cur ^ 1) * D::BUFB, &bar[cur ^ 1]);
+      if (!HY) line_issue_load<M, AX, G>(&in_map, a, next, base + (cur ^ 1) * D::BUFB, &bar[cur ^ 1]);
     }
-    line_item<M, AX, NL, G, WarT, PP, TS>(cb, cbo, wt, a, pre, &bar[cur],
-                                          (uint32_t)((NBUF == 2 ? (it >> 1) : it) & 1), war, item);
+    line_item<M, AX, NL, G, WarT, PP, TS, HY>(cb, cbo, wt, a, pre, &bar[cur],
+                                              (uint32_t)((NBUF == 2 ? (it >> 1) : it) & 1), war, item,
+                                              base + (cur ^ 1) * D::BUFB, &in_map, &bar[cur ^ 1], next);
     fence_proxy_async_smem();
     __syncthreads();
     if (tid == 0) {
@@ -1333,12 +1364,12 @@ static thread_local const int* t_line_skip = nullptr;
 LineSkipScope::LineSkipScope(const int* flag) : prev(t_line_skip) { t_line_skip = flag; }
 LineSkipScope::~LineSkipScope() { t_line_skip = prev; }
 
-template <int M, int AX, bool NL, int G, int NBUF, bool PP = false, bool TS = false>
+template <int M, int AX, bool NL, int G, int NBUF, bool PP = false, bool TS = false, bool HY = false>
 static cudaError_t launch_line(const Geom& g, const DstTables& t, const Poly& P, const double* in, double* out,
                                long nslices, cudaStream_t st, const PeerOut* peer = nullptr) {
   using D = LGeo<M, G, NBUF>;
   static_assert(!TS || AX != AX_ROW, "the transposed store is a COL layout");
-  auto k = k_line<M, AX, NL, G, NBUF, PP, TS>;
+  auto k = k_line<M, AX, NL, G, NBUF, PP, TS, HY>;
   static DevOnce once;  // per instantiation and device
   int per_sm = 1;
   if (cudaError_t e = smem_optin(once, k, D::SMEM, D::THREADS, &per_sm); e != cudaSuccess) return e;
@@ -1393,6 +1424,17 @@ static int colv() {
   }
   return v;
 }
+// The hybrid buffer schedule of the default line kernels (line_item HY; EXPD_LINE_HY=0 keeps
+// the in-place schedule with the next item's load issued at the item's start).  Measured on c5
+// (profiles/r02/line_hy_ab.txt): stage 3 15.88 -> 15.55 ms, sweep 21.92 -> 21.67 ms.
+static bool line_hy() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("EXPD_LINE_HY");
+    v = e ? atoi(e) : 1;
+  }
+  return v != 0;
+}
 // EXPD_COLTS=0: the strided-axis result compacted in shared memory and stored as boxes of
 // CBR rows (the round-1/2 layout) instead of the transposed store (A/B at M = 2048)
 static bool colts() {
@@ -1424,6 +1466,10 @@ static cudaError_t launch_col(const Geom& g, const DstTables& t, const Poly& P, 
         if (!colts()) {
           if constexpr (NL) return launch_line<M, AX, NL, 1, 2>(g, t, P, in, out, nslices, st);
           else return launch_line<M, AX, NL, 2, 2>(g, t, P, in, out, nslices, st);
+        }
+        if (line_hy()) {
+          if constexpr (NL) return launch_line<M, AX, NL, 1, 2, false, true, true>(g, t, P, in, out, nslices, st);
+          else return launch_line<M, AX, NL, 2, 2, false, true, true>(g, t, P, in, out, nslices, st);
         }
         if constexpr (NL) return launch_line<M, AX, NL, 1, 2, false, true>(g, t, P, in, out, nslices, st);
         else return launch_line<M, AX, NL, 2, 2, false, true>(g, t, P, in, out, nslices, st);
@@ -1500,6 +1546,9 @@ static cudaError_t line_pass_m(const Geom& g, const DstTables& t, const Poly& P,
     }
     if (rv == 1) return launch_line<M, AX_ROW, false, 1, 1>(g, t, P, in, out, nslices, st);
     if (rv == 3) return launch_line<M, AX_ROW, false, 1, 2, true>(g, t, P, in, out, nslices, st);  // ping-pong
+    if constexpr (M == 2048) {
+      if (line_hy()) return launch_line<M, AX_ROW, false, 1, 2, false, false, true>(g, t, P, in, out, nslices, st);
+    }
     return launch_line<M, AX_ROW, false, 1, 2>(g, t, P, in, out, nslices, st);
   }
   if (ax == AX_COL_Y)

@@ -477,12 +477,13 @@ def test_opt_in_variants_match_default(orc, env, monkeypatch):
 
 
 @pytest.mark.parametrize("env", [{"EXPD_COLV": "13", "EXPD_ROWV": "3"}, {"EXPD_COLV": "11", "EXPD_ROWV": "1"},
-                                 {"EXPD_COLV": "22"}, {"EXPD_COLTS": "0"}])
+                                 {"EXPD_COLV": "22"}, {"EXPD_COLTS": "0"}, {"EXPD_LINE_HY": "0"}])
 def test_line_launch_variants_match_oracle(tmp_path, env):
     """The line kernels' launch variants read once per process (EXPD_COLV / EXPD_ROWV: the
     ping-pong buffers, one buffer per CTA, two column pairs per item; EXPD_COLTS=0: the
     strided-axis result compacted and stored in boxes of 256 rows instead of the transposed
-    store), each in a fresh process:
+    store; EXPD_LINE_HY=0: the in-place buffer schedule instead of the hybrid one), each in a
+    fresh process:
     the c5 Picard solve at n + 1 = 2048 takes the oracle's iterations, and stage 3 matches the
     oracle at sampled modes."""
     import os
