@@ -1475,8 +1475,10 @@ static cudaError_t launch_col(const Geom& g, const DstTables& t, const Poly& P, 
         else return launch_line<M, AX, NL, 2, 2, false, true>(g, t, P, in, out, nslices, st);
     }
   } else if constexpr (M == 4096) {
+    if (line_hy()) return launch_line<M, AX, NL, 1, 2, false, true, true>(g, t, P, in, out, nslices, st);
     return launch_line<M, AX, NL, 1, 2, false, true>(g, t, P, in, out, nslices, st);
   } else {
+    if (line_hy()) return launch_line<M, AX, NL, 2, 2, false, true, true>(g, t, P, in, out, nslices, st);
     return launch_line<M, AX, NL, 2, 2, false, true>(g, t, P, in, out, nslices, st);
   }
 }
@@ -1546,9 +1548,7 @@ static cudaError_t line_pass_m(const Geom& g, const DstTables& t, const Poly& P,
     }
     if (rv == 1) return launch_line<M, AX_ROW, false, 1, 1>(g, t, P, in, out, nslices, st);
     if (rv == 3) return launch_line<M, AX_ROW, false, 1, 2, true>(g, t, P, in, out, nslices, st);  // ping-pong
-    if constexpr (M == 2048) {
-      if (line_hy()) return launch_line<M, AX_ROW, false, 1, 2, false, false, true>(g, t, P, in, out, nslices, st);
-    }
+    if (line_hy()) return launch_line<M, AX_ROW, false, 1, 2, false, false, true>(g, t, P, in, out, nslices, st);
     return launch_line<M, AX_ROW, false, 1, 2>(g, t, P, in, out, nslices, st);
   }
   if (ax == AX_COL_Y)
