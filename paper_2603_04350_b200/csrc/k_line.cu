@@ -143,6 +143,9 @@ struct WarMask {
   }
 };
 constexpr int kWarPoints = 3;  // 0: middle stage, 1: stage 0, 2: last stage -> unpack
+#ifndef EXPD_LINE_DEFER
+#define EXPD_LINE_DEFER 1  // defer the last prefix's cross-warp barrier (line_offw)
+#endif
 #ifndef EXPD_WAR_MODE
 #define EXPD_WAR_MODE 0  // 0: WarSync in k_line, 1: WarMbar (A/B)
 #endif
@@ -335,7 +338,8 @@ __device__ __forceinline__ void lmid(double2* in, double2* buf, const double2* _
 template <int M, int G, class W>
 __device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* X, double2* Y, double2* Z,
                                       double2* wt, const double2* __restrict__ tw,
-                                      double2 (&out)[2 * LGeo<M, G, 1>::L], const LPre<M, G>& pre, W& war) {
+                                      double2 (&out)[2 * LGeo<M, G, 1>::L], const LPre<M, G>& pre, W& war,
+                                      bool defer = false, double2* offw = nullptr) {
   using D = LGeo<M, G, 1>;
   constexpr int R0 = D::R0, RL = D::RL, NSL = D::NSL, T = D::T, L = D::L, PADP = D::PADP;
   const int g = threadIdx.x % G, j = threadIdx.x / G;
@@ -439,11 +443,26 @@ __device__ __forceinline__ void lcore(double2 (&v)[LGeo<M, G, 1>::R0], double2* 
   if constexpr (D::NWB > 1) {
     const int jw = j / D::JW;
     if (j % D::JW == D::JW - 1) wt[jw * G + g] = inc;
+    if (defer) {  // the caller adds the earlier warps' totals after its next barrier (line_offw)
+      *offw = off;
+      return;
+    }
     __syncthreads();
     for (int b = 0; b < jw; ++b) off = cadd(off, wt[b * G + g]);
   }
 #pragma unroll
   for (int l = 0; l < L; ++l) out[2 * l] = cadd(out[2 * l], off);
+}
+
+// The deferred end of lcore's prefix (defer = true): after a barrier that follows the wt
+// writes, the same additions in the same order (bitwise equal to the immediate form).
+template <int M, int G>
+__device__ __forceinline__ void line_offw(const double2* wt, double2 off, double2 (&out)[2 * LGeo<M, G, 1>::L]) {
+  using D = LGeo<M, G, 1>;
+  const int g = threadIdx.x % G, j = threadIdx.x / G, jw = j / D::JW;
+  for (int b = 0; b < jw; ++b) off = cadd(off, wt[b * G + g]);
+#pragma unroll
+  for (int l = 0; l < D::L; ++l) out[2 * l] = cadd(out[2 * l], off);
 }
 
 // ---------------------------------------------------------------------------------------
@@ -576,6 +595,7 @@ __device__ __forceinline__ void line_item(char* cb, char* cbo, double2* wt, cons
     // pass the N step writes the other buffer too (no barrier before it) and pass 1 reads it,
     // which makes every barrier of pass 1's transform a read-after-write one
     double2* oth = reinterpret_cast<double2*>(coth);
+    double2 offw = make_double2(0.0, 0.0);
 #pragma unroll 1
     for (int pass = 0; pass < npass; ++pass) {
       double2* src = (HY && pass) ? oth : buf;  // stage-0 input of this pass
@@ -609,13 +629,16 @@ __device__ __forceinline__ void line_item(char* cb, char* cbo, double2* wt, cons
           v[r] = lpre(src[q1 * G + g], src[q2 * G + g], av, a.c);
         }
       });
+      // the last pass defers the prefix's cross-warp barrier to the one before the result's
+      // writes (the wt totals are read after it; EXPD_LINE_DEFER=0 at build time disables)
+      const bool defer = EXPD_LINE_DEFER && !PP && D::NWB > 1 && pass + 1 == npass;
       if constexpr (HY) {
         // X = buf (in place over pass 0's input: its stage-0 reads are ordered by point 1; pass
         // 1's input is in oth), Y = oth, Z = buf
         WarMask wm{pass ? 0u : 2u};
-        lcore<M, G>(v, buf, oth, buf, wt, tw, out, pre, wm);
+        lcore<M, G>(v, buf, oth, buf, wt, tw, out, pre, wm, defer, &offw);
       } else {
-        lcore<M, G>(v, PP ? bufo : buf, buf, PP ? bufo : buf, wt, tw, out, pre, war);
+        lcore<M, G>(v, PP ? bufo : buf, buf, PP ? bufo : buf, wt, tw, out, pre, war, defer, &offw);
       }
       if (NL && pass + 1 < npass) {
         if (!PP && !HY) __syncthreads();  // everyone has read (e, w) of pass 0
@@ -634,6 +657,7 @@ __device__ __forceinline__ void line_item(char* cb, char* cbo, double2* wt, cons
     // (e, w) reads done before the result overwrites their buffer (PP: only the row result
     // goes to it, and the prefix's cross-warp barrier already ordered them unless NWB == 1)
     if (!PP || TS || (AX == AX_ROW && D::NWB == 1)) __syncthreads();
+    if (EXPD_LINE_DEFER && !PP && D::NWB > 1) line_offw<M, G>(wt, offw, out);
     if constexpr (AX != AX_ROW && TS) {
       // transposed store (TS): position p = 2L a + q of pair g goes to slot (q (T-1) + a) G + g,
       // the smem layout of the transposed TMA view (col_ts_map, box a < T-1): in each write
