@@ -23,3 +23,4 @@ timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__byte
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_time_(ring|wp)" -s 2 -c 1 -o $O/${tag}_prof_k1 $CMD > $O/${tag}_ncu_k1.log 2>&1; echo "ncu k1 exit $?"
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_line.*bool.1" -s 20 -c 1 -o $O/${tag}_prof_colnl $CMD > $O/${tag}_ncu_colnl.log 2>&1; echo "ncu colnl exit $?"
 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled -k "regex:k_line.*2048, .int.0," -s 2 -c 1 -o $O/${tag}_prof_row $CMD > $O/${tag}_ncu_row.log 2>&1; echo "ncu row exit $?"
+gzip -f $O/${tag}_prof_*.ncu-rep  # keep the copy-back under the 64 MiB limit (tools/promote_final.sh unpacks)

@@ -4,6 +4,7 @@
 # Usage: bash tools/promote_final.sh <tag>
 tag=$1; O=gpurun_out; P=profiles/r02
 set -e
+for f in $O/${tag}_prof_*.ncu-rep.gz; do [ -e "$f" ] && gunzip -kf "$f"; done
 tail -1 $O/${tag}_bench.json > $P/bench_final.json
 tail -1 $O/${tag}_bench_ref.json > $P/bench_reference_final.json
 tail -1 $O/${tag}_bench_c3.json > $P/bench_final_c3.json
