@@ -1318,6 +1318,12 @@ struct WpLayout {
                                   sizeof(double) * 2 * NT + 8 * NBUF + 16;
 };
 
+// EXPD_WP_LATE_REFILL (A/B): 0 = the refill right after the tile's store (the issuing thread
+// waits for the store to read the buffer), 1 = deferred to after the group's next mbarrier
+// wait, 2 = deferred to after the group's next phase-A barrier
+#ifndef EXPD_WP_LATE_REFILL
+#define EXPD_WP_LATE_REFILL 0
+#endif
 // (t, s) of a staged tile with the 128-byte swizzle: row t of 8 pairs (16-byte chunks)
 __device__ __forceinline__ int wp_sw(int t, int s) { return t * 8 + (s ^ (t & 7)); }
 
@@ -1408,6 +1414,8 @@ __global__ void __launch_bounds__(512, 1)
   const int ja = kWpPj[j];  // partner jobs
   const int jb = ja == 0 ? NSL / 2 : NSL - ja;
   const int barid = 1 + grp;
+  long pend_nxt = -1;  // EXPD_WP_LATE_REFILL: the refill this group's thread 0 still owes
+  int pend_b = 0;
   // scratch layouts (16-byte slots of the warp's region): L1 / L2 / L4 one pad slot per 8
   // positions (p + p/8), L3 one per 32 (p + p/32); every stage's reads and writes are
   // affine in r with a per-lane base and hit eight distinct bank groups per quarter warp
@@ -1424,6 +1432,11 @@ __global__ void __launch_bounds__(512, 1)
     const int b = (int)(i % NBUF);
     double2* stg = smem + b * PL::STAGE;
     mbar_wait(&full[b], (uint32_t)((i / NBUF) & 1));
+    if (EXPD_WP_LATE_REFILL == 1 && tid == 0 && pend_nxt >= 0) {
+      bulk_wait_read0();
+      wp_issue<NT, RM, NL>(&mx, &mn, a, pend_nxt, smem + pend_b * PL::STAGE, &full[pend_b]);
+      pend_nxt = -1;
+    }
     double2* X = stg;                              // Û tile (swizzled); later the staged result
     const double2* NH = stg + TILE;                // N̂ tile (swizzled)
     const double2* aux = stg + PL::AUXOFF;
@@ -1455,6 +1468,11 @@ __global__ void __launch_bounds__(512, 1)
     }
     DFT<R0, +1>::run(y);
     named_bar(barid, GT);  // the group has read the N̂ tile: it becomes the warps' scratch
+    if (EXPD_WP_LATE_REFILL == 2 && tid == 0 && pend_nxt >= 0) {
+      bulk_wait_read0();
+      wp_issue<NT, RM, NL>(&mx, &mn, a, pend_nxt, smem + pend_b * PL::STAGE, &full[pend_b]);
+      pend_nxt = -1;
+    }
 #pragma unroll
     for (int r = 0; r < R0; ++r) W[l1w + r] = y[r];
     __syncwarp();
@@ -1547,10 +1565,19 @@ __global__ void __launch_bounds__(512, 1)
       bulk_commit();
       const long nxt = blockIdx.x + (i + NBUF) * gridDim.x;
       if (nxt < ntiles) {
-        bulk_wait_read0();  // the store has read the staged result: refill the buffer
-        wp_issue<NT, RM, NL>(&mx, &mn, a, nxt, stg, &full[b]);
+        if (EXPD_WP_LATE_REFILL) {
+          pend_nxt = nxt;
+          pend_b = b;
+        } else {
+          bulk_wait_read0();  // the store has read the staged result: refill the buffer
+          wp_issue<NT, RM, NL>(&mx, &mn, a, nxt, stg, &full[b]);
+        }
       }
     }
+  }
+  if (tid == 0 && pend_nxt >= 0) {  // a refill another group's tile still needs
+    bulk_wait_read0();
+    wp_issue<NT, RM, NL>(&mx, &mn, a, pend_nxt, smem + pend_b * PL::STAGE, &full[pend_b]);
   }
   if (tid == 0) bulk_wait0();
 
